@@ -1,0 +1,164 @@
+/* meshperm_b200 — B200-native patch-based nested-dissection permutation.
+ *
+ * The C ABI the reference's symbolic-analysis callers bind to.  The
+ * reference (meshperm, /root/reference/proj) exposes free C++ functions in
+ * namespace meshperm; each entry point below names the reference interface
+ * it replaces (core/include/meshperm/<file>:<line>).  Plain pointers and
+ * sizes only: no C++ or torch types cross this boundary.
+ *
+ * Conventions (reference types.hpp:10-11): vertex/patch ids are int32,
+ * counts and weights int64.  A CSR graph (graph.hpp:10-24) has
+ * offsets[n+1] and neighbors[offsets[n]] with sorted, duplicate-free,
+ * symmetric lists and no self loops.
+ *
+ * Memory: every array argument is either host memory or device memory of
+ * the context's GPU, selected per call by the `on_device` flag of the struct
+ * it belongs to (mp_csr.on_device for inputs, mp_result.on_device for
+ * outputs).  Host arrays are staged through pinned buffers owned by the
+ * context.  Outputs are caller-allocated; sizes follow from n and nd_level.
+ *
+ * Errors: every function returns MP_OK (0) or an MP_E* code; the message of
+ * the last failure on the calling thread is mp_last_error().  Contract
+ * violations the reference reports with std::invalid_argument return
+ * MP_EINVAL with the same message text.
+ *
+ * Threading: a context is used by one host thread at a time; independent
+ * contexts (one per GPU, or several per GPU) run concurrently.  Results are
+ * independent of the stream, the context and the GPU count.
+ */
+#ifndef MESHPERM_B200_H
+#define MESHPERM_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  MP_OK = 0,
+  MP_EINVAL = 1,  /* std::invalid_argument in the reference */
+  MP_ECUDA = 2,   /* CUDA runtime / launch failure */
+  MP_ENOMEM = 3,  /* device or pinned allocation failed */
+  MP_ELOGIC = 4   /* std::logic_error in the reference (self-check) */
+};
+
+enum { MP_LOCAL_APPROX = 0, MP_LOCAL_EXACT = 1, MP_LOCAL_NATURAL = 2 }; /* local_order.hpp:10 OrderMode */
+enum { MP_SCHEDULE_POSTORDER = 0, MP_SCHEDULE_LEVELORDER = 1 };          /* pipeline.hpp:15 ScheduleKind */
+
+typedef struct mp_context mp_context;
+
+typedef struct {
+  int32_t n;
+  const int32_t* offsets;   /* n + 1 */
+  const int32_t* neighbors; /* offsets[n] */
+  int32_t on_device;        /* 1: both arrays live on the context's GPU */
+} mp_csr;
+
+/* RunConfig (pipeline.hpp:17-37), the fields the ordering path reads. */
+typedef struct {
+  int32_t patch_size;   /* 256 */
+  int32_t nd_level;     /* -1: default_nd_level(n) */
+  uint64_t seed;        /* 0 */
+  int32_t local_mode;   /* MP_LOCAL_* (approx_md) */
+  int32_t schedule;     /* MP_SCHEDULE_* (postorder) */
+  int32_t block_size;   /* 1; >1 expands perm/tree by b (assemble.hpp:43) */
+  int32_t want_fill;    /* 1: factor etree + column counts + nnz(L) (symbolic.hpp:23-31) */
+} mp_config;
+
+/* PipelineResult (pipeline.hpp:56-61) flattened.  Array pointers may be
+ * NULL when not wanted.  Sizes: nn = 2^(nd_level+1) - 1 tree nodes,
+ * N = block_size * n rows. */
+typedef struct {
+  int32_t on_device;           /* 1: array outputs are device pointers */
+  int32_t* patch_of;           /* n      GroupMap.assignment */
+  int32_t* tree_node_offsets;  /* nn+1   EliminationTree node i holds   */
+  int32_t* tree_vertices;      /* N        tree_vertices[off[i]..off[i+1]) */
+  int32_t* tree_local_perm;    /* N      EtreeNode.local_perm, same layout */
+  int32_t* perm;               /* N      Permutation.perm (new -> old) */
+  int32_t* inverse;            /* N      Permutation.inverse */
+  int32_t* etree_parent;       /* N      factor_etree_parents (positions) */
+  int64_t* column_counts;      /* N      FillReport.column_counts */
+  /* scalars, always written to host */
+  int32_t patch_count;
+  int32_t nd_level;
+  int64_t nnz_A, nnz_L, cost;
+  double fill_ratio;
+  /* device-timed stage times (CUDA events), ms:
+     0 patch, 1 quotient, 2 etree, 3 local, 4 assemble, 5 symbolic */
+  float stage_ms[6];
+  int64_t kernel_launches;     /* kernels launched by this call */
+} mp_result;
+
+const char* mp_last_error(void);
+const char* mp_version(void);
+
+/* Context: owns the device workspace (grown on demand, reused across calls),
+ * pinned staging buffers, a stream and the timing events. */
+int mp_context_create(mp_context** ctx, int32_t device);
+void mp_context_destroy(mp_context* ctx);
+/* cudaStream_t to run on; NULL restores the context's own stream. */
+int mp_context_set_stream(mp_context* ctx, void* stream);
+
+/* ---- whole path: run_pipeline's ordering stages (pipeline.cpp:100-140) ---- */
+int mp_order(mp_context* ctx, const mp_csr* g, const mp_config* cfg, mp_result* out);
+
+/* ---- stage entry points (reference free functions) ---- */
+/* etree.hpp:35-36 default_nd_level */
+int32_t mp_default_nd_level(int32_t n);
+
+/* patching.hpp:26-27 compute_patches(g, target_size, seed).to_group_map() */
+int mp_compute_patches(mp_context* ctx, const mp_csr* g, int32_t target_size, uint64_t seed,
+                       int32_t* assignment, int32_t on_device, int32_t* patch_count);
+
+/* patching.hpp:31-32 enforce_connectivity(partition, g) */
+int mp_enforce_connectivity(mp_context* ctx, const mp_csr* g, const int32_t* assignment,
+                            int32_t patch_count, int32_t* out, int32_t on_device,
+                            int32_t* out_count);
+
+/* quotient.hpp:41 build_quotient + QuotientGraph::positive_edges (quotient.hpp:36).
+ * Two-call: edge arrays NULL returns only *n_edges. Host outputs. */
+int mp_build_quotient(mp_context* ctx, const mp_csr* g, const int32_t* assignment,
+                      int32_t patch_count, int64_t* node_weight, int32_t* edge_p,
+                      int32_t* edge_q, int64_t* edge_w, int64_t* n_edges);
+
+/* etree.hpp:52-53 build_etree(g, gmap, nd_level, seed).  Host or device
+ * outputs per on_device; assignment follows g->on_device. */
+int mp_build_etree(mp_context* ctx, const mp_csr* g, const int32_t* assignment,
+                   int32_t patch_count, int32_t nd_level, uint64_t seed,
+                   int32_t* node_offsets, int32_t* node_vertices, int32_t on_device);
+
+/* local_order.hpp:36 order_tree_nodes(tree, g, mode) -> local_perm per node */
+int mp_order_tree_nodes(mp_context* ctx, const mp_csr* g, int32_t nd_level,
+                        const int32_t* node_offsets, const int32_t* node_vertices,
+                        int32_t mode, int32_t* local_perm, int32_t on_device);
+
+/* assemble.hpp:25-38 schedule_* + compute_perm */
+int mp_compute_perm(mp_context* ctx, int32_t n, int32_t nd_level, const int32_t* node_offsets,
+                    const int32_t* node_vertices, const int32_t* local_perm, int32_t schedule,
+                    int32_t* perm, int32_t* inverse, int32_t on_device);
+
+/* symbolic.hpp:23 elimination_fill + :31 factor_etree_parents for a
+ * permutation produced from an ND tree (perm = compute_perm(tree, ...)).
+ * Requires the tree because the device game runs subtree by subtree. */
+int mp_tree_fill(mp_context* ctx, const mp_csr* g, int32_t nd_level, const int32_t* node_offsets,
+                 const int32_t* node_vertices, const int32_t* local_perm, int32_t schedule,
+                 int64_t* column_counts, int32_t* etree_parent, int32_t on_device,
+                 int64_t* nnz_A, int64_t* nnz_L, int64_t* cost, double* fill_ratio);
+
+/* ---- synthetic inputs and host CSR build (outside the timed path) ---- */
+int64_t mp_grid_mesh_triangles(int32_t rows, int32_t cols);
+int mp_make_grid_mesh(int32_t rows, int32_t cols, int32_t* tris);          /* pipeline.hpp:65 */
+int mp_make_random_mesh(int32_t rows, int32_t cols, uint64_t seed, int32_t* tris);
+int64_t mp_torus_mesh_triangles(int32_t rows, int32_t cols);
+int mp_make_torus_mesh(int32_t rows, int32_t cols, int32_t* tris);
+int64_t mp_icosphere_vertices(int32_t f);
+int64_t mp_icosphere_triangles(int32_t f);
+int mp_make_icosphere_mesh(int32_t f, int32_t* tris);
+/* graph.hpp:56 mesh_to_graph; nbr NULL = count only */
+int mp_mesh_to_graph(int32_t nv, int64_t ntri, const int32_t* tris, int32_t* off, int32_t* nbr,
+                     int64_t* nnz);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

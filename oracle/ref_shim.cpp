@@ -1,0 +1,304 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product library.
+//
+// C-ABI shim over the UNMODIFIED reference meshperm core, compiled from the
+// sources where they lie under /root/reference/proj/core (see oracle/Makefile).
+// The resulting oracle/_ref/libmeshperm_ref.so is the "reference" oracle:
+// tests/ use it to pin the C restatement (oracle/mp_oracle.c) and the CUDA
+// path, and bench.py's reference arm / cpu_baseline leg time it on the GPU
+// box's host cores.  Every entry point forwards to the reference stage
+// function named in its comment; nothing here re-implements an algorithm.
+#include <bit>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "meshperm/assemble.hpp"
+#include "meshperm/etree.hpp"
+#include "meshperm/graph.hpp"
+#include "meshperm/local_order.hpp"
+#include "meshperm/patching.hpp"
+#include "meshperm/pipeline.hpp"
+#include "meshperm/quotient.hpp"
+#include "meshperm/symbolic.hpp"
+
+using namespace meshperm;
+
+namespace {
+thread_local std::string g_err;
+
+AdjacencyGraph make_graph(int32_t n, const int32_t* off, const int32_t* nbr) {
+  AdjacencyGraph g;
+  g.n = n;
+  g.offsets.assign(off, off + n + 1);
+  g.neighbors.assign(nbr, nbr + off[n]);
+  return g;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_err = std::string("invalid_argument: ") + e.what();
+    return 1;
+  } catch (const std::logic_error& e) {
+    g_err = std::string("logic_error: ") + e.what();
+    return 3;
+  } catch (const std::exception& e) {
+    g_err = std::string("error: ") + e.what();
+    return 2;
+  }
+}
+
+double ms_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+      .count();
+}
+
+OrderMode mode_of(int m) {
+  return m == 0 ? OrderMode::approx_md : m == 1 ? OrderMode::exact_md : OrderMode::natural;
+}
+
+void flatten_tree(const EliminationTree& tree, int32_t* node_offsets, int32_t* node_vertices,
+                  int32_t* local_perm) {
+  int32_t pos = 0;
+  for (index_t i = 0; i < tree.node_count(); ++i) {
+    node_offsets[i] = pos;
+    const auto& nd = tree.nodes[i];
+    for (std::size_t k = 0; k < nd.vertices.size(); ++k) {
+      if (node_vertices) node_vertices[pos + k] = nd.vertices[k];
+      if (local_perm) local_perm[pos + k] = k < nd.local_perm.size() ? nd.local_perm[k] : -1;
+    }
+    pos += static_cast<int32_t>(nd.vertices.size());
+  }
+  node_offsets[tree.node_count()] = pos;
+}
+
+EliminationTree unflatten_tree(int32_t n, int32_t nd_level, const int32_t* node_offsets,
+                               const int32_t* node_vertices, const int32_t* local_perm) {
+  EliminationTree tree;
+  tree.n = n;
+  tree.nd_level = nd_level;
+  tree.nodes.resize((std::size_t{1} << (nd_level + 1)) - 1);
+  for (std::size_t i = 0; i < tree.nodes.size(); ++i) {
+    auto& nd = tree.nodes[i];
+    nd.level = static_cast<index_t>(std::bit_width(static_cast<unsigned>(i + 1)) - 1);
+    nd.vertices.assign(node_vertices + node_offsets[i], node_vertices + node_offsets[i + 1]);
+    if (local_perm)
+      nd.local_perm.assign(local_perm + node_offsets[i], local_perm + node_offsets[i + 1]);
+  }
+  return tree;
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// graph.cpp:63-75 mesh_to_graph (validates, builds sorted dedup CSR).
+// Two-call: pass nbr_out == nullptr to learn the neighbor count.
+int ref_mesh_to_graph(int32_t nv, int64_t ntri, const int32_t* tris, int32_t* off_out,
+                      int32_t* nbr_out, int64_t* nnz_out) {
+  return guarded([&] {
+    TriangleMesh mesh;
+    mesh.vertex_count = nv;
+    mesh.triangles.resize(ntri);
+    for (int64_t t = 0; t < ntri; ++t)
+      mesh.triangles[t] = {tris[3 * t], tris[3 * t + 1], tris[3 * t + 2]};
+    AdjacencyGraph g = mesh_to_graph(mesh);
+    *nnz_out = static_cast<int64_t>(g.neighbors.size());
+    if (off_out) std::memcpy(off_out, g.offsets.data(), sizeof(int32_t) * (nv + 1));
+    if (nbr_out) std::memcpy(nbr_out, g.neighbors.data(), sizeof(int32_t) * g.neighbors.size());
+  });
+}
+
+// pipeline.cpp:38-55 make_grid_mesh.  tris_out holds 2*(r-1)*(c-1)*3 ints.
+int ref_make_grid_mesh(int32_t rows, int32_t cols, int32_t* tris_out) {
+  return guarded([&] {
+    TriangleMesh m = make_grid_mesh(rows, cols);
+    for (std::size_t t = 0; t < m.triangles.size(); ++t)
+      for (int c = 0; c < 3; ++c) tris_out[3 * t + c] = m.triangles[t][c];
+  });
+}
+
+// etree.cpp:42-46
+int32_t ref_default_nd_level(int32_t n) { return default_nd_level(n); }
+
+// patching.cpp:295-345 compute_patches
+int ref_compute_patches(int32_t n, const int32_t* off, const int32_t* nbr, int32_t target,
+                        uint64_t seed, int32_t* assignment, int32_t* patch_count) {
+  return guarded([&] {
+    AdjacencyGraph g = make_graph(n, off, nbr);
+    PatchPartition p = compute_patches(g, target, seed);
+    std::memcpy(assignment, p.assignment.data(), sizeof(int32_t) * n);
+    *patch_count = p.patch_count;
+  });
+}
+
+// patching.cpp:347-384 enforce_connectivity
+int ref_enforce_connectivity(int32_t n, const int32_t* off, const int32_t* nbr,
+                             const int32_t* assignment, int32_t patch_count, int32_t* out,
+                             int32_t* out_count) {
+  return guarded([&] {
+    AdjacencyGraph g = make_graph(n, off, nbr);
+    PatchPartition p;
+    p.assignment.assign(assignment, assignment + n);
+    p.patch_count = patch_count;
+    PatchPartition r = enforce_connectivity(p, g);
+    std::memcpy(out, r.assignment.data(), sizeof(int32_t) * n);
+    *out_count = r.patch_count;
+  });
+}
+
+// quotient.cpp:47-80 build_quotient -> node weights + sorted positive edges.
+// Two-call on the edge arrays (pass edge_p == nullptr to get the count).
+int ref_build_quotient(int32_t n, const int32_t* off, const int32_t* nbr,
+                       const int32_t* assignment, int32_t patch_count, int64_t* node_weight,
+                       int32_t* edge_p, int32_t* edge_q, int64_t* edge_w, int64_t* n_edges) {
+  return guarded([&] {
+    AdjacencyGraph g = make_graph(n, off, nbr);
+    GroupMap gm{std::vector<index_t>(assignment, assignment + n), patch_count};
+    QuotientGraph q = build_quotient(g, gm);
+    auto edges = q.positive_edges();
+    *n_edges = static_cast<int64_t>(edges.size());
+    if (node_weight) std::memcpy(node_weight, q.node_weight.data(), sizeof(int64_t) * patch_count);
+    if (edge_p)
+      for (std::size_t i = 0; i < edges.size(); ++i) {
+        edge_p[i] = std::get<0>(edges[i]);
+        edge_q[i] = std::get<1>(edges[i]);
+        edge_w[i] = std::get<2>(edges[i]);
+      }
+  });
+}
+
+// etree.cpp:86-147 build_etree (root quotient built inside, as in
+// pipeline.cpp:118-125).  node_offsets has 2^(L+1) entries, node_vertices n.
+int ref_build_etree(int32_t n, const int32_t* off, const int32_t* nbr, const int32_t* assignment,
+                    int32_t patch_count, int32_t nd_level, uint64_t seed, int32_t* node_offsets,
+                    int32_t* node_vertices) {
+  return guarded([&] {
+    AdjacencyGraph g = make_graph(n, off, nbr);
+    GroupMap gm{std::vector<index_t>(assignment, assignment + n), patch_count};
+    EliminationTree t = build_etree(g, gm, nd_level, seed);
+    flatten_tree(t, node_offsets, node_vertices, nullptr);
+  });
+}
+
+// local_order.cpp:57-87 order_tree_nodes.  mode 0 approx, 1 exact, 2 natural.
+int ref_order_tree_nodes(int32_t n, const int32_t* off, const int32_t* nbr, int32_t nd_level,
+                         const int32_t* node_offsets, const int32_t* node_vertices, int32_t mode,
+                         int32_t threads, int32_t* local_perm) {
+  return guarded([&] {
+    AdjacencyGraph g = make_graph(n, off, nbr);
+    EliminationTree t = unflatten_tree(n, nd_level, node_offsets, node_vertices, nullptr);
+    order_tree_nodes(t, g, mode_of(mode), threads);
+    std::vector<int32_t> tmp(t.node_count() + 1);
+    flatten_tree(t, tmp.data(), nullptr, local_perm);
+  });
+}
+
+// local_order.cpp:10-42 minimum_degree on a whole graph.
+int ref_minimum_degree(int32_t n, const int32_t* off, const int32_t* nbr, int32_t mode,
+                       int32_t* order) {
+  return guarded([&] {
+    AdjacencyGraph g = make_graph(n, off, nbr);
+    LocalPermutation lp = minimum_degree(g, mode_of(mode));
+    std::memcpy(order, lp.order.data(), sizeof(int32_t) * n);
+  });
+}
+
+// assemble.cpp:24-85 schedule_postorder|levelorder + compute_perm.
+int ref_compute_perm(int32_t n, const int32_t* off, const int32_t* nbr, int32_t nd_level,
+                     const int32_t* node_offsets, const int32_t* node_vertices,
+                     const int32_t* local_perm, int32_t levelorder, int32_t* perm,
+                     int32_t* inverse) {
+  return guarded([&] {
+    AdjacencyGraph g = make_graph(n, off, nbr);
+    EliminationTree t = unflatten_tree(n, nd_level, node_offsets, node_vertices, local_perm);
+    Schedule s = levelorder ? schedule_levelorder(t) : schedule_postorder(t);
+    Permutation p = compute_perm(t, g, s);
+    std::memcpy(perm, p.perm.data(), sizeof(int32_t) * n);
+    std::memcpy(inverse, p.inverse.data(), sizeof(int32_t) * n);
+  });
+}
+
+// symbolic.cpp:33-45 elimination_fill
+int ref_elimination_fill(int32_t n, const int32_t* off, const int32_t* nbr, const int32_t* perm,
+                         int64_t* column_counts, int64_t* nnz_A, int64_t* nnz_L, int64_t* cost,
+                         double* fill_ratio) {
+  return guarded([&] {
+    AdjacencyGraph g = make_graph(n, off, nbr);
+    Permutation p = Permutation::from_order(std::vector<index_t>(perm, perm + n));
+    FillReport r = elimination_fill(g, p);
+    if (column_counts) std::memcpy(column_counts, r.column_counts.data(), sizeof(int64_t) * n);
+    *nnz_A = r.nnz_A;
+    *nnz_L = r.nnz_L;
+    *cost = r.cost;
+    *fill_ratio = r.fill_ratio;
+  });
+}
+
+// symbolic.cpp:82-96 factor_etree_parents
+int ref_factor_etree_parents(int32_t n, const int32_t* off, const int32_t* nbr,
+                             const int32_t* perm, int32_t* parents) {
+  return guarded([&] {
+    AdjacencyGraph g = make_graph(n, off, nbr);
+    Permutation p = Permutation::from_order(std::vector<index_t>(perm, perm + n));
+    auto par = factor_etree_parents(g, p);
+    std::memcpy(parents, par.data(), sizeof(int32_t) * n);
+  });
+}
+
+// symbolic.cpp:98-119 cross_block_fill
+int ref_cross_block_fill(int32_t n, const int32_t* off, const int32_t* nbr, const int32_t* perm,
+                         int32_t nd_level, const int32_t* node_offsets,
+                         const int32_t* node_vertices, int64_t* crossing) {
+  return guarded([&] {
+    AdjacencyGraph g = make_graph(n, off, nbr);
+    Permutation p = Permutation::from_order(std::vector<index_t>(perm, perm + n));
+    EliminationTree t = unflatten_tree(n, nd_level, node_offsets, node_vertices, nullptr);
+    *crossing = cross_block_fill(g, p, t);
+  });
+}
+
+// The ordering stages of run_pipeline (pipeline.cpp:100-138) on an in-memory
+// graph, timed per stage exactly like time_stage (pipeline.cpp:16-21).
+// stage_ms[0..4] = patch, quotient, etree, local, assemble.
+int ref_order(int32_t n, const int32_t* off, const int32_t* nbr, int32_t patch_size,
+              int32_t nd_level, uint64_t seed, int32_t mode, int32_t levelorder, int32_t threads,
+              int32_t* assignment, int32_t* patch_count, int32_t* nd_level_out,
+              int32_t* node_offsets, int32_t* node_vertices, int32_t* local_perm, int32_t* perm,
+              int32_t* inverse, double* stage_ms) {
+  return guarded([&] {
+    AdjacencyGraph g = make_graph(n, off, nbr);
+    index_t L = nd_level >= 0 ? nd_level : default_nd_level(n);
+    *nd_level_out = L;
+    auto t0 = std::chrono::steady_clock::now();
+    GroupMap gm = compute_patches(g, patch_size, seed).to_group_map();
+    stage_ms[0] = ms_since(t0);
+    t0 = std::chrono::steady_clock::now();
+    QuotientGraph q = build_quotient(g, gm);
+    stage_ms[1] = ms_since(t0);
+    t0 = std::chrono::steady_clock::now();
+    EliminationTree tree = build_etree(g, gm, std::move(q), L, seed);
+    stage_ms[2] = ms_since(t0);
+    t0 = std::chrono::steady_clock::now();
+    order_tree_nodes(tree, g, mode_of(mode), threads < 1 ? 1 : threads);
+    stage_ms[3] = ms_since(t0);
+    t0 = std::chrono::steady_clock::now();
+    Schedule s = levelorder ? schedule_levelorder(tree) : schedule_postorder(tree);
+    Permutation p = compute_perm(tree, g, s);
+    stage_ms[4] = ms_since(t0);
+    if (assignment) std::memcpy(assignment, gm.assignment.data(), sizeof(int32_t) * n);
+    *patch_count = gm.patch_count;
+    if (node_offsets) flatten_tree(tree, node_offsets, node_vertices, local_perm);
+    if (perm) std::memcpy(perm, p.perm.data(), sizeof(int32_t) * n);
+    if (inverse) std::memcpy(inverse, p.inverse.data(), sizeof(int32_t) * n);
+  });
+}
+
+}  // extern "C"

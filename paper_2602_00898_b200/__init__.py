@@ -1,0 +1,13 @@
+"""meshperm_b200: B200-native patch-based nested-dissection permutation.
+
+Drop-in for the ordering path of the reference meshperm library
+(/root/reference/proj, arxiv 2602.00898): mesh/CSR in, patches, ND tree,
+permutation, factor etree and nnz(L) out, computed by sm_100a CUDA kernels
+behind the C ABI in include/meshperm_b200.h.
+"""
+from .api import (  # noqa: F401
+    AdjacencyGraph, Context, EliminationTree, FillReport, PatchPartition, Permutation, PipelineResult,
+    QuotientGraph, TriangleMesh, build_etree, build_quotient, compute_patches, compute_perm, default_context,
+    default_nd_level, enforce_connectivity, make_grid_mesh, make_icosphere_mesh, make_random_mesh,
+    make_torus_mesh, mesh_to_graph, order, order_device, order_tree_nodes, tree_fill,
+)

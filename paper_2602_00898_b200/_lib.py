@@ -1,0 +1,127 @@
+"""ctypes binding of the C ABI in include/meshperm_b200.h.
+
+Loads the in-tree libmeshperm_b200.so and fails loudly when it is missing:
+there is no CPU fallback for the ordering path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libmeshperm_b200.so"
+
+MP_OK, MP_EINVAL, MP_ECUDA, MP_ENOMEM, MP_ELOGIC = 0, 1, 2, 3, 4
+LOCAL_MODES = {"approx_md": 0, "exact_md": 1, "natural": 2}
+SCHEDULES = {"postorder": 0, "levelorder": 1}
+
+i32p = C.POINTER(C.c_int32)
+i64p = C.POINTER(C.c_int64)
+
+
+class MpCsr(C.Structure):
+    _fields_ = [("n", C.c_int32), ("offsets", C.c_void_p), ("neighbors", C.c_void_p), ("on_device", C.c_int32)]
+
+
+class MpConfig(C.Structure):
+    _fields_ = [
+        ("patch_size", C.c_int32),
+        ("nd_level", C.c_int32),
+        ("seed", C.c_uint64),
+        ("local_mode", C.c_int32),
+        ("schedule", C.c_int32),
+        ("block_size", C.c_int32),
+        ("want_fill", C.c_int32),
+    ]
+
+
+class MpResult(C.Structure):
+    _fields_ = [
+        ("on_device", C.c_int32),
+        ("patch_of", C.c_void_p),
+        ("tree_node_offsets", C.c_void_p),
+        ("tree_vertices", C.c_void_p),
+        ("tree_local_perm", C.c_void_p),
+        ("perm", C.c_void_p),
+        ("inverse", C.c_void_p),
+        ("etree_parent", C.c_void_p),
+        ("column_counts", C.c_void_p),
+        ("patch_count", C.c_int32),
+        ("nd_level", C.c_int32),
+        ("nnz_A", C.c_int64),
+        ("nnz_L", C.c_int64),
+        ("cost", C.c_int64),
+        ("fill_ratio", C.c_double),
+        ("stage_ms", C.c_float * 6),
+        ("kernel_launches", C.c_int64),
+    ]
+
+
+# (name, restype, argtypes) of every exported entry point; tests check that the
+# library exports exactly these.
+SIGNATURES = [
+    ("mp_last_error", C.c_char_p, []),
+    ("mp_version", C.c_char_p, []),
+    ("mp_context_create", C.c_int, [C.POINTER(C.c_void_p), C.c_int32]),
+    ("mp_context_destroy", None, [C.c_void_p]),
+    ("mp_context_set_stream", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("mp_order", C.c_int, [C.c_void_p, C.POINTER(MpCsr), C.POINTER(MpConfig), C.POINTER(MpResult)]),
+    ("mp_default_nd_level", C.c_int32, [C.c_int32]),
+    ("mp_compute_patches", C.c_int,
+     [C.c_void_p, C.POINTER(MpCsr), C.c_int32, C.c_uint64, C.c_void_p, C.c_int32, i32p]),
+    ("mp_enforce_connectivity", C.c_int,
+     [C.c_void_p, C.POINTER(MpCsr), C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, i32p]),
+    ("mp_build_quotient", C.c_int,
+     [C.c_void_p, C.POINTER(MpCsr), C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, i64p]),
+    ("mp_build_etree", C.c_int,
+     [C.c_void_p, C.POINTER(MpCsr), C.c_void_p, C.c_int32, C.c_int32, C.c_uint64, C.c_void_p, C.c_void_p, C.c_int32]),
+    ("mp_order_tree_nodes", C.c_int,
+     [C.c_void_p, C.POINTER(MpCsr), C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32]),
+    ("mp_compute_perm", C.c_int,
+     [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+      C.c_int32]),
+    ("mp_tree_fill", C.c_int,
+     [C.c_void_p, C.POINTER(MpCsr), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p,
+      C.c_void_p, C.c_int32, i64p, i64p, i64p, C.POINTER(C.c_double)]),
+    ("mp_grid_mesh_triangles", C.c_int64, [C.c_int32, C.c_int32]),
+    ("mp_make_grid_mesh", C.c_int, [C.c_int32, C.c_int32, C.c_void_p]),
+    ("mp_make_random_mesh", C.c_int, [C.c_int32, C.c_int32, C.c_uint64, C.c_void_p]),
+    ("mp_torus_mesh_triangles", C.c_int64, [C.c_int32, C.c_int32]),
+    ("mp_make_torus_mesh", C.c_int, [C.c_int32, C.c_int32, C.c_void_p]),
+    ("mp_icosphere_vertices", C.c_int64, [C.c_int32]),
+    ("mp_icosphere_triangles", C.c_int64, [C.c_int32]),
+    ("mp_make_icosphere_mesh", C.c_int, [C.c_int32, C.c_void_p]),
+    ("mp_mesh_to_graph", C.c_int, [C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, i64p]),
+]
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """The loaded library (raises if the CUDA extension has not been built)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2602_00898_b200.build` "
+                "(there is no CPU fallback for the ordering path)")
+        l = C.CDLL(str(LIB_PATH))
+        for name, res, args in SIGNATURES:
+            f = getattr(l, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = l
+    return _lib
+
+
+class MeshpermError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+def check(code: int) -> None:
+    if code != MP_OK:
+        msg = (lib().mp_last_error() or b"").decode()
+        if code == MP_EINVAL:
+            raise ValueError(msg)  # std::invalid_argument in the reference
+        raise MeshpermError(code, msg)

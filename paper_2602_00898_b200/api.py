@@ -1,0 +1,349 @@
+"""Python mirror of the reference meshperm interface, backed by the CUDA library.
+
+Names, argument meaning and error behaviour follow the reference free
+functions in /root/reference/proj/core/include/meshperm/*.hpp (cited per
+function); contract violations raise ValueError where the reference throws
+std::invalid_argument.  Host inputs are numpy int32 arrays; torch CUDA
+tensors are accepted wherever a device-resident call makes sense (order()).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import LOCAL_MODES, SCHEDULES, MpConfig, MpCsr, MpResult, check, lib
+
+
+# ----------------------------------------------------------------- data model
+@dataclass
+class TriangleMesh:  # types.hpp:15-18
+    vertex_count: int
+    triangles: np.ndarray  # (T, 3) int32
+
+
+@dataclass
+class AdjacencyGraph:  # graph.hpp:12-24
+    n: int
+    offsets: np.ndarray    # int32, n + 1
+    neighbors: np.ndarray  # int32, offsets[n]
+
+    def neighbors_of(self, v: int) -> np.ndarray:
+        return self.neighbors[self.offsets[v]:self.offsets[v + 1]]
+
+    def edge_count(self) -> int:
+        return int(self.offsets[self.n]) // 2
+
+
+@dataclass
+class PatchPartition:  # patching.hpp:11-17
+    assignment: np.ndarray
+    patch_count: int
+    target_size: int = 256
+
+
+@dataclass
+class QuotientGraph:  # quotient.hpp:17-37 (positive edges only)
+    patch_count: int
+    node_weight: np.ndarray
+    edges: list  # sorted (p, q, w), p < q, w > 0
+
+    def positive_edges(self):
+        return list(self.edges)
+
+
+@dataclass
+class EliminationTree:  # etree.hpp:19-33, flattened
+    n: int
+    nd_level: int
+    node_offsets: np.ndarray   # 2^(L+1)
+    vertices: np.ndarray       # n
+    local_perm: np.ndarray | None = None
+
+    def node_count(self) -> int:
+        return len(self.node_offsets) - 1
+
+    def node(self, i: int) -> np.ndarray:
+        return self.vertices[self.node_offsets[i]:self.node_offsets[i + 1]]
+
+    def node_perm(self, i: int) -> np.ndarray:
+        return self.local_perm[self.node_offsets[i]:self.node_offsets[i + 1]]
+
+
+@dataclass
+class Permutation:  # assemble.hpp:12-20
+    perm: np.ndarray
+    inverse: np.ndarray
+
+
+@dataclass
+class FillReport:  # symbolic.hpp:13-19
+    nnz_A: int
+    nnz_L: int
+    fill_ratio: float
+    column_counts: np.ndarray
+    cost: int
+    parents: np.ndarray | None = None
+
+
+@dataclass
+class PipelineResult:  # pipeline.hpp:56-61
+    patch: PatchPartition
+    tree: EliminationTree
+    perm: Permutation
+    fill: FillReport | None
+    stage_ms: dict = field(default_factory=dict)
+    kernel_launches: int = 0
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _ptr(a: np.ndarray) -> C.c_void_p:
+    return C.c_void_p(a.ctypes.data) if a is not None and a.size else C.c_void_p(0)
+
+
+# ----------------------------------------------------------------- context
+class Context:
+    """Owns the device workspace and stream for one GPU (mp_context)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        check(lib().mp_context_create(C.byref(h), device))
+        self.handle = h
+        self.device = device
+
+    def close(self):
+        if self.handle:
+            lib().mp_context_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_ptr: int | None):
+        check(lib().mp_context_set_stream(self.handle, C.c_void_p(stream_ptr or 0)))
+
+
+_default: dict[int, Context] = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _default:
+        _default[device] = Context(device)
+    return _default[device]
+
+
+def _csr(g: AdjacencyGraph) -> MpCsr:
+    off, nbr = _i32(g.offsets), _i32(g.neighbors)
+    c = MpCsr(int(g.n), _ptr(off), _ptr(nbr) if nbr.size else C.c_void_p(0), 0)
+    c._keep = (off, nbr)  # keep buffers alive
+    return c
+
+
+# ----------------------------------------------------------------- generators (host)
+def make_grid_mesh(rows: int, cols: int) -> TriangleMesh:  # pipeline.hpp:63-65
+    t = lib().mp_grid_mesh_triangles(rows, cols)
+    tris = np.zeros((max(t, 0), 3), np.int32)
+    check(lib().mp_make_grid_mesh(rows, cols, _ptr(tris)))
+    return TriangleMesh(rows * cols, tris)
+
+
+def make_random_mesh(rows: int, cols: int, seed: int) -> TriangleMesh:  # tests/test_support.hpp:66-86
+    t = lib().mp_grid_mesh_triangles(rows, cols)
+    tris = np.zeros((max(t, 0), 3), np.int32)
+    check(lib().mp_make_random_mesh(rows, cols, C.c_uint64(seed), _ptr(tris)))
+    return TriangleMesh(rows * cols, tris)
+
+
+def make_torus_mesh(rows: int, cols: int) -> TriangleMesh:
+    t = lib().mp_torus_mesh_triangles(rows, cols)
+    tris = np.zeros((max(t, 0), 3), np.int32)
+    check(lib().mp_make_torus_mesh(rows, cols, _ptr(tris)))
+    return TriangleMesh(rows * cols, tris)
+
+
+def make_icosphere_mesh(f: int) -> TriangleMesh:
+    tris = np.zeros((lib().mp_icosphere_triangles(f), 3), np.int32)
+    check(lib().mp_make_icosphere_mesh(f, _ptr(tris)))
+    return TriangleMesh(int(lib().mp_icosphere_vertices(f)), tris)
+
+
+def mesh_to_graph(mesh: TriangleMesh) -> AdjacencyGraph:  # graph.hpp:56
+    tris = _i32(mesh.triangles).reshape(-1, 3)
+    n = int(mesh.vertex_count)
+    off = np.zeros(n + 1, np.int32)
+    nnz = C.c_int64()
+    check(lib().mp_mesh_to_graph(n, len(tris), _ptr(tris), _ptr(off), C.c_void_p(0), C.byref(nnz)))
+    nbr = np.zeros(nnz.value, np.int32)
+    check(lib().mp_mesh_to_graph(n, len(tris), _ptr(tris), _ptr(off), _ptr(nbr), C.byref(nnz)))
+    return AdjacencyGraph(n, off, nbr)
+
+
+def default_nd_level(n: int) -> int:  # etree.hpp:35-36
+    return int(lib().mp_default_nd_level(n))
+
+
+# ----------------------------------------------------------------- stages
+def compute_patches(g: AdjacencyGraph, target_size: int = 256, seed: int = 0,
+                    ctx: Context | None = None) -> PatchPartition:  # patching.hpp:26-27
+    ctx = ctx or default_context()
+    out = np.zeros(max(g.n, 1), np.int32)
+    pc = C.c_int32()
+    check(lib().mp_compute_patches(ctx.handle, C.byref(_csr(g)), target_size, C.c_uint64(seed), _ptr(out), 0,
+                                   C.byref(pc)))
+    return PatchPartition(out[:g.n], pc.value, target_size)
+
+
+def enforce_connectivity(partition: PatchPartition, g: AdjacencyGraph,
+                         ctx: Context | None = None) -> PatchPartition:  # patching.hpp:31-32
+    ctx = ctx or default_context()
+    asg = _i32(partition.assignment)
+    if len(asg) != g.n:
+        raise ValueError("assignment does not cover the graph")
+    out = np.zeros(max(g.n, 1), np.int32)
+    pc = C.c_int32()
+    check(lib().mp_enforce_connectivity(ctx.handle, C.byref(_csr(g)), _ptr(asg), partition.patch_count, _ptr(out),
+                                        0, C.byref(pc)))
+    return PatchPartition(out[:g.n], pc.value, partition.target_size)
+
+
+def build_quotient(g: AdjacencyGraph, assignment, patch_count: int,
+                   ctx: Context | None = None) -> QuotientGraph:  # quotient.hpp:41
+    ctx = ctx or default_context()
+    asg = _i32(assignment)
+    if len(asg) != g.n:
+        raise ValueError(f"patch assignment covers {len(asg)} vertices, graph has {g.n}")
+    nw = np.zeros(max(patch_count, 1), np.int64)
+    ne = C.c_int64()
+    csr = _csr(g)
+    check(lib().mp_build_quotient(ctx.handle, C.byref(csr), _ptr(asg), patch_count, _ptr(nw), C.c_void_p(0),
+                                  C.c_void_p(0), C.c_void_p(0), C.byref(ne)))
+    ep = np.zeros(max(ne.value, 1), np.int32)
+    eq = np.zeros(max(ne.value, 1), np.int32)
+    ew = np.zeros(max(ne.value, 1), np.int64)
+    check(lib().mp_build_quotient(ctx.handle, C.byref(csr), _ptr(asg), patch_count, _ptr(nw), _ptr(ep), _ptr(eq),
+                                  _ptr(ew), C.byref(ne)))
+    m = ne.value
+    return QuotientGraph(patch_count, nw[:patch_count],
+                         list(zip(ep[:m].tolist(), eq[:m].tolist(), ew[:m].tolist())))
+
+
+def build_etree(g: AdjacencyGraph, assignment, patch_count: int, nd_level: int, seed: int = 0,
+                ctx: Context | None = None) -> EliminationTree:  # etree.hpp:52-53
+    ctx = ctx or default_context()
+    asg = _i32(assignment)
+    if len(asg) != g.n:
+        raise ValueError("patch map does not cover the graph")
+    if nd_level < 0 or nd_level > 24:
+        raise ValueError("nd_level out of range")
+    nn = (1 << (nd_level + 1)) - 1
+    off = np.zeros(nn + 1, np.int32)
+    verts = np.zeros(max(g.n, 1), np.int32)
+    check(lib().mp_build_etree(ctx.handle, C.byref(_csr(g)), _ptr(asg), patch_count, nd_level, C.c_uint64(seed),
+                               _ptr(off), _ptr(verts), 0))
+    return EliminationTree(g.n, nd_level, off, verts[:g.n])
+
+
+def order_tree_nodes(tree: EliminationTree, g: AdjacencyGraph, mode: str = "approx_md",
+                     ctx: Context | None = None) -> EliminationTree:  # local_order.hpp:36
+    ctx = ctx or default_context()
+    lp = np.zeros(max(g.n, 1), np.int32)
+    off, verts = _i32(tree.node_offsets), _i32(tree.vertices)
+    check(lib().mp_order_tree_nodes(ctx.handle, C.byref(_csr(g)), tree.nd_level, _ptr(off), _ptr(verts),
+                                    LOCAL_MODES[mode], _ptr(lp), 0))
+    tree.local_perm = lp[:g.n]
+    return tree
+
+
+def compute_perm(tree: EliminationTree, g: AdjacencyGraph, schedule: str = "postorder",
+                 ctx: Context | None = None) -> Permutation:  # assemble.hpp:25-38
+    ctx = ctx or default_context()
+    if tree.n != g.n:
+        raise ValueError("tree was built for a different graph")
+    if tree.local_perm is None:
+        raise ValueError("tree nodes have no local order")
+    pm = np.zeros(max(g.n, 1), np.int32)
+    inv = np.zeros(max(g.n, 1), np.int32)
+    check(lib().mp_compute_perm(ctx.handle, g.n, tree.nd_level, _ptr(_i32(tree.node_offsets)),
+                                _ptr(_i32(tree.vertices)), _ptr(_i32(tree.local_perm)), SCHEDULES[schedule], _ptr(pm),
+                                _ptr(inv), 0))
+    return Permutation(pm[:g.n], inv[:g.n])
+
+
+def tree_fill(g: AdjacencyGraph, tree: EliminationTree, schedule: str = "postorder",
+              ctx: Context | None = None) -> FillReport:  # symbolic.hpp:23 + :31
+    ctx = ctx or default_context()
+    cc = np.zeros(max(g.n, 1), np.int64)
+    par = np.zeros(max(g.n, 1), np.int32)
+    a, l, c = C.c_int64(), C.c_int64(), C.c_int64()
+    r = C.c_double()
+    check(lib().mp_tree_fill(ctx.handle, C.byref(_csr(g)), tree.nd_level, _ptr(_i32(tree.node_offsets)),
+                             _ptr(_i32(tree.vertices)), _ptr(_i32(tree.local_perm)), SCHEDULES[schedule], _ptr(cc),
+                             _ptr(par), 0, C.byref(a), C.byref(l), C.byref(c), C.byref(r)))
+    return FillReport(a.value, l.value, r.value, cc[:g.n], c.value, par[:g.n])
+
+
+# ----------------------------------------------------------------- whole path
+def make_config(patch_size=256, nd_level=-1, seed=0, local_mode="approx_md", schedule="postorder", block_size=1,
+                want_fill=True) -> MpConfig:
+    return MpConfig(patch_size, nd_level, seed, LOCAL_MODES[local_mode], SCHEDULES[schedule], block_size,
+                    1 if want_fill else 0)
+
+
+def order(g: AdjacencyGraph, patch_size: int = 256, nd_level: int = -1, seed: int = 0, local_mode="approx_md",
+          schedule="postorder", block_size: int = 1, want_fill: bool = True,
+          ctx: Context | None = None) -> PipelineResult:
+    """run_pipeline's ordering stages (pipeline.cpp:100-140) on host arrays."""
+    ctx = ctx or default_context()
+    cfg = make_config(patch_size, nd_level, seed, local_mode, schedule, block_size, want_fill)
+    L = nd_level if nd_level >= 0 else default_nd_level(g.n)
+    nn = (1 << (L + 1)) - 1
+    N = block_size * g.n
+    bufs = {
+        "patch_of": np.zeros(max(g.n, 1), np.int32),
+        "tree_node_offsets": np.zeros(nn + 1, np.int32),
+        "tree_vertices": np.zeros(max(N, 1), np.int32),
+        "tree_local_perm": np.zeros(max(N, 1), np.int32),
+        "perm": np.zeros(max(N, 1), np.int32),
+        "inverse": np.zeros(max(N, 1), np.int32),
+        "etree_parent": np.zeros(max(N, 1), np.int32),
+        "column_counts": np.zeros(max(N, 1), np.int64),
+    }
+    res = MpResult()
+    res.on_device = 0
+    for k, v in bufs.items():
+        setattr(res, k, _ptr(v))
+    if not want_fill:
+        res.etree_parent = None
+        res.column_counts = None
+    check(lib().mp_order(ctx.handle, C.byref(_csr(g)), C.byref(cfg), C.byref(res)))
+    tree = EliminationTree(N, res.nd_level, bufs["tree_node_offsets"], bufs["tree_vertices"][:N],
+                           bufs["tree_local_perm"][:N])
+    fill = None
+    if want_fill:
+        fill = FillReport(res.nnz_A, res.nnz_L, res.fill_ratio, bufs["column_counts"][:N], res.cost,
+                          bufs["etree_parent"][:N])
+    names = ["patch", "quotient", "etree", "local", "assemble", "symbolic"]
+    return PipelineResult(PatchPartition(bufs["patch_of"][:g.n], res.patch_count, patch_size), tree,
+                          Permutation(bufs["perm"][:N], bufs["inverse"][:N]), fill,
+                          {k: float(res.stage_ms[i]) for i, k in enumerate(names)}, int(res.kernel_launches))
+
+
+def order_device(ctx: Context, n: int, offsets_ptr: int, neighbors_ptr: int, out: dict, patch_size=256,
+                 nd_level=-1, seed=0, local_mode="approx_md", schedule="postorder", block_size=1,
+                 want_fill=True) -> MpResult:
+    """mp_order on device-resident CSR and device output pointers (dict of name -> ptr)."""
+    cfg = make_config(patch_size, nd_level, seed, local_mode, schedule, block_size, want_fill)
+    csr = MpCsr(n, C.c_void_p(offsets_ptr), C.c_void_p(neighbors_ptr), 1)
+    res = MpResult()
+    res.on_device = 1
+    for k, v in out.items():
+        setattr(res, k, C.c_void_p(v))
+    check(lib().mp_order(ctx.handle, C.byref(csr), C.byref(cfg), C.byref(res)))
+    return res

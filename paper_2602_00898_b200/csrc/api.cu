@@ -1,0 +1,444 @@
+// C ABI (include/meshperm_b200.h): context management, host<->device
+// marshalling and the mp_order pipeline (reference run_pipeline ordering
+// stages, core/src/pipeline.cpp:100-140).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "mp_context.h"
+#include "mp_device.cuh"
+
+namespace mp {
+
+thread_local std::string g_last_error;
+
+int set_error(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+std::vector<int32_t> make_schedule(int32_t L, int32_t kind);
+void compute_perm_blocks_dev(mp_context& ctx, int32_t n, int32_t L, const int32_t* node_offsets,
+                             const int32_t* node_vertices, const int32_t* local_perm, int32_t schedule,
+                             int32_t b, int32_t* perm, int32_t* inverse, int32_t* node_pos_dev);
+
+namespace {
+
+int32_t default_nd_level_host(int32_t n) {  // etree.cpp:42-46
+  int32_t level = 0;
+  for (int32_t x = n / 512; x > 1; x >>= 1) ++level;
+  return std::min<int32_t>(8, level);
+}
+
+// Device view of a caller CSR (copied when it is host memory).
+struct GraphView {
+  DevBuf<int32_t> off, nbr;
+  DGraph g{};
+  int64_t m2 = 0;
+};
+
+void make_view(mp_context& ctx, const mp_csr* c, GraphView& gv) {
+  if (!c) throw Error(MP_EINVAL, "null graph");
+  if (c->n < 0) throw Error(MP_EINVAL, "negative vertex count");
+  cudaStream_t s = ctx.stream;
+  const int32_t n = c->n;
+  if (c->on_device) {
+    int32_t m2 = 0;
+    MP_CUDA(cudaMemcpyAsync(&m2, c->offsets + n, 4, cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+    gv.g = {n, c->offsets, c->neighbors};
+    gv.m2 = m2;
+  } else {
+    gv.m2 = c->offsets[n];
+    gv.off.alloc(n + 1, s);
+    gv.nbr.alloc(std::max<int64_t>(gv.m2, 1), s);
+    MP_CUDA(cudaMemcpyAsync(gv.off.get(), c->offsets, sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice, s));
+    if (gv.m2)
+      MP_CUDA(cudaMemcpyAsync(gv.nbr.get(), c->neighbors, sizeof(int32_t) * gv.m2, cudaMemcpyHostToDevice, s));
+    gv.g = {n, gv.off.get(), gv.nbr.get()};
+  }
+}
+
+// Input array: device pointer as-is, or a device copy of host memory.
+template <class T>
+const T* input_ptr(mp_context& ctx, const T* p, int64_t count, bool on_device, DevBuf<T>& hold) {
+  if (on_device || !p) return p;
+  hold.alloc(std::max<int64_t>(count, 1), ctx.stream);
+  if (count) MP_CUDA(cudaMemcpyAsync(hold.get(), p, sizeof(T) * count, cudaMemcpyHostToDevice, ctx.stream));
+  return hold.get();
+}
+
+template <class T>
+void output_copy(mp_context& ctx, T* dst, const T* src, int64_t count, bool on_device) {
+  if (!dst || count == 0) return;
+  MP_CUDA(cudaMemcpyAsync(dst, src, sizeof(T) * count,
+                          on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx.stream));
+}
+
+// expand_blocks (assemble.cpp:87-114) for the tree, and the closed-form
+// expansion of column counts / parents.
+__global__ void expand_tree(int32_t n, int32_t b, const int32_t* verts, const int32_t* lperm, int32_t* verts_b,
+                            int32_t* lperm_b) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    for (int32_t t = 0; t < b; ++t) {
+      if (verts_b) verts_b[static_cast<int64_t>(b) * i + t] = b * verts[i] + t;
+      if (lperm_b) lperm_b[static_cast<int64_t>(b) * i + t] = b * lperm[i] + t;
+    }
+}
+__global__ void scale_offsets(int32_t nn1, int32_t b, const int32_t* off, int32_t* out) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nn1; i += gridDim.x * blockDim.x) out[i] = b * off[i];
+}
+__global__ void expand_counts(int32_t n, int32_t b, const int64_t* cc, const int32_t* par, int64_t* cc_b,
+                              int32_t* par_b, unsigned long long* sums) {
+  __shared__ int64_t red[32];
+  int64_t s = 0, q = 0;
+  for (int32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int64_t c = cc[k];
+    for (int32_t t = 0; t < b; ++t) {
+      const int64_t d = static_cast<int64_t>(b) * (c - 1) + (b - t);
+      const int64_t pos = static_cast<int64_t>(b) * k + t;
+      if (cc_b) cc_b[pos] = d;
+      if (par_b) par_b[pos] = t + 1 < b ? static_cast<int32_t>(pos + 1) : (par[k] < 0 ? -1 : b * par[k]);
+      s += d;
+      q += d * d;
+    }
+  }
+  s = block_sum_i64(s, red);
+  q = block_sum_i64(q, red);
+  if (threadIdx.x == 0) {
+    atomicAdd(&sums[0], static_cast<unsigned long long>(s));
+    atomicAdd(&sums[1], static_cast<unsigned long long>(q));
+  }
+}
+
+int grid_for(const mp_context& ctx, int64_t n) {
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), ctx.num_sms * 16LL)));
+}
+
+struct ScopedDevice {
+  int prev = 0;
+  explicit ScopedDevice(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~ScopedDevice() {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+}  // namespace mp
+
+using namespace mp;
+
+extern "C" {
+
+const char* mp_last_error(void) { return g_last_error.c_str(); }
+const char* mp_version(void) { return "meshperm_b200 0.1 (sm_100a)"; }
+int32_t mp_default_nd_level(int32_t n) { return default_nd_level_host(n); }
+
+int mp_context_create(mp_context** out, int32_t device) {
+  return guarded([&] {
+    if (!out) throw Error(MP_EINVAL, "null context pointer");
+    int count = 0;
+    MP_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) throw Error(MP_EINVAL, "no CUDA device " + std::to_string(device));
+    auto* ctx = new mp_context();
+    ctx->device = device;
+    ScopedDevice sd(device);
+    MP_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+    ctx->stream = ctx->own_stream;
+    MP_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
+    for (auto& e : ctx->ev) MP_CUDA(cudaEventCreate(&e));
+    // keep freed scratch in the pool between calls (stream-ordered allocator)
+    cudaMemPool_t pool;
+    MP_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    MP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    *out = ctx;
+  });
+}
+
+void mp_context_destroy(mp_context* ctx) {
+  if (!ctx) return;
+  ScopedDevice sd(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+}
+
+int mp_context_set_stream(mp_context* ctx, void* stream) {
+  return guarded([&] {
+    if (!ctx) throw Error(MP_EINVAL, "null context");
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+  });
+}
+
+int mp_compute_patches(mp_context* ctx, const mp_csr* g, int32_t target, uint64_t seed, int32_t* assignment,
+                       int32_t on_device, int32_t* patch_count) {
+  return guarded([&] {
+    if (!ctx) throw Error(MP_EINVAL, "null context");
+    ScopedDevice sd(ctx->device);
+    GraphView gv;
+    make_view(*ctx, g, gv);
+    DevBuf<int32_t> asg(std::max(g->n, 1), ctx->stream);
+    int32_t pc = compute_patches_dev(*ctx, gv.g, target, seed, asg);
+    output_copy(*ctx, assignment, asg.get(), g->n, on_device);
+    MP_CUDA(cudaStreamSynchronize(ctx->stream));
+    *patch_count = pc;
+  });
+}
+
+int mp_enforce_connectivity(mp_context* ctx, const mp_csr* g, const int32_t* assignment, int32_t patch_count,
+                            int32_t* out, int32_t on_device, int32_t* out_count) {
+  return guarded([&] {
+    if (!ctx) throw Error(MP_EINVAL, "null context");
+    ScopedDevice sd(ctx->device);
+    GraphView gv;
+    make_view(*ctx, g, gv);
+    DevBuf<int32_t> hold, res(std::max(g->n, 1), ctx->stream);
+    const int32_t* in = input_ptr(*ctx, assignment, g->n, on_device != 0, hold);
+    int32_t pc = enforce_connectivity_dev(*ctx, gv.g, in, patch_count, res);
+    output_copy(*ctx, out, res.get(), g->n, on_device);
+    MP_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out_count = pc;
+  });
+}
+
+int mp_build_quotient(mp_context* ctx, const mp_csr* g, const int32_t* assignment, int32_t patch_count,
+                      int64_t* node_weight, int32_t* edge_p, int32_t* edge_q, int64_t* edge_w, int64_t* n_edges) {
+  return guarded([&] {
+    if (!ctx) throw Error(MP_EINVAL, "null context");
+    ScopedDevice sd(ctx->device);
+    cudaStream_t s = ctx->stream;
+    GraphView gv;
+    make_view(*ctx, g, gv);
+    DevBuf<int32_t> hold;
+    const int32_t* in = input_ptr(*ctx, assignment, g->n, g->on_device != 0, hold);
+    DevBuf<int64_t> nw(std::max(patch_count, 1), s);
+    int32_t *ep = nullptr, *eq = nullptr;
+    int64_t* ew = nullptr;
+    int64_t U = build_quotient_dev(*ctx, gv.g, in, patch_count, nw, &ep, &eq, &ew);
+    if (node_weight) output_copy(*ctx, node_weight, nw.get(), patch_count, false);
+    if (edge_p) {
+      output_copy(*ctx, edge_p, ep, U, false);
+      output_copy(*ctx, edge_q, eq, U, false);
+      output_copy(*ctx, edge_w, ew, U, false);
+    }
+    MP_CUDA(cudaStreamSynchronize(s));
+    cudaFreeAsync(ep, s), cudaFreeAsync(eq, s), cudaFreeAsync(ew, s);
+    *n_edges = U;
+  });
+}
+
+int mp_build_etree(mp_context* ctx, const mp_csr* g, const int32_t* assignment, int32_t patch_count,
+                   int32_t nd_level, uint64_t seed, int32_t* node_offsets, int32_t* node_vertices, int32_t on_device) {
+  (void)seed;  // bipartition_quotient ignores it (partition.cpp:27)
+  return guarded([&] {
+    if (!ctx) throw Error(MP_EINVAL, "null context");
+    if (nd_level < 0 || nd_level > 24) throw Error(MP_EINVAL, "nd_level out of range");
+    ScopedDevice sd(ctx->device);
+    cudaStream_t s = ctx->stream;
+    GraphView gv;
+    make_view(*ctx, g, gv);
+    DevBuf<int32_t> hold;
+    const int32_t* in = input_ptr(*ctx, assignment, g->n, g->on_device != 0, hold);
+    const int64_t nn = (1LL << (nd_level + 1)) - 1;
+    DevBuf<int32_t> node_of(std::max(g->n, 1), s), off(nn + 1, s), verts(std::max(g->n, 1), s);
+    build_etree_dev(*ctx, gv.g, in, patch_count, nd_level, node_of, off, verts);
+    output_copy(*ctx, node_offsets, off.get(), nn + 1, on_device);
+    output_copy(*ctx, node_vertices, verts.get(), g->n, on_device);
+    MP_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int mp_order_tree_nodes(mp_context* ctx, const mp_csr* g, int32_t nd_level, const int32_t* node_offsets,
+                        const int32_t* node_vertices, int32_t mode, int32_t* local_perm, int32_t on_device) {
+  return guarded([&] {
+    if (!ctx) throw Error(MP_EINVAL, "null context");
+    if (nd_level < 0 || nd_level > 24) throw Error(MP_EINVAL, "nd_level out of range");
+    if (mode < 0 || mode > 2) throw Error(MP_EINVAL, "unknown local ordering mode");
+    ScopedDevice sd(ctx->device);
+    cudaStream_t s = ctx->stream;
+    GraphView gv;
+    make_view(*ctx, g, gv);
+    const int32_t nn = static_cast<int32_t>((1LL << (nd_level + 1)) - 1);
+    DevBuf<int32_t> h1, h2, node_of(std::max(g->n, 1), s), lp(std::max(g->n, 1), s);
+    const int32_t* off = input_ptr(*ctx, node_offsets, nn + 1, on_device != 0, h1);
+    const int32_t* verts = input_ptr(*ctx, node_vertices, g->n, on_device != 0, h2);
+    node_of_from_tree_dev(*ctx, g->n, nn, off, verts, node_of);
+    order_tree_nodes_dev(*ctx, gv.g, nd_level, node_of, off, verts, mode, lp);
+    output_copy(*ctx, local_perm, lp.get(), g->n, on_device);
+    MP_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int mp_compute_perm(mp_context* ctx, int32_t n, int32_t nd_level, const int32_t* node_offsets,
+                    const int32_t* node_vertices, const int32_t* local_perm, int32_t schedule, int32_t* perm,
+                    int32_t* inverse, int32_t on_device) {
+  return guarded([&] {
+    if (!ctx) throw Error(MP_EINVAL, "null context");
+    if (nd_level < 0 || nd_level > 24) throw Error(MP_EINVAL, "nd_level out of range");
+    ScopedDevice sd(ctx->device);
+    cudaStream_t s = ctx->stream;
+    const int32_t nn = static_cast<int32_t>((1LL << (nd_level + 1)) - 1);
+    DevBuf<int32_t> h1, h2, h3, pm(std::max(n, 1), s), inv(std::max(n, 1), s), pos(nn + 1, s);
+    const int32_t* off = input_ptr(*ctx, node_offsets, nn + 1, on_device != 0, h1);
+    const int32_t* verts = input_ptr(*ctx, node_vertices, n, on_device != 0, h2);
+    const int32_t* lp = input_ptr(*ctx, local_perm, n, on_device != 0, h3);
+    compute_perm_dev(*ctx, n, nd_level, off, verts, lp, schedule, pm, inv, pos);
+    output_copy(*ctx, perm, pm.get(), n, on_device);
+    output_copy(*ctx, inverse, inv.get(), n, on_device);
+    MP_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int mp_tree_fill(mp_context* ctx, const mp_csr* g, int32_t nd_level, const int32_t* node_offsets,
+                 const int32_t* node_vertices, const int32_t* local_perm, int32_t schedule, int64_t* column_counts,
+                 int32_t* etree_parent, int32_t on_device, int64_t* nnz_A, int64_t* nnz_L, int64_t* cost,
+                 double* fill_ratio) {
+  return guarded([&] {
+    if (!ctx) throw Error(MP_EINVAL, "null context");
+    if (nd_level < 0 || nd_level > 24) throw Error(MP_EINVAL, "nd_level out of range");
+    ScopedDevice sd(ctx->device);
+    cudaStream_t s = ctx->stream;
+    GraphView gv;
+    make_view(*ctx, g, gv);
+    const int32_t n = g->n;
+    const int32_t nn = static_cast<int32_t>((1LL << (nd_level + 1)) - 1);
+    DevBuf<int32_t> h1, h2, h3, node_of(std::max(n, 1), s), pm(std::max(n, 1), s), inv(std::max(n, 1), s),
+        pos(nn + 1, s), par(std::max(n, 1), s);
+    DevBuf<int64_t> cc(std::max(n, 1), s);
+    const int32_t* off = input_ptr(*ctx, node_offsets, nn + 1, on_device != 0, h1);
+    const int32_t* verts = input_ptr(*ctx, node_vertices, n, on_device != 0, h2);
+    const int32_t* lp = input_ptr(*ctx, local_perm, n, on_device != 0, h3);
+    compute_perm_dev(*ctx, n, nd_level, off, verts, lp, schedule, pm, inv, pos);
+    node_of_from_tree_dev(*ctx, n, nn, off, verts, node_of);
+    int64_t L = 0, C = 0;
+    tree_fill_dev(*ctx, gv.g, nd_level, node_of, off, verts, lp, pos, inv, cc, par, &L, &C);
+    output_copy(*ctx, column_counts, cc.get(), n, on_device);
+    output_copy(*ctx, etree_parent, par.get(), n, on_device);
+    MP_CUDA(cudaStreamSynchronize(s));
+    const int64_t A = static_cast<int64_t>(n) + gv.m2;
+    if (nnz_A) *nnz_A = A;
+    if (nnz_L) *nnz_L = L;
+    if (cost) *cost = C;
+    if (fill_ratio) *fill_ratio = A > 0 ? static_cast<double>(L) / static_cast<double>(A) : 0.0;
+  });
+}
+
+// run_pipeline's ordering stages (pipeline.cpp:100-140) on a device CSR.
+int mp_order(mp_context* ctx, const mp_csr* g, const mp_config* cfg, mp_result* out) {
+  return guarded([&] {
+    if (!ctx || !g || !cfg || !out) throw Error(MP_EINVAL, "null argument");
+    if (cfg->block_size < 1) throw Error(MP_EINVAL, "block size must be positive");
+    if (cfg->patch_size < 1) throw Error(MP_EINVAL, "patch size must be positive");
+    if (cfg->local_mode < 0 || cfg->local_mode > 2) throw Error(MP_EINVAL, "unknown local ordering mode");
+    if (cfg->schedule < 0 || cfg->schedule > 1) throw Error(MP_EINVAL, "unknown schedule");
+    ScopedDevice sd(ctx->device);
+    cudaStream_t s = ctx->stream;
+    const int64_t launches0 = ctx->launches;
+    const int32_t n = g->n, b = cfg->block_size;
+    const int32_t L = cfg->nd_level >= 0 ? cfg->nd_level : default_nd_level_host(n);
+    if (L > 24) throw Error(MP_EINVAL, "nd_level out of range");
+    const int32_t nn = static_cast<int32_t>((1LL << (L + 1)) - 1);
+    const int64_t N = static_cast<int64_t>(b) * n;
+
+    MP_CUDA(cudaEventRecord(ctx->ev[0], s));
+    GraphView gv;
+    make_view(*ctx, g, gv);
+    DevBuf<int32_t> asg(std::max(n, 1), s), node_of(std::max(n, 1), s), off(nn + 1, s), verts(std::max(n, 1), s),
+        lp(std::max(n, 1), s), pm(std::max<int64_t>(N, 1), s), inv(std::max<int64_t>(N, 1), s), pos(nn + 1, s);
+    MP_CUDA(cudaEventRecord(ctx->ev[1], s));
+    const int32_t pc = compute_patches_dev(*ctx, gv.g, cfg->patch_size, cfg->seed, asg);
+    MP_CUDA(cudaEventRecord(ctx->ev[2], s));
+    // the per-level quotient is rebuilt inside the level loop (ndtree.cu), so
+    // the quotient stage has no separate launch; its time is part of etree
+    MP_CUDA(cudaEventRecord(ctx->ev[3], s));
+    build_etree_dev(*ctx, gv.g, asg, pc, L, node_of, off, verts);
+    MP_CUDA(cudaEventRecord(ctx->ev[4], s));
+    order_tree_nodes_dev(*ctx, gv.g, L, node_of, off, verts, cfg->local_mode, lp);
+    MP_CUDA(cudaEventRecord(ctx->ev[5], s));
+    DevBuf<int32_t> pm1, inv1;
+    if (b == 1) {
+      compute_perm_blocks_dev(*ctx, n, L, off, verts, lp, cfg->schedule, 1, pm, inv, pos);
+    } else {
+      pm1.alloc(std::max(n, 1), s);
+      inv1.alloc(std::max(n, 1), s);
+      compute_perm_blocks_dev(*ctx, n, L, off, verts, lp, cfg->schedule, 1, pm1, inv1, pos);
+      compute_perm_blocks_dev(*ctx, n, L, off, verts, lp, cfg->schedule, b, pm, inv, pos);
+    }
+    MP_CUDA(cudaEventRecord(ctx->ev[6], s));
+    int64_t nnzL = 0, cost = 0;
+    DevBuf<int64_t> cc;
+    DevBuf<int32_t> par;
+    if (cfg->want_fill) {
+      cc.alloc(std::max<int64_t>(N, 1), s);
+      par.alloc(std::max<int64_t>(N, 1), s);
+      if (b == 1) {
+        tree_fill_dev(*ctx, gv.g, L, node_of, off, verts, lp, pos, inv, cc, par, &nnzL, &cost);
+      } else {
+        DevBuf<int64_t> cc1(std::max(n, 1), s);
+        DevBuf<int32_t> par1(std::max(n, 1), s);
+        DevBuf<unsigned long long> sums(2, s);
+        int64_t l1 = 0, c1 = 0;
+        tree_fill_dev(*ctx, gv.g, L, node_of, off, verts, lp, pos, inv1, cc1, par1, &l1, &c1);
+        MP_CUDA(cudaMemsetAsync(sums, 0, 16, s));
+        MP_KERNEL(*ctx, expand_counts<<<grid_for(*ctx, n), 256, 0, s>>>(n, b, cc1, par1, cc, par, sums));
+        unsigned long long h[2];
+        MP_CUDA(cudaMemcpyAsync(h, sums, 16, cudaMemcpyDeviceToHost, s));
+        MP_CUDA(cudaStreamSynchronize(s));
+        nnzL = static_cast<int64_t>(h[0]);
+        cost = static_cast<int64_t>(h[1]);
+      }
+    }
+    MP_CUDA(cudaEventRecord(ctx->ev[7], s));
+    // outputs
+    const bool od = out->on_device != 0;
+    output_copy(*ctx, out->patch_of, asg.get(), n, od);
+    if (b == 1) {
+      output_copy(*ctx, out->tree_node_offsets, off.get(), nn + 1, od);
+      output_copy(*ctx, out->tree_vertices, verts.get(), n, od);
+      output_copy(*ctx, out->tree_local_perm, lp.get(), n, od);
+    } else {
+      DevBuf<int32_t> offb(nn + 1, s), vb(N, s), lpb(N, s);
+      MP_KERNEL(*ctx, scale_offsets<<<grid_for(*ctx, nn + 1), 256, 0, s>>>(nn + 1, b, off, offb));
+      MP_KERNEL(*ctx, expand_tree<<<grid_for(*ctx, n), 256, 0, s>>>(n, b, verts, lp, vb, lpb));
+      output_copy(*ctx, out->tree_node_offsets, offb.get(), nn + 1, od);
+      output_copy(*ctx, out->tree_vertices, vb.get(), N, od);
+      output_copy(*ctx, out->tree_local_perm, lpb.get(), N, od);
+      MP_CUDA(cudaStreamSynchronize(s));
+    }
+    output_copy(*ctx, out->perm, pm.get(), N, od);
+    output_copy(*ctx, out->inverse, inv.get(), N, od);
+    if (cfg->want_fill) {
+      output_copy(*ctx, out->column_counts, cc.get(), N, od);
+      output_copy(*ctx, out->etree_parent, par.get(), N, od);
+    }
+    MP_CUDA(cudaStreamSynchronize(s));
+    out->patch_count = pc;
+    out->nd_level = L;
+    // nnz_A of the measured system: b^2 (n + 2m) (pipeline.cpp:174-175 on expand_graph)
+    out->nnz_A = static_cast<int64_t>(b) * b * (n + gv.m2);
+    out->nnz_L = nnzL;
+    out->cost = cost;
+    out->fill_ratio = out->nnz_A > 0 ? static_cast<double>(nnzL) / static_cast<double>(out->nnz_A) : 0.0;
+    float ms = 0;
+    const int pairs[6][2] = {{1, 2}, {2, 3}, {3, 4}, {4, 5}, {5, 6}, {6, 7}};
+    for (int i = 0; i < 6; ++i) {
+      MP_CUDA(cudaEventElapsedTime(&ms, ctx->ev[pairs[i][0]], ctx->ev[pairs[i][1]]));
+      out->stage_ms[i] = ms;
+    }
+    if (!cfg->want_fill) out->stage_ms[5] = 0;
+    out->kernel_launches = ctx->launches - launches0;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,79 @@
+// The library context and the internal stage interfaces (device pointers).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "mp_internal.h"
+
+struct mp_context {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  int64_t launches = 0;  // kernels launched through this context (cumulative)
+  cudaEvent_t ev[8] = {};
+  // pinned staging for host-memory arguments
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  // symbolic-pool size learnt from earlier calls (ints)
+  int64_t sym_pool_hint = 0;
+};
+
+namespace mp {
+
+struct DGraph {
+  int32_t n;
+  const int32_t* off;
+  const int32_t* nbr;
+};
+
+// Count a launch and check it.
+#define MP_KERNEL(ctx, ...)        \
+  do {                             \
+    __VA_ARGS__;                   \
+    ++(ctx).launches;              \
+    MP_CUDA(cudaGetLastError());   \
+  } while (0)
+
+// Stage 1 (patching.cu): compute_patches -> assignment (device, n), returns patch count.
+int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, uint64_t seed,
+                            int32_t* assignment);
+// patching.cu: enforce_connectivity on a device assignment; returns the new patch count.
+int32_t enforce_connectivity_dev(mp_context& ctx, const DGraph& g, const int32_t* in,
+                                 int32_t patch_count, int32_t* out);
+
+// ND tree (ndtree.cu).  node_of[v] receives the tree node of every vertex;
+// node_offsets (nn+1) / node_vertices (n) the flattened EliminationTree.
+void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assignment,
+                     int32_t patch_count, int32_t nd_level, int32_t* node_of,
+                     int32_t* node_offsets, int32_t* node_vertices);
+
+// Quotient (ndtree.cu): node weights (P) + positive edges, device outputs; returns #edges.
+int64_t build_quotient_dev(mp_context& ctx, const DGraph& g, const int32_t* assignment,
+                           int32_t patch_count, int64_t* node_weight, int32_t** edge_p,
+                           int32_t** edge_q, int64_t** edge_w);
+
+// Local ordering (md.cu): local_perm per node, layout of node_vertices.
+void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t nd_level,
+                          const int32_t* node_of, const int32_t* node_offsets,
+                          const int32_t* node_vertices, int32_t mode, int32_t* local_perm);
+
+// Assembly (assemble.cu): schedule + perm/inverse.  node_pos (nn+1) receives
+// the first permutation position of every node.
+void compute_perm_dev(mp_context& ctx, int32_t n, int32_t nd_level, const int32_t* node_offsets,
+                      const int32_t* node_vertices, const int32_t* local_perm, int32_t schedule,
+                      int32_t* perm, int32_t* inverse, int32_t* node_pos);
+
+// Symbolic (symbolic.cu): column counts (by position) and factor etree parents.
+void tree_fill_dev(mp_context& ctx, const DGraph& g, int32_t nd_level, const int32_t* node_of,
+                   const int32_t* node_offsets, const int32_t* node_vertices,
+                   const int32_t* local_perm, const int32_t* node_pos, const int32_t* inverse,
+                   int64_t* column_counts, int32_t* etree_parent, int64_t* nnz_L, int64_t* cost);
+
+// node_of[v] from the flattened tree (assemble.cu).
+void node_of_from_tree_dev(mp_context& ctx, int32_t n, int32_t nn, const int32_t* node_offsets,
+                           const int32_t* node_vertices, int32_t* node_of);
+
+}  // namespace mp

@@ -1,0 +1,845 @@
+// Stages 2+4 — separator extraction and the patch-guided ND tree
+// (reference core/src/{quotient,partition,etree}.cpp).
+//
+// The reference recurses depth first, keeping one master quotient updated
+// incrementally (quotient_remove, quotient.cpp:82-103) and restricting it per
+// node (restrict_quotient, :105-127).  Sibling subtrees touch disjoint patch
+// sets and no edge joins two alive vertices of different subtrees, so the
+// restricted quotient of a node equals the quotient of the node's alive
+// vertices.  The device version therefore runs level by level: every level
+// rebuilds the per-node quotients from the alive vertices (one sort of the
+// crossing-edge keys), then one CTA per node runs bipartition_quotient
+// (partition.cpp:25-163) and one CTA per node refine_separator
+// (:187-283); the super separator (:165-185) is a grid pass.  Results are
+// identical to the depth-first recursion.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "mp_context.h"
+#include "mp_device.cuh"
+
+namespace mp {
+namespace {
+
+constexpr int kFmPasses = 10;        // partition.cpp:13
+constexpr double kBalanceTol = 1.2;  // partition.hpp:34
+constexpr int kMaxNdLevel = 24;      // etree.cpp:16
+constexpr int kNodeThreads = 1024;
+constexpr int32_t kGainBias = 0x40000000;
+
+int grid_for(const mp_context& ctx, int64_t n, int threads = 256) {
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), ctx.num_sms * 16LL)));
+}
+
+__global__ void iota32(int32_t n, int32_t* a) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = i;
+}
+__global__ void fill32(int64_t n, int32_t* a, int32_t v) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    a[i] = v;
+}
+
+// ---------------------------------------------------------------- per level
+struct LevelArgs {
+  DGraph g;
+  const int32_t* assign;
+  int32_t P;
+  int32_t first;           // first node id of the level
+  int32_t width;           // nodes at the level
+  const int32_t* vlist;    // vertices grouped by node, ascending inside a node
+  const int32_t* seg_start;// per level node (local index)
+  const int32_t* seg_cnt;
+  int32_t* node_of;
+  int32_t* pw;             // patch weights at this level (P)
+  int32_t* pnode;          // node (local index) of each weighted patch
+  int32_t* np_node;        // alive patches per level node
+  int32_t* active;         // per level node
+  int32_t* lidx;           // patch -> index inside its node's patch list
+  const int32_t* plist;    // alive patches grouped by node, ascending
+  const int32_t* poff;     // per level node (width+1)
+  const int32_t* qoff;     // per patch (P+1), quotient adjacency at this level
+  const int32_t* qnbr;
+  const int32_t* qw;
+  uint8_t* side;           // per patch
+  int8_t* region;          // per vertex
+  uint8_t* in_super;       // per vertex
+  uint8_t* in_list;        // per vertex
+  int32_t* bcount;         // per level node: [2*i] left boundary, [2*i+1] right
+  int32_t* sep_list;       // scratch, vlist layout
+  int32_t* next_vlist;
+  int32_t* next_start;     // per next-level node
+  int32_t* next_cnt;
+  int32_t* stats;          // [0] moves FM, [1] moves refine (diagnostics)
+  // FM scratch (per patch, in plist layout)
+  int32_t* fm_gain;
+  int32_t* fm_fifo;        // capacity per node: poff span + edges -> allocated 2*P + E
+  const int64_t* fm_fifo_off;  // per level node
+  int32_t* fm_moves;
+  int64_t* fm_rec;         // 3 per move: cut, sw0, sw1
+};
+
+__global__ void level_weights(LevelArgs a) {
+  for (int32_t li = blockIdx.y; li < a.width; li += gridDim.y) {
+    const int32_t s0 = a.seg_start[li], cnt = a.seg_cnt[li];
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+      int32_t p = a.assign[a.vlist[s0 + i]];
+      if (atomicAdd(&a.pw[p], 1) == 0) a.pnode[p] = li;
+    }
+  }
+}
+__global__ void level_patch_counts(LevelArgs a) {
+  for (int32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < a.P; p += gridDim.x * blockDim.x)
+    if (a.pw[p] > 0) atomicAdd(&a.np_node[a.pnode[p]], 1);
+}
+__global__ void level_activity(LevelArgs a, int32_t nd_level, int32_t level, int32_t* n_active) {
+  for (int32_t li = blockIdx.x * blockDim.x + threadIdx.x; li < a.width; li += gridDim.x * blockDim.x) {
+    // etree.cpp:123-131: leaf at nd_level, below 2 vertices, or <= 1 alive patch
+    bool act = level < nd_level && a.seg_cnt[li] >= 2 && a.np_node[li] >= 2;
+    a.active[li] = act ? 1 : 0;
+    if (act) atomicAdd(n_active, 1);
+  }
+}
+__global__ void flag_alive_patches(int32_t P, const int32_t* pw, const int32_t* pnode,
+                                   const int32_t* active, int32_t* flag, int32_t* key) {
+  for (int32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x) {
+    bool ok = pw[p] > 0 && active[pnode[p]];
+    flag[p] = ok ? 1 : 0;
+    key[p] = ok ? pnode[p] : 0;
+  }
+}
+__global__ void masked_counts(int32_t width, const int32_t* active, const int32_t* np_node, int32_t* out) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= width; i += gridDim.x * blockDim.x)
+    out[i] = (i < width && active[i]) ? np_node[i] : 0;
+}
+__global__ void node_edge_count(int32_t na, const int32_t* plist, const int32_t* pnode, const int32_t* qoff,
+                                int64_t* ecnt) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
+    const int32_t p = plist[i];
+    atomicAdd(reinterpret_cast<unsigned long long*>(&ecnt[pnode[p]]),
+              static_cast<unsigned long long>(qoff[p + 1] - qoff[p] + 1));
+  }
+}
+__global__ void set_lidx(int32_t total, const int32_t* plist, const int32_t* pnode, const int32_t* poff,
+                         int32_t* lidx) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    int32_t p = plist[i];
+    lidx[p] = i - poff[pnode[p]];
+  }
+}
+// Crossing-edge keys among alive vertices of active nodes; both directions.
+__global__ void emit_crossing(LevelArgs a, uint64_t* keys, int32_t* count) {
+  for (int32_t li = blockIdx.y; li < a.width; li += gridDim.y) {
+    if (!a.active[li]) continue;
+    const int32_t s0 = a.seg_start[li], cnt = a.seg_cnt[li], node = a.first + li;
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+      const int32_t u = a.vlist[s0 + i];
+      const int32_t pu = a.assign[u];
+      for (int32_t j = a.g.off[u]; j < a.g.off[u + 1]; ++j) {
+        const int32_t v = a.g.nbr[j];
+        if (v <= u || a.node_of[v] != node) continue;
+        const int32_t pv = a.assign[v];
+        if (pv == pu) continue;
+        int32_t slot = atomicAdd(count, 2);
+        keys[slot] = (static_cast<uint64_t>(pu) << 32) | static_cast<uint32_t>(pv);
+        keys[slot + 1] = (static_cast<uint64_t>(pv) << 32) | static_cast<uint32_t>(pu);
+      }
+    }
+  }
+}
+__global__ void quotient_csr(int32_t U, const uint64_t* ukeys, const int32_t* ucnt, int32_t* qdeg,
+                             int32_t* qnbr, int32_t* qw) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < U; i += gridDim.x * blockDim.x) {
+    qnbr[i] = static_cast<int32_t>(ukeys[i] & 0xffffffffu);
+    qw[i] = ucnt[i];
+    atomicAdd(&qdeg[static_cast<int32_t>(ukeys[i] >> 32)], 1);
+  }
+}
+
+// ---------------------------------------------------------------- FM (one CTA per node)
+// bipartition_quotient, partition.cpp:25-163.
+__global__ void __launch_bounds__(kNodeThreads) fm_kernel(LevelArgs a) {
+  const int32_t li = blockIdx.x;
+  if (!a.active[li]) return;
+  const int32_t pbeg = a.poff[li], np = a.poff[li + 1] - pbeg;
+  const int32_t* pl = a.plist + pbeg;
+  int32_t* gain = a.fm_gain + pbeg;
+  int32_t* fifo = a.fm_fifo + a.fm_fifo_off[li];
+  int32_t* moves = a.fm_moves + pbeg;
+  int64_t* rec = a.fm_rec + 3LL * pbeg;
+
+  extern __shared__ uint8_t smem[];
+  // smem layout: side[np] locked/visited[np]
+  uint8_t* side = smem;
+  uint8_t* flag = smem + np;
+  __shared__ uint64_t red[32];
+  __shared__ int64_t s_total, s_left, s_cut, s_sw[2], s_best_cut, s_pass_cut;
+  __shared__ double s_thr, s_cur_imb, s_best_imb, s_pass_imb;
+  __shared__ int32_t s_nm, s_best_len, s_head, s_tail, s_u, s_stop;
+
+  int64_t tot = 0;
+  for (int32_t i = threadIdx.x; i < np; i += blockDim.x) {
+    side[i] = 1;  // right (partition.cpp:34)
+    flag[i] = 0;
+    tot += a.pw[pl[i]];
+  }
+  tot = block_sum_i64(tot, reinterpret_cast<int64_t*>(red));
+  if (threadIdx.x == 0) s_total = tot, s_left = 0, s_head = 0, s_tail = 0;
+  __syncthreads();
+
+  // ---- greedy growing from the heaviest patch (partition.cpp:53-79)
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    if (s_left * 2 >= s_total) break;
+    // pop the fifo skipping visited (warp 0 lane 0), else heaviest unvisited
+    if (threadIdx.x == 0) {
+      int32_t h = s_head;
+      while (h < s_tail && flag[fifo[h]]) ++h;
+      s_u = h < s_tail ? fifo[h++] : -1;
+      s_head = h;
+    }
+    __syncthreads();
+    if (s_u < 0) {
+      uint64_t best = 0;
+      for (int32_t i = threadIdx.x; i < np; i += blockDim.x)
+        if (!flag[i]) {
+          uint64_t k = key_max(static_cast<uint32_t>(a.pw[pl[i]]), static_cast<uint32_t>(pl[i]));
+          best = k > best ? k : best;
+        }
+      best = block_max_u64(best, red);
+      if (threadIdx.x == 0) s_u = a.lidx[key_max_id(best)];
+      __syncthreads();
+    }
+    if (threadIdx.x < 32) {
+      const int32_t u = s_u;
+      if (lane == 0) {
+        flag[u] = 1;
+        side[u] = 0;
+        s_left += a.pw[pl[u]];
+      }
+      __syncwarp();
+      const int32_t p = pl[u];
+      const int32_t e0 = a.qoff[p], e1 = a.qoff[p + 1];
+      int32_t tail = s_tail;
+      __syncwarp();
+      for (int32_t j0 = e0; j0 < e1; j0 += 32) {
+        const int32_t j = j0 + lane;
+        int32_t nb = -1;
+        if (j < e1) nb = a.lidx[a.qnbr[j]];
+        const bool push = j < e1 && !flag[nb];
+        const uint32_t m = __ballot_sync(0xffffffffu, push);
+        if (push) fifo[tail + __popc(m & ((1u << lane) - 1))] = nb;
+        tail += __popc(m);
+      }
+      if (lane == 0) s_tail = tail;
+    }
+    __syncthreads();
+  }
+  // cut of the grown split (partition.cpp:81-84)
+  int64_t cut = 0;
+  for (int32_t i = threadIdx.x; i < np; i += blockDim.x) {
+    const int32_t p = pl[i];
+    for (int32_t j = a.qoff[p]; j < a.qoff[p + 1]; ++j) {
+      const int32_t q = a.qnbr[j];
+      if (q > p && side[i] != side[a.lidx[q]]) cut += a.qw[j];
+    }
+  }
+  cut = block_sum_i64(cut, reinterpret_cast<int64_t*>(red));
+  if (threadIdx.x == 0) {
+    s_cut = cut;
+    s_sw[0] = s_left;
+    s_sw[1] = s_total - s_left;
+  }
+  __syncthreads();
+
+  // ---- FM passes with rollback to the best prefix (partition.cpp:95-159)
+  int64_t total_moves = 0;
+  for (int pass = 0; pass < kFmPasses; ++pass) {
+    for (int32_t i = threadIdx.x; i < np; i += blockDim.x) {
+      const int32_t p = pl[i];
+      int32_t val = 0;
+      for (int32_t j = a.qoff[p]; j < a.qoff[p + 1]; ++j)
+        val += side[a.lidx[a.qnbr[j]]] != side[i] ? a.qw[j] : -a.qw[j];
+      gain[i] = val;
+      flag[i] = 0;  // unlocked
+    }
+    if (threadIdx.x == 0) {
+      s_pass_cut = s_cut;
+      s_pass_imb = imbalance_of(s_sw[0], s_sw[1]);
+      s_best_cut = s_pass_cut;
+      s_best_imb = s_pass_imb;
+      s_cur_imb = s_pass_imb;
+      s_thr = kBalanceTol > s_cur_imb ? kBalanceTol : s_cur_imb;
+      s_nm = 0;
+      s_best_len = 0;
+    }
+    __syncthreads();
+    for (;;) {
+      const int64_t sw0 = s_sw[0], sw1 = s_sw[1];
+      const double thr = s_thr;
+      uint64_t best = 0;
+      for (int32_t i = threadIdx.x; i < np; i += blockDim.x) {
+        if (flag[i]) continue;
+        const int32_t s = side[i];
+        const int64_t w = a.pw[pl[i]];
+        const int64_t ns = (s ? sw1 : sw0) - w, nt = (s ? sw0 : sw1) + w;
+        if (ns <= 0) continue;  // never empty a side
+        if (imbalance_of(ns, nt) > thr) continue;
+        const uint64_t k = key_max(static_cast<uint32_t>(gain[i] + kGainBias), static_cast<uint32_t>(i));
+        best = k > best ? k : best;
+      }
+      best = block_max_u64(best, red);
+      if (best == 0) break;
+      const int32_t ch = static_cast<int32_t>(key_max_id(best));
+      if (threadIdx.x == 0) {
+        flag[ch] = 1;
+        const int32_t m = s_nm++;
+        moves[m] = ch;
+        rec[3 * m] = s_cut, rec[3 * m + 1] = s_sw[0], rec[3 * m + 2] = s_sw[1];
+        const int32_t s = side[ch];
+        const int64_t w = a.pw[pl[ch]];
+        s_sw[s] -= w;
+        s_sw[1 - s] += w;
+        side[ch] = static_cast<uint8_t>(1 - s);
+        s_cut -= gain[ch];
+      }
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        const int32_t p = pl[ch];
+        const uint8_t sc = side[ch];
+        for (int32_t j = a.qoff[p] + lane; j < a.qoff[p + 1]; j += 32) {
+          const int32_t nb = a.lidx[a.qnbr[j]];
+          if (flag[nb]) continue;
+          gain[nb] += side[nb] == sc ? -2 * a.qw[j] : 2 * a.qw[j];
+        }
+        if (lane == 0) {
+          const double imb = imbalance_of(s_sw[0], s_sw[1]);
+          if (s_cut < s_best_cut || (s_cut == s_best_cut && imb < s_best_imb)) {
+            s_best_cut = s_cut;
+            s_best_imb = imb;
+            s_best_len = s_nm;
+          }
+          s_cur_imb = imb;
+          s_thr = kBalanceTol > imb ? kBalanceTol : imb;
+        }
+      }
+      __syncthreads();
+    }
+    const int32_t nm = s_nm, bl = s_best_len;
+    total_moves += nm;
+    for (int32_t m = bl + threadIdx.x; m < nm; m += blockDim.x) side[moves[m]] ^= 1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (nm > bl) {
+        s_cut = rec[3 * bl];
+        s_sw[0] = rec[3 * bl + 1];
+        s_sw[1] = rec[3 * bl + 2];
+      }
+      const bool improved = s_best_cut < s_pass_cut || (s_best_cut == s_pass_cut && s_best_imb < s_pass_imb);
+      s_stop = improved ? 0 : 1;
+    }
+    __syncthreads();
+    if (s_stop) break;
+  }
+  for (int32_t i = threadIdx.x; i < np; i += blockDim.x) a.side[pl[i]] = side[i];
+  if (threadIdx.x == 0) atomicAdd(&a.stats[0], static_cast<int32_t>(total_moves));
+}
+
+// ---------------------------------------------------------------- super separator
+// partition.cpp:165-185 plus refine's boundary counts (:212-214).
+__global__ void super_pass(LevelArgs a) {
+  for (int32_t li = blockIdx.y; li < a.width; li += gridDim.y) {
+    if (!a.active[li]) continue;
+    const int32_t s0 = a.seg_start[li], cnt = a.seg_cnt[li], node = a.first + li;
+    int32_t nl = 0, nr = 0;
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+      const int32_t u = a.vlist[s0 + i];
+      const uint8_t su = a.side[a.assign[u]];
+      uint8_t sup = 0;
+      for (int32_t j = a.g.off[u]; j < a.g.off[u + 1] && !sup; ++j) {
+        const int32_t v = a.g.nbr[j];
+        if (a.node_of[v] == node && a.side[a.assign[v]] != su) sup = 1;
+      }
+      a.region[u] = static_cast<int8_t>(su);
+      a.in_super[u] = sup;
+      if (sup) (su == 0 ? nl : nr)++;
+    }
+    if (nl) atomicAdd(&a.bcount[2 * li], nl);
+    if (nr) atomicAdd(&a.bcount[2 * li + 1], nr);
+  }
+}
+
+// ---------------------------------------------------------------- refine (one CTA per node)
+struct RefKey {
+  uint64_t hi, lo;  // (new_size, new_imb bits, vertex) lexicographic
+};
+__device__ __forceinline__ bool ref_less(const RefKey& x, const RefKey& y) {
+  return x.hi < y.hi || (x.hi == y.hi && x.lo < y.lo);
+}
+__device__ __forceinline__ RefKey warp_min_ref(RefKey k) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    RefKey t;
+    t.hi = __shfl_xor_sync(0xffffffffu, k.hi, o);
+    t.lo = __shfl_xor_sync(0xffffffffu, k.lo, o);
+    if (ref_less(t, k)) k = t;
+  }
+  return k;
+}
+
+__global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a, int32_t next_first_local) {
+  const int32_t li = blockIdx.x;
+  const int32_t s0 = a.seg_start[li], cnt = a.seg_cnt[li], node = a.first + li;
+  __shared__ int32_t shi[32];
+  __shared__ RefKey sred[32];
+  __shared__ int64_t s_rw[2], s_size;
+  __shared__ double s_imb;
+  __shared__ int32_t s_list, s_mv, s_own, s_moves;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int32_t lc = 2 * li, rc = 2 * li + 1;  // children, local to the next level
+  if (!a.active[li]) {
+    if (threadIdx.x == 0) {
+      a.next_start[lc] = s0, a.next_cnt[lc] = 0;
+      a.next_start[rc] = s0, a.next_cnt[rc] = 0;
+    }
+    return;
+  }
+  const int32_t* seg = a.vlist + s0;
+  int32_t* list = a.sep_list + s0;
+  // initial separator: the smaller boundary, ties to the left (partition.cpp:212-222)
+  const int8_t take = a.bcount[2 * li] <= a.bcount[2 * li + 1] ? 0 : 1;
+  {
+    int32_t run = 0;
+    int32_t c0 = 0, c1 = 0;
+    for (int32_t i0 = 0; i0 < cnt; i0 += blockDim.x) {
+      const int32_t i = i0 + threadIdx.x;
+      int32_t v = -1, in = 0;
+      if (i < cnt) {
+        v = seg[i];
+        in = a.in_super[v] && a.region[v] == take;
+      }
+      int32_t tot;
+      const int32_t e = block_excl_scan(in, shi, &tot);
+      if (in) {
+        list[run + e] = v;
+        a.region[v] = 2;
+        a.in_list[v] = 1;
+      } else if (i < cnt) {
+        (a.region[v] == 0 ? c0 : c1)++;
+      }
+      run += tot;
+    }
+    int64_t r0 = block_sum_i64(c0, reinterpret_cast<int64_t*>(sred));
+    int64_t r1 = block_sum_i64(c1, reinterpret_cast<int64_t*>(sred));
+    if (threadIdx.x == 0) {
+      s_list = run;
+      s_size = run;
+      s_rw[0] = r0, s_rw[1] = r1;
+      s_imb = imbalance_of(r0, r1);
+      s_moves = 0;
+    }
+    __syncthreads();
+  }
+  // greedy moves (partition.cpp:235-274)
+  for (;;) {
+    const int64_t cur = s_size;
+    const double cimb = s_imb;
+    const double thr = kBalanceTol > cimb ? kBalanceTol : cimb;
+    const int64_t rw0 = s_rw[0], rw1 = s_rw[1];
+    const int32_t nl = s_list;
+    RefKey best{~0ull, ~0ull};
+    for (int32_t i = threadIdx.x; i < nl; i += blockDim.x) {
+      const int32_t v = list[i];
+      if (a.region[v] != 2) continue;
+      const int8_t own = static_cast<int8_t>(a.side[a.assign[v]]), opp = 1 - own;
+      int32_t pull = 0;
+      for (int32_t j = a.g.off[v]; j < a.g.off[v + 1]; ++j) {
+        const int32_t w = a.g.nbr[j];
+        if (a.node_of[w] == node && a.region[w] == opp) ++pull;
+      }
+      const int64_t ns = cur - 1 + pull;
+      if (ns > cur) continue;
+      const double ni = imbalance_of((own ? rw1 : rw0) + 1, (own ? rw0 : rw1) - pull);
+      if (ni > thr) continue;
+      if (!(ns < cur || ni < cimb)) continue;
+      const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(ni));
+      RefKey k{(static_cast<uint64_t>(ns) << 32) | (bits >> 32),
+               ((bits & 0xffffffffull) << 32) | static_cast<uint32_t>(v)};
+      if (ref_less(k, best)) best = k;
+    }
+    best = warp_min_ref(best);
+    if (lane == 0) sred[wid] = best;
+    __syncthreads();
+    if (wid == 0) {
+      RefKey k = lane < (blockDim.x >> 5) ? sred[lane] : RefKey{~0ull, ~0ull};
+      k = warp_min_ref(k);
+      if (lane == 0) {
+        s_mv = k.hi == ~0ull ? -1 : static_cast<int32_t>(k.lo & 0xffffffffu);
+      }
+    }
+    __syncthreads();
+    const int32_t mv = s_mv;
+    if (mv < 0) break;
+    if (wid == 0) {
+      const int8_t own = static_cast<int8_t>(a.side[a.assign[mv]]), opp = 1 - own;
+      int32_t pulled = 0;
+      int32_t tail = s_list;
+      for (int32_t j0 = a.g.off[mv]; j0 < a.g.off[mv + 1]; j0 += 32) {
+        const int32_t j = j0 + lane;
+        int32_t w = -1;
+        bool pull = false;
+        if (j < a.g.off[mv + 1]) {
+          w = a.g.nbr[j];
+          pull = a.node_of[w] == node && a.region[w] == opp;
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, pull);
+        const bool app = pull && !a.in_list[w];
+        const uint32_t ma = __ballot_sync(0xffffffffu, app);
+        if (pull) a.region[w] = 2;
+        if (app) {
+          list[tail + __popc(ma & ((1u << lane) - 1))] = w;
+          a.in_list[w] = 1;
+        }
+        tail += __popc(ma);
+        pulled += __popc(m);
+      }
+      if (lane == 0) {
+        a.region[mv] = own;
+        s_rw[own] += 1;
+        s_rw[opp] -= pulled;
+        s_size = s_size - 1 + pulled;
+        s_imb = imbalance_of(s_rw[0], s_rw[1]);
+        s_list = tail;
+        ++s_moves;
+      }
+    }
+    __syncthreads();
+  }
+  // split the node: separator stays at `node`, sides go to the children
+  // (stable, so each child's vertex list stays ascending)
+  int32_t* out = a.next_vlist + s0;
+  int32_t nleft_total;
+  {
+    int32_t c = 0;
+    for (int32_t i = threadIdx.x; i < cnt; i += blockDim.x) c += a.region[seg[i]] == 0;
+    nleft_total = static_cast<int32_t>(block_sum_i64(c, reinterpret_cast<int64_t*>(sred)));
+  }
+  int32_t runl = 0, runr = 0;
+  for (int32_t i0 = 0; i0 < cnt; i0 += blockDim.x) {
+    const int32_t i = i0 + threadIdx.x;
+    int32_t v = -1;
+    int8_t r = 3;
+    if (i < cnt) {
+      v = seg[i];
+      r = a.region[v];
+    }
+    int32_t tl, tr;
+    const int32_t el = block_excl_scan(r == 0 ? 1 : 0, shi, &tl);
+    const int32_t er = block_excl_scan(r == 1 ? 1 : 0, shi, &tr);
+    if (r == 0) {
+      out[runl + el] = v;
+      a.node_of[v] = 2 * node + 1;
+    } else if (r == 1) {
+      out[nleft_total + runr + er] = v;
+      a.node_of[v] = 2 * node + 2;
+    }
+    runl += tl, runr += tr;
+  }
+  for (int32_t i = threadIdx.x; i < s_list; i += blockDim.x) a.in_list[list[i]] = 0;
+  if (threadIdx.x == 0) {
+    a.next_start[lc] = s0, a.next_cnt[lc] = runl;
+    a.next_start[rc] = s0 + runl, a.next_cnt[rc] = runr;
+    atomicAdd(&a.stats[1], s_moves);
+  }
+  (void)next_first_local;
+}
+
+template <class T>
+void cub_sort_keys(const T* in, T* out, int64_t n, int end_bit, cudaStream_t s) {
+  size_t tmp = 0;
+  MP_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, in, out, n, 0, end_bit, s));
+  DevBuf<char> t(tmp, s);
+  MP_CUDA(cub::DeviceRadixSort::SortKeys(t.get(), tmp, in, out, n, 0, end_bit, s));
+}
+
+int bits_for(int64_t x) {
+  int b = 1;
+  while ((1LL << b) <= x) ++b;
+  return b;
+}
+
+// Per-patch quotient CSR of the crossing-edge keys (sorted, run-length
+// encoded): qoff (P+1), qnbr, qw.  Returns the number of directed entries.
+int64_t quotient_from_keys(mp_context& ctx, uint64_t* keys, int64_t nkeys, int32_t P, DevBuf<int32_t>& qoff,
+                           DevBuf<int32_t>& qnbr, DevBuf<int32_t>& qw) {
+  cudaStream_t s = ctx.stream;
+  DevBuf<uint64_t> sorted(std::max<int64_t>(nkeys, 1), s), ukeys(std::max<int64_t>(nkeys, 1), s);
+  DevBuf<int32_t> ucnt(std::max<int64_t>(nkeys, 1), s), nruns(1, s), qdeg(P + 1, s);
+  MP_CUDA(cudaMemsetAsync(qdeg, 0, sizeof(int32_t) * (P + 1), s));
+  int32_t U = 0;
+  if (nkeys > 0) {
+    const int pb = bits_for(P);
+    cub_sort_keys(keys, sorted.get(), nkeys, 32 + pb, s);
+    size_t tmp = 0;
+    MP_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tmp, sorted.get(), ukeys.get(), ucnt.get(), nruns.get(),
+                                               nkeys, s));
+    DevBuf<char> t(tmp, s);
+    MP_CUDA(cub::DeviceRunLengthEncode::Encode(t.get(), tmp, sorted.get(), ukeys.get(), ucnt.get(), nruns.get(),
+                                               nkeys, s));
+    MP_CUDA(cudaMemcpyAsync(&U, nruns.get(), 4, cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+  }
+  qoff.alloc(P + 1, s);
+  qnbr.alloc(std::max(U, 1), s);
+  qw.alloc(std::max(U, 1), s);
+  if (U > 0)
+    MP_KERNEL(ctx, quotient_csr<<<grid_for(ctx, U), 256, 0, s>>>(U, ukeys, ucnt, qdeg, qnbr, qw));
+  size_t tmp = 0;
+  MP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, qdeg.get(), qoff.get(), P + 1, s));
+  DevBuf<char> t(tmp, s);
+  MP_CUDA(cub::DeviceScan::ExclusiveSum(t.get(), tmp, qdeg.get(), qoff.get(), P + 1, s));
+  return U;
+}
+
+__global__ void node_hist(int32_t n, const int32_t* node_of, int32_t* cnt) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    atomicAdd(&cnt[node_of[v]], 1);
+}
+
+__global__ void count_weights_all(int32_t n, const int32_t* assign, int32_t* pw) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    atomicAdd(&pw[assign[v]], 1);
+}
+__global__ void emit_crossing_all(DGraph g, const int32_t* assign, uint64_t* keys, int32_t* count) {
+  for (int32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < g.n; u += gridDim.x * blockDim.x) {
+    const int32_t pu = assign[u];
+    for (int32_t j = g.off[u]; j < g.off[u + 1]; ++j) {
+      const int32_t v = g.nbr[j];
+      if (v <= u) continue;
+      const int32_t pv = assign[v];
+      if (pv == pu) continue;
+      int32_t lo = min(pu, pv), hi = max(pu, pv);
+      keys[atomicAdd(count, 1)] = (static_cast<uint64_t>(lo) << 32) | static_cast<uint32_t>(hi);
+    }
+  }
+}
+__global__ void check_assign(int32_t n, const int32_t* assign, int32_t P, int32_t* bad) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    if (assign[v] < 0 || assign[v] >= P) atomicMin(bad, v);
+}
+__global__ void split_keys(int32_t U, const uint64_t* k, const int32_t* c, int32_t* ep, int32_t* eq,
+                           int64_t* ew) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < U; i += gridDim.x * blockDim.x) {
+    ep[i] = static_cast<int32_t>(k[i] >> 32);
+    eq[i] = static_cast<int32_t>(k[i] & 0xffffffffu);
+    ew[i] = c[i];
+  }
+}
+__global__ void widen(int32_t P, const int32_t* a, int64_t* b) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) b[i] = a[i];
+}
+
+void validate_assignment(mp_context& ctx, int32_t n, const int32_t* assign, int32_t P) {
+  cudaStream_t s = ctx.stream;
+  DevBuf<int32_t> bad(1, s);
+  MP_KERNEL(ctx, fill32<<<1, 32, 0, s>>>(1, bad, 0x7fffffff));
+  MP_KERNEL(ctx, check_assign<<<grid_for(ctx, n), 256, 0, s>>>(n, assign, P, bad));
+  int32_t h;
+  MP_CUDA(cudaMemcpyAsync(&h, bad, 4, cudaMemcpyDeviceToHost, s));
+  MP_CUDA(cudaStreamSynchronize(s));
+  if (h != 0x7fffffff) {
+    int32_t pv = 0;
+    MP_CUDA(cudaMemcpy(&pv, assign + h, 4, cudaMemcpyDeviceToHost));
+    throw Error(MP_EINVAL, "patch id " + std::to_string(pv) + " out of range for vertex " + std::to_string(h));
+  }
+}
+
+}  // namespace
+
+int64_t build_quotient_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, int32_t P,
+                           int64_t* node_weight, int32_t** edge_p, int32_t** edge_q, int64_t** edge_w) {
+  cudaStream_t s = ctx.stream;
+  validate_assignment(ctx, g.n, assign, P);
+  DevBuf<int32_t> pw(std::max(P, 1), s), cnt(1, s);
+  MP_CUDA(cudaMemsetAsync(pw, 0, sizeof(int32_t) * std::max(P, 1), s));
+  MP_KERNEL(ctx, count_weights_all<<<grid_for(ctx, g.n), 256, 0, s>>>(g.n, assign, pw));
+  if (P > 0) MP_KERNEL(ctx, widen<<<grid_for(ctx, P), 256, 0, s>>>(P, pw, node_weight));
+  int32_t m2 = 0;
+  MP_CUDA(cudaMemcpyAsync(&m2, g.off + g.n, 4, cudaMemcpyDeviceToHost, s));
+  MP_CUDA(cudaStreamSynchronize(s));
+  DevBuf<uint64_t> keys(std::max(m2 / 2, 1), s), sorted(std::max(m2 / 2, 1), s), uk(std::max(m2 / 2, 1), s);
+  DevBuf<int32_t> uc(std::max(m2 / 2, 1), s), nr(1, s);
+  MP_CUDA(cudaMemsetAsync(cnt, 0, 4, s));
+  MP_KERNEL(ctx, emit_crossing_all<<<grid_for(ctx, g.n), 256, 0, s>>>(g, assign, keys, cnt));
+  int32_t nk = 0;
+  MP_CUDA(cudaMemcpyAsync(&nk, cnt, 4, cudaMemcpyDeviceToHost, s));
+  MP_CUDA(cudaStreamSynchronize(s));
+  int32_t U = 0;
+  if (nk > 0) {
+    cub_sort_keys(keys.get(), sorted.get(), nk, 32 + bits_for(P), s);
+    size_t tmp = 0;
+    MP_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, tmp, sorted.get(), uk.get(), uc.get(), nr.get(), nk, s));
+    DevBuf<char> t(tmp, s);
+    MP_CUDA(cub::DeviceRunLengthEncode::Encode(t.get(), tmp, sorted.get(), uk.get(), uc.get(), nr.get(), nk, s));
+    MP_CUDA(cudaMemcpyAsync(&U, nr.get(), 4, cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+  }
+  if (edge_p) {
+    MP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(edge_p), sizeof(int32_t) * std::max(U, 1), s));
+    MP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(edge_q), sizeof(int32_t) * std::max(U, 1), s));
+    MP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(edge_w), sizeof(int64_t) * std::max(U, 1), s));
+    if (U > 0) MP_KERNEL(ctx, split_keys<<<grid_for(ctx, U), 256, 0, s>>>(U, uk, uc, *edge_p, *edge_q, *edge_w));
+  }
+  return U;
+}
+
+void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, int32_t P, int32_t L,
+                     int32_t* node_of, int32_t* node_offsets, int32_t* node_vertices) {
+  if (L < 0 || L > kMaxNdLevel) throw Error(MP_EINVAL, "nd_level out of range");
+  cudaStream_t s = ctx.stream;
+  const int32_t n = g.n;
+  const int64_t nn = (1LL << (L + 1)) - 1;
+  validate_assignment(ctx, n, assign, P);
+  int32_t m2 = 0;
+  if (n > 0) {
+    MP_CUDA(cudaMemcpyAsync(&m2, g.off + n, 4, cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+  }
+  const int32_t Pm = std::max(P, 1);
+  DevBuf<int32_t> vl_a(std::max(n, 1), s), vl_b(std::max(n, 1), s), seplist(std::max(n, 1), s);
+  DevBuf<int32_t> pw(Pm, s), pnode(Pm, s), lidx(Pm, s), flag(Pm, s), pkey(Pm, s), pkey_out(Pm, s);
+  DevBuf<int32_t> alive_p(Pm, s), plist(Pm, s), fm_gain(Pm, s), fm_moves(Pm, s), stats(2, s), cnt(4, s);
+  DevBuf<int64_t> fm_rec(3LL * Pm, s);
+  DevBuf<int8_t> region(std::max(n, 1), s);
+  DevBuf<uint8_t> in_super(std::max(n, 1), s), in_list(std::max(n, 1), s), side(Pm, s);
+  DevBuf<uint64_t> keys(std::max(m2, 1), s);
+  MP_CUDA(cudaMemsetAsync(in_list, 0, std::max(n, 1), s));
+  MP_CUDA(cudaMemsetAsync(stats, 0, 8, s));
+  MP_KERNEL(ctx, fill32<<<grid_for(ctx, n), 256, 0, s>>>(n, node_of, 0));
+  MP_KERNEL(ctx, iota32<<<grid_for(ctx, n), 256, 0, s>>>(n, vl_a));
+
+  // level-node segment tables (host-built for the root, device afterwards)
+  int32_t width = 1;
+  DevBuf<int32_t> seg_start(1, s), seg_cnt(1, s);
+  MP_CUDA(cudaMemsetAsync(seg_start, 0, 4, s));
+  MP_CUDA(cudaMemcpyAsync(seg_cnt.get(), &n, 4, cudaMemcpyHostToDevice, s));
+  int32_t* cur_list = vl_a.get();
+  int32_t* nxt_list = vl_b.get();
+
+  for (int32_t level = 0; level < L && n > 0; ++level) {
+    const int32_t first = (1 << level) - 1;
+    int32_t na_level = 0;
+    DevBuf<int32_t> np_node(width, s), active(width, s), poff(width + 1, s), bcount(2 * width, s),
+        next_start(2 * width, s), next_cnt(2 * width, s);
+    DevBuf<int64_t> fifo_off(width + 1, s);
+    MP_CUDA(cudaMemsetAsync(pw, 0, sizeof(int32_t) * Pm, s));
+    MP_CUDA(cudaMemsetAsync(np_node, 0, sizeof(int32_t) * width, s));
+    MP_CUDA(cudaMemsetAsync(bcount, 0, sizeof(int32_t) * 2 * width, s));
+    MP_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * 4, s));
+    LevelArgs a{};
+    a.g = g, a.assign = assign, a.P = P, a.first = first, a.width = width;
+    a.vlist = cur_list, a.seg_start = seg_start, a.seg_cnt = seg_cnt, a.node_of = node_of;
+    a.pw = pw, a.pnode = pnode, a.np_node = np_node, a.active = active, a.lidx = lidx;
+    a.side = side, a.region = region, a.in_super = in_super, a.in_list = in_list, a.bcount = bcount;
+    a.sep_list = seplist, a.next_vlist = nxt_list, a.next_start = next_start, a.next_cnt = next_cnt;
+    a.stats = stats, a.fm_gain = fm_gain, a.fm_moves = fm_moves, a.fm_rec = fm_rec;
+    const dim3 lgrid(std::max(1, grid_for(ctx, n) / std::max(1, width)), std::min(width, 65535));
+    MP_KERNEL(ctx, level_weights<<<lgrid, 256, 0, s>>>(a));
+    MP_KERNEL(ctx, level_patch_counts<<<grid_for(ctx, P), 256, 0, s>>>(a));
+    MP_KERNEL(ctx, level_activity<<<grid_for(ctx, width), 256, 0, s>>>(a, L, level, cnt.get()));
+    // alive patches of active nodes, grouped by node, ascending
+    MP_KERNEL(ctx, flag_alive_patches<<<grid_for(ctx, P), 256, 0, s>>>(P, pw, pnode, active, flag, pkey));
+    {
+      DevBuf<int32_t> ids(Pm, s), sel(Pm, s), selkey(Pm, s);
+      MP_KERNEL(ctx, iota32<<<grid_for(ctx, P), 256, 0, s>>>(P, ids));
+      size_t tmp = 0;
+      MP_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, ids.get(), flag.get(), sel.get(), cnt.get() + 1, P, s));
+      DevBuf<char> t(tmp, s);
+      MP_CUDA(cub::DeviceSelect::Flagged(t.get(), tmp, ids.get(), flag.get(), sel.get(), cnt.get() + 1, P, s));
+      MP_CUDA(cub::DeviceSelect::Flagged(nullptr, tmp, pkey.get(), flag.get(), selkey.get(), cnt.get() + 2, P, s));
+      DevBuf<char> t2(tmp, s);
+      MP_CUDA(cub::DeviceSelect::Flagged(t2.get(), tmp, pkey.get(), flag.get(), selkey.get(), cnt.get() + 2, P, s));
+      int32_t hc[2];
+      MP_CUDA(cudaMemcpyAsync(hc, cnt.get(), 8, cudaMemcpyDeviceToHost, s));
+      MP_CUDA(cudaStreamSynchronize(s));
+      if (hc[0] == 0) break;  // no active node at this level: the tree is complete
+      const int32_t na = hc[1];
+      // stable radix sort by node keeps ascending patch ids inside each node
+      size_t tmp2 = 0;
+      const int nb = bits_for(width);
+      MP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp2, selkey.get(), pkey_out.get(), sel.get(), plist.get(),
+                                              na, 0, nb, s));
+      DevBuf<char> t3(tmp2, s);
+      MP_CUDA(cub::DeviceRadixSort::SortPairs(t3.get(), tmp2, selkey.get(), pkey_out.get(), sel.get(), plist.get(),
+                                              na, 0, nb, s));
+      // poff: exclusive scan of np_node masked by activity
+      DevBuf<int32_t> npm(width + 1, s);
+      MP_KERNEL(ctx, masked_counts<<<grid_for(ctx, width + 1), 256, 0, s>>>(width, active, np_node, npm));
+      size_t tmp3 = 0;
+      MP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp3, npm.get(), poff.get(), width + 1, s));
+      DevBuf<char> t4(tmp3, s);
+      MP_CUDA(cub::DeviceScan::ExclusiveSum(t4.get(), tmp3, npm.get(), poff.get(), width + 1, s));
+      na_level = na;
+      MP_KERNEL(ctx, set_lidx<<<grid_for(ctx, na), 256, 0, s>>>(na, plist, pnode, poff, lidx));
+    }
+    a.plist = plist, a.poff = poff;
+    // quotient of the alive vertices, per node
+    MP_CUDA(cudaMemsetAsync(cnt.get() + 3, 0, 4, s));
+    MP_KERNEL(ctx, emit_crossing<<<lgrid, 256, 0, s>>>(a, keys, cnt.get() + 3));
+    int32_t nkeys = 0;
+    MP_CUDA(cudaMemcpyAsync(&nkeys, cnt.get() + 3, 4, cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+    DevBuf<int32_t> qoff, qnbr, qw;
+    const int64_t U = quotient_from_keys(ctx, keys, nkeys, P, qoff, qnbr, qw);
+    a.qoff = qoff, a.qnbr = qnbr, a.qw = qw;
+    // fifo slab per node: every push follows a directed quotient entry of the
+    // node, so its entries + 1 bound the pushes (partition.cpp:76-77)
+    DevBuf<int64_t> ecnt(width + 1, s);
+    MP_CUDA(cudaMemsetAsync(ecnt, 0, sizeof(int64_t) * (width + 1), s));
+    if (na_level > 0)
+      MP_KERNEL(ctx, node_edge_count<<<grid_for(ctx, na_level), 256, 0, s>>>(na_level, plist, pnode, qoff, ecnt));
+    {
+      size_t tmp = 0;
+      MP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ecnt.get(), fifo_off.get(), width + 1, s));
+      DevBuf<char> t(tmp, s);
+      MP_CUDA(cub::DeviceScan::ExclusiveSum(t.get(), tmp, ecnt.get(), fifo_off.get(), width + 1, s));
+    }
+    DevBuf<int32_t> fifo(U + na_level + 1, s);
+    a.fm_fifo = fifo, a.fm_fifo_off = fifo_off;
+    // bipartition per node
+    const int32_t maxnp = na_level;
+    const size_t fm_smem = 2 * static_cast<size_t>(maxnp) + 16;
+    if (fm_smem > 48 * 1024)
+      MP_CUDA(cudaFuncSetAttribute(fm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fm_smem)));
+    MP_KERNEL(ctx, fm_kernel<<<width, kNodeThreads, fm_smem, s>>>(a));
+    MP_KERNEL(ctx, super_pass<<<lgrid, 256, 0, s>>>(a));
+    MP_KERNEL(ctx, refine_kernel<<<width, kNodeThreads, 0, s>>>(a, 0));
+    // next level
+    seg_start = std::move(next_start);
+    seg_cnt = std::move(next_cnt);
+    std::swap(cur_list, nxt_list);
+    width *= 2;
+  }
+  // flatten: stable sort of vertices by node id (ascending vertex inside a node)
+  if (n > 0) {
+    DevBuf<int32_t> ids(n, s), kout(n, s), hist(nn + 1, s);
+    MP_KERNEL(ctx, iota32<<<grid_for(ctx, n), 256, 0, s>>>(n, ids));
+    size_t tmp = 0;
+    const int nb = bits_for(nn);
+    MP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, node_of, kout.get(), ids.get(), node_vertices, n, 0, nb, s));
+    DevBuf<char> t(tmp, s);
+    MP_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, node_of, kout.get(), ids.get(), node_vertices, n, 0, nb, s));
+    MP_CUDA(cudaMemsetAsync(hist, 0, sizeof(int32_t) * (nn + 1), s));
+    MP_KERNEL(ctx, node_hist<<<grid_for(ctx, n), 256, 0, s>>>(n, node_of, hist));
+    size_t tmp2 = 0;
+    MP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp2, hist.get(), node_offsets, nn + 1, s));
+    DevBuf<char> t2(tmp2, s);
+    MP_CUDA(cub::DeviceScan::ExclusiveSum(t2.get(), tmp2, hist.get(), node_offsets, nn + 1, s));
+  } else {
+    MP_CUDA(cudaMemsetAsync(node_offsets, 0, sizeof(int32_t) * (nn + 1), s));
+  }
+}
+
+}  // namespace mp

@@ -1,0 +1,1055 @@
+// Stage 1 — mesh patch partitioning (reference core/src/patching.cpp).
+//
+//   connected components   graph.cpp:183-205   union-find hooking to the min id
+//   farthest-point seeds   patching.cpp:26-65  one CTA per component, tile-max tree
+//   Lloyd assign/recenter  patching.cpp:69-139 one cooperative persistent kernel,
+//                                              level-synchronous BFS, atomicMin ties
+//   enforce_connectivity   patching.cpp:347-384 same-patch union-find + fresh ids
+//   repair_sizes           patching.cpp:149-291 one CTA, member chains
+//
+// Every tie-break of the reference is reproduced exactly:
+// FPS argmax = (dist desc, id asc); assign = lower label on equal distance;
+// recenter = deepest, then lowest id; repair = (size, id) orders.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "mp_context.h"
+#include "mp_device.cuh"
+
+namespace mp {
+namespace {
+
+constexpr int kLloydRounds = 10;  // patching.cpp:15
+constexpr int kTile = 256;        // FPS argmax tile (positions in the component list)
+constexpr int kFpsThreads = 1024;
+constexpr int kTouchCap = 2048;   // touched-tile list capacity per round (overflow = full rescan)
+
+enum CompMode : int32_t { kModeSingletons = 0, kModeOne = 1, kModeFps = 2 };
+
+__host__ __device__ inline uint64_t splitmix64(uint64_t x) {  // patching.cpp:17-22
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d649bb133111ebULL;
+  return x ^ (x >> 31);
+}
+
+// ------------------------------------------------------------ union-find CC
+__device__ __forceinline__ int32_t uf_find(int32_t* par, int32_t x) {
+  volatile int32_t* vp = par;
+  for (;;) {
+    int32_t p = vp[x];
+    if (p == x) return x;
+    int32_t gp = vp[p];
+    if (gp == p) return p;
+    vp[x] = gp;  // path halving; gp is an ancestor, benign race
+    x = gp;
+  }
+}
+
+__global__ void uf_init(int32_t n, int32_t* par) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    par[v] = v;
+}
+
+// Hook the larger root under the smaller one, so every root is the minimum
+// vertex of its set.  label != nullptr restricts to edges inside a label class.
+__global__ void uf_hook(DGraph g, int32_t* par, const int32_t* label) {
+  for (int32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < g.n; u += gridDim.x * blockDim.x) {
+    const int32_t lu = label ? label[u] : 0;
+    for (int32_t j = g.off[u]; j < g.off[u + 1]; ++j) {
+      int32_t v = g.nbr[j];
+      if (v <= u) continue;
+      if (label && label[v] != lu) continue;
+      int32_t ru = uf_find(par, u), rv = uf_find(par, v);
+      while (ru != rv) {
+        if (ru < rv) {
+          int32_t t = ru;
+          ru = rv;
+          rv = t;
+        }
+        int32_t old = atomicCAS(&par[ru], ru, rv);
+        if (old == ru) break;
+        ru = uf_find(par, old);
+        rv = uf_find(par, rv);
+      }
+    }
+  }
+}
+
+__global__ void uf_compress(int32_t n, int32_t* par) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    par[v] = uf_find(par, v);
+}
+
+void union_find(mp_context& ctx, const DGraph& g, const int32_t* label, int32_t* par) {
+  const int blocks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(g.n, 256), ctx.num_sms * 8));
+  MP_KERNEL(ctx, uf_init<<<blocks, 256, 0, ctx.stream>>>(g.n, par));
+  MP_KERNEL(ctx, uf_hook<<<blocks, 256, 0, ctx.stream>>>(g, par, label));
+  MP_KERNEL(ctx, uf_compress<<<blocks, 256, 0, ctx.stream>>>(g.n, par));
+}
+
+// ------------------------------------------------------------ components
+__global__ void root_flags(int32_t n, const int32_t* par, int32_t* flag) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    flag[v] = par[v] == v ? 1 : 0;
+}
+__global__ void comp_of_kernel(int32_t n, const int32_t* par, const int32_t* rank, int32_t* comp_of,
+                               int32_t* comp_size) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    int32_t c = rank[par[v]];
+    comp_of[v] = c;
+    atomicAdd(&comp_size[c], 1);
+  }
+}
+__global__ void iota_kernel(int32_t n, int32_t* a) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    a[v] = v;
+}
+__global__ void scatter_pos(int32_t n, const int32_t* list, int32_t* pos_of) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    pos_of[list[i]] = i;
+}
+
+// Per-component plan (patching.cpp:307-322): k = max(1, llround(|comp|/target)),
+// mode, patch base, FPS tile bases.  One CTA, chunked block scans.
+__global__ void plan_components(int32_t C, const int32_t* comp_size, int32_t target,
+                                int32_t* comp_start, int32_t* comp_k, int32_t* comp_mode,
+                                int32_t* comp_base, int32_t* tile_base, int32_t* super_base,
+                                int32_t* totals /* [0]=patches [1]=tiles [2]=supers */) {
+  __shared__ int32_t sh[32];
+  int32_t run_start = 0, run_base = 0, run_tile = 0, run_super = 0;
+  for (int32_t c0 = 0; c0 < C; c0 += blockDim.x) {
+    int32_t c = c0 + threadIdx.x;
+    int32_t sz = 0, k = 0, np = 0, nt = 0, ns = 0, mode = 0;
+    if (c < C) {
+      sz = comp_size[c];
+      long long kk = llround(static_cast<double>(sz) / static_cast<double>(target));
+      k = kk < 1 ? 1 : static_cast<int32_t>(kk);
+      if (k >= sz) mode = kModeSingletons, np = sz;
+      else if (k == 1) mode = kModeOne, np = 1;
+      else {
+        mode = kModeFps, np = k;
+        nt = static_cast<int32_t>(ceil_div(sz, kTile));
+        ns = static_cast<int32_t>(ceil_div(nt, kTile));
+      }
+    }
+    int32_t tot;
+    int32_t es = block_excl_scan(sz, sh, &tot);
+    int32_t add_s = tot;
+    int32_t eb = block_excl_scan(np, sh, &tot);
+    int32_t add_b = tot;
+    int32_t et = block_excl_scan(nt, sh, &tot);
+    int32_t add_t = tot;
+    int32_t eu = block_excl_scan(ns, sh, &tot);
+    int32_t add_u = tot;
+    if (c < C) {
+      comp_start[c] = run_start + es;
+      comp_k[c] = k;
+      comp_mode[c] = mode;
+      comp_base[c] = run_base + eb;
+      tile_base[c] = run_tile + et;
+      super_base[c] = run_super + eu;
+    }
+    run_start += add_s, run_base += add_b, run_tile += add_t, run_super += add_u;
+  }
+  if (threadIdx.x == 0) totals[0] = run_base, totals[1] = run_tile, totals[2] = run_super;
+}
+
+// Assignments of singleton / one-patch components (patching.cpp:313-322).
+__global__ void assign_trivial(int32_t n, const int32_t* comp_list, const int32_t* comp_of,
+                               const int32_t* comp_start, const int32_t* comp_mode,
+                               const int32_t* comp_base, int32_t* assignment) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int32_t v = comp_list ? comp_list[i] : i;
+    int32_t c = comp_of ? comp_of[v] : 0;
+    int32_t mode = comp_mode[c];
+    if (mode == kModeSingletons) assignment[v] = comp_base[c] + (i - comp_start[c]);
+    else if (mode == kModeOne) assignment[v] = comp_base[c];
+  }
+}
+
+// ------------------------------------------------------------ farthest-point seeds
+// One CTA per FPS component (patching.cpp:26-65).  dist lives in HBM/L2; the
+// argmax over the component is a two-level tile-max tree of packed
+// (dist desc, id asc) keys, refreshed only over tiles a relaxation touched.
+struct FpsArgs {
+  DGraph g;
+  const int32_t* comp_list;  // nullptr: identity (single component)
+  const int32_t* pos_of;     // nullptr: identity
+  const int32_t* comp_start;
+  const int32_t* comp_size;
+  const int32_t* comp_k;
+  const int32_t* comp_mode;
+  const int32_t* comp_base;
+  const int32_t* tile_base;
+  const int32_t* super_base;
+  int32_t* dist;
+  uint64_t* tile_key;
+  uint64_t* super_key;
+  uint32_t* tile_bits;   // touched bitmap, one bit per tile (global, kept zero between rounds)
+  int32_t* frontier;     // 2 * n scratch; component c uses [2*start, 2*start + 2*size)
+  int32_t* seeds;        // by global patch id
+  uint64_t seed;
+};
+
+__device__ __forceinline__ int32_t vtx_at(const FpsArgs& a, int32_t pos) {
+  return a.comp_list ? a.comp_list[pos] : pos;
+}
+__device__ __forceinline__ int32_t pos_in(const FpsArgs& a, int32_t v) {
+  return a.pos_of ? a.pos_of[v] : v;
+}
+
+__global__ void __launch_bounds__(kFpsThreads) fps_kernel(FpsArgs a) {
+  const int32_t c = blockIdx.x;
+  if (a.comp_mode[c] != kModeFps) return;
+  const int32_t start = a.comp_start[c], size = a.comp_size[c], k = a.comp_k[c];
+  const int32_t ntile = static_cast<int32_t>(ceil_div(size, kTile));
+  const int32_t nsuper = static_cast<int32_t>(ceil_div(ntile, kTile));
+  uint64_t* tkey = a.tile_key + a.tile_base[c];
+  uint64_t* skey = a.super_key + a.super_base[c];
+  uint32_t* tbits = a.tile_bits + (a.tile_base[c] + 31) / 32 + c;  // word-aligned per component
+  int32_t* fa = a.frontier + 2LL * start;
+  int32_t* fb = fa + size;
+
+  __shared__ int32_t touched[kTouchCap];
+  __shared__ int32_t n_touched, overflow, n_next;
+  __shared__ uint32_t super_bits[64];  // up to 2048 supertiles (524M vertices)
+  __shared__ uint64_t red[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+
+  for (int32_t i = threadIdx.x; i < size; i += blockDim.x) a.dist[vtx_at(a, start + i)] = kUnreached;
+  for (int32_t i = threadIdx.x; i < 64; i += blockDim.x) super_bits[i] = 0;
+  if (threadIdx.x == 0) n_touched = 0, overflow = 0, n_next = 0;
+  __syncthreads();
+
+  auto tile_max = [&](int32_t t) -> uint64_t {  // warp-cooperative
+    uint64_t best = 0;
+    const int32_t lo = t * kTile, hi = min(size, lo + kTile);
+    for (int32_t p = lo + lane; p < hi; p += 32) {
+      int32_t v = vtx_at(a, start + p);
+      int32_t d = __ldcg(&a.dist[v]);
+      uint64_t kk = key_max(static_cast<uint32_t>(d), static_cast<uint32_t>(v));
+      best = kk > best ? kk : best;
+    }
+    return warp_max_u64(best);
+  };
+  auto super_max = [&](int32_t s) -> uint64_t {
+    uint64_t best = 0;
+    const int32_t lo = s * kTile, hi = min(ntile, lo + kTile);
+    for (int32_t t = lo + lane; t < hi; t += 32) {
+      uint64_t kk = __ldcg(&tkey[t]);
+      best = kk > best ? kk : best;
+    }
+    return warp_max_u64(best);
+  };
+
+  int32_t cur = vtx_at(a, start + static_cast<int32_t>(splitmix64(a.seed) % static_cast<uint64_t>(size)));
+  for (int32_t s = 0; s < k; ++s) {
+    if (s > 0) {  // argmax (patching.cpp:52-60) from the top of the tree
+      uint64_t best = 0;
+      for (int32_t i = threadIdx.x; i < nsuper; i += blockDim.x) {
+        uint64_t kk = __ldcg(&skey[i]);
+        best = kk > best ? kk : best;
+      }
+      best = block_max_u64(best, red);
+      // resolve supertile -> tile -> vertex is implicit: the key carries the id
+      cur = static_cast<int32_t>(key_max_id(best));
+    }
+    if (threadIdx.x == 0) {
+      a.seeds[a.comp_base[c] + s] = cur;
+      a.dist[cur] = 0;
+      fa[0] = cur;
+      int32_t t = pos_in(a, cur) - start;
+      t /= kTile;
+      if (!(atomicOr(&tbits[t >> 5], 1u << (t & 31)) & (1u << (t & 31)))) touched[n_touched++] = t;
+    }
+    __syncthreads();
+    // relax_from (patching.cpp:35-49): single-source BFS with strict decrease
+    int32_t nf = 1, d = 0;
+    int32_t *front = fa, *next = fb;
+    while (nf > 0) {
+      for (int32_t i = threadIdx.x; i < nf; i += blockDim.x) {
+        const int32_t u = front[i];
+        const int32_t e = a.g.off[u + 1];
+        for (int32_t j = a.g.off[u]; j < e; ++j) {
+          const int32_t w = a.g.nbr[j];
+          if (d + 1 < __ldcg(&a.dist[w])) {
+            int32_t old = atomicMin(&a.dist[w], d + 1);
+            if (old > d + 1) {
+              next[atomicAdd(&n_next, 1)] = w;
+              int32_t t = (pos_in(a, w) - start) / kTile;
+              uint32_t bit = 1u << (t & 31);
+              if (!(atomicOr(&tbits[t >> 5], bit) & bit)) {
+                int32_t slot = atomicAdd(&n_touched, 1);
+                if (slot < kTouchCap) touched[slot] = t;
+                else overflow = 1;
+              }
+            }
+          }
+        }
+      }
+      __syncthreads();
+      nf = n_next;
+      int32_t* tmp = front;
+      front = next;
+      next = tmp;
+      ++d;
+      __syncthreads();
+      if (threadIdx.x == 0) n_next = 0;
+      __syncthreads();
+    }
+    // refresh touched tiles, then touched supertiles
+    if (overflow) {
+      for (int32_t t = wid; t < ntile; t += nwarp) {
+        uint64_t m = tile_max(t);
+        if (lane == 0) tkey[t] = m;
+      }
+      for (int32_t i = threadIdx.x; i < (ntile + 31) / 32; i += blockDim.x) tbits[i] = 0;
+      __syncthreads();
+      for (int32_t sidx = wid; sidx < nsuper; sidx += nwarp) {
+        uint64_t m = super_max(sidx);
+        if (lane == 0) skey[sidx] = m;
+      }
+    } else {
+      const int32_t nt = n_touched;
+      for (int32_t i = wid; i < nt; i += nwarp) {
+        int32_t t = touched[i];
+        uint64_t m = tile_max(t);
+        if (lane == 0) {
+          tkey[t] = m;
+          atomicAnd(&tbits[t >> 5], ~(1u << (t & 31)));
+          int32_t su = t / kTile;
+          atomicOr(&super_bits[su >> 5], 1u << (su & 31));
+        }
+      }
+      __syncthreads();
+      const int32_t nwords = (nsuper + 31) / 32;
+      for (int32_t wi = 0; wi < nwords; ++wi) {
+        uint32_t bits = super_bits[wi];
+        // distribute set bits over warps
+        int32_t rank = 0;
+        while (bits) {
+          int32_t b = __ffs(bits) - 1;
+          bits &= bits - 1;
+          if (rank % nwarp == wid) {
+            uint64_t m = super_max(wi * 32 + b);
+            if (lane == 0) skey[wi * 32 + b] = m;
+          }
+          ++rank;
+        }
+      }
+    }
+    __syncthreads();
+    for (int32_t i = threadIdx.x; i < 64; i += blockDim.x) super_bits[i] = 0;
+    if (threadIdx.x == 0) n_touched = 0, overflow = 0;
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------ Lloyd rounds
+struct LloydArgs {
+  DGraph g;
+  const int32_t* comp_of;    // nullptr: single component 0
+  const int32_t* comp_mode;
+  int32_t* comp_active;      // per component
+  int32_t* changed;          // [kLloydRounds][C], zero-initialised
+  int32_t C;
+  const int32_t* patch_comp; // per global patch id: its component (nullptr: 0)
+  int32_t P;                 // global patch ids [0, P)
+  int32_t* seeds;
+  int32_t* dist;
+  int32_t* label;
+  int32_t* prev;
+  uint64_t* best;            // per patch, recenter argmax
+  int32_t* fa;
+  int32_t* fb;
+  int32_t* counters;         // [3] rotating frontier counters + [3] = any-active
+};
+
+__device__ __forceinline__ bool lloyd_active(const LloydArgs& a, int32_t v) {
+  int32_t c = a.comp_of ? a.comp_of[v] : 0;
+  return a.comp_mode[c] == kModeFps && __ldcg(&a.comp_active[c]) != 0;
+}
+
+__global__ void lloyd_kernel(LloydArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int32_t n = a.g.n;
+
+  for (int round = 0; round < kLloydRounds; ++round) {
+    // ---- assign_to_seeds (patching.cpp:69-99)
+    if (tid == 0) a.counters[0] = 0, a.counters[1] = 0, a.counters[2] = 0;
+    for (int64_t v = tid; v < n; v += nthreads)
+      if (lloyd_active(a, v)) a.dist[v] = kUnreached, a.label[v] = 0x7fffffff;
+    grid.sync();
+    for (int64_t p = tid; p < a.P; p += nthreads) {
+      int32_t c = a.patch_comp ? a.patch_comp[p] : 0;
+      if (a.comp_mode[c] != kModeFps || !__ldcg(&a.comp_active[c])) continue;
+      int32_t s = a.seeds[p];
+      a.dist[s] = 0;
+      a.label[s] = static_cast<int32_t>(p);
+      a.fa[atomicAdd(&a.counters[0], 1)] = s;
+    }
+    grid.sync();
+    {
+      int32_t* front = a.fa;
+      int32_t* next = a.fb;
+      for (int32_t d = 0;; ++d) {
+        const int32_t cin = d % 3, cout = (d + 1) % 3, cclr = (d + 2) % 3;
+        const int32_t nf = __ldcg(&a.counters[cin]);
+        if (nf == 0) break;
+        if (tid == 0) a.counters[cclr] = 0;
+        for (int64_t i = tid; i < nf; i += nthreads) {
+          const int32_t u = front[i];
+          const int32_t lu = __ldcg(&a.label[u]);
+          for (int32_t j = a.g.off[u]; j < a.g.off[u + 1]; ++j) {
+            const int32_t w = a.g.nbr[j];
+            int32_t dw = __ldcg(&a.dist[w]);
+            if (dw == kUnreached) {
+              dw = atomicCAS(&a.dist[w], kUnreached, d + 1);
+              if (dw == kUnreached) {
+                next[atomicAdd(&a.counters[cout], 1)] = w;
+                dw = d + 1;
+              }
+            }
+            if (dw == d + 1) atomicMin(&a.label[w], lu);
+          }
+        }
+        grid.sync();
+        int32_t* t = front;
+        front = next;
+        next = t;
+      }
+    }
+    // ---- stability test (patching.cpp:327-334) per component
+    int32_t* chg = a.changed + static_cast<int64_t>(round) * a.C;
+    for (int64_t v = tid; v < n; v += nthreads)
+      if (lloyd_active(a, v) && __ldcg(&a.label[v]) != a.prev[v]) chg[a.comp_of ? a.comp_of[v] : 0] = 1;
+    grid.sync();
+    if (tid == 0) a.counters[3] = 0;
+    for (int64_t v = tid; v < n; v += nthreads) {
+      if (!lloyd_active(a, v)) continue;
+      int32_t c = a.comp_of ? a.comp_of[v] : 0;
+      if (__ldcg(&chg[c])) a.prev[v] = __ldcg(&a.label[v]);
+    }
+    grid.sync();
+    for (int64_t c = tid; c < a.C; c += nthreads) {
+      if (a.comp_mode[c] != kModeFps || !a.comp_active[c]) continue;
+      if (!__ldcg(&chg[c])) a.comp_active[c] = 0;
+      else atomicAdd(&a.counters[3], 1);
+    }
+    grid.sync();
+    if (__ldcg(&a.counters[3]) == 0 || round == kLloydRounds - 1) break;
+
+    // ---- recenter_seeds (patching.cpp:103-139); dist is reused as depth
+    if (tid == 0) a.counters[0] = 0, a.counters[1] = 0, a.counters[2] = 0;
+    for (int64_t p = tid; p < a.P; p += nthreads) a.best[p] = 0;
+    grid.sync();
+    for (int64_t v = tid; v < n; v += nthreads) {
+      if (!lloyd_active(a, v)) continue;
+      const int32_t lv = __ldcg(&a.label[v]);
+      bool boundary = false;
+      for (int32_t j = a.g.off[v]; j < a.g.off[v + 1] && !boundary; ++j)
+        boundary = __ldcg(&a.label[a.g.nbr[j]]) != lv;
+      a.dist[v] = boundary ? 0 : kUnreached;
+      if (boundary) a.fa[atomicAdd(&a.counters[0], 1)] = static_cast<int32_t>(v);
+    }
+    grid.sync();
+    {
+      int32_t* front = a.fa;
+      int32_t* next = a.fb;
+      for (int32_t d = 0;; ++d) {
+        const int32_t cin = d % 3, cout = (d + 1) % 3, cclr = (d + 2) % 3;
+        const int32_t nf = __ldcg(&a.counters[cin]);
+        if (nf == 0) break;
+        if (tid == 0) a.counters[cclr] = 0;
+        for (int64_t i = tid; i < nf; i += nthreads) {
+          const int32_t u = front[i];
+          const int32_t lu = __ldcg(&a.label[u]);
+          for (int32_t j = a.g.off[u]; j < a.g.off[u + 1]; ++j) {
+            const int32_t w = a.g.nbr[j];
+            if (__ldcg(&a.label[w]) != lu || __ldcg(&a.dist[w]) != kUnreached) continue;
+            if (atomicCAS(&a.dist[w], kUnreached, d + 1) == kUnreached)
+              next[atomicAdd(&a.counters[cout], 1)] = w;
+          }
+        }
+        grid.sync();
+        int32_t* t = front;
+        front = next;
+        next = t;
+      }
+    }
+    for (int64_t v = tid; v < n; v += nthreads) {
+      if (!lloyd_active(a, v)) continue;
+      const int32_t dv = __ldcg(&a.dist[v]);
+      if (dv == kUnreached) continue;
+      atomicMax(reinterpret_cast<unsigned long long*>(&a.best[__ldcg(&a.label[v])]),
+                static_cast<unsigned long long>(key_max(static_cast<uint32_t>(dv) + 1u, static_cast<uint32_t>(v))));
+    }
+    grid.sync();
+    for (int64_t p = tid; p < a.P; p += nthreads) {
+      int32_t c = a.patch_comp ? a.patch_comp[p] : 0;
+      if (a.comp_mode[c] != kModeFps || !__ldcg(&a.comp_active[c])) continue;
+      uint64_t b = __ldcg(&a.best[p]);
+      if (b != 0) a.seeds[p] = static_cast<int32_t>(key_max_id(b));
+    }
+    grid.sync();
+  }
+}
+
+__global__ void lloyd_finish(int32_t n, const int32_t* comp_of, const int32_t* comp_mode,
+                             const int32_t* prev, int32_t* assignment) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    int32_t c = comp_of ? comp_of[v] : 0;
+    if (comp_mode[c] == kModeFps) assignment[v] = prev[v];
+  }
+}
+
+__global__ void patch_comp_kernel(int32_t C, const int32_t* comp_mode, const int32_t* comp_base,
+                                  const int32_t* comp_k, int32_t* patch_comp) {
+  for (int32_t c = blockIdx.x; c < C; c += gridDim.x) {
+    if (comp_mode[c] != kModeFps) continue;
+    for (int32_t p = threadIdx.x; p < comp_k[c]; p += blockDim.x) patch_comp[comp_base[c] + p] = c;
+  }
+}
+
+__global__ void fill_i32(int64_t n, int32_t* a, int32_t v) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    a[i] = v;
+}
+
+// ------------------------------------------------------------ enforce_connectivity
+__global__ void patch_min_vertex(int32_t n, const int32_t* assignment, int32_t* minv) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    atomicMin(&minv[assignment[v]], v);
+}
+__global__ void collect_extra_roots(int32_t n, const int32_t* par, const int32_t* assignment,
+                                    const int32_t* minv, uint64_t* keys, int32_t* count) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    if (par[v] != v) continue;
+    int32_t p = assignment[v];
+    if (minv[p] == v) continue;
+    keys[atomicAdd(count, 1)] = (static_cast<uint64_t>(p) << 32) | static_cast<uint32_t>(v);
+  }
+}
+__global__ void fresh_ids(int32_t E, const uint64_t* keys, int32_t P, int32_t* root_id) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < E; i += gridDim.x * blockDim.x)
+    root_id[static_cast<int32_t>(keys[i] & 0xffffffffu)] = P + i;
+}
+__global__ void relabel_components(int32_t n, const int32_t* par, const int32_t* assignment,
+                                   const int32_t* root_id, int32_t* out) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    int32_t r = root_id[par[v]];
+    out[v] = r >= 0 ? r : assignment[v];
+  }
+}
+__global__ void check_range(int32_t n, const int32_t* assignment, int32_t P, int32_t* bad) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    int32_t p = assignment[v];
+    if (p < 0 || p >= P) atomicMin(bad, v);
+  }
+}
+
+// ------------------------------------------------------------ repair_sizes
+// One CTA (patching.cpp:149-291).  Members of a patch are a chain of
+// segments in `pool`; merges splice chains, splits write two new segments.
+struct RepairArgs {
+  DGraph g;
+  int32_t* assignment;
+  int32_t P0;
+  int32_t cap_p;       // capacity for patch ids (P0 + splits)
+  int32_t cap_seg;
+  int64_t cap_pool;
+  int32_t target;
+  int32_t* size;       // cap_p
+  int32_t* exempt;     // cap_p
+  int32_t* head;       // cap_p (segment id, -1 = none)
+  int32_t* tail;       // cap_p
+  int32_t* seg_start;  // cap_seg
+  int32_t* seg_len;
+  int32_t* seg_next;
+  int32_t* pool;       // cap_pool
+  int32_t* dist;       // n, kUnreached outside the current patch work
+  int32_t* lab;        // n
+  int32_t* fa;         // n
+  int32_t* fb;         // n
+  int32_t* remap;      // cap_p
+  int32_t* out;        // [0] patch count, [1] error
+};
+
+__global__ void __launch_bounds__(1024) repair_kernel(RepairArgs a) {
+  __shared__ uint64_t red[32];
+  __shared__ int32_t shi[32];
+  __shared__ int32_t s_P, s_nseg, s_cnt, s_err;
+  __shared__ int64_t s_pool;
+  const int32_t low = (a.target + 1) / 2;
+  const int64_t high = 2LL * a.target;
+  if (threadIdx.x == 0) {
+    s_P = a.P0;
+    s_nseg = a.P0;
+    s_pool = a.g.n;
+    s_err = 0;
+  }
+  __syncthreads();
+  const int64_t max_iter = 4LL * a.P0 + 64;
+
+  // iterate the member chain of patch p: f(v) for every member, block-parallel
+  auto for_members = [&](int32_t p, auto&& f) {
+    for (int32_t sgi = a.head[p]; sgi >= 0; sgi = a.seg_next[sgi]) {
+      const int32_t st = a.seg_start[sgi], len = a.seg_len[sgi];
+      for (int32_t i = threadIdx.x; i < len; i += blockDim.x) f(a.pool[st + i]);
+    }
+  };
+
+  for (int64_t iter = 0; iter < max_iter; ++iter) {
+    const int32_t P = s_P;
+    // smallest mergeable patch (size, id)
+    uint64_t best = ~0ull;
+    for (int32_t p = threadIdx.x; p < P; p += blockDim.x) {
+      int32_t sz = a.size[p];
+      if (sz <= 0 || sz >= low || a.exempt[p]) continue;
+      uint64_t kk = key_min(static_cast<uint32_t>(sz), static_cast<uint32_t>(p));
+      best = kk < best ? kk : best;
+    }
+    best = block_min_u64(best, red);
+    if (best != ~0ull) {
+      const int32_t mp = static_cast<int32_t>(best & 0xffffffffu);
+      uint64_t tb = ~0ull;
+      for_members(mp, [&](int32_t v) {
+        for (int32_t j = a.g.off[v]; j < a.g.off[v + 1]; ++j) {
+          int32_t q = a.assignment[a.g.nbr[j]];
+          if (q == mp) continue;
+          uint64_t kk = key_min(static_cast<uint32_t>(a.size[q]), static_cast<uint32_t>(q));
+          tb = kk < tb ? kk : tb;
+        }
+      });
+      tb = block_min_u64(tb, red);
+      if (tb == ~0ull) {
+        if (threadIdx.x == 0) a.exempt[mp] = 1;
+        __syncthreads();
+        continue;
+      }
+      const int32_t tgt = static_cast<int32_t>(tb & 0xffffffffu);
+      for_members(mp, [&](int32_t v) { a.assignment[v] = tgt; });
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        a.seg_next[a.tail[tgt]] = a.head[mp];
+        a.tail[tgt] = a.tail[mp];
+        a.head[mp] = a.tail[mp] = -1;
+        a.size[tgt] += a.size[mp];
+        a.size[mp] = 0;
+      }
+      __syncthreads();
+      continue;
+    }
+    // largest oversized patch (size desc, id asc)
+    uint64_t big = 0;
+    for (int32_t p = threadIdx.x; p < P; p += blockDim.x) {
+      int32_t sz = a.size[p];
+      if (sz <= high) continue;
+      uint64_t kk = key_max(static_cast<uint32_t>(sz), static_cast<uint32_t>(p));
+      big = kk > big ? kk : big;
+    }
+    big = block_max_u64(big, red);
+    if (big == 0) break;
+    const int32_t sp = static_cast<int32_t>(key_max_id(big));
+    const int32_t spsize = a.size[sp];
+    if (P >= a.cap_p || s_nseg + 2 > a.cap_seg || s_pool + 2LL * spsize > a.cap_pool) {
+      if (threadIdx.x == 0) s_err = 1;
+      __syncthreads();
+      break;
+    }
+    // gather members contiguously into the pool (new segment region)
+    const int64_t gbase = s_pool;
+    __syncthreads();
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    for_members(sp, [&](int32_t v) { a.pool[gbase + atomicAdd(&s_cnt, 1)] = v; });
+    __syncthreads();
+    const int32_t* mem = a.pool + gbase;
+    // farthest-vertex sweeps (patching.cpp:165-185, 231-233)
+    uint64_t mn = ~0ull;
+    for (int32_t i = threadIdx.x; i < spsize; i += blockDim.x)
+      mn = min(mn, static_cast<uint64_t>(mem[i]));
+    mn = block_min_u64(mn, red);
+    int32_t ends[3];
+    ends[0] = static_cast<int32_t>(mn);
+    for (int sweep = 1; sweep <= 2; ++sweep) {
+      for (int32_t i = threadIdx.x; i < spsize; i += blockDim.x) a.dist[mem[i]] = kUnreached;
+      __syncthreads();
+      const int32_t from = ends[sweep - 1];
+      if (threadIdx.x == 0) {
+        a.dist[from] = 0;
+        a.fa[0] = from;
+        s_cnt = 0;
+      }
+      __syncthreads();
+      int32_t nf = 1, d = 0;
+      int32_t *front = a.fa, *next = a.fb;
+      uint64_t far = key_max(0u, static_cast<uint32_t>(from));
+      while (nf > 0) {
+        for (int32_t i = threadIdx.x; i < nf; i += blockDim.x) {
+          const int32_t u = front[i];
+          for (int32_t j = a.g.off[u]; j < a.g.off[u + 1]; ++j) {
+            const int32_t w = a.g.nbr[j];
+            if (a.assignment[w] != sp) continue;
+            if (atomicCAS(&a.dist[w], kUnreached, d + 1) == kUnreached) {
+              next[atomicAdd(&s_cnt, 1)] = w;
+              uint64_t kk = key_max(static_cast<uint32_t>(d + 1), static_cast<uint32_t>(w));
+              far = kk > far ? kk : far;
+            }
+          }
+        }
+        __syncthreads();
+        nf = s_cnt;
+        __syncthreads();
+        if (threadIdx.x == 0) s_cnt = 0;
+        int32_t* t = front;
+        front = next;
+        next = t;
+        ++d;
+        __syncthreads();
+      }
+      far = block_max_u64(far, red);
+      ends[sweep] = static_cast<int32_t>(key_max_id(far));
+    }
+    // two-source competition, ties to b's half (patching.cpp:234-261)
+    const int32_t b = ends[1], cc = ends[2];
+    for (int32_t i = threadIdx.x; i < spsize; i += blockDim.x) {
+      a.dist[mem[i]] = kUnreached;
+      a.lab[mem[i]] = 0x7fffffff;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      a.dist[b] = 0, a.lab[b] = 0;
+      a.dist[cc] = 0, a.lab[cc] = 1;
+      a.fa[0] = b, a.fa[1] = cc;
+      s_cnt = 0;
+    }
+    __syncthreads();
+    {
+      int32_t nf = 2, d = 0;
+      int32_t *front = a.fa, *next = a.fb;
+      while (nf > 0) {
+        for (int32_t i = threadIdx.x; i < nf; i += blockDim.x) {
+          const int32_t u = front[i];
+          const int32_t lu = a.lab[u];
+          for (int32_t j = a.g.off[u]; j < a.g.off[u + 1]; ++j) {
+            const int32_t w = a.g.nbr[j];
+            if (a.assignment[w] != sp) continue;
+            int32_t dw = atomicCAS(&a.dist[w], kUnreached, d + 1);
+            if (dw == kUnreached) {
+              next[atomicAdd(&s_cnt, 1)] = w;
+              dw = d + 1;
+            }
+            if (dw == d + 1) atomicMin(&a.lab[w], lu);
+          }
+        }
+        __syncthreads();
+        nf = s_cnt;
+        __syncthreads();
+        if (threadIdx.x == 0) s_cnt = 0;
+        int32_t* t = front;
+        front = next;
+        next = t;
+        ++d;
+        __syncthreads();
+      }
+    }
+    // split members stably: keep (label != 1) then fresh (label == 1)
+    const int32_t fresh = P;
+    const int64_t kbase = gbase + spsize;  // keep list, then fresh list after it
+    int32_t nkeep_total = 0;
+    {
+      int32_t run_keep = 0, run_fresh = 0;
+      // first pass: count keep
+      int32_t cnt = 0;
+      for (int32_t i = threadIdx.x; i < spsize; i += blockDim.x) cnt += (a.lab[mem[i]] != 1);
+      int64_t ck = block_sum_i64(cnt, reinterpret_cast<int64_t*>(red));
+      nkeep_total = static_cast<int32_t>(ck);
+      for (int32_t i0 = 0; i0 < spsize; i0 += blockDim.x) {
+        int32_t i = i0 + threadIdx.x;
+        int32_t v = i < spsize ? mem[i] : -1;
+        int32_t isf = (i < spsize && a.lab[v] == 1) ? 1 : 0;
+        int32_t isk = (i < spsize && !isf) ? 1 : 0;
+        int32_t tk, tf;
+        int32_t ek = block_excl_scan(isk, shi, &tk);
+        int32_t ef = block_excl_scan(isf, shi, &tf);
+        if (isk) a.pool[kbase + run_keep + ek] = v;
+        if (isf) {
+          a.pool[kbase + nkeep_total + run_fresh + ef] = v;
+          a.assignment[v] = fresh;
+        }
+        run_keep += tk, run_fresh += tf;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int32_t sk = s_nseg, sf = s_nseg + 1;
+      a.seg_start[sk] = static_cast<int32_t>(kbase);
+      a.seg_len[sk] = nkeep_total;
+      a.seg_next[sk] = -1;
+      a.seg_start[sf] = static_cast<int32_t>(kbase + nkeep_total);
+      a.seg_len[sf] = spsize - nkeep_total;
+      a.seg_next[sf] = -1;
+      a.head[sp] = a.tail[sp] = sk;
+      a.head[fresh] = a.tail[fresh] = sf;
+      a.size[sp] = nkeep_total;
+      a.size[fresh] = spsize - nkeep_total;
+      a.exempt[fresh] = 0;
+      s_nseg += 2;
+      s_pool = kbase + spsize;
+      s_P = P + 1;
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  // compact ids ascending (patching.cpp:282-290)
+  const int32_t P = s_P;
+  int32_t run = 0;
+  for (int32_t p0 = 0; p0 < P; p0 += blockDim.x) {
+    int32_t p = p0 + threadIdx.x;
+    int32_t live = (p < P && a.size[p] > 0) ? 1 : 0;
+    int32_t tot;
+    int32_t e = block_excl_scan(live, shi, &tot);
+    if (p < P) a.remap[p] = live ? run + e : -1;
+    run += tot;
+  }
+  if (threadIdx.x == 0) a.out[0] = run, a.out[1] = s_err;
+}
+
+__global__ void seg_init(int32_t P, const int32_t* start, const int32_t* count, int32_t* head,
+                         int32_t* tail, int32_t* seg_start, int32_t* seg_len, int32_t* seg_next,
+                         int32_t* size, int32_t* exempt) {
+  for (int32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x) {
+    head[p] = tail[p] = p;
+    seg_start[p] = start[p];
+    seg_len[p] = count[p];
+    seg_next[p] = -1;
+    size[p] = count[p];
+    exempt[p] = 0;
+  }
+}
+__global__ void count_patches(int32_t n, const int32_t* assignment, int32_t* cnt) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    atomicAdd(&cnt[assignment[v]], 1);
+}
+__global__ void apply_remap(int32_t n, const int32_t* remap, int32_t* assignment) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    assignment[v] = remap[assignment[v]];
+}
+
+int grid_for(const mp_context& ctx, int64_t n, int threads = 256) {
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), ctx.num_sms * 16LL)));
+}
+
+// Stable counting sort of vertices by patch id (ascending id within a patch).
+void bucket_by_patch(mp_context& ctx, int32_t n, const int32_t* assignment, int32_t P,
+                     int32_t* start, int32_t* count, int32_t* list) {
+  cudaStream_t s = ctx.stream;
+  MP_CUDA(cudaMemsetAsync(count, 0, sizeof(int32_t) * P, s));
+  MP_KERNEL(ctx, count_patches<<<grid_for(ctx, n), 256, 0, s>>>(n, assignment, count));
+  size_t tmp = 0;
+  MP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, start, P, s));
+  DevBuf<char> t(tmp, s);
+  MP_CUDA(cub::DeviceScan::ExclusiveSum(t.get(), tmp, count, start, P, s));
+  DevBuf<int32_t> keys_out(n, s), vals_in(n, s);
+  MP_KERNEL(ctx, iota_kernel<<<grid_for(ctx, n), 256, 0, s>>>(n, vals_in));
+  int end_bit = 1;
+  while ((1LL << end_bit) < P) ++end_bit;
+  size_t tmp2 = 0;
+  MP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp2, assignment, keys_out.get(), vals_in.get(),
+                                          list, n, 0, end_bit, s));
+  DevBuf<char> t2(tmp2, s);
+  MP_CUDA(cub::DeviceRadixSort::SortPairs(t2.get(), tmp2, assignment, keys_out.get(), vals_in.get(),
+                                          list, n, 0, end_bit, s));
+}
+
+int32_t repair_sizes_dev(mp_context& ctx, const DGraph& g, int32_t* assignment, int32_t P,
+                         int32_t target) {
+  cudaStream_t s = ctx.stream;
+  const int32_t n = g.n;
+  RepairArgs a{};
+  a.g = g;
+  a.assignment = assignment;
+  a.P0 = P;
+  a.cap_p = P + std::max<int32_t>(1024, P);
+  a.cap_seg = 2 * a.cap_p + 16;
+  a.cap_pool = 3LL * n + 1024;
+  a.target = target;
+  DevBuf<int32_t> size(a.cap_p, s), exempt(a.cap_p, s), head(a.cap_p, s), tail(a.cap_p, s),
+      seg_start(a.cap_seg, s), seg_len(a.cap_seg, s), seg_next(a.cap_seg, s), pool(a.cap_pool, s),
+      dist(n, s), lab(n, s), fa(n, s), fb(n, s), remap(a.cap_p, s), out(2, s), cnt(P, s), st(P, s);
+  bucket_by_patch(ctx, n, assignment, P, st, cnt, pool);
+  MP_KERNEL(ctx, seg_init<<<grid_for(ctx, P), 256, 0, s>>>(P, st, cnt, head, tail, seg_start, seg_len,
+                                                          seg_next, size, exempt));
+  a.size = size, a.exempt = exempt, a.head = head, a.tail = tail, a.seg_start = seg_start;
+  a.seg_len = seg_len, a.seg_next = seg_next, a.pool = pool, a.dist = dist, a.lab = lab;
+  a.fa = fa, a.fb = fb, a.remap = remap, a.out = out;
+  MP_KERNEL(ctx, repair_kernel<<<1, 1024, 0, s>>>(a));
+  int32_t h_out[2];
+  MP_CUDA(cudaMemcpyAsync(h_out, out, sizeof h_out, cudaMemcpyDeviceToHost, s));
+  MP_CUDA(cudaStreamSynchronize(s));
+  if (h_out[1]) throw Error(MP_ENOMEM, "repair_sizes: split workspace exhausted");
+  MP_KERNEL(ctx, apply_remap<<<grid_for(ctx, n), 256, 0, s>>>(n, remap, assignment));
+  return h_out[0];
+}
+
+}  // namespace
+
+int32_t enforce_connectivity_dev(mp_context& ctx, const DGraph& g, const int32_t* in,
+                                 int32_t P, int32_t* out) {
+  cudaStream_t s = ctx.stream;
+  const int32_t n = g.n;
+  if (n == 0) return P;
+  DevBuf<int32_t> bad(1, s);
+  MP_KERNEL(ctx, fill_i32<<<1, 32, 0, s>>>(1, bad, 0x7fffffff));
+  MP_KERNEL(ctx, check_range<<<grid_for(ctx, n), 256, 0, s>>>(n, in, P, bad));
+  int32_t h_bad;
+  MP_CUDA(cudaMemcpyAsync(&h_bad, bad, sizeof h_bad, cudaMemcpyDeviceToHost, s));
+  MP_CUDA(cudaStreamSynchronize(s));
+  if (h_bad != 0x7fffffff)
+    throw Error(MP_EINVAL, "patch id out of range at vertex " + std::to_string(h_bad));
+  DevBuf<int32_t> par(n, s), minv(std::max(P, 1), s), root_id(n, s), cnt(1, s);
+  DevBuf<uint64_t> keys(n, s);
+  union_find(ctx, g, in, par);
+  MP_KERNEL(ctx, fill_i32<<<grid_for(ctx, P), 256, 0, s>>>(P, minv, 0x7fffffff));
+  MP_KERNEL(ctx, patch_min_vertex<<<grid_for(ctx, n), 256, 0, s>>>(n, in, minv));
+  MP_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t), s));
+  MP_KERNEL(ctx, collect_extra_roots<<<grid_for(ctx, n), 256, 0, s>>>(n, par, in, minv, keys, cnt));
+  int32_t E = 0;
+  MP_CUDA(cudaMemcpyAsync(&E, cnt, sizeof E, cudaMemcpyDeviceToHost, s));
+  MP_CUDA(cudaStreamSynchronize(s));
+  MP_KERNEL(ctx, fill_i32<<<grid_for(ctx, n), 256, 0, s>>>(n, root_id, -1));
+  if (E > 0) {
+    DevBuf<uint64_t> sorted(E, s);
+    size_t tmp = 0;
+    MP_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys.get(), sorted.get(), E, 0, 64, s));
+    DevBuf<char> t(tmp, s);
+    MP_CUDA(cub::DeviceRadixSort::SortKeys(t.get(), tmp, keys.get(), sorted.get(), E, 0, 64, s));
+    MP_KERNEL(ctx, fresh_ids<<<grid_for(ctx, E), 256, 0, s>>>(E, sorted, P, root_id));
+  }
+  MP_KERNEL(ctx, relabel_components<<<grid_for(ctx, n), 256, 0, s>>>(n, par, in, root_id, out));
+  return P + E;
+}
+
+int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, uint64_t seed,
+                            int32_t* assignment) {
+  if (target < 1) throw Error(MP_EINVAL, "target patch size must be positive");
+  cudaStream_t s = ctx.stream;
+  const int32_t n = g.n;
+  if (n == 0) return 0;
+
+  // connected components, ordered by smallest member (graph.cpp:183-205)
+  DevBuf<int32_t> par(n, s), flag(n, s), rank(n, s);
+  union_find(ctx, g, nullptr, par);
+  MP_KERNEL(ctx, root_flags<<<grid_for(ctx, n), 256, 0, s>>>(n, par, flag));
+  {
+    size_t tmp = 0;
+    MP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, flag.get(), rank.get(), n, s));
+    DevBuf<char> t(tmp, s);
+    MP_CUDA(cub::DeviceScan::ExclusiveSum(t.get(), tmp, flag.get(), rank.get(), n, s));
+  }
+  int32_t last[2];
+  MP_CUDA(cudaMemcpyAsync(&last[0], rank.get() + n - 1, 4, cudaMemcpyDeviceToHost, s));
+  MP_CUDA(cudaMemcpyAsync(&last[1], flag.get() + n - 1, 4, cudaMemcpyDeviceToHost, s));
+  MP_CUDA(cudaStreamSynchronize(s));
+  const int32_t C = last[0] + last[1];
+
+  DevBuf<int32_t> comp_of, comp_list, pos_of;
+  DevBuf<int32_t> comp_size(C, s), comp_start(C, s), comp_k(C, s), comp_mode(C, s), comp_base(C, s),
+      tile_base(C, s), super_base(C, s), totals(3, s);
+  if (C == 1) {
+    int32_t hn = n;
+    MP_CUDA(cudaMemcpyAsync(comp_size.get(), &hn, 4, cudaMemcpyHostToDevice, s));
+  } else {
+    comp_of.alloc(n, s);
+    comp_list.alloc(n, s);
+    pos_of.alloc(n, s);
+    MP_CUDA(cudaMemsetAsync(comp_size, 0, sizeof(int32_t) * C, s));
+    MP_KERNEL(ctx, comp_of_kernel<<<grid_for(ctx, n), 256, 0, s>>>(n, par, rank, comp_of, comp_size));
+    DevBuf<int32_t> vals(n, s), keys_out(n, s);
+    MP_KERNEL(ctx, iota_kernel<<<grid_for(ctx, n), 256, 0, s>>>(n, vals));
+    int end_bit = 1;
+    while ((1LL << end_bit) < C) ++end_bit;
+    size_t tmp = 0;
+    MP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, comp_of.get(), keys_out.get(), vals.get(),
+                                            comp_list.get(), n, 0, end_bit, s));
+    DevBuf<char> t(tmp, s);
+    MP_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, comp_of.get(), keys_out.get(), vals.get(),
+                                            comp_list.get(), n, 0, end_bit, s));
+    MP_KERNEL(ctx, scatter_pos<<<grid_for(ctx, n), 256, 0, s>>>(n, comp_list, pos_of));
+  }
+  MP_KERNEL(ctx, plan_components<<<1, 1024, 0, s>>>(C, comp_size, target, comp_start, comp_k, comp_mode,
+                                                   comp_base, tile_base, super_base, totals));
+  int32_t h_tot[3];
+  MP_CUDA(cudaMemcpyAsync(h_tot, totals, sizeof h_tot, cudaMemcpyDeviceToHost, s));
+  MP_CUDA(cudaStreamSynchronize(s));
+  const int32_t P0 = h_tot[0];
+
+  MP_KERNEL(ctx, assign_trivial<<<grid_for(ctx, n), 256, 0, s>>>(n, comp_list, comp_of, comp_start,
+                                                                comp_mode, comp_base, assignment));
+  if (h_tot[1] > 0) {  // at least one FPS component
+    DevBuf<int32_t> dist(n, s), fr(2LL * n, s), seeds(P0, s);
+    DevBuf<uint64_t> tkey(h_tot[1], s), skey(h_tot[2], s);
+    DevBuf<uint32_t> tbits(h_tot[1] / 32 + 2LL * C + 2, s);
+    MP_CUDA(cudaMemsetAsync(tbits, 0, sizeof(uint32_t) * tbits.n, s));
+    FpsArgs fa{};
+    fa.g = g;
+    fa.comp_list = comp_list.get();
+    fa.pos_of = pos_of.get();
+    fa.comp_start = comp_start, fa.comp_size = comp_size, fa.comp_k = comp_k;
+    fa.comp_mode = comp_mode, fa.comp_base = comp_base, fa.tile_base = tile_base;
+    fa.super_base = super_base, fa.dist = dist, fa.tile_key = tkey, fa.super_key = skey;
+    fa.tile_bits = tbits, fa.frontier = fr, fa.seeds = seeds, fa.seed = seed;
+    MP_KERNEL(ctx, fps_kernel<<<C, kFpsThreads, 0, s>>>(fa));
+
+    // Lloyd rounds: one cooperative kernel
+    DevBuf<int32_t> label(n, s), prev(n, s), active(C, s), changed(static_cast<int64_t>(kLloydRounds) * C, s),
+        counters(4, s), patch_comp;
+    DevBuf<uint64_t> best(P0, s);
+    MP_KERNEL(ctx, fill_i32<<<grid_for(ctx, n), 256, 0, s>>>(n, prev, kNone));
+    MP_KERNEL(ctx, fill_i32<<<grid_for(ctx, C), 256, 0, s>>>(C, active, 1));
+    MP_CUDA(cudaMemsetAsync(changed, 0, sizeof(int32_t) * changed.n, s));
+    if (C > 1) {
+      patch_comp.alloc(P0, s);
+      MP_KERNEL(ctx, fill_i32<<<grid_for(ctx, P0), 256, 0, s>>>(P0, patch_comp, 0));
+      MP_KERNEL(ctx, patch_comp_kernel<<<std::min(C, 4096), 256, 0, s>>>(C, comp_mode, comp_base, comp_k,
+                                                                        patch_comp));
+    }
+    LloydArgs la{};
+    la.g = g;
+    la.comp_of = comp_of.get();
+    la.comp_mode = comp_mode;
+    la.comp_active = active;
+    la.changed = changed;
+    la.C = C;
+    la.patch_comp = patch_comp.get();
+    la.P = P0;
+    la.seeds = seeds;
+    la.dist = dist;
+    la.label = label;
+    la.prev = prev;
+    la.best = best;
+    la.fa = fr.get();
+    la.fb = fr.get() + n;
+    la.counters = counters;
+    int bpsm = 0;
+    MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, lloyd_kernel, 256, 0));
+    int blocks = std::max(1, std::min(bpsm, 4)) * ctx.num_sms;
+    void* args[] = {&la};
+    MP_KERNEL(ctx, MP_CUDA(cudaLaunchCooperativeKernel((void*)lloyd_kernel, blocks, 256, args, 0, s)));
+    MP_KERNEL(ctx, lloyd_finish<<<grid_for(ctx, n), 256, 0, s>>>(n, comp_of.get(), comp_mode, prev, assignment));
+  }
+  DevBuf<int32_t> conn(n, s);
+  int32_t P1 = enforce_connectivity_dev(ctx, g, assignment, P0, conn);
+  MP_CUDA(cudaMemcpyAsync(assignment, conn, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
+  return repair_sizes_dev(ctx, g, assignment, P1, target);
+}
+
+}  // namespace mp

@@ -1,0 +1,349 @@
+// Stage 5b — factor elimination tree and column counts, nnz(L)
+// (reference core/src/symbolic.cpp:33-45 elimination_fill, :82-96
+// factor_etree_parents, on the EliminationState game of elimination.cpp).
+//
+// The reference plays one sequential elimination game over the whole graph
+// in permutation order.  The ND tree splits that game exactly: once the
+// vertices of a subtree are eliminated, what the rest of the game sees of
+// them is one live element per connected piece, with a boundary inside the
+// ancestor separators.  So the device plays the game node by node, bottom-up
+// one tree level per launch, one CTA per node:
+//   * variables of a node vertex = its neighbours in the node or in an
+//     ancestor (neighbours below are represented by the children's leftover
+//     elements, which keep exactly the same reach sets);
+//   * inherited elements = the children's live elements, attached to the node
+//     vertices in their boundary (or passed up when none is in the node);
+//   * pivots in local_perm order; |reach| + 1 is the column count, the
+//     smallest permutation position in the reach is the etree parent.
+// Reach sets are identical to the sequential game, so column counts, nnz(L),
+// Σ counts² and parents are bit-exact for any schedule.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "mp_context.h"
+#include "mp_device.cuh"
+
+namespace mp {
+namespace {
+
+constexpr int kSymThreads = 512;
+
+int grid_for(const mp_context& ctx, int64_t n, int threads = 256) {
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), ctx.num_sms * 16LL)));
+}
+
+struct SymArgs {
+  DGraph g;
+  int32_t nn;
+  int32_t level;
+  const int32_t* node_of;
+  const int32_t* node_offsets;
+  const int32_t* node_vertices;
+  const int32_t* local_perm;
+  const int32_t* local_of;
+  const int32_t* node_pos;   // first permutation position per node
+  const int32_t* inverse;    // vertex -> permutation position
+  int32_t* adj;              // CSR slots
+  int32_t* el;               // CSR slots
+  int32_t* nadj;
+  int32_t* nel;
+  int64_t* bptr;             // per element
+  int32_t* bsz;              // per element
+  int32_t* emark;            // per element, token = pivot + 1
+  int32_t* pool;
+  int64_t pool_cap;
+  unsigned long long* pool_cursor;
+  const int64_t* ws_off;     // per level-local node: private mark + scratch workspace
+  int32_t* ws;
+  const int64_t* left_off;   // per node: leftover-element list slab
+  int32_t* left_cnt;         // per node
+  int32_t* left_list;
+  int64_t* column_counts;    // by position
+  int32_t* parent;           // by position
+  int32_t* overflow;
+};
+
+// private index of w (in node A, an ancestor-or-self of the CTA's node)
+__device__ __forceinline__ int32_t priv_idx(const SymArgs& a, const int32_t* abase, int32_t w) {
+  return abase[tree_level(a.node_of[w])] + a.local_of[w];
+}
+
+__global__ void __launch_bounds__(kSymThreads) sym_kernel(SymArgs a) {
+  const int32_t first = (1 << a.level) - 1;
+  const int32_t X = first + blockIdx.x;
+  if (X >= a.nn) return;
+  const int32_t xb = a.node_offsets[X], nx = a.node_offsets[X + 1] - xb;
+  const int32_t lc = 2 * X + 1, rc = 2 * X + 2;
+  const bool has_children = lc < a.nn;
+  const int64_t lslab = a.left_off[X];
+  int32_t* myleft = a.left_list + lslab;
+  __shared__ int32_t abase[32];
+  __shared__ int32_t s_cnt, s_nleft, s_abort;
+  __shared__ unsigned long long s_at;
+  __shared__ uint64_t red[32];
+  if (threadIdx.x == 0) {
+    s_nleft = 0;
+    s_abort = 0;
+    // ancestor sizes along the path: abase[level] = sum of the sizes above
+    int32_t path[32];
+    int32_t depth = 0;
+    for (int32_t t = X;; t = (t - 1) / 2) {
+      path[depth++] = t;
+      if (t == 0) break;
+    }
+    int32_t run = 0;
+    for (int32_t l = 0; l < depth; ++l) {
+      const int32_t A = path[depth - 1 - l];
+      abase[l] = run;
+      run += a.node_offsets[A + 1] - a.node_offsets[A];
+    }
+    abase[depth] = run;
+  }
+  __syncthreads();
+  const int32_t path_size = abase[a.level + 1];
+  int32_t* marks = a.ws + a.ws_off[blockIdx.x];
+  int32_t* scratch = marks + path_size;
+  for (int32_t i = threadIdx.x; i < path_size; i += blockDim.x) marks[i] = 0;
+  const int32_t* verts = a.node_vertices + xb;
+
+  // ---- variables: neighbours in X or an ancestor
+  for (int32_t k = threadIdx.x; k < nx; k += blockDim.x) {
+    const int32_t v = verts[k];
+    const int32_t o = a.g.off[v];
+    int32_t c = 0;
+    for (int32_t j = o; j < a.g.off[v + 1]; ++j) {
+      const int32_t w = a.g.nbr[j];
+      if (is_ancestor_or_self(a.node_of[w], X)) a.adj[o + c++] = w;
+    }
+    a.nadj[v] = c;
+    a.nel[v] = 0;
+  }
+  __syncthreads();
+  // ---- inherited elements (warp per element)
+  if (has_children) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int side = 0; side < 2; ++side) {
+      const int32_t c = side ? rc : lc;
+      const int32_t* cl = a.left_list + a.left_off[c];
+      const int32_t ncl = a.left_cnt[c];
+      for (int32_t i = wid; i < ncl; i += nw) {
+        const int32_t e = cl[i];
+        const int32_t* bd = a.pool + a.bptr[e];
+        const int32_t sz = a.bsz[e];
+        bool any = false;
+        for (int32_t j = lane; j < sz; j += 32) {
+          const int32_t w = bd[j];
+          const bool mine = a.node_of[w] == X;
+          if (mine) a.el[a.g.off[w] + atomicAdd(&a.nel[w], 1)] = e;
+          any |= mine;
+        }
+        any = __any_sync(0xffffffffu, any);
+        if (!any && lane == 0) myleft[atomicAdd(&s_nleft, 1)] = e;
+      }
+    }
+  }
+  __syncthreads();
+  // ---- the game on X, pivots in local_perm order
+  const int32_t pos0 = a.node_pos[X];
+  for (int32_t k = 0; k < nx; ++k) {
+    const int32_t p = verts[a.local_perm[xb + k]];
+    const int32_t tok = k + 1;
+    if (threadIdx.x == 0) {
+      s_cnt = 0;
+      marks[priv_idx(a, abase, p)] = tok;
+    }
+    __syncthreads();
+    const int32_t np_adj = a.nadj[p], np_el = a.nel[p];
+    const int32_t* padj = a.adj + a.g.off[p];
+    const int32_t* pel = a.el + a.g.off[p];
+    for (int32_t i = threadIdx.x; i < np_adj; i += blockDim.x) {
+      const int32_t w = padj[i];
+      if (atomicExch(&marks[priv_idx(a, abase, w)], tok) != tok) scratch[atomicAdd(&s_cnt, 1)] = w;
+    }
+    for (int32_t ei = 0; ei < np_el; ++ei) {
+      const int32_t e = pel[ei];
+      const int32_t* bd = a.pool + a.bptr[e];
+      const int32_t sz = a.bsz[e];
+      for (int32_t i = threadIdx.x; i < sz; i += blockDim.x) {
+        const int32_t w = bd[i];
+        if (atomicExch(&marks[priv_idx(a, abase, w)], tok) != tok) scratch[atomicAdd(&s_cnt, 1)] = w;
+      }
+    }
+    for (int32_t ei = threadIdx.x; ei < np_el; ei += blockDim.x) a.emark[pel[ei]] = p + 1;
+    __syncthreads();
+    const int32_t nb = s_cnt;
+    // column count and etree parent (symbolic.cpp:40-43, :86-93)
+    uint64_t mn = ~0ull;
+    for (int32_t i = threadIdx.x; i < nb; i += blockDim.x) mn = min(mn, static_cast<uint64_t>(a.inverse[scratch[i]]));
+    mn = block_min_u64(mn, red);
+    if (threadIdx.x == 0) {
+      a.column_counts[pos0 + k] = static_cast<int64_t>(nb) + 1;
+      a.parent[pos0 + k] = nb ? static_cast<int32_t>(mn) : -1;
+      unsigned long long at = atomicAdd(a.pool_cursor, static_cast<unsigned long long>(nb));
+      s_at = at;
+      if (static_cast<int64_t>(at + nb) > a.pool_cap) {
+        s_abort = 1;
+        atomicExch(a.overflow, 1);
+      }
+    }
+    __syncthreads();
+    if (s_abort) return;  // host retries with a larger pool
+    int32_t* dst = a.pool + s_at;
+    for (int32_t i = threadIdx.x; i < nb; i += blockDim.x) dst[i] = scratch[i];
+    // update the node's own boundary members (elimination.cpp:75-83)
+    for (int32_t i = threadIdx.x; i < nb; i += blockDim.x) {
+      const int32_t w = scratch[i];
+      if (a.node_of[w] != X) continue;
+      const int32_t o = a.g.off[w];
+      int32_t* wa = a.adj + o;
+      int32_t c = 0;
+      const int32_t na = a.nadj[w];
+      for (int32_t j = 0; j < na; ++j) {
+        const int32_t x = wa[j];
+        if (marks[priv_idx(a, abase, x)] != tok) wa[c++] = x;
+      }
+      a.nadj[w] = c;
+      int32_t* we = a.el + o;
+      int32_t ce = 0;
+      const int32_t ne = a.nel[w];
+      for (int32_t j = 0; j < ne; ++j) {
+        const int32_t e = we[j];
+        if (a.emark[e] != p + 1) we[ce++] = e;
+      }
+      we[ce++] = p;
+      a.nel[w] = ce;
+    }
+    __syncthreads();
+    for (int32_t ei = threadIdx.x; ei < np_el; ei += blockDim.x) a.bsz[pel[ei]] = 0;
+    if (threadIdx.x == 0) {
+      a.bptr[p] = static_cast<int64_t>(s_at);
+      a.bsz[p] = nb;
+      a.nadj[p] = 0;
+      a.nel[p] = 0;
+    }
+    __syncthreads();
+  }
+  // ---- leftover: live elements created here, plus the pass-through ones
+  for (int32_t k = threadIdx.x; k < nx; k += blockDim.x) {
+    const int32_t v = verts[k];
+    if (a.bsz[v] > 0) myleft[atomicAdd(&s_nleft, 1)] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) a.left_cnt[X] = s_nleft;
+}
+
+__global__ void local_of_kernel(int32_t n, const int32_t* node_of, const int32_t* node_offsets,
+                                const int32_t* node_vertices, int32_t* local_of) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int32_t v = node_vertices[i];
+    local_of[v] = i - node_offsets[node_of[v]];
+  }
+}
+__global__ void sum_counts(int32_t n, const int64_t* cc, unsigned long long* out) {
+  __shared__ int64_t red[32];
+  int64_t s = 0, q = 0;
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    s += cc[i];
+    q += cc[i] * cc[i];
+  }
+  s = block_sum_i64(s, red);
+  q = block_sum_i64(q, red);
+  if (threadIdx.x == 0) {
+    atomicAdd(&out[0], static_cast<unsigned long long>(s));
+    atomicAdd(&out[1], static_cast<unsigned long long>(q));
+  }
+}
+__global__ void clear_bsz(int32_t n, int32_t* bsz) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) bsz[i] = 0;
+}
+
+}  // namespace
+
+void tree_fill_dev(mp_context& ctx, const DGraph& g, int32_t L, const int32_t* node_of,
+                   const int32_t* node_offsets, const int32_t* node_vertices, const int32_t* local_perm,
+                   const int32_t* node_pos, const int32_t* inverse, int64_t* column_counts,
+                   int32_t* etree_parent, int64_t* nnz_L, int64_t* cost) {
+  cudaStream_t s = ctx.stream;
+  const int32_t n = g.n;
+  const int32_t nn = static_cast<int32_t>((1LL << (L + 1)) - 1);
+  *nnz_L = 0;
+  *cost = 0;
+  if (n == 0) return;
+  // host view of the tree shape (nn+1 ints)
+  std::vector<int32_t> hoff(nn + 1);
+  MP_CUDA(cudaMemcpyAsync(hoff.data(), node_offsets, sizeof(int32_t) * (nn + 1), cudaMemcpyDeviceToHost, s));
+  int32_t m2 = 0;
+  MP_CUDA(cudaMemcpyAsync(&m2, g.off + n, 4, cudaMemcpyDeviceToHost, s));
+  MP_CUDA(cudaStreamSynchronize(s));
+  auto size_of = [&](int32_t i) -> int64_t { return hoff[i + 1] - hoff[i]; };
+  // leftover slabs: subtree sizes
+  std::vector<int64_t> sub(nn, 0), left_off(nn + 1, 0);
+  for (int32_t i = nn - 1; i >= 0; --i) {
+    sub[i] = size_of(i);
+    if (2 * i + 1 < nn) sub[i] += sub[2 * i + 1] + sub[2 * i + 2];
+  }
+  for (int32_t i = 0; i < nn; ++i) left_off[i + 1] = left_off[i] + sub[i];
+  // path sizes (node + ancestors), per level workspace offsets
+  std::vector<int64_t> path(nn, 0);
+  for (int32_t i = 0; i < nn; ++i) path[i] = size_of(i) + (i ? path[(i - 1) / 2] : 0);
+  int64_t ws_max = 0;
+  std::vector<std::vector<int64_t>> ws_offs(L + 1);
+  for (int32_t l = 0; l <= L; ++l) {
+    const int32_t first = (1 << l) - 1, width = 1 << l;
+    auto& wo = ws_offs[l];
+    wo.assign(width + 1, 0);
+    for (int32_t j = 0; j < width; ++j) wo[j + 1] = wo[j] + 2 * path[first + j] + 2;
+    ws_max = std::max(ws_max, wo[width]);
+  }
+  DevBuf<int32_t> local_of(n, s), nadj(n, s), nel(n, s), bsz(n, s), emark(n, s), ws(std::max<int64_t>(ws_max, 1), s),
+      left_cnt(nn, s), left_list(std::max<int64_t>(left_off[nn], 1), s), overflow(1, s);
+  DevBuf<int64_t> bptr(n, s), d_left_off(nn + 1, s), d_ws_off(static_cast<size_t>(1) << L | 1, s);
+  DevBuf<int32_t> adj(std::max(m2, 1), s), el(std::max(m2, 1), s);
+  DevBuf<unsigned long long> cursor(1, s), sums(2, s);
+  MP_KERNEL(ctx, local_of_kernel<<<grid_for(ctx, n), 256, 0, s>>>(n, node_of, node_offsets, node_vertices, local_of));
+  MP_CUDA(cudaMemcpyAsync(d_left_off, left_off.data(), sizeof(int64_t) * (nn + 1), cudaMemcpyHostToDevice, s));
+  int64_t cap = ctx.sym_pool_hint > 0 ? ctx.sym_pool_hint : 48LL * n + 4096;
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    DevBuf<int32_t> pool(cap, s);
+    MP_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), s));
+    MP_CUDA(cudaMemsetAsync(overflow, 0, 4, s));
+    MP_CUDA(cudaMemsetAsync(emark, 0, sizeof(int32_t) * n, s));
+    MP_KERNEL(ctx, clear_bsz<<<grid_for(ctx, n), 256, 0, s>>>(n, bsz));
+    SymArgs a{};
+    a.g = g, a.nn = nn, a.node_of = node_of, a.node_offsets = node_offsets, a.node_vertices = node_vertices;
+    a.local_perm = local_perm, a.local_of = local_of, a.node_pos = node_pos, a.inverse = inverse;
+    a.adj = adj, a.el = el, a.nadj = nadj, a.nel = nel, a.bptr = bptr, a.bsz = bsz, a.emark = emark;
+    a.pool = pool, a.pool_cap = cap, a.pool_cursor = cursor, a.ws = ws, a.left_off = d_left_off;
+    a.left_cnt = left_cnt, a.left_list = left_list, a.column_counts = column_counts, a.parent = etree_parent;
+    a.overflow = overflow;
+    for (int32_t l = L; l >= 0; --l) {
+      const int32_t width = 1 << l;
+      MP_CUDA(cudaMemcpyAsync(d_ws_off, ws_offs[l].data(), sizeof(int64_t) * (width + 1), cudaMemcpyHostToDevice, s));
+      a.level = l;
+      a.ws_off = d_ws_off;
+      MP_KERNEL(ctx, sym_kernel<<<width, kSymThreads, 0, s>>>(a));
+    }
+    int32_t h_over = 0;
+    unsigned long long used = 0;
+    MP_CUDA(cudaMemcpyAsync(&h_over, overflow, 4, cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaMemcpyAsync(&used, cursor, 8, cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+    if (!h_over) {
+      ctx.sym_pool_hint = std::max<int64_t>(ctx.sym_pool_hint, static_cast<int64_t>(used) + 4096);
+      break;
+    }
+    cap = std::max<int64_t>(2 * cap, static_cast<int64_t>(used) * 2);
+    if (attempt == 7) throw Error(MP_ENOMEM, "symbolic: element pool exhausted");
+  }
+  MP_CUDA(cudaMemsetAsync(sums, 0, 16, s));
+  MP_KERNEL(ctx, sum_counts<<<grid_for(ctx, n), 256, 0, s>>>(n, column_counts, sums));
+  unsigned long long h[2];
+  MP_CUDA(cudaMemcpyAsync(h, sums, 16, cudaMemcpyDeviceToHost, s));
+  MP_CUDA(cudaStreamSynchronize(s));
+  *nnz_L = static_cast<int64_t>(h[0]);
+  *cost = static_cast<int64_t>(h[1]);
+}
+
+}  // namespace mp
