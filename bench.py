@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""Benchmark: patch-based ND permutation of a ~1M-vertex mesh on B200.
+
+BASELINE.json metric: "permutation ms (device-timed) at 1M-vertex mesh;
+nnz(L) bit-exact vs CPU ref".  Workload (configs[1]): frequency-316 geodesic
+icosphere, n = 998,562, Laplacian (mesh-edge) pattern, patch 256, seed 0,
+default nd_level (8), approx MD, postorder.
+
+One step = one mp_order call: compute_patches -> ND tree -> per-node MD ->
+assembly (the permutation, timed per stage with CUDA events inside the
+library, summed like the reference's BenchRow t_* columns,
+pipeline.hpp:46-50) followed by the factor etree / column counts / nnz(L)
+(timed separately).  `value` = mean permutation ms per step, device-resident
+CSR, L2 flushed (512 MiB write) before every step.  `e2e` = the same call
+through the public API on pinned HOST buffers (H2D of the CSR and D2H of all
+outputs inside the timed region, host wall clock).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c2|c1|ico158|grid1000]
+
+Under torchrun (N > 1) every rank orders its own replica (the C2 path does
+not shard: SURVEY §8e "replicas only"); times are the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    # name: (generator, arg, golden nnz_L from the reference, description)
+    "c2": ("icosphere", 316, "icosphere f=316 (n=998,562), patch 256, seed 0, L=8, approx_md, postorder"),
+    "c1": ("grid", 64, "64x64 grid (n=4,096), patch 256, seed 0, L=3, approx_md, postorder"),
+    "ico158": ("icosphere", 158, "icosphere f=158 (n=249,642), one C4 frame"),
+    "grid1000": ("grid", 1000, "1000x1000 grid (n=1,000,000)"),
+}
+
+
+def load_graph(name):
+    import paper_2602_00898_b200 as mp
+    kind, arg, _ = WORKLOADS[name]
+    mesh = mp.make_icosphere_mesh(arg) if kind == "icosphere" else mp.make_grid_mesh(arg, arg)
+    return mp.mesh_to_graph(mesh)
+
+
+def golden(name):
+    p = ROOT / "tests" / "golden" / "bench_golden.json"
+    if p.exists():
+        return json.loads(p.read_text()).get(name)
+    return None
+
+
+def alg_bytes(g, L, r_fps, kernel):
+    """Algorithmic HBM bytes.  Whole path: S*(4(n+1)+8m+8n) + 8 R_fps + 12 n."""
+    n, m = g.n, g.edge_count()
+    unit = 4 * (n + 1) + 8 * m + 8 * n
+    if kernel == "path":
+        return (28 + L) * unit + 8 * r_fps + 12 * n
+    if kernel == "fps":  # each relaxation scan reads one neighbour id and its dist; dist init/readback
+        return 8 * r_fps + 8 * n
+    if kernel == "lloyd":  # 10 rounds x (assign + recenter) CSR sweeps with per-vertex state
+        return 20 * unit
+    if kernel in ("md", "symbolic"):  # one gather of the node CSRs + per-vertex state
+        return unit
+    return unit
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        import torch
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return ws, rank, local
+
+
+def max_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def cpu_reference(g, steps, warmup, threads):
+    """The unmodified reference (oracle/_ref/libmeshperm_ref.so) ordering stages."""
+    from oracle.oracle import Reference
+    R = Reference()
+    for _ in range(warmup):
+        R.order_timed(g, threads=threads)
+    times, stage = [], None
+    for _ in range(steps):
+        r = R.order_timed(g, threads=threads)
+        times.append(r["ms"])
+        stage = r["stage_ms"]
+    return float(np.mean(times)), stage, r
+
+
+def run_reference_arm(args):
+    ws, rank, _ = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    if rank != 0:
+        return 0
+    g = load_graph(args.workload)
+    threads = os.cpu_count() or 1
+    warm = min(args.warmup, 1)
+    t0 = time.time()
+    ms, stage, r = cpu_reference(g, args.steps, warm, threads)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(ms, 3), "unit": "ms", "n_gpus": ws,
+        "steps": args.steps, "warmup": warm, "ms_per_step": round(ms, 3), "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.workload][2], "n": g.n, "patch_size": 256, "seed": 0,
+                   "parallelism": f"replicas{ws}", "l2_flush": "n/a (CPU)"},
+        "stage_ms": {k: round(v, 3) for k, v in zip(["patch", "quotient", "etree", "local", "assemble"], stage)},
+        "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": threads, "kind": "reference",
+                         "sample": f"full {args.workload} ordering (stages 1-5) per step, order_tree_nodes "
+                                   f"threads={threads}"},
+        "e2e": {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": round(time.time() - t0, 1),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+METRIC = "permutation ms (device-timed) at 1M-vertex mesh; nnz(L) bit-exact vs CPU ref"
+
+
+def run_ours(args):
+    import torch
+    import paper_2602_00898_b200 as mp
+    from paper_2602_00898_b200 import api
+
+    ws, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    g = load_graph(args.workload)
+    n, m2 = g.n, int(g.offsets[-1])
+    L = mp.default_nd_level(n)
+    nn = (1 << (L + 1)) - 1
+    ctx = mp.Context(local)
+    stream = torch.cuda.Stream(device=dev)
+    ctx.set_stream(stream.cuda_stream)
+
+    d_off = torch.from_numpy(g.offsets).to(dev)
+    d_nbr = torch.from_numpy(g.neighbors).to(dev)
+    outs = {
+        "patch_of": torch.empty(n, dtype=torch.int32, device=dev),
+        "tree_node_offsets": torch.empty(nn + 1, dtype=torch.int32, device=dev),
+        "tree_vertices": torch.empty(n, dtype=torch.int32, device=dev),
+        "tree_local_perm": torch.empty(n, dtype=torch.int32, device=dev),
+        "perm": torch.empty(n, dtype=torch.int32, device=dev),
+        "inverse": torch.empty(n, dtype=torch.int32, device=dev),
+        "etree_parent": torch.empty(n, dtype=torch.int32, device=dev),
+        "column_counts": torch.empty(n, dtype=torch.int64, device=dev),
+    }
+    ptrs = {k: v.data_ptr() for k, v in outs.items()}
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        with torch.cuda.stream(stream):
+            flush.fill_(1)  # evict the L2 (126 MB) before every step
+        return api.order_device(ctx, n, d_off.data_ptr(), d_nbr.data_ptr(), ptrs)
+
+    for _ in range(args.warmup):
+        res = step()
+    torch.cuda.synchronize()
+    barrier(ws)
+    perm_ms, fill_ms, kms, launches, tot_ms = [], [], np.zeros(6), 0, []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(1)
+            ev0.record(stream)
+            res = api.order_device(ctx, n, d_off.data_ptr(), d_nbr.data_ptr(), ptrs)
+            ev1.record(stream)
+            perm_ms.append(sum(res.stage_ms[i] for i in range(5)))
+            fill_ms.append(res.stage_ms[5])
+            kms += np.array([res.kernel_ms[i] for i in range(6)])
+            launches += res.kernel_launches
+            ev1.synchronize()
+            tot_ms.append(ev0.elapsed_time(ev1))
+        torch.cuda.synchronize()
+    barrier(ws)
+    ms = max_over_ranks(float(np.mean(perm_ms)), ws)
+    ms_fill = max_over_ranks(float(np.mean(fill_ms)), ws)
+    ms_tot = max_over_ranks(float(np.mean(tot_ms)), ws)
+    kms /= args.steps
+    nnz_L = int(res.nnz_L)
+    gold = golden(args.workload)
+    r_fps = int(res.work[0])
+
+    # parity spot-check of the last step against the committed golden
+    parity = {"nnz_L": nnz_L, "golden_nnz_L": gold.get("nnz_L") if gold else None}
+    if gold:
+        parity["match"] = (nnz_L == gold["nnz_L"] and int(res.cost) == gold["cost"]
+                           and int(res.patch_count) == gold["patch_count"])
+
+    # e2e: public API on pinned host buffers (H2D + D2H inside the timed region)
+    h_off = torch.from_numpy(g.offsets).pin_memory()
+    h_nbr = torch.from_numpy(g.neighbors).pin_memory()
+    h_outs = {k: torch.empty(v.numel(), dtype=v.dtype).pin_memory() for k, v in outs.items()}
+    h_ptrs = {k: v.data_ptr() for k, v in h_outs.items()}
+    cfg = api.make_config()
+    from paper_2602_00898_b200._lib import MpCsr, MpResult, check, lib
+    import ctypes as C
+
+    def e2e_call():
+        csr = MpCsr(n, C.c_void_p(h_off.data_ptr()), C.c_void_p(h_nbr.data_ptr()), 0)
+        r = MpResult()
+        r.on_device = 0
+        for k, v in h_ptrs.items():
+            setattr(r, k, C.c_void_p(v))
+        check(lib().mp_order(ctx.handle, C.byref(csr), C.byref(cfg), C.byref(r)))
+        return r
+
+    e2e_call()
+    e2e_ms = []
+    for _ in range(max(1, min(args.steps, 5))):
+        with torch.cuda.stream(stream):
+            flush.fill_(1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = e2e_call()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_v = max_over_ranks(float(np.mean(e2e_ms)), ws)
+    h2d = 4 * (n + 1) + 4 * m2
+    d2h = sum(v.numel() * v.element_size() for v in h_outs.values())
+
+    line = None
+    if rank == 0:
+        names = ["fps", "lloyd", "fm", "refine", "md", "symbolic"]
+        dom = int(np.argmax(kms))
+        dom_name = names[dom]
+        ab = alg_bytes(g, L, r_fps, dom_name)
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() \
+            else {"hbm_gbs": 6650.0}
+        peak = float(peaks.get("hbm_gbs", 6650.0))
+        achieved = ab / (kms[dom] * 1e-3) / 1e9 if kms[dom] > 0 else 0.0
+        path_bytes = alg_bytes(g, L, r_fps, "path")
+        traffic = None
+        tp = ROOT / "profiles" / "traffic.json"
+        if tp.exists():
+            traffic = json.loads(tp.read_text()).get(dom_name)
+        cpu = None
+        if not args.no_cpu and ws >= 1:
+            threads = os.cpu_count() or 1
+            try:
+                cms, cstage, _ = cpu_reference(g, 1, 0, threads)
+                cpu = {"value": round(cms, 3), "unit": "ms", "cores": threads, "kind": "reference",
+                       "sample": f"one full {args.workload} ordering (stages 1-5) with the reference core, "
+                                 f"order_tree_nodes threads={threads}",
+                       "stage_ms": {k: round(v, 2) for k, v in
+                                    zip(["patch", "quotient", "etree", "local", "assemble"], cstage)}}
+            except Exception as e:  # reference .so missing on this box
+                cpu = {"value": None, "unit": "ms", "cores": None, "kind": "reference", "sample": f"unavailable: {e}"}
+        line = {
+            "metric": METRIC, "value": round(ms, 3), "unit": "ms", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_tot, 3), "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.workload][2], "n": n, "nnz_A": int(res.nnz_A),
+                       "patch_size": 256, "seed": 0, "nd_level": L, "parallelism": f"replicas{ws}",
+                       "l2_flush": "512 MiB write before every step"},
+            "vertices_per_s": round(ws * n / (ms * 1e-3), 1),
+            "fill_ms": round(ms_fill, 3),
+            "stage_ms": {k: round(float(res.stage_ms[i]), 3) for i, k in
+                         enumerate(["patch", "quotient", "etree", "local", "assemble", "symbolic"])},
+            "kernel_ms": {k: round(float(v), 3) for k, v in zip(names, kms)},
+            "parity": parity,
+            "patch_count": int(res.patch_count),
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "kernel": dom_name, "achieved": round(achieved, 2), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 5), "traffic": traffic,
+                         "alg_bytes_per_launch": int(ab),
+                         "path": {"alg_bytes": int(path_bytes),
+                                  "achieved": round(path_bytes / (ms * 1e-3) / 1e9, 2),
+                                  "frac": round(path_bytes / (ms * 1e-3) / 1e9 / peak, 5)}},
+            "work": {"r_fps": r_fps, "fm_moves": int(res.work[1]), "refine_moves": int(res.work[2]),
+                     "lloyd_levels": int(res.work[3])},
+            "e2e": {"value": round(e2e_v, 3), "unit": "ms", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

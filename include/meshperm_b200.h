@@ -87,6 +87,13 @@ typedef struct {
      0 patch, 1 quotient, 2 etree, 3 local, 4 assemble, 5 symbolic */
   float stage_ms[6];
   int64_t kernel_launches;     /* kernels launched by this call */
+  /* device time (CUDA events) of the dominant kernels, ms, summed over launches:
+     0 farthest-point seeds, 1 Lloyd rounds, 2 FM bipartition, 3 separator
+     refinement, 4 minimum degree, 5 symbolic game */
+  float kernel_ms[6];
+  /* work counters of this call: 0 FPS adjacency scans (R_fps), 1 FM moves,
+     2 refine moves, 3 Lloyd BFS levels */
+  int64_t work[4];
 } mp_result;
 
 const char* mp_last_error(void);

@@ -53,6 +53,8 @@ class MpResult(C.Structure):
         ("fill_ratio", C.c_double),
         ("stage_ms", C.c_float * 6),
         ("kernel_launches", C.c_int64),
+        ("kernel_ms", C.c_float * 6),
+        ("work", C.c_int64 * 4),
     ]
 
 

@@ -134,6 +134,19 @@ struct ScopedDevice {
 }  // namespace
 }  // namespace mp
 
+int mp_context::ktime_begin(int slot) {
+  const size_t first = 2 * kev_used.size();
+  while (kev.size() < first + 2) {
+    cudaEvent_t e;
+    MP_CUDA(cudaEventCreate(&e));
+    kev.push_back(e);
+  }
+  MP_CUDA(cudaEventRecord(kev[first], stream));
+  kev_used.push_back({slot, static_cast<int>(first)});
+  return static_cast<int>(first);
+}
+void mp_context::ktime_end(int first) { MP_CUDA(cudaEventRecord(kev[first + 1], stream)); }
+
 using namespace mp;
 
 extern "C" {
@@ -155,6 +168,8 @@ int mp_context_create(mp_context** out, int32_t device) {
     ctx->stream = ctx->own_stream;
     MP_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
     for (auto& e : ctx->ev) MP_CUDA(cudaEventCreate(&e));
+    MP_CUDA(cudaMalloc(reinterpret_cast<void**>(&ctx->dwork), 4 * sizeof(unsigned long long)));
+    MP_CUDA(cudaMemset(ctx->dwork, 0, 4 * sizeof(unsigned long long)));
     // keep freed scratch in the pool between calls (stream-ordered allocator)
     cudaMemPool_t pool;
     MP_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -170,6 +185,8 @@ void mp_context_destroy(mp_context* ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->kev) cudaEventDestroy(e);
+  if (ctx->dwork) cudaFree(ctx->dwork);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }
@@ -351,6 +368,8 @@ int mp_order(mp_context* ctx, const mp_csr* g, const mp_config* cfg, mp_result* 
     const int32_t nn = static_cast<int32_t>((1LL << (L + 1)) - 1);
     const int64_t N = static_cast<int64_t>(b) * n;
 
+    ctx->ktime_reset();
+    MP_CUDA(cudaMemsetAsync(ctx->dwork, 0, 4 * sizeof(unsigned long long), s));
     MP_CUDA(cudaEventRecord(ctx->ev[0], s));
     GraphView gv;
     make_view(*ctx, g, gv);
@@ -437,7 +456,15 @@ int mp_order(mp_context* ctx, const mp_csr* g, const mp_config* cfg, mp_result* 
       out->stage_ms[i] = ms;
     }
     if (!cfg->want_fill) out->stage_ms[5] = 0;
+    for (int i = 0; i < kKSlots; ++i) out->kernel_ms[i] = 0;
+    for (auto& [slot, first] : ctx->kev_used) {
+      MP_CUDA(cudaEventElapsedTime(&ms, ctx->kev[first], ctx->kev[first + 1]));
+      out->kernel_ms[slot] += ms;
+    }
     out->kernel_launches = ctx->launches - launches0;
+    unsigned long long hw[4];
+    MP_CUDA(cudaMemcpy(hw, ctx->dwork, sizeof hw, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < 4; ++i) out->work[i] = static_cast<int64_t>(hw[i]);
   });
 }
 

@@ -310,7 +310,7 @@ void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t L, const int
   a.pool_off = pool_off, a.order_ws = order, a.local_perm = local_perm, a.overflow = overflow;
   const size_t smem = sizeof(uint32_t) * kSmemDegCap;
   MP_CUDA(cudaFuncSetAttribute(md_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  MP_KERNEL(ctx, md_kernel<<<nn, kMdThreads, smem, s>>>(a));
+  { const int kt__ = ctx.ktime_begin(kKMd); MP_KERNEL(ctx, md_kernel<<<nn, kMdThreads, smem, s>>>(a)); ctx.ktime_end(kt__); }
   int32_t h_over = 0;
   MP_CUDA(cudaMemcpyAsync(&h_over, overflow, 4, cudaMemcpyDeviceToHost, s));
   MP_CUDA(cudaStreamSynchronize(s));

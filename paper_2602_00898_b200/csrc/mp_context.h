@@ -17,8 +17,20 @@ struct mp_context {
   // pinned staging for host-memory arguments
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
-  // symbolic-pool size learnt from earlier calls (ints)
-  int64_t sym_pool_hint = 0;
+  // symbolic boundary-pool size learnt from earlier calls (ints per vertex)
+  double sym_pool_ratio = 0.0;
+  // per-kernel event pairs of the current call (mp_result.kernel_ms)
+  std::vector<cudaEvent_t> kev;
+  std::vector<std::pair<int, int>> kev_used;  // (kernel slot, first event index)
+  void ktime_reset() {
+    kev_used.clear();
+    for (auto& w : work) w = 0;
+  }
+  // device work counters of the current call (mp_result.work), device memory
+  unsigned long long* dwork = nullptr;
+  int64_t work[4] = {0, 0, 0, 0};
+  int ktime_begin(int slot);
+  void ktime_end(int first);
 };
 
 namespace mp {
@@ -28,6 +40,9 @@ struct DGraph {
   const int32_t* off;
   const int32_t* nbr;
 };
+
+// Kernel-time slots reported in mp_result.kernel_ms.
+enum KernelSlot { kKFps = 0, kKLloyd = 1, kKFm = 2, kKRefine = 3, kKMd = 4, kKSym = 5, kKSlots = 6 };
 
 // Count a launch and check it.
 #define MP_KERNEL(ctx, ...)        \

@@ -72,7 +72,7 @@ struct LevelArgs {
   int32_t* next_vlist;
   int32_t* next_start;     // per next-level node
   int32_t* next_cnt;
-  int32_t* stats;          // [0] moves FM, [1] moves refine (diagnostics)
+  unsigned long long* stats;  // [0] moves FM, [1] moves refine (work counters)
   // FM scratch (per patch, in plist layout)
   int32_t* fm_gain;
   int32_t* fm_fifo;        // capacity per node: poff span + edges -> allocated 2*P + E
@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(kNodeThreads) fm_kernel(LevelArgs a) {
     if (s_stop) break;
   }
   for (int32_t i = threadIdx.x; i < np; i += blockDim.x) a.side[pl[i]] = side[i];
-  if (threadIdx.x == 0) atomicAdd(&a.stats[0], static_cast<int32_t>(total_moves));
+  if (threadIdx.x == 0) atomicAdd(&a.stats[0], static_cast<unsigned long long>(total_moves));
 }
 
 // ---------------------------------------------------------------- super separator
@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a, int32
   if (threadIdx.x == 0) {
     a.next_start[lc] = s0, a.next_cnt[lc] = runl;
     a.next_start[rc] = s0 + runl, a.next_cnt[rc] = runr;
-    atomicAdd(&a.stats[1], s_moves);
+    atomicAdd(&a.stats[1], static_cast<unsigned long long>(s_moves));
   }
   (void)next_first_local;
 }
@@ -710,13 +710,14 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
   const int32_t Pm = std::max(P, 1);
   DevBuf<int32_t> vl_a(std::max(n, 1), s), vl_b(std::max(n, 1), s), seplist(std::max(n, 1), s);
   DevBuf<int32_t> pw(Pm, s), pnode(Pm, s), lidx(Pm, s), flag(Pm, s), pkey(Pm, s), pkey_out(Pm, s);
-  DevBuf<int32_t> alive_p(Pm, s), plist(Pm, s), fm_gain(Pm, s), fm_moves(Pm, s), stats(2, s), cnt(4, s);
+  DevBuf<int32_t> alive_p(Pm, s), plist(Pm, s), fm_gain(Pm, s), fm_moves(Pm, s), cnt(4, s);
+  DevBuf<unsigned long long> stats(2, s);
   DevBuf<int64_t> fm_rec(3LL * Pm, s);
   DevBuf<int8_t> region(std::max(n, 1), s);
   DevBuf<uint8_t> in_super(std::max(n, 1), s), in_list(std::max(n, 1), s), side(Pm, s);
   DevBuf<uint64_t> keys(std::max(m2, 1), s);
   MP_CUDA(cudaMemsetAsync(in_list, 0, std::max(n, 1), s));
-  MP_CUDA(cudaMemsetAsync(stats, 0, 8, s));
+  MP_CUDA(cudaMemsetAsync(stats, 0, 16, s));
   MP_KERNEL(ctx, fill32<<<grid_for(ctx, n), 256, 0, s>>>(n, node_of, 0));
   MP_KERNEL(ctx, iota32<<<grid_for(ctx, n), 256, 0, s>>>(n, vl_a));
 
@@ -744,7 +745,7 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     a.pw = pw, a.pnode = pnode, a.np_node = np_node, a.active = active, a.lidx = lidx;
     a.side = side, a.region = region, a.in_super = in_super, a.in_list = in_list, a.bcount = bcount;
     a.sep_list = seplist, a.next_vlist = nxt_list, a.next_start = next_start, a.next_cnt = next_cnt;
-    a.stats = stats, a.fm_gain = fm_gain, a.fm_moves = fm_moves, a.fm_rec = fm_rec;
+    a.stats = ctx.dwork ? ctx.dwork + 1 : stats.get(), a.fm_gain = fm_gain, a.fm_moves = fm_moves, a.fm_rec = fm_rec;
     const dim3 lgrid(std::max(1, grid_for(ctx, n) / std::max(1, width)), std::min(width, 65535));
     MP_KERNEL(ctx, level_weights<<<lgrid, 256, 0, s>>>(a));
     MP_KERNEL(ctx, level_patch_counts<<<grid_for(ctx, P), 256, 0, s>>>(a));
@@ -813,9 +814,9 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     const size_t fm_smem = 2 * static_cast<size_t>(maxnp) + 16;
     if (fm_smem > 48 * 1024)
       MP_CUDA(cudaFuncSetAttribute(fm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fm_smem)));
-    MP_KERNEL(ctx, fm_kernel<<<width, kNodeThreads, fm_smem, s>>>(a));
+    { const int kt__ = ctx.ktime_begin(kKFm); MP_KERNEL(ctx, fm_kernel<<<width, kNodeThreads, fm_smem, s>>>(a)); ctx.ktime_end(kt__); }
     MP_KERNEL(ctx, super_pass<<<lgrid, 256, 0, s>>>(a));
-    MP_KERNEL(ctx, refine_kernel<<<width, kNodeThreads, 0, s>>>(a, 0));
+    { const int kt__ = ctx.ktime_begin(kKRefine); MP_KERNEL(ctx, refine_kernel<<<width, kNodeThreads, 0, s>>>(a, 0)); ctx.ktime_end(kt__); }
     // next level
     seg_start = std::move(next_start);
     seg_cnt = std::move(next_cnt);

@@ -193,6 +193,7 @@ struct FpsArgs {
   int32_t* frontier;     // 2 * n scratch; component c uses [2*start, 2*start + 2*size)
   int32_t* seeds;        // by global patch id
   uint64_t seed;
+  unsigned long long* work;  // [0] += adjacency scans of the relaxations (R_fps)
 };
 
 __device__ __forceinline__ int32_t vtx_at(const FpsArgs& a, int32_t pos) {
@@ -269,11 +270,13 @@ __global__ void __launch_bounds__(kFpsThreads) fps_kernel(FpsArgs a) {
     __syncthreads();
     // relax_from (patching.cpp:35-49): single-source BFS with strict decrease
     int32_t nf = 1, d = 0;
+    unsigned long long scans = 0;
     int32_t *front = fa, *next = fb;
     while (nf > 0) {
       for (int32_t i = threadIdx.x; i < nf; i += blockDim.x) {
         const int32_t u = front[i];
         const int32_t e = a.g.off[u + 1];
+        scans += e - a.g.off[u];
         for (int32_t j = a.g.off[u]; j < e; ++j) {
           const int32_t w = a.g.nbr[j];
           if (d + 1 < __ldcg(&a.dist[w])) {
@@ -301,6 +304,7 @@ __global__ void __launch_bounds__(kFpsThreads) fps_kernel(FpsArgs a) {
       if (threadIdx.x == 0) n_next = 0;
       __syncthreads();
     }
+    if (a.work && scans) atomicAdd(&a.work[0], scans);
     // refresh touched tiles, then touched supertiles
     if (overflow) {
       for (int32_t t = wid; t < ntile; t += nwarp) {
@@ -367,6 +371,7 @@ struct LloydArgs {
   int32_t* fa;
   int32_t* fb;
   int32_t* counters;         // [3] rotating frontier counters + [3] = any-active
+  unsigned long long* work;  // [3] += BFS levels
 };
 
 __device__ __forceinline__ bool lloyd_active(const LloydArgs& a, int32_t v) {
@@ -420,6 +425,7 @@ __global__ void lloyd_kernel(LloydArgs a) {
           }
         }
         grid.sync();
+        if (tid == 0 && a.work) atomicAdd(&a.work[3], 1ull);
         int32_t* t = front;
         front = next;
         next = t;
@@ -1006,8 +1012,8 @@ int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, ui
     fa.comp_start = comp_start, fa.comp_size = comp_size, fa.comp_k = comp_k;
     fa.comp_mode = comp_mode, fa.comp_base = comp_base, fa.tile_base = tile_base;
     fa.super_base = super_base, fa.dist = dist, fa.tile_key = tkey, fa.super_key = skey;
-    fa.tile_bits = tbits, fa.frontier = fr, fa.seeds = seeds, fa.seed = seed;
-    MP_KERNEL(ctx, fps_kernel<<<C, kFpsThreads, 0, s>>>(fa));
+    fa.tile_bits = tbits, fa.frontier = fr, fa.seeds = seeds, fa.seed = seed, fa.work = ctx.dwork;
+    { const int kt__ = ctx.ktime_begin(kKFps); MP_KERNEL(ctx, fps_kernel<<<C, kFpsThreads, 0, s>>>(fa)); ctx.ktime_end(kt__); }
 
     // Lloyd rounds: one cooperative kernel
     DevBuf<int32_t> label(n, s), prev(n, s), active(C, s), changed(static_cast<int64_t>(kLloydRounds) * C, s),
@@ -1039,11 +1045,12 @@ int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, ui
     la.fa = fr.get();
     la.fb = fr.get() + n;
     la.counters = counters;
+    la.work = ctx.dwork;
     int bpsm = 0;
     MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, lloyd_kernel, 256, 0));
     int blocks = std::max(1, std::min(bpsm, 4)) * ctx.num_sms;
     void* args[] = {&la};
-    MP_KERNEL(ctx, MP_CUDA(cudaLaunchCooperativeKernel((void*)lloyd_kernel, blocks, 256, args, 0, s)));
+    { const int kt__ = ctx.ktime_begin(kKLloyd); MP_KERNEL(ctx, MP_CUDA(cudaLaunchCooperativeKernel((void*)lloyd_kernel, blocks, 256, args, 0, s))); ctx.ktime_end(kt__); }
     MP_KERNEL(ctx, lloyd_finish<<<grid_for(ctx, n), 256, 0, s>>>(n, comp_of.get(), comp_mode, prev, assignment));
   }
   DevBuf<int32_t> conn(n, s);

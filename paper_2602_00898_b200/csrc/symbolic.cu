@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(kSymThreads) sym_kernel(SymArgs a) {
   const int32_t first = (1 << a.level) - 1;
   const int32_t X = first + blockIdx.x;
   if (X >= a.nn) return;
+  if (*static_cast<volatile int32_t*>(a.overflow)) return;  // an earlier node ran out of pool
   const int32_t xb = a.node_offsets[X], nx = a.node_offsets[X + 1] - xb;
   const int32_t lc = 2 * X + 1, rc = 2 * X + 2;
   const bool has_children = lc < a.nn;
@@ -299,12 +300,14 @@ void tree_fill_dev(mp_context& ctx, const DGraph& g, int32_t L, const int32_t* n
   }
   DevBuf<int32_t> local_of(n, s), nadj(n, s), nel(n, s), bsz(n, s), emark(n, s), ws(std::max<int64_t>(ws_max, 1), s),
       left_cnt(nn, s), left_list(std::max<int64_t>(left_off[nn], 1), s), overflow(1, s);
-  DevBuf<int64_t> bptr(n, s), d_left_off(nn + 1, s), d_ws_off(static_cast<size_t>(1) << L | 1, s);
+  DevBuf<int64_t> bptr(n, s), d_left_off(nn + 1, s), d_ws_off((static_cast<size_t>(1) << L) + 1, s);
   DevBuf<int32_t> adj(std::max(m2, 1), s), el(std::max(m2, 1), s);
   DevBuf<unsigned long long> cursor(1, s), sums(2, s);
   MP_KERNEL(ctx, local_of_kernel<<<grid_for(ctx, n), 256, 0, s>>>(n, node_of, node_offsets, node_vertices, local_of));
   MP_CUDA(cudaMemcpyAsync(d_left_off, left_off.data(), sizeof(int64_t) * (nn + 1), cudaMemcpyHostToDevice, s));
-  int64_t cap = ctx.sym_pool_hint > 0 ? ctx.sym_pool_hint : 48LL * n + 4096;
+  // boundary pool: sum of reach sizes = nnz(L) - n; start from the ratio seen
+  // on earlier calls of this context, grow and replay on overflow
+  int64_t cap = std::max<int64_t>(48LL * n, static_cast<int64_t>(ctx.sym_pool_ratio * 1.25 * n)) + 4096;
   for (int attempt = 0; attempt < 8; ++attempt) {
     DevBuf<int32_t> pool(cap, s);
     MP_CUDA(cudaMemsetAsync(cursor, 0, sizeof(unsigned long long), s));
@@ -323,7 +326,7 @@ void tree_fill_dev(mp_context& ctx, const DGraph& g, int32_t L, const int32_t* n
       MP_CUDA(cudaMemcpyAsync(d_ws_off, ws_offs[l].data(), sizeof(int64_t) * (width + 1), cudaMemcpyHostToDevice, s));
       a.level = l;
       a.ws_off = d_ws_off;
-      MP_KERNEL(ctx, sym_kernel<<<width, kSymThreads, 0, s>>>(a));
+      { const int kt__ = ctx.ktime_begin(kKSym); MP_KERNEL(ctx, sym_kernel<<<width, kSymThreads, 0, s>>>(a)); ctx.ktime_end(kt__); }
     }
     int32_t h_over = 0;
     unsigned long long used = 0;
@@ -331,7 +334,7 @@ void tree_fill_dev(mp_context& ctx, const DGraph& g, int32_t L, const int32_t* n
     MP_CUDA(cudaMemcpyAsync(&used, cursor, 8, cudaMemcpyDeviceToHost, s));
     MP_CUDA(cudaStreamSynchronize(s));
     if (!h_over) {
-      ctx.sym_pool_hint = std::max<int64_t>(ctx.sym_pool_hint, static_cast<int64_t>(used) + 4096);
+      ctx.sym_pool_ratio = std::max(ctx.sym_pool_ratio, static_cast<double>(used) / std::max(n, 1));
       break;
     }
     cap = std::max<int64_t>(2 * cap, static_cast<int64_t>(used) * 2);
