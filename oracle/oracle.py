@@ -46,10 +46,10 @@ class _Base:
         if not self.path.exists():
             raise FileNotFoundError(f"{self.path} missing; run `make -C oracle`")
         self.lib = C.CDLL(str(self.path))
-        self.lib[self.prefix + "last_error"].restype = C.c_char_p
+        getattr(self.lib, self.prefix + "last_error").restype = C.c_char_p
 
     def _f(self, name):
-        return self.lib[self.prefix + name]
+        return getattr(self.lib, self.prefix + name)
 
     def _check(self, rc):
         if rc != 0:

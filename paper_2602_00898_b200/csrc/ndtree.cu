@@ -75,8 +75,18 @@ struct LevelArgs {
   unsigned long long* stats;  // [0] moves FM, [1] moves refine (work counters)
   // FM scratch (per patch, in plist layout)
   int32_t* fm_gain;
+  int32_t* fm_w;           // global fallback state for nodes beyond kFmSmemPatches
+  int32_t* fm_ab;
+  int32_t* fm_ae;
+  uint8_t* fm_side;        // 2 * P bytes: side then lock flags
+  const int32_t* qloc;     // quotient adjacency as node-local patch indices
   int32_t* fm_fifo;        // capacity per node: poff span + edges -> allocated 2*P + E
   const int64_t* fm_fifo_off;  // per level node
+  int32_t* slot_of;        // refine: vertex -> candidate-list slot
+  int32_t* ref_pull;       // refine: global fallback lists (vlist layout)
+  uint8_t* ref_own;
+  uint8_t* ref_in;
+  int32_t* ref_pulled;
   int32_t* fm_moves;
   int64_t* fm_rec;         // 3 per move: cut, sw0, sw1
 };
@@ -159,41 +169,56 @@ __global__ void quotient_csr(int32_t U, const uint64_t* ukeys, const int32_t* uc
 }
 
 // ---------------------------------------------------------------- FM (one CTA per node)
-// bipartition_quotient, partition.cpp:25-163.
+// bipartition_quotient, partition.cpp:25-163.  The node's patch state
+// (weight, gain, side, lock, adjacency bounds) lives in shared memory when it
+// fits (global scratch otherwise); the adjacency carries node-local indices
+// (qloc).  A move is the block argmax of (gain desc, id asc) over the feasible
+// unlocked patches -- the first feasible entry of the reference's
+// std::set<(-gain,id)> -- followed by a warp-0 update: two barriers per move.
+constexpr int32_t kFmSmemPatches = 10 * 1024;
+constexpr int kFmBytesPerPatch = 18;
+
 __global__ void __launch_bounds__(kNodeThreads) fm_kernel(LevelArgs a) {
   const int32_t li = blockIdx.x;
   if (!a.active[li]) return;
   const int32_t pbeg = a.poff[li], np = a.poff[li + 1] - pbeg;
   const int32_t* pl = a.plist + pbeg;
-  int32_t* gain = a.fm_gain + pbeg;
   int32_t* fifo = a.fm_fifo + a.fm_fifo_off[li];
   int32_t* moves = a.fm_moves + pbeg;
   int64_t* rec = a.fm_rec + 3LL * pbeg;
 
-  extern __shared__ uint8_t smem[];
-  // smem layout: side[np] locked/visited[np]
-  uint8_t* side = smem;
-  uint8_t* flag = smem + np;
+  extern __shared__ int32_t fm_sm[];
+  const bool in_smem = np <= kFmSmemPatches;
+  int32_t* w = in_smem ? fm_sm : a.fm_w + pbeg;
+  int32_t* gain = in_smem ? fm_sm + np : a.fm_gain + pbeg;
+  int32_t* ab = in_smem ? fm_sm + 2 * np : a.fm_ab + pbeg;
+  int32_t* ae = in_smem ? fm_sm + 3 * np : a.fm_ae + pbeg;
+  uint8_t* side = in_smem ? reinterpret_cast<uint8_t*>(fm_sm + 4 * np) : a.fm_side + pbeg;
+  uint8_t* flag = side + (in_smem ? np : a.P);  // visited / locked
+
   __shared__ uint64_t red[32];
   __shared__ int64_t s_total, s_left, s_cut, s_sw[2], s_best_cut, s_pass_cut;
-  __shared__ double s_thr, s_cur_imb, s_best_imb, s_pass_imb;
+  __shared__ double s_thr, s_best_imb, s_pass_imb;
   __shared__ int32_t s_nm, s_best_len, s_head, s_tail, s_u, s_stop;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
 
   int64_t tot = 0;
   for (int32_t i = threadIdx.x; i < np; i += blockDim.x) {
+    const int32_t p = pl[i];
+    w[i] = a.pw[p];
+    ab[i] = a.qoff[p];
+    ae[i] = a.qoff[p + 1];
     side[i] = 1;  // right (partition.cpp:34)
     flag[i] = 0;
-    tot += a.pw[pl[i]];
+    tot += w[i];
   }
   tot = block_sum_i64(tot, reinterpret_cast<int64_t*>(red));
   if (threadIdx.x == 0) s_total = tot, s_left = 0, s_head = 0, s_tail = 0;
   __syncthreads();
 
   // ---- greedy growing from the heaviest patch (partition.cpp:53-79)
-  const int lane = threadIdx.x & 31;
   for (;;) {
     if (s_left * 2 >= s_total) break;
-    // pop the fifo skipping visited (warp 0 lane 0), else heaviest unvisited
     if (threadIdx.x == 0) {
       int32_t h = s_head;
       while (h < s_tail && flag[fifo[h]]) ++h;
@@ -201,33 +226,30 @@ __global__ void __launch_bounds__(kNodeThreads) fm_kernel(LevelArgs a) {
       s_head = h;
     }
     __syncthreads();
-    if (s_u < 0) {
+    if (s_u < 0) {  // fifo empty: heaviest unvisited patch (weight desc, id asc)
       uint64_t best = 0;
       for (int32_t i = threadIdx.x; i < np; i += blockDim.x)
         if (!flag[i]) {
-          uint64_t k = key_max(static_cast<uint32_t>(a.pw[pl[i]]), static_cast<uint32_t>(pl[i]));
+          const uint64_t k = key_max(static_cast<uint32_t>(w[i]), static_cast<uint32_t>(i));
           best = k > best ? k : best;
         }
       best = block_max_u64(best, red);
-      if (threadIdx.x == 0) s_u = a.lidx[key_max_id(best)];
+      if (threadIdx.x == 0) s_u = static_cast<int32_t>(key_max_id(best));
       __syncthreads();
     }
-    if (threadIdx.x < 32) {
+    if (wid == 0) {
       const int32_t u = s_u;
       if (lane == 0) {
         flag[u] = 1;
         side[u] = 0;
-        s_left += a.pw[pl[u]];
+        s_left += w[u];
       }
       __syncwarp();
-      const int32_t p = pl[u];
-      const int32_t e0 = a.qoff[p], e1 = a.qoff[p + 1];
+      const int32_t e0 = ab[u], e1 = ae[u];
       int32_t tail = s_tail;
-      __syncwarp();
       for (int32_t j0 = e0; j0 < e1; j0 += 32) {
         const int32_t j = j0 + lane;
-        int32_t nb = -1;
-        if (j < e1) nb = a.lidx[a.qnbr[j]];
+        const int32_t nb = j < e1 ? __ldg(&a.qloc[j]) : 0;
         const bool push = j < e1 && !flag[nb];
         const uint32_t m = __ballot_sync(0xffffffffu, push);
         if (push) fifo[tail + __popc(m & ((1u << lane) - 1))] = nb;
@@ -239,13 +261,11 @@ __global__ void __launch_bounds__(kNodeThreads) fm_kernel(LevelArgs a) {
   }
   // cut of the grown split (partition.cpp:81-84)
   int64_t cut = 0;
-  for (int32_t i = threadIdx.x; i < np; i += blockDim.x) {
-    const int32_t p = pl[i];
-    for (int32_t j = a.qoff[p]; j < a.qoff[p + 1]; ++j) {
-      const int32_t q = a.qnbr[j];
-      if (q > p && side[i] != side[a.lidx[q]]) cut += a.qw[j];
+  for (int32_t i = threadIdx.x; i < np; i += blockDim.x)
+    for (int32_t j = ab[i]; j < ae[i]; ++j) {
+      const int32_t nb = __ldg(&a.qloc[j]);
+      if (nb > i && side[i] != side[nb]) cut += __ldg(&a.qw[j]);  // local order == patch id order
     }
-  }
   cut = block_sum_i64(cut, reinterpret_cast<int64_t*>(red));
   if (threadIdx.x == 0) {
     s_cut = cut;
@@ -258,10 +278,12 @@ __global__ void __launch_bounds__(kNodeThreads) fm_kernel(LevelArgs a) {
   int64_t total_moves = 0;
   for (int pass = 0; pass < kFmPasses; ++pass) {
     for (int32_t i = threadIdx.x; i < np; i += blockDim.x) {
-      const int32_t p = pl[i];
       int32_t val = 0;
-      for (int32_t j = a.qoff[p]; j < a.qoff[p + 1]; ++j)
-        val += side[a.lidx[a.qnbr[j]]] != side[i] ? a.qw[j] : -a.qw[j];
+      const uint8_t si = side[i];
+      for (int32_t j = ab[i]; j < ae[i]; ++j) {
+        const int32_t wj = __ldg(&a.qw[j]);
+        val += side[__ldg(&a.qloc[j])] != si ? wj : -wj;
+      }
       gain[i] = val;
       flag[i] = 0;  // unlocked
     }
@@ -270,10 +292,10 @@ __global__ void __launch_bounds__(kNodeThreads) fm_kernel(LevelArgs a) {
       s_pass_imb = imbalance_of(s_sw[0], s_sw[1]);
       s_best_cut = s_pass_cut;
       s_best_imb = s_pass_imb;
-      s_cur_imb = s_pass_imb;
-      s_thr = kBalanceTol > s_cur_imb ? kBalanceTol : s_cur_imb;
+      s_thr = kBalanceTol > s_pass_imb ? kBalanceTol : s_pass_imb;
       s_nm = 0;
       s_best_len = 0;
+      s_stop = 0;
     }
     __syncthreads();
     for (;;) {
@@ -282,50 +304,58 @@ __global__ void __launch_bounds__(kNodeThreads) fm_kernel(LevelArgs a) {
       uint64_t best = 0;
       for (int32_t i = threadIdx.x; i < np; i += blockDim.x) {
         if (flag[i]) continue;
-        const int32_t s = side[i];
-        const int64_t w = a.pw[pl[i]];
-        const int64_t ns = (s ? sw1 : sw0) - w, nt = (s ? sw0 : sw1) + w;
+        const int32_t sd = side[i];
+        const int64_t wi = w[i];
+        const int64_t ns = (sd ? sw1 : sw0) - wi, nt = (sd ? sw0 : sw1) + wi;
         if (ns <= 0) continue;  // never empty a side
-        if (imbalance_of(ns, nt) > thr) continue;
         const uint64_t k = key_max(static_cast<uint32_t>(gain[i] + kGainBias), static_cast<uint32_t>(i));
-        best = k > best ? k : best;
+        if (k <= best) continue;
+        if (imbalance_of(ns, nt) > thr) continue;
+        best = k;
       }
-      best = block_max_u64(best, red);
-      if (best == 0) break;
-      const int32_t ch = static_cast<int32_t>(key_max_id(best));
-      if (threadIdx.x == 0) {
-        flag[ch] = 1;
-        const int32_t m = s_nm++;
-        moves[m] = ch;
-        rec[3 * m] = s_cut, rec[3 * m + 1] = s_sw[0], rec[3 * m + 2] = s_sw[1];
-        const int32_t s = side[ch];
-        const int64_t w = a.pw[pl[ch]];
-        s_sw[s] -= w;
-        s_sw[1 - s] += w;
-        side[ch] = static_cast<uint8_t>(1 - s);
-        s_cut -= gain[ch];
-      }
+      best = warp_max_u64(best);
+      if (lane == 0) red[wid] = best;
       __syncthreads();
-      if (threadIdx.x < 32) {
-        const int32_t p = pl[ch];
-        const uint8_t sc = side[ch];
-        for (int32_t j = a.qoff[p] + lane; j < a.qoff[p + 1]; j += 32) {
-          const int32_t nb = a.lidx[a.qnbr[j]];
-          if (flag[nb]) continue;
-          gain[nb] += side[nb] == sc ? -2 * a.qw[j] : 2 * a.qw[j];
-        }
-        if (lane == 0) {
-          const double imb = imbalance_of(s_sw[0], s_sw[1]);
-          if (s_cut < s_best_cut || (s_cut == s_best_cut && imb < s_best_imb)) {
-            s_best_cut = s_cut;
-            s_best_imb = imb;
-            s_best_len = s_nm;
+      if (wid == 0) {
+        uint64_t k = lane < nw ? red[lane] : 0;
+        k = warp_max_u64(k);
+        if (k == 0) {
+          if (lane == 0) s_stop = 1;
+        } else {
+          const int32_t ch = static_cast<int32_t>(key_max_id(k));
+          const int32_t gch = gain[ch];
+          if (lane == 0) {
+            flag[ch] = 1;
+            const int32_t m = s_nm++;
+            moves[m] = ch;
+            rec[3 * m] = s_cut, rec[3 * m + 1] = s_sw[0], rec[3 * m + 2] = s_sw[1];
+            const int32_t sd = side[ch];
+            s_sw[sd] -= w[ch];
+            s_sw[1 - sd] += w[ch];
+            side[ch] = static_cast<uint8_t>(1 - sd);
+            s_cut -= gch;
           }
-          s_cur_imb = imb;
-          s_thr = kBalanceTol > imb ? kBalanceTol : imb;
+          __syncwarp();
+          const uint8_t sc = side[ch];
+          for (int32_t j = ab[ch] + lane; j < ae[ch]; j += 32) {
+            const int32_t nb = __ldg(&a.qloc[j]);
+            if (flag[nb]) continue;
+            const int32_t wj = __ldg(&a.qw[j]);
+            gain[nb] += side[nb] == sc ? -2 * wj : 2 * wj;
+          }
+          if (lane == 0) {
+            const double imb = imbalance_of(s_sw[0], s_sw[1]);
+            if (s_cut < s_best_cut || (s_cut == s_best_cut && imb < s_best_imb)) {
+              s_best_cut = s_cut;
+              s_best_imb = imb;
+              s_best_len = s_nm;
+            }
+            s_thr = kBalanceTol > imb ? kBalanceTol : imb;
+          }
         }
       }
       __syncthreads();
+      if (s_stop) break;
     }
     const int32_t nm = s_nm, bl = s_best_len;
     total_moves += nm;
@@ -345,6 +375,10 @@ __global__ void __launch_bounds__(kNodeThreads) fm_kernel(LevelArgs a) {
   }
   for (int32_t i = threadIdx.x; i < np; i += blockDim.x) a.side[pl[i]] = side[i];
   if (threadIdx.x == 0) atomicAdd(&a.stats[0], static_cast<unsigned long long>(total_moves));
+}
+
+__global__ void local_adjacency(int32_t U, const int32_t* qnbr, const int32_t* lidx, int32_t* qloc) {
+  for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < U; j += gridDim.x * blockDim.x) qloc[j] = lidx[qnbr[j]];
 }
 
 // ---------------------------------------------------------------- super separator
@@ -389,15 +423,25 @@ __device__ __forceinline__ RefKey warp_min_ref(RefKey k) {
   return k;
 }
 
-__global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a, int32_t next_first_local) {
+// refine_separator (partition.cpp:187-283).  The candidate list (every
+// vertex that has been in the separator) lives in shared memory with, per
+// entry, the vertex, its patch side, an in-separator flag and its pull count
+// (neighbours in the opposite region), maintained incrementally: a move only
+// changes the regions of the moved vertex and the vertices it pulls, so only
+// their neighbours' counts change.  A move is then a block argmin of
+// (new size, new imbalance, vertex) over in-separator entries.
+constexpr int32_t kRefSmemList = 6 * 1024;
+
+__global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
   const int32_t li = blockIdx.x;
   const int32_t s0 = a.seg_start[li], cnt = a.seg_cnt[li], node = a.first + li;
   __shared__ int32_t shi[32];
   __shared__ RefKey sred[32];
   __shared__ int64_t s_rw[2], s_size;
   __shared__ double s_imb;
-  __shared__ int32_t s_list, s_mv, s_own, s_moves;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __shared__ int32_t s_list, s_mv, s_moves, s_np;
+  extern __shared__ int32_t ref_sm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int32_t lc = 2 * li, rc = 2 * li + 1;  // children, local to the next level
   if (!a.active[li]) {
     if (threadIdx.x == 0) {
@@ -407,12 +451,18 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a, int32
     return;
   }
   const int32_t* seg = a.vlist + s0;
-  int32_t* list = a.sep_list + s0;
+  const bool in_smem = cnt <= kRefSmemList;
+  int32_t* lv = in_smem ? ref_sm : a.sep_list + s0;
+  int32_t* lpull = in_smem ? ref_sm + kRefSmemList : a.ref_pull + s0;
+  uint8_t* lown = in_smem ? reinterpret_cast<uint8_t*>(ref_sm + 2 * kRefSmemList) : a.ref_own + s0;
+  uint8_t* lin = in_smem ? lown + kRefSmemList : a.ref_in + s0;
+  auto inside = [&](int32_t w) { return a.node_of[w] == node; };
+  int32_t* s_pulled = a.ref_pulled + s0;  // vertices pulled by the current move
+
   // initial separator: the smaller boundary, ties to the left (partition.cpp:212-222)
   const int8_t take = a.bcount[2 * li] <= a.bcount[2 * li + 1] ? 0 : 1;
   {
-    int32_t run = 0;
-    int32_t c0 = 0, c1 = 0;
+    int32_t run = 0, c0 = 0, c1 = 0;
     for (int32_t i0 = 0; i0 < cnt; i0 += blockDim.x) {
       const int32_t i = i0 + threadIdx.x;
       int32_t v = -1, in = 0;
@@ -423,22 +473,36 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a, int32
       int32_t tot;
       const int32_t e = block_excl_scan(in, shi, &tot);
       if (in) {
-        list[run + e] = v;
+        const int32_t k = run + e;
+        lv[k] = v;
+        lown[k] = static_cast<uint8_t>(take);
+        lin[k] = 1;
+        a.slot_of[v] = k;
         a.region[v] = 2;
-        a.in_list[v] = 1;
       } else if (i < cnt) {
         (a.region[v] == 0 ? c0 : c1)++;
       }
       run += tot;
     }
-    int64_t r0 = block_sum_i64(c0, reinterpret_cast<int64_t*>(sred));
-    int64_t r1 = block_sum_i64(c1, reinterpret_cast<int64_t*>(sred));
+    const int64_t r0 = block_sum_i64(c0, reinterpret_cast<int64_t*>(sred));
+    const int64_t r1 = block_sum_i64(c1, reinterpret_cast<int64_t*>(sred));
     if (threadIdx.x == 0) {
       s_list = run;
       s_size = run;
       s_rw[0] = r0, s_rw[1] = r1;
       s_imb = imbalance_of(r0, r1);
       s_moves = 0;
+    }
+    __syncthreads();
+    for (int32_t k = threadIdx.x; k < run; k += blockDim.x) {
+      const int32_t v = lv[k];
+      const int8_t opp = 1 - static_cast<int8_t>(lown[k]);
+      int32_t pull = 0;
+      for (int32_t j = a.g.off[v]; j < a.g.off[v + 1]; ++j) {
+        const int32_t w = a.g.nbr[j];
+        pull += inside(w) && a.region[w] == opp;
+      }
+      lpull[k] = pull;
     }
     __syncthreads();
   }
@@ -451,71 +515,109 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a, int32
     const int32_t nl = s_list;
     RefKey best{~0ull, ~0ull};
     for (int32_t i = threadIdx.x; i < nl; i += blockDim.x) {
-      const int32_t v = list[i];
-      if (a.region[v] != 2) continue;
-      const int8_t own = static_cast<int8_t>(a.side[a.assign[v]]), opp = 1 - own;
-      int32_t pull = 0;
-      for (int32_t j = a.g.off[v]; j < a.g.off[v + 1]; ++j) {
-        const int32_t w = a.g.nbr[j];
-        if (a.node_of[w] == node && a.region[w] == opp) ++pull;
-      }
+      if (!lin[i]) continue;
+      const int32_t pull = lpull[i];
       const int64_t ns = cur - 1 + pull;
       if (ns > cur) continue;
+      const uint8_t own = lown[i];
       const double ni = imbalance_of((own ? rw1 : rw0) + 1, (own ? rw0 : rw1) - pull);
       if (ni > thr) continue;
       if (!(ns < cur || ni < cimb)) continue;
       const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(ni));
-      RefKey k{(static_cast<uint64_t>(ns) << 32) | (bits >> 32),
-               ((bits & 0xffffffffull) << 32) | static_cast<uint32_t>(v)};
+      const RefKey k{(static_cast<uint64_t>(ns) << 32) | (bits >> 32),
+                     ((bits & 0xffffffffull) << 32) | static_cast<uint32_t>(lv[i])};
       if (ref_less(k, best)) best = k;
     }
     best = warp_min_ref(best);
     if (lane == 0) sred[wid] = best;
     __syncthreads();
     if (wid == 0) {
-      RefKey k = lane < (blockDim.x >> 5) ? sred[lane] : RefKey{~0ull, ~0ull};
+      RefKey k = lane < nwarps ? sred[lane] : RefKey{~0ull, ~0ull};
       k = warp_min_ref(k);
-      if (lane == 0) {
-        s_mv = k.hi == ~0ull ? -1 : static_cast<int32_t>(k.lo & 0xffffffffu);
+      const int32_t mv = k.hi == ~0ull ? -1 : static_cast<int32_t>(k.lo & 0xffffffffu);
+      if (lane == 0) s_mv = mv;
+      if (mv >= 0) {
+        const int32_t im = a.slot_of[mv];
+        const int8_t own = static_cast<int8_t>(lown[im]), opp = 1 - own;
+        const int32_t mb = a.g.off[mv], me = a.g.off[mv + 1];
+        // 1. pull mv's opposite-region neighbours into the separator
+        int32_t tail = s_list, np = 0;
+        for (int32_t j0 = mb; j0 < me; j0 += 32) {
+          const int32_t j = j0 + lane;
+          int32_t w = -1;
+          bool pull = false;
+          if (j < me) {
+            w = a.g.nbr[j];
+            pull = inside(w) && a.region[w] == opp;
+          }
+          const uint32_t m = __ballot_sync(0xffffffffu, pull);
+          const bool fresh = pull && !a.in_list[w];
+          const uint32_t mf = __ballot_sync(0xffffffffu, fresh);
+          if (pull) {
+            a.region[w] = 2;
+            s_pulled[np + __popc(m & ((1u << lane) - 1))] = w;
+          }
+          if (fresh) {
+            const int32_t k2 = tail + __popc(mf & ((1u << lane) - 1));
+            lv[k2] = w;
+            lown[k2] = static_cast<uint8_t>(a.side[a.assign[w]]);
+            a.slot_of[w] = k2;
+            a.in_list[w] = 1;
+          }
+          tail += __popc(mf);
+          np += __popc(m);
+        }
+        __syncwarp();
+        for (int32_t t = lane; t < np; t += 32) lin[a.slot_of[s_pulled[t]]] = 2;  // 2 = pulled by this move
+        if (lane == 0) {
+          a.region[mv] = own;
+          lin[im] = 0;
+          s_list = tail;
+          s_np = np;
+        }
+        __syncwarp();
+        // 2. incremental pull counts of the other separator vertices
+        for (int32_t j = mb + lane; j < me; j += 32) {  // mv: 2 -> own
+          const int32_t x = a.g.nbr[j];
+          if (!inside(x) || a.region[x] != 2) continue;
+          const int32_t ix = a.slot_of[x];
+          if (lin[ix] == 1 && lown[ix] == opp) atomicAdd(&lpull[ix], 1);
+        }
+        for (int32_t t = lane; t < np; t += 32) {  // pulled w: opp -> 2
+          const int32_t wv = s_pulled[t];
+          for (int32_t j = a.g.off[wv]; j < a.g.off[wv + 1]; ++j) {
+            const int32_t x = a.g.nbr[j];
+            if (!inside(x) || a.region[x] != 2) continue;
+            const int32_t ix = a.slot_of[x];
+            if (lin[ix] == 1 && lown[ix] == own) atomicSub(&lpull[ix], 1);
+          }
+        }
+        __syncwarp();
+        // 3. fresh counts for the pulled vertices
+        for (int32_t t = lane; t < np; t += 32) {
+          const int32_t wv = s_pulled[t];
+          const int32_t iw = a.slot_of[wv];
+          const int8_t wopp = 1 - static_cast<int8_t>(lown[iw]);
+          int32_t pull = 0;
+          for (int32_t j = a.g.off[wv]; j < a.g.off[wv + 1]; ++j) {
+            const int32_t x = a.g.nbr[j];
+            pull += inside(x) && a.region[x] == wopp;
+          }
+          lpull[iw] = pull;
+        }
+        __syncwarp();
+        for (int32_t t = lane; t < np; t += 32) lin[a.slot_of[s_pulled[t]]] = 1;
+        if (lane == 0) {
+          s_rw[own] += 1;
+          s_rw[opp] -= np;
+          s_size = s_size - 1 + np;
+          s_imb = imbalance_of(s_rw[0], s_rw[1]);
+          ++s_moves;
+        }
       }
     }
     __syncthreads();
-    const int32_t mv = s_mv;
-    if (mv < 0) break;
-    if (wid == 0) {
-      const int8_t own = static_cast<int8_t>(a.side[a.assign[mv]]), opp = 1 - own;
-      int32_t pulled = 0;
-      int32_t tail = s_list;
-      for (int32_t j0 = a.g.off[mv]; j0 < a.g.off[mv + 1]; j0 += 32) {
-        const int32_t j = j0 + lane;
-        int32_t w = -1;
-        bool pull = false;
-        if (j < a.g.off[mv + 1]) {
-          w = a.g.nbr[j];
-          pull = a.node_of[w] == node && a.region[w] == opp;
-        }
-        const uint32_t m = __ballot_sync(0xffffffffu, pull);
-        const bool app = pull && !a.in_list[w];
-        const uint32_t ma = __ballot_sync(0xffffffffu, app);
-        if (pull) a.region[w] = 2;
-        if (app) {
-          list[tail + __popc(ma & ((1u << lane) - 1))] = w;
-          a.in_list[w] = 1;
-        }
-        tail += __popc(ma);
-        pulled += __popc(m);
-      }
-      if (lane == 0) {
-        a.region[mv] = own;
-        s_rw[own] += 1;
-        s_rw[opp] -= pulled;
-        s_size = s_size - 1 + pulled;
-        s_imb = imbalance_of(s_rw[0], s_rw[1]);
-        s_list = tail;
-        ++s_moves;
-      }
-    }
-    __syncthreads();
+    if (s_mv < 0) break;
   }
   // split the node: separator stays at `node`, sides go to the children
   // (stable, so each child's vertex list stays ascending)
@@ -547,13 +649,12 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a, int32
     }
     runl += tl, runr += tr;
   }
-  for (int32_t i = threadIdx.x; i < s_list; i += blockDim.x) a.in_list[list[i]] = 0;
+  for (int32_t i = threadIdx.x; i < s_list; i += blockDim.x) a.in_list[lv[i]] = 0;
   if (threadIdx.x == 0) {
     a.next_start[lc] = s0, a.next_cnt[lc] = runl;
     a.next_start[rc] = s0 + runl, a.next_cnt[rc] = runr;
     atomicAdd(&a.stats[1], static_cast<unsigned long long>(s_moves));
   }
-  (void)next_first_local;
 }
 
 template <class T>
@@ -713,6 +814,10 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
   DevBuf<int32_t> alive_p(Pm, s), plist(Pm, s), fm_gain(Pm, s), fm_moves(Pm, s), cnt(4, s);
   DevBuf<unsigned long long> stats(2, s);
   DevBuf<int64_t> fm_rec(3LL * Pm, s);
+  DevBuf<int32_t> fm_w(Pm, s), fm_ab(Pm, s), fm_ae(Pm, s);
+  DevBuf<uint8_t> fm_side(2LL * Pm, s);
+  DevBuf<int32_t> slot_of(std::max(n, 1), s), ref_pull(std::max(n, 1), s), ref_pulled(std::max(n, 1), s);
+  DevBuf<uint8_t> ref_own(std::max(n, 1), s), ref_in(std::max(n, 1), s);
   DevBuf<int8_t> region(std::max(n, 1), s);
   DevBuf<uint8_t> in_super(std::max(n, 1), s), in_list(std::max(n, 1), s), side(Pm, s);
   DevBuf<uint64_t> keys(std::max(m2, 1), s);
@@ -745,6 +850,8 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     a.pw = pw, a.pnode = pnode, a.np_node = np_node, a.active = active, a.lidx = lidx;
     a.side = side, a.region = region, a.in_super = in_super, a.in_list = in_list, a.bcount = bcount;
     a.sep_list = seplist, a.next_vlist = nxt_list, a.next_start = next_start, a.next_cnt = next_cnt;
+    a.fm_w = fm_w, a.fm_ab = fm_ab, a.fm_ae = fm_ae, a.fm_side = fm_side;
+    a.slot_of = slot_of, a.ref_pull = ref_pull, a.ref_own = ref_own, a.ref_in = ref_in, a.ref_pulled = ref_pulled;
     a.stats = ctx.dwork ? ctx.dwork + 1 : stats.get(), a.fm_gain = fm_gain, a.fm_moves = fm_moves, a.fm_rec = fm_rec;
     const dim3 lgrid(std::max(1, grid_for(ctx, n) / std::max(1, width)), std::min(width, 65535));
     MP_KERNEL(ctx, level_weights<<<lgrid, 256, 0, s>>>(a));
@@ -811,12 +918,16 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     a.fm_fifo = fifo, a.fm_fifo_off = fifo_off;
     // bipartition per node
     const int32_t maxnp = na_level;
-    const size_t fm_smem = 2 * static_cast<size_t>(maxnp) + 16;
-    if (fm_smem > 48 * 1024)
-      MP_CUDA(cudaFuncSetAttribute(fm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fm_smem)));
+    DevBuf<int32_t> qloc(std::max<int64_t>(U, 1), s);
+    if (U > 0) MP_KERNEL(ctx, local_adjacency<<<grid_for(ctx, U), 256, 0, s>>>(static_cast<int32_t>(U), qnbr, lidx, qloc));
+    a.qloc = qloc;
+    const size_t fm_smem = static_cast<size_t>(std::min(maxnp, kFmSmemPatches)) * kFmBytesPerPatch + 64;
+    MP_CUDA(cudaFuncSetAttribute(fm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fm_smem)));
     { const int kt__ = ctx.ktime_begin(kKFm); MP_KERNEL(ctx, fm_kernel<<<width, kNodeThreads, fm_smem, s>>>(a)); ctx.ktime_end(kt__); }
     MP_KERNEL(ctx, super_pass<<<lgrid, 256, 0, s>>>(a));
-    { const int kt__ = ctx.ktime_begin(kKRefine); MP_KERNEL(ctx, refine_kernel<<<width, kNodeThreads, 0, s>>>(a, 0)); ctx.ktime_end(kt__); }
+    const size_t ref_smem = static_cast<size_t>(kRefSmemList) * 10;
+    MP_CUDA(cudaFuncSetAttribute(refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ref_smem)));
+    { const int kt__ = ctx.ktime_begin(kKRefine); MP_KERNEL(ctx, refine_kernel<<<width, kNodeThreads, ref_smem, s>>>(a)); ctx.ktime_end(kt__); }
     // next level
     seg_start = std::move(next_start);
     seg_cnt = std::move(next_cnt);

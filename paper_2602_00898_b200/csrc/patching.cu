@@ -79,16 +79,23 @@ __global__ void uf_hook(DGraph g, int32_t* par, const int32_t* label) {
   }
 }
 
-__global__ void uf_compress(int32_t n, int32_t* par) {
-  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
-    par[v] = uf_find(par, v);
+// Read-only root lookup into a second array: a path-halving find racing with
+// the final writes could leave a non-root pointer behind.
+__global__ void uf_roots(int32_t n, const int32_t* par, int32_t* root) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    int32_t x = v, p = par[x];
+    while (p != x) x = p, p = par[x];
+    root[v] = x;
+  }
 }
 
+// par receives, for every vertex, the smallest vertex of its set.
 void union_find(mp_context& ctx, const DGraph& g, const int32_t* label, int32_t* par) {
   const int blocks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(g.n, 256), ctx.num_sms * 8));
-  MP_KERNEL(ctx, uf_init<<<blocks, 256, 0, ctx.stream>>>(g.n, par));
-  MP_KERNEL(ctx, uf_hook<<<blocks, 256, 0, ctx.stream>>>(g, par, label));
-  MP_KERNEL(ctx, uf_compress<<<blocks, 256, 0, ctx.stream>>>(g.n, par));
+  DevBuf<int32_t> work(std::max(g.n, 1), ctx.stream);
+  MP_KERNEL(ctx, uf_init<<<blocks, 256, 0, ctx.stream>>>(g.n, work));
+  MP_KERNEL(ctx, uf_hook<<<blocks, 256, 0, ctx.stream>>>(g, work, label));
+  MP_KERNEL(ctx, uf_roots<<<blocks, 256, 0, ctx.stream>>>(g.n, work, par));
 }
 
 // ------------------------------------------------------------ components
@@ -175,8 +182,17 @@ __global__ void assign_trivial(int32_t n, const int32_t* comp_list, const int32_
 // One CTA per FPS component (patching.cpp:26-65).  dist lives in HBM/L2; the
 // argmax over the component is a two-level tile-max tree of packed
 // (dist desc, id asc) keys, refreshed only over tiles a relaxation touched.
+// A relaxation is a single-source BFS with strict decrease; it runs edge
+// parallel (one thread per (frontier vertex, neighbour slot) of an 8-wide ELL
+// copy of the adjacency), with the frontier and the touched-tile bitmap in
+// shared memory and one barrier per level (rotating frontier counters).
+constexpr int kEll = 8;
+constexpr int kFrontCap = 4096;          // smem frontier entries per buffer (overflow -> global)
+constexpr int kSmemTileWords = 2048;     // smem touched bitmap: components up to 16.7M vertices
+
 struct FpsArgs {
   DGraph g;
+  const int32_t* ell;        // n * kEll: neighbours, -1 padded; slot 7 < -1 encodes a CSR tail
   const int32_t* comp_list;  // nullptr: identity (single component)
   const int32_t* pos_of;     // nullptr: identity
   const int32_t* comp_start;
@@ -189,7 +205,7 @@ struct FpsArgs {
   int32_t* dist;
   uint64_t* tile_key;
   uint64_t* super_key;
-  uint32_t* tile_bits;   // touched bitmap, one bit per tile (global, kept zero between rounds)
+  uint32_t* tile_bits;   // global touched bitmap for components too large for smem
   int32_t* frontier;     // 2 * n scratch; component c uses [2*start, 2*start + 2*size)
   int32_t* seeds;        // by global patch id
   uint64_t seed;
@@ -203,6 +219,16 @@ __device__ __forceinline__ int32_t pos_in(const FpsArgs& a, int32_t v) {
   return a.pos_of ? a.pos_of[v] : v;
 }
 
+__global__ void build_ell(DGraph g, int32_t* ell) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < g.n; v += gridDim.x * blockDim.x) {
+    const int32_t o = g.off[v], deg = g.off[v + 1] - o;
+    int32_t* e = ell + static_cast<int64_t>(v) * kEll;
+#pragma unroll
+    for (int k = 0; k < kEll; ++k) e[k] = k < deg ? g.nbr[o + k] : -1;
+    if (deg > kEll) e[kEll - 1] = -(o + kEll - 1) - 2;  // CSR tail from index o+7
+  }
+}
+
 __global__ void __launch_bounds__(kFpsThreads) fps_kernel(FpsArgs a) {
   const int32_t c = blockIdx.x;
   if (a.comp_mode[c] != kModeFps) return;
@@ -211,135 +237,143 @@ __global__ void __launch_bounds__(kFpsThreads) fps_kernel(FpsArgs a) {
   const int32_t nsuper = static_cast<int32_t>(ceil_div(ntile, kTile));
   uint64_t* tkey = a.tile_key + a.tile_base[c];
   uint64_t* skey = a.super_key + a.super_base[c];
-  uint32_t* tbits = a.tile_bits + (a.tile_base[c] + 31) / 32 + c;  // word-aligned per component
-  int32_t* fa = a.frontier + 2LL * start;
-  int32_t* fb = fa + size;
+  int32_t* gfront0 = a.frontier + 2LL * start;  // overflow parts of the two frontier buffers
+  int32_t* gfront1 = gfront0 + size;
+
+  extern __shared__ int32_t fsm[];
+  int32_t* sfront0 = fsm;
+  int32_t* sfront1 = fsm + kFrontCap;
+  uint32_t* sbits = reinterpret_cast<uint32_t*>(fsm + 2 * kFrontCap);
+  const int32_t nwords = (ntile + 31) / 32;
+  uint32_t* tbits = nwords <= kSmemTileWords ? sbits : a.tile_bits + (a.tile_base[c] + 31) / 32 + c;
 
   __shared__ int32_t touched[kTouchCap];
-  __shared__ int32_t n_touched, overflow, n_next;
+  __shared__ int32_t n_touched, overflow, cnt[3], s_cur;
   __shared__ uint32_t super_bits[64];  // up to 2048 supertiles (524M vertices)
-  __shared__ uint64_t red[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
 
   for (int32_t i = threadIdx.x; i < size; i += blockDim.x) a.dist[vtx_at(a, start + i)] = kUnreached;
   for (int32_t i = threadIdx.x; i < 64; i += blockDim.x) super_bits[i] = 0;
-  if (threadIdx.x == 0) n_touched = 0, overflow = 0, n_next = 0;
+  for (int32_t i = threadIdx.x; i < nwords; i += blockDim.x) tbits[i] = 0;
+  if (threadIdx.x == 0) {
+    n_touched = 0, overflow = 0;
+    s_cur = vtx_at(a, start + static_cast<int32_t>(splitmix64(a.seed) % static_cast<uint64_t>(size)));
+  }
   __syncthreads();
 
+  auto mark_tile = [&](int32_t v) {
+    const int32_t t = (pos_in(a, v) - start) / kTile;
+    const uint32_t bit = 1u << (t & 31);
+    if (!(atomicOr(&tbits[t >> 5], bit) & bit)) {
+      const int32_t slot = atomicAdd(&n_touched, 1);
+      if (slot < kTouchCap) touched[slot] = t;
+      else overflow = 1;
+    }
+  };
   auto tile_max = [&](int32_t t) -> uint64_t {  // warp-cooperative
     uint64_t best = 0;
     const int32_t lo = t * kTile, hi = min(size, lo + kTile);
     for (int32_t p = lo + lane; p < hi; p += 32) {
-      int32_t v = vtx_at(a, start + p);
-      int32_t d = __ldcg(&a.dist[v]);
-      uint64_t kk = key_max(static_cast<uint32_t>(d), static_cast<uint32_t>(v));
+      const int32_t v = vtx_at(a, start + p);
+      const int32_t dv = __ldcg(&a.dist[v]);
+      const uint64_t kk = key_max(static_cast<uint32_t>(dv), static_cast<uint32_t>(v));
       best = kk > best ? kk : best;
     }
     return warp_max_u64(best);
   };
-  auto super_max = [&](int32_t s) -> uint64_t {
+  auto super_max = [&](int32_t sidx) -> uint64_t {
     uint64_t best = 0;
-    const int32_t lo = s * kTile, hi = min(ntile, lo + kTile);
+    const int32_t lo = sidx * kTile, hi = min(ntile, lo + kTile);
     for (int32_t t = lo + lane; t < hi; t += 32) {
-      uint64_t kk = __ldcg(&tkey[t]);
+      const uint64_t kk = __ldcg(&tkey[t]);
       best = kk > best ? kk : best;
     }
     return warp_max_u64(best);
   };
 
-  int32_t cur = vtx_at(a, start + static_cast<int32_t>(splitmix64(a.seed) % static_cast<uint64_t>(size)));
+  unsigned long long scans = 0;
   for (int32_t s = 0; s < k; ++s) {
-    if (s > 0) {  // argmax (patching.cpp:52-60) from the top of the tree
-      uint64_t best = 0;
-      for (int32_t i = threadIdx.x; i < nsuper; i += blockDim.x) {
-        uint64_t kk = __ldcg(&skey[i]);
-        best = kk > best ? kk : best;
-      }
-      best = block_max_u64(best, red);
-      // resolve supertile -> tile -> vertex is implicit: the key carries the id
-      cur = static_cast<int32_t>(key_max_id(best));
-    }
+    const int32_t cur = s_cur;
     if (threadIdx.x == 0) {
       a.seeds[a.comp_base[c] + s] = cur;
       a.dist[cur] = 0;
-      fa[0] = cur;
-      int32_t t = pos_in(a, cur) - start;
-      t /= kTile;
-      if (!(atomicOr(&tbits[t >> 5], 1u << (t & 31)) & (1u << (t & 31)))) touched[n_touched++] = t;
+      sfront0[0] = cur;
+      cnt[0] = 1, cnt[1] = 0, cnt[2] = 0;
+      mark_tile(cur);
     }
     __syncthreads();
-    // relax_from (patching.cpp:35-49): single-source BFS with strict decrease
-    int32_t nf = 1, d = 0;
-    unsigned long long scans = 0;
-    int32_t *front = fa, *next = fb;
-    while (nf > 0) {
-      for (int32_t i = threadIdx.x; i < nf; i += blockDim.x) {
-        const int32_t u = front[i];
-        const int32_t e = a.g.off[u + 1];
-        scans += e - a.g.off[u];
-        for (int32_t j = a.g.off[u]; j < e; ++j) {
-          const int32_t w = a.g.nbr[j];
-          if (d + 1 < __ldcg(&a.dist[w])) {
-            int32_t old = atomicMin(&a.dist[w], d + 1);
-            if (old > d + 1) {
-              next[atomicAdd(&n_next, 1)] = w;
-              int32_t t = (pos_in(a, w) - start) / kTile;
-              uint32_t bit = 1u << (t & 31);
-              if (!(atomicOr(&tbits[t >> 5], bit) & bit)) {
-                int32_t slot = atomicAdd(&n_touched, 1);
-                if (slot < kTouchCap) touched[slot] = t;
-                else overflow = 1;
-              }
-            }
+    // relax_from (patching.cpp:35-49)
+    for (int32_t d = 0;; ++d) {
+      const int32_t nf = cnt[d % 3];
+      if (nf == 0) break;
+      if (threadIdx.x == 0) cnt[(d + 2) % 3] = 0;
+      const int32_t* sin = (d & 1) ? sfront1 : sfront0;
+      const int32_t* gin = (d & 1) ? gfront1 : gfront0;
+      int32_t* sout = (d & 1) ? sfront0 : sfront1;
+      int32_t* gout = (d & 1) ? gfront0 : gfront1;
+      int32_t* cout = &cnt[(d + 1) % 3];
+      auto relax = [&](int32_t w) {
+        if (d + 1 < __ldcg(&a.dist[w])) {
+          if (atomicMin(&a.dist[w], d + 1) > d + 1) {
+            const int32_t slot = atomicAdd(cout, 1);
+            if (slot < kFrontCap) sout[slot] = w;
+            else gout[slot - kFrontCap] = w;
+            mark_tile(w);
+          }
+        }
+      };
+      const int32_t items = nf * kEll;
+      for (int32_t it = threadIdx.x; it < items; it += blockDim.x) {
+        const int32_t i = it >> 3, slot = it & (kEll - 1);
+        const int32_t u = i < kFrontCap ? sin[i] : __ldcg(&gin[i - kFrontCap]);
+        const int32_t x = a.ell[static_cast<int64_t>(u) * kEll + slot];
+        if (x >= 0) {
+          ++scans;
+          relax(x);
+        } else if (x < -1) {  // degree > 8: this slot walks the CSR tail
+          const int32_t e = a.g.off[u + 1];
+          for (int32_t j = -x - 2; j < e; ++j) {
+            ++scans;
+            relax(a.g.nbr[j]);
           }
         }
       }
       __syncthreads();
-      nf = n_next;
-      int32_t* tmp = front;
-      front = next;
-      next = tmp;
-      ++d;
-      __syncthreads();
-      if (threadIdx.x == 0) n_next = 0;
-      __syncthreads();
     }
-    if (a.work && scans) atomicAdd(&a.work[0], scans);
-    // refresh touched tiles, then touched supertiles
+    // refresh touched tiles, then touched supertiles, then the top
     if (overflow) {
       for (int32_t t = wid; t < ntile; t += nwarp) {
-        uint64_t m = tile_max(t);
+        const uint64_t m = tile_max(t);
         if (lane == 0) tkey[t] = m;
       }
-      for (int32_t i = threadIdx.x; i < (ntile + 31) / 32; i += blockDim.x) tbits[i] = 0;
+      for (int32_t i = threadIdx.x; i < nwords; i += blockDim.x) tbits[i] = 0;
       __syncthreads();
       for (int32_t sidx = wid; sidx < nsuper; sidx += nwarp) {
-        uint64_t m = super_max(sidx);
+        const uint64_t m = super_max(sidx);
         if (lane == 0) skey[sidx] = m;
       }
     } else {
       const int32_t nt = n_touched;
       for (int32_t i = wid; i < nt; i += nwarp) {
-        int32_t t = touched[i];
-        uint64_t m = tile_max(t);
+        const int32_t t = touched[i];
+        const uint64_t m = tile_max(t);
         if (lane == 0) {
           tkey[t] = m;
           atomicAnd(&tbits[t >> 5], ~(1u << (t & 31)));
-          int32_t su = t / kTile;
+          const int32_t su = t / kTile;
           atomicOr(&super_bits[su >> 5], 1u << (su & 31));
         }
       }
       __syncthreads();
-      const int32_t nwords = (nsuper + 31) / 32;
-      for (int32_t wi = 0; wi < nwords; ++wi) {
+      const int32_t swords = (nsuper + 31) / 32;
+      int32_t rank = 0;
+      for (int32_t wi = 0; wi < swords; ++wi) {
         uint32_t bits = super_bits[wi];
-        // distribute set bits over warps
-        int32_t rank = 0;
         while (bits) {
-          int32_t b = __ffs(bits) - 1;
+          const int32_t b = __ffs(bits) - 1;
           bits &= bits - 1;
           if (rank % nwarp == wid) {
-            uint64_t m = super_max(wi * 32 + b);
+            const uint64_t m = super_max(wi * 32 + b);
             if (lane == 0) skey[wi * 32 + b] = m;
           }
           ++rank;
@@ -347,10 +381,24 @@ __global__ void __launch_bounds__(kFpsThreads) fps_kernel(FpsArgs a) {
       }
     }
     __syncthreads();
-    for (int32_t i = threadIdx.x; i < 64; i += blockDim.x) super_bits[i] = 0;
-    if (threadIdx.x == 0) n_touched = 0, overflow = 0;
+    // argmax over the component (patching.cpp:52-60): (dist desc, id asc)
+    if (wid == 0) {
+      uint64_t best = 0;
+      for (int32_t i = lane; i < nsuper; i += 32) {
+        const uint64_t kk = __ldcg(&skey[i]);
+        best = kk > best ? kk : best;
+      }
+      best = warp_max_u64(best);
+      if (lane == 0) {
+        s_cur = static_cast<int32_t>(key_max_id(best));
+        n_touched = 0;
+        overflow = 0;
+      }
+      for (int32_t i = lane; i < 64; i += 32) super_bits[i] = 0;
+    }
     __syncthreads();
   }
+  if (a.work && scans) atomicAdd(&a.work[0], scans);
 }
 
 // ------------------------------------------------------------ Lloyd rounds
@@ -393,7 +441,7 @@ __global__ void lloyd_kernel(LloydArgs a) {
     grid.sync();
     for (int64_t p = tid; p < a.P; p += nthreads) {
       int32_t c = a.patch_comp ? a.patch_comp[p] : 0;
-      if (a.comp_mode[c] != kModeFps || !__ldcg(&a.comp_active[c])) continue;
+      if (c < 0 || a.comp_mode[c] != kModeFps || !__ldcg(&a.comp_active[c])) continue;
       int32_t s = a.seeds[p];
       a.dist[s] = 0;
       a.label[s] = static_cast<int32_t>(p);
@@ -499,7 +547,7 @@ __global__ void lloyd_kernel(LloydArgs a) {
     grid.sync();
     for (int64_t p = tid; p < a.P; p += nthreads) {
       int32_t c = a.patch_comp ? a.patch_comp[p] : 0;
-      if (a.comp_mode[c] != kModeFps || !__ldcg(&a.comp_active[c])) continue;
+      if (c < 0 || a.comp_mode[c] != kModeFps || !__ldcg(&a.comp_active[c])) continue;
       uint64_t b = __ldcg(&a.best[p]);
       if (b != 0) a.seeds[p] = static_cast<int32_t>(key_max_id(b));
     }
@@ -1013,7 +1061,12 @@ int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, ui
     fa.comp_mode = comp_mode, fa.comp_base = comp_base, fa.tile_base = tile_base;
     fa.super_base = super_base, fa.dist = dist, fa.tile_key = tkey, fa.super_key = skey;
     fa.tile_bits = tbits, fa.frontier = fr, fa.seeds = seeds, fa.seed = seed, fa.work = ctx.dwork;
-    { const int kt__ = ctx.ktime_begin(kKFps); MP_KERNEL(ctx, fps_kernel<<<C, kFpsThreads, 0, s>>>(fa)); ctx.ktime_end(kt__); }
+    DevBuf<int32_t> ell(static_cast<int64_t>(n) * kEll, s);
+    MP_KERNEL(ctx, build_ell<<<grid_for(ctx, n), 256, 0, s>>>(g, ell));
+    fa.ell = ell;
+    const size_t fps_smem = sizeof(int32_t) * (2 * kFrontCap + kSmemTileWords);
+    MP_CUDA(cudaFuncSetAttribute(fps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fps_smem)));
+    { const int kt__ = ctx.ktime_begin(kKFps); MP_KERNEL(ctx, fps_kernel<<<C, kFpsThreads, fps_smem, s>>>(fa)); ctx.ktime_end(kt__); }
 
     // Lloyd rounds: one cooperative kernel
     DevBuf<int32_t> label(n, s), prev(n, s), active(C, s), changed(static_cast<int64_t>(kLloydRounds) * C, s),
@@ -1024,7 +1077,7 @@ int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, ui
     MP_CUDA(cudaMemsetAsync(changed, 0, sizeof(int32_t) * changed.n, s));
     if (C > 1) {
       patch_comp.alloc(P0, s);
-      MP_KERNEL(ctx, fill_i32<<<grid_for(ctx, P0), 256, 0, s>>>(P0, patch_comp, 0));
+      MP_KERNEL(ctx, fill_i32<<<grid_for(ctx, P0), 256, 0, s>>>(P0, patch_comp, -1));
       MP_KERNEL(ctx, patch_comp_kernel<<<std::min(C, 4096), 256, 0, s>>>(C, comp_mode, comp_base, comp_k,
                                                                         patch_comp));
     }

@@ -1,0 +1,245 @@
+"""GPU parity: the CUDA path (through the C ABI) is bit-exact against the
+reference on the committed golden fixtures, the reference's known answers,
+the CPU oracle on random meshes, and the BASELINE-scale goldens (C1, one C4
+frame, C2) via size-independent properties and digests."""
+import hashlib
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden_cases
+
+import paper_2602_00898_b200 as mp
+
+pytestmark = pytest.mark.gpu
+MODES = ["approx_md", "exact_md", "natural"]
+SCHED = ["postorder", "levelorder"]
+
+
+def graph(n, edges):
+    adj = [set() for _ in range(n)]
+    for u, v in edges:
+        adj[u].add(v), adj[v].add(u)
+    off = np.zeros(n + 1, np.int32)
+    nbr = []
+    for v in range(n):
+        nbr += sorted(adj[v])
+        off[v + 1] = len(nbr)
+    return mp.AdjacencyGraph(n, off, np.array(nbr, np.int32))
+
+
+def digest(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:16]
+
+
+def whole_graph_tree(n, order):
+    """An L=0 tree holding every vertex: the device game then plays `order`."""
+    return mp.EliminationTree(n, 0, np.array([0, n], np.int32), np.arange(n, dtype=np.int32),
+                              np.asarray(order, np.int32))
+
+
+def md(g, mode):
+    t = mp.EliminationTree(g.n, 0, np.array([0, g.n], np.int32), np.arange(g.n, dtype=np.int32))
+    return mp.order_tree_nodes(t, g, mode).local_perm
+
+
+@pytest.mark.parametrize("case", golden_cases(), ids=lambda c: c.name)
+def test_pipeline_matches_golden(case):
+    r = mp.order(case.g, patch_size=case.patch, nd_level=case.L_arg, local_mode=MODES[case.mode],
+                 schedule=SCHED[case.levelorder])
+    assert r.patch.patch_count == case.patch_count
+    assert np.array_equal(r.patch.assignment, case.assignment)
+    assert r.tree.nd_level == case.L
+    assert np.array_equal(r.tree.node_offsets, case.node_offsets)
+    assert np.array_equal(r.tree.vertices, case.node_vertices)
+    assert np.array_equal(r.tree.local_perm, case.local_perm)
+    assert np.array_equal(r.perm.perm, case.perm) and np.array_equal(r.perm.inverse, case.inverse)
+    assert (r.fill.nnz_A, r.fill.nnz_L, r.fill.cost) == (case.nnz_A, case.nnz_L, case.cost)
+    assert np.array_equal(r.fill.column_counts, case.column_counts)
+    assert np.array_equal(r.fill.parents, case.parents)
+    assert r.fill.fill_ratio == case.nnz_L / case.nnz_A
+    assert r.kernel_launches > 0
+
+
+@pytest.mark.parametrize("case", golden_cases(), ids=lambda c: c.name)
+def test_stages_match_golden(case):
+    g = case.g
+    p = mp.compute_patches(g, case.patch, 0)
+    assert p.patch_count == case.patch_count and np.array_equal(p.assignment, case.assignment)
+    t = mp.build_etree(g, case.assignment, case.patch_count, case.L)
+    assert np.array_equal(t.node_offsets, case.node_offsets) and np.array_equal(t.vertices, case.node_vertices)
+    mp.order_tree_nodes(t, g, MODES[case.mode])
+    assert np.array_equal(t.local_perm, case.local_perm)
+    P = mp.compute_perm(t, g, SCHED[case.levelorder])
+    assert np.array_equal(P.perm, case.perm)
+    F = mp.tree_fill(g, t, SCHED[case.levelorder])
+    assert F.nnz_L == case.nnz_L and np.array_equal(F.column_counts, case.column_counts)
+    assert np.array_equal(F.parents, case.parents)
+
+
+def test_quotient_matches_oracle(cases):
+    from oracle.oracle import Restatement
+    R = Restatement()
+    for c in cases:
+        q = mp.build_quotient(c.g, c.assignment, c.patch_count)
+        nw, e = R.build_quotient(c.g, c.assignment, c.patch_count)
+        assert np.array_equal(q.node_weight, nw) and q.edges == e, c.name
+    q = mp.build_quotient(graph(4, [(0, 1), (1, 2), (2, 3)]), [0, 0, 1, 1], 2)  # quotient_test.cpp:11-23
+    assert q.node_weight.tolist() == [2, 2] and q.edges == [(0, 1, 1)]
+
+
+def test_known_answers_on_device():
+    path = lambda n: graph(n, [(v, v + 1) for v in range(n - 1)])
+    star = lambda n: graph(n, [(0, v) for v in range(1, n)])
+    cycle = lambda n: graph(n, [(v, (v + 1) % n) for v in range(n)])
+    assert md(path(3), "approx_md").tolist() == [0, 2, 1]  # local_order_test.cpp:48-54
+    assert md(path(3), "exact_md").tolist() == [0, 1, 2]
+    assert md(star(5), "approx_md").tolist() == [1, 2, 3, 4, 0]
+    ex = md(star(5), "exact_md")
+    assert ex.tolist() == [1, 2, 3, 0, 4]
+    assert mp.tree_fill(star(5), whole_graph_tree(5, ex)).nnz_L == 9
+    assert md(cycle(4), "approx_md").tolist() == [0, 2, 1, 3]
+    f = mp.tree_fill(cycle(4), whole_graph_tree(4, np.arange(4)))  # symbolic_test.cpp:12-21
+    assert (f.nnz_A, f.nnz_L, f.cost) == (12, 9, 23) and f.column_counts.tolist() == [3, 3, 2, 1]
+    for n in (2, 5, 17, 64):
+        f = mp.tree_fill(path(n), whole_graph_tree(n, np.arange(n)))
+        assert f.nnz_L == 2 * n - 1 and f.cost == 4 * (n - 1) + 1
+    assert mp.tree_fill(star(10), whole_graph_tree(10, np.arange(10))).nnz_L == 55
+    for seed in range(5):  # patching_test.cpp:27-35
+        p = mp.compute_patches(path(4), 2, seed)
+        assert p.patch_count == 2 and p.assignment[0] == p.assignment[1] != p.assignment[2] == p.assignment[3]
+    lat = graph(25, [(i * 5 + j, i * 5 + j + 1) for i in range(5) for j in range(4)] +
+                [(i * 5 + j, i * 5 + j + 5) for i in range(4) for j in range(5)])
+    p = mp.compute_patches(lat, 1, 3)
+    assert p.patch_count == 25 and np.array_equal(p.assignment, np.arange(25))
+    e = mp.enforce_connectivity(mp.PatchPartition(np.array([0, 1, 0, 1, 0], np.int32), 2), path(5))
+    assert e.patch_count == 5 and e.assignment.tolist() == [0, 1, 2, 4, 3]
+    t = mp.build_etree(path(3), np.arange(3), 3, 1)  # etree_test.cpp:52-62
+    assert [t.node(i).tolist() for i in range(3)] == [[1], [0], [2]]
+
+
+def test_errors_are_value_errors():
+    g = mp.mesh_to_graph(mp.make_grid_mesh(6, 6))
+    with pytest.raises(ValueError, match="out of range"):
+        mp.build_etree(g, np.full(g.n, 7, np.int32), 3, 1)
+    with pytest.raises(ValueError, match="nd_level"):
+        mp.build_etree(g, np.zeros(g.n, np.int32), 1, 30)
+    with pytest.raises(ValueError, match="positive"):
+        mp.compute_patches(g, 0, 0)
+    with pytest.raises(ValueError):
+        mp.order(g, block_size=0)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_meshes_match_oracle(seed):
+    from oracle.oracle import Restatement
+    R = Restatement()
+    rng = np.random.default_rng(100 + seed)
+    r, c = int(rng.integers(5, 70)), int(rng.integers(5, 70))
+    g = mp.mesh_to_graph(mp.make_random_mesh(r, c, seed))
+    patch, mode = int(rng.integers(1, 80)), int(rng.integers(0, 3))
+    L = int(rng.integers(0, 6))
+    o = R.order(g, patch_size=patch, nd_level=L, mode=mode)
+    res = mp.order(g, patch_size=patch, nd_level=L, local_mode=MODES[mode])
+    assert np.array_equal(res.patch.assignment, o["assignment"])
+    assert np.array_equal(res.tree.vertices, o["node_vertices"])
+    assert np.array_equal(res.perm.perm, o["perm"])
+    f = R.elimination_fill(g, o["perm"])
+    assert res.fill.nnz_L == f["nnz_L"] and np.array_equal(res.fill.column_counts, f["column_counts"])
+
+
+def test_disconnected_and_tiny_graphs():
+    from oracle.oracle import Restatement
+    R = Restatement()
+    # isolated vertices, a triangle, a long path: singleton / one-patch / FPS components
+    g = graph(40, [(1, 2), (2, 3), (1, 3)] + [(v, v + 1) for v in range(10, 39)])
+    for patch in (1, 3, 8):
+        o = R.order(g, patch_size=patch, nd_level=2)
+        res = mp.order(g, patch_size=patch, nd_level=2)
+        assert np.array_equal(res.patch.assignment, o["assignment"])
+        assert np.array_equal(res.perm.perm, o["perm"])
+    g1 = graph(1, [])
+    res = mp.order(g1, nd_level=0)
+    assert res.perm.perm.tolist() == [0] and res.fill.nnz_L == 1
+
+
+def test_block_expansion_closed_form():
+    """b = 3: expand_blocks layout and nnz(L) of the expanded system equal the
+    reference's elimination game on expand_graph (graph.cpp:96-128)."""
+    from oracle.oracle import Restatement
+    R = Restatement()
+    g = mp.mesh_to_graph(mp.make_grid_mesh(12, 10))
+    b = 3
+    res1 = mp.order(g, patch_size=16, nd_level=2)
+    resb = mp.order(g, patch_size=16, nd_level=2, block_size=b)
+    p1 = res1.perm.perm
+    assert resb.perm.perm.tolist() == [b * k + t for k in p1 for t in range(b)]
+    assert np.array_equal(resb.tree.node_offsets, b * res1.tree.node_offsets)
+    # expanded graph: node cliques + dense block pairs
+    n = g.n
+    eb = []
+    for v in range(n):
+        for s in range(b):
+            for t in range(s + 1, b):
+                eb.append((b * v + s, b * v + t))
+        for w in g.neighbors_of(v):
+            if w > v:
+                eb += [(b * v + s, b * w + t) for s in range(b) for t in range(b)]
+    gx = graph(b * n, eb)
+    f = R.elimination_fill(gx, resb.perm.perm)
+    assert resb.fill.nnz_L == f["nnz_L"] and resb.fill.cost == f["cost"]
+    assert np.array_equal(resb.fill.column_counts, f["column_counts"])
+    assert np.array_equal(resb.fill.parents, R.factor_etree_parents(gx, resb.perm.perm))
+    assert resb.fill.nnz_A == f["nnz_A"]
+
+
+def check_tree_properties(g, res):
+    n = g.n
+    perm, inv = res.perm.perm, res.perm.inverse
+    assert np.array_equal(np.sort(perm), np.arange(n)) and np.array_equal(inv[perm], np.arange(n))
+    off = res.tree.node_offsets
+    node_of = np.repeat(np.arange(len(off) - 1), np.diff(off))
+    owner = np.empty(n, np.int64)
+    owner[res.tree.vertices] = node_of
+    # every edge joins ancestor-related nodes (no cross-block fill possible)
+    u = np.repeat(np.arange(n), np.diff(g.offsets))
+    a, b = owner[u], owner[g.neighbors]
+    lo, hi = np.minimum(a, b), np.maximum(a, b)
+    for _ in range(30):
+        hi = np.where(hi > lo, (hi - 1) // 2, hi)
+    assert np.array_equal(hi, lo)
+    assert int(res.fill.column_counts.sum()) == res.fill.nnz_L
+
+
+@pytest.mark.parametrize("name", ["c1", "ico158", "c2"])
+def test_baseline_configs_match_reference_digests(name):
+    gold = json.loads((GOLDEN / "bench_golden.json").read_text())[name]
+    if name == "c1":
+        g = mp.mesh_to_graph(mp.make_grid_mesh(64, 64))
+    else:
+        g = mp.mesh_to_graph(mp.make_icosphere_mesh(158 if name == "ico158" else 316))
+    res = mp.order(g)
+    assert res.patch.patch_count == gold["patch_count"]
+    assert res.tree.nd_level == gold["nd_level"]
+    assert res.tree.node_offsets[1] - res.tree.node_offsets[0] == gold["root_separator"]
+    assert (res.fill.nnz_A, res.fill.nnz_L, res.fill.cost) == (gold["nnz_A"], gold["nnz_L"], gold["cost"])
+    assert digest(res.patch.assignment) == gold["sha_assignment"]
+    assert digest(res.tree.node_offsets) == gold["sha_node_offsets"]
+    assert digest(res.tree.vertices) == gold["sha_node_vertices"]
+    assert digest(res.tree.local_perm) == gold["sha_local_perm"]
+    assert digest(res.perm.perm) == gold["sha_perm"]
+    assert digest(res.fill.column_counts) == gold["sha_column_counts"]
+    assert digest(res.fill.parents) == gold["sha_parents"]
+    check_tree_properties(g, res)
+
+
+def test_deterministic_across_calls_and_contexts():
+    g = mp.mesh_to_graph(mp.make_icosphere_mesh(40))
+    a = mp.order(g)
+    ctx = mp.Context(0)
+    b = mp.order(g, ctx=ctx)
+    c = mp.order(g, ctx=ctx)
+    for x in (b, c):
+        assert np.array_equal(a.perm.perm, x.perm.perm) and a.fill.nnz_L == x.fill.nnz_L
+        assert np.array_equal(a.fill.parents, x.fill.parents)
