@@ -76,6 +76,8 @@ struct LevelArgs {
   // FM scratch (per patch, in plist layout)
   int32_t* fm_gain;
   int32_t* fm_w;           // global fallback state for nodes beyond kFmSmemPatches
+  uint64_t* fm_lk;
+  uint64_t* fm_bm;
   int32_t* fm_ab;
   int32_t* fm_ae;
   uint8_t* fm_side;        // 2 * P bytes: side then lock flags
@@ -177,8 +179,9 @@ __global__ void quotient_csr(int32_t U, const uint64_t* ukeys, const int32_t* uc
 // std::set<(-gain,id)> -- followed by a warp-0 update: two barriers per move.
 constexpr int32_t kFmSmemPatches = 10 * 1024;
 constexpr int kFmBytesPerPatch = 18;
+constexpr int kFmThreads = 256;  // power of two: patch i is owned by thread i & (kFmThreads-1)
 
-__global__ void __launch_bounds__(kNodeThreads) fm_kernel(LevelArgs a) {
+__global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
   const int32_t li = blockIdx.x;
   if (!a.active[li]) return;
   const int32_t pbeg = a.poff[li], np = a.poff[li + 1] - pbeg;
@@ -196,7 +199,7 @@ __global__ void __launch_bounds__(kNodeThreads) fm_kernel(LevelArgs a) {
   uint8_t* side = in_smem ? reinterpret_cast<uint8_t*>(fm_sm + 4 * np) : a.fm_side + pbeg;
   uint8_t* flag = side + (in_smem ? np : a.P);  // visited / locked
 
-  __shared__ uint64_t red[32];
+  __shared__ uint64_t red[32], red2[64];
   __shared__ int64_t s_total, s_left, s_cut, s_sw[2], s_best_cut, s_pass_cut;
   __shared__ double s_thr, s_best_imb, s_pass_imb;
   __shared__ int32_t s_nm, s_best_len, s_head, s_tail, s_u, s_stop;
@@ -274,7 +277,12 @@ __global__ void __launch_bounds__(kNodeThreads) fm_kernel(LevelArgs a) {
   }
   __syncthreads();
 
-  // ---- FM passes with rollback to the best prefix (partition.cpp:95-159)
+  // ---- FM passes with rollback to the best prefix (partition.cpp:95-159).
+  // Patch i is owned by thread i % blockDim: only the owner reads or writes its
+  // gain / lock / side during a pass.  Every thread keeps an identical
+  // register copy of the scalar state (side weights, cut, best prefix), the
+  // winner's side rides in the key's low bit, and the reduction slots are
+  // double buffered, so a move costs one barrier.
   int64_t total_moves = 0;
   for (int pass = 0; pass < kFmPasses; ++pass) {
     for (int32_t i = threadIdx.x; i < np; i += blockDim.x) {
@@ -287,91 +295,106 @@ __global__ void __launch_bounds__(kNodeThreads) fm_kernel(LevelArgs a) {
       gain[i] = val;
       flag[i] = 0;  // unlocked
     }
-    if (threadIdx.x == 0) {
-      s_pass_cut = s_cut;
-      s_pass_imb = imbalance_of(s_sw[0], s_sw[1]);
-      s_best_cut = s_pass_cut;
-      s_best_imb = s_pass_imb;
-      s_thr = kBalanceTol > s_pass_imb ? kBalanceTol : s_pass_imb;
-      s_nm = 0;
-      s_best_len = 0;
-      s_stop = 0;
-    }
     __syncthreads();
-    for (;;) {
-      const int64_t sw0 = s_sw[0], sw1 = s_sw[1];
-      const double thr = s_thr;
+    const int64_t pass_cut = s_cut;
+    int64_t sw0 = s_sw[0], sw1 = s_sw[1], cut = s_cut;
+    const double pass_imb = imbalance_of(sw0, sw1);
+    int64_t best_cut = pass_cut;
+    double best_imb = pass_imb, thr = kBalanceTol > pass_imb ? kBalanceTol : pass_imb;
+    int32_t nm = 0, best_len = 0;
+    // per-thread cache: the unconstrained best (gain desc, id asc) of the
+    // owned unlocked patches, recomputed only when one of them changed
+    auto own_key = [&](int32_t i) -> uint64_t {
+      return (static_cast<uint64_t>(static_cast<uint32_t>(gain[i] + kGainBias)) << 32) |
+             ((0x7fffffffu - static_cast<uint32_t>(i)) << 1) | side[i];
+    };
+    auto feasible = [&](int32_t i, uint32_t sd) {
+      const int64_t wi = w[i];
+      const int64_t ns = (sd ? sw1 : sw0) - wi, nt = (sd ? sw0 : sw1) + wi;
+      return ns > 0 && !(imbalance_of(ns, nt) > thr);  // never empty a side
+    };
+    auto recompute = [&]() -> uint64_t {
+      uint64_t m = 0;
+      for (int32_t i = threadIdx.x; i < np; i += kFmThreads)
+        if (!flag[i]) m = max(m, own_key(i));
+      return m;
+    };
+    uint64_t mine = recompute();
+    for (int32_t mv = 0;; ++mv) {
       uint64_t best = 0;
-      for (int32_t i = threadIdx.x; i < np; i += blockDim.x) {
-        if (flag[i]) continue;
-        const int32_t sd = side[i];
-        const int64_t wi = w[i];
-        const int64_t ns = (sd ? sw1 : sw0) - wi, nt = (sd ? sw0 : sw1) + wi;
-        if (ns <= 0) continue;  // never empty a side
-        const uint64_t k = key_max(static_cast<uint32_t>(gain[i] + kGainBias), static_cast<uint32_t>(i));
-        if (k <= best) continue;
-        if (imbalance_of(ns, nt) > thr) continue;
-        best = k;
-      }
-      best = warp_max_u64(best);
-      if (lane == 0) red[wid] = best;
-      __syncthreads();
-      if (wid == 0) {
-        uint64_t k = lane < nw ? red[lane] : 0;
-        k = warp_max_u64(k);
-        if (k == 0) {
-          if (lane == 0) s_stop = 1;
-        } else {
-          const int32_t ch = static_cast<int32_t>(key_max_id(k));
-          const int32_t gch = gain[ch];
-          if (lane == 0) {
-            flag[ch] = 1;
-            const int32_t m = s_nm++;
-            moves[m] = ch;
-            rec[3 * m] = s_cut, rec[3 * m + 1] = s_sw[0], rec[3 * m + 2] = s_sw[1];
-            const int32_t sd = side[ch];
-            s_sw[sd] -= w[ch];
-            s_sw[1 - sd] += w[ch];
-            side[ch] = static_cast<uint8_t>(1 - sd);
-            s_cut -= gch;
-          }
-          __syncwarp();
-          const uint8_t sc = side[ch];
-          for (int32_t j = ab[ch] + lane; j < ae[ch]; j += 32) {
-            const int32_t nb = __ldg(&a.qloc[j]);
-            if (flag[nb]) continue;
-            const int32_t wj = __ldg(&a.qw[j]);
-            gain[nb] += side[nb] == sc ? -2 * wj : 2 * wj;
-          }
-          if (lane == 0) {
-            const double imb = imbalance_of(s_sw[0], s_sw[1]);
-            if (s_cut < s_best_cut || (s_cut == s_best_cut && imb < s_best_imb)) {
-              s_best_cut = s_cut;
-              s_best_imb = imb;
-              s_best_len = s_nm;
-            }
-            s_thr = kBalanceTol > imb ? kBalanceTol : imb;
+      if (mine) {
+        const int32_t ci = static_cast<int32_t>(0x7fffffffu - static_cast<uint32_t>((mine & 0xffffffffu) >> 1));
+        if (feasible(ci, static_cast<uint32_t>(mine & 1u))) {
+          best = mine;
+        } else {  // the owned maximum is infeasible: best feasible owned patch
+          for (int32_t i = threadIdx.x; i < np; i += kFmThreads) {
+            if (flag[i]) continue;
+            const uint64_t k = own_key(i);
+            if (k > best && feasible(i, side[i])) best = k;
           }
         }
       }
+      best = warp_max_u64(best);
+      uint64_t* slot = red2 + 32 * (mv & 1);
+      if (lane == 0) slot[wid] = best;
       __syncthreads();
-      if (s_stop) break;
+      uint64_t k = lane < nw ? slot[lane] : 0;
+      k = warp_max_u64(k);
+      if (k == 0) break;
+      const int32_t ch = static_cast<int32_t>(0x7fffffffu - static_cast<uint32_t>((k & 0xffffffffu) >> 1));
+      const uint32_t sd = static_cast<uint32_t>(k & 1u);
+      const int32_t gch = static_cast<int32_t>(static_cast<uint32_t>(k >> 32)) - kGainBias;
+      const int64_t wc = w[ch];
+      if (threadIdx.x == 0) {
+        moves[nm] = ch;
+        rec[3 * nm] = cut, rec[3 * nm + 1] = sw0, rec[3 * nm + 2] = sw1;
+      }
+      bool dirty = false;
+      if ((ch & (kFmThreads - 1)) == static_cast<int32_t>(threadIdx.x)) {
+        flag[ch] = 1;
+        side[ch] = static_cast<uint8_t>(1 - sd);
+        dirty = true;
+      }
+      ++nm;
+      if (sd) sw1 -= wc, sw0 += wc;
+      else sw0 -= wc, sw1 += wc;
+      cut -= gch;
+      // neighbours' gains, each updated by its owner (partition.cpp:137-142)
+      const uint32_t sc = 1 - sd;
+      const int32_t e0 = ab[ch], e1 = ae[ch];
+      for (int32_t j = e0; j < e1; ++j) {
+        const int32_t nb = __ldg(&a.qloc[j]);
+        if ((nb & (kFmThreads - 1)) != static_cast<int32_t>(threadIdx.x) || flag[nb]) continue;
+        const int32_t wj = __ldg(&a.qw[j]);
+        gain[nb] += side[nb] == sc ? -2 * wj : 2 * wj;
+        dirty = true;
+      }
+      if (dirty) mine = recompute();
+      const double imb = imbalance_of(sw0, sw1);
+      if (cut < best_cut || (cut == best_cut && imb < best_imb)) {
+        best_cut = cut;
+        best_imb = imb;
+        best_len = nm;
+      }
+      thr = kBalanceTol > imb ? kBalanceTol : imb;
     }
-    const int32_t nm = s_nm, bl = s_best_len;
     total_moves += nm;
-    for (int32_t m = bl + threadIdx.x; m < nm; m += blockDim.x) side[moves[m]] ^= 1;
+    __syncthreads();
+    for (int32_t m = best_len + threadIdx.x; m < nm; m += blockDim.x) side[moves[m]] ^= 1;
     __syncthreads();
     if (threadIdx.x == 0) {
-      if (nm > bl) {
-        s_cut = rec[3 * bl];
-        s_sw[0] = rec[3 * bl + 1];
-        s_sw[1] = rec[3 * bl + 2];
+      if (nm > best_len) {
+        s_cut = rec[3 * best_len];
+        s_sw[0] = rec[3 * best_len + 1];
+        s_sw[1] = rec[3 * best_len + 2];
+      } else {
+        s_cut = cut;
+        s_sw[0] = sw0, s_sw[1] = sw1;
       }
-      const bool improved = s_best_cut < s_pass_cut || (s_best_cut == s_pass_cut && s_best_imb < s_pass_imb);
-      s_stop = improved ? 0 : 1;
     }
     __syncthreads();
-    if (s_stop) break;
+    const bool improved = best_cut < pass_cut || (best_cut == pass_cut && best_imb < pass_imb);
+    if (!improved) break;
   }
   for (int32_t i = threadIdx.x; i < np; i += blockDim.x) a.side[pl[i]] = side[i];
   if (threadIdx.x == 0) atomicAdd(&a.stats[0], static_cast<unsigned long long>(total_moves));
@@ -815,6 +838,7 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
   DevBuf<unsigned long long> stats(2, s);
   DevBuf<int64_t> fm_rec(3LL * Pm, s);
   DevBuf<int32_t> fm_w(Pm, s), fm_ab(Pm, s), fm_ae(Pm, s);
+  DevBuf<uint64_t> fm_lk(Pm, s), fm_bm(Pm / 32 + (1LL << std::min(L, 20)) + 64, s);
   DevBuf<uint8_t> fm_side(2LL * Pm, s);
   DevBuf<int32_t> slot_of(std::max(n, 1), s), ref_pull(std::max(n, 1), s), ref_pulled(std::max(n, 1), s);
   DevBuf<uint8_t> ref_own(std::max(n, 1), s), ref_in(std::max(n, 1), s);
@@ -850,7 +874,7 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     a.pw = pw, a.pnode = pnode, a.np_node = np_node, a.active = active, a.lidx = lidx;
     a.side = side, a.region = region, a.in_super = in_super, a.in_list = in_list, a.bcount = bcount;
     a.sep_list = seplist, a.next_vlist = nxt_list, a.next_start = next_start, a.next_cnt = next_cnt;
-    a.fm_w = fm_w, a.fm_ab = fm_ab, a.fm_ae = fm_ae, a.fm_side = fm_side;
+    a.fm_w = fm_w, a.fm_ab = fm_ab, a.fm_ae = fm_ae, a.fm_side = fm_side, a.fm_lk = fm_lk, a.fm_bm = fm_bm;
     a.slot_of = slot_of, a.ref_pull = ref_pull, a.ref_own = ref_own, a.ref_in = ref_in, a.ref_pulled = ref_pulled;
     a.stats = ctx.dwork ? ctx.dwork + 1 : stats.get(), a.fm_gain = fm_gain, a.fm_moves = fm_moves, a.fm_rec = fm_rec;
     const dim3 lgrid(std::max(1, grid_for(ctx, n) / std::max(1, width)), std::min(width, 65535));
@@ -921,9 +945,9 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     DevBuf<int32_t> qloc(std::max<int64_t>(U, 1), s);
     if (U > 0) MP_KERNEL(ctx, local_adjacency<<<grid_for(ctx, U), 256, 0, s>>>(static_cast<int32_t>(U), qnbr, lidx, qloc));
     a.qloc = qloc;
-    const size_t fm_smem = static_cast<size_t>(std::min(maxnp, kFmSmemPatches)) * kFmBytesPerPatch + 64;
+    const size_t fm_smem = static_cast<size_t>(std::min(maxnp, kFmSmemPatches)) * kFmBytesPerPatch + 512;
     MP_CUDA(cudaFuncSetAttribute(fm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fm_smem)));
-    { const int kt__ = ctx.ktime_begin(kKFm); MP_KERNEL(ctx, fm_kernel<<<width, kNodeThreads, fm_smem, s>>>(a)); ctx.ktime_end(kt__); }
+    { const int kt__ = ctx.ktime_begin(kKFm); MP_KERNEL(ctx, fm_kernel<<<width, kFmThreads, fm_smem, s>>>(a)); ctx.ktime_end(kt__); }
     MP_KERNEL(ctx, super_pass<<<lgrid, 256, 0, s>>>(a));
     const size_t ref_smem = static_cast<size_t>(kRefSmemList) * 10;
     MP_CUDA(cudaFuncSetAttribute(refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ref_smem)));
