@@ -26,6 +26,7 @@ constexpr int kLloydRounds = 10;  // patching.cpp:15
 constexpr int kTile = 256;        // FPS argmax tile (positions in the component list)
 constexpr int kFpsThreads = 1024;
 constexpr int kTouchCap = 2048;   // touched-tile list capacity per round (overflow = full rescan)
+constexpr int32_t kBatchedFpsMin = 1 << 15;  // single components from this size use fps_batched_dev
 
 enum CompMode : int32_t { kModeSingletons = 0, kModeOne = 1, kModeFps = 2 };
 
@@ -956,6 +957,8 @@ int32_t repair_sizes_dev(mp_context& ctx, const DGraph& g, int32_t* assignment, 
 
 }  // namespace
 
+void fps_batched_dev(mp_context& ctx, const DGraph& g, int32_t k, uint64_t seed, int32_t* seeds, int32_t* dist);
+
 int32_t enforce_connectivity_dev(mp_context& ctx, const DGraph& g, const int32_t* in,
                                  int32_t P, int32_t* out) {
   cudaStream_t s = ctx.stream;
@@ -1061,12 +1064,17 @@ int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, ui
     fa.comp_mode = comp_mode, fa.comp_base = comp_base, fa.tile_base = tile_base;
     fa.super_base = super_base, fa.dist = dist, fa.tile_key = tkey, fa.super_key = skey;
     fa.tile_bits = tbits, fa.frontier = fr, fa.seeds = seeds, fa.seed = seed, fa.work = ctx.dwork;
-    DevBuf<int32_t> ell(static_cast<int64_t>(n) * kEll, s);
-    MP_KERNEL(ctx, build_ell<<<grid_for(ctx, n), 256, 0, s>>>(g, ell));
-    fa.ell = ell;
-    const size_t fps_smem = sizeof(int32_t) * (2 * kFrontCap + kSmemTileWords);
-    MP_CUDA(cudaFuncSetAttribute(fps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fps_smem)));
-    { const int kt__ = ctx.ktime_begin(kKFps); MP_KERNEL(ctx, fps_kernel<<<C, kFpsThreads, fps_smem, s>>>(fa)); ctx.ktime_end(kt__); }
+    if (C == 1 && n >= kBatchedFpsMin) {
+      // one large component: exact speculative batches over the whole GPU
+      fps_batched_dev(ctx, g, P0, seed, seeds, dist);
+    } else {
+      DevBuf<int32_t> ell(static_cast<int64_t>(n) * kEll, s);
+      MP_KERNEL(ctx, build_ell<<<grid_for(ctx, n), 256, 0, s>>>(g, ell));
+      fa.ell = ell;
+      const size_t fps_smem = sizeof(int32_t) * (2 * kFrontCap + kSmemTileWords);
+      MP_CUDA(cudaFuncSetAttribute(fps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fps_smem)));
+      { const int kt__ = ctx.ktime_begin(kKFps); MP_KERNEL(ctx, fps_kernel<<<C, kFpsThreads, fps_smem, s>>>(fa)); ctx.ktime_end(kt__); }
+    }
 
     // Lloyd rounds: one cooperative kernel
     DevBuf<int32_t> label(n, s), prev(n, s), active(C, s), changed(static_cast<int64_t>(kLloydRounds) * C, s),
