@@ -92,8 +92,11 @@ typedef struct {
      refinement, 4 minimum degree, 5 symbolic game */
   float kernel_ms[6];
   /* work counters of this call: 0 FPS adjacency scans (R_fps), 1 FM moves,
-     2 refine moves, 3 Lloyd BFS levels */
-  int64_t work[4];
+     2 refine moves, 3 Lloyd BFS levels, 4 FPS batches, 5 FPS grid-mode BFS
+     levels, 6 FPS candidates evaluated, 7 FPS worker-region BFS levels,
+     8..15 FPS phase timers (ns, CTA 0: grid-mode, regions, walk+commit,
+     refresh, candidate selection) */
+  int64_t work[16];
 } mp_result;
 
 const char* mp_last_error(void);

@@ -54,7 +54,7 @@ class MpResult(C.Structure):
         ("stage_ms", C.c_float * 6),
         ("kernel_launches", C.c_int64),
         ("kernel_ms", C.c_float * 6),
-        ("work", C.c_int64 * 4),
+        ("work", C.c_int64 * 16),
     ]
 
 

@@ -168,8 +168,8 @@ int mp_context_create(mp_context** out, int32_t device) {
     ctx->stream = ctx->own_stream;
     MP_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
     for (auto& e : ctx->ev) MP_CUDA(cudaEventCreate(&e));
-    MP_CUDA(cudaMalloc(reinterpret_cast<void**>(&ctx->dwork), 4 * sizeof(unsigned long long)));
-    MP_CUDA(cudaMemset(ctx->dwork, 0, 4 * sizeof(unsigned long long)));
+    MP_CUDA(cudaMalloc(reinterpret_cast<void**>(&ctx->dwork), 16 * sizeof(unsigned long long)));
+    MP_CUDA(cudaMemset(ctx->dwork, 0, 16 * sizeof(unsigned long long)));
     // keep freed scratch in the pool between calls (stream-ordered allocator)
     cudaMemPool_t pool;
     MP_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
@@ -369,7 +369,7 @@ int mp_order(mp_context* ctx, const mp_csr* g, const mp_config* cfg, mp_result* 
     const int64_t N = static_cast<int64_t>(b) * n;
 
     ctx->ktime_reset();
-    MP_CUDA(cudaMemsetAsync(ctx->dwork, 0, 4 * sizeof(unsigned long long), s));
+    MP_CUDA(cudaMemsetAsync(ctx->dwork, 0, 16 * sizeof(unsigned long long), s));
     MP_CUDA(cudaEventRecord(ctx->ev[0], s));
     GraphView gv;
     make_view(*ctx, g, gv);
@@ -462,9 +462,9 @@ int mp_order(mp_context* ctx, const mp_csr* g, const mp_config* cfg, mp_result* 
       out->kernel_ms[slot] += ms;
     }
     out->kernel_launches = ctx->launches - launches0;
-    unsigned long long hw[4];
+    unsigned long long hw[16];
     MP_CUDA(cudaMemcpy(hw, ctx->dwork, sizeof hw, cudaMemcpyDeviceToHost));
-    for (int i = 0; i < 4; ++i) out->work[i] = static_cast<int64_t>(hw[i]);
+    for (int i = 0; i < 16; ++i) out->work[i] = static_cast<int64_t>(hw[i]);
   });
 }
 

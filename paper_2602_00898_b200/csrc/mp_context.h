@@ -28,7 +28,7 @@ struct mp_context {
   }
   // device work counters of the current call (mp_result.work), device memory
   unsigned long long* dwork = nullptr;
-  int64_t work[4] = {0, 0, 0, 0};
+  int64_t work[16] = {};
   int ktime_begin(int slot);
   void ktime_end(int first);
 };

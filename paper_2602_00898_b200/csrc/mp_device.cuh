@@ -123,6 +123,18 @@ __device__ __forceinline__ int32_t block_excl_scan(int32_t v, int32_t* sh, int32
   return base + x - v;
 }
 
+// Warp-aggregated append: one atomic per warp; every lane of the warp must
+// call it (pred may differ).  Returns the slot for predicated lanes, else -1.
+__device__ __forceinline__ int32_t warp_append(int32_t* counter, bool pred) {
+  const uint32_t mask = __ballot_sync(0xffffffffu, pred);
+  if (!mask) return -1;
+  const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
+  int32_t base = 0;
+  if (lane == leader) base = atomicAdd(counter, __popc(mask));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  return pred ? base + __popc(mask & ((1u << lane) - 1)) : -1;
+}
+
 // IEEE double imbalance ratio, partition.cpp:15-21.  Division is the
 // correctly rounded __ddiv_rn regardless of compiler flags.
 __device__ __forceinline__ double imbalance_of(int64_t a, int64_t b) {

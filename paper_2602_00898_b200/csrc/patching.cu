@@ -405,6 +405,7 @@ __global__ void __launch_bounds__(kFpsThreads) fps_kernel(FpsArgs a) {
 // ------------------------------------------------------------ Lloyd rounds
 struct LloydArgs {
   DGraph g;
+  const int32_t* ell;        // n * 8 ELL adjacency (build_ell)
   const int32_t* comp_of;    // nullptr: single component 0
   const int32_t* comp_mode;
   int32_t* comp_active;      // per component
@@ -430,6 +431,7 @@ __device__ __forceinline__ bool lloyd_active(const LloydArgs& a, int32_t v) {
 
 __global__ void lloyd_kernel(LloydArgs a) {
   cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31;
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int32_t n = a.g.n;
@@ -457,20 +459,35 @@ __global__ void lloyd_kernel(LloydArgs a) {
         const int32_t nf = __ldcg(&a.counters[cin]);
         if (nf == 0) break;
         if (tid == 0) a.counters[cclr] = 0;
-        for (int64_t i = tid; i < nf; i += nthreads) {
-          const int32_t u = front[i];
-          const int32_t lu = __ldcg(&a.label[u]);
-          for (int32_t j = a.g.off[u]; j < a.g.off[u + 1]; ++j) {
-            const int32_t w = a.g.nbr[j];
+        // edge parallel over (frontier vertex, ELL slot); warp-aggregated appends
+        const int64_t items = static_cast<int64_t>(nf) * 8;
+        for (int64_t base = tid - lane; base < items; base += nthreads) {
+          const int64_t it = base + lane;
+          int32_t u = -1, x = -1;
+          if (it < items) {
+            u = front[it >> 3];
+            x = a.ell[static_cast<int64_t>(u) * 8 + (it & 7)];
+          }
+          auto visit = [&](int32_t w, int32_t lu) -> bool {
             int32_t dw = __ldcg(&a.dist[w]);
+            bool fresh = false;
             if (dw == kUnreached) {
               dw = atomicCAS(&a.dist[w], kUnreached, d + 1);
-              if (dw == kUnreached) {
-                next[atomicAdd(&a.counters[cout], 1)] = w;
-                dw = d + 1;
-              }
+              if (dw == kUnreached) fresh = true, dw = d + 1;
             }
             if (dw == d + 1) atomicMin(&a.label[w], lu);
+            return fresh;
+          };
+          bool push = false;
+          if (x >= 0) push = visit(x, __ldcg(&a.label[u]));
+          const int32_t slot = warp_append(&a.counters[cout], push);
+          if (push) next[slot] = x;
+          if (x < -1) {  // degree > 8: CSR tail
+            const int32_t lu = __ldcg(&a.label[u]);
+            for (int32_t j = -x - 2; j < a.g.off[u + 1]; ++j) {
+              const int32_t w = a.g.nbr[j];
+              if (visit(w, lu)) next[atomicAdd(&a.counters[cout], 1)] = w;
+            }
           }
         }
         grid.sync();
@@ -522,14 +539,28 @@ __global__ void lloyd_kernel(LloydArgs a) {
         const int32_t nf = __ldcg(&a.counters[cin]);
         if (nf == 0) break;
         if (tid == 0) a.counters[cclr] = 0;
-        for (int64_t i = tid; i < nf; i += nthreads) {
-          const int32_t u = front[i];
-          const int32_t lu = __ldcg(&a.label[u]);
-          for (int32_t j = a.g.off[u]; j < a.g.off[u + 1]; ++j) {
-            const int32_t w = a.g.nbr[j];
-            if (__ldcg(&a.label[w]) != lu || __ldcg(&a.dist[w]) != kUnreached) continue;
-            if (atomicCAS(&a.dist[w], kUnreached, d + 1) == kUnreached)
-              next[atomicAdd(&a.counters[cout], 1)] = w;
+        const int64_t items = static_cast<int64_t>(nf) * 8;
+        for (int64_t base = tid - lane; base < items; base += nthreads) {
+          const int64_t it = base + lane;
+          int32_t u = -1, x = -1;
+          if (it < items) {
+            u = front[it >> 3];
+            x = a.ell[static_cast<int64_t>(u) * 8 + (it & 7)];
+          }
+          auto visit = [&](int32_t w, int32_t lu) -> bool {
+            if (__ldcg(&a.label[w]) != lu || __ldcg(&a.dist[w]) != kUnreached) return false;
+            return atomicCAS(&a.dist[w], kUnreached, d + 1) == kUnreached;
+          };
+          bool push = false;
+          if (x >= 0) push = visit(x, __ldcg(&a.label[u]));
+          const int32_t slot = warp_append(&a.counters[cout], push);
+          if (push) next[slot] = x;
+          if (x < -1) {
+            const int32_t lu = __ldcg(&a.label[u]);
+            for (int32_t j = -x - 2; j < a.g.off[u + 1]; ++j) {
+              const int32_t w = a.g.nbr[j];
+              if (visit(w, lu)) next[atomicAdd(&a.counters[cout], 1)] = w;
+            }
           }
         }
         grid.sync();
@@ -957,7 +988,8 @@ int32_t repair_sizes_dev(mp_context& ctx, const DGraph& g, int32_t* assignment, 
 
 }  // namespace
 
-void fps_batched_dev(mp_context& ctx, const DGraph& g, int32_t k, uint64_t seed, int32_t* seeds, int32_t* dist);
+void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32_t k, uint64_t seed, int32_t* seeds,
+                     int32_t* dist);
 
 int32_t enforce_connectivity_dev(mp_context& ctx, const DGraph& g, const int32_t* in,
                                  int32_t P, int32_t* out) {
@@ -1052,7 +1084,8 @@ int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, ui
   MP_KERNEL(ctx, assign_trivial<<<grid_for(ctx, n), 256, 0, s>>>(n, comp_list, comp_of, comp_start,
                                                                 comp_mode, comp_base, assignment));
   if (h_tot[1] > 0) {  // at least one FPS component
-    DevBuf<int32_t> dist(n, s), fr(2LL * n, s), seeds(P0, s);
+    DevBuf<int32_t> dist(n, s), fr(2LL * n, s), seeds(P0, s), ell(static_cast<int64_t>(n) * kEll, s);
+    MP_KERNEL(ctx, build_ell<<<grid_for(ctx, n), 256, 0, s>>>(g, ell));
     DevBuf<uint64_t> tkey(h_tot[1], s), skey(h_tot[2], s);
     DevBuf<uint32_t> tbits(h_tot[1] / 32 + 2LL * C + 2, s);
     MP_CUDA(cudaMemsetAsync(tbits, 0, sizeof(uint32_t) * tbits.n, s));
@@ -1066,10 +1099,8 @@ int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, ui
     fa.tile_bits = tbits, fa.frontier = fr, fa.seeds = seeds, fa.seed = seed, fa.work = ctx.dwork;
     if (C == 1 && n >= kBatchedFpsMin) {
       // one large component: exact speculative batches over the whole GPU
-      fps_batched_dev(ctx, g, P0, seed, seeds, dist);
+      fps_batched_dev(ctx, g, ell, P0, seed, seeds, dist);
     } else {
-      DevBuf<int32_t> ell(static_cast<int64_t>(n) * kEll, s);
-      MP_KERNEL(ctx, build_ell<<<grid_for(ctx, n), 256, 0, s>>>(g, ell));
       fa.ell = ell;
       const size_t fps_smem = sizeof(int32_t) * (2 * kFrontCap + kSmemTileWords);
       MP_CUDA(cudaFuncSetAttribute(fps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fps_smem)));
@@ -1106,6 +1137,7 @@ int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, ui
     la.fa = fr.get();
     la.fb = fr.get() + n;
     la.counters = counters;
+    la.ell = ell;
     la.work = ctx.dwork;
     int bpsm = 0;
     MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, lloyd_kernel, 256, 0));

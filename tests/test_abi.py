@@ -78,7 +78,7 @@ def test_mesh_to_graph_invariants_and_errors():
 
 
 def test_result_struct_layout():
-    # mp_result as declared: 8 pointers + scalars + float[6] + int64 + float[6] + int64[4]
-    assert C.sizeof(_lib.MpResult) >= 8 * 8 + 8 + 3 * 8 + 8 + 24 + 8 + 24 + 32
+    # mp_result as declared: 8 pointers + scalars + float[6] + int64 + float[6] + int64[16]
+    assert C.sizeof(_lib.MpResult) >= 8 * 8 + 8 + 3 * 8 + 8 + 24 + 8 + 24 + 128
     assert [f[0] for f in _lib.MpConfig._fields_] == ["patch_size", "nd_level", "seed", "local_mode", "schedule",
                                                       "block_size", "want_fill"]
