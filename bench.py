@@ -241,6 +241,9 @@ def run_ours(args):
             res = api.order_device(ctx, n, d_off.data_ptr(), d_nbr.data_ptr(), ptrs)
             ev1.record(stream)
             perm_ms.append(sum(res.stage_ms[i] for i in range(5)))
+            if os.environ.get("MP_BENCH_VERBOSE"):
+                print("step", [round(res.stage_ms[i], 2) for i in range(6)], [round(res.kernel_ms[i], 2) for i in range(6)],
+                      file=sys.stderr)
             fill_ms.append(res.stage_ms[5])
             kms += np.array([res.kernel_ms[i] for i in range(6)])
             launches += res.kernel_launches

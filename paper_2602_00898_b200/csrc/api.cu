@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -12,6 +15,23 @@
 #include "mp_device.cuh"
 
 namespace mp {
+
+static double now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+SectionTimer::SectionTimer(cudaStream_t st, const char* sc) : s(st), scope(sc) {
+  const char* e = getenv("MP_PROFILE");
+  on = e && e[0] == '1';
+  if (on) cudaStreamSynchronize(s);
+  t0 = now_ms();
+}
+void SectionTimer::mark(const char* what) {
+  if (!on) return;
+  cudaStreamSynchronize(s);
+  const double t = now_ms();
+  fprintf(stderr, "[mp] %s/%s %.3f ms\n", scope, what, t - t0);
+  t0 = t;
+}
 
 thread_local std::string g_last_error;
 

@@ -54,6 +54,7 @@ struct MdArgs {
   int32_t* order_ws;         // per vertex scratch: pivots in order (node_vertices layout)
   int32_t* local_perm;       // output, node_vertices layout
   int32_t* overflow;         // set on pool exhaustion
+  int32_t min_nv;            // md_kernel: only nodes with at least this many vertices
 };
 
 __device__ __forceinline__ uint32_t md_key_deg(int64_t d) {
@@ -63,7 +64,7 @@ __device__ __forceinline__ uint32_t md_key_deg(int64_t d) {
 __global__ void __launch_bounds__(kMdThreads) md_kernel(MdArgs a) {
   const int32_t node = blockIdx.x;
   const int32_t vb = a.node_offsets[node], nv = a.node_offsets[node + 1] - vb;
-  if (nv == 0) return;
+  if (nv == 0 || nv < a.min_nv) return;
   const int32_t* verts = a.node_vertices + vb;
   int32_t* lperm = a.local_perm + vb;
   int32_t* order = a.order_ws + vb;
@@ -249,6 +250,194 @@ __global__ void __launch_bounds__(kMdThreads) md_kernel(MdArgs a) {
   }
 }
 
+// Fast approximate-MD kernel (the default mode).  Node-local ids throughout:
+// variable and element lists hold local ids (an element is named by its
+// pivot's local id), and the per-vertex state lives in shared memory:
+//   st[v]   = |adj| | |elems| << 16    deg[v] = approx degree (INF once gone)
+//   mark[v] = token: a vertex mark while v is alive, the absorption mark of
+//             element v once v is eliminated (the two uses never overlap)
+//   bsz[e]  = boundary size of element e (0 = absorbed / empty)
+//   blk[b]  = min (degree, id) key of the 32 vertices of block b
+// Per pivot: argmin over blk (every warp, redundantly), reach collection,
+// member updates, dirty-block refresh: three barriers.
+constexpr int32_t kMdFastCap = 6 * 1024;  // nodes up to this size use the fast kernel
+
+__global__ void __launch_bounds__(kMdThreads) md_fast_kernel(MdArgs a) {
+  const int32_t node = a.nn - 1 - static_cast<int32_t>(blockIdx.x);  // leaves (the big nodes) first
+  const int32_t vb = a.node_offsets[node], nv = a.node_offsets[node + 1] - vb;
+  if (nv == 0 || nv > kMdFastCap) return;
+  const int32_t* verts = a.node_vertices + vb;
+  int32_t* lperm = a.local_perm + vb;
+  int32_t* order = a.order_ws + vb;
+  int32_t* bp = a.bptr + vb;  // element boundary offsets, local ids (node slab)
+  extern __shared__ uint64_t md_sm[];
+  const int32_t nb = (nv + 31) / 32;
+  uint64_t* blk = md_sm;
+  uint32_t* deg = reinterpret_cast<uint32_t*>(blk + nb);
+  int32_t* mark = reinterpret_cast<int32_t*>(deg + nv);
+  int32_t* bsz = mark + nv;
+  int32_t* st = bsz + nv;
+  uint32_t* dirty = reinterpret_cast<uint32_t*>(st + nv);  // nb bits
+  __shared__ int32_t s_nb, s_cursor, s_half, s_need, s_p, s_dcnt;
+  __shared__ int32_t s_dlist[kMdThreads];  // dirty blocks of this pivot (<= reach + 1 distinct)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int64_t pbase = a.pool_off[node];
+  const int64_t pcap = (a.pool_off[node + 1] - pbase) / 2;
+
+  // induced subgraph in local ids; list slots at the vertex's CSR range
+  for (int32_t k = threadIdx.x; k < nv; k += blockDim.x) {
+    const int32_t v = verts[k];
+    const int32_t o = a.g.off[v];
+    int32_t c = 0;
+    for (int32_t j = o; j < a.g.off[v + 1]; ++j) {
+      const int32_t w = a.g.nbr[j];
+      if (a.node_of[w] == node) a.adj[o + c++] = a.local_of[w];
+    }
+    if (c > 0x7fff) atomicExch(a.overflow, 2);  // packed list lengths: the general kernel redoes it
+    st[k] = c;
+    deg[k] = static_cast<uint32_t>(c);
+    mark[k] = 0;
+    bsz[k] = 0;
+  }
+  for (int32_t b = threadIdx.x; b < (nb + 31) / 32; b += blockDim.x) dirty[b] = 0;
+  if (threadIdx.x == 0) s_cursor = 0, s_half = 0, s_dcnt = 0;
+  __syncthreads();
+  for (int32_t b = wid; b < nb; b += nwarp) {
+    const int32_t i = b * 32 + lane;
+    const uint64_t m = warp_min_u64(i < nv ? key_min(deg[i], static_cast<uint32_t>(i)) : ~0ull);
+    if (lane == 0) blk[b] = m;
+  }
+  __syncthreads();
+
+  for (int32_t k = 0; k < nv; ++k) {
+    // ---- pivot: min (degree, local id), warp 0
+    if (wid == 0) {
+      uint64_t best = ~0ull;
+      for (int32_t b = lane; b < nb; b += 32) best = min(best, blk[b]);
+      best = warp_min_u64(best);
+      if (lane == 0) {
+        s_p = static_cast<int32_t>(best & 0xffffffffu);
+        s_need = (s_cursor + (nv - k)) > pcap;
+        s_nb = 0;
+      }
+    }
+    __syncthreads();  // B1
+    const int32_t p = s_p;
+    const int32_t tok = k + 1;
+    const int32_t gp = verts[p];
+    const int32_t po = a.g.off[gp];
+    const int32_t pst = st[p];
+    const int32_t np_adj = pst & 0xffff, np_el = pst >> 16;
+    if (s_need) {  // compact live boundaries into the other half
+      int32_t* src = a.pool + pbase + (s_half ? pcap : 0);
+      int32_t* dst = a.pool + pbase + (s_half ? 0 : pcap);
+      int32_t run = 0;
+      for (int32_t i0 = 0; i0 < k; i0 += blockDim.x) {
+        const int32_t i = i0 + threadIdx.x;
+        const int32_t e = i < k ? order[i] : -1;
+        const int32_t sz = e >= 0 ? bsz[e] : 0;
+        int32_t tot;
+        __shared__ int32_t shs[32];
+        const int32_t off = block_excl_scan(sz, shs, &tot);
+        if (sz > 0) {
+          const int32_t from = bp[e];
+          for (int32_t t = 0; t < sz; ++t) dst[run + off + t] = src[from + t];
+          bp[e] = run + off;
+        }
+        run += tot;
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) {
+        s_half ^= 1;
+        s_cursor = run;
+        if (run + (nv - k) > pcap) atomicExch(a.overflow, 1);
+      }
+      __syncthreads();
+    }
+    int32_t* half = a.pool + pbase + (s_half ? pcap : 0);
+    int32_t* out = half + s_cursor;
+    if (threadIdx.x == 0) mark[p] = tok;
+    __syncthreads();
+    // ---- reach set: variables of p plus boundaries of p's elements
+    const int32_t* padj = a.adj + po;
+    const int32_t* pel = a.el + po;
+    for (int32_t i = threadIdx.x; i < np_adj; i += blockDim.x) {
+      const int32_t w = padj[i];
+      if (atomicExch(&mark[w], tok) != tok) out[atomicAdd(&s_nb, 1)] = w;
+    }
+    for (int32_t ei = 0; ei < np_el; ++ei) {
+      const int32_t e = pel[ei];
+      const int32_t* bd = half + bp[e];
+      const int32_t sz = bsz[e];
+      for (int32_t i = threadIdx.x; i < sz; i += blockDim.x) {
+        const int32_t w = bd[i];
+        if (atomicExch(&mark[w], tok) != tok) out[atomicAdd(&s_nb, 1)] = w;
+      }
+    }
+    __syncthreads();  // B2
+    const int32_t nbd = s_nb;
+    // absorbed elements get the pivot's token (their own vertex marks are dead)
+    for (int32_t ei = threadIdx.x; ei < np_el; ei += blockDim.x) mark[pel[ei]] = tok;
+    if (threadIdx.x == 0) {
+      bp[p] = s_cursor;
+      order[k] = p;
+      lperm[k] = p;
+      deg[p] = 0xffffffffu;
+      if (!(atomicOr(&dirty[(p >> 5) >> 5], 1u << ((p >> 5) & 31)) & (1u << ((p >> 5) & 31))))
+        s_dlist[atomicAdd(&s_dcnt, 1)] = p >> 5;
+    }
+    __syncthreads();  // B2b: absorption marks visible
+    // ---- member updates (elimination.cpp:75-83) and their approx degrees
+    for (int32_t i = threadIdx.x; i < nbd; i += blockDim.x) {
+      const int32_t w = out[i];
+      const int32_t o = a.g.off[verts[w]];
+      const int32_t wst = st[w];
+      int32_t* wa = a.adj + o;
+      int32_t c = 0;
+      const int32_t na = wst & 0xffff, ne = wst >> 16;
+      for (int32_t j = 0; j < na; ++j) {
+        const int32_t x = wa[j];
+        if (mark[x] != tok) wa[c++] = x;
+      }
+      int32_t* we = a.el + o;
+      int32_t ce = 0;
+      int64_t d = c + nbd;
+      for (int32_t j = 0; j < ne; ++j) {
+        const int32_t e = we[j];
+        if (mark[e] != tok) {
+          we[ce++] = e;
+          d += bsz[e];
+        }
+      }
+      we[ce++] = p;
+      st[w] = c | (ce << 16);
+      deg[w] = md_key_deg(d);
+      const uint32_t bit = 1u << ((w >> 5) & 31);
+      if (!(atomicOr(&dirty[(w >> 5) >> 5], bit) & bit)) s_dlist[atomicAdd(&s_dcnt, 1)] = w >> 5;
+    }
+    __syncthreads();  // B3
+    for (int32_t ei = threadIdx.x; ei < np_el; ei += blockDim.x) bsz[pel[ei]] = 0;
+    if (threadIdx.x == 0) {
+      bsz[p] = nbd;
+      st[p] = 0;
+      s_cursor += nbd;
+    }
+    // ---- refresh dirty blocks
+    const int32_t ndirty = s_dcnt;
+    for (int32_t q = wid; q < ndirty; q += nwarp) {
+      const int32_t b = s_dlist[q];
+      const int32_t i = b * 32 + lane;
+      const uint64_t m = warp_min_u64(i < nv ? key_min(deg[i], static_cast<uint32_t>(i)) : ~0ull);
+      if (lane == 0) {
+        blk[b] = m;
+        dirty[b >> 5] = 0;  // every set bit of the word is in the list
+      }
+    }
+    __syncthreads();  // B4
+    if (threadIdx.x == 0) s_dcnt = 0;
+  }
+}
+
 __global__ void local_of_kernel(int32_t n, const int32_t* node_of, const int32_t* node_offsets,
                                 const int32_t* node_vertices, int32_t* local_of) {
   for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -310,7 +499,33 @@ void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t L, const int
   a.pool_off = pool_off, a.order_ws = order, a.local_perm = local_perm, a.overflow = overflow;
   const size_t smem = sizeof(uint32_t) * kSmemDegCap;
   MP_CUDA(cudaFuncSetAttribute(md_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  { const int kt__ = ctx.ktime_begin(kKMd); MP_KERNEL(ctx, md_kernel<<<nn, kMdThreads, smem, s>>>(a)); ctx.ktime_end(kt__); }
+  const int kt__ = ctx.ktime_begin(kKMd);
+  if (mode == 0) {
+    // largest node decides the shared-memory footprint of the fast kernel
+    std::vector<int32_t> hoff(nn + 1);
+    MP_CUDA(cudaMemcpyAsync(hoff.data(), node_offsets, sizeof(int32_t) * (nn + 1), cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+    int32_t maxnv = 0;
+    for (int32_t i = 0; i < nn; ++i) maxnv = std::max(maxnv, hoff[i + 1] - hoff[i]);
+    const int32_t fast_nv = std::min(maxnv, kMdFastCap);
+    const int32_t fnb = (fast_nv + 31) / 32;
+    const size_t fsmem = sizeof(uint64_t) * fnb + sizeof(int32_t) * 4 * fast_nv + sizeof(uint32_t) * ((fnb + 31) / 32 + 1);
+    MP_CUDA(cudaFuncSetAttribute(md_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fsmem)));
+    MP_KERNEL(ctx, md_fast_kernel<<<nn, kMdThreads, fsmem, s>>>(a));
+    int32_t h_flag = 0;
+    MP_CUDA(cudaMemcpyAsync(&h_flag, overflow.get(), 4, cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+    if (h_flag == 2) {  // a vertex of degree > 32767: the general kernel orders every node
+      MP_CUDA(cudaMemsetAsync(overflow, 0, 4, s));
+      MP_KERNEL(ctx, md_kernel<<<nn, kMdThreads, smem, s>>>(a));
+    } else if (maxnv > kMdFastCap) {
+      a.min_nv = kMdFastCap + 1;  // the general kernel takes the remaining (large) nodes
+      MP_KERNEL(ctx, md_kernel<<<nn, kMdThreads, smem, s>>>(a));
+    }
+  } else {
+    MP_KERNEL(ctx, md_kernel<<<nn, kMdThreads, smem, s>>>(a));
+  }
+  ctx.ktime_end(kt__);
   int32_t h_over = 0;
   MP_CUDA(cudaMemcpyAsync(&h_over, overflow, 4, cudaMemcpyDeviceToHost, s));
   MP_CUDA(cudaStreamSynchronize(s));

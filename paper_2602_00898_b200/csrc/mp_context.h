@@ -35,6 +35,17 @@ struct mp_context {
 
 namespace mp {
 
+// Debug section timer: with MP_PROFILE=1 in the environment, synchronises the
+// stream at every mark and prints host wall time between marks to stderr.
+struct SectionTimer {
+  cudaStream_t s;
+  const char* scope;
+  bool on;
+  double t0;
+  SectionTimer(cudaStream_t st, const char* sc);
+  void mark(const char* what);
+};
+
 struct DGraph {
   int32_t n;
   const int32_t* off;

@@ -78,6 +78,7 @@ struct LevelArgs {
   int32_t* fm_w;           // global fallback state for nodes beyond kFmSmemPatches
   uint64_t* fm_lk;
   uint64_t* fm_bm;
+  int32_t* fm_bw;
   int32_t* fm_ab;
   int32_t* fm_ae;
   uint8_t* fm_side;        // 2 * P bytes: side then lock flags
@@ -178,8 +179,8 @@ __global__ void quotient_csr(int32_t U, const uint64_t* ukeys, const int32_t* uc
 // unlocked patches -- the first feasible entry of the reference's
 // std::set<(-gain,id)> -- followed by a warp-0 update: two barriers per move.
 constexpr int32_t kFmSmemPatches = 10 * 1024;
-constexpr int kFmBytesPerPatch = 18;
-constexpr int kFmThreads = 256;  // power of two: patch i is owned by thread i & (kFmThreads-1)
+constexpr int kFmBytesPerPatch = 18 + 1;  // + block summaries (24 bytes per 32 patches)
+constexpr int kFmThreads = 256;
 
 __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
   const int32_t li = blockIdx.x;
@@ -190,8 +191,12 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
   int32_t* moves = a.fm_moves + pbeg;
   int64_t* rec = a.fm_rec + 3LL * pbeg;
 
-  extern __shared__ int32_t fm_sm[];
+  extern __shared__ uint64_t fm_sm64[];
   const bool in_smem = np <= kFmSmemPatches;
+  const int32_t nb_ = (np + 31) / 32;
+  uint64_t* bk = in_smem ? fm_sm64 : a.fm_bm + 2LL * ((pbeg >> 5) + li);         // block max keys, 2 sides
+  int32_t* bwt = in_smem ? reinterpret_cast<int32_t*>(fm_sm64 + 2 * nb_) : a.fm_bw + 2LL * ((pbeg >> 5) + li);
+  int32_t* fm_sm = reinterpret_cast<int32_t*>(fm_sm64 + 2 * nb_ + nb_);  // after 2*nb keys + 2*nb ints
   int32_t* w = in_smem ? fm_sm : a.fm_w + pbeg;
   int32_t* gain = in_smem ? fm_sm + np : a.fm_gain + pbeg;
   int32_t* ab = in_smem ? fm_sm + 2 * np : a.fm_ab + pbeg;
@@ -278,11 +283,14 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
   __syncthreads();
 
   // ---- FM passes with rollback to the best prefix (partition.cpp:95-159).
-  // Patch i is owned by thread i % blockDim: only the owner reads or writes its
-  // gain / lock / side during a pass.  Every thread keeps an identical
-  // register copy of the scalar state (side weights, cut, best prefix), the
-  // winner's side rides in the key's low bit, and the reduction slots are
-  // double buffered, so a move costs one barrier.
+  // The move loop runs in warp 0 alone.  Per side s, the unlocked patches of
+  // that side sit under 32-wide blocks holding their max key (gain desc, id
+  // asc) and min weight.  Feasibility of a side-s move is monotone in the
+  // weight (w <= W_s), so the answer is the best feasible side top; a side
+  // whose top is infeasible is searched only in blocks that can still hold a
+  // feasible patch (min weight <= a conservative bound on W_s) and beat the
+  // current best.  Every feasibility verdict is the exact double test.
+  const int32_t nblk = (np + 31) / 32;
   int64_t total_moves = 0;
   for (int pass = 0; pass < kFmPasses; ++pass) {
     for (int32_t i = threadIdx.x; i < np; i += blockDim.x) {
@@ -296,105 +304,165 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
       flag[i] = 0;  // unlocked
     }
     __syncthreads();
-    const int64_t pass_cut = s_cut;
-    int64_t sw0 = s_sw[0], sw1 = s_sw[1], cut = s_cut;
-    const double pass_imb = imbalance_of(sw0, sw1);
-    int64_t best_cut = pass_cut;
-    double best_imb = pass_imb, thr = kBalanceTol > pass_imb ? kBalanceTol : pass_imb;
-    int32_t nm = 0, best_len = 0;
-    // per-thread cache: the unconstrained best (gain desc, id asc) of the
-    // owned unlocked patches, recomputed only when one of them changed
-    auto own_key = [&](int32_t i) -> uint64_t {
-      return (static_cast<uint64_t>(static_cast<uint32_t>(gain[i] + kGainBias)) << 32) |
-             ((0x7fffffffu - static_cast<uint32_t>(i)) << 1) | side[i];
+    auto leaf_key = [&](int32_t i) -> uint64_t {
+      return flag[i] ? 0 : key_max(static_cast<uint32_t>(gain[i] + kGainBias), static_cast<uint32_t>(i));
     };
-    auto feasible = [&](int32_t i, uint32_t sd) {
-      const int64_t wi = w[i];
-      const int64_t ns = (sd ? sw1 : sw0) - wi, nt = (sd ? sw0 : sw1) + wi;
-      return ns > 0 && !(imbalance_of(ns, nt) > thr);  // never empty a side
+    // (re)build the per-side block summaries of block b (one warp)
+    auto block_sum = [&](int32_t b) {
+      const int32_t i = b * 32 + lane;
+      uint64_t k0 = 0, k1 = 0;
+      int32_t w0 = INT32_MAX, w1 = INT32_MAX;
+      if (i < np && !flag[i]) {
+        const uint64_t k = leaf_key(i);
+        if (side[i]) k1 = k, w1 = w[i];
+        else k0 = k, w0 = w[i];
+      }
+      k0 = warp_max_u64(k0), k1 = warp_max_u64(k1);
+      w0 = __reduce_min_sync(0xffffffffu, w0), w1 = __reduce_min_sync(0xffffffffu, w1);
+      if (lane == 0) bk[b] = k0, bk[nblk + b] = k1, bwt[b] = w0, bwt[nblk + b] = w1;
     };
-    auto recompute = [&]() -> uint64_t {
-      uint64_t m = 0;
-      for (int32_t i = threadIdx.x; i < np; i += kFmThreads)
-        if (!flag[i]) m = max(m, own_key(i));
-      return m;
-    };
-    uint64_t mine = recompute();
-    for (int32_t mv = 0;; ++mv) {
-      uint64_t best = 0;
-      if (mine) {
-        const int32_t ci = static_cast<int32_t>(0x7fffffffu - static_cast<uint32_t>((mine & 0xffffffffu) >> 1));
-        if (feasible(ci, static_cast<uint32_t>(mine & 1u))) {
-          best = mine;
-        } else {  // the owned maximum is infeasible: best feasible owned patch
-          for (int32_t i = threadIdx.x; i < np; i += kFmThreads) {
-            if (flag[i]) continue;
-            const uint64_t k = own_key(i);
-            if (k > best && feasible(i, side[i])) best = k;
+    for (int32_t b = wid; b < nblk; b += nw) block_sum(b);
+    __syncthreads();
+    if (wid == 0) {
+      const int64_t pass_cut = s_cut;
+      int64_t sw0 = s_sw[0], sw1 = s_sw[1], cut = s_cut;
+      const double pass_imb = imbalance_of(sw0, sw1);
+      int64_t best_cut = pass_cut;
+      double best_imb = pass_imb, thr = kBalanceTol > pass_imb ? kBalanceTol : pass_imb;
+      int32_t nm = 0, best_len = 0;
+      auto feasible = [&](int32_t i, int32_t sd) {
+        const int64_t wi = w[i];
+        const int64_t ns = (sd ? sw1 : sw0) - wi, nt = (sd ? sw0 : sw1) + wi;
+        return ns > 0 && !(imbalance_of(ns, nt) > thr);
+      };
+      for (;;) {
+        // side tops
+        uint64_t t0 = 0, t1 = 0;
+        for (int32_t b = lane; b < nblk; b += 32) t0 = max(t0, bk[b]), t1 = max(t1, bk[nblk + b]);
+        t0 = warp_max_u64(t0), t1 = warp_max_u64(t1);
+        if ((t0 | t1) == 0) break;
+        // exact verdicts on the two tops, in parallel lanes
+        bool ok = false;
+        if (lane < 2) {
+          const uint64_t t = lane ? t1 : t0;
+          ok = t != 0 && feasible(static_cast<int32_t>(key_max_id(t)), lane);
+        }
+        const uint32_t okm = __ballot_sync(0xffffffffu, ok);
+        uint64_t best = 0;
+        if (okm & 1u) best = t0;
+        if ((okm & 2u) && t1 > best) best = t1;
+        // sides whose top is infeasible: blocks that may hold a better feasible patch
+        for (int sd = 0; sd < 2; ++sd) {
+          const uint64_t top = sd ? t1 : t0;
+          if (((okm >> sd) & 1u) || top <= best) continue;
+          const int64_t S = sd ? sw1 : sw0, T = sd ? sw0 : sw1;
+          int64_t wmax = S - 1;  // conservative bound on the feasible weights
+          if (!isinf(thr)) {
+            const double e = (thr * static_cast<double>(S) - static_cast<double>(T)) / (1.0 + thr);
+            wmax = min(wmax, static_cast<int64_t>(floor(e)) + 2);
+          }
+          for (int32_t b0 = 0; b0 < nblk; b0 += 32) {
+            const int32_t b = b0 + lane;
+            const bool maybe = b < nblk && bk[sd * nblk + b] > best && bwt[sd * nblk + b] <= wmax;
+            uint32_t cand = __ballot_sync(0xffffffffu, maybe);
+            while (cand) {
+              const int32_t bb = b0 + __ffs(cand) - 1;
+              cand &= cand - 1;
+              if (bk[sd * nblk + bb] <= best) continue;
+              const int32_t i = bb * 32 + lane;
+              uint64_t k = 0;
+              if (i < np && !flag[i] && side[i] == sd && w[i] <= wmax) {
+                k = leaf_key(i);
+                if (k <= best || !feasible(i, sd)) k = 0;
+              }
+              best = max(best, warp_max_u64(k));
+            }
           }
         }
+        if (best == 0) break;
+        const int32_t ch = static_cast<int32_t>(key_max_id(best));
+        const int32_t gch = gain[ch];
+        const uint8_t sd = side[ch];
+        const int64_t wc = w[ch];
+        __syncwarp();
+        if (lane == 0) {
+          flag[ch] = 1;
+          moves[nm] = ch;
+          rec[3 * nm] = cut, rec[3 * nm + 1] = sw0, rec[3 * nm + 2] = sw1;
+          side[ch] = static_cast<uint8_t>(1 - sd);
+        }
+        ++nm;
+        if (sd) sw1 -= wc, sw0 += wc;
+        else sw0 -= wc, sw1 += wc;
+        cut -= gch;
+        __syncwarp();
+        // neighbours' gains (partition.cpp:137-142).  A raised key only needs a
+        // max into its block summary; a lowered key forces a rebuild only if it
+        // was the block's maximum; ch's own block is rebuilt (ch is now locked).
+        const uint8_t sc = static_cast<uint8_t>(1 - sd);
+        const int32_t e0 = ab[ch], e1 = ae[ch];
+        for (int32_t j0 = e0; j0 < e1; j0 += 32) {
+          const int32_t j = j0 + lane;
+          int32_t rb = -1;  // block to rebuild (side-qualified index)
+          if (j < e1) {
+            const int32_t nb = __ldg(&a.qloc[j]);
+            if (!flag[nb]) {
+              const int32_t wj = __ldg(&a.qw[j]);
+              const uint64_t oldk = leaf_key(nb);
+              const int32_t delta = side[nb] == sc ? -2 * wj : 2 * wj;
+              gain[nb] += delta;
+              const int32_t slot = side[nb] * nblk + (nb >> 5);
+              if (delta > 0) atomicMax(reinterpret_cast<unsigned long long*>(&bk[slot]),
+                                       static_cast<unsigned long long>(leaf_key(nb)));
+              else if (delta < 0 && bk[slot] == oldk) rb = nb >> 5;
+            }
+          }
+          __syncwarp();
+          const uint32_t same = __match_any_sync(0xffffffffu, rb);
+          uint32_t leaders = __ballot_sync(0xffffffffu, rb >= 0 && (__ffs(same) - 1) == lane);
+          while (leaders) {
+            const int32_t l = __ffs(leaders) - 1;
+            leaders &= leaders - 1;
+            block_sum(__shfl_sync(0xffffffffu, rb, l));
+          }
+        }
+        block_sum(ch >> 5);
+        const double imb = imbalance_of(sw0, sw1);
+        if (cut < best_cut || (cut == best_cut && imb < best_imb)) {
+          best_cut = cut;
+          best_imb = imb;
+          best_len = nm;
+        }
+        thr = kBalanceTol > imb ? kBalanceTol : imb;
+        __syncwarp();
       }
-      best = warp_max_u64(best);
-      uint64_t* slot = red2 + 32 * (mv & 1);
-      if (lane == 0) slot[wid] = best;
-      __syncthreads();
-      uint64_t k = lane < nw ? slot[lane] : 0;
-      k = warp_max_u64(k);
-      if (k == 0) break;
-      const int32_t ch = static_cast<int32_t>(0x7fffffffu - static_cast<uint32_t>((k & 0xffffffffu) >> 1));
-      const uint32_t sd = static_cast<uint32_t>(k & 1u);
-      const int32_t gch = static_cast<int32_t>(static_cast<uint32_t>(k >> 32)) - kGainBias;
-      const int64_t wc = w[ch];
-      if (threadIdx.x == 0) {
-        moves[nm] = ch;
-        rec[3 * nm] = cut, rec[3 * nm + 1] = sw0, rec[3 * nm + 2] = sw1;
-      }
-      bool dirty = false;
-      if ((ch & (kFmThreads - 1)) == static_cast<int32_t>(threadIdx.x)) {
-        flag[ch] = 1;
-        side[ch] = static_cast<uint8_t>(1 - sd);
-        dirty = true;
-      }
-      ++nm;
-      if (sd) sw1 -= wc, sw0 += wc;
-      else sw0 -= wc, sw1 += wc;
-      cut -= gch;
-      // neighbours' gains, each updated by its owner (partition.cpp:137-142)
-      const uint32_t sc = 1 - sd;
-      const int32_t e0 = ab[ch], e1 = ae[ch];
-      for (int32_t j = e0; j < e1; ++j) {
-        const int32_t nb = __ldg(&a.qloc[j]);
-        if ((nb & (kFmThreads - 1)) != static_cast<int32_t>(threadIdx.x) || flag[nb]) continue;
-        const int32_t wj = __ldg(&a.qw[j]);
-        gain[nb] += side[nb] == sc ? -2 * wj : 2 * wj;
-        dirty = true;
-      }
-      if (dirty) mine = recompute();
-      const double imb = imbalance_of(sw0, sw1);
-      if (cut < best_cut || (cut == best_cut && imb < best_imb)) {
-        best_cut = cut;
-        best_imb = imb;
-        best_len = nm;
-      }
-      thr = kBalanceTol > imb ? kBalanceTol : imb;
-    }
-    total_moves += nm;
-    __syncthreads();
-    for (int32_t m = best_len + threadIdx.x; m < nm; m += blockDim.x) side[moves[m]] ^= 1;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      if (nm > best_len) {
-        s_cut = rec[3 * best_len];
-        s_sw[0] = rec[3 * best_len + 1];
-        s_sw[1] = rec[3 * best_len + 2];
-      } else {
+      if (lane == 0) {
+        s_nm = nm;
+        s_best_len = best_len;
+        s_best_cut = best_cut;
+        s_best_imb = best_imb;
+        s_pass_cut = pass_cut;
+        s_pass_imb = pass_imb;
         s_cut = cut;
         s_sw[0] = sw0, s_sw[1] = sw1;
       }
     }
     __syncthreads();
-    const bool improved = best_cut < pass_cut || (best_cut == pass_cut && best_imb < pass_imb);
-    if (!improved) break;
+    const int32_t nm = s_nm, bl = s_best_len;
+    total_moves += nm;
+    for (int32_t m = bl + threadIdx.x; m < nm; m += blockDim.x) side[moves[m]] ^= 1;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (nm > bl) {
+        s_cut = rec[3 * bl];
+        s_sw[0] = rec[3 * bl + 1];
+        s_sw[1] = rec[3 * bl + 2];
+      }
+      const bool improved = s_best_cut < s_pass_cut || (s_best_cut == s_pass_cut && s_best_imb < s_pass_imb);
+      s_stop = improved ? 0 : 1;
+    }
+    __syncthreads();
+    if (s_stop) break;
   }
   for (int32_t i = threadIdx.x; i < np; i += blockDim.x) a.side[pl[i]] = side[i];
   if (threadIdx.x == 0) atomicAdd(&a.stats[0], static_cast<unsigned long long>(total_moves));
@@ -838,7 +906,8 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
   DevBuf<unsigned long long> stats(2, s);
   DevBuf<int64_t> fm_rec(3LL * Pm, s);
   DevBuf<int32_t> fm_w(Pm, s), fm_ab(Pm, s), fm_ae(Pm, s);
-  DevBuf<uint64_t> fm_lk(Pm, s), fm_bm(Pm / 32 + (1LL << std::min(L, 20)) + 64, s);
+  DevBuf<uint64_t> fm_lk(Pm, s), fm_bm(2 * (Pm / 32 + (1LL << std::min(L, 20)) + 64), s);
+  DevBuf<int32_t> fm_bw(2 * (Pm / 32 + (1LL << std::min(L, 20)) + 64), s);
   DevBuf<uint8_t> fm_side(2LL * Pm, s);
   DevBuf<int32_t> slot_of(std::max(n, 1), s), ref_pull(std::max(n, 1), s), ref_pulled(std::max(n, 1), s);
   DevBuf<uint8_t> ref_own(std::max(n, 1), s), ref_in(std::max(n, 1), s);
@@ -858,6 +927,8 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
   int32_t* cur_list = vl_a.get();
   int32_t* nxt_list = vl_b.get();
 
+  SectionTimer st(s, "etree");
+  st.mark("setup");
   for (int32_t level = 0; level < L && n > 0; ++level) {
     const int32_t first = (1 << level) - 1;
     int32_t na_level = 0;
@@ -874,7 +945,7 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     a.pw = pw, a.pnode = pnode, a.np_node = np_node, a.active = active, a.lidx = lidx;
     a.side = side, a.region = region, a.in_super = in_super, a.in_list = in_list, a.bcount = bcount;
     a.sep_list = seplist, a.next_vlist = nxt_list, a.next_start = next_start, a.next_cnt = next_cnt;
-    a.fm_w = fm_w, a.fm_ab = fm_ab, a.fm_ae = fm_ae, a.fm_side = fm_side, a.fm_lk = fm_lk, a.fm_bm = fm_bm;
+    a.fm_w = fm_w, a.fm_ab = fm_ab, a.fm_ae = fm_ae, a.fm_side = fm_side, a.fm_lk = fm_lk, a.fm_bm = fm_bm, a.fm_bw = fm_bw;
     a.slot_of = slot_of, a.ref_pull = ref_pull, a.ref_own = ref_own, a.ref_in = ref_in, a.ref_pulled = ref_pulled;
     a.stats = ctx.dwork ? ctx.dwork + 1 : stats.get(), a.fm_gain = fm_gain, a.fm_moves = fm_moves, a.fm_rec = fm_rec;
     const dim3 lgrid(std::max(1, grid_for(ctx, n) / std::max(1, width)), std::min(width, 65535));
@@ -917,6 +988,7 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
       MP_KERNEL(ctx, set_lidx<<<grid_for(ctx, na), 256, 0, s>>>(na, plist, pnode, poff, lidx));
     }
     a.plist = plist, a.poff = poff;
+    st.mark("level/patches");
     // quotient of the alive vertices, per node
     MP_CUDA(cudaMemsetAsync(cnt.get() + 3, 0, 4, s));
     MP_KERNEL(ctx, emit_crossing<<<lgrid, 256, 0, s>>>(a, keys, cnt.get() + 3));
@@ -940,6 +1012,7 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     }
     DevBuf<int32_t> fifo(U + na_level + 1, s);
     a.fm_fifo = fifo, a.fm_fifo_off = fifo_off;
+    st.mark("level/quotient");
     // bipartition per node
     const int32_t maxnp = na_level;
     DevBuf<int32_t> qloc(std::max<int64_t>(U, 1), s);
@@ -948,10 +1021,12 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     const size_t fm_smem = static_cast<size_t>(std::min(maxnp, kFmSmemPatches)) * kFmBytesPerPatch + 512;
     MP_CUDA(cudaFuncSetAttribute(fm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fm_smem)));
     { const int kt__ = ctx.ktime_begin(kKFm); MP_KERNEL(ctx, fm_kernel<<<width, kFmThreads, fm_smem, s>>>(a)); ctx.ktime_end(kt__); }
+    st.mark("level/fm");
     MP_KERNEL(ctx, super_pass<<<lgrid, 256, 0, s>>>(a));
     const size_t ref_smem = static_cast<size_t>(kRefSmemList) * 10;
     MP_CUDA(cudaFuncSetAttribute(refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ref_smem)));
     { const int kt__ = ctx.ktime_begin(kKRefine); MP_KERNEL(ctx, refine_kernel<<<width, kNodeThreads, ref_smem, s>>>(a)); ctx.ktime_end(kt__); }
+    st.mark("level/super+refine");
     // next level
     seg_start = std::move(next_start);
     seg_cnt = std::move(next_cnt);

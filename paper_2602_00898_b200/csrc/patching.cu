@@ -1033,6 +1033,7 @@ int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, ui
   cudaStream_t s = ctx.stream;
   const int32_t n = g.n;
   if (n == 0) return 0;
+  SectionTimer st(s, "patch");
 
   // connected components, ordered by smallest member (graph.cpp:183-205)
   DevBuf<int32_t> par(n, s), flag(n, s), rank(n, s);
@@ -1074,6 +1075,7 @@ int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, ui
                                             comp_list.get(), n, 0, end_bit, s));
     MP_KERNEL(ctx, scatter_pos<<<grid_for(ctx, n), 256, 0, s>>>(n, comp_list, pos_of));
   }
+  st.mark("components");
   MP_KERNEL(ctx, plan_components<<<1, 1024, 0, s>>>(C, comp_size, target, comp_start, comp_k, comp_mode,
                                                    comp_base, tile_base, super_base, totals));
   int32_t h_tot[3];
@@ -1097,6 +1099,7 @@ int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, ui
     fa.comp_mode = comp_mode, fa.comp_base = comp_base, fa.tile_base = tile_base;
     fa.super_base = super_base, fa.dist = dist, fa.tile_key = tkey, fa.super_key = skey;
     fa.tile_bits = tbits, fa.frontier = fr, fa.seeds = seeds, fa.seed = seed, fa.work = ctx.dwork;
+    st.mark("plan+ell");
     if (C == 1 && n >= kBatchedFpsMin) {
       // one large component: exact speculative batches over the whole GPU
       fps_batched_dev(ctx, g, ell, P0, seed, seeds, dist);
@@ -1107,6 +1110,7 @@ int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, ui
       { const int kt__ = ctx.ktime_begin(kKFps); MP_KERNEL(ctx, fps_kernel<<<C, kFpsThreads, fps_smem, s>>>(fa)); ctx.ktime_end(kt__); }
     }
 
+    st.mark("fps");
     // Lloyd rounds: one cooperative kernel
     DevBuf<int32_t> label(n, s), prev(n, s), active(C, s), changed(static_cast<int64_t>(kLloydRounds) * C, s),
         counters(4, s), patch_comp;
@@ -1146,10 +1150,14 @@ int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, ui
     { const int kt__ = ctx.ktime_begin(kKLloyd); MP_KERNEL(ctx, MP_CUDA(cudaLaunchCooperativeKernel((void*)lloyd_kernel, blocks, 256, args, 0, s))); ctx.ktime_end(kt__); }
     MP_KERNEL(ctx, lloyd_finish<<<grid_for(ctx, n), 256, 0, s>>>(n, comp_of.get(), comp_mode, prev, assignment));
   }
+  st.mark("lloyd");
   DevBuf<int32_t> conn(n, s);
   int32_t P1 = enforce_connectivity_dev(ctx, g, assignment, P0, conn);
   MP_CUDA(cudaMemcpyAsync(assignment, conn, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
-  return repair_sizes_dev(ctx, g, assignment, P1, target);
+  st.mark("connectivity");
+  const int32_t P2 = repair_sizes_dev(ctx, g, assignment, P1, target);
+  st.mark("repair");
+  return P2;
 }
 
 }  // namespace mp

@@ -1,2 +1,4 @@
-for rc in "300 1" "200 1" "120 1" "200 4"; do set -- $rc; MP_FPS_GRID_RADIUS=$1 MP_FPS_GRID_CANDS=$2 timeout 600 python bench.py --steps 2 --warmup 1 --no-cpu > gpurun_out/bench_c2_x.log 2>&1; python -c "
-import json; d=json.loads(open('gpurun_out/bench_c2_x.log').read().strip().splitlines()[-1]); w=d['work']; print('$rc', d['value'], d['kernel_ms']['fps'], d['parity']['match'], {k:w[k] for k in w if k.startswith('fps')})" || tail -3 gpurun_out/bench_c2_x.log; done
+for c in grid12x9 grid64 rand ico10 torus exact single grid300; do timeout 120 python tools/parity_check.py $c > gpurun_out/p_$c.log 2>&1; done
+grep -h "ALL PASS\|FAIL" gpurun_out/p_*.log | sort | uniq -c
+timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -2
+MP_BENCH_VERBOSE=1 timeout 600 python bench.py --steps 2 --warmup 1 --no-cpu 2>&1 | grep "^step"
