@@ -348,7 +348,8 @@ def run_ours(args):
                      "lloyd_levels": int(res.work[3]), "fps_batches": int(res.work[4]),
                      "fps_grid_levels": int(res.work[5]), "fps_candidates": int(res.work[6]),
                      "fps_region_levels_cta0": int(res.work[7]),
-                     "fps_phase_cycles": [int(res.work[i]) for i in range(8, 13)]},
+                     "fps_phase_cycles": [int(res.work[i]) for i in range(8, 13)],
+                     "fm_root_cycles": [int(res.work[i]) for i in range(13, 16)]},
             "e2e": {"value": round(e2e_v, 3), "unit": "ms", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "cpu_baseline": cpu,

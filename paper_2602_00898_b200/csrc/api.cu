@@ -167,6 +167,22 @@ int mp_context::ktime_begin(int slot) {
 }
 void mp_context::ktime_end(int first) { MP_CUDA(cudaEventRecord(kev[first + 1], stream)); }
 
+void* mp_context::slab(int id, size_t bytes) {
+  if (static_cast<int>(slabs.size()) <= id) slabs.resize(id + 1, {nullptr, 0});
+  auto& sl = slabs[id];
+  if (sl.second < bytes) {
+    if (sl.first) {
+      MP_CUDA(cudaStreamSynchronize(stream));
+      MP_CUDA(cudaFree(sl.first));
+      sl = {nullptr, 0};
+    }
+    const size_t grow = bytes + bytes / 8;
+    MP_CUDA(cudaMalloc(&sl.first, grow));
+    sl.second = grow;
+  }
+  return sl.first;
+}
+
 using namespace mp;
 
 extern "C" {
@@ -206,6 +222,8 @@ void mp_context_destroy(mp_context* ctx) {
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->kev) cudaEventDestroy(e);
+  for (auto& sl : ctx->slabs)
+    if (sl.first) cudaFree(sl.first);
   if (ctx->dwork) cudaFree(ctx->dwork);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;

@@ -514,20 +514,28 @@ void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32
   MP_CUDA(cudaFuncSetAttribute(fps_batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, fps_batched_kernel, kThreads, smem));
   if (bpsm < 1) throw Error(MP_ECUDA, "fps_batched_kernel does not fit on an SM");
-  // workers: one per SM, bounded by the bit-matrix width and by memory (12 bytes/vertex each)
-  int W = std::min(ctx.num_sms, kMaxWorkers);
-  size_t free_b = 0, total_b = 0;
-  MP_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  while (W > 1 && 12ull * n * W > free_b / 2) W /= 2;
-  DevBuf<int32_t> vis(static_cast<int64_t>(W) * n, s), dw(static_cast<int64_t>(W) * n, s),
-      reg(static_cast<int64_t>(W) * n, s), tlist(ntile, s), cand(kSCap, s), regn(kMaxWorkers, s), ctl(8, s);
+  // workers: one per SM, bounded by the bit-matrix width and by memory
+  // (12 bytes/vertex each); decided once per context
+  if (ctx.fps_workers == 0) {
+    int W0 = std::min(ctx.num_sms, kMaxWorkers);
+    size_t free_b = 0, total_b = 0;
+    MP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    while (W0 > 1 && 20ull * n * W0 > free_b / 2) W0 /= 2;
+    ctx.fps_workers = W0;
+  }
+  const int W = ctx.fps_workers;
+  const int64_t wn = static_cast<int64_t>(W) * n;
+  int32_t* vis = static_cast<int32_t*>(ctx.slab(0, sizeof(int32_t) * wn));
+  int32_t* dw = static_cast<int32_t*>(ctx.slab(1, sizeof(int32_t) * wn));
+  int32_t* reg = static_cast<int32_t*>(ctx.slab(2, sizeof(int32_t) * wn));
+  uint64_t* glist = static_cast<uint64_t*>(ctx.slab(3, sizeof(uint64_t) * (static_cast<int64_t>(std::min(W, kGridCands)) * n + 64)));
+  DevBuf<int32_t> tlist(ntile, s), cand(kSCap, s), regn(kMaxWorkers, s), ctl(16, s);
   DevBuf<uint64_t> tkey(ntile, s), ckey(kSCap, s), mkey(kMaxWorkers, s);
   DevBuf<uint32_t> tbits(ntile / 32 + 1, s), inm(kMaxWorkers * kMaskWords, s);
   DevBuf<int32_t> tscratch(ntile, s), bar(1, s);
   MP_CUDA(cudaMemsetAsync(bar, 0, sizeof(int32_t), s));
-  DevBuf<uint64_t> glist(static_cast<int64_t>(std::min(W, kGridCands)) * n + 64, s);
   MP_CUDA(cudaMemsetAsync(inm, 0, sizeof(uint32_t) * inm.n, s));
-  MP_CUDA(cudaMemsetAsync(vis, 0, sizeof(int32_t) * vis.n, s));
+  MP_CUDA(cudaMemsetAsync(vis, 0, sizeof(int32_t) * wn, s));
   MP_CUDA(cudaMemsetAsync(tbits, 0, sizeof(uint32_t) * tbits.n, s));
   BatchArgs a{};
   a.g = g, a.ell = ell, a.n = n, a.k = k, a.tile_shift = tile_shift, a.ntile = ntile, a.seed = seed;

@@ -31,6 +31,11 @@ struct mp_context {
   int64_t work[16] = {};
   int ktime_begin(int slot);
   void ktime_end(int first);
+  // Persistent device slabs (cudaMalloc, grown on demand, kept across calls)
+  // for the large per-call scratch, so repeated calls do no pool traffic.
+  std::vector<std::pair<void*, size_t>> slabs;
+  void* slab(int id, size_t bytes);
+  int fps_workers = 0;  // worker CTAs of the batched FPS (decided once)
 };
 
 namespace mp {

@@ -40,21 +40,19 @@ __device__ __forceinline__ uint32_t key_max_id(uint64_t k) {
   return 0xffffffffu - static_cast<uint32_t>(k & 0xffffffffu);
 }
 
+// 64-bit warp max/min as two 32-bit redux.sync steps (high word, then the
+// low word among the lanes holding the winning high word); full warp only.
 __device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    uint64_t x = __shfl_xor_sync(0xffffffffu, v, o);
-    v = x > v ? x : v;
-  }
-  return v;
+  const uint32_t hi = static_cast<uint32_t>(v >> 32), lo = static_cast<uint32_t>(v);
+  const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
+  const uint32_t ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+  return (static_cast<uint64_t>(mh) << 32) | ml;
 }
 __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    uint64_t x = __shfl_xor_sync(0xffffffffu, v, o);
-    v = x < v ? x : v;
-  }
-  return v;
+  const uint32_t hi = static_cast<uint32_t>(v >> 32), lo = static_cast<uint32_t>(v);
+  const uint32_t mh = __reduce_min_sync(0xffffffffu, hi);
+  const uint32_t ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
+  return (static_cast<uint64_t>(mh) << 32) | ml;
 }
 __device__ __forceinline__ int64_t warp_sum_i64(int64_t v) {
 #pragma unroll

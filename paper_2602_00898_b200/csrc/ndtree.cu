@@ -90,6 +90,9 @@ struct LevelArgs {
   uint8_t* ref_own;
   uint8_t* ref_in;
   int32_t* ref_pulled;
+  uint8_t* vside;          // per vertex: side of its patch (this level)
+  const int32_t* ell;      // n * 8 ELL adjacency
+  int64_t fm_smem_bytes;   // dynamic shared memory of the FM launch
   int32_t* fm_moves;
   int64_t* fm_rec;         // 3 per move: cut, sw0, sw1
 };
@@ -121,6 +124,15 @@ __global__ void flag_alive_patches(int32_t P, const int32_t* pw, const int32_t* 
     bool ok = pw[p] > 0 && active[pnode[p]];
     flag[p] = ok ? 1 : 0;
     key[p] = ok ? pnode[p] : 0;
+  }
+}
+__global__ void build_ell_nd(DGraph g, int32_t* ell) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < g.n; v += gridDim.x * blockDim.x) {
+    const int32_t o = g.off[v], deg = g.off[v + 1] - o;
+    int32_t* e = ell + static_cast<int64_t>(v) * 8;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) e[k] = k < deg ? g.nbr[o + k] : -1;
+    if (deg > 8) e[7] = -(o + 7) - 2;
   }
 }
 __global__ void masked_counts(int32_t width, const int32_t* active, const int32_t* np_node, int32_t* out) {
@@ -211,6 +223,7 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
 
   int64_t tot = 0;
+  int32_t heavy = 0;
   for (int32_t i = threadIdx.x; i < np; i += blockDim.x) {
     const int32_t p = pl[i];
     w[i] = a.pw[p];
@@ -221,6 +234,41 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
     tot += w[i];
   }
   tot = block_sum_i64(tot, reinterpret_cast<int64_t*>(red));
+  // node-local adjacency packed (local id << 16 | weight) in shared memory when
+  // it fits; otherwise the global arrays (qloc, qw) are read directly
+  uint32_t* packed = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(side + 2 * np) + 15) & ~uintptr_t(15));
+  const int64_t e_node = (a.fm_fifo_off[li + 1] - a.fm_fifo_off[li]) - np;
+  const bool adj_smem = in_smem && np < 65536 &&
+                        static_cast<int64_t>(reinterpret_cast<uint8_t*>(packed + e_node) - reinterpret_cast<uint8_t*>(fm_sm64)) +
+                        16 <= a.fm_smem_bytes;
+  if (adj_smem) {
+    int32_t run = 0;
+    for (int32_t i0 = 0; i0 < np; i0 += blockDim.x) {
+      const int32_t i = i0 + threadIdx.x;
+      const int32_t d = i < np ? ae[i] - ab[i] : 0;
+      int32_t tt;
+      const int32_t off = block_excl_scan(d, reinterpret_cast<int32_t*>(red), &tt);
+      if (i < np) {
+        const int32_t g0 = ab[i];
+        for (int32_t q = 0; q < d; ++q) {
+          const int32_t wq = __ldg(&a.qw[g0 + q]);
+          heavy |= wq > 0xffff;
+          packed[run + off + q] = (static_cast<uint32_t>(__ldg(&a.qloc[g0 + q])) << 16) | (wq & 0xffff);
+        }
+        ab[i] = run + off;
+        ae[i] = run + off + d;
+      }
+      run += tt;
+    }
+  }
+  heavy = __syncthreads_or(heavy);
+  if (heavy) {  // a weight does not fit 16 bits: undo (global offsets again)
+    for (int32_t i = threadIdx.x; i < np; i += blockDim.x) ab[i] = a.qoff[pl[i]], ae[i] = a.qoff[pl[i] + 1];
+    __syncthreads();
+  }
+  const bool adj_local = adj_smem && !heavy;
+  auto A_nb = [&](int32_t j) -> int32_t { return adj_local ? static_cast<int32_t>(packed[j] >> 16) : __ldg(&a.qloc[j]); };
+  auto A_w = [&](int32_t j) -> int32_t { return adj_local ? static_cast<int32_t>(packed[j] & 0xffffu) : __ldg(&a.qw[j]); };
   if (threadIdx.x == 0) s_total = tot, s_left = 0, s_head = 0, s_tail = 0;
   __syncthreads();
 
@@ -257,7 +305,7 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
       int32_t tail = s_tail;
       for (int32_t j0 = e0; j0 < e1; j0 += 32) {
         const int32_t j = j0 + lane;
-        const int32_t nb = j < e1 ? __ldg(&a.qloc[j]) : 0;
+        const int32_t nb = j < e1 ? A_nb(j) : 0;
         const bool push = j < e1 && !flag[nb];
         const uint32_t m = __ballot_sync(0xffffffffu, push);
         if (push) fifo[tail + __popc(m & ((1u << lane) - 1))] = nb;
@@ -271,8 +319,8 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
   int64_t cut = 0;
   for (int32_t i = threadIdx.x; i < np; i += blockDim.x)
     for (int32_t j = ab[i]; j < ae[i]; ++j) {
-      const int32_t nb = __ldg(&a.qloc[j]);
-      if (nb > i && side[i] != side[nb]) cut += __ldg(&a.qw[j]);  // local order == patch id order
+      const int32_t nb = A_nb(j);
+      if (nb > i && side[i] != side[nb]) cut += A_w(j);  // local order == patch id order
     }
   cut = block_sum_i64(cut, reinterpret_cast<int64_t*>(red));
   if (threadIdx.x == 0) {
@@ -297,8 +345,8 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
       int32_t val = 0;
       const uint8_t si = side[i];
       for (int32_t j = ab[i]; j < ae[i]; ++j) {
-        const int32_t wj = __ldg(&a.qw[j]);
-        val += side[__ldg(&a.qloc[j])] != si ? wj : -wj;
+        const int32_t wj = A_w(j);
+        val += side[A_nb(j)] != si ? wj : -wj;
       }
       gain[i] = val;
       flag[i] = 0;  // unlocked
@@ -330,40 +378,68 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
       int64_t best_cut = pass_cut;
       double best_imb = pass_imb, thr = kBalanceTol > pass_imb ? kBalanceTol : pass_imb;
       int32_t nm = 0, best_len = 0;
-      auto feasible = [&](int32_t i, int32_t sd) {
-        const int64_t wi = w[i];
+      // exact feasibility predicate of moving weight wi off side sd
+      auto pred = [&](int64_t wi, int32_t sd) {
         const int64_t ns = (sd ? sw1 : sw0) - wi, nt = (sd ? sw0 : sw1) + wi;
         return ns > 0 && !(imbalance_of(ns, nt) > thr);
       };
+      long long c_w = 0, c_s = 0, c_u = 0;
       for (;;) {
+        long long c0 = clock64();
+        // Feasible weights of a side form [0, W_s]: the ratio falls until the
+        // sides cross and rises after, and the rounded division is monotone.
+        // W_s from the real-valued estimate, fixed up with exact predicates
+        // evaluated in parallel lanes (lanes 0-1 side 0, lanes 2-3 side 1).
+        int64_t Wsd[2];
+        {
+          // lanes 0-15 probe side 0 at est-7 .. est+8, lanes 16-31 side 1
+          const int32_t sd = lane >> 4;
+          const int64_t S = sd ? sw1 : sw0, T = sd ? sw0 : sw1;
+          int64_t est = S - 1;
+          if (!isinf(thr)) {  // estimate only (exact predicates decide): float math
+            const float tf = static_cast<float>(thr);
+            const float e = __fdividef(tf * static_cast<float>(S) - static_cast<float>(T), 1.0f + tf);
+            const int64_t fe = static_cast<int64_t>(floorf(e));
+            est = fe < est ? fe : est;
+          }
+          const int64_t probe = est - 7 + (lane & 15);
+          const bool pv = probe >= 0 && pred(probe, sd);
+          const uint32_t pm = __ballot_sync(0xffffffffu, pv);
+          for (int q = 0; q < 2; ++q) {
+            const uint32_t m = (pm >> (16 * q)) & 0xffffu;
+            const int64_t e2 = __shfl_sync(0xffffffffu, est, 16 * q);
+            int64_t W;
+            if (m == 0xffffu) {  // window all feasible: walk up (rare)
+              W = e2 + 8;
+              while (pred(W + 1, q)) ++W;
+            } else if (m == 0 && e2 - 7 > 0) {  // window all infeasible: walk down (rare)
+              W = e2 - 8;
+              while (W >= 0 && !pred(W, q)) --W;
+            } else {  // feasible probes form a prefix of the window
+              W = e2 - 7 + (32 - __clz(static_cast<int>(m))) - 1;
+            }
+            Wsd[q] = W;
+          }
+        }
         // side tops
         uint64_t t0 = 0, t1 = 0;
         for (int32_t b = lane; b < nblk; b += 32) t0 = max(t0, bk[b]), t1 = max(t1, bk[nblk + b]);
         t0 = warp_max_u64(t0), t1 = warp_max_u64(t1);
         if ((t0 | t1) == 0) break;
-        // exact verdicts on the two tops, in parallel lanes
-        bool ok = false;
-        if (lane < 2) {
-          const uint64_t t = lane ? t1 : t0;
-          ok = t != 0 && feasible(static_cast<int32_t>(key_max_id(t)), lane);
-        }
-        const uint32_t okm = __ballot_sync(0xffffffffu, ok);
         uint64_t best = 0;
-        if (okm & 1u) best = t0;
-        if ((okm & 2u) && t1 > best) best = t1;
-        // sides whose top is infeasible: blocks that may hold a better feasible patch
+        bool ok0 = t0 && w[key_max_id(t0)] <= Wsd[0], ok1 = t1 && w[key_max_id(t1)] <= Wsd[1];
+        if (ok0) best = t0;
+        if (ok1 && t1 > best) best = t1;
+        long long c1 = clock64();
+        c_w += c1 - c0;
+        // a side whose top is too heavy: the best block-wise patch with w <= W_s
         for (int sd = 0; sd < 2; ++sd) {
           const uint64_t top = sd ? t1 : t0;
-          if (((okm >> sd) & 1u) || top <= best) continue;
-          const int64_t S = sd ? sw1 : sw0, T = sd ? sw0 : sw1;
-          int64_t wmax = S - 1;  // conservative bound on the feasible weights
-          if (!isinf(thr)) {
-            const double e = (thr * static_cast<double>(S) - static_cast<double>(T)) / (1.0 + thr);
-            wmax = min(wmax, static_cast<int64_t>(floor(e)) + 2);
-          }
+          if ((sd ? ok1 : ok0) || top <= best) continue;
+          const int64_t W = Wsd[sd];
           for (int32_t b0 = 0; b0 < nblk; b0 += 32) {
             const int32_t b = b0 + lane;
-            const bool maybe = b < nblk && bk[sd * nblk + b] > best && bwt[sd * nblk + b] <= wmax;
+            const bool maybe = b < nblk && bk[sd * nblk + b] > best && bwt[sd * nblk + b] <= W;
             uint32_t cand = __ballot_sync(0xffffffffu, maybe);
             while (cand) {
               const int32_t bb = b0 + __ffs(cand) - 1;
@@ -371,14 +447,13 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
               if (bk[sd * nblk + bb] <= best) continue;
               const int32_t i = bb * 32 + lane;
               uint64_t k = 0;
-              if (i < np && !flag[i] && side[i] == sd && w[i] <= wmax) {
-                k = leaf_key(i);
-                if (k <= best || !feasible(i, sd)) k = 0;
-              }
+              if (i < np && !flag[i] && side[i] == sd && w[i] <= W) k = leaf_key(i);
               best = max(best, warp_max_u64(k));
             }
           }
         }
+        long long c2 = clock64();
+        c_s += c2 - c1;
         if (best == 0) break;
         const int32_t ch = static_cast<int32_t>(key_max_id(best));
         const int32_t gch = gain[ch];
@@ -405,9 +480,9 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
           const int32_t j = j0 + lane;
           int32_t rb = -1;  // block to rebuild (side-qualified index)
           if (j < e1) {
-            const int32_t nb = __ldg(&a.qloc[j]);
+            const int32_t nb = A_nb(j);
             if (!flag[nb]) {
-              const int32_t wj = __ldg(&a.qw[j]);
+              const int32_t wj = A_w(j);
               const uint64_t oldk = leaf_key(nb);
               const int32_t delta = side[nb] == sc ? -2 * wj : 2 * wj;
               gain[nb] += delta;
@@ -435,6 +510,12 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
         }
         thr = kBalanceTol > imb ? kBalanceTol : imb;
         __syncwarp();
+        c_u += clock64() - c2;
+      }
+      if (lane == 0 && li == 0 && a.first == 0) {
+        atomicAdd(&a.stats[12], static_cast<unsigned long long>(c_w));
+        atomicAdd(&a.stats[13], static_cast<unsigned long long>(c_s));
+        atomicAdd(&a.stats[14], static_cast<unsigned long long>(c_u));
       }
       if (lane == 0) {
         s_nm = nm;
@@ -488,6 +569,7 @@ __global__ void super_pass(LevelArgs a) {
         if (a.node_of[v] == node && a.side[a.assign[v]] != su) sup = 1;
       }
       a.region[u] = static_cast<int8_t>(su);
+      a.vside[u] = su;
       a.in_super[u] = sup;
       if (sup) (su == 0 ? nl : nr)++;
     }
@@ -503,37 +585,44 @@ struct RefKey {
 __device__ __forceinline__ bool ref_less(const RefKey& x, const RefKey& y) {
   return x.hi < y.hi || (x.hi == y.hi && x.lo < y.lo);
 }
-__device__ __forceinline__ RefKey warp_min_ref(RefKey k) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    RefKey t;
-    t.hi = __shfl_xor_sync(0xffffffffu, k.hi, o);
-    t.lo = __shfl_xor_sync(0xffffffffu, k.lo, o);
-    if (ref_less(t, k)) k = t;
-  }
-  return k;
-}
-
 // refine_separator (partition.cpp:187-283).  The candidate list (every
 // vertex that has been in the separator) lives in shared memory with, per
 // entry, the vertex, its patch side, an in-separator flag and its pull count
 // (neighbours in the opposite region), maintained incrementally: a move only
 // changes the regions of the moved vertex and the vertices it pulls, so only
-// their neighbours' counts change.  A move is then a block argmin of
-// (new size, new imbalance, vertex) over in-separator entries.
+// their neighbours' counts change.  A candidate's new imbalance depends only on
+// (side, pull), so the divisions are a per-move table (warp 0), and a move is
+// a block argmin of (new size, new imbalance, vertex) over the entries.
+// Per-vertex state is one byte of region (0/1 sides, 2 separator, 3 gone --
+// dead vertices never count as neighbours) plus the vertex's patch side, so
+// no node-membership lookups are needed; adjacency comes from the ELL copy.
 constexpr int32_t kRefSmemList = 6 * 1024;
+constexpr int kRefTab = 16;  // pulls tabulated per side
+
+__device__ __forceinline__ RefKey warp_min_ref(RefKey k) {
+  // lexicographic (hi, lo) minimum in four 32-bit redux steps
+  const uint32_t h1 = static_cast<uint32_t>(k.hi >> 32), h0 = static_cast<uint32_t>(k.hi);
+  const uint32_t l1 = static_cast<uint32_t>(k.lo >> 32), l0 = static_cast<uint32_t>(k.lo);
+  const uint32_t m1 = __reduce_min_sync(0xffffffffu, h1);
+  const uint32_t m0 = __reduce_min_sync(0xffffffffu, h1 == m1 ? h0 : 0xffffffffu);
+  const bool e1 = h1 == m1 && h0 == m0;
+  const uint32_t n1 = __reduce_min_sync(0xffffffffu, e1 ? l1 : 0xffffffffu);
+  const uint32_t n0 = __reduce_min_sync(0xffffffffu, e1 && l1 == n1 ? l0 : 0xffffffffu);
+  return RefKey{(static_cast<uint64_t>(m1) << 32) | m0, (static_cast<uint64_t>(n1) << 32) | n0};
+}
 
 __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
   const int32_t li = blockIdx.x;
-  const int32_t s0 = a.seg_start[li], cnt = a.seg_cnt[li], node = a.first + li;
+  const int32_t s0 = a.seg_start[li], cnt = a.seg_cnt[li];
   __shared__ int32_t shi[32];
   __shared__ RefKey sred[32];
   __shared__ int64_t s_rw[2], s_size;
-  __shared__ double s_imb;
-  __shared__ int32_t s_list, s_mv, s_moves, s_np;
+  __shared__ double s_imb, s_ni[2][kRefTab];
+  __shared__ int32_t s_list, s_mv, s_moves;
   extern __shared__ int32_t ref_sm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int32_t lc = 2 * li, rc = 2 * li + 1;  // children, local to the next level
+  const int32_t node = a.first + li;
   if (!a.active[li]) {
     if (threadIdx.x == 0) {
       a.next_start[lc] = s0, a.next_cnt[lc] = 0;
@@ -547,8 +636,19 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
   int32_t* lpull = in_smem ? ref_sm + kRefSmemList : a.ref_pull + s0;
   uint8_t* lown = in_smem ? reinterpret_cast<uint8_t*>(ref_sm + 2 * kRefSmemList) : a.ref_own + s0;
   uint8_t* lin = in_smem ? lown + kRefSmemList : a.ref_in + s0;
-  auto inside = [&](int32_t w) { return a.node_of[w] == node; };
-  int32_t* s_pulled = a.ref_pulled + s0;  // vertices pulled by the current move
+  int8_t* region = a.region;
+  const int32_t* ell = a.ell;
+
+  // neighbour w of v through the ELL copy, slot k of a warp-uniform walk;
+  // returns -1 past the end (the CSR tail serves vertices of degree > 8)
+  auto nbr_at = [&](int32_t v, int32_t k) -> int32_t {
+    if (k < 7) return ell[static_cast<int64_t>(v) * 8 + k];
+    const int32_t x7 = ell[static_cast<int64_t>(v) * 8 + 7];
+    if (x7 >= -1) return k == 7 ? x7 : -1;
+    const int32_t j = -x7 - 2 + (k - 7);
+    return j < a.g.off[v + 1] ? a.g.nbr[j] : -1;
+  };
+  auto degree = [&](int32_t v) { return a.g.off[v + 1] - a.g.off[v]; };
 
   // initial separator: the smaller boundary, ties to the left (partition.cpp:212-222)
   const int8_t take = a.bcount[2 * li] <= a.bcount[2 * li + 1] ? 0 : 1;
@@ -559,7 +659,7 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
       int32_t v = -1, in = 0;
       if (i < cnt) {
         v = seg[i];
-        in = a.in_super[v] && a.region[v] == take;
+        in = a.in_super[v] && region[v] == take;
       }
       int32_t tot;
       const int32_t e = block_excl_scan(in, shi, &tot);
@@ -569,9 +669,9 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
         lown[k] = static_cast<uint8_t>(take);
         lin[k] = 1;
         a.slot_of[v] = k;
-        a.region[v] = 2;
+        region[v] = 2;
       } else if (i < cnt) {
-        (a.region[v] == 0 ? c0 : c1)++;
+        (region[v] == 0 ? c0 : c1)++;
       }
       run += tot;
     }
@@ -584,15 +684,17 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
       s_imb = imbalance_of(r0, r1);
       s_moves = 0;
     }
+    if (wid == 0) {  // imbalance table for the first move
+      const int32_t own = lane >> 4, pull = lane & 15;
+      const int64_t ro = own ? r1 : r0, rp = own ? r0 : r1;
+      s_ni[own][pull] = imbalance_of(ro + 1, rp - pull);
+    }
     __syncthreads();
     for (int32_t k = threadIdx.x; k < run; k += blockDim.x) {
       const int32_t v = lv[k];
       const int8_t opp = 1 - static_cast<int8_t>(lown[k]);
       int32_t pull = 0;
-      for (int32_t j = a.g.off[v]; j < a.g.off[v + 1]; ++j) {
-        const int32_t w = a.g.nbr[j];
-        pull += inside(w) && a.region[w] == opp;
-      }
+      for (int32_t j = a.g.off[v]; j < a.g.off[v + 1]; ++j) pull += region[a.g.nbr[j]] == opp;
       lpull[k] = pull;
     }
     __syncthreads();
@@ -606,12 +708,13 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
     const int32_t nl = s_list;
     RefKey best{~0ull, ~0ull};
     for (int32_t i = threadIdx.x; i < nl; i += blockDim.x) {
-      if (!lin[i]) continue;
+      if (lin[i] != 1) continue;
       const int32_t pull = lpull[i];
       const int64_t ns = cur - 1 + pull;
       if (ns > cur) continue;
       const uint8_t own = lown[i];
-      const double ni = imbalance_of((own ? rw1 : rw0) + 1, (own ? rw0 : rw1) - pull);
+      const double ni = pull < kRefTab ? s_ni[own][pull]
+                                       : imbalance_of((own ? rw1 : rw0) + 1, (own ? rw0 : rw1) - pull);
       if (ni > thr) continue;
       if (!(ns < cur || ni < cimb)) continue;
       const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(ni));
@@ -630,79 +733,81 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
       if (mv >= 0) {
         const int32_t im = a.slot_of[mv];
         const int8_t own = static_cast<int8_t>(lown[im]), opp = 1 - own;
-        const int32_t mb = a.g.off[mv], me = a.g.off[mv + 1];
         // 1. pull mv's opposite-region neighbours into the separator
+        const int32_t dmv = degree(mv);
         int32_t tail = s_list, np = 0;
-        for (int32_t j0 = mb; j0 < me; j0 += 32) {
-          const int32_t j = j0 + lane;
-          int32_t w = -1;
-          bool pull = false;
-          if (j < me) {
-            w = a.g.nbr[j];
-            pull = inside(w) && a.region[w] == opp;
-          }
+        int32_t* pulled = a.ref_pulled + s0;
+        for (int32_t k0 = 0; k0 < dmv; k0 += 32) {
+          const int32_t w = k0 + lane < dmv ? nbr_at(mv, k0 + lane) : -1;
+          const bool pull = w >= 0 && region[w] == opp;
           const uint32_t m = __ballot_sync(0xffffffffu, pull);
-          const bool fresh = pull && !a.in_list[w];
+          const bool fresh = pull && a.slot_of[w] < 0;
           const uint32_t mf = __ballot_sync(0xffffffffu, fresh);
           if (pull) {
-            a.region[w] = 2;
-            s_pulled[np + __popc(m & ((1u << lane) - 1))] = w;
+            region[w] = 2;
+            pulled[np + __popc(m & ((1u << lane) - 1))] = w;
           }
           if (fresh) {
             const int32_t k2 = tail + __popc(mf & ((1u << lane) - 1));
             lv[k2] = w;
-            lown[k2] = static_cast<uint8_t>(a.side[a.assign[w]]);
+            lown[k2] = a.vside[w];
             a.slot_of[w] = k2;
-            a.in_list[w] = 1;
           }
           tail += __popc(mf);
           np += __popc(m);
         }
         __syncwarp();
-        for (int32_t t = lane; t < np; t += 32) lin[a.slot_of[s_pulled[t]]] = 2;  // 2 = pulled by this move
+        for (int32_t t = lane; t < np; t += 32) lin[a.slot_of[pulled[t]]] = 2;  // 2 = pulled by this move
         if (lane == 0) {
-          a.region[mv] = own;
+          region[mv] = own;
           lin[im] = 0;
           s_list = tail;
-          s_np = np;
         }
         __syncwarp();
-        // 2. incremental pull counts of the other separator vertices
-        for (int32_t j = mb + lane; j < me; j += 32) {  // mv: 2 -> own
-          const int32_t x = a.g.nbr[j];
-          if (!inside(x) || a.region[x] != 2) continue;
-          const int32_t ix = a.slot_of[x];
-          if (lin[ix] == 1 && lown[ix] == opp) atomicAdd(&lpull[ix], 1);
-        }
-        for (int32_t t = lane; t < np; t += 32) {  // pulled w: opp -> 2
-          const int32_t wv = s_pulled[t];
-          for (int32_t j = a.g.off[wv]; j < a.g.off[wv + 1]; ++j) {
-            const int32_t x = a.g.nbr[j];
-            if (!inside(x) || a.region[x] != 2) continue;
+        // 2a. mv: 2 -> own raises the pull of separator neighbours whose opposite is own
+        for (int32_t k0 = 0; k0 < dmv; k0 += 32) {
+          const int32_t x = k0 + lane < dmv ? nbr_at(mv, k0 + lane) : -1;
+          if (x >= 0 && region[x] == 2) {
             const int32_t ix = a.slot_of[x];
-            if (lin[ix] == 1 && lown[ix] == own) atomicSub(&lpull[ix], 1);
+            if (lin[ix] == 1 && lown[ix] == opp) atomicAdd(&lpull[ix], 1);
           }
         }
-        __syncwarp();
-        // 3. fresh counts for the pulled vertices
-        for (int32_t t = lane; t < np; t += 32) {
-          const int32_t wv = s_pulled[t];
-          const int32_t iw = a.slot_of[wv];
-          const int8_t wopp = 1 - static_cast<int8_t>(lown[iw]);
-          int32_t pull = 0;
-          for (int32_t j = a.g.off[wv]; j < a.g.off[wv + 1]; ++j) {
-            const int32_t x = a.g.nbr[j];
-            pull += inside(x) && a.region[x] == wopp;
+        // 2b/3. every pulled w (opp -> 2): (w, slot) pairs across the warp
+        for (int32_t t0 = 0; t0 < np; t0 += 4) {
+          const int32_t t = t0 + (lane >> 3);
+          const int32_t wv = t < np ? pulled[t] : -1;
+          const int32_t dw = wv >= 0 ? degree(wv) : 0;
+          const uint8_t wopp = wv >= 0 ? static_cast<uint8_t>(1 - a.vside[wv]) : 0;
+          int32_t cntp = 0;
+          for (int32_t k = (lane & 7); k < dw; k += 8) {
+            const int32_t x = nbr_at(wv, k);
+            if (x < 0) continue;
+            const int8_t rx = region[x];
+            cntp += rx == wopp;
+            if (rx == 2) {
+              const int32_t ix = a.slot_of[x];
+              if (lin[ix] == 1 && lown[ix] == own) atomicSub(&lpull[ix], 1);
+            }
           }
-          lpull[iw] = pull;
+          // fresh pull count of wv: sum over its 8-lane group
+          cntp += __shfl_xor_sync(0xffffffffu, cntp, 1);
+          cntp += __shfl_xor_sync(0xffffffffu, cntp, 2);
+          cntp += __shfl_xor_sync(0xffffffffu, cntp, 4);
+          if (wv >= 0 && (lane & 7) == 0) lpull[a.slot_of[wv]] = cntp;
         }
         __syncwarp();
-        for (int32_t t = lane; t < np; t += 32) lin[a.slot_of[s_pulled[t]]] = 1;
+        for (int32_t t = lane; t < np; t += 32) lin[a.slot_of[pulled[t]]] = 1;
+        const int64_t nrw0 = s_rw[0] + (own == 0 ? 1 : -np), nrw1 = s_rw[1] + (own == 1 ? 1 : -np);
+        // imbalance table of the next move
+        {
+          const int32_t o2 = lane >> 4, pull = lane & 15;
+          const int64_t ro = o2 ? nrw1 : nrw0, rp = o2 ? nrw0 : nrw1;
+          s_ni[o2][pull] = imbalance_of(ro + 1, rp - pull);
+        }
         if (lane == 0) {
-          s_rw[own] += 1;
-          s_rw[opp] -= np;
+          s_rw[0] = nrw0, s_rw[1] = nrw1;
           s_size = s_size - 1 + np;
-          s_imb = imbalance_of(s_rw[0], s_rw[1]);
+          s_imb = imbalance_of(nrw0, nrw1);
           ++s_moves;
         }
       }
@@ -710,13 +815,13 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
     __syncthreads();
     if (s_mv < 0) break;
   }
-  // split the node: separator stays at `node`, sides go to the children
-  // (stable, so each child's vertex list stays ascending)
+  // split the node: separator stays at `node` (and leaves play: region 3),
+  // sides go to the children (stable, so each child's list stays ascending)
   int32_t* out = a.next_vlist + s0;
   int32_t nleft_total;
   {
     int32_t c = 0;
-    for (int32_t i = threadIdx.x; i < cnt; i += blockDim.x) c += a.region[seg[i]] == 0;
+    for (int32_t i = threadIdx.x; i < cnt; i += blockDim.x) c += region[seg[i]] == 0;
     nleft_total = static_cast<int32_t>(block_sum_i64(c, reinterpret_cast<int64_t*>(sred)));
   }
   int32_t runl = 0, runr = 0;
@@ -726,7 +831,7 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
     int8_t r = 3;
     if (i < cnt) {
       v = seg[i];
-      r = a.region[v];
+      r = region[v];
     }
     int32_t tl, tr;
     const int32_t el = block_excl_scan(r == 0 ? 1 : 0, shi, &tl);
@@ -740,7 +845,12 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
     }
     runl += tl, runr += tr;
   }
-  for (int32_t i = threadIdx.x; i < s_list; i += blockDim.x) a.in_list[lv[i]] = 0;
+  __syncthreads();
+  for (int32_t i = threadIdx.x; i < s_list; i += blockDim.x) {
+    const int32_t v = lv[i];
+    a.slot_of[v] = -1;
+    if (region[v] == 2) region[v] = 3;  // the separator leaves the game
+  }
   if (threadIdx.x == 0) {
     a.next_start[lc] = s0, a.next_cnt[lc] = runl;
     a.next_start[rc] = s0 + runl, a.next_cnt[rc] = runr;
@@ -915,8 +1025,13 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
   DevBuf<uint8_t> in_super(std::max(n, 1), s), in_list(std::max(n, 1), s), side(Pm, s);
   DevBuf<uint64_t> keys(std::max(m2, 1), s);
   MP_CUDA(cudaMemsetAsync(in_list, 0, std::max(n, 1), s));
+  MP_CUDA(cudaMemsetAsync(region, 3, std::max(n, 1), s));  // 3 = not in play
+  DevBuf<uint8_t> vside(std::max(n, 1), s);
+  DevBuf<int32_t> ell(8LL * std::max(n, 1), s);
+  if (n > 0) MP_KERNEL(ctx, build_ell_nd<<<grid_for(ctx, n), 256, 0, s>>>(g, ell));
   MP_CUDA(cudaMemsetAsync(stats, 0, 16, s));
   MP_KERNEL(ctx, fill32<<<grid_for(ctx, n), 256, 0, s>>>(n, node_of, 0));
+  MP_KERNEL(ctx, fill32<<<grid_for(ctx, n), 256, 0, s>>>(n, slot_of, -1));
   MP_KERNEL(ctx, iota32<<<grid_for(ctx, n), 256, 0, s>>>(n, vl_a));
 
   // level-node segment tables (host-built for the root, device afterwards)
@@ -947,6 +1062,7 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     a.sep_list = seplist, a.next_vlist = nxt_list, a.next_start = next_start, a.next_cnt = next_cnt;
     a.fm_w = fm_w, a.fm_ab = fm_ab, a.fm_ae = fm_ae, a.fm_side = fm_side, a.fm_lk = fm_lk, a.fm_bm = fm_bm, a.fm_bw = fm_bw;
     a.slot_of = slot_of, a.ref_pull = ref_pull, a.ref_own = ref_own, a.ref_in = ref_in, a.ref_pulled = ref_pulled;
+    a.vside = vside, a.ell = ell;
     a.stats = ctx.dwork ? ctx.dwork + 1 : stats.get(), a.fm_gain = fm_gain, a.fm_moves = fm_moves, a.fm_rec = fm_rec;
     const dim3 lgrid(std::max(1, grid_for(ctx, n) / std::max(1, width)), std::min(width, 65535));
     MP_KERNEL(ctx, level_weights<<<lgrid, 256, 0, s>>>(a));
@@ -1018,7 +1134,24 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     DevBuf<int32_t> qloc(std::max<int64_t>(U, 1), s);
     if (U > 0) MP_KERNEL(ctx, local_adjacency<<<grid_for(ctx, U), 256, 0, s>>>(static_cast<int32_t>(U), qnbr, lidx, qloc));
     a.qloc = qloc;
-    const size_t fm_smem = static_cast<size_t>(std::min(maxnp, kFmSmemPatches)) * kFmBytesPerPatch + 512;
+    size_t fm_smem = static_cast<size_t>(std::min(maxnp, kFmSmemPatches)) * kFmBytesPerPatch + 512;
+    {
+      // room for the packed adjacency of the largest node that fits
+      std::vector<int64_t> hfo(width + 1);
+      std::vector<int32_t> hpo(width + 1);
+      MP_CUDA(cudaMemcpyAsync(hfo.data(), fifo_off.get(), sizeof(int64_t) * (width + 1), cudaMemcpyDeviceToHost, s));
+      MP_CUDA(cudaMemcpyAsync(hpo.data(), poff.get(), sizeof(int32_t) * (width + 1), cudaMemcpyDeviceToHost, s));
+      MP_CUDA(cudaStreamSynchronize(s));
+      size_t need = 0;
+      for (int32_t i = 0; i < width; ++i) {
+        const int64_t np_i = hpo[i + 1] - hpo[i];
+        if (np_i == 0 || np_i > kFmSmemPatches) continue;
+        const int64_t e_i = (hfo[i + 1] - hfo[i]) - np_i;
+        need = std::max<size_t>(need, static_cast<size_t>(np_i) * kFmBytesPerPatch + 4 * e_i + 1024);
+      }
+      fm_smem = std::min<size_t>(std::max(fm_smem, need), 227 * 1024);
+    }
+    a.fm_smem_bytes = static_cast<int64_t>(fm_smem);
     MP_CUDA(cudaFuncSetAttribute(fm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fm_smem)));
     { const int kt__ = ctx.ktime_begin(kKFm); MP_KERNEL(ctx, fm_kernel<<<width, kFmThreads, fm_smem, s>>>(a)); ctx.ktime_end(kt__); }
     st.mark("level/fm");
