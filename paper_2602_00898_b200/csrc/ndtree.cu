@@ -194,6 +194,29 @@ constexpr int32_t kFmSmemPatches = 10 * 1024;
 constexpr int kFmBytesPerPatch = 18 + 1;  // + block summaries (24 bytes per 32 patches)
 constexpr int kFmThreads = 256;
 
+// FM move keys (gain desc, id asc): 32-bit when the node has < 65536 patches
+// and |gain| < 32768 (one redux per warp max), 64-bit otherwise.
+template <class K> struct FmKey;
+template <> struct FmKey<uint32_t> {
+  static __device__ __forceinline__ uint32_t make(int32_t gain, int32_t i) {
+    return (static_cast<uint32_t>(gain + 32768) << 16) | (0xffffu - static_cast<uint32_t>(i));
+  }
+  static __device__ __forceinline__ int32_t id(uint32_t k) { return static_cast<int32_t>(0xffffu - (k & 0xffffu)); }
+  static __device__ __forceinline__ uint32_t wmax(uint32_t v) { return __reduce_max_sync(0xffffffffu, v); }
+  static __device__ __forceinline__ void amax(uint32_t* p, uint32_t v) { atomicMax(p, v); }
+};
+template <> struct FmKey<uint64_t> {
+  static __device__ __forceinline__ uint64_t make(int32_t gain, int32_t i) {
+    return key_max(static_cast<uint32_t>(gain + kGainBias), static_cast<uint32_t>(i));
+  }
+  static __device__ __forceinline__ int32_t id(uint64_t k) { return static_cast<int32_t>(key_max_id(k)); }
+  static __device__ __forceinline__ uint64_t wmax(uint64_t v) { return warp_max_u64(v); }
+  static __device__ __forceinline__ void amax(uint64_t* p, uint64_t v) {
+    atomicMax(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(v));
+  }
+};
+
+template <class K>
 __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
   const int32_t li = blockIdx.x;
   if (!a.active[li]) return;
@@ -206,7 +229,7 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
   extern __shared__ uint64_t fm_sm64[];
   const bool in_smem = np <= kFmSmemPatches;
   const int32_t nb_ = (np + 31) / 32;
-  uint64_t* bk = in_smem ? fm_sm64 : a.fm_bm + 2LL * ((pbeg >> 5) + li);         // block max keys, 2 sides
+  K* bk = in_smem ? reinterpret_cast<K*>(fm_sm64) : reinterpret_cast<K*>(a.fm_bm + 2LL * ((pbeg >> 5) + li));  // block max keys, 2 sides
   int32_t* bwt = in_smem ? reinterpret_cast<int32_t*>(fm_sm64 + 2 * nb_) : a.fm_bw + 2LL * ((pbeg >> 5) + li);
   int32_t* fm_sm = reinterpret_cast<int32_t*>(fm_sm64 + 2 * nb_ + nb_);  // after 2*nb keys + 2*nb ints
   int32_t* w = in_smem ? fm_sm : a.fm_w + pbeg;
@@ -352,20 +375,18 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
       flag[i] = 0;  // unlocked
     }
     __syncthreads();
-    auto leaf_key = [&](int32_t i) -> uint64_t {
-      return flag[i] ? 0 : key_max(static_cast<uint32_t>(gain[i] + kGainBias), static_cast<uint32_t>(i));
-    };
+    auto leaf_key = [&](int32_t i) -> K { return flag[i] ? K(0) : FmKey<K>::make(gain[i], i); };
     // (re)build the per-side block summaries of block b (one warp)
     auto block_sum = [&](int32_t b) {
       const int32_t i = b * 32 + lane;
-      uint64_t k0 = 0, k1 = 0;
+      K k0 = 0, k1 = 0;
       int32_t w0 = INT32_MAX, w1 = INT32_MAX;
       if (i < np && !flag[i]) {
-        const uint64_t k = leaf_key(i);
+        const K k = leaf_key(i);
         if (side[i]) k1 = k, w1 = w[i];
         else k0 = k, w0 = w[i];
       }
-      k0 = warp_max_u64(k0), k1 = warp_max_u64(k1);
+      k0 = FmKey<K>::wmax(k0), k1 = FmKey<K>::wmax(k1);
       w0 = __reduce_min_sync(0xffffffffu, w0), w1 = __reduce_min_sync(0xffffffffu, w1);
       if (lane == 0) bk[b] = k0, bk[nblk + b] = k1, bwt[b] = w0, bwt[nblk + b] = w1;
     };
@@ -383,79 +404,95 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
         const int64_t ns = (sd ? sw1 : sw0) - wi, nt = (sd ? sw0 : sw1) + wi;
         return ns > 0 && !(imbalance_of(ns, nt) > thr);
       };
-      long long c_w = 0, c_s = 0, c_u = 0;
+      long long c_w = 0, c_s = 0, c_u = 0, c_x1 = 0, c_x2 = 0, c_x3 = 0, c_x4 = 0;
       for (;;) {
         long long c0 = clock64();
         // Feasible weights of a side form [0, W_s]: the ratio falls until the
         // sides cross and rises after, and the rounded division is monotone.
         // W_s from the real-valued estimate, fixed up with exact predicates
         // evaluated in parallel lanes (lanes 0-1 side 0, lanes 2-3 side 1).
-        int64_t Wsd[2];
-        {
-          // lanes 0-15 probe side 0 at est-7 .. est+8, lanes 16-31 side 1
-          const int32_t sd = lane >> 4;
+        // side tops
+        K t0 = 0, t1 = 0;
+        for (int32_t b = lane; b < nblk; b += 32) t0 = max(t0, bk[b]), t1 = max(t1, bk[nblk + b]);
+        t0 = FmKey<K>::wmax(t0), t1 = FmKey<K>::wmax(t1);
+        if ((t0 | t1) == 0) break;
+        // Feasibility.  Moving w off the heavier side with 2w <= S - T lowers the
+        // ratio (<= cur <= thr): feasible without a division.  Otherwise the
+        // exact predicate; a side whose top fails needs its weight bound W_s
+        // (feasible weights form [0, W_s]: the ratio falls until the sides
+        // cross, and the rounded division is monotone after) for a block search.
+        auto quick = [&](int32_t i, int32_t sd) {
           const int64_t S = sd ? sw1 : sw0, T = sd ? sw0 : sw1;
-          int64_t est = S - 1;
-          if (!isinf(thr)) {  // estimate only (exact predicates decide): float math
-            const float tf = static_cast<float>(thr);
-            const float e = __fdividef(tf * static_cast<float>(S) - static_cast<float>(T), 1.0f + tf);
-            const int64_t fe = static_cast<int64_t>(floorf(e));
-            est = fe < est ? fe : est;
-          }
-          const int64_t probe = est - 7 + (lane & 15);
-          const bool pv = probe >= 0 && pred(probe, sd);
-          const uint32_t pm = __ballot_sync(0xffffffffu, pv);
-          for (int q = 0; q < 2; ++q) {
-            const uint32_t m = (pm >> (16 * q)) & 0xffffu;
-            const int64_t e2 = __shfl_sync(0xffffffffu, est, 16 * q);
-            int64_t W;
-            if (m == 0xffffu) {  // window all feasible: walk up (rare)
-              W = e2 + 8;
-              while (pred(W + 1, q)) ++W;
-            } else if (m == 0 && e2 - 7 > 0) {  // window all infeasible: walk down (rare)
-              W = e2 - 8;
-              while (W >= 0 && !pred(W, q)) --W;
-            } else {  // feasible probes form a prefix of the window
-              W = e2 - 7 + (32 - __clz(static_cast<int>(m))) - 1;
+          return S >= T && 2 * static_cast<int64_t>(w[i]) <= S - T;
+        };
+        const K hiT = max(t0, t1), loT = min(t0, t1);
+        const int32_t hs = t1 > t0 ? 1 : 0;
+        K best = 0;
+        int32_t fail_side = -1;
+        {
+          const int32_t ih = FmKey<K>::id(hiT);
+          if (quick(ih, hs) || pred(w[ih], hs)) {
+            best = hiT;
+          } else {
+            fail_side = hs;
+            if (loT) {
+              const int32_t il = FmKey<K>::id(loT);
+              if (quick(il, 1 - hs) || pred(w[il], 1 - hs)) best = loT;
+              // (if the lower top fails too, its side can hold nothing better than
+              //  loT that the search of fail_side would miss: searched below)
+              else if (loT > 0) best = 0, fail_side = 2;  // both sides need the block search
             }
-            Wsd[q] = W;
           }
         }
-        // side tops
-        uint64_t t0 = 0, t1 = 0;
-        for (int32_t b = lane; b < nblk; b += 32) t0 = max(t0, bk[b]), t1 = max(t1, bk[nblk + b]);
-        t0 = warp_max_u64(t0), t1 = warp_max_u64(t1);
-        if ((t0 | t1) == 0) break;
-        uint64_t best = 0;
-        bool ok0 = t0 && w[key_max_id(t0)] <= Wsd[0], ok1 = t1 && w[key_max_id(t1)] <= Wsd[1];
-        if (ok0) best = t0;
-        if (ok1 && t1 > best) best = t1;
         long long c1 = clock64();
         c_w += c1 - c0;
-        // a side whose top is too heavy: the best block-wise patch with w <= W_s
-        for (int sd = 0; sd < 2; ++sd) {
-          const uint64_t top = sd ? t1 : t0;
-          if ((sd ? ok1 : ok0) || top <= best) continue;
-          const int64_t W = Wsd[sd];
-          for (int32_t b0 = 0; b0 < nblk; b0 += 32) {
-            const int32_t b = b0 + lane;
-            const bool maybe = b < nblk && bk[sd * nblk + b] > best && bwt[sd * nblk + b] <= W;
-            uint32_t cand = __ballot_sync(0xffffffffu, maybe);
-            while (cand) {
-              const int32_t bb = b0 + __ffs(cand) - 1;
-              cand &= cand - 1;
-              if (bk[sd * nblk + bb] <= best) continue;
-              const int32_t i = bb * 32 + lane;
-              uint64_t k = 0;
-              if (i < np && !flag[i] && side[i] == sd && w[i] <= W) k = leaf_key(i);
-              best = max(best, warp_max_u64(k));
+        if (fail_side >= 0) {
+          for (int sd = 0; sd < 2; ++sd) {
+            if (fail_side != 2 && sd != fail_side) continue;
+            const K top = sd ? t1 : t0;
+            if (top <= best) continue;
+            // W_s: lanes 0-15 probe a window around the real-valued estimate
+            const int64_t S = sd ? sw1 : sw0, T = sd ? sw0 : sw1;
+            int64_t est = S - 1;
+            if (!isinf(thr)) {
+              const float tf = static_cast<float>(thr);
+              const float e = __fdividef(tf * static_cast<float>(S) - static_cast<float>(T), 1.0f + tf);
+              const int64_t fe = static_cast<int64_t>(floorf(e));
+              est = fe < est ? fe : est;
+            }
+            const int64_t probe = est - 7 + (lane & 15);
+            const bool pv = lane < 16 && probe >= 0 && pred(probe, sd);
+            const uint32_t m = __ballot_sync(0xffffffffu, pv) & 0xffffu;
+            int64_t W;
+            if (m == 0xffffu) {
+              W = est + 8;
+              while (pred(W + 1, sd)) ++W;
+            } else if (m == 0 && est - 7 > 0) {
+              W = est - 8;
+              while (W >= 0 && !pred(W, sd)) --W;
+            } else {
+              W = est - 7 + (32 - __clz(static_cast<int>(m))) - 1;
+            }
+            for (int32_t b0 = 0; b0 < nblk; b0 += 32) {
+              const int32_t b = b0 + lane;
+              const bool maybe = b < nblk && bk[sd * nblk + b] > best && bwt[sd * nblk + b] <= W;
+              uint32_t cand = __ballot_sync(0xffffffffu, maybe);
+              while (cand) {
+                const int32_t bb = b0 + __ffs(cand) - 1;
+                cand &= cand - 1;
+                if (bk[sd * nblk + bb] <= best) continue;
+                const int32_t i = bb * 32 + lane;
+                K k = 0;
+                if (i < np && !flag[i] && side[i] == sd && w[i] <= W) k = leaf_key(i);
+                best = max(best, FmKey<K>::wmax(k));
+              }
             }
           }
         }
         long long c2 = clock64();
         c_s += c2 - c1;
         if (best == 0) break;
-        const int32_t ch = static_cast<int32_t>(key_max_id(best));
+        const int32_t ch = FmKey<K>::id(best);
         const int32_t gch = gain[ch];
         const uint8_t sd = side[ch];
         const int64_t wc = w[ch];
@@ -474,6 +511,8 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
         // neighbours' gains (partition.cpp:137-142).  A raised key only needs a
         // max into its block summary; a lowered key forces a rebuild only if it
         // was the block's maximum; ch's own block is rebuilt (ch is now locked).
+        long long cu1 = clock64();
+        c_w += 0;
         const uint8_t sc = static_cast<uint8_t>(1 - sd);
         const int32_t e0 = ab[ch], e1 = ae[ch];
         for (int32_t j0 = e0; j0 < e1; j0 += 32) {
@@ -483,25 +522,28 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
             const int32_t nb = A_nb(j);
             if (!flag[nb]) {
               const int32_t wj = A_w(j);
-              const uint64_t oldk = leaf_key(nb);
+              const K oldk = leaf_key(nb);
               const int32_t delta = side[nb] == sc ? -2 * wj : 2 * wj;
               gain[nb] += delta;
               const int32_t slot = side[nb] * nblk + (nb >> 5);
-              if (delta > 0) atomicMax(reinterpret_cast<unsigned long long*>(&bk[slot]),
-                                       static_cast<unsigned long long>(leaf_key(nb)));
+              if (delta > 0) FmKey<K>::amax(&bk[slot], leaf_key(nb));
               else if (delta < 0 && bk[slot] == oldk) rb = nb >> 5;
             }
           }
           __syncwarp();
-          const uint32_t same = __match_any_sync(0xffffffffu, rb);
-          uint32_t leaders = __ballot_sync(0xffffffffu, rb >= 0 && (__ffs(same) - 1) == lane);
-          while (leaders) {
-            const int32_t l = __ffs(leaders) - 1;
-            leaders &= leaders - 1;
-            block_sum(__shfl_sync(0xffffffffu, rb, l));
+          uint32_t todo = __ballot_sync(0xffffffffu, rb >= 0);  // usually 0-2 lanes
+          int32_t last = -1;
+          while (todo) {
+            const int32_t l = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int32_t blk = __shfl_sync(0xffffffffu, rb, l);
+            if (blk != last && blk != (ch >> 5)) block_sum(blk);
+            last = blk;
           }
         }
+        long long cu2 = clock64();
         block_sum(ch >> 5);
+        long long cu3 = clock64();
         const double imb = imbalance_of(sw0, sw1);
         if (cut < best_cut || (cut == best_cut && imb < best_imb)) {
           best_cut = cut;
@@ -510,12 +552,18 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
         }
         thr = kBalanceTol > imb ? kBalanceTol : imb;
         __syncwarp();
-        c_u += clock64() - c2;
+        long long cu4 = clock64();
+        c_u += cu4 - c2;
+        c_x1 += cu1 - c2, c_x2 += cu2 - cu1, c_x3 += cu3 - cu2, c_x4 += cu4 - cu3;
       }
       if (lane == 0 && li == 0 && a.first == 0) {
         atomicAdd(&a.stats[12], static_cast<unsigned long long>(c_w));
         atomicAdd(&a.stats[13], static_cast<unsigned long long>(c_s));
         atomicAdd(&a.stats[14], static_cast<unsigned long long>(c_u));
+        atomicAdd(&a.stats[6], static_cast<unsigned long long>(c_x1));
+        atomicAdd(&a.stats[7], static_cast<unsigned long long>(c_x2));
+        atomicAdd(&a.stats[8], static_cast<unsigned long long>(c_x3));
+        atomicAdd(&a.stats[9], static_cast<unsigned long long>(c_x4));
       }
       if (lane == 0) {
         s_nm = nm;
@@ -549,6 +597,15 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
   if (threadIdx.x == 0) atomicAdd(&a.stats[0], static_cast<unsigned long long>(total_moves));
 }
 
+// largest total quotient edge weight of a patch: bounds |gain| for the key width
+__global__ void fm_gain_bound(int32_t na, const int32_t* plist, const int32_t* qoff, const int32_t* qw, int32_t* out) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
+    const int32_t p = plist[i];
+    int64_t sum = 0;
+    for (int32_t j = qoff[p]; j < qoff[p + 1]; ++j) sum += qw[j];
+    atomicMax(out, static_cast<int32_t>(sum < 0x7fffffff ? sum : 0x7fffffff));
+  }
+}
 __global__ void local_adjacency(int32_t U, const int32_t* qnbr, const int32_t* lidx, int32_t* qloc) {
   for (int32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < U; j += gridDim.x * blockDim.x) qloc[j] = lidx[qnbr[j]];
 }
@@ -1152,8 +1209,27 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
       fm_smem = std::min<size_t>(std::max(fm_smem, need), 227 * 1024);
     }
     a.fm_smem_bytes = static_cast<int64_t>(fm_smem);
-    MP_CUDA(cudaFuncSetAttribute(fm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fm_smem)));
-    { const int kt__ = ctx.ktime_begin(kKFm); MP_KERNEL(ctx, fm_kernel<<<width, kFmThreads, fm_smem, s>>>(a)); ctx.ktime_end(kt__); }
+    // 32-bit move keys when every node fits (patch count and gain range)
+    int32_t hgb = 0;
+    {
+      DevBuf<int32_t> gb(1, s);
+      MP_CUDA(cudaMemsetAsync(gb, 0, 4, s));
+      if (na_level > 0) MP_KERNEL(ctx, fm_gain_bound<<<grid_for(ctx, na_level), 256, 0, s>>>(na_level, plist, qoff, qw, gb));
+      MP_CUDA(cudaMemcpyAsync(&hgb, gb.get(), 4, cudaMemcpyDeviceToHost, s));
+      MP_CUDA(cudaStreamSynchronize(s));
+    }
+    const bool k32 = maxnp < 65536 && hgb < 32768;
+    if (k32) {
+      MP_CUDA(cudaFuncSetAttribute(fm_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fm_smem)));
+      const int kt__ = ctx.ktime_begin(kKFm);
+      MP_KERNEL(ctx, fm_kernel<uint32_t><<<width, kFmThreads, fm_smem, s>>>(a));
+      ctx.ktime_end(kt__);
+    } else {
+      MP_CUDA(cudaFuncSetAttribute(fm_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fm_smem)));
+      const int kt__ = ctx.ktime_begin(kKFm);
+      MP_KERNEL(ctx, fm_kernel<uint64_t><<<width, kFmThreads, fm_smem, s>>>(a));
+      ctx.ktime_end(kt__);
+    }
     st.mark("level/fm");
     MP_KERNEL(ctx, super_pass<<<lgrid, 256, 0, s>>>(a));
     const size_t ref_smem = static_cast<size_t>(kRefSmemList) * 10;
