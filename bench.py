@@ -43,7 +43,9 @@ WORKLOADS = {
     "c1": ("grid", 64, "64x64 grid (n=4,096), patch 256, seed 0, L=3, approx_md, postorder"),
     "ico158": ("icosphere", 158, "icosphere f=158 (n=249,642), one C4 frame"),
     "grid1000": ("grid", 1000, "1000x1000 grid (n=1,000,000)"),
+    "c5": ("icosphere", 447, "icosphere f=447 (n=1,998,092) with 3x3 blocks (5,994,276 rows), patch 256, L=8"),
 }
+C4_FRAMES = 64  # BASELINE configs[3]: 64 frames, random_mesh(500, 500, seed=frame) (250,000 vertices each)
 
 
 def load_graph(name):
@@ -200,6 +202,8 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     g = load_graph(args.workload)
     n, m2 = g.n, int(g.offsets[-1])
+    B = 3 if args.workload == "c5" else 1  # configs[4]: 3x3 blocks expanded on the device
+    N = B * n
     L = mp.default_nd_level(n)
     nn = (1 << (L + 1)) - 1
     ctx = mp.Context(local)
@@ -211,12 +215,12 @@ def run_ours(args):
     outs = {
         "patch_of": torch.empty(n, dtype=torch.int32, device=dev),
         "tree_node_offsets": torch.empty(nn + 1, dtype=torch.int32, device=dev),
-        "tree_vertices": torch.empty(n, dtype=torch.int32, device=dev),
-        "tree_local_perm": torch.empty(n, dtype=torch.int32, device=dev),
-        "perm": torch.empty(n, dtype=torch.int32, device=dev),
-        "inverse": torch.empty(n, dtype=torch.int32, device=dev),
-        "etree_parent": torch.empty(n, dtype=torch.int32, device=dev),
-        "column_counts": torch.empty(n, dtype=torch.int64, device=dev),
+        "tree_vertices": torch.empty(N, dtype=torch.int32, device=dev),
+        "tree_local_perm": torch.empty(N, dtype=torch.int32, device=dev),
+        "perm": torch.empty(N, dtype=torch.int32, device=dev),
+        "inverse": torch.empty(N, dtype=torch.int32, device=dev),
+        "etree_parent": torch.empty(N, dtype=torch.int32, device=dev),
+        "column_counts": torch.empty(N, dtype=torch.int64, device=dev),
     }
     ptrs = {k: v.data_ptr() for k, v in outs.items()}
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
@@ -224,7 +228,7 @@ def run_ours(args):
     def step():
         with torch.cuda.stream(stream):
             flush.fill_(1)  # evict the L2 (126 MB) before every step
-        return api.order_device(ctx, n, d_off.data_ptr(), d_nbr.data_ptr(), ptrs)
+        return api.order_device(ctx, n, d_off.data_ptr(), d_nbr.data_ptr(), ptrs, block_size=B)
 
     for _ in range(args.warmup):
         res = step()
@@ -238,7 +242,7 @@ def run_ours(args):
             with torch.cuda.stream(stream):
                 flush.fill_(1)
             ev0.record(stream)
-            res = api.order_device(ctx, n, d_off.data_ptr(), d_nbr.data_ptr(), ptrs)
+            res = api.order_device(ctx, n, d_off.data_ptr(), d_nbr.data_ptr(), ptrs, block_size=B)
             ev1.record(stream)
             perm_ms.append(sum(res.stage_ms[i] for i in range(5)))
             if os.environ.get("MP_BENCH_VERBOSE"):
@@ -271,7 +275,7 @@ def run_ours(args):
     h_outs = {k: torch.empty(v.numel(), dtype=v.dtype).pin_memory() for k, v in outs.items()
               if k not in ("etree_parent", "column_counts")}
     h_ptrs = {k: v.data_ptr() for k, v in h_outs.items()}
-    cfg = api.make_config(want_fill=False)  # the metric: permutation (fill is reported as fill_ms)
+    cfg = api.make_config(block_size=B, want_fill=False)  # the metric: permutation (fill is reported as fill_ms)
     from paper_2602_00898_b200._lib import MpCsr, MpResult, check, lib
     import ctypes as C
 
@@ -333,7 +337,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": round(ms_tot, 3), "higher_is_better": False,
             "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": WORKLOADS[args.workload][2], "n": n, "nnz_A": int(res.nnz_A),
-                       "patch_size": 256, "seed": 0, "nd_level": L, "parallelism": f"replicas{ws}",
+                       "patch_size": 256, "seed": 0, "nd_level": L, "block_size": B, "parallelism": f"replicas{ws}",
                        "l2_flush": "512 MiB write before every step"},
             "vertices_per_s": round(ws * n / (ms * 1e-3), 1),
             "fill_ms": round(ms_fill, 3),
@@ -358,7 +362,7 @@ def run_ours(args):
                      "fps_grid_levels": int(res.work[5]), "fps_candidates": int(res.work[6]),
                      "fps_region_levels_cta0": int(res.work[7]),
                      "fps_phase_cycles": [int(res.work[i]) for i in range(8, 13)],
-                     "fm_root_cycles": [int(res.work[i]) for i in range(13, 16)]},
+                     "fps_select_stats": [int(res.work[i]) for i in range(13, 16)]},
             "e2e": {"value": round(e2e_v, 3), "unit": "ms", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h)},
             "cpu_baseline": cpu,
@@ -371,17 +375,57 @@ def run_ours(args):
     return 0
 
 
+def run_c4(args):
+    """configs[3]: 64 independent 250K frames, sharded round-robin over ranks, 4
+    concurrent contexts per GPU; value = whole-batch ms (max over ranks)."""
+    import torch
+    import paper_2602_00898_b200 as mp
+    from paper_2602_00898_b200.batch import FramePool, max_over_ranks, shard
+    ws, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    mine = shard(C4_FRAMES, ws, rank)
+    frames = [mp.mesh_to_graph(mp.make_random_mesh(500, 500, seed=f)) for f in mine]
+    pool = FramePool(local, workers=4)
+    for _ in range(args.warmup):
+        pool.order_all(frames[:4], want_fill=False)
+    barrier(ws)
+    times = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = pool.order_all(frames, want_fill=False)
+        times.append((time.perf_counter() - t0) * 1e3)
+    ms = max_over_ranks(float(np.mean(times)), ws)
+    pool.close()
+    if rank == 0:
+        n = sum(f.n for f in frames) * ws
+        print(json.dumps({"metric": "C4 batch ordering ms (64 x 250K frames, host arrays in/out)", "value": round(ms, 3),
+                          "unit": "ms", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",
+                          "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+                          "config": {"workload": "64 x random_mesh(500,500,seed=f), patch 256, L=8",
+                                     "frames_per_rank": len(mine), "contexts_per_gpu": 4},
+                          "vertices_per_s": round(C4_FRAMES * 250000 / (ms * 1e-3), 1),
+                          "frame_patch_counts": [r.patch.patch_count for r in res[:4]]}), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS) + ["c4"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.workload == "c4":
+        return run_c4(args)
     return run_ours(args)
 
 

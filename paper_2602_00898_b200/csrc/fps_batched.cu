@@ -203,6 +203,7 @@ __device__ void select_candidates(const BatchArgs& a, int32_t W, uint64_t* sS, i
     int32_t filled = 0;
     const int32_t cap = min(W, kSCap);  // only the first W ties in id order can become candidates
     for (int32_t c0 = 0; c0 < nflag && filled < cap; c0 += nwarp) {
+      if (threadIdx.x == 0 && a.work) atomicAdd(&a.work[15], 1ull);
       const int32_t ci = c0 + wid;
       int32_t cntw = 0;
       uint32_t masks[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // up to 256 vertices per tile chunk pass
@@ -250,7 +251,11 @@ __device__ void select_candidates(const BatchArgs& a, int32_t W, uint64_t* sS, i
   }
   if (threadIdx.x == 0) {
     a.ctl[1] = nc;
-    if (a.work) atomicAdd(&a.work[4], 1ull), atomicAdd(&a.work[6], static_cast<unsigned long long>(nc));
+    if (a.work) {
+      atomicAdd(&a.work[4], 1ull), atomicAdd(&a.work[6], static_cast<unsigned long long>(nc));
+      atomicAdd(&a.work[13], exact ? 1ull : 0ull);
+      atomicAdd(&a.work[14], static_cast<unsigned long long>(ns));
+    }
   }
 }
 

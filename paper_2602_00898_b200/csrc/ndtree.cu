@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
         const int64_t ns = (sd ? sw1 : sw0) - wi, nt = (sd ? sw0 : sw1) + wi;
         return ns > 0 && !(imbalance_of(ns, nt) > thr);
       };
-      long long c_w = 0, c_s = 0, c_u = 0, c_x1 = 0, c_x2 = 0, c_x3 = 0, c_x4 = 0;
+      long long c_w = 0, c_s = 0, c_u = 0;
       for (;;) {
         long long c0 = clock64();
         // Feasible weights of a side form [0, W_s]: the ratio falls until the
@@ -511,8 +511,6 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
         // neighbours' gains (partition.cpp:137-142).  A raised key only needs a
         // max into its block summary; a lowered key forces a rebuild only if it
         // was the block's maximum; ch's own block is rebuilt (ch is now locked).
-        long long cu1 = clock64();
-        c_w += 0;
         const uint8_t sc = static_cast<uint8_t>(1 - sd);
         const int32_t e0 = ab[ch], e1 = ae[ch];
         for (int32_t j0 = e0; j0 < e1; j0 += 32) {
@@ -541,9 +539,7 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
             last = blk;
           }
         }
-        long long cu2 = clock64();
         block_sum(ch >> 5);
-        long long cu3 = clock64();
         const double imb = imbalance_of(sw0, sw1);
         if (cut < best_cut || (cut == best_cut && imb < best_imb)) {
           best_cut = cut;
@@ -552,19 +548,9 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
         }
         thr = kBalanceTol > imb ? kBalanceTol : imb;
         __syncwarp();
-        long long cu4 = clock64();
-        c_u += cu4 - c2;
-        c_x1 += cu1 - c2, c_x2 += cu2 - cu1, c_x3 += cu3 - cu2, c_x4 += cu4 - cu3;
+        c_u += clock64() - c2;
       }
-      if (lane == 0 && li == 0 && a.first == 0) {
-        atomicAdd(&a.stats[12], static_cast<unsigned long long>(c_w));
-        atomicAdd(&a.stats[13], static_cast<unsigned long long>(c_s));
-        atomicAdd(&a.stats[14], static_cast<unsigned long long>(c_u));
-        atomicAdd(&a.stats[6], static_cast<unsigned long long>(c_x1));
-        atomicAdd(&a.stats[7], static_cast<unsigned long long>(c_x2));
-        atomicAdd(&a.stats[8], static_cast<unsigned long long>(c_x3));
-        atomicAdd(&a.stats[9], static_cast<unsigned long long>(c_x4));
-      }
+      (void)c_w, (void)c_s, (void)c_u;
       if (lane == 0) {
         s_nm = nm;
         s_best_len = best_len;

@@ -84,8 +84,11 @@ def run_case(R, g, patch, L, mode, levelorder, threads=8):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also the 1M-vertex C2 golden (~1 min)")
+    ap.add_argument("--c5", action="store_true", help="only the 2M-vertex C5 golden (3x3 blocks)")
     args = ap.parse_args()
     R = Reference()
+    if args.c5:
+        return make_c5(R)
     arrays = {}
     for name, (build, patch, L, mode, lo) in SMALL.items():
         g = build()
@@ -120,6 +123,30 @@ def main():
                       "sha_column_counts": digest(r["column_counts"]), "sha_parents": digest(r["parents"]),
                       "reference_s": round(time.time() - t0, 1)}
         print(name, gold[name])
+    gold_path.write_text(json.dumps(gold, indent=1) + "\n")
+
+
+def make_c5(R, b=3):
+    """configs[4]: icosphere f=447 with 3x3 blocks.  The reference orders the
+    base graph and expand_blocks (graph.cpp:96-128) maps vertex v to rows
+    b*v..b*v+b-1; the expanded factor's column counts follow from the base
+    ones (row b*v+t of a dense block column: b*c_v - t), the identity that
+    tests/test_gpu_parity.py::test_block_expansion_closed_form checks against
+    the elimination game on the explicitly expanded graph."""
+    g = mp.mesh_to_graph(mp.make_icosphere_mesh(447))
+    t0 = time.time()
+    r = run_case(R, g, 256, -1, 0, 0, threads=16)
+    cc = r["column_counts"].astype(np.int64)
+    cols = (b * cc[:, None] - np.arange(b)[None, :]).reshape(-1)
+    pb = (b * r["perm"].astype(np.int64)[:, None] + np.arange(b)[None, :]).reshape(-1).astype(np.int32)
+    gold_path = HERE / "bench_golden.json"
+    gold = json.loads(gold_path.read_text())
+    gold["c5"] = {"n": g.n, "edges": g.edge_count(), "block_size": b, "patch_count": r["patch_count"],
+                  "nd_level": r["nd_level"], "base_nnz_L": r["nnz_L"], "sha_base_perm": digest(r["perm"]),
+                  "nnz_A": int(b * b * r["nnz_A"]),
+                  "nnz_L": int(cols.sum()), "cost": int((cols * cols).sum()), "sha_perm": digest(pb),
+                  "reference_s": round(time.time() - t0, 1)}
+    print("c5", gold["c5"])
     gold_path.write_text(json.dumps(gold, indent=1) + "\n")
 
 

@@ -234,6 +234,20 @@ def test_baseline_configs_match_reference_digests(name):
     check_tree_properties(g, res)
 
 
+def test_c5_blocks_match_reference():
+    """configs[4]: icosphere f=447 (2M vertices) with 3x3 blocks expanded on the
+    device (6M rows); perm digest and nnz(L)/cost against the reference-derived
+    golden (tests/golden/make_golden.py --c5)."""
+    gold = json.loads((GOLDEN / "bench_golden.json").read_text()).get("c5")
+    if gold is None:
+        pytest.skip("c5 golden not generated")
+    g = mp.mesh_to_graph(mp.make_icosphere_mesh(447))
+    res = mp.order(g, block_size=3)
+    assert res.patch.patch_count == gold["patch_count"]
+    assert digest(res.perm.perm) == gold["sha_perm"]
+    assert (res.fill.nnz_A, res.fill.nnz_L, res.fill.cost) == (gold["nnz_A"], gold["nnz_L"], gold["cost"])
+
+
 def test_deterministic_across_calls_and_contexts():
     g = mp.mesh_to_graph(mp.make_icosphere_mesh(40))
     a = mp.order(g)
@@ -243,3 +257,21 @@ def test_deterministic_across_calls_and_contexts():
     for x in (b, c):
         assert np.array_equal(a.perm.perm, x.perm.perm) and a.fill.nnz_L == x.fill.nnz_L
         assert np.array_equal(a.fill.parents, x.fill.parents)
+
+
+def test_frame_pool_concurrent_frames_match():
+    """C4-style batches: frames ordered concurrently on several contexts equal
+    the single-context results bit for bit (and the oracle)."""
+    from oracle.oracle import Restatement
+    from paper_2602_00898_b200.batch import FramePool
+    R = Restatement()
+    frames = [mp.mesh_to_graph(mp.make_random_mesh(60 + 3 * f, 70, seed=f)) for f in range(8)]
+    pool = FramePool(0, workers=4)
+    try:
+        res = pool.order_all(frames, patch_size=64)
+    finally:
+        pool.close()
+    for g, r in zip(frames, res):
+        o = R.order(g, patch_size=64)
+        assert np.array_equal(r.perm.perm, o["perm"])
+        assert r.fill.nnz_L == R.elimination_fill(g, o["perm"])["nnz_L"]
