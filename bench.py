@@ -385,18 +385,35 @@ def run_c4(args):
     torch.cuda.set_device(local)
     mine = shard(C4_FRAMES, ws, rank)
     frames = [mp.mesh_to_graph(mp.make_random_mesh(500, 500, seed=f)) for f in mine]
-    pool = FramePool(local, workers=4)
+    pool = FramePool(local, workers=args.c4_workers)
     for _ in range(args.warmup):
         pool.order_all(frames[:4], want_fill=False)
     barrier(ws)
-    times = []
+    times, launches = [], 0
     for _ in range(args.steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         res = pool.order_all(frames, want_fill=False)
         times.append((time.perf_counter() - t0) * 1e3)
+        launches += sum(r.kernel_launches for r in res)
     ms = max_over_ranks(float(np.mean(times)), ws)
     pool.close()
+    cpu, parity = None, None
+    if rank == 0 and not args.no_cpu:
+        # reference core on a bounded sample (2 frames, all host threads), scaled to 64 frames
+        from oracle.oracle import Reference
+        from paper_2602_00898_b200.batch import frame_digest
+        R = Reference()
+        threads = os.cpu_count() or 1
+        t_ref, ok = [], True
+        for i in range(2):
+            o = R.order_timed(frames[i], threads=threads)
+            t_ref.append(o["ms"])
+            ok &= frame_digest(o["perm"], 0) == frame_digest(res[i].perm.perm, 0)
+        cpu = {"value": round(float(np.mean(t_ref)) * C4_FRAMES, 1), "unit": "ms", "cores": threads,
+               "kind": "reference", "sample": f"frames {mine[:2]} ordered by the reference core (stages 1-5, "
+                                                f"threads={threads}), mean x {C4_FRAMES}"}
+        parity = {"frames_checked": 2, "perm_match": bool(ok)}
     if rank == 0:
         n = sum(f.n for f in frames) * ws
         print(json.dumps({"metric": "C4 batch ordering ms (64 x 250K frames, host arrays in/out)", "value": round(ms, 3),
@@ -404,7 +421,8 @@ def run_c4(args):
                           "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",
                           "vs_baseline": None, "dtype": "int32", "data": "synthetic",
                           "config": {"workload": "64 x random_mesh(500,500,seed=f), patch 256, L=8",
-                                     "frames_per_rank": len(mine), "contexts_per_gpu": 4},
+                                     "frames_per_rank": len(mine), "contexts_per_gpu": args.c4_workers},
+                          "cpu_baseline": cpu, "parity": parity, "gpu_launches": int(launches),
                           "vertices_per_s": round(C4_FRAMES * 250000 / (ms * 1e-3), 1),
                           "frame_patch_counts": [r.patch.patch_count for r in res[:4]]}), flush=True)
     if ws > 1:
@@ -420,6 +438,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS) + ["c4"])
+    ap.add_argument("--c4-workers", type=int, default=8, help="concurrent contexts per GPU for c4")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -203,6 +203,7 @@ int mp_context_create(mp_context** out, int32_t device) {
     MP_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
     ctx->stream = ctx->own_stream;
     MP_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
+    MP_CUDA(cudaDeviceGetAttribute(&ctx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     for (auto& e : ctx->ev) MP_CUDA(cudaEventCreate(&e));
     MP_CUDA(cudaMalloc(reinterpret_cast<void**>(&ctx->dwork), 16 * sizeof(unsigned long long)));
     MP_CUDA(cudaMemset(ctx->dwork, 0, 16 * sizeof(unsigned long long)));

@@ -516,7 +516,7 @@ void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32
   const int32_t ntile = static_cast<int32_t>((static_cast<int64_t>(n) + (1 << tile_shift) - 1) >> tile_shift);
   int bpsm = 0;
   const size_t smem = sizeof(uint64_t) * kSCap + sizeof(int32_t) * kBins;
-  MP_CUDA(cudaFuncSetAttribute(fps_batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  allow_max_smem(fps_batched_kernel, ctx.device);
   MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, fps_batched_kernel, kThreads, smem));
   if (bpsm < 1) throw Error(MP_ECUDA, "fps_batched_kernel does not fit on an SM");
   // workers: one per SM, bounded by the bit-matrix width and by memory

@@ -498,7 +498,7 @@ void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t L, const int
   a.bptr = bptr, a.bsz = bsz, a.vmark = vmark, a.emark = emark, a.gdeg = gdeg, a.pool = pool;
   a.pool_off = pool_off, a.order_ws = order, a.local_perm = local_perm, a.overflow = overflow;
   const size_t smem = sizeof(uint32_t) * kSmemDegCap;
-  MP_CUDA(cudaFuncSetAttribute(md_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  allow_max_smem(md_kernel, ctx.device);
   const int kt__ = ctx.ktime_begin(kKMd);
   if (mode == 0) {
     // largest node decides the shared-memory footprint of the fast kernel
@@ -510,7 +510,7 @@ void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t L, const int
     const int32_t fast_nv = std::min(maxnv, kMdFastCap);
     const int32_t fnb = (fast_nv + 31) / 32;
     const size_t fsmem = sizeof(uint64_t) * fnb + sizeof(int32_t) * 4 * fast_nv + sizeof(uint32_t) * ((fnb + 31) / 32 + 1);
-    MP_CUDA(cudaFuncSetAttribute(md_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fsmem)));
+    allow_max_smem(md_fast_kernel, ctx.device);
     MP_KERNEL(ctx, md_fast_kernel<<<nn, kMdThreads, fsmem, s>>>(a));
     int32_t h_flag = 0;
     MP_CUDA(cudaMemcpyAsync(&h_flag, overflow.get(), 4, cudaMemcpyDeviceToHost, s));

@@ -12,6 +12,7 @@ struct mp_context {
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
   int num_sms = 148;
+  int smem_optin = 232448;  // cudaDevAttrMaxSharedMemoryPerBlockOptin
   int64_t launches = 0;  // kernels launched through this context (cumulative)
   cudaEvent_t ev[8] = {};
   // pinned staging for host-memory arguments

@@ -5,7 +5,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <string>
+#include <unordered_set>
 
 #include "mp_internal.h"
 
@@ -151,6 +153,26 @@ __host__ __device__ inline int32_t tree_level(int32_t idx) {
   int32_t l = 0;
   for (uint32_t x = static_cast<uint32_t>(idx) + 1; x > 1; x >>= 1) ++l;
   return l;
+}
+
+// Raise a kernel's dynamic shared memory limit to the device maximum, once
+// per kernel.  The attribute is process-wide, so it is never sized per call:
+// concurrent contexts (FramePool threads) launching the same kernel with
+// different dynamic sizes would otherwise race on it.
+template <class K>
+inline void allow_max_smem(K* kernel, int device) {
+  static std::mutex mu;
+  static std::unordered_set<uint64_t> done;
+  const uint64_t key = reinterpret_cast<uint64_t>(reinterpret_cast<const void*>(kernel)) ^ (uint64_t(device) << 56);
+  std::lock_guard<std::mutex> g(mu);
+  if (done.count(key)) return;
+  int optin = 0;
+  MP_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  cudaFuncAttributes fa{};
+  MP_CUDA(cudaFuncGetAttributes(&fa, kernel));
+  MP_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               optin - static_cast<int>(fa.sharedSizeBytes)));
+  done.insert(key);
 }
 
 // Stream-ordered scratch buffer (cudaMallocAsync from the context pool).

@@ -1192,7 +1192,12 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
         const int64_t e_i = (hfo[i + 1] - hfo[i]) - np_i;
         need = std::max<size_t>(need, static_cast<size_t>(np_i) * kFmBytesPerPatch + 4 * e_i + 1024);
       }
-      fm_smem = std::min<size_t>(std::max(fm_smem, need), 227 * 1024);
+      // opt-in limit minus the kernels' static shared memory
+      cudaFuncAttributes fa32{}, fa64{};
+      MP_CUDA(cudaFuncGetAttributes(&fa32, fm_kernel<uint32_t>));
+      MP_CUDA(cudaFuncGetAttributes(&fa64, fm_kernel<uint64_t>));
+      const size_t cap = static_cast<size_t>(ctx.smem_optin) - std::max(fa32.sharedSizeBytes, fa64.sharedSizeBytes);
+      fm_smem = std::min<size_t>(std::max(fm_smem, need), cap);
     }
     a.fm_smem_bytes = static_cast<int64_t>(fm_smem);
     // 32-bit move keys when every node fits (patch count and gain range)
@@ -1206,12 +1211,12 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     }
     const bool k32 = maxnp < 65536 && hgb < 32768;
     if (k32) {
-      MP_CUDA(cudaFuncSetAttribute(fm_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fm_smem)));
+      allow_max_smem(fm_kernel<uint32_t>, ctx.device);
       const int kt__ = ctx.ktime_begin(kKFm);
       MP_KERNEL(ctx, fm_kernel<uint32_t><<<width, kFmThreads, fm_smem, s>>>(a));
       ctx.ktime_end(kt__);
     } else {
-      MP_CUDA(cudaFuncSetAttribute(fm_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fm_smem)));
+      allow_max_smem(fm_kernel<uint64_t>, ctx.device);
       const int kt__ = ctx.ktime_begin(kKFm);
       MP_KERNEL(ctx, fm_kernel<uint64_t><<<width, kFmThreads, fm_smem, s>>>(a));
       ctx.ktime_end(kt__);
@@ -1219,7 +1224,7 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     st.mark("level/fm");
     MP_KERNEL(ctx, super_pass<<<lgrid, 256, 0, s>>>(a));
     const size_t ref_smem = static_cast<size_t>(kRefSmemList) * 10;
-    MP_CUDA(cudaFuncSetAttribute(refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ref_smem)));
+    allow_max_smem(refine_kernel, ctx.device);
     { const int kt__ = ctx.ktime_begin(kKRefine); MP_KERNEL(ctx, refine_kernel<<<width, kNodeThreads, ref_smem, s>>>(a)); ctx.ktime_end(kt__); }
     st.mark("level/super+refine");
     // next level

@@ -1106,7 +1106,7 @@ int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, ui
     } else {
       fa.ell = ell;
       const size_t fps_smem = sizeof(int32_t) * (2 * kFrontCap + kSmemTileWords);
-      MP_CUDA(cudaFuncSetAttribute(fps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fps_smem)));
+      allow_max_smem(fps_kernel, ctx.device);
       { const int kt__ = ctx.ktime_begin(kKFps); MP_KERNEL(ctx, fps_kernel<<<C, kFpsThreads, fps_smem, s>>>(fa)); ctx.ktime_end(kt__); }
     }
 
