@@ -25,6 +25,7 @@ namespace {
 
 constexpr int kFmPasses = 10;        // partition.cpp:13
 constexpr double kBalanceTol = 1.2;  // partition.hpp:34
+constexpr bool kFmProf = false;  // clock64 split of the FM move loop into work[13..15] (li == 0 CTAs)
 constexpr int kMaxNdLevel = 24;      // etree.cpp:16
 constexpr int kNodeThreads = 1024;
 constexpr int32_t kGainBias = 0x40000000;
@@ -226,9 +227,14 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
   int32_t* moves = a.fm_moves + pbeg;
   int64_t* rec = a.fm_rec + 3LL * pbeg;
 
-  extern __shared__ uint64_t fm_sm64[];
+  extern __shared__ uint64_t fm_sm64_[];
   const bool in_smem = np <= kFmSmemPatches;
   const int32_t nb_ = (np + 31) / 32;
+  // super-blocks (32 blocks = 1024 patches) always in shared memory
+  const int32_t nsb = (nb_ + 31) / 32;
+  K* sbk = reinterpret_cast<K*>(fm_sm64_);                          // 2*nsb keys
+  int32_t* sbw = reinterpret_cast<int32_t*>(fm_sm64_ + 2 * nsb);   // 2*nsb min weights
+  uint64_t* fm_sm64 = fm_sm64_ + 3 * nsb;
   K* bk = in_smem ? reinterpret_cast<K*>(fm_sm64) : reinterpret_cast<K*>(a.fm_bm + 2LL * ((pbeg >> 5) + li));  // block max keys, 2 sides
   int32_t* bwt = in_smem ? reinterpret_cast<int32_t*>(fm_sm64 + 2 * nb_) : a.fm_bw + 2LL * ((pbeg >> 5) + li);
   int32_t* fm_sm = reinterpret_cast<int32_t*>(fm_sm64 + 2 * nb_ + nb_);  // after 2*nb keys + 2*nb ints
@@ -262,7 +268,7 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
   uint32_t* packed = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(side + 2 * np) + 15) & ~uintptr_t(15));
   const int64_t e_node = (a.fm_fifo_off[li + 1] - a.fm_fifo_off[li]) - np;
   const bool adj_smem = in_smem && np < 65536 &&
-                        static_cast<int64_t>(reinterpret_cast<uint8_t*>(packed + e_node) - reinterpret_cast<uint8_t*>(fm_sm64)) +
+                        static_cast<int64_t>(reinterpret_cast<uint8_t*>(packed + e_node) - reinterpret_cast<uint8_t*>(fm_sm64_)) +
                         16 <= a.fm_smem_bytes;
   if (adj_smem) {
     int32_t run = 0;
@@ -390,30 +396,51 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
       w0 = __reduce_min_sync(0xffffffffu, w0), w1 = __reduce_min_sync(0xffffffffu, w1);
       if (lane == 0) bk[b] = k0, bk[nblk + b] = k1, bwt[b] = w0, bwt[nblk + b] = w1;
     };
+    // super-block summary of super-block sb (one warp; block summaries written)
+    auto super_sum = [&](int32_t sb) {
+      const int32_t b = sb * 32 + lane;
+      K k0 = 0, k1 = 0;
+      int32_t w0 = INT32_MAX, w1 = INT32_MAX;
+      if (b < nblk) k0 = bk[b], k1 = bk[nblk + b], w0 = bwt[b], w1 = bwt[nblk + b];
+      k0 = FmKey<K>::wmax(k0), k1 = FmKey<K>::wmax(k1);
+      w0 = __reduce_min_sync(0xffffffffu, w0), w1 = __reduce_min_sync(0xffffffffu, w1);
+      if (lane == 0) sbk[sb] = k0, sbk[nsb + sb] = k1, sbw[sb] = w0, sbw[nsb + sb] = w1;
+    };
     for (int32_t b = wid; b < nblk; b += nw) block_sum(b);
+    __syncthreads();
+    for (int32_t sb = wid; sb < nsb; sb += nw) super_sum(sb);
     __syncthreads();
     if (wid == 0) {
       const int64_t pass_cut = s_cut;
       int64_t sw0 = s_sw[0], sw1 = s_sw[1], cut = s_cut;
       const double pass_imb = imbalance_of(sw0, sw1);
       int64_t best_cut = pass_cut;
+      // Divisions are lazy: thr = max(tol, imbalance) is needed only when the
+      // division-free feasibility test fails, and the best prefix's imbalance
+      // only on a cut tie.
       double best_imb = pass_imb, thr = kBalanceTol > pass_imb ? kBalanceTol : pass_imb;
+      bool thr_ok = true, best_imb_ok = true;
+      int64_t best_s0 = sw0, best_s1 = sw1;
       int32_t nm = 0, best_len = 0;
+      auto get_thr = [&]() {
+        if (!thr_ok) {
+          const double imb = imbalance_of(sw0, sw1);
+          thr = kBalanceTol > imb ? kBalanceTol : imb;
+          thr_ok = true;
+        }
+        return thr;
+      };
       // exact feasibility predicate of moving weight wi off side sd
       auto pred = [&](int64_t wi, int32_t sd) {
         const int64_t ns = (sd ? sw1 : sw0) - wi, nt = (sd ? sw0 : sw1) + wi;
-        return ns > 0 && !(imbalance_of(ns, nt) > thr);
+        return ns > 0 && !(imbalance_of(ns, nt) > get_thr());
       };
-      long long c_w = 0, c_s = 0, c_u = 0;
+      long long pc_sel = 0, pc_upd = 0, pc_t0 = 0, pc_t1 = 0;
       for (;;) {
-        long long c0 = clock64();
-        // Feasible weights of a side form [0, W_s]: the ratio falls until the
-        // sides cross and rises after, and the rounded division is monotone.
-        // W_s from the real-valued estimate, fixed up with exact predicates
-        // evaluated in parallel lanes (lanes 0-1 side 0, lanes 2-3 side 1).
+        if (kFmProf) pc_t0 = clock64();
         // side tops
         K t0 = 0, t1 = 0;
-        for (int32_t b = lane; b < nblk; b += 32) t0 = max(t0, bk[b]), t1 = max(t1, bk[nblk + b]);
+        for (int32_t b = lane; b < nsb; b += 32) t0 = max(t0, sbk[b]), t1 = max(t1, sbk[nsb + b]);
         t0 = FmKey<K>::wmax(t0), t1 = FmKey<K>::wmax(t1);
         if ((t0 | t1) == 0) break;
         // Feasibility.  Moving w off the heavier side with 2w <= S - T lowers the
@@ -444,8 +471,6 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
             }
           }
         }
-        long long c1 = clock64();
-        c_w += c1 - c0;
         if (fail_side >= 0) {
           for (int sd = 0; sd < 2; ++sd) {
             if (fail_side != 2 && sd != fail_side) continue;
@@ -454,6 +479,7 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
             // W_s: lanes 0-15 probe a window around the real-valued estimate
             const int64_t S = sd ? sw1 : sw0, T = sd ? sw0 : sw1;
             int64_t est = S - 1;
+            get_thr();
             if (!isinf(thr)) {
               const float tf = static_cast<float>(thr);
               const float e = __fdividef(tf * static_cast<float>(S) - static_cast<float>(T), 1.0f + tf);
@@ -473,24 +499,31 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
             } else {
               W = est - 7 + (32 - __clz(static_cast<int>(m))) - 1;
             }
-            for (int32_t b0 = 0; b0 < nblk; b0 += 32) {
-              const int32_t b = b0 + lane;
-              const bool maybe = b < nblk && bk[sd * nblk + b] > best && bwt[sd * nblk + b] <= W;
-              uint32_t cand = __ballot_sync(0xffffffffu, maybe);
-              while (cand) {
-                const int32_t bb = b0 + __ffs(cand) - 1;
-                cand &= cand - 1;
-                if (bk[sd * nblk + bb] <= best) continue;
-                const int32_t i = bb * 32 + lane;
-                K k = 0;
-                if (i < np && !flag[i] && side[i] == sd && w[i] <= W) k = leaf_key(i);
-                best = max(best, FmKey<K>::wmax(k));
+            for (int32_t s0 = 0; s0 < nsb; s0 += 32) {
+              const int32_t sb = s0 + lane;
+              const bool smaybe = sb < nsb && sbk[sd * nsb + sb] > best && sbw[sd * nsb + sb] <= W;
+              uint32_t scand = __ballot_sync(0xffffffffu, smaybe);
+              while (scand) {
+                const int32_t ss = s0 + __ffs(scand) - 1;
+                scand &= scand - 1;
+                if (sbk[sd * nsb + ss] <= best) continue;
+                const int32_t b = ss * 32 + lane;
+                const bool maybe = b < nblk && bk[sd * nblk + b] > best && bwt[sd * nblk + b] <= W;
+                uint32_t cand = __ballot_sync(0xffffffffu, maybe);
+                while (cand) {
+                  const int32_t bb = ss * 32 + __ffs(cand) - 1;
+                  cand &= cand - 1;
+                  if (bk[sd * nblk + bb] <= best) continue;
+                  const int32_t i = bb * 32 + lane;
+                  K k = 0;
+                  if (i < np && !flag[i] && side[i] == sd && w[i] <= W) k = leaf_key(i);
+                  best = max(best, FmKey<K>::wmax(k));
+                }
               }
             }
           }
         }
-        long long c2 = clock64();
-        c_s += c2 - c1;
+        if (kFmProf) pc_t1 = clock64(), pc_sel += pc_t1 - pc_t0;
         if (best == 0) break;
         const int32_t ch = FmKey<K>::id(best);
         const int32_t gch = gain[ch];
@@ -524,8 +557,13 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
               const int32_t delta = side[nb] == sc ? -2 * wj : 2 * wj;
               gain[nb] += delta;
               const int32_t slot = side[nb] * nblk + (nb >> 5);
-              if (delta > 0) FmKey<K>::amax(&bk[slot], leaf_key(nb));
-              else if (delta < 0 && bk[slot] == oldk) rb = nb >> 5;
+              if (delta > 0) {
+                const K nk = leaf_key(nb);
+                FmKey<K>::amax(&bk[slot], nk);
+                FmKey<K>::amax(&sbk[side[nb] * nsb + (nb >> 10)], nk);
+              } else if (delta < 0 && bk[slot] == oldk) {
+                rb = nb >> 5;
+              }
             }
           }
           __syncwarp();
@@ -535,22 +573,36 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
             const int32_t l = __ffs(todo) - 1;
             todo &= todo - 1;
             const int32_t blk = __shfl_sync(0xffffffffu, rb, l);
-            if (blk != last && blk != (ch >> 5)) block_sum(blk);
+            if (blk != last && blk != (ch >> 5)) {
+              block_sum(blk);
+              __syncwarp();
+              super_sum(blk >> 5);
+            }
             last = blk;
           }
         }
         block_sum(ch >> 5);
-        const double imb = imbalance_of(sw0, sw1);
-        if (cut < best_cut || (cut == best_cut && imb < best_imb)) {
-          best_cut = cut;
-          best_imb = imb;
-          best_len = nm;
-        }
-        thr = kBalanceTol > imb ? kBalanceTol : imb;
         __syncwarp();
-        c_u += clock64() - c2;
+        super_sum(ch >> 10);
+        if (cut < best_cut) {
+          best_cut = cut;
+          best_len = nm;
+          best_s0 = sw0, best_s1 = sw1, best_imb_ok = false;
+        } else if (cut == best_cut) {
+          const double imb = imbalance_of(sw0, sw1);
+          if (!best_imb_ok) best_imb = imbalance_of(best_s0, best_s1), best_imb_ok = true;
+          if (imb < best_imb) best_imb = imb, best_len = nm, best_s0 = sw0, best_s1 = sw1;
+        }
+        thr_ok = false;
+        __syncwarp();
+        if (kFmProf) pc_upd += clock64() - pc_t1;
       }
-      (void)c_w, (void)c_s, (void)c_u;
+      if (kFmProf && lane == 0 && li == 0) {
+        atomicAdd(&a.stats[12], static_cast<unsigned long long>(nm));
+        atomicAdd(&a.stats[13], static_cast<unsigned long long>(pc_sel));
+        atomicAdd(&a.stats[14], static_cast<unsigned long long>(pc_upd));
+      }
+      if (!best_imb_ok) best_imb = imbalance_of(best_s0, best_s1);
       if (lane == 0) {
         s_nm = nm;
         s_best_len = best_len;
@@ -1190,7 +1242,8 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
         const int64_t np_i = hpo[i + 1] - hpo[i];
         if (np_i == 0 || np_i > kFmSmemPatches) continue;
         const int64_t e_i = (hfo[i + 1] - hfo[i]) - np_i;
-        need = std::max<size_t>(need, static_cast<size_t>(np_i) * kFmBytesPerPatch + 4 * e_i + 1024);
+        need = std::max<size_t>(need, static_cast<size_t>(np_i) * kFmBytesPerPatch + 4 * e_i + 1024 +
+                                          24 * static_cast<size_t>((np_i + 1023) / 1024));
       }
       // opt-in limit minus the kernels' static shared memory
       cudaFuncAttributes fa32{}, fa64{};

@@ -85,10 +85,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also the 1M-vertex C2 golden (~1 min)")
     ap.add_argument("--c5", action="store_true", help="only the 2M-vertex C5 golden (3x3 blocks)")
+    ap.add_argument("--c3", action="store_true", help="only the 10M-vertex C3 torus golden (~15 min)")
     args = ap.parse_args()
     R = Reference()
     if args.c5:
         return make_c5(R)
+    if args.c3:
+        return make_big(R, "c3", lambda: mp.mesh_to_graph(mp.make_torus_mesh(2000, 5000)))
     arrays = {}
     for name, (build, patch, L, mode, lo) in SMALL.items():
         g = build()
@@ -111,19 +114,31 @@ def main():
     if args.big:
         big.append(("c2", lambda: mp.mesh_to_graph(mp.make_icosphere_mesh(316))))
     for name, build in big:
-        g = build()
-        t0 = time.time()
-        r = run_case(R, g, 256, -1, 0, 0)
-        off = r["node_offsets"]
-        gold[name] = {"n": g.n, "edges": g.edge_count(), "patch_count": r["patch_count"], "nd_level": r["nd_level"],
-                      "root_separator": int(off[1] - off[0]), "nnz_A": r["nnz_A"], "nnz_L": r["nnz_L"],
-                      "cost": r["cost"], "sha_assignment": digest(r["assignment"]),
-                      "sha_node_offsets": digest(off), "sha_node_vertices": digest(r["node_vertices"]),
-                      "sha_local_perm": digest(r["local_perm"]), "sha_perm": digest(r["perm"]),
-                      "sha_column_counts": digest(r["column_counts"]), "sha_parents": digest(r["parents"]),
-                      "reference_s": round(time.time() - t0, 1)}
+        gold[name] = big_entry(R, build)
         print(name, gold[name])
     gold_path.write_text(json.dumps(gold, indent=1) + "\n")
+
+
+def make_big(R, name, build):
+    gold_path = HERE / "bench_golden.json"
+    gold = json.loads(gold_path.read_text())
+    gold[name] = big_entry(R, build)
+    print(name, gold[name])
+    gold_path.write_text(json.dumps(gold, indent=1) + "\n")
+
+
+def big_entry(R, build):
+    g = build()
+    t0 = time.time()
+    r = run_case(R, g, 256, -1, 0, 0, threads=16)
+    off = r["node_offsets"]
+    return {"n": g.n, "edges": g.edge_count(), "patch_count": r["patch_count"], "nd_level": r["nd_level"],
+            "root_separator": int(off[1] - off[0]), "nnz_A": r["nnz_A"], "nnz_L": r["nnz_L"],
+            "cost": r["cost"], "sha_assignment": digest(r["assignment"]),
+            "sha_node_offsets": digest(off), "sha_node_vertices": digest(r["node_vertices"]),
+            "sha_local_perm": digest(r["local_perm"]), "sha_perm": digest(r["perm"]),
+            "sha_column_counts": digest(r["column_counts"]), "sha_parents": digest(r["parents"]),
+            "reference_s": round(time.time() - t0, 1)}
 
 
 def make_c5(R, b=3):

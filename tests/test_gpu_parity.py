@@ -275,3 +275,18 @@ def test_frame_pool_concurrent_frames_match():
         o = R.order(g, patch_size=64)
         assert np.array_equal(r.perm.perm, o["perm"])
         assert r.fill.nnz_L == R.elimination_fill(g, o["perm"])["nnz_L"]
+
+
+@pytest.mark.parametrize("rows,patch", [(240, 4), (150, 2)])
+def test_fm_large_nodes_global_state(rows, patch):
+    """Root quotients beyond the shared-memory FM capacity (>10,240 patches,
+    C3 has 39,063) take the global-state path with super-block summaries."""
+    from oracle.oracle import Restatement
+    R = Restatement()
+    g = mp.mesh_to_graph(mp.make_grid_mesh(rows, rows))
+    o = R.order(g, patch_size=patch)
+    res = mp.order(g, patch_size=patch)
+    assert o["patch_count"] > 10240 and res.patch.patch_count == o["patch_count"]
+    assert np.array_equal(res.tree.node_offsets, o["node_offsets"])
+    assert np.array_equal(res.tree.vertices, o["node_vertices"])
+    assert np.array_equal(res.perm.perm, o["perm"])
