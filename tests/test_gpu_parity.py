@@ -212,11 +212,13 @@ def check_tree_properties(g, res):
     assert int(res.fill.column_counts.sum()) == res.fill.nnz_L
 
 
-@pytest.mark.parametrize("name", ["c1", "ico158", "c2"])
+@pytest.mark.parametrize("name", ["c1", "ico158", "c2", "c3"])
 def test_baseline_configs_match_reference_digests(name):
     gold = json.loads((GOLDEN / "bench_golden.json").read_text())[name]
     if name == "c1":
         g = mp.mesh_to_graph(mp.make_grid_mesh(64, 64))
+    elif name == "c3":  # 10M-vertex torus (reference: 758 s on 8 cores)
+        g = mp.mesh_to_graph(mp.make_torus_mesh(2000, 5000))
     else:
         g = mp.mesh_to_graph(mp.make_icosphere_mesh(158 if name == "ico158" else 316))
     res = mp.order(g)
