@@ -438,6 +438,105 @@ def run_c4(args):
     return 0
 
 
+def run_c3(args):
+    """configs[2]: 10M-vertex torus, local orderings sharded across ranks
+    (paper_2602_00898_b200/subtree.py).  Every rank runs patching + the ND tree
+    on its device-resident CSR, orders its subtrees, and one all-gather
+    assembles the permutation.  value = device ms of the whole step, max over
+    ranks."""
+    import ctypes as C
+    import torch
+    import paper_2602_00898_b200 as mp
+    from paper_2602_00898_b200 import subtree as st
+    from paper_2602_00898_b200._lib import MpCsr, check, lib
+
+    ws, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    g = load_graph("c3")
+    n = g.n
+    L = mp.default_nd_level(n)
+    nn = (1 << (L + 1)) - 1
+    ctx = mp.Context(local)
+    stream = torch.cuda.Stream(device=dev)
+    ctx.set_stream(stream.cuda_stream)
+    d_off = torch.from_numpy(g.offsets).to(dev)
+    d_nbr = torch.from_numpy(g.neighbors).to(dev)
+    patch_of = torch.empty(n, dtype=torch.int32, device=dev)
+    node_off = torch.empty(nn + 1, dtype=torch.int32, device=dev)
+    node_verts = torch.empty(n, dtype=torch.int32, device=dev)
+    lp = torch.zeros(n, dtype=torch.int32, device=dev)
+    perm = torch.zeros(n, dtype=torch.int32, device=dev)
+    inv = torch.empty(n, dtype=torch.int32, device=dev)
+    mask = torch.empty(nn, dtype=torch.uint8, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    csr = MpCsr(n, C.c_void_p(d_off.data_ptr()), C.c_void_p(d_nbr.data_ptr()), 1)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+
+    def step():
+        with torch.cuda.stream(stream):
+            flush.fill_(1)
+            ev[0].record(stream)
+            pc = C.c_int32()
+            check(lib().mp_compute_patches(ctx.handle, C.byref(csr), 256, C.c_uint64(0),
+                                           C.c_void_p(patch_of.data_ptr()), 1, C.byref(pc)))
+            ev[1].record(stream)
+            check(lib().mp_build_etree(ctx.handle, C.byref(csr), C.c_void_p(patch_of.data_ptr()), pc.value, L,
+                                       C.c_uint64(0), C.c_void_p(node_off.data_ptr()),
+                                       C.c_void_p(node_verts.data_ptr()), 1))
+            ev[2].record(stream)
+            h_off = node_off.cpu().numpy()
+            own = st.owners(h_off, L, ws)
+            mask.copy_(torch.from_numpy((own == rank).astype(np.uint8)))
+            st.order_subtrees_device(ctx, n, d_off.data_ptr(), d_nbr.data_ptr(), L, node_off.data_ptr(),
+                                     node_verts.data_ptr(), mask.data_ptr(), lp.data_ptr(), perm.data_ptr())
+            ev[3].record(stream)
+            st.gather_perm(perm, h_off, L, own, ws, rank)
+            inv.scatter_(0, perm.long(), torch.arange(n, dtype=torch.int32, device=dev))
+            ev[4].record(stream)
+        stream.synchronize()
+        return [ev[i].elapsed_time(ev[i + 1]) for i in range(4)], own
+
+    for _ in range(args.warmup):
+        step()
+    barrier(ws)
+    rows = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            parts, own = step()
+            rows.append(parts)
+    barrier(ws)
+    rows = np.array(rows)
+    ms = max_over_ranks(float(rows.sum(1).mean()), ws)
+    parts = [max_over_ranks(float(x), ws) for x in rows.mean(0)]
+    gold = golden("c3")
+    import hashlib
+    sha = hashlib.sha256(perm.cpu().numpy().tobytes()).hexdigest()[:16]
+    if rank == 0:
+        sizes = np.diff(node_off.cpu().numpy())
+        line = {
+            "metric": "C3 sharded permutation ms (device-timed, 10M-vertex torus)", "value": round(ms, 3),
+            "unit": "ms", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic",
+            "config": {"workload": WORKLOADS["c3"][2], "n": n, "nd_level": L, "parallelism": f"subtrees{ws}",
+                       "l2_flush": "512 MiB write before every step"},
+            "vertices_per_s": round(n / (ms * 1e-3), 1),
+            "stage_ms_max_over_ranks": {"patch": round(parts[0], 3), "etree": round(parts[1], 3),
+                                        "local+assemble (own subtrees)": round(parts[2], 3),
+                                        "gather+inverse": round(parts[3], 3)},
+            "rank0_vertices_owned": int(sizes[own == 0].sum()),
+            "parity": {"sha_perm": sha, "golden": gold.get("sha_perm") if gold else None,
+                       "match": bool(gold and sha == gold["sha_perm"])},
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -445,6 +544,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS) + ["c4"])
+    ap.add_argument("--c3-unsharded", action="store_true", help="c3 through mp_order (stats, fill) instead")
     ap.add_argument("--c4-workers", type=int, default=8, help="concurrent contexts per GPU for c4")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
@@ -452,6 +552,8 @@ def main():
         return run_reference_arm(args)
     if args.workload == "c4":
         return run_c4(args)
+    if args.workload == "c3" and not args.c3_unsharded:
+        return run_c3(args)
     return run_ours(args)
 
 

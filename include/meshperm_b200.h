@@ -142,6 +142,15 @@ int mp_order_tree_nodes(mp_context* ctx, const mp_csr* g, int32_t nd_level,
                         const int32_t* node_offsets, const int32_t* node_vertices,
                         int32_t mode, int32_t* local_perm, int32_t on_device);
 
+/* Sharded local orderings: order_tree_nodes for the nodes
+ * with node_mask[i] != 0 only, then compute_perm's scatter for those nodes:
+ * local_perm and perm entries of masked nodes are written, all others are
+ * left untouched (another rank owns them).  local_order.hpp:36 +
+ * assemble.hpp:25-38 restricted to a node subset.  node_mask has nn entries. */
+int mp_order_subtrees(mp_context* ctx, const mp_csr* g, int32_t nd_level, const int32_t* node_offsets,
+                      const int32_t* node_vertices, int32_t mode, int32_t schedule, const uint8_t* node_mask,
+                      int32_t* local_perm, int32_t* perm, int32_t on_device);
+
 /* assemble.hpp:25-38 schedule_* + compute_perm */
 int mp_compute_perm(mp_context* ctx, int32_t n, int32_t nd_level, const int32_t* node_offsets,
                     const int32_t* node_vertices, const int32_t* local_perm, int32_t schedule,

@@ -78,6 +78,9 @@ SIGNATURES = [
      [C.c_void_p, C.POINTER(MpCsr), C.c_void_p, C.c_int32, C.c_int32, C.c_uint64, C.c_void_p, C.c_void_p, C.c_int32]),
     ("mp_order_tree_nodes", C.c_int,
      [C.c_void_p, C.POINTER(MpCsr), C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32]),
+    ("mp_order_subtrees", C.c_int,
+     [C.c_void_p, C.POINTER(MpCsr), C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
+      C.c_void_p, C.c_void_p, C.c_int32]),
     ("mp_compute_perm", C.c_int,
      [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
       C.c_int32]),

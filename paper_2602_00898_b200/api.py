@@ -261,6 +261,23 @@ def order_tree_nodes(tree: EliminationTree, g: AdjacencyGraph, mode: str = "appr
     return tree
 
 
+def order_subtrees(tree: EliminationTree, g: AdjacencyGraph, node_mask, local_perm, perm,
+                   mode: str = "approx_md", schedule: str = "postorder", ctx: Context | None = None):
+    """mp_order_subtrees on host arrays: local_perm / perm entries of the masked
+    nodes are written in place (int32 arrays of length n), others untouched."""
+    ctx = ctx or default_context()
+    nn = (1 << (tree.nd_level + 1)) - 1
+    mask = np.ascontiguousarray(node_mask, np.uint8)
+    if mask.shape != (nn,):
+        raise ValueError("node_mask needs one entry per tree node")
+    for a in (local_perm, perm):
+        if a.dtype != np.int32 or a.shape != (g.n,) or not a.flags.c_contiguous:
+            raise ValueError("local_perm / perm must be contiguous int32 arrays of length n")
+    off, verts = _i32(tree.node_offsets), _i32(tree.vertices)
+    check(lib().mp_order_subtrees(ctx.handle, C.byref(_csr(g)), tree.nd_level, _ptr(off), _ptr(verts),
+                                  LOCAL_MODES[mode], SCHEDULES[schedule], _ptr(mask), _ptr(local_perm), _ptr(perm), 0))
+
+
 def compute_perm(tree: EliminationTree, g: AdjacencyGraph, schedule: str = "postorder",
                  ctx: Context | None = None) -> Permutation:  # assemble.hpp:25-38
     ctx = ctx or default_context()

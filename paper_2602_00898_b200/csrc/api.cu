@@ -336,6 +336,47 @@ int mp_order_tree_nodes(mp_context* ctx, const mp_csr* g, int32_t nd_level, cons
   });
 }
 
+int mp_order_subtrees(mp_context* ctx, const mp_csr* g, int32_t nd_level, const int32_t* node_offsets,
+                      const int32_t* node_vertices, int32_t mode, int32_t schedule, const uint8_t* node_mask,
+                      int32_t* local_perm, int32_t* perm, int32_t on_device) {
+  return guarded([&] {
+    if (!ctx) throw Error(MP_EINVAL, "null context");
+    if (nd_level < 0 || nd_level > 24) throw Error(MP_EINVAL, "nd_level out of range");
+    if (mode < 0 || mode > 2) throw Error(MP_EINVAL, "unknown local ordering mode");
+    if (!node_mask || !local_perm || !perm) throw Error(MP_EINVAL, "null node_mask / local_perm / perm");
+    ScopedDevice sd(ctx->device);
+    cudaStream_t s = ctx->stream;
+    GraphView gv;
+    make_view(*ctx, g, gv);
+    const int32_t n = g->n;
+    const int32_t nn = static_cast<int32_t>((1LL << (nd_level + 1)) - 1);
+    DevBuf<int32_t> h1, h2, node_of(std::max(n, 1), s);
+    DevBuf<uint8_t> h3;
+    const int32_t* off = input_ptr(*ctx, node_offsets, nn + 1, on_device != 0, h1);
+    const int32_t* verts = input_ptr(*ctx, node_vertices, n, on_device != 0, h2);
+    const uint8_t* mask = input_ptr(*ctx, node_mask, nn, on_device != 0, h3);
+    // outputs: entries of unmasked nodes are left as the caller had them
+    DevBuf<int32_t> lp_h, pm_h;
+    int32_t* lp = local_perm;
+    int32_t* pm = perm;
+    if (!on_device) {
+      lp_h.alloc(std::max(n, 1), s);
+      pm_h.alloc(std::max(n, 1), s);
+      MP_CUDA(cudaMemcpyAsync(lp_h.get(), local_perm, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+      MP_CUDA(cudaMemcpyAsync(pm_h.get(), perm, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+      lp = lp_h, pm = pm_h;
+    }
+    node_of_from_tree_dev(*ctx, n, nn, off, verts, node_of);
+    order_tree_nodes_dev(*ctx, gv.g, nd_level, node_of, off, verts, mode, lp, mask);
+    compute_perm_partial_dev(*ctx, n, nd_level, off, verts, lp, schedule, mask, pm);
+    if (!on_device) {
+      MP_CUDA(cudaMemcpyAsync(local_perm, lp, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+      MP_CUDA(cudaMemcpyAsync(perm, pm, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+    }
+    MP_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
 int mp_compute_perm(mp_context* ctx, int32_t n, int32_t nd_level, const int32_t* node_offsets,
                     const int32_t* node_vertices, const int32_t* local_perm, int32_t schedule, int32_t* perm,
                     int32_t* inverse, int32_t on_device) {

@@ -31,8 +31,9 @@ __global__ void fill_neg(int64_t n, int32_t* a) {
 // perm[b*(pos+j)+t] = b*vertices[local_perm[j]] + t ; inverse likewise.
 __global__ void scatter_perm(int32_t nn, const int32_t* node_offsets, const int32_t* node_vertices,
                              const int32_t* local_perm, const int32_t* node_pos, int32_t n, int32_t b,
-                             int32_t* perm, int32_t* inverse, int32_t* bad) {
+                             const uint8_t* node_mask, int32_t* perm, int32_t* inverse, int32_t* bad) {
   for (int32_t node = blockIdx.x; node < nn; node += gridDim.x) {
+    if (node_mask && !node_mask[node]) continue;
     const int32_t o = node_offsets[node], sz = node_offsets[node + 1] - o, pos = node_pos[node];
     for (int32_t j = threadIdx.x; j < sz; j += blockDim.x) {
       const int32_t lp = local_perm[o + j];
@@ -48,7 +49,7 @@ __global__ void scatter_perm(int32_t nn, const int32_t* node_offsets, const int3
       for (int32_t t = 0; t < b; ++t) {
         const int32_t newpos = b * (pos + j) + t, old = b * v + t;
         perm[newpos] = old;
-        if (atomicExch(&inverse[old], newpos) != -1) atomicExch(bad, 2);
+        if (inverse && atomicExch(&inverse[old], newpos) != -1) atomicExch(bad, 2);
       }
     }
   }
@@ -127,7 +128,7 @@ void compute_perm_blocks_dev(mp_context& ctx, int32_t n, int32_t L, const int32_
   MP_KERNEL(ctx, fill_neg<<<static_cast<int>(std::min<int64_t>(ceil_div(std::max<int64_t>(N, 1), 256), ctx.num_sms * 16LL)),
                            256, 0, s>>>(N, inverse));
   MP_KERNEL(ctx, scatter_perm<<<std::min(nn, 8192), 256, 0, s>>>(nn, node_offsets, node_vertices, local_perm,
-                                                                 node_pos_dev, n, b, perm, inverse, bad));
+                                                                 node_pos_dev, n, b, nullptr, perm, inverse, bad));
   int32_t h_bad = 0;
   MP_CUDA(cudaMemcpyAsync(&h_bad, bad, 4, cudaMemcpyDeviceToHost, s));
   MP_CUDA(cudaStreamSynchronize(s));
@@ -139,6 +140,30 @@ void compute_perm_dev(mp_context& ctx, int32_t n, int32_t L, const int32_t* node
                       const int32_t* node_vertices, const int32_t* local_perm, int32_t schedule, int32_t* perm,
                       int32_t* inverse, int32_t* node_pos) {
   compute_perm_blocks_dev(ctx, n, L, node_offsets, node_vertices, local_perm, schedule, 1, perm, inverse, node_pos);
+}
+
+void compute_perm_partial_dev(mp_context& ctx, int32_t n, int32_t L, const int32_t* node_offsets,
+                              const int32_t* node_vertices, const int32_t* local_perm, int32_t schedule,
+                              const uint8_t* node_mask, int32_t* perm) {
+  cudaStream_t s = ctx.stream;
+  const int32_t nn = static_cast<int32_t>((1LL << (L + 1)) - 1);
+  std::vector<int32_t> hoff(nn + 1);
+  MP_CUDA(cudaMemcpyAsync(hoff.data(), node_offsets, sizeof(int32_t) * (nn + 1), cudaMemcpyDeviceToHost, s));
+  MP_CUDA(cudaStreamSynchronize(s));
+  for (int32_t i = 0; i < nn; ++i)
+    if (hoff[i + 1] < hoff[i]) throw Error(MP_EINVAL, "tree node offsets are not monotone");
+  if (hoff[nn] - hoff[0] != n || hoff[0] != 0)
+    throw Error(MP_EINVAL, "tree vertex lists do not cover the graph");
+  std::vector<int32_t> pos = node_positions(hoff, L, schedule);
+  DevBuf<int32_t> pos_dev(nn + 1, s), bad(1, s);
+  MP_CUDA(cudaMemcpyAsync(pos_dev, pos.data(), sizeof(int32_t) * (nn + 1), cudaMemcpyHostToDevice, s));
+  MP_CUDA(cudaMemsetAsync(bad, 0, 4, s));
+  MP_KERNEL(ctx, scatter_perm<<<std::min(nn, 8192), 256, 0, s>>>(nn, node_offsets, node_vertices, local_perm, pos_dev,
+                                                                 n, 1, node_mask, perm, nullptr, bad));
+  int32_t h_bad = 0;
+  MP_CUDA(cudaMemcpyAsync(&h_bad, bad, 4, cudaMemcpyDeviceToHost, s));
+  MP_CUDA(cudaStreamSynchronize(s));
+  if (h_bad) throw Error(MP_EINVAL, "permutation entry out of range");
 }
 
 }  // namespace mp

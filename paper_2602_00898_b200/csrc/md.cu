@@ -55,6 +55,7 @@ struct MdArgs {
   int32_t* local_perm;       // output, node_vertices layout
   int32_t* overflow;         // set on pool exhaustion
   int32_t min_nv;            // md_kernel: only nodes with at least this many vertices
+  const uint8_t* node_mask;  // non-null: order only nodes with mask != 0 (sharded C3 path)
 };
 
 __device__ __forceinline__ uint32_t md_key_deg(int64_t d) {
@@ -64,7 +65,7 @@ __device__ __forceinline__ uint32_t md_key_deg(int64_t d) {
 __global__ void __launch_bounds__(kMdThreads) md_kernel(MdArgs a) {
   const int32_t node = blockIdx.x;
   const int32_t vb = a.node_offsets[node], nv = a.node_offsets[node + 1] - vb;
-  if (nv == 0 || nv < a.min_nv) return;
+  if (nv == 0 || nv < a.min_nv || (a.node_mask && !a.node_mask[node])) return;
   const int32_t* verts = a.node_vertices + vb;
   int32_t* lperm = a.local_perm + vb;
   int32_t* order = a.order_ws + vb;
@@ -265,7 +266,7 @@ constexpr int32_t kMdFastCap = 6 * 1024;  // nodes up to this size use the fast 
 __global__ void __launch_bounds__(kMdThreads) md_fast_kernel(MdArgs a) {
   const int32_t node = a.nn - 1 - static_cast<int32_t>(blockIdx.x);  // leaves (the big nodes) first
   const int32_t vb = a.node_offsets[node], nv = a.node_offsets[node + 1] - vb;
-  if (nv == 0 || nv > kMdFastCap) return;
+  if (nv == 0 || nv > kMdFastCap || (a.node_mask && !a.node_mask[node])) return;
   const int32_t* verts = a.node_vertices + vb;
   int32_t* lperm = a.local_perm + vb;
   int32_t* order = a.order_ws + vb;
@@ -447,9 +448,9 @@ __global__ void local_of_kernel(int32_t n, const int32_t* node_of, const int32_t
 }
 // per node pool capacity: 2 halves of (4 * degree sum + 2 * size + 64)
 __global__ void node_pool_need(int32_t nn, const int32_t* node_offsets, const int32_t* node_vertices,
-                               const int32_t* off, int64_t* need) {
+                               const int32_t* off, const uint8_t* node_mask, int64_t* need) {
   for (int32_t node = blockIdx.x; node < nn; node += gridDim.x) {
-    const int32_t b = node_offsets[node], e = node_offsets[node + 1];
+    const int32_t b = node_offsets[node], e = (node_mask && !node_mask[node]) ? b : node_offsets[node + 1];
     int64_t d = 0;
     for (int32_t i = b + threadIdx.x; i < e; i += blockDim.x) {
       const int32_t v = node_vertices[i];
@@ -465,7 +466,7 @@ __global__ void node_pool_need(int32_t nn, const int32_t* node_offsets, const in
 
 void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t L, const int32_t* node_of,
                           const int32_t* node_offsets, const int32_t* node_vertices, int32_t mode,
-                          int32_t* local_perm) {
+                          int32_t* local_perm, const uint8_t* node_mask) {
   cudaStream_t s = ctx.stream;
   const int32_t n = g.n;
   const int32_t nn = static_cast<int32_t>((1LL << (L + 1)) - 1);
@@ -480,7 +481,7 @@ void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t L, const int
   DevBuf<int32_t> adj(std::max(m2, 1), s), el(std::max(m2, 1), s);
   MP_KERNEL(ctx, local_of_kernel<<<grid_for(ctx, n), 256, 0, s>>>(n, node_of, node_offsets, node_vertices, local_of));
   MP_CUDA(cudaMemsetAsync(need, 0, sizeof(int64_t) * (nn + 1), s));
-  MP_KERNEL(ctx, node_pool_need<<<std::min(nn, 4096), 256, 0, s>>>(nn, node_offsets, node_vertices, g.off, need));
+  MP_KERNEL(ctx, node_pool_need<<<std::min(nn, 4096), 256, 0, s>>>(nn, node_offsets, node_vertices, g.off, node_mask, need));
   {
     size_t tmp = 0;
     MP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, need.get(), pool_off.get(), nn + 1, s));
@@ -497,6 +498,7 @@ void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t L, const int
   a.local_of = local_of, a.mode = mode, a.adj = adj, a.el = el, a.nadj = nadj, a.nel = nel;
   a.bptr = bptr, a.bsz = bsz, a.vmark = vmark, a.emark = emark, a.gdeg = gdeg, a.pool = pool;
   a.pool_off = pool_off, a.order_ws = order, a.local_perm = local_perm, a.overflow = overflow;
+  a.node_mask = node_mask;
   const size_t smem = sizeof(uint32_t) * kSmemDegCap;
   allow_max_smem(md_kernel, ctx.device);
   const int kt__ = ctx.ktime_begin(kKMd);

@@ -90,13 +90,19 @@ int64_t build_quotient_dev(mp_context& ctx, const DGraph& g, const int32_t* assi
 // Local ordering (md.cu): local_perm per node, layout of node_vertices.
 void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t nd_level,
                           const int32_t* node_of, const int32_t* node_offsets,
-                          const int32_t* node_vertices, int32_t mode, int32_t* local_perm);
+                          const int32_t* node_vertices, int32_t mode, int32_t* local_perm,
+                          const uint8_t* node_mask = nullptr);
 
 // Assembly (assemble.cu): schedule + perm/inverse.  node_pos (nn+1) receives
 // the first permutation position of every node.
 void compute_perm_dev(mp_context& ctx, int32_t n, int32_t nd_level, const int32_t* node_offsets,
                       const int32_t* node_vertices, const int32_t* local_perm, int32_t schedule,
                       int32_t* perm, int32_t* inverse, int32_t* node_pos);
+// Sharded assembly: perm entries of the masked nodes only (no inverse, no
+// bijection check -- the other ranks own the remaining positions).
+void compute_perm_partial_dev(mp_context& ctx, int32_t n, int32_t nd_level, const int32_t* node_offsets,
+                              const int32_t* node_vertices, const int32_t* local_perm, int32_t schedule,
+                              const uint8_t* node_mask, int32_t* perm);
 
 // Symbolic (symbolic.cu): column counts (by position) and factor etree parents.
 void tree_fill_dev(mp_context& ctx, const DGraph& g, int32_t nd_level, const int32_t* node_of,

@@ -76,3 +76,67 @@ def test_gloo_sharded_frames_match_single_process():
     expect = {f: _order_frame(frames[f]) for f in range(len(frames))}
     assert merged == expect
     assert tmax == 2.0
+
+
+def test_subtree_owners_cover_and_balance():
+    from paper_2602_00898_b200 import subtree as st
+    rng = np.random.default_rng(3)
+    L = 5
+    nn = (1 << (L + 1)) - 1
+    sizes = rng.integers(0, 50, nn)
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+    n = int(off[-1])
+    for world in (1, 2, 3, 5, 8):
+        own = st.owners(off, L, world)
+        cover = np.zeros(n, np.int32)
+        for r in range(world):
+            for s, k in st.rank_ranges(off, L, own, r):
+                cover[s:s + k] += 1
+        assert np.all(cover == 1)
+        # a subtree below level k is owned by one rank
+        k = min(L, int(np.ceil(np.log2(world)))) if world > 1 else 0
+        for i in range(nn):
+            if (i + 1).bit_length() - 1 > k:
+                assert own[i] == own[(i - 1) // 2]
+    # postorder positions equal the schedule scan
+    pos = st.node_positions(off, L)
+    order = st.schedule(L)
+    assert pos[order[0]] == 0 and pos[nn] == n
+
+
+def _gather_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    from paper_2602_00898_b200 import subtree as st
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    L = 4
+    nn = (1 << (L + 1)) - 1
+    sizes = np.random.default_rng(11).integers(0, 30, nn)
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int32)
+    n = int(off[-1])
+    truth = np.random.default_rng(5).permutation(n).astype(np.int32)
+    own = st.owners(off, L, world)
+    perm = torch.full((n,), -1, dtype=torch.int32)
+    for s, k in st.rank_ranges(off, L, own, rank):
+        perm[s:s + k] = torch.from_numpy(truth[s:s + k])
+    st.gather_perm(perm, off, L, own, world, rank)
+    q.put((rank, bool(np.array_equal(perm.numpy(), truth))))
+    dist.destroy_process_group()
+
+
+def test_gloo_subtree_gather_rebuilds_permutation():
+    import multiprocessing as mpx
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mpx.get_context("spawn")
+    q = ctx.Queue()
+    world = 3
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {r: True for r in range(world)}

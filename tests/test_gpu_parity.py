@@ -292,3 +292,28 @@ def test_fm_large_nodes_global_state(rows, patch):
     assert np.array_equal(res.tree.node_offsets, o["node_offsets"])
     assert np.array_equal(res.tree.vertices, o["node_vertices"])
     assert np.array_equal(res.perm.perm, o["perm"])
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_order_subtrees_shards_merge_to_full_order(world):
+    """C3 sharding: every rank orders its subtrees (mp_order_subtrees); the
+    union of the ranks' permutation ranges is the single-GPU permutation, and
+    entries outside a rank's nodes are left untouched."""
+    from paper_2602_00898_b200 import subtree as st
+    g = mp.mesh_to_graph(mp.make_torus_mesh(60, 80))
+    full = mp.order(g, patch_size=32)
+    L = full.tree.nd_level
+    tree = mp.EliminationTree(g.n, L, full.tree.node_offsets, full.tree.vertices)
+    own = st.owners(tree.node_offsets, L, world)
+    merged = np.full(g.n, -1, np.int32)
+    for r in range(world):
+        lp = np.full(g.n, -7, np.int32)
+        pm = np.full(g.n, -7, np.int32)
+        mp.order_subtrees(tree, g, (own == r).astype(np.uint8), lp, pm)
+        ranges = st.rank_ranges(tree.node_offsets, L, own, r)
+        inside = np.zeros(g.n, bool)
+        for s, n in ranges:
+            inside[s:s + n] = True
+            merged[s:s + n] = pm[s:s + n]
+        assert np.all(pm[~inside] == -7)
+    assert np.array_equal(merged, full.perm.perm)
