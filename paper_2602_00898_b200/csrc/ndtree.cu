@@ -25,7 +25,6 @@ namespace {
 
 constexpr int kFmPasses = 10;        // partition.cpp:13
 constexpr double kBalanceTol = 1.2;  // partition.hpp:34
-constexpr bool kFmProf = false;  // clock64 split of the FM move loop into work[13..15] (li == 0 CTAs)
 constexpr int kMaxNdLevel = 24;      // etree.cpp:16
 constexpr int kNodeThreads = 1024;
 constexpr int32_t kGainBias = 0x40000000;
@@ -77,12 +76,9 @@ struct LevelArgs {
   // FM scratch (per patch, in plist layout)
   int32_t* fm_gain;
   int32_t* fm_w;           // global fallback state for nodes beyond kFmSmemPatches
-  uint64_t* fm_lk;
-  uint64_t* fm_bm;
-  int32_t* fm_bw;
   int32_t* fm_ab;
   int32_t* fm_ae;
-  uint8_t* fm_side;        // 2 * P bytes: side then lock flags
+  uint8_t* fm_side;        // 3 * P bytes: side, lock flags, cache slots
   const int32_t* qloc;     // quotient adjacency as node-local patch indices
   int32_t* fm_fifo;        // capacity per node: poff span + edges -> allocated 2*P + E
   const int64_t* fm_fifo_off;  // per level node
@@ -186,36 +182,172 @@ __global__ void quotient_csr(int32_t U, const uint64_t* ukeys, const int32_t* uc
 
 // ---------------------------------------------------------------- FM (one CTA per node)
 // bipartition_quotient, partition.cpp:25-163.  The node's patch state
-// (weight, gain, side, lock, adjacency bounds) lives in shared memory when it
-// fits (global scratch otherwise); the adjacency carries node-local indices
-// (qloc).  A move is the block argmax of (gain desc, id asc) over the feasible
-// unlocked patches -- the first feasible entry of the reference's
-// std::set<(-gain,id)> -- followed by a warp-0 update: two barriers per move.
+// (weight, gain, side, lock, adjacency bounds, cache slot) lives in shared
+// memory when it fits (global scratch otherwise); the adjacency carries
+// node-local indices (qloc).
+//
+// Move selection.  The reference takes the first feasible entry of its
+// std::set<(-gain, id)>: the max key (gain desc, id asc) over the feasible
+// unlocked patches.  The move loop runs in warp 0 alone over a per-side
+// candidate cache: lane l holds entry l of side 0 and entry l of side 1
+// (key, patch, weight), and a bound B_s says every unlocked side-s patch
+// outside the cache has key <= B_s.  The best feasible cached key f_s is the
+// side's answer when f_s > B_s (or nothing is outside); the move is the larger
+// answer provided no side with an unknown answer could beat it (B_s < best).
+// A move changes only its neighbours' keys: cached ones are re-read, raised
+// uncached ones above B_s are inserted (a full cache evicts its minimum into
+// B_s).  When a side's answer is unknown the whole CTA refills that side with
+// its top 32 keys (radix select); if it is still unknown right after a
+// refill, the CTA takes the exact argmax over all patches for one move.  The
+// chosen move is always the reference's; on the C2 root (3,901 patches,
+// 23,406 moves) the cache needs 35 refills.
 constexpr int32_t kFmSmemPatches = 10 * 1024;
-constexpr int kFmBytesPerPatch = 18 + 1;  // + block summaries (24 bytes per 32 patches)
+constexpr int kFmBytesPerPatch = 19;  // w, gain, ab, ae (int32) + side, flag, cache slot (bytes)
 constexpr int kFmThreads = 256;
+constexpr uint8_t kNoSlot = 0xff;
+constexpr int kFmDone = 8, kFmExact = 4;  // segment exit reasons (1, 2: refill side 0 / 1)
 
 // FM move keys (gain desc, id asc): 32-bit when the node has < 65536 patches
-// and |gain| < 32768 (one redux per warp max), 64-bit otherwise.
+// and |gain| < 32768, 64-bit otherwise.  0 is never a key.
 template <class K> struct FmKey;
 template <> struct FmKey<uint32_t> {
   static __device__ __forceinline__ uint32_t make(int32_t gain, int32_t i) {
     return (static_cast<uint32_t>(gain + 32768) << 16) | (0xffffu - static_cast<uint32_t>(i));
   }
   static __device__ __forceinline__ int32_t id(uint32_t k) { return static_cast<int32_t>(0xffffu - (k & 0xffffu)); }
+  static __device__ __forceinline__ int32_t gain(uint32_t k) { return static_cast<int32_t>(k >> 16) - 32768; }
   static __device__ __forceinline__ uint32_t wmax(uint32_t v) { return __reduce_max_sync(0xffffffffu, v); }
-  static __device__ __forceinline__ void amax(uint32_t* p, uint32_t v) { atomicMax(p, v); }
+  static __device__ __forceinline__ uint32_t wmin(uint32_t v) { return __reduce_min_sync(0xffffffffu, v); }
 };
 template <> struct FmKey<uint64_t> {
   static __device__ __forceinline__ uint64_t make(int32_t gain, int32_t i) {
     return key_max(static_cast<uint32_t>(gain + kGainBias), static_cast<uint32_t>(i));
   }
   static __device__ __forceinline__ int32_t id(uint64_t k) { return static_cast<int32_t>(key_max_id(k)); }
-  static __device__ __forceinline__ uint64_t wmax(uint64_t v) { return warp_max_u64(v); }
-  static __device__ __forceinline__ void amax(uint64_t* p, uint64_t v) {
-    atomicMax(reinterpret_cast<unsigned long long*>(p), static_cast<unsigned long long>(v));
+  static __device__ __forceinline__ int32_t gain(uint64_t k) {
+    return static_cast<int32_t>(static_cast<uint32_t>(k >> 32) - static_cast<uint32_t>(kGainBias));
   }
+  static __device__ __forceinline__ uint64_t wmax(uint64_t v) { return warp_max_u64(v); }
+  static __device__ __forceinline__ uint64_t wmin(uint64_t v) { return warp_min_u64(v); }
 };
+
+// imbalance_of(ns, nt) > max(tol, imbalance_of(H, L)) with tol = 1.2, the
+// reference's double test (partition.cpp:114-124), in exact integer form for
+// node weights below 2^26:
+//  * fl(h/l) > fl(1.2) <=> 5h > 6l: a ratio h/l != 6/5 lies at least 1/(5l)
+//    from 6/5, far beyond the rounding of either double;
+//  * fl(h/l) > fl(H/L) <=> hL > Hl: distinct ratios with hL, Hl < 2^52 are
+//    more than one rounding apart, so the rounded doubles keep their order.
+// Infinite ratios (l = 0 or L = 0) come out right: 0 > ... is false.
+static_assert(kBalanceTol == 1.2, "fm_infeasible encodes tol = 6/5");
+constexpr int64_t kFmExactWeights = int64_t(1) << 26;
+__device__ __forceinline__ bool fm_infeasible(int64_t ns, int64_t nt, int64_t H, int64_t L, bool exact_int) {
+  const int64_t h = ns > nt ? ns : nt, l = ns < nt ? ns : nt;
+  if (exact_int) return 5 * h > 6 * l && h * L > H * l;
+  const double cur = imbalance_of(H, L);
+  return imbalance_of(ns, nt) > (kBalanceTol > cur ? kBalanceTol : cur);
+}
+// imbalance_of(a0, a1) < imbalance_of(b0, b1) (the best-prefix tie test)
+__device__ __forceinline__ bool fm_imb_less(int64_t a0, int64_t a1, int64_t b0, int64_t b1, bool exact_int) {
+  const int64_t ah = a0 > a1 ? a0 : a1, al = a0 < a1 ? a0 : a1, bh = b0 > b1 ? b0 : b1, bl = b0 < b1 ? b0 : b1;
+  if (exact_int) return ah * bl < bh * al;
+  return imbalance_of(a0, a1) < imbalance_of(b0, b1);
+}
+
+// CTA-wide: refill the side-t cache with the 32 largest keys of the unlocked
+// side-t patches; B[t] = the 33rd largest (0 when there are at most 32).
+// The threshold is an MSD radix select over the bits below the common prefix
+// of the largest and smallest candidate key.
+template <class K>
+__device__ void fm_refill(int32_t t, int32_t np, const int32_t* gain, const uint8_t* side, const uint8_t* flag,
+                          uint8_t* cslot, K (*ck)[32], int32_t (*cp)[32], K* B, int32_t* hist, uint64_t* red,
+                          int32_t* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (threadIdx.x < 32) {
+    const int32_t p = cp[t][threadIdx.x];
+    if (p >= 0) cslot[p] = kNoSlot;
+    cp[t][threadIdx.x] = -1;
+    ck[t][threadIdx.x] = 0;
+  }
+  int64_t c = 0;
+  uint64_t mx = 0, mn = ~0ull;
+  for (int32_t i = threadIdx.x; i < np; i += blockDim.x)
+    if (!flag[i] && side[i] == t) {
+      const uint64_t k = FmKey<K>::make(gain[i], i);
+      ++c, mx = k > mx ? k : mx, mn = k < mn ? k : mn;
+    }
+  c = block_sum_i64(c, reinterpret_cast<int64_t*>(red));
+  mx = block_max_u64(mx, red);
+  mn = block_min_u64(mn, red);
+  uint64_t T = 0;
+  if (c > 32) {
+    const int hb = 63 - __clzll(static_cast<long long>(mx ^ mn));  // keys are distinct: mx != mn
+    const uint64_t low = hb == 63 ? ~0ull : ((1ull << (hb + 1)) - 1);
+    uint64_t prefix = mx & ~low, pmask = ~low;
+    int32_t rank = 33;
+    for (int lo = hb + 1; lo > 0;) {
+      const int dbits = lo < 8 ? lo : 8;
+      lo -= dbits;
+      const int32_t nbins = 1 << dbits;
+      for (int32_t b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0;
+      __syncthreads();
+      for (int32_t i0 = wid * 32; i0 < np; i0 += nw * 32) {
+        const int32_t i = i0 + lane;
+        int32_t d = -1;
+        if (i < np && !flag[i] && side[i] == t) {
+          const uint64_t k = FmKey<K>::make(gain[i], i);
+          if ((k & pmask) == prefix) d = static_cast<int32_t>((k >> lo) & static_cast<uint64_t>(nbins - 1));
+        }
+        const uint32_t m = __match_any_sync(0xffffffffu, d);
+        if (d >= 0 && lane == __ffs(m) - 1) atomicAdd(&hist[d], __popc(m));
+      }
+      __syncthreads();
+      if (wid == 0) {  // digit holding the rank-th largest: bins from the top
+        int32_t loc = 0;
+        for (int q = 0; q < 8; ++q) {
+          const int32_t b = nbins - 1 - (lane * 8 + q);
+          if (b >= 0) loc += hist[b];
+        }
+        int32_t inc = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += y;
+        }
+        int32_t run = inc - loc;
+        if (run < rank && rank <= inc) {
+          for (int q = 0; q < 8; ++q) {
+            const int32_t b = nbins - 1 - (lane * 8 + q);
+            if (run + hist[b] >= rank) {
+              sh[0] = b, sh[1] = rank - run;
+              break;
+            }
+            run += hist[b];
+          }
+        }
+      }
+      __syncthreads();
+      prefix |= static_cast<uint64_t>(sh[0]) << lo;
+      pmask |= static_cast<uint64_t>(nbins - 1) << lo;
+      rank = sh[1];
+      __syncthreads();
+    }
+    T = prefix;  // the 33rd largest key itself
+  }
+  if (threadIdx.x == 0) sh[2] = 0;
+  __syncthreads();
+  for (int32_t i = threadIdx.x; i < np; i += blockDim.x)
+    if (!flag[i] && side[i] == t) {
+      const K k = FmKey<K>::make(gain[i], i);
+      if (k > T) {
+        const int32_t slot = atomicAdd(&sh[2], 1);
+        ck[t][slot] = k, cp[t][slot] = i;
+        cslot[i] = static_cast<uint8_t>((t << 5) | slot);
+      }
+    }
+  if (threadIdx.x == 0) B[t] = static_cast<K>(T);
+  __syncthreads();
+}
 
 template <class K>
 __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
@@ -229,27 +361,23 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
 
   extern __shared__ uint64_t fm_sm64_[];
   const bool in_smem = np <= kFmSmemPatches;
-  const int32_t nb_ = (np + 31) / 32;
-  // super-blocks (32 blocks = 1024 patches) always in shared memory
-  const int32_t nsb = (nb_ + 31) / 32;
-  K* sbk = reinterpret_cast<K*>(fm_sm64_);                          // 2*nsb keys
-  int32_t* sbw = reinterpret_cast<int32_t*>(fm_sm64_ + 2 * nsb);   // 2*nsb min weights
-  uint64_t* fm_sm64 = fm_sm64_ + 3 * nsb;
-  K* bk = in_smem ? reinterpret_cast<K*>(fm_sm64) : reinterpret_cast<K*>(a.fm_bm + 2LL * ((pbeg >> 5) + li));  // block max keys, 2 sides
-  int32_t* bwt = in_smem ? reinterpret_cast<int32_t*>(fm_sm64 + 2 * nb_) : a.fm_bw + 2LL * ((pbeg >> 5) + li);
-  int32_t* fm_sm = reinterpret_cast<int32_t*>(fm_sm64 + 2 * nb_ + nb_);  // after 2*nb keys + 2*nb ints
+  int32_t* fm_sm = reinterpret_cast<int32_t*>(fm_sm64_);
   int32_t* w = in_smem ? fm_sm : a.fm_w + pbeg;
   int32_t* gain = in_smem ? fm_sm + np : a.fm_gain + pbeg;
   int32_t* ab = in_smem ? fm_sm + 2 * np : a.fm_ab + pbeg;
   int32_t* ae = in_smem ? fm_sm + 3 * np : a.fm_ae + pbeg;
   uint8_t* side = in_smem ? reinterpret_cast<uint8_t*>(fm_sm + 4 * np) : a.fm_side + pbeg;
   uint8_t* flag = side + (in_smem ? np : a.P);  // visited / locked
+  uint8_t* cslot = flag + (in_smem ? np : a.P);  // cache slot (side << 5 | lane) or kNoSlot
 
-  __shared__ uint64_t red[32], red2[64];
-  __shared__ int64_t s_total, s_left, s_cut, s_sw[2], s_best_cut, s_pass_cut;
-  __shared__ double s_thr, s_best_imb, s_pass_imb;
-  __shared__ int32_t s_nm, s_best_len, s_head, s_tail, s_u, s_stop;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __shared__ uint64_t red[32];
+  __shared__ int32_t hist[256], sh[4];
+  __shared__ K s_ck[2][32], s_B[2], s_exact;
+  __shared__ int32_t s_cp[2][32];
+  __shared__ int64_t s_total, s_left, s_cut, s_sw[2], s_best_cut, s_pass_cut, s_best_s[2];
+  __shared__ int64_t s_pass_s[2];
+  __shared__ int32_t s_nm, s_best_len, s_need, s_stop;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 
   int64_t tot = 0;
   int32_t heavy = 0;
@@ -265,7 +393,7 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
   tot = block_sum_i64(tot, reinterpret_cast<int64_t*>(red));
   // node-local adjacency packed (local id << 16 | weight) in shared memory when
   // it fits; otherwise the global arrays (qloc, qw) are read directly
-  uint32_t* packed = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(side + 2 * np) + 15) & ~uintptr_t(15));
+  uint32_t* packed = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(side + 3 * np) + 15) & ~uintptr_t(15));
   const int64_t e_node = (a.fm_fifo_off[li + 1] - a.fm_fifo_off[li]) - np;
   const bool adj_smem = in_smem && np < 65536 &&
                         static_cast<int64_t>(reinterpret_cast<uint8_t*>(packed + e_node) - reinterpret_cast<uint8_t*>(fm_sm64_)) +
@@ -298,40 +426,38 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
   const bool adj_local = adj_smem && !heavy;
   auto A_nb = [&](int32_t j) -> int32_t { return adj_local ? static_cast<int32_t>(packed[j] >> 16) : __ldg(&a.qloc[j]); };
   auto A_w = [&](int32_t j) -> int32_t { return adj_local ? static_cast<int32_t>(packed[j] & 0xffffu) : __ldg(&a.qw[j]); };
-  if (threadIdx.x == 0) s_total = tot, s_left = 0, s_head = 0, s_tail = 0;
-  __syncthreads();
 
-  // ---- greedy growing from the heaviest patch (partition.cpp:53-79)
-  for (;;) {
-    if (s_left * 2 >= s_total) break;
-    if (threadIdx.x == 0) {
-      int32_t h = s_head;
-      while (h < s_tail && flag[fifo[h]]) ++h;
-      s_u = h < s_tail ? fifo[h++] : -1;
-      s_head = h;
-    }
-    __syncthreads();
-    if (s_u < 0) {  // fifo empty: heaviest unvisited patch (weight desc, id asc)
-      uint64_t best = 0;
-      for (int32_t i = threadIdx.x; i < np; i += blockDim.x)
-        if (!flag[i]) {
-          const uint64_t k = key_max(static_cast<uint32_t>(w[i]), static_cast<uint32_t>(i));
-          best = k > best ? k : best;
+  // ---- greedy growing from the heaviest patch (partition.cpp:53-79), warp 0
+  if (wid == 0) {
+    int64_t left = 0;
+    int32_t head = 0, tail = 0;
+    while (left * 2 < tot) {
+      int32_t u = -1;
+      while (head < tail) {  // first unvisited fifo entry
+        const int32_t h = head + lane;
+        const int32_t x = h < tail ? fifo[h] : 0;
+        const uint32_t m = __ballot_sync(0xffffffffu, h < tail && !flag[x]);
+        if (m) {
+          const int l = __ffs(m) - 1;
+          u = __shfl_sync(0xffffffffu, x, l);
+          head += l + 1;
+          break;
         }
-      best = block_max_u64(best, red);
-      if (threadIdx.x == 0) s_u = static_cast<int32_t>(key_max_id(best));
-      __syncthreads();
-    }
-    if (wid == 0) {
-      const int32_t u = s_u;
-      if (lane == 0) {
-        flag[u] = 1;
-        side[u] = 0;
-        s_left += w[u];
+        head = min(head + 32, tail);
       }
+      if (u < 0) {  // fifo empty: heaviest unvisited patch (weight desc, id asc)
+        uint64_t best = 0;
+        for (int32_t i = lane; i < np; i += 32)
+          if (!flag[i]) {
+            const uint64_t k = key_max(static_cast<uint32_t>(w[i]), static_cast<uint32_t>(i));
+            best = k > best ? k : best;
+          }
+        u = static_cast<int32_t>(key_max_id(warp_max_u64(best)));
+      }
+      if (lane == 0) flag[u] = 1, side[u] = 0;
+      left += w[u];
       __syncwarp();
       const int32_t e0 = ab[u], e1 = ae[u];
-      int32_t tail = s_tail;
       for (int32_t j0 = e0; j0 < e1; j0 += 32) {
         const int32_t j = j0 + lane;
         const int32_t nb = j < e1 ? A_nb(j) : 0;
@@ -340,10 +466,11 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
         if (push) fifo[tail + __popc(m & ((1u << lane) - 1))] = nb;
         tail += __popc(m);
       }
-      if (lane == 0) s_tail = tail;
+      __syncwarp();
     }
-    __syncthreads();
+    if (lane == 0) s_left = left;
   }
+  __syncthreads();
   // cut of the grown split (partition.cpp:81-84)
   int64_t cut = 0;
   for (int32_t i = threadIdx.x; i < np; i += blockDim.x)
@@ -353,21 +480,15 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
     }
   cut = block_sum_i64(cut, reinterpret_cast<int64_t*>(red));
   if (threadIdx.x == 0) {
+    s_total = tot;
     s_cut = cut;
     s_sw[0] = s_left;
-    s_sw[1] = s_total - s_left;
+    s_sw[1] = tot - s_left;
   }
   __syncthreads();
 
-  // ---- FM passes with rollback to the best prefix (partition.cpp:95-159).
-  // The move loop runs in warp 0 alone.  Per side s, the unlocked patches of
-  // that side sit under 32-wide blocks holding their max key (gain desc, id
-  // asc) and min weight.  Feasibility of a side-s move is monotone in the
-  // weight (w <= W_s), so the answer is the best feasible side top; a side
-  // whose top is infeasible is searched only in blocks that can still hold a
-  // feasible patch (min weight <= a conservative bound on W_s) and beat the
-  // current best.  Every feasibility verdict is the exact double test.
-  const int32_t nblk = (np + 31) / 32;
+  // ---- FM passes with rollback to the best prefix (partition.cpp:95-159)
+  const bool exact_int = tot < kFmExactWeights;
   int64_t total_moves = 0;
   for (int pass = 0; pass < kFmPasses; ++pass) {
     for (int32_t i = threadIdx.x; i < np; i += blockDim.x) {
@@ -379,242 +500,171 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
       }
       gain[i] = val;
       flag[i] = 0;  // unlocked
+      cslot[i] = kNoSlot;
+    }
+    if (threadIdx.x < 64) s_cp[threadIdx.x >> 5][threadIdx.x & 31] = -1;
+    if (threadIdx.x == 0) {
+      s_pass_cut = s_best_cut = s_cut;
+      s_pass_s[0] = s_best_s[0] = s_sw[0];
+      s_pass_s[1] = s_best_s[1] = s_sw[1];
+      s_nm = 0, s_best_len = 0;
+      s_need = 3;
     }
     __syncthreads();
-    auto leaf_key = [&](int32_t i) -> K { return flag[i] ? K(0) : FmKey<K>::make(gain[i], i); };
-    // (re)build the per-side block summaries of block b (one warp)
-    auto block_sum = [&](int32_t b) {
-      const int32_t i = b * 32 + lane;
-      K k0 = 0, k1 = 0;
-      int32_t w0 = INT32_MAX, w1 = INT32_MAX;
-      if (i < np && !flag[i]) {
-        const K k = leaf_key(i);
-        if (side[i]) k1 = k, w1 = w[i];
-        else k0 = k, w0 = w[i];
+    for (;;) {
+      const int32_t need = s_need;
+      if (need & 1) fm_refill<K>(0, np, gain, side, flag, cslot, s_ck, s_cp, s_B, hist, red, sh);
+      if (need & 2) fm_refill<K>(1, np, gain, side, flag, cslot, s_ck, s_cp, s_B, hist, red, sh);
+      if (need & kFmExact) {  // the reference's own scan: max key over every feasible unlocked patch
+        const int64_t sw0 = s_sw[0], sw1 = s_sw[1];
+        const int64_t H = sw0 > sw1 ? sw0 : sw1, L = sw0 < sw1 ? sw0 : sw1;
+        uint64_t best = 0;
+        for (int32_t i = threadIdx.x; i < np; i += blockDim.x) {
+          if (flag[i]) continue;
+          const int64_t wi = w[i], S = side[i] ? sw1 : sw0, T = side[i] ? sw0 : sw1;
+          if (S - wi > 0 && !fm_infeasible(S - wi, T + wi, H, L, exact_int)) {
+            const uint64_t k = FmKey<K>::make(gain[i], i);
+            best = k > best ? k : best;
+          }
+        }
+        best = block_max_u64(best, red);
+        if (threadIdx.x == 0) s_exact = static_cast<K>(best);
+        __syncthreads();
       }
-      k0 = FmKey<K>::wmax(k0), k1 = FmKey<K>::wmax(k1);
-      w0 = __reduce_min_sync(0xffffffffu, w0), w1 = __reduce_min_sync(0xffffffffu, w1);
-      if (lane == 0) bk[b] = k0, bk[nblk + b] = k1, bwt[b] = w0, bwt[nblk + b] = w1;
-    };
-    // super-block summary of super-block sb (one warp; block summaries written)
-    auto super_sum = [&](int32_t sb) {
-      const int32_t b = sb * 32 + lane;
-      K k0 = 0, k1 = 0;
-      int32_t w0 = INT32_MAX, w1 = INT32_MAX;
-      if (b < nblk) k0 = bk[b], k1 = bk[nblk + b], w0 = bwt[b], w1 = bwt[nblk + b];
-      k0 = FmKey<K>::wmax(k0), k1 = FmKey<K>::wmax(k1);
-      w0 = __reduce_min_sync(0xffffffffu, w0), w1 = __reduce_min_sync(0xffffffffu, w1);
-      if (lane == 0) sbk[sb] = k0, sbk[nsb + sb] = k1, sbw[sb] = w0, sbw[nsb + sb] = w1;
-    };
-    for (int32_t b = wid; b < nblk; b += nw) block_sum(b);
-    __syncthreads();
-    for (int32_t sb = wid; sb < nsb; sb += nw) super_sum(sb);
-    __syncthreads();
-    if (wid == 0) {
-      const int64_t pass_cut = s_cut;
-      int64_t sw0 = s_sw[0], sw1 = s_sw[1], cut = s_cut;
-      const double pass_imb = imbalance_of(sw0, sw1);
-      int64_t best_cut = pass_cut;
-      // Divisions are lazy: thr = max(tol, imbalance) is needed only when the
-      // division-free feasibility test fails, and the best prefix's imbalance
-      // only on a cut tie.
-      double best_imb = pass_imb, thr = kBalanceTol > pass_imb ? kBalanceTol : pass_imb;
-      bool thr_ok = true, best_imb_ok = true;
-      int64_t best_s0 = sw0, best_s1 = sw1;
-      int32_t nm = 0, best_len = 0;
-      auto get_thr = [&]() {
-        if (!thr_ok) {
-          const double imb = imbalance_of(sw0, sw1);
-          thr = kBalanceTol > imb ? kBalanceTol : imb;
-          thr_ok = true;
-        }
-        return thr;
-      };
-      // exact feasibility predicate of moving weight wi off side sd
-      auto pred = [&](int64_t wi, int32_t sd) {
-        const int64_t ns = (sd ? sw1 : sw0) - wi, nt = (sd ? sw0 : sw1) + wi;
-        return ns > 0 && !(imbalance_of(ns, nt) > get_thr());
-      };
-      long long pc_sel = 0, pc_upd = 0, pc_t0 = 0, pc_t1 = 0;
-      for (;;) {
-        if (kFmProf) pc_t0 = clock64();
-        // side tops
-        K t0 = 0, t1 = 0;
-        for (int32_t b = lane; b < nsb; b += 32) t0 = max(t0, sbk[b]), t1 = max(t1, sbk[nsb + b]);
-        t0 = FmKey<K>::wmax(t0), t1 = FmKey<K>::wmax(t1);
-        if ((t0 | t1) == 0) break;
-        // Feasibility.  Moving w off the heavier side with 2w <= S - T lowers the
-        // ratio (<= cur <= thr): feasible without a division.  Otherwise the
-        // exact predicate; a side whose top fails needs its weight bound W_s
-        // (feasible weights form [0, W_s]: the ratio falls until the sides
-        // cross, and the rounded division is monotone after) for a block search.
-        auto quick = [&](int32_t i, int32_t sd) {
-          const int64_t S = sd ? sw1 : sw0, T = sd ? sw0 : sw1;
-          return S >= T && 2 * static_cast<int64_t>(w[i]) <= S - T;
-        };
-        const K hiT = max(t0, t1), loT = min(t0, t1);
-        const int32_t hs = t1 > t0 ? 1 : 0;
-        K best = 0;
-        int32_t fail_side = -1;
-        {
-          const int32_t ih = FmKey<K>::id(hiT);
-          if (quick(ih, hs) || pred(w[ih], hs)) {
-            best = hiT;
-          } else {
-            fail_side = hs;
-            if (loT) {
-              const int32_t il = FmKey<K>::id(loT);
-              if (quick(il, 1 - hs) || pred(w[il], 1 - hs)) best = loT;
-              // (if the lower top fails too, its side can hold nothing better than
-              //  loT that the search of fail_side would miss: searched below)
-              else if (loT > 0) best = 0, fail_side = 2;  // both sides need the block search
-            }
+      if (wid == 0) {
+        // node weights and cut fit int32 (n < 2^31 vertices, 2m < 2^31 entries)
+        int32_t sw0 = static_cast<int32_t>(s_sw[0]), sw1 = static_cast<int32_t>(s_sw[1]);
+        int32_t cut = static_cast<int32_t>(s_cut), best_cut = static_cast<int32_t>(s_best_cut);
+        int32_t best_s0 = static_cast<int32_t>(s_best_s[0]), best_s1 = static_cast<int32_t>(s_best_s[1]);
+        int32_t nm = s_nm, best_len = s_best_len;
+        K B0 = s_B[0], B1 = s_B[1];
+        int32_t cp0 = s_cp[0][lane], cp1 = s_cp[1][lane];
+        K ck0 = cp0 >= 0 ? FmKey<K>::make(gain[cp0], cp0) : K(0);
+        K ck1 = cp1 >= 0 ? FmKey<K>::make(gain[cp1], cp1) : K(0);
+        int32_t cw0 = cp0 >= 0 ? w[cp0] : 0, cw1 = cp1 >= 0 ? w[cp1] : 0;
+        uint32_t refilled = static_cast<uint32_t>(need & 3);
+        // one move: lock ch, flip it, update the neighbours' gains and the caches
+        auto apply = [&](K kbest, int32_t sd) {
+          const int32_t ch = FmKey<K>::id(kbest);
+          const int32_t e0 = ab[ch], e1 = ae[ch], wc = w[ch];
+          const uint32_t own = __ballot_sync(0xffffffffu, (sd ? cp1 : cp0) == ch);
+          if (own && lane == __ffs(own) - 1) {
+            if (sd) cp1 = -1, ck1 = 0, cw1 = 0;
+            else cp0 = -1, ck0 = 0, cw0 = 0;
           }
-        }
-        if (fail_side >= 0) {
-          for (int sd = 0; sd < 2; ++sd) {
-            if (fail_side != 2 && sd != fail_side) continue;
-            const K top = sd ? t1 : t0;
-            if (top <= best) continue;
-            // W_s: lanes 0-15 probe a window around the real-valued estimate
-            const int64_t S = sd ? sw1 : sw0, T = sd ? sw0 : sw1;
-            int64_t est = S - 1;
-            get_thr();
-            if (!isinf(thr)) {
-              const float tf = static_cast<float>(thr);
-              const float e = __fdividef(tf * static_cast<float>(S) - static_cast<float>(T), 1.0f + tf);
-              const int64_t fe = static_cast<int64_t>(floorf(e));
-              est = fe < est ? fe : est;
-            }
-            const int64_t probe = est - 7 + (lane & 15);
-            const bool pv = lane < 16 && probe >= 0 && pred(probe, sd);
-            const uint32_t m = __ballot_sync(0xffffffffu, pv) & 0xffffu;
-            int64_t W;
-            if (m == 0xffffu) {
-              W = est + 8;
-              while (pred(W + 1, sd)) ++W;
-            } else if (m == 0 && est - 7 > 0) {
-              W = est - 8;
-              while (W >= 0 && !pred(W, sd)) --W;
-            } else {
-              W = est - 7 + (32 - __clz(static_cast<int>(m))) - 1;
-            }
-            for (int32_t s0 = 0; s0 < nsb; s0 += 32) {
-              const int32_t sb = s0 + lane;
-              const bool smaybe = sb < nsb && sbk[sd * nsb + sb] > best && sbw[sd * nsb + sb] <= W;
-              uint32_t scand = __ballot_sync(0xffffffffu, smaybe);
-              while (scand) {
-                const int32_t ss = s0 + __ffs(scand) - 1;
-                scand &= scand - 1;
-                if (sbk[sd * nsb + ss] <= best) continue;
-                const int32_t b = ss * 32 + lane;
-                const bool maybe = b < nblk && bk[sd * nblk + b] > best && bwt[sd * nblk + b] <= W;
-                uint32_t cand = __ballot_sync(0xffffffffu, maybe);
-                while (cand) {
-                  const int32_t bb = ss * 32 + __ffs(cand) - 1;
-                  cand &= cand - 1;
-                  if (bk[sd * nblk + bb] <= best) continue;
-                  const int32_t i = bb * 32 + lane;
-                  K k = 0;
-                  if (i < np && !flag[i] && side[i] == sd && w[i] <= W) k = leaf_key(i);
-                  best = max(best, FmKey<K>::wmax(k));
-                }
-              }
-            }
+          if (lane == 0) {
+            flag[ch] = 1;
+            side[ch] = static_cast<uint8_t>(1 - sd);
+            cslot[ch] = kNoSlot;
+            moves[nm] = ch;
+            rec[3 * nm] = cut, rec[3 * nm + 1] = sw0, rec[3 * nm + 2] = sw1;
           }
-        }
-        if (kFmProf) pc_t1 = clock64(), pc_sel += pc_t1 - pc_t0;
-        if (best == 0) break;
-        const int32_t ch = FmKey<K>::id(best);
-        const int32_t gch = gain[ch];
-        const uint8_t sd = side[ch];
-        const int64_t wc = w[ch];
-        __syncwarp();
-        if (lane == 0) {
-          flag[ch] = 1;
-          moves[nm] = ch;
-          rec[3 * nm] = cut, rec[3 * nm + 1] = sw0, rec[3 * nm + 2] = sw1;
-          side[ch] = static_cast<uint8_t>(1 - sd);
-        }
-        ++nm;
-        if (sd) sw1 -= wc, sw0 += wc;
-        else sw0 -= wc, sw1 += wc;
-        cut -= gch;
-        __syncwarp();
-        // neighbours' gains (partition.cpp:137-142).  A raised key only needs a
-        // max into its block summary; a lowered key forces a rebuild only if it
-        // was the block's maximum; ch's own block is rebuilt (ch is now locked).
-        const uint8_t sc = static_cast<uint8_t>(1 - sd);
-        const int32_t e0 = ab[ch], e1 = ae[ch];
-        for (int32_t j0 = e0; j0 < e1; j0 += 32) {
-          const int32_t j = j0 + lane;
-          int32_t rb = -1;  // block to rebuild (side-qualified index)
-          if (j < e1) {
-            const int32_t nb = A_nb(j);
-            if (!flag[nb]) {
-              const int32_t wj = A_w(j);
-              const K oldk = leaf_key(nb);
-              const int32_t delta = side[nb] == sc ? -2 * wj : 2 * wj;
-              gain[nb] += delta;
-              const int32_t slot = side[nb] * nblk + (nb >> 5);
-              if (delta > 0) {
-                const K nk = leaf_key(nb);
-                FmKey<K>::amax(&bk[slot], nk);
-                FmKey<K>::amax(&sbk[side[nb] * nsb + (nb >> 10)], nk);
-              } else if (delta < 0 && bk[slot] == oldk) {
-                rb = nb >> 5;
-              }
-            }
-          }
+          ++nm;
+          if (sd) sw1 -= wc, sw0 += wc;
+          else sw0 -= wc, sw1 += wc;
+          cut -= FmKey<K>::gain(kbest);
           __syncwarp();
-          uint32_t todo = __ballot_sync(0xffffffffu, rb >= 0);  // usually 0-2 lanes
-          int32_t last = -1;
-          while (todo) {
-            const int32_t l = __ffs(todo) - 1;
-            todo &= todo - 1;
-            const int32_t blk = __shfl_sync(0xffffffffu, rb, l);
-            if (blk != last && blk != (ch >> 5)) {
-              block_sum(blk);
-              __syncwarp();
-              super_sum(blk >> 5);
+          // neighbours' gains (partition.cpp:137-142)
+          const int32_t sc = 1 - sd;
+          for (int32_t j0 = e0; j0 < e1; j0 += 32) {
+            const int32_t j = j0 + lane;
+            bool upd = false, ins = false;
+            int32_t nb = 0, sn = 0;
+            K nk = 0;
+            if (j < e1) {
+              nb = A_nb(j);
+              const int32_t wj = A_w(j);
+              if (!flag[nb]) {
+                sn = side[nb];
+                const int32_t g = gain[nb] + (sn == sc ? -2 * wj : 2 * wj);
+                gain[nb] = g;
+                nk = FmKey<K>::make(g, nb);
+                upd = cslot[nb] != kNoSlot;
+                ins = !upd && nk > (sn ? B1 : B0);
+              }
             }
-            last = blk;
+            __syncwarp();
+            if (__any_sync(0xffffffffu, upd)) {  // re-read the cached keys
+              if (cp0 >= 0) ck0 = FmKey<K>::make(gain[cp0], cp0);
+              if (cp1 >= 0) ck1 = FmKey<K>::make(gain[cp1], cp1);
+            }
+            uint32_t im = __ballot_sync(0xffffffffu, ins);
+            while (im) {  // raised uncached keys above the bound join the cache
+              const int l = __ffs(im) - 1;
+              im &= im - 1;
+              const K nbk = __shfl_sync(0xffffffffu, nk, l);
+              const int32_t nbp = __shfl_sync(0xffffffffu, nb, l);
+              const int32_t t = __shfl_sync(0xffffffffu, sn, l);
+              const K ct = t ? ck1 : ck0;
+              const uint32_t fr = __ballot_sync(0xffffffffu, ct == 0);
+              int o;
+              if (fr) {
+                o = __ffs(fr) - 1;
+              } else {
+                const K mn = FmKey<K>::wmin(ct);
+                if (nbk < mn) {  // below the whole cache: it only raises the bound
+                  if (t) B1 = max(B1, nbk);
+                  else B0 = max(B0, nbk);
+                  continue;
+                }
+                o = __ffs(__ballot_sync(0xffffffffu, ct == mn)) - 1;
+                if (t) B1 = max(B1, mn);
+                else B0 = max(B0, mn);
+                if (lane == o) cslot[t ? cp1 : cp0] = kNoSlot;
+              }
+              if (lane == o) {
+                const int32_t wq = w[nbp];
+                if (t) ck1 = nbk, cp1 = nbp, cw1 = wq;
+                else ck0 = nbk, cp0 = nbp, cw0 = wq;
+                cslot[nbp] = static_cast<uint8_t>((t << 5) | o);
+              }
+            }
+            __syncwarp();
           }
+          if (cut < best_cut || (cut == best_cut && fm_imb_less(sw0, sw1, best_s0, best_s1, exact_int))) {
+            best_cut = cut;
+            best_len = nm;
+            best_s0 = sw0, best_s1 = sw1;
+          }
+        };
+        int32_t reason = 0;
+        if (need & kFmExact) {
+          const K e = s_exact;
+          if (e == 0) reason = kFmDone;
+          else apply(e, side[FmKey<K>::id(e)]), refilled = 0;
         }
-        block_sum(ch >> 5);
-        __syncwarp();
-        super_sum(ch >> 10);
-        if (cut < best_cut) {
-          best_cut = cut;
-          best_len = nm;
-          best_s0 = sw0, best_s1 = sw1, best_imb_ok = false;
-        } else if (cut == best_cut) {
-          const double imb = imbalance_of(sw0, sw1);
-          if (!best_imb_ok) best_imb = imbalance_of(best_s0, best_s1), best_imb_ok = true;
-          if (imb < best_imb) best_imb = imb, best_len = nm, best_s0 = sw0, best_s1 = sw1;
+        while (!reason) {
+          // feasibility of the cached entries (exact, division-free)
+          const int32_t H = max(sw0, sw1), L = min(sw0, sw1);
+          const bool f0 = ck0 != 0 && sw0 - cw0 > 0 && !fm_infeasible(sw0 - cw0, sw1 + cw0, H, L, exact_int);
+          const bool f1 = ck1 != 0 && sw1 - cw1 > 0 && !fm_infeasible(sw1 - cw1, sw0 + cw1, H, L, exact_int);
+          const K fk0 = FmKey<K>::wmax(f0 ? ck0 : K(0)), fk1 = FmKey<K>::wmax(f1 ? ck1 : K(0));
+          const K best = max(fk0, fk1);
+          const bool u0 = B0 != 0 && !(fk0 > B0) && B0 > best;
+          const bool u1 = B1 != 0 && !(fk1 > B1) && B1 > best;
+          if (u0 || u1) {  // a side's answer may lie outside its cache
+            reason = ((u0 && (refilled & 1)) || (u1 && (refilled & 2))) ? kFmExact : (u0 ? 1 : 0) | (u1 ? 2 : 0);
+            break;
+          }
+          if (best == 0) {
+            reason = kFmDone;
+            break;
+          }
+          refilled = 0;
+          apply(best, fk1 == best ? 1 : 0);
         }
-        thr_ok = false;
-        __syncwarp();
-        if (kFmProf) pc_upd += clock64() - pc_t1;
+        s_cp[0][lane] = cp0, s_cp[1][lane] = cp1;
+        if (lane == 0) {
+          s_sw[0] = sw0, s_sw[1] = sw1, s_cut = cut, s_best_cut = best_cut;
+          s_best_s[0] = best_s0, s_best_s[1] = best_s1;
+          s_nm = nm, s_best_len = best_len;
+          s_B[0] = B0, s_B[1] = B1;
+          s_need = reason;
+        }
       }
-      if (kFmProf && lane == 0 && li == 0) {
-        atomicAdd(&a.stats[12], static_cast<unsigned long long>(nm));
-        atomicAdd(&a.stats[13], static_cast<unsigned long long>(pc_sel));
-        atomicAdd(&a.stats[14], static_cast<unsigned long long>(pc_upd));
-      }
-      if (!best_imb_ok) best_imb = imbalance_of(best_s0, best_s1);
-      if (lane == 0) {
-        s_nm = nm;
-        s_best_len = best_len;
-        s_best_cut = best_cut;
-        s_best_imb = best_imb;
-        s_pass_cut = pass_cut;
-        s_pass_imb = pass_imb;
-        s_cut = cut;
-        s_sw[0] = sw0, s_sw[1] = sw1;
-      }
+      __syncthreads();
+      if (s_need == kFmDone) break;
     }
-    __syncthreads();
     const int32_t nm = s_nm, bl = s_best_len;
     total_moves += nm;
     for (int32_t m = bl + threadIdx.x; m < nm; m += blockDim.x) side[moves[m]] ^= 1;
@@ -625,7 +675,9 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
         s_sw[0] = rec[3 * bl + 1];
         s_sw[1] = rec[3 * bl + 2];
       }
-      const bool improved = s_best_cut < s_pass_cut || (s_best_cut == s_pass_cut && s_best_imb < s_pass_imb);
+      const bool improved = s_best_cut < s_pass_cut ||
+                            (s_best_cut == s_pass_cut &&
+                             fm_imb_less(s_best_s[0], s_best_s[1], s_pass_s[0], s_pass_s[1], exact_int));
       s_stop = improved ? 0 : 1;
     }
     __syncthreads();
@@ -1111,9 +1163,7 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
   DevBuf<unsigned long long> stats(2, s);
   DevBuf<int64_t> fm_rec(3LL * Pm, s);
   DevBuf<int32_t> fm_w(Pm, s), fm_ab(Pm, s), fm_ae(Pm, s);
-  DevBuf<uint64_t> fm_lk(Pm, s), fm_bm(2 * (Pm / 32 + (1LL << std::min(L, 20)) + 64), s);
-  DevBuf<int32_t> fm_bw(2 * (Pm / 32 + (1LL << std::min(L, 20)) + 64), s);
-  DevBuf<uint8_t> fm_side(2LL * Pm, s);
+  DevBuf<uint8_t> fm_side(3LL * Pm, s);
   DevBuf<int32_t> slot_of(std::max(n, 1), s), ref_pull(std::max(n, 1), s), ref_pulled(std::max(n, 1), s);
   DevBuf<uint8_t> ref_own(std::max(n, 1), s), ref_in(std::max(n, 1), s);
   DevBuf<int8_t> region(std::max(n, 1), s);
@@ -1155,7 +1205,7 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     a.pw = pw, a.pnode = pnode, a.np_node = np_node, a.active = active, a.lidx = lidx;
     a.side = side, a.region = region, a.in_super = in_super, a.in_list = in_list, a.bcount = bcount;
     a.sep_list = seplist, a.next_vlist = nxt_list, a.next_start = next_start, a.next_cnt = next_cnt;
-    a.fm_w = fm_w, a.fm_ab = fm_ab, a.fm_ae = fm_ae, a.fm_side = fm_side, a.fm_lk = fm_lk, a.fm_bm = fm_bm, a.fm_bw = fm_bw;
+    a.fm_w = fm_w, a.fm_ab = fm_ab, a.fm_ae = fm_ae, a.fm_side = fm_side;
     a.slot_of = slot_of, a.ref_pull = ref_pull, a.ref_own = ref_own, a.ref_in = ref_in, a.ref_pulled = ref_pulled;
     a.vside = vside, a.ell = ell;
     a.stats = ctx.dwork ? ctx.dwork + 1 : stats.get(), a.fm_gain = fm_gain, a.fm_moves = fm_moves, a.fm_rec = fm_rec;
@@ -1242,8 +1292,7 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
         const int64_t np_i = hpo[i + 1] - hpo[i];
         if (np_i == 0 || np_i > kFmSmemPatches) continue;
         const int64_t e_i = (hfo[i + 1] - hfo[i]) - np_i;
-        need = std::max<size_t>(need, static_cast<size_t>(np_i) * kFmBytesPerPatch + 4 * e_i + 1024 +
-                                          24 * static_cast<size_t>((np_i + 1023) / 1024));
+        need = std::max<size_t>(need, static_cast<size_t>(np_i) * kFmBytesPerPatch + 4 * e_i + 1024);
       }
       // opt-in limit minus the kernels' static shared memory
       cudaFuncAttributes fa32{}, fa64{};
