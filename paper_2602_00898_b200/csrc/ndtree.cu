@@ -75,10 +75,10 @@ struct LevelArgs {
   unsigned long long* stats;  // [0] moves FM, [1] moves refine (work counters)
   // FM scratch (per patch, in plist layout)
   int32_t* fm_gain;
-  int32_t* fm_w;           // global fallback state for nodes beyond kFmSmemPatches
-  int32_t* fm_ab;
+  int32_t* fm_w;           // global state for nodes whose state does not fit shared memory
+  int32_t* fm_ab;          // (ab, ae) pairs, 2 * P
   int32_t* fm_ae;
-  uint8_t* fm_side;        // 3 * P bytes: side, lock flags, cache slots
+  uint8_t* fm_side;        // 4 * P bytes: status words (fm_st)
   const int32_t* qloc;     // quotient adjacency as node-local patch indices
   int32_t* fm_fifo;        // capacity per node: poff span + edges -> allocated 2*P + E
   const int64_t* fm_fifo_off;  // per level node
@@ -91,7 +91,6 @@ struct LevelArgs {
   const int32_t* ell;      // n * 8 ELL adjacency
   int64_t fm_smem_bytes;   // dynamic shared memory of the FM launch
   int32_t* fm_moves;
-  int64_t* fm_rec;         // 3 per move: cut, sw0, sw1
 };
 
 __global__ void level_weights(LevelArgs a) {
@@ -201,8 +200,11 @@ __global__ void quotient_csr(int32_t U, const uint64_t* ukeys, const int32_t* uc
 // refill, the CTA takes the exact argmax over all patches for one move.  The
 // chosen move is always the reference's; on the C2 root (3,901 patches,
 // 23,406 moves) the cache needs 35 refills.
-constexpr int32_t kFmSmemPatches = 10 * 1024;
-constexpr int kFmBytesPerPatch = 19;  // w, gain, ab, ae (int32) + side, flag, cache slot (bytes)
+// Per-patch status word: side (byte 0), lock / visited flag (byte 1), cache
+// slot (byte 2: side << 5 | lane, or kNoSlot).
+__device__ __forceinline__ uint32_t fm_st(uint32_t side, uint32_t flag, uint32_t slot) {
+  return side | (flag << 8) | (slot << 16);
+}
 constexpr int kFmThreads = 256;
 constexpr uint8_t kNoSlot = 0xff;
 constexpr int kFmDone = 8, kFmExact = 4;  // segment exit reasons (1, 2: refill side 0 / 1)
@@ -232,8 +234,8 @@ template <> struct FmKey<uint64_t> {
 };
 
 // imbalance_of(ns, nt) > max(tol, imbalance_of(H, L)) with tol = 1.2, the
-// reference's double test (partition.cpp:114-124), in exact integer form for
-// node weights below 2^26:
+// reference's double test (partition.cpp:114-124).  EXACT: integer form, valid
+// for node weights below 2^26 (the host checks n):
 //  * fl(h/l) > fl(1.2) <=> 5h > 6l: a ratio h/l != 6/5 lies at least 1/(5l)
 //    from 6/5, far beyond the rounding of either double;
 //  * fl(h/l) > fl(H/L) <=> hL > Hl: distinct ratios with hL, Hl < 2^52 are
@@ -241,38 +243,44 @@ template <> struct FmKey<uint64_t> {
 // Infinite ratios (l = 0 or L = 0) come out right: 0 > ... is false.
 static_assert(kBalanceTol == 1.2, "fm_infeasible encodes tol = 6/5");
 constexpr int64_t kFmExactWeights = int64_t(1) << 26;
-__device__ __forceinline__ bool fm_infeasible(int64_t ns, int64_t nt, int64_t H, int64_t L, bool exact_int) {
-  const int64_t h = ns > nt ? ns : nt, l = ns < nt ? ns : nt;
-  if (exact_int) return 5 * h > 6 * l && h * L > H * l;
-  const double cur = imbalance_of(H, L);
-  return imbalance_of(ns, nt) > (kBalanceTol > cur ? kBalanceTol : cur);
+template <bool EXACT>
+__device__ __forceinline__ bool fm_infeasible(int32_t ns, int32_t nt, int32_t H, int32_t L) {
+  const int32_t h = max(ns, nt), l = min(ns, nt);
+  if constexpr (EXACT) {
+    return (5 * h > 6 * l) & (static_cast<int64_t>(h) * L > static_cast<int64_t>(H) * l);  // 5h < 2^29
+  } else {
+    const double cur = imbalance_of(H, L);
+    return imbalance_of(ns, nt) > (kBalanceTol > cur ? kBalanceTol : cur);
+  }
 }
 // imbalance_of(a0, a1) < imbalance_of(b0, b1) (the best-prefix tie test)
-__device__ __forceinline__ bool fm_imb_less(int64_t a0, int64_t a1, int64_t b0, int64_t b1, bool exact_int) {
-  const int64_t ah = a0 > a1 ? a0 : a1, al = a0 < a1 ? a0 : a1, bh = b0 > b1 ? b0 : b1, bl = b0 < b1 ? b0 : b1;
-  if (exact_int) return ah * bl < bh * al;
-  return imbalance_of(a0, a1) < imbalance_of(b0, b1);
+template <bool EXACT>
+__device__ __forceinline__ bool fm_imb_less(int32_t a0, int32_t a1, int32_t b0, int32_t b1) {
+  if constexpr (EXACT) {
+    return static_cast<int64_t>(max(a0, a1)) * min(b0, b1) < static_cast<int64_t>(max(b0, b1)) * min(a0, a1);
+  } else {
+    return imbalance_of(a0, a1) < imbalance_of(b0, b1);
+  }
 }
 
 // CTA-wide: refill the side-t cache with the 32 largest keys of the unlocked
 // side-t patches; B[t] = the 33rd largest (0 when there are at most 32).
 // The threshold is an MSD radix select over the bits below the common prefix
 // of the largest and smallest candidate key.
-template <class K>
-__device__ void fm_refill(int32_t t, int32_t np, const int32_t* gain, const uint8_t* side, const uint8_t* flag,
-                          uint8_t* cslot, K (*ck)[32], int32_t (*cp)[32], K* B, int32_t* hist, uint64_t* red,
+template <class K, class G, class W>
+__device__ __forceinline__ void fm_refill(int32_t t, int32_t np, G gain, W st, K (*ck)[32], int32_t (*cp)[32], K* B, int32_t* hist, uint64_t* red,
                           int32_t* sh) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if (threadIdx.x < 32) {
     const int32_t p = cp[t][threadIdx.x];
-    if (p >= 0) cslot[p] = kNoSlot;
+    if (p >= 0) reinterpret_cast<uint8_t*>(st)[4 * p + 2] = kNoSlot;
     cp[t][threadIdx.x] = -1;
     ck[t][threadIdx.x] = 0;
   }
   int64_t c = 0;
   uint64_t mx = 0, mn = ~0ull;
   for (int32_t i = threadIdx.x; i < np; i += blockDim.x)
-    if (!flag[i] && side[i] == t) {
+    if ((st[i] & 0xffffu) == static_cast<uint32_t>(t)) {  // unlocked, side t
       const uint64_t k = FmKey<K>::make(gain[i], i);
       ++c, mx = k > mx ? k : mx, mn = k < mn ? k : mn;
     }
@@ -294,7 +302,7 @@ __device__ void fm_refill(int32_t t, int32_t np, const int32_t* gain, const uint
       for (int32_t i0 = wid * 32; i0 < np; i0 += nw * 32) {
         const int32_t i = i0 + lane;
         int32_t d = -1;
-        if (i < np && !flag[i] && side[i] == t) {
+        if (i < np && (st[i] & 0xffffu) == static_cast<uint32_t>(t)) {
           const uint64_t k = FmKey<K>::make(gain[i], i);
           if ((k & pmask) == prefix) d = static_cast<int32_t>((k >> lo) & static_cast<uint64_t>(nbins - 1));
         }
@@ -337,95 +345,91 @@ __device__ void fm_refill(int32_t t, int32_t np, const int32_t* gain, const uint
   if (threadIdx.x == 0) sh[2] = 0;
   __syncthreads();
   for (int32_t i = threadIdx.x; i < np; i += blockDim.x)
-    if (!flag[i] && side[i] == t) {
+    if ((st[i] & 0xffffu) == static_cast<uint32_t>(t)) {
       const K k = FmKey<K>::make(gain[i], i);
       if (k > T) {
         const int32_t slot = atomicAdd(&sh[2], 1);
         ck[t][slot] = k, cp[t][slot] = i;
-        cslot[i] = static_cast<uint8_t>((t << 5) | slot);
+        reinterpret_cast<uint8_t*>(st)[4 * i + 2] = static_cast<uint8_t>((t << 5) | slot);
       }
     }
   if (threadIdx.x == 0) B[t] = static_cast<K>(T);
   __syncthreads();
 }
 
-template <class K>
-__global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
-  const int32_t li = blockIdx.x;
-  if (!a.active[li]) return;
-  const int32_t pbeg = a.poff[li], np = a.poff[li + 1] - pbeg;
+// One node's bipartition.  SM: the patch state and the packed adjacency
+// (local id << 16 | weight) live in shared memory; otherwise in global
+// scratch (plist layout) with the adjacency read from qloc / qw.
+template <class K, bool EXACT, bool SM>
+__device__ __forceinline__ void fm_node(const LevelArgs& a, int32_t li, int32_t pbeg, int32_t np) {
   const int32_t* pl = a.plist + pbeg;
   int32_t* fifo = a.fm_fifo + a.fm_fifo_off[li];
   int32_t* moves = a.fm_moves + pbeg;
-  int64_t* rec = a.fm_rec + 3LL * pbeg;
-
   extern __shared__ uint64_t fm_sm64_[];
-  const bool in_smem = np <= kFmSmemPatches;
-  int32_t* fm_sm = reinterpret_cast<int32_t*>(fm_sm64_);
-  int32_t* w = in_smem ? fm_sm : a.fm_w + pbeg;
-  int32_t* gain = in_smem ? fm_sm + np : a.fm_gain + pbeg;
-  int32_t* ab = in_smem ? fm_sm + 2 * np : a.fm_ab + pbeg;
-  int32_t* ae = in_smem ? fm_sm + 3 * np : a.fm_ae + pbeg;
-  uint8_t* side = in_smem ? reinterpret_cast<uint8_t*>(fm_sm + 4 * np) : a.fm_side + pbeg;
-  uint8_t* flag = side + (in_smem ? np : a.P);  // visited / locked
-  uint8_t* cslot = flag + (in_smem ? np : a.P);  // cache slot (side << 5 | lane) or kNoSlot
+  int32_t* w;
+  int32_t* gain;
+  int2* abe;
+  uint32_t* st;  // status words (fm_st)
+  uint32_t* packed = nullptr;
+  if constexpr (SM) {  // byte offsets from the shared base (keeps the address space visible)
+    char* base = reinterpret_cast<char*>(fm_sm64_);
+    w = reinterpret_cast<int32_t*>(base);
+    gain = w + np;
+    abe = reinterpret_cast<int2*>(base + 8LL * np);
+    st = reinterpret_cast<uint32_t*>(base + 16LL * np);
+    packed = reinterpret_cast<uint32_t*>(base + ((20LL * np + 15) & ~15LL));
+  } else {
+    w = a.fm_w + pbeg;
+    gain = a.fm_gain + pbeg;
+    abe = reinterpret_cast<int2*>(a.fm_ab) + pbeg;
+    st = reinterpret_cast<uint32_t*>(a.fm_side) + pbeg;
+  }
+  uint8_t* stb = reinterpret_cast<uint8_t*>(st);
+  auto side = [&](int32_t i) -> uint32_t { return stb[4 * i]; };
+  auto flag = [&](int32_t i) -> uint32_t { return stb[4 * i + 1]; };
+  auto A_nb = [&](int32_t j) -> int32_t {
+    if constexpr (SM) return static_cast<int32_t>(packed[j] >> 16);
+    else return __ldg(&a.qloc[j]);
+  };
+  auto A_w = [&](int32_t j) -> int32_t {
+    if constexpr (SM) return static_cast<int32_t>(packed[j] & 0xffffu);
+    else return __ldg(&a.qw[j]);
+  };
 
   __shared__ uint64_t red[32];
   __shared__ int32_t hist[256], sh[4];
   __shared__ K s_ck[2][32], s_B[2], s_exact;
   __shared__ int32_t s_cp[2][32];
-  __shared__ int64_t s_total, s_left, s_cut, s_sw[2], s_best_cut, s_pass_cut, s_best_s[2];
-  __shared__ int64_t s_pass_s[2];
+  __shared__ int32_t s_left, s_cut, s_sw[2], s_best_cut, s_pass_cut, s_best_s[2], s_pass_s[2];
   __shared__ int32_t s_nm, s_best_len, s_need, s_stop;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 
   int64_t tot = 0;
-  int32_t heavy = 0;
   for (int32_t i = threadIdx.x; i < np; i += blockDim.x) {
     const int32_t p = pl[i];
     w[i] = a.pw[p];
-    ab[i] = a.qoff[p];
-    ae[i] = a.qoff[p + 1];
-    side[i] = 1;  // right (partition.cpp:34)
-    flag[i] = 0;
+    abe[i] = make_int2(a.qoff[p], a.qoff[p + 1]);
+    st[i] = fm_st(1, 0, kNoSlot);  // right (partition.cpp:34)
     tot += w[i];
   }
   tot = block_sum_i64(tot, reinterpret_cast<int64_t*>(red));
-  // node-local adjacency packed (local id << 16 | weight) in shared memory when
-  // it fits; otherwise the global arrays (qloc, qw) are read directly
-  uint32_t* packed = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(side + 3 * np) + 15) & ~uintptr_t(15));
-  const int64_t e_node = (a.fm_fifo_off[li + 1] - a.fm_fifo_off[li]) - np;
-  const bool adj_smem = in_smem && np < 65536 &&
-                        static_cast<int64_t>(reinterpret_cast<uint8_t*>(packed + e_node) - reinterpret_cast<uint8_t*>(fm_sm64_)) +
-                        16 <= a.fm_smem_bytes;
-  if (adj_smem) {
+  if constexpr (SM) {  // node-local packed adjacency
     int32_t run = 0;
     for (int32_t i0 = 0; i0 < np; i0 += blockDim.x) {
       const int32_t i = i0 + threadIdx.x;
-      const int32_t d = i < np ? ae[i] - ab[i] : 0;
+      const int2 e = i < np ? abe[i] : make_int2(0, 0);
+      const int32_t d = e.y - e.x;
       int32_t tt;
       const int32_t off = block_excl_scan(d, reinterpret_cast<int32_t*>(red), &tt);
       if (i < np) {
-        const int32_t g0 = ab[i];
-        for (int32_t q = 0; q < d; ++q) {
-          const int32_t wq = __ldg(&a.qw[g0 + q]);
-          heavy |= wq > 0xffff;
-          packed[run + off + q] = (static_cast<uint32_t>(__ldg(&a.qloc[g0 + q])) << 16) | (wq & 0xffff);
-        }
-        ab[i] = run + off;
-        ae[i] = run + off + d;
+        for (int32_t q = 0; q < d; ++q)
+          packed[run + off + q] = (static_cast<uint32_t>(__ldg(&a.qloc[e.x + q])) << 16) | __ldg(&a.qw[e.x + q]);
+        abe[i] = make_int2(run + off, run + off + d);
       }
       run += tt;
     }
-  }
-  heavy = __syncthreads_or(heavy);
-  if (heavy) {  // a weight does not fit 16 bits: undo (global offsets again)
-    for (int32_t i = threadIdx.x; i < np; i += blockDim.x) ab[i] = a.qoff[pl[i]], ae[i] = a.qoff[pl[i] + 1];
     __syncthreads();
   }
-  const bool adj_local = adj_smem && !heavy;
-  auto A_nb = [&](int32_t j) -> int32_t { return adj_local ? static_cast<int32_t>(packed[j] >> 16) : __ldg(&a.qloc[j]); };
-  auto A_w = [&](int32_t j) -> int32_t { return adj_local ? static_cast<int32_t>(packed[j] & 0xffffu) : __ldg(&a.qw[j]); };
 
   // ---- greedy growing from the heaviest patch (partition.cpp:53-79), warp 0
   if (wid == 0) {
@@ -436,7 +440,7 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
       while (head < tail) {  // first unvisited fifo entry
         const int32_t h = head + lane;
         const int32_t x = h < tail ? fifo[h] : 0;
-        const uint32_t m = __ballot_sync(0xffffffffu, h < tail && !flag[x]);
+        const uint32_t m = __ballot_sync(0xffffffffu, h < tail && !flag(x));
         if (m) {
           const int l = __ffs(m) - 1;
           u = __shfl_sync(0xffffffffu, x, l);
@@ -448,59 +452,62 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
       if (u < 0) {  // fifo empty: heaviest unvisited patch (weight desc, id asc)
         uint64_t best = 0;
         for (int32_t i = lane; i < np; i += 32)
-          if (!flag[i]) {
+          if (!flag(i)) {
             const uint64_t k = key_max(static_cast<uint32_t>(w[i]), static_cast<uint32_t>(i));
             best = k > best ? k : best;
           }
         u = static_cast<int32_t>(key_max_id(warp_max_u64(best)));
       }
-      if (lane == 0) flag[u] = 1, side[u] = 0;
+      if (lane == 0) st[u] = fm_st(0, 1, kNoSlot);
       left += w[u];
       __syncwarp();
-      const int32_t e0 = ab[u], e1 = ae[u];
-      for (int32_t j0 = e0; j0 < e1; j0 += 32) {
+      const int2 e = abe[u];
+      for (int32_t j0 = e.x; j0 < e.y; j0 += 32) {
         const int32_t j = j0 + lane;
-        const int32_t nb = j < e1 ? A_nb(j) : 0;
-        const bool push = j < e1 && !flag[nb];
+        const int32_t nb = j < e.y ? A_nb(j) : 0;
+        const bool push = j < e.y && !flag(nb);
         const uint32_t m = __ballot_sync(0xffffffffu, push);
         if (push) fifo[tail + __popc(m & ((1u << lane) - 1))] = nb;
         tail += __popc(m);
       }
       __syncwarp();
     }
-    if (lane == 0) s_left = left;
+    if (lane == 0) s_left = static_cast<int32_t>(left);
   }
   __syncthreads();
   // cut of the grown split (partition.cpp:81-84)
   int64_t cut = 0;
-  for (int32_t i = threadIdx.x; i < np; i += blockDim.x)
-    for (int32_t j = ab[i]; j < ae[i]; ++j) {
+  for (int32_t i = threadIdx.x; i < np; i += blockDim.x) {
+    const int2 e = abe[i];
+    for (int32_t j = e.x; j < e.y; ++j) {
       const int32_t nb = A_nb(j);
-      if (nb > i && side[i] != side[nb]) cut += A_w(j);  // local order == patch id order
+      if (nb > i && side(i) != side(nb)) cut += A_w(j);  // local order == patch id order
     }
+  }
   cut = block_sum_i64(cut, reinterpret_cast<int64_t*>(red));
   if (threadIdx.x == 0) {
-    s_total = tot;
-    s_cut = cut;
+    s_cut = static_cast<int32_t>(cut);  // node weights and cut fit int32 (n < 2^31, 2m < 2^31)
     s_sw[0] = s_left;
-    s_sw[1] = tot - s_left;
+    s_sw[1] = static_cast<int32_t>(tot) - s_left;
   }
   __syncthreads();
 
   // ---- FM passes with rollback to the best prefix (partition.cpp:95-159)
-  const bool exact_int = tot < kFmExactWeights;
   int64_t total_moves = 0;
   for (int pass = 0; pass < kFmPasses; ++pass) {
     for (int32_t i = threadIdx.x; i < np; i += blockDim.x) {
       int32_t val = 0;
-      const uint8_t si = side[i];
-      for (int32_t j = ab[i]; j < ae[i]; ++j) {
+      const uint32_t si = side(i);
+      const int2 e = abe[i];
+      for (int32_t j = e.x; j < e.y; ++j) {
         const int32_t wj = A_w(j);
-        val += side[A_nb(j)] != si ? wj : -wj;
+        val += side(A_nb(j)) != si ? wj : -wj;
       }
       gain[i] = val;
-      flag[i] = 0;  // unlocked
-      cslot[i] = kNoSlot;
+    }
+    __syncthreads();
+    for (int32_t i = threadIdx.x; i < np; i += blockDim.x) {
+      st[i] = fm_st(side(i), 0, kNoSlot);  // unlocked
     }
     if (threadIdx.x < 64) s_cp[threadIdx.x >> 5][threadIdx.x & 31] = -1;
     if (threadIdx.x == 0) {
@@ -513,16 +520,15 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
     __syncthreads();
     for (;;) {
       const int32_t need = s_need;
-      if (need & 1) fm_refill<K>(0, np, gain, side, flag, cslot, s_ck, s_cp, s_B, hist, red, sh);
-      if (need & 2) fm_refill<K>(1, np, gain, side, flag, cslot, s_ck, s_cp, s_B, hist, red, sh);
+      if (need & 1) fm_refill<K>(0, np, gain, st, s_ck, s_cp, s_B, hist, red, sh);
+      if (need & 2) fm_refill<K>(1, np, gain, st, s_ck, s_cp, s_B, hist, red, sh);
       if (need & kFmExact) {  // the reference's own scan: max key over every feasible unlocked patch
-        const int64_t sw0 = s_sw[0], sw1 = s_sw[1];
-        const int64_t H = sw0 > sw1 ? sw0 : sw1, L = sw0 < sw1 ? sw0 : sw1;
+        const int32_t sw0 = s_sw[0], sw1 = s_sw[1], H = max(sw0, sw1), L = min(sw0, sw1);
         uint64_t best = 0;
         for (int32_t i = threadIdx.x; i < np; i += blockDim.x) {
-          if (flag[i]) continue;
-          const int64_t wi = w[i], S = side[i] ? sw1 : sw0, T = side[i] ? sw0 : sw1;
-          if (S - wi > 0 && !fm_infeasible(S - wi, T + wi, H, L, exact_int)) {
+          if (flag(i)) continue;
+          const int32_t wi = w[i], S = side(i) ? sw1 : sw0, T = side(i) ? sw0 : sw1;
+          if (S - wi > 0 && !fm_infeasible<EXACT>(S - wi, T + wi, H, L)) {
             const uint64_t k = FmKey<K>::make(gain[i], i);
             best = k > best ? k : best;
           }
@@ -532,10 +538,8 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
         __syncthreads();
       }
       if (wid == 0) {
-        // node weights and cut fit int32 (n < 2^31 vertices, 2m < 2^31 entries)
-        int32_t sw0 = static_cast<int32_t>(s_sw[0]), sw1 = static_cast<int32_t>(s_sw[1]);
-        int32_t cut = static_cast<int32_t>(s_cut), best_cut = static_cast<int32_t>(s_best_cut);
-        int32_t best_s0 = static_cast<int32_t>(s_best_s[0]), best_s1 = static_cast<int32_t>(s_best_s[1]);
+        int32_t sw0 = s_sw[0], sw1 = s_sw[1], cut = s_cut, best_cut = s_best_cut;
+        int32_t best_s0 = s_best_s[0], best_s1 = s_best_s[1];
         int32_t nm = s_nm, best_len = s_best_len;
         K B0 = s_B[0], B1 = s_B[1];
         int32_t cp0 = s_cp[0][lane], cp1 = s_cp[1][lane];
@@ -546,40 +550,39 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
         // one move: lock ch, flip it, update the neighbours' gains and the caches
         auto apply = [&](K kbest, int32_t sd) {
           const int32_t ch = FmKey<K>::id(kbest);
-          const int32_t e0 = ab[ch], e1 = ae[ch], wc = w[ch];
+          const int2 e = abe[ch];
+          const int32_t wc = w[ch];
           const uint32_t own = __ballot_sync(0xffffffffu, (sd ? cp1 : cp0) == ch);
           if (own && lane == __ffs(own) - 1) {
             if (sd) cp1 = -1, ck1 = 0, cw1 = 0;
             else cp0 = -1, ck0 = 0, cw0 = 0;
           }
           if (lane == 0) {
-            flag[ch] = 1;
-            side[ch] = static_cast<uint8_t>(1 - sd);
-            cslot[ch] = kNoSlot;
+            st[ch] = fm_st(1 - sd, 1, kNoSlot);
             moves[nm] = ch;
-            rec[3 * nm] = cut, rec[3 * nm + 1] = sw0, rec[3 * nm + 2] = sw1;
           }
           ++nm;
-          if (sd) sw1 -= wc, sw0 += wc;
-          else sw0 -= wc, sw1 += wc;
+          sw0 += sd ? wc : -wc;
+          sw1 += sd ? -wc : wc;
           cut -= FmKey<K>::gain(kbest);
           __syncwarp();
           // neighbours' gains (partition.cpp:137-142)
           const int32_t sc = 1 - sd;
-          for (int32_t j0 = e0; j0 < e1; j0 += 32) {
+          for (int32_t j0 = e.x; j0 < e.y; j0 += 32) {
             const int32_t j = j0 + lane;
             bool upd = false, ins = false;
             int32_t nb = 0, sn = 0;
             K nk = 0;
-            if (j < e1) {
+            if (j < e.y) {
               nb = A_nb(j);
               const int32_t wj = A_w(j);
-              if (!flag[nb]) {
-                sn = side[nb];
+              const uint32_t sw = st[nb];
+              if (!(sw & 0xff00u)) {  // unlocked
+                sn = static_cast<int32_t>(sw & 1u);
                 const int32_t g = gain[nb] + (sn == sc ? -2 * wj : 2 * wj);
                 gain[nb] = g;
                 nk = FmKey<K>::make(g, nb);
-                upd = cslot[nb] != kNoSlot;
+                upd = (sw >> 16) != kNoSlot;
                 ins = !upd && nk > (sn ? B1 : B0);
               }
             }
@@ -610,18 +613,18 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
                 o = __ffs(__ballot_sync(0xffffffffu, ct == mn)) - 1;
                 if (t) B1 = max(B1, mn);
                 else B0 = max(B0, mn);
-                if (lane == o) cslot[t ? cp1 : cp0] = kNoSlot;
+                if (lane == o) stb[4 * (t ? cp1 : cp0) + 2] = kNoSlot;
               }
               if (lane == o) {
                 const int32_t wq = w[nbp];
                 if (t) ck1 = nbk, cp1 = nbp, cw1 = wq;
                 else ck0 = nbk, cp0 = nbp, cw0 = wq;
-                cslot[nbp] = static_cast<uint8_t>((t << 5) | o);
+                stb[4 * nbp + 2] = static_cast<uint8_t>((t << 5) | o);
               }
             }
             __syncwarp();
           }
-          if (cut < best_cut || (cut == best_cut && fm_imb_less(sw0, sw1, best_s0, best_s1, exact_int))) {
+          if (cut < best_cut || (cut == best_cut && fm_imb_less<EXACT>(sw0, sw1, best_s0, best_s1))) {
             best_cut = cut;
             best_len = nm;
             best_s0 = sw0, best_s1 = sw1;
@@ -631,13 +634,13 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
         if (need & kFmExact) {
           const K e = s_exact;
           if (e == 0) reason = kFmDone;
-          else apply(e, side[FmKey<K>::id(e)]), refilled = 0;
+          else apply(e, static_cast<int32_t>(side(FmKey<K>::id(e)))), refilled = 0;
         }
         while (!reason) {
-          // feasibility of the cached entries (exact, division-free)
+          // feasibility of the cached entries
           const int32_t H = max(sw0, sw1), L = min(sw0, sw1);
-          const bool f0 = ck0 != 0 && sw0 - cw0 > 0 && !fm_infeasible(sw0 - cw0, sw1 + cw0, H, L, exact_int);
-          const bool f1 = ck1 != 0 && sw1 - cw1 > 0 && !fm_infeasible(sw1 - cw1, sw0 + cw1, H, L, exact_int);
+          const bool f0 = (ck0 != 0) & (sw0 - cw0 > 0) & !fm_infeasible<EXACT>(sw0 - cw0, sw1 + cw0, H, L);
+          const bool f1 = (ck1 != 0) & (sw1 - cw1 > 0) & !fm_infeasible<EXACT>(sw1 - cw1, sw0 + cw1, H, L);
           const K fk0 = FmKey<K>::wmax(f0 ? ck0 : K(0)), fk1 = FmKey<K>::wmax(f1 ? ck1 : K(0));
           const K best = max(fk0, fk1);
           const bool u0 = B0 != 0 && !(fk0 > B0) && B0 > best;
@@ -667,24 +670,45 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
     }
     const int32_t nm = s_nm, bl = s_best_len;
     total_moves += nm;
-    for (int32_t m = bl + threadIdx.x; m < nm; m += blockDim.x) side[moves[m]] ^= 1;
+    for (int32_t m = bl + threadIdx.x; m < nm; m += blockDim.x) stb[4 * moves[m]] ^= 1;
     __syncthreads();
-    if (threadIdx.x == 0) {
-      if (nm > bl) {
-        s_cut = rec[3 * bl];
-        s_sw[0] = rec[3 * bl + 1];
-        s_sw[1] = rec[3 * bl + 2];
-      }
+    if (threadIdx.x == 0) {  // the state after the best prefix (partition.cpp:150-156)
+      s_cut = s_best_cut;
+      s_sw[0] = s_best_s[0];
+      s_sw[1] = s_best_s[1];
       const bool improved = s_best_cut < s_pass_cut ||
                             (s_best_cut == s_pass_cut &&
-                             fm_imb_less(s_best_s[0], s_best_s[1], s_pass_s[0], s_pass_s[1], exact_int));
+                             fm_imb_less<EXACT>(s_best_s[0], s_best_s[1], s_pass_s[0], s_pass_s[1]));
       s_stop = improved ? 0 : 1;
     }
     __syncthreads();
     if (s_stop) break;
   }
-  for (int32_t i = threadIdx.x; i < np; i += blockDim.x) a.side[pl[i]] = side[i];
+  for (int32_t i = threadIdx.x; i < np; i += blockDim.x) a.side[pl[i]] = static_cast<uint8_t>(side(i));
   if (threadIdx.x == 0) atomicAdd(&a.stats[0], static_cast<unsigned long long>(total_moves));
+}
+
+// Shared-memory bytes of a node's FM state + packed adjacency (fm_node<SM>).
+__host__ __device__ inline int64_t fm_node_smem(int64_t np, int64_t entries) {
+  return ((20 * np + 15) & ~int64_t(15)) + 4 * entries + 16;
+}
+
+// EXACT: integer feasibility (n < 2^26).  32-bit keys imply < 65536 patches
+// and edge weights < 32768, so a node whose state fits uses the packed
+// shared-memory layout; 64-bit-key nodes always use the global layout.
+template <class K, bool EXACT>
+__global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
+  const int32_t li = blockIdx.x;
+  if (!a.active[li]) return;
+  const int32_t pbeg = a.poff[li], np = a.poff[li + 1] - pbeg;
+  if constexpr (sizeof(K) == 4) {
+    const int64_t e_node = (a.fm_fifo_off[li + 1] - a.fm_fifo_off[li]) - np;
+    if (fm_node_smem(np, e_node) <= a.fm_smem_bytes) {
+      fm_node<K, EXACT, true>(a, li, pbeg, np);
+      return;
+    }
+  }
+  fm_node<K, EXACT, false>(a, li, pbeg, np);
 }
 
 // largest total quotient edge weight of a patch: bounds |gain| for the key width
@@ -1161,9 +1185,8 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
   DevBuf<int32_t> pw(Pm, s), pnode(Pm, s), lidx(Pm, s), flag(Pm, s), pkey(Pm, s), pkey_out(Pm, s);
   DevBuf<int32_t> alive_p(Pm, s), plist(Pm, s), fm_gain(Pm, s), fm_moves(Pm, s), cnt(4, s);
   DevBuf<unsigned long long> stats(2, s);
-  DevBuf<int64_t> fm_rec(3LL * Pm, s);
-  DevBuf<int32_t> fm_w(Pm, s), fm_ab(Pm, s), fm_ae(Pm, s);
-  DevBuf<uint8_t> fm_side(3LL * Pm, s);
+  DevBuf<int32_t> fm_w(Pm, s), fm_ab(2LL * Pm, s), fm_ae(1, s);
+  DevBuf<uint8_t> fm_side(4LL * Pm, s);
   DevBuf<int32_t> slot_of(std::max(n, 1), s), ref_pull(std::max(n, 1), s), ref_pulled(std::max(n, 1), s);
   DevBuf<uint8_t> ref_own(std::max(n, 1), s), ref_in(std::max(n, 1), s);
   DevBuf<int8_t> region(std::max(n, 1), s);
@@ -1208,7 +1231,7 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     a.fm_w = fm_w, a.fm_ab = fm_ab, a.fm_ae = fm_ae, a.fm_side = fm_side;
     a.slot_of = slot_of, a.ref_pull = ref_pull, a.ref_own = ref_own, a.ref_in = ref_in, a.ref_pulled = ref_pulled;
     a.vside = vside, a.ell = ell;
-    a.stats = ctx.dwork ? ctx.dwork + 1 : stats.get(), a.fm_gain = fm_gain, a.fm_moves = fm_moves, a.fm_rec = fm_rec;
+    a.stats = ctx.dwork ? ctx.dwork + 1 : stats.get(), a.fm_gain = fm_gain, a.fm_moves = fm_moves;
     const dim3 lgrid(std::max(1, grid_for(ctx, n) / std::max(1, width)), std::min(width, 65535));
     MP_KERNEL(ctx, level_weights<<<lgrid, 256, 0, s>>>(a));
     MP_KERNEL(ctx, level_patch_counts<<<grid_for(ctx, P), 256, 0, s>>>(a));
@@ -1279,7 +1302,7 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     DevBuf<int32_t> qloc(std::max<int64_t>(U, 1), s);
     if (U > 0) MP_KERNEL(ctx, local_adjacency<<<grid_for(ctx, U), 256, 0, s>>>(static_cast<int32_t>(U), qnbr, lidx, qloc));
     a.qloc = qloc;
-    size_t fm_smem = static_cast<size_t>(std::min(maxnp, kFmSmemPatches)) * kFmBytesPerPatch + 512;
+    size_t fm_smem = 1024;
     {
       // room for the packed adjacency of the largest node that fits
       std::vector<int64_t> hfo(width + 1);
@@ -1290,14 +1313,13 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
       size_t need = 0;
       for (int32_t i = 0; i < width; ++i) {
         const int64_t np_i = hpo[i + 1] - hpo[i];
-        if (np_i == 0 || np_i > kFmSmemPatches) continue;
-        const int64_t e_i = (hfo[i + 1] - hfo[i]) - np_i;
-        need = std::max<size_t>(need, static_cast<size_t>(np_i) * kFmBytesPerPatch + 4 * e_i + 1024);
+        if (np_i == 0) continue;
+        need = std::max<size_t>(need, static_cast<size_t>(fm_node_smem(np_i, (hfo[i + 1] - hfo[i]) - np_i)));
       }
       // opt-in limit minus the kernels' static shared memory
       cudaFuncAttributes fa32{}, fa64{};
-      MP_CUDA(cudaFuncGetAttributes(&fa32, fm_kernel<uint32_t>));
-      MP_CUDA(cudaFuncGetAttributes(&fa64, fm_kernel<uint64_t>));
+      MP_CUDA(cudaFuncGetAttributes(&fa32, fm_kernel<uint32_t, true>));
+      MP_CUDA(cudaFuncGetAttributes(&fa64, fm_kernel<uint64_t, false>));
       const size_t cap = static_cast<size_t>(ctx.smem_optin) - std::max(fa32.sharedSizeBytes, fa64.sharedSizeBytes);
       fm_smem = std::min<size_t>(std::max(fm_smem, need), cap);
     }
@@ -1312,17 +1334,15 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
       MP_CUDA(cudaStreamSynchronize(s));
     }
     const bool k32 = maxnp < 65536 && hgb < 32768;
-    if (k32) {
-      allow_max_smem(fm_kernel<uint32_t>, ctx.device);
+    const bool exact = n < kFmExactWeights;  // node weights < 2^26: integer feasibility
+    auto launch_fm = [&](auto kernel) {
+      allow_max_smem(kernel, ctx.device);
       const int kt__ = ctx.ktime_begin(kKFm);
-      MP_KERNEL(ctx, fm_kernel<uint32_t><<<width, kFmThreads, fm_smem, s>>>(a));
+      MP_KERNEL(ctx, kernel<<<width, kFmThreads, fm_smem, s>>>(a));
       ctx.ktime_end(kt__);
-    } else {
-      allow_max_smem(fm_kernel<uint64_t>, ctx.device);
-      const int kt__ = ctx.ktime_begin(kKFm);
-      MP_KERNEL(ctx, fm_kernel<uint64_t><<<width, kFmThreads, fm_smem, s>>>(a));
-      ctx.ktime_end(kt__);
-    }
+    };
+    if (k32) exact ? launch_fm(fm_kernel<uint32_t, true>) : launch_fm(fm_kernel<uint32_t, false>);
+    else exact ? launch_fm(fm_kernel<uint64_t, true>) : launch_fm(fm_kernel<uint64_t, false>);
     st.mark("level/fm");
     MP_KERNEL(ctx, super_pass<<<lgrid, 256, 0, s>>>(a));
     const size_t ref_smem = static_cast<size_t>(kRefSmemList) * 10;
