@@ -53,6 +53,7 @@ struct BatchArgs {
   uint64_t seed;
   int32_t* dist;
   uint64_t* tkey;          // ntile tile maxima
+  int32_t* smax;           // n/32 subtile maximum distances (refreshed with the tiles)
   uint32_t* tbits;         // touched tiles
   int32_t* tlist;          // ntile
   int32_t* vis;            // W * n private visit tokens
@@ -116,6 +117,8 @@ __device__ void bitonic_desc(uint64_t* s, int32_t m) {
 // Leader: the downward-closed candidate list of this batch.
 __device__ void select_candidates(const BatchArgs& a, int32_t W, uint64_t* sS, int32_t* hist, int32_t* shi) {
   __shared__ int32_t s_n, s_thr;
+  int32_t* ssub = hist;                   // subtile list (reuses the histogram, kBins >= kSCap)
+  __shared__ int32_t scnt[kMaxWorkers];   // exact mode: per-subtile counts / offsets
   __shared__ uint64_t red[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int32_t tsize = 1 << a.tile_shift;
@@ -127,8 +130,14 @@ __device__ void select_candidates(const BatchArgs& a, int32_t W, uint64_t* sS, i
   while ((mx >> shift) >= static_cast<uint64_t>(kBins)) ++shift;
   for (int32_t b = threadIdx.x; b < kBins; b += blockDim.x) hist[b] = 0;
   __syncthreads();
-  for (int32_t t = threadIdx.x; t < a.ntile; t += blockDim.x)
-    atomicAdd(&hist[static_cast<int32_t>((__ldcg(&a.tkey[t]) >> 32) >> shift)], 1);
+  // late batches put most tiles in a few bins: one shared atomic per distinct
+  // bin per warp instead of one per tile
+  for (int32_t t0 = 0; t0 < a.ntile; t0 += blockDim.x) {
+    const int32_t t = t0 + threadIdx.x;
+    const int32_t b = t < a.ntile ? static_cast<int32_t>((__ldcg(&a.tkey[t]) >> 32) >> shift) : -1;
+    const uint32_t m = __match_any_sync(0xffffffffu, b);
+    if (b >= 0 && lane == __ffs(m) - 1) atomicAdd(&hist[b], __popc(m));
+  }
   __syncthreads();
   // the highest bin b where the suffix count reaches W: tiles in bins > b are
   // fewer than W and form the threshold; if there are none, the top bin's
@@ -164,78 +173,99 @@ __device__ void select_candidates(const BatchArgs& a, int32_t W, uint64_t* sS, i
   }
   if (threadIdx.x == 0) s_n = 0;
   __syncthreads();
-  if (!exact) {
-    for (int32_t t = wid; t < a.ntile; t += nwarp) {
-      if (static_cast<int64_t>(__ldcg(&a.tkey[t]) >> 32) < thr_d) continue;
-      const int32_t lo = t * tsize, hi = min(a.n, lo + tsize);
-      for (int32_t v = lo + lane; v < hi; v += 32) {
-        const int32_t dv = __ldcg(&a.dist[v]);
-        if (dv >= thr_d) {
-          const int32_t slot = atomicAdd(&s_n, 1);
-          if (slot < kSCap) sS[slot] = vkey(dv, v);
-        }
-      }
-    }
-    __syncthreads();
-    if (s_n > kSCap) {  // a non-tie set cannot be truncated: exact-max rule instead
-      thr_d = static_cast<int64_t>(mx);
-      exact = true;
-    }
-    __syncthreads();
-    if (exact && threadIdx.x == 0) s_n = 0;
-    __syncthreads();
-  }
-  if (exact) {
-    // ties at the maximum distance, truncated in ascending id order: compact
-    // the tiles at that distance in order, then take them 32 at a time (one
-    // warp per tile) with a block scan of their match counts
+  // Candidates: every vertex with dist >= thr_d (or, in exact mode, the first
+  // W vertices in id order with dist == thr_d).  Tiles at or above the
+  // threshold are compacted in order, then their 32-vertex subtiles whose
+  // maximum qualifies, then those subtiles are swept one warp each.
+  for (int pass = 0; pass < 2; ++pass) {
+    const bool ex = exact;
     int32_t* tl = a.tscratch;
-    int32_t run = 0;
+    int32_t nq = 0;
     for (int32_t t0 = 0; t0 < a.ntile; t0 += blockDim.x) {
       const int32_t t = t0 + threadIdx.x;
-      const int32_t f = (t < a.ntile && static_cast<int64_t>(__ldcg(&a.tkey[t]) >> 32) == thr_d) ? 1 : 0;
+      int32_t f = 0;
+      if (t < a.ntile) {
+        const int64_t td = static_cast<int64_t>(__ldcg(&a.tkey[t]) >> 32);
+        f = ex ? td == thr_d : td >= thr_d;
+      }
       int32_t tt;
       const int32_t e = block_excl_scan(f, shi, &tt);
-      if (f) tl[run + e] = t;
-      run += tt;
+      if (f) tl[nq + e] = t;
+      nq += tt;
     }
-    const int32_t nflag = run;
-    int32_t filled = 0;
-    const int32_t cap = min(W, kSCap);  // only the first W ties in id order can become candidates
-    for (int32_t c0 = 0; c0 < nflag && filled < cap; c0 += nwarp) {
-      if (threadIdx.x == 0 && a.work) atomicAdd(&a.work[15], 1ull);
-      const int32_t ci = c0 + wid;
-      int32_t cntw = 0;
-      uint32_t masks[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // up to 256 vertices per tile chunk pass
-      int32_t t = -1, lo = 0, hi = 0;
-      if (ci < nflag) {
-        t = __ldcg(&tl[ci]);
-        lo = t * tsize;
-        hi = min(a.n, lo + tsize);
+    __syncthreads();
+    // qualifying subtiles, in order (capacity: kSCap; exact mode needs only W)
+    const int32_t spt = tsize >> 5;  // subtiles per tile
+    const int32_t cap_sub = ex ? min(W, kSCap) : kSCap;
+    int32_t nsub = 0;
+    for (int64_t q0 = 0; q0 < static_cast<int64_t>(nq) * spt && nsub < cap_sub; q0 += blockDim.x) {
+      const int64_t q = q0 + threadIdx.x;
+      int32_t f = 0, sub = 0;
+      if (q < static_cast<int64_t>(nq) * spt) {
+        sub = __ldcg(&tl[q / spt]) * spt + static_cast<int32_t>(q % spt);
+        if ((static_cast<int64_t>(sub) << 5) < a.n) {
+          const int64_t sd = __ldcg(&a.smax[sub]);
+          f = ex ? sd == thr_d : sd >= thr_d;
+        }
       }
-      // count matches of this warp's tile (tiles larger than 256 are walked in passes)
-      for (int32_t v0 = lo; v0 < hi; v0 += 32) {
-        const int32_t v = v0 + lane;
-        const bool take = v < hi && __ldcg(&a.dist[v]) == thr_d;
-        cntw += __popc(__ballot_sync(0xffffffffu, take));
+      int32_t tt;
+      const int32_t e = block_excl_scan(f, shi, &tt);
+      if (f && nsub + e < cap_sub) ssub[nsub + e] = sub;
+      nsub += tt;
+    }
+    if (!ex && nsub > cap_sub) {  // more than kSCap candidates: the exact-max rule instead
+      __syncthreads();
+      thr_d = static_cast<int64_t>(mx);
+      exact = true;
+      continue;
+    }
+    nsub = min(nsub, cap_sub);
+    __syncthreads();
+    if (!ex) {
+      for (int32_t k = wid; k < nsub; k += nwarp) {
+        const int32_t v = (ssub[k] << 5) + lane;
+        const int32_t dv = v < a.n ? __ldcg(&a.dist[v]) : -1;
+        const bool take = dv >= thr_d;
+        const int32_t slot = warp_append(&s_n, take);
+        if (take && slot < kSCap) sS[slot] = vkey(dv, v);
       }
-      (void)masks;
-      int32_t tot2;
-      const int32_t warp_base = block_excl_scan(lane == 0 ? cntw : 0, shi, &tot2);
-      const int32_t wb = __shfl_sync(0xffffffffu, warp_base, 0);
-      int32_t pos = filled + wb;
-      for (int32_t v0 = lo; v0 < hi && pos < cap; v0 += 32) {
-        const int32_t v = v0 + lane;
-        const int32_t dv = v < hi ? __ldcg(&a.dist[v]) : -1;
+      __syncthreads();
+      if (s_n > kSCap) {  // a non-tie set cannot be truncated: the exact-max rule instead
+        thr_d = static_cast<int64_t>(mx);
+        exact = true;
+        __syncthreads();
+        if (threadIdx.x == 0) s_n = 0;
+        __syncthreads();
+        continue;
+      }
+    } else {
+      // ties at the maximum, truncated in ascending id order: per-subtile
+      // counts, one block scan (<= W subtiles), then ordered writes
+      int32_t cnt = 0;
+      for (int32_t k = wid; k < nsub; k += nwarp) {
+        const int32_t v = (ssub[k] << 5) + lane;
+        const int32_t c = __popc(__ballot_sync(0xffffffffu, v < a.n && __ldcg(&a.dist[v]) == thr_d));
+        if (lane == 0) scnt[k] = c;
+      }
+      __syncthreads();
+      if (threadIdx.x < nsub) cnt = scnt[threadIdx.x];
+      int32_t tt;
+      const int32_t base = block_excl_scan(cnt, shi, &tt);
+      if (threadIdx.x < nsub) scnt[threadIdx.x] = base;
+      __syncthreads();
+      const int32_t capv = min(W, kSCap);
+      for (int32_t k = wid; k < nsub; k += nwarp) {
+        const int32_t v = (ssub[k] << 5) + lane;
+        const int32_t dv = v < a.n ? __ldcg(&a.dist[v]) : -1;
         const bool take = dv == thr_d;
         const uint32_t m = __ballot_sync(0xffffffffu, take);
-        const int32_t p2 = pos + __popc(m & ((1u << lane) - 1));
-        if (take && p2 < cap) sS[p2] = vkey(dv, v);
-        pos += __popc(m);
+        const int32_t pos = scnt[k] + __popc(m & ((1u << lane) - 1));
+        if (take && pos < capv) sS[pos] = vkey(dv, v);
       }
-      filled += tot2;
+      if (threadIdx.x == 0) s_n = min(tt, capv);
+      if (threadIdx.x == 0 && a.work) atomicAdd(&a.work[15], 1ull);
     }
-    if (threadIdx.x == 0) s_n = min(filled, cap);
+    break;
   }
   __syncthreads();
   const int32_t ns = min(s_n, kSCap);
@@ -318,11 +348,11 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
           const int32_t j = static_cast<int32_t>(e >> 32);
           int32_t* jvis = a.vis + static_cast<int64_t>(j) * a.n;
           int32_t* jdw = a.dw + static_cast<int64_t>(j) * a.n;
+          uint64_t mk = 0;  // largest key this lane claims (the region's max key, mkey)
           auto claim = [&](int32_t w) -> bool {
             if (d + 1 < __ldcg(&a.dist[w]) && atomicExch(&jvis[w], token) != token) {
               jdw[w] = d + 1;
-              atomicMax(reinterpret_cast<unsigned long long*>(&a.mkey[j]),
-                        static_cast<unsigned long long>(vkey(d + 1, w)));
+              mk = max(mk, vkey(d + 1, w));
               return true;
             }
             return false;
@@ -336,6 +366,13 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
               const int32_t w = a.g.nbr[q];
               if (claim(w)) a.glist[lnext + atomicAdd(cout, 1)] = (static_cast<uint64_t>(j) << 32) | static_cast<uint32_t>(w);
             }
+          }
+          // one atomic per warp when its lanes share the candidate (always with one)
+          if (__match_any_sync(0xffffffffu, j) == 0xffffffffu) {
+            const uint64_t gm = warp_max_u64(mk);
+            if (lane == 0 && gm) atomicMax(reinterpret_cast<unsigned long long*>(&a.mkey[j]), static_cast<unsigned long long>(gm));
+          } else if (mk) {
+            atomicMax(reinterpret_cast<unsigned long long*>(&a.mkey[j]), static_cast<unsigned long long>(mk));
           }
         }
         grid.sync();
@@ -469,7 +506,13 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
         const int32_t t = __ldcg(&a.tlist[i]);
         uint64_t best = 0;
         const int32_t lo = t * tsize, hi = min(a.n, lo + tsize);
-        for (int32_t v = lo + lane; v < hi; v += 32) best = max(best, vkey(__ldcg(&a.dist[v]), v));
+        for (int32_t v0 = lo; v0 < hi; v0 += 32) {  // one 32-vertex subtile per step
+          const int32_t v = v0 + lane;
+          const int32_t dv = v < hi ? __ldcg(&a.dist[v]) : -1;
+          if (v < hi) best = max(best, vkey(dv, v));
+          const int32_t sm = __reduce_max_sync(0xffffffffu, dv);
+          if (lane == 0) a.smax[v0 >> 5] = sm;
+        }
         best = warp_max_u64(best);
         if (lane == 0) {
           a.tkey[t] = best;
@@ -537,7 +580,7 @@ void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32
   DevBuf<int32_t> tlist(ntile, s), cand(kSCap, s), regn(kMaxWorkers, s), ctl(16, s);
   DevBuf<uint64_t> tkey(ntile, s), ckey(kSCap, s), mkey(kMaxWorkers, s);
   DevBuf<uint32_t> tbits(ntile / 32 + 1, s), inm(kMaxWorkers * kMaskWords, s);
-  DevBuf<int32_t> tscratch(ntile, s), bar(1, s);
+  DevBuf<int32_t> tscratch(ntile, s), bar(1, s), smax(n / 32 + 1, s);
   MP_CUDA(cudaMemsetAsync(bar, 0, sizeof(int32_t), s));
   MP_CUDA(cudaMemsetAsync(inm, 0, sizeof(uint32_t) * inm.n, s));
   MP_CUDA(cudaMemsetAsync(vis, 0, sizeof(int32_t) * wn, s));
@@ -549,6 +592,7 @@ void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32
   a.work = ctx.dwork;
   a.glist = glist;
   a.tscratch = tscratch;
+  a.smax = smax;
   a.bar = reinterpret_cast<unsigned int*>(bar.get());
   a.grid_radius = grid_radius;
   a.grid_cands = grid_cands;
