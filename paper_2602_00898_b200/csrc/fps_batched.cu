@@ -38,6 +38,7 @@ constexpr int kFront = 4096;      // smem frontier per buffer in a worker
 constexpr int kMaxWorkers = 256;  // candidates per batch (bit-matrix width)
 constexpr int kMaskWords = kMaxWorkers / 32;
 constexpr int kGridCands = 64;    // candidates per grid-mode batch
+constexpr int kMaxDepth = 250;    // worker BFS depth bound (< the grid radius, clamped to it)
 
 __host__ __device__ inline uint64_t splitmix64(uint64_t x) {  // patching.cpp:17-22
   x += 0x9e3779b97f4a7c15ULL;
@@ -56,9 +57,9 @@ struct BatchArgs {
   int32_t* smax;           // n/32 subtile maximum distances (refreshed with the tiles)
   uint32_t* tbits;         // touched tiles
   int32_t* tlist;          // ntile
-  int32_t* vis;            // W * n private visit tokens
-  int32_t* dw;             // W * n private distances
-  int32_t* reg;            // W * n region lists
+  uint32_t* vm;            // n * kMaskWords visit bits: bit j of vertex v = v is in region j this batch
+  int32_t* dw;             // grid-mode distances, grid_cands * n
+  int32_t* reg;            // W * n worker region lists (level-ordered)
   int32_t* cand;           // kSCap
   uint64_t* ckey;          // kSCap
   uint64_t* mkey;          // kMaxWorkers: largest key a region leaves
@@ -300,9 +301,10 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
   __shared__ int32_t s_acc[kMaxWorkers];
   unsigned long long scans = 0;
   const int32_t W = min(static_cast<int32_t>(gridDim.x), kMaxWorkers);
-  int32_t* my_vis = a.vis + static_cast<int64_t>(blockIdx.x) * a.n;
-  int32_t* my_dw = a.dw + static_cast<int64_t>(blockIdx.x) * a.n;
   int32_t* my_reg = a.reg + static_cast<int64_t>(blockIdx.x) * a.n;
+  const int32_t my_word = static_cast<int32_t>(blockIdx.x) >> 5;
+  const uint32_t my_bit = 1u << (blockIdx.x & 31);
+  __shared__ int32_t s_lstart[kMaxDepth + 2], s_nlev;  // worker: region-list offset of each BFS level
 
   for (int64_t v = gtid; v < a.n; v += gthreads) a.dist[v] = kUnreached;
   if (gtid == 0) {
@@ -316,13 +318,12 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
     // whole grid (one grid barrier per level, entries (cand, vertex) appended
     // to one list).  Small radii: one worker CTA per candidate.
     const int32_t nc = __ldcg(&a.ctl[1]);
-    const int32_t token = batch + 1;
     const bool gridmode = __ldcg(&a.ctl[3]) != 0;
     long long t_reg0 = clock64();
     if (gridmode) {
       for (int32_t j = static_cast<int32_t>(gtid); j < nc; j += static_cast<int32_t>(gthreads)) {
         const int32_t c = __ldcg(&a.cand[j]);
-        a.vis[static_cast<int64_t>(j) * a.n + c] = token;
+        atomicOr(&a.vm[static_cast<int64_t>(c) * kMaskWords + (j >> 5)], 1u << (j & 31));
         a.dw[static_cast<int64_t>(j) * a.n + c] = 0;
         a.glist[j] = (static_cast<uint64_t>(j) << 32) | static_cast<uint32_t>(c);
         a.mkey[j] = vkey(0, c);
@@ -346,11 +347,12 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
             x = a.ell[static_cast<int64_t>(static_cast<uint32_t>(e)) * 8 + (it & 7)];
           }
           const int32_t j = static_cast<int32_t>(e >> 32);
-          int32_t* jvis = a.vis + static_cast<int64_t>(j) * a.n;
           int32_t* jdw = a.dw + static_cast<int64_t>(j) * a.n;
+          const int32_t jword = j >> 5;
+          const uint32_t jbit = 1u << (j & 31);
           uint64_t mk = 0;  // largest key this lane claims (the region's max key, mkey)
           auto claim = [&](int32_t w) -> bool {
-            if (d + 1 < __ldcg(&a.dist[w]) && atomicExch(&jvis[w], token) != token) {
+            if (d + 1 < __ldcg(&a.dist[w]) && !(atomicOr(&a.vm[static_cast<int64_t>(w) * kMaskWords + jword], jbit) & jbit)) {
               jdw[w] = d + 1;
               mk = max(mk, vkey(d + 1, w));
               return true;
@@ -382,7 +384,7 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
       if (gtid == 0) a.ctl[8] = lbeg;  // entries in glist
       for (int32_t q = static_cast<int32_t>(gtid); q < nc * nc; q += static_cast<int32_t>(gthreads)) {
         const int32_t i = q / nc, j = q % nc;
-        if (__ldcg(&a.vis[static_cast<int64_t>(i) * a.n + __ldcg(&a.cand[j])]) == token)
+        if ((__ldcg(&a.vm[static_cast<int64_t>(__ldcg(&a.cand[j])) * kMaskWords + (i >> 5)]) >> (i & 31)) & 1u)
           atomicOr(&a.inm[i * kMaskWords + (j >> 5)], 1u << (j & 31));
       }
     } else if (static_cast<int32_t>(blockIdx.x) < nc) {
@@ -390,9 +392,9 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
       int32_t* sf0 = reinterpret_cast<int32_t*>(bsm);
       int32_t* sf1 = sf0 + kFront;
       if (threadIdx.x == 0) {
-        my_vis[c] = token;
-        my_dw[c] = 0;
+        atomicOr(&a.vm[static_cast<int64_t>(c) * kMaskWords + my_word], my_bit);
         my_reg[0] = c;
+        s_lstart[0] = 0;
         sf0[0] = c;
         s_cnt[0] = 1, s_cnt[1] = 0, s_cnt[2] = 0;
         s_n = 1;  // region size
@@ -401,12 +403,16 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
       uint64_t mk = vkey(0, c);
       for (int32_t d = 0;; ++d) {
         const int32_t nf = s_cnt[d % 3];
-        if (nf == 0) break;
+        if (nf == 0) {
+          if (threadIdx.x == 0) s_nlev = d;
+          break;
+        }
         if (threadIdx.x == 0) s_cnt[(d + 2) % 3] = 0;
         const int32_t* fin = (d & 1) ? sf1 : sf0;
         int32_t* fout = (d & 1) ? sf0 : sf1;
         const int32_t rbase = s_n - nf;  // this level's vertices end the region list
         const int32_t rtop = s_n;
+        if (threadIdx.x == 0) s_lstart[d + 1] = rtop;  // depth d+1 entries start here
         int32_t* cout = &s_cnt[(d + 1) % 3];
         const int32_t items = nf * 8;
         for (int32_t it = threadIdx.x; it < items; it += blockDim.x) {
@@ -414,8 +420,8 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
           const int32_t u = i < kFront ? fin[i] : __ldcg(&my_reg[rbase + i]);
           const int32_t x = a.ell[static_cast<int64_t>(u) * 8 + (it & 7)];
           auto relax = [&](int32_t w) {
-            if (d + 1 < __ldcg(&a.dist[w]) && atomicExch(&my_vis[w], token) != token) {
-              my_dw[w] = d + 1;
+            if (d + 1 < __ldcg(&a.dist[w]) &&
+                !(atomicOr(&a.vm[static_cast<int64_t>(w) * kMaskWords + my_word], my_bit) & my_bit)) {
               const int32_t slot = atomicAdd(cout, 1);
               if (slot < kFront) fout[slot] = w;
               my_reg[rtop + slot] = w;
@@ -435,7 +441,7 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
       }
       mk = block_max_u64(mk, s_red);
       for (int32_t j = threadIdx.x; j < kMaxWorkers; j += blockDim.x) {
-        const bool in = j < nc && __ldcg(&my_vis[__ldcg(&a.cand[j])]) == token;
+        const bool in = j < nc && (__ldcg(&a.vm[static_cast<int64_t>(__ldcg(&a.cand[j])) * kMaskWords + my_word]) & my_bit);
         const uint32_t bits = __ballot_sync(0xffffffffu, in);
         if (lane == 0) a.inm[blockIdx.x * kMaskWords + (j >> 5)] = bits;
       }
@@ -473,6 +479,7 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
       for (int32_t q = static_cast<int32_t>(gtid); q < ne; q += static_cast<int32_t>(gthreads)) {
         const uint64_t e = __ldcg(&a.glist[q]);
         const int32_t j = static_cast<int32_t>(e >> 32), w = static_cast<int32_t>(static_cast<uint32_t>(e));
+        a.vm[static_cast<int64_t>(w) * kMaskWords + (j >> 5)] = 0;  // every region is finished: clear its bits
         if (!s_acc[j]) continue;
         atomicMin(&a.dist[w], __ldcg(&a.dw[static_cast<int64_t>(j) * a.n + w]));
         const int32_t t = w >> a.tile_shift;
@@ -480,11 +487,21 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
         if (!(atomicOr(&a.tbits[t >> 5], bit) & bit)) a.tlist[atomicAdd(&a.ctl[2], 1)] = t;
         scans += a.g.off[w + 1] - a.g.off[w];
       }
-    } else if (static_cast<int32_t>(blockIdx.x) < nc && s_acc[blockIdx.x]) {
+    } else if (static_cast<int32_t>(blockIdx.x) < nc) {
       const int32_t rn = __ldcg(&a.regn[blockIdx.x]);
+      const bool acc = s_acc[blockIdx.x] != 0;
+      const int32_t nlev = s_nlev;
       for (int32_t i = threadIdx.x; i < rn; i += blockDim.x) {
-        const int32_t w = my_reg[i];
-        atomicMin(&a.dist[w], my_dw[w]);
+        const int32_t w = __ldcg(&my_reg[i]);
+        a.vm[static_cast<int64_t>(w) * kMaskWords + my_word] = 0;  // clear (every worker's region is finished)
+        if (!acc) continue;
+        int32_t lo = 0, hi = nlev - 1;  // depth of entry i: last level starting at or before i
+        while (lo < hi) {
+          const int32_t mid = (lo + hi + 1) >> 1;
+          if (s_lstart[mid] <= i) lo = mid;
+          else hi = mid - 1;
+        }
+        atomicMin(&a.dist[w], lo);
         const int32_t t = w >> a.tile_shift;
         const uint32_t bit = 1u << (t & 31);
         if (!(atomicOr(&a.tbits[t >> 5], bit) & bit)) a.tlist[atomicAdd(&a.ctl[2], 1)] = t;
@@ -549,7 +566,9 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
 void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32_t k, uint64_t seed, int32_t* seeds,
                      int32_t* dist) {
   const char* gr = getenv("MP_FPS_GRID_RADIUS");  // tuning knobs
-  const int32_t grid_radius = gr ? atoi(gr) : 200;
+  // worker-mode regions are shallower than the grid radius (their depth is
+  // below the candidate's distance): kMaxDepth bounds the per-level offsets
+  const int32_t grid_radius = std::min(gr ? atoi(gr) : 200, kMaxDepth);
   const char* gc = getenv("MP_FPS_GRID_CANDS");
   const int32_t grid_cands = std::max(1, std::min(gc ? atoi(gc) : 1, kGridCands));
   cudaStream_t s = ctx.stream;
@@ -563,31 +582,32 @@ void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32
   MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, fps_batched_kernel, kThreads, smem));
   if (bpsm < 1) throw Error(MP_ECUDA, "fps_batched_kernel does not fit on an SM");
   // workers: one per SM, bounded by the bit-matrix width and by memory
-  // (12 bytes/vertex each); decided once per context
+  // (a 4-byte region list per vertex each); decided once per context
   if (ctx.fps_workers == 0) {
     int W0 = std::min(ctx.num_sms, kMaxWorkers);
     size_t free_b = 0, total_b = 0;
     MP_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    while (W0 > 1 && 20ull * n * W0 > free_b / 2) W0 /= 2;
+    while (W0 > 1 && 4ull * n * W0 > free_b / 2) W0 /= 2;
     ctx.fps_workers = W0;
   }
   const int W = ctx.fps_workers;
   const int64_t wn = static_cast<int64_t>(W) * n;
-  int32_t* vis = static_cast<int32_t*>(ctx.slab(0, sizeof(int32_t) * wn));
-  int32_t* dw = static_cast<int32_t*>(ctx.slab(1, sizeof(int32_t) * wn));
+  // visit bits: 32 bytes per vertex, shared by all regions (L2-resident at 1M)
+  uint32_t* vm = static_cast<uint32_t*>(ctx.slab(0, sizeof(uint32_t) * kMaskWords * static_cast<int64_t>(n)));
+  int32_t* dw = static_cast<int32_t*>(ctx.slab(1, sizeof(int32_t) * static_cast<int64_t>(grid_cands) * n));
   int32_t* reg = static_cast<int32_t*>(ctx.slab(2, sizeof(int32_t) * wn));
-  uint64_t* glist = static_cast<uint64_t*>(ctx.slab(3, sizeof(uint64_t) * (static_cast<int64_t>(std::min(W, kGridCands)) * n + 64)));
+  uint64_t* glist = static_cast<uint64_t*>(ctx.slab(3, sizeof(uint64_t) * (static_cast<int64_t>(grid_cands) * n + 64)));
   DevBuf<int32_t> tlist(ntile, s), cand(kSCap, s), regn(kMaxWorkers, s), ctl(16, s);
   DevBuf<uint64_t> tkey(ntile, s), ckey(kSCap, s), mkey(kMaxWorkers, s);
   DevBuf<uint32_t> tbits(ntile / 32 + 1, s), inm(kMaxWorkers * kMaskWords, s);
   DevBuf<int32_t> tscratch(ntile, s), bar(1, s), smax(n / 32 + 1, s);
   MP_CUDA(cudaMemsetAsync(bar, 0, sizeof(int32_t), s));
   MP_CUDA(cudaMemsetAsync(inm, 0, sizeof(uint32_t) * inm.n, s));
-  MP_CUDA(cudaMemsetAsync(vis, 0, sizeof(int32_t) * wn, s));
+  MP_CUDA(cudaMemsetAsync(vm, 0, sizeof(uint32_t) * kMaskWords * static_cast<int64_t>(n), s));
   MP_CUDA(cudaMemsetAsync(tbits, 0, sizeof(uint32_t) * tbits.n, s));
   BatchArgs a{};
   a.g = g, a.ell = ell, a.n = n, a.k = k, a.tile_shift = tile_shift, a.ntile = ntile, a.seed = seed;
-  a.dist = dist, a.tkey = tkey, a.tbits = tbits, a.tlist = tlist, a.vis = vis, a.dw = dw, a.reg = reg;
+  a.dist = dist, a.tkey = tkey, a.tbits = tbits, a.tlist = tlist, a.vm = vm, a.dw = dw, a.reg = reg;
   a.cand = cand, a.ckey = ckey, a.mkey = mkey, a.inm = inm, a.regn = regn, a.ctl = ctl, a.seeds = seeds;
   a.work = ctx.dwork;
   a.glist = glist;
