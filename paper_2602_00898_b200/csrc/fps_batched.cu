@@ -35,7 +35,9 @@ constexpr int kThreads = 1024;
 constexpr int kBins = 4096;       // tile-max dist histogram (distances binned by >> shift)
 constexpr int kSCap = 4096;       // candidate list capacity
 constexpr int kFront = 4096;      // smem frontier per buffer in a worker
-constexpr int kMaxWorkers = 256;  // candidates per batch (bit-matrix width)
+constexpr int kMaxWorkers = 640;  // candidates per batch (bit-matrix width)
+constexpr int kMaxSub = 4;        // worker groups per CTA when regions are small
+constexpr int kSubRegion = 4096;  // ... i.e. when the last batch's largest region was below this
 constexpr int kMaskWords = kMaxWorkers / 32;
 constexpr int kGridCands = 64;    // candidates per grid-mode batch
 constexpr int kMaxDepth = 250;    // worker BFS depth bound (< the grid radius, clamped to it)
@@ -66,6 +68,7 @@ struct BatchArgs {
   uint32_t* inm;           // kMaxWorkers * kMaskWords membership bits
   int32_t* regn;           // kMaxWorkers region sizes
   int32_t* ctl;            // [0] seeds done [1] ncand [2] touched count [3] grid mode [4..6] level counters [8] glist size
+                           // [9] worker groups per CTA [10] list overflow [11] largest region
   uint64_t* glist;         // grid-mode region entries (cand << 32 | vertex)
   int32_t* tscratch;       // ntile: tiles at the tied maximum distance
   unsigned int* bar;       // grid barrier counter (zeroed before the launch)
@@ -300,15 +303,14 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
   __shared__ uint64_t s_red[32];
   __shared__ int32_t s_acc[kMaxWorkers];
   unsigned long long scans = 0;
-  const int32_t W = min(static_cast<int32_t>(gridDim.x), kMaxWorkers);
-  int32_t* my_reg = a.reg + static_cast<int64_t>(blockIdx.x) * a.n;
-  const int32_t my_word = static_cast<int32_t>(blockIdx.x) >> 5;
-  const uint32_t my_bit = 1u << (blockIdx.x & 31);
-  __shared__ int32_t s_lstart[kMaxDepth + 2], s_nlev;  // worker: region-list offset of each BFS level
+  // worker groups (per batch): nsub groups of G threads per CTA, one candidate each
+  __shared__ int32_t s_wcnt[kMaxSub][3], s_wn[kMaxSub], s_wnlev[kMaxSub];
+  __shared__ int32_t s_wlstart[kMaxSub][kMaxDepth + 2];  // region-list offset of each BFS level
 
   for (int64_t v = gtid; v < a.n; v += gthreads) a.dist[v] = kUnreached;
   if (gtid == 0) {
     a.ctl[0] = 0, a.ctl[2] = 0, a.ctl[1] = 1, a.ctl[3] = 1;  // batch 0: the start vertex, grid mode
+    a.ctl[9] = 1, a.ctl[10] = 0, a.ctl[11] = 0;
     a.cand[0] = static_cast<int32_t>(splitmix64(a.seed) % static_cast<uint64_t>(a.n));  // patching.cpp:32
     a.ckey[0] = ~0ull;
   }
@@ -317,9 +319,26 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
     // ---- 2. regions.  Large radii: all candidates advance together over the
     // whole grid (one grid barrier per level, entries (cand, vertex) appended
     // to one list).  Small radii: one worker CTA per candidate.
-    const int32_t nc = __ldcg(&a.ctl[1]);
     const bool gridmode = __ldcg(&a.ctl[3]) != 0;
+    int32_t nc, nsub, G, sub, gt, wk, my_word;
+    uint32_t my_bit;
+    int64_t reg_cap;
+    int32_t* my_reg;
     long long t_reg0 = clock64();
+    for (;;) {  // a worker whose region outgrows its list share: redo with one group per CTA
+    nc = __ldcg(&a.ctl[1]);
+    nsub = __ldcg(&a.ctl[9]);  // worker groups per CTA (1 or kMaxSub)
+    G = static_cast<int32_t>(blockDim.x) / nsub;
+    sub = static_cast<int32_t>(threadIdx.x) / G, gt = static_cast<int32_t>(threadIdx.x) - sub * G;
+    wk = static_cast<int32_t>(blockIdx.x) * nsub + sub;  // candidate of this group
+    my_word = wk >> 5;
+    my_bit = 1u << (wk & 31);
+    reg_cap = a.n / nsub;
+    my_reg = a.reg + static_cast<int64_t>(blockIdx.x) * a.n + static_cast<int64_t>(sub) * reg_cap;
+    auto gsync = [&]() {
+      if (nsub == 1) __syncthreads();
+      else asm volatile("bar.sync %0, %1;" ::"r"(1 + sub), "r"(G) : "memory");
+    };
     if (gridmode) {
       for (int32_t j = static_cast<int32_t>(gtid); j < nc; j += static_cast<int32_t>(gthreads)) {
         const int32_t c = __ldcg(&a.cand[j]);
@@ -387,70 +406,122 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
         if ((__ldcg(&a.vm[static_cast<int64_t>(__ldcg(&a.cand[j])) * kMaskWords + (i >> 5)]) >> (i & 31)) & 1u)
           atomicOr(&a.inm[i * kMaskWords + (j >> 5)], 1u << (j & 31));
       }
-    } else if (static_cast<int32_t>(blockIdx.x) < nc) {
-      const int32_t c = __ldcg(&a.cand[blockIdx.x]);
-      int32_t* sf0 = reinterpret_cast<int32_t*>(bsm);
-      int32_t* sf1 = sf0 + kFront;
-      if (threadIdx.x == 0) {
+    } else if (wk < nc) {
+      // worker group `sub` of this CTA (G threads) grows the region of candidate wk
+      const int32_t c = __ldcg(&a.cand[wk]);
+      const int32_t fcap = kFront / nsub;
+      int32_t* sf0 = reinterpret_cast<int32_t*>(bsm) + 2 * fcap * sub;
+      int32_t* sf1 = sf0 + fcap;
+      int32_t* cnt3 = s_wcnt[sub];
+      int32_t* lstart = s_wlstart[sub];
+      if (gt == 0) {
         atomicOr(&a.vm[static_cast<int64_t>(c) * kMaskWords + my_word], my_bit);
         my_reg[0] = c;
-        s_lstart[0] = 0;
+        lstart[0] = 0;
         sf0[0] = c;
-        s_cnt[0] = 1, s_cnt[1] = 0, s_cnt[2] = 0;
-        s_n = 1;  // region size
+        cnt3[0] = 1, cnt3[1] = 0, cnt3[2] = 0;
+        s_wn[sub] = 1;  // region size
       }
-      __syncthreads();
+      gsync();
       uint64_t mk = vkey(0, c);
       for (int32_t d = 0;; ++d) {
-        const int32_t nf = s_cnt[d % 3];
+        const int32_t nf = cnt3[d % 3];
         if (nf == 0) {
-          if (threadIdx.x == 0) s_nlev = d;
+          if (gt == 0) s_wnlev[sub] = d;
           break;
         }
-        if (threadIdx.x == 0) s_cnt[(d + 2) % 3] = 0;
+        if (gt == 0) cnt3[(d + 2) % 3] = 0;
         const int32_t* fin = (d & 1) ? sf1 : sf0;
         int32_t* fout = (d & 1) ? sf0 : sf1;
-        const int32_t rbase = s_n - nf;  // this level's vertices end the region list
-        const int32_t rtop = s_n;
-        if (threadIdx.x == 0) s_lstart[d + 1] = rtop;  // depth d+1 entries start here
-        int32_t* cout = &s_cnt[(d + 1) % 3];
+        const int32_t rbase = s_wn[sub] - nf;  // this level's vertices end the region list
+        const int32_t rtop = s_wn[sub];
+        if (gt == 0) lstart[d + 1] = rtop;  // depth d+1 entries start here
+        int32_t* cout = &cnt3[(d + 1) % 3];
         const int32_t items = nf * 8;
-        for (int32_t it = threadIdx.x; it < items; it += blockDim.x) {
-          const int32_t i = it >> 3;
-          const int32_t u = i < kFront ? fin[i] : __ldcg(&my_reg[rbase + i]);
-          const int32_t x = a.ell[static_cast<int64_t>(u) * 8 + (it & 7)];
-          auto relax = [&](int32_t w) {
-            if (d + 1 < __ldcg(&a.dist[w]) &&
-                !(atomicOr(&a.vm[static_cast<int64_t>(w) * kMaskWords + my_word], my_bit) & my_bit)) {
+        auto relax = [&](int32_t w) {
+          if (d + 1 < __ldcg(&a.dist[w]) &&
+              !(atomicOr(&a.vm[static_cast<int64_t>(w) * kMaskWords + my_word], my_bit) & my_bit)) {
+            const int32_t slot = atomicAdd(cout, 1);
+            if (slot < fcap) fout[slot] = w;
+            if (rtop + slot < reg_cap) my_reg[rtop + slot] = w;
+            mk = max(mk, vkey(d + 1, w));
+          }
+        };
+        // kUnroll items per thread with their loads and claims in flight together
+        constexpr int kUnroll = 4;
+        for (int32_t it0 = 0; it0 < items; it0 += kUnroll * G) {
+          int32_t us[kUnroll], xs[kUnroll], ds[kUnroll];
+#pragma unroll
+          for (int q = 0; q < kUnroll; ++q) {
+            const int32_t it = it0 + q * G + gt;
+            us[q] = -1, xs[q] = -1;
+            if (it < items) {
+              const int32_t i = it >> 3;
+              us[q] = i < fcap ? fin[i] : __ldcg(&my_reg[rbase + i]);
+              xs[q] = a.ell[static_cast<int64_t>(us[q]) * 8 + (it & 7)];
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < kUnroll; ++q) ds[q] = xs[q] >= 0 ? __ldcg(&a.dist[xs[q]]) : 0;
+          uint32_t old[kUnroll];
+#pragma unroll
+          for (int q = 0; q < kUnroll; ++q)
+            old[q] = (xs[q] >= 0 && d + 1 < ds[q])
+                         ? atomicOr(&a.vm[static_cast<int64_t>(xs[q]) * kMaskWords + my_word], my_bit)
+                         : my_bit;
+#pragma unroll
+          for (int q = 0; q < kUnroll; ++q) {
+            if (!(old[q] & my_bit)) {
+              const int32_t w = xs[q];
               const int32_t slot = atomicAdd(cout, 1);
-              if (slot < kFront) fout[slot] = w;
-              my_reg[rtop + slot] = w;
+              if (slot < fcap) fout[slot] = w;
+              if (rtop + slot < reg_cap) my_reg[rtop + slot] = w;
               mk = max(mk, vkey(d + 1, w));
             }
-          };
-          if (x >= 0) relax(x);
-          else if (x < -1)
-            for (int32_t j = -x - 2; j < a.g.off[u + 1]; ++j) relax(a.g.nbr[j]);
+            if (xs[q] < -1)  // CSR tail of a vertex with more than 8 neighbours
+              for (int32_t j = -xs[q] - 2; j < a.g.off[us[q] + 1]; ++j) relax(a.g.nbr[j]);
+          }
         }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          s_n += *cout;
-          if (a.work && blockIdx.x == 0) atomicAdd(&a.work[7], 1ull);
+        gsync();
+        if (s_wn[sub] + *cout > reg_cap) {  // the region outgrew this group's list share
+          if (gt == 0) s_wnlev[sub] = 0, atomicExch(&a.ctl[10], 1);
+          break;
         }
-        __syncthreads();
+        gsync();
+        if (gt == 0) {
+          s_wn[sub] += *cout;
+          if (a.work && wk == 0) atomicAdd(&a.work[7], 1ull);
+        }
+        gsync();
       }
-      mk = block_max_u64(mk, s_red);
-      for (int32_t j = threadIdx.x; j < kMaxWorkers; j += blockDim.x) {
+      // group max of mk
+      mk = warp_max_u64(mk);
+      if (lane == 0) s_red[wid] = mk;
+      gsync();
+      if (gt < 32) {
+        const int32_t w0 = sub * (G >> 5);
+        uint64_t r = gt < (G >> 5) ? s_red[w0 + gt] : 0;
+        r = warp_max_u64(r);
+        if (gt == 0) {
+          a.mkey[wk] = r;
+          a.regn[wk] = s_wn[sub];
+          atomicMax(&a.ctl[11], s_wn[sub]);
+        }
+      }
+      for (int32_t j0 = 0; j0 < nc; j0 += G) {  // which candidates lie in this region
+        const int32_t j = j0 + gt;
         const bool in = j < nc && (__ldcg(&a.vm[static_cast<int64_t>(__ldcg(&a.cand[j])) * kMaskWords + my_word]) & my_bit);
         const uint32_t bits = __ballot_sync(0xffffffffu, in);
-        if (lane == 0) a.inm[blockIdx.x * kMaskWords + (j >> 5)] = bits;
-      }
-      if (threadIdx.x == 0) {
-        a.mkey[blockIdx.x] = mk;
-        a.regn[blockIdx.x] = s_n;
+        if (lane == 0 && j < kMaxWorkers) a.inm[wk * kMaskWords + (j >> 5)] = bits;
       }
     }
     grid.sync();
+    if (__ldcg(&a.ctl[10]) == 0) break;
+    for (int64_t q = gtid; q < static_cast<int64_t>(a.n) * kMaskWords; q += gthreads) a.vm[q] = 0;
+    grid.sync();
+    if (gtid == 0) a.ctl[10] = 0, a.ctl[9] = 1, a.ctl[1] = min(nc, static_cast<int32_t>(gridDim.x));
+    grid.sync();
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0 && a.work) atomicAdd(&a.work[9], static_cast<unsigned long long>(clock64() - t_reg0));
     // ---- 3. the walk, every CTA redundantly (exact sequential argmax semantics)
     if (wid == 0) {
@@ -487,18 +558,19 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
         if (!(atomicOr(&a.tbits[t >> 5], bit) & bit)) a.tlist[atomicAdd(&a.ctl[2], 1)] = t;
         scans += a.g.off[w + 1] - a.g.off[w];
       }
-    } else if (static_cast<int32_t>(blockIdx.x) < nc) {
-      const int32_t rn = __ldcg(&a.regn[blockIdx.x]);
-      const bool acc = s_acc[blockIdx.x] != 0;
-      const int32_t nlev = s_nlev;
-      for (int32_t i = threadIdx.x; i < rn; i += blockDim.x) {
+    } else if (wk < nc) {
+      const int32_t rn = __ldcg(&a.regn[wk]);
+      const bool acc = s_acc[wk] != 0;
+      const int32_t nlev = s_wnlev[sub];
+      const int32_t* lstart = s_wlstart[sub];
+      for (int32_t i = gt; i < rn; i += G) {
         const int32_t w = __ldcg(&my_reg[i]);
         a.vm[static_cast<int64_t>(w) * kMaskWords + my_word] = 0;  // clear (every worker's region is finished)
         if (!acc) continue;
         int32_t lo = 0, hi = nlev - 1;  // depth of entry i: last level starting at or before i
         while (lo < hi) {
           const int32_t mid = (lo + hi + 1) >> 1;
-          if (s_lstart[mid] <= i) lo = mid;
+          if (lstart[mid] <= i) lo = mid;
           else hi = mid - 1;
         }
         atomicMin(&a.dist[w], lo);
@@ -542,7 +614,11 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
     // ---- 1. next candidates (leader); grid mode while the radius is large
     if (blockIdx.x == 0) {
       long long t_s0 = clock64();
-      if (threadIdx.x == 0) a.ctl[0] = s_done, a.ctl[2] = 0;
+      // small regions last batch: kMaxSub worker groups per CTA (more candidates)
+      const int32_t nsub_next = (!gridmode && __ldcg(&a.ctl[11]) < kSubRegion) ? kMaxSub : 1;
+      const int32_t W = min(static_cast<int32_t>(gridDim.x) * nsub_next, kMaxWorkers);
+      __syncthreads();
+      if (threadIdx.x == 0) a.ctl[0] = s_done, a.ctl[2] = 0, a.ctl[9] = nsub_next, a.ctl[11] = 0;
       select_candidates(a, W, bsm, reinterpret_cast<int32_t*>(bsm + kSCap), shi);
       if (threadIdx.x == 0) {
         const int32_t top = static_cast<int32_t>(__ldcg(&a.ckey[0]) >> 32);
