@@ -74,6 +74,7 @@ struct BatchArgs {
   unsigned int* bar;       // grid barrier counter (zeroed before the launch)
   int32_t grid_radius;     // candidates farther than this use the grid-mode regions
   int32_t grid_cands;      // candidates per grid-mode batch
+  int32_t sub_region;      // largest region (last batch) that still runs kMaxSub groups per CTA
   int32_t* seeds;          // output, k
   unsigned long long* work;
 };
@@ -615,7 +616,7 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
     if (blockIdx.x == 0) {
       long long t_s0 = clock64();
       // small regions last batch: kMaxSub worker groups per CTA (more candidates)
-      const int32_t nsub_next = (!gridmode && __ldcg(&a.ctl[11]) < kSubRegion) ? kMaxSub : 1;
+      const int32_t nsub_next = (!gridmode && __ldcg(&a.ctl[11]) < a.sub_region) ? kMaxSub : 1;
       const int32_t W = min(static_cast<int32_t>(gridDim.x) * nsub_next, kMaxWorkers);
       __syncthreads();
       if (threadIdx.x == 0) a.ctl[0] = s_done, a.ctl[2] = 0, a.ctl[9] = nsub_next, a.ctl[11] = 0;
@@ -692,6 +693,8 @@ void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32
   a.bar = reinterpret_cast<unsigned int*>(bar.get());
   a.grid_radius = grid_radius;
   a.grid_cands = grid_cands;
+  const char* sr = getenv("MP_FPS_SUB_REGION");
+  a.sub_region = sr ? atoi(sr) : kSubRegion;
   void* args[] = {&a};
   const int kt = ctx.ktime_begin(kKFps);
   MP_KERNEL(ctx, MP_CUDA(cudaLaunchCooperativeKernel((void*)fps_batched_kernel, W, kThreads, args, smem, s)));
