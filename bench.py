@@ -49,14 +49,17 @@ WORKLOADS = {
 C4_FRAMES = 64  # BASELINE configs[3]: 64 frames, random_mesh(500, 500, seed=frame) (250,000 vertices each)
 
 
-def load_graph(name):
+def load_mesh(name):
     import paper_2602_00898_b200 as mp
     kind, arg, _ = WORKLOADS[name]
     if kind == "torus":
-        mesh = mp.make_torus_mesh(*arg)
-    else:
-        mesh = mp.make_icosphere_mesh(arg) if kind == "icosphere" else mp.make_grid_mesh(arg, arg)
-    return mp.mesh_to_graph(mesh)
+        return mp.make_torus_mesh(*arg)
+    return mp.make_icosphere_mesh(arg) if kind == "icosphere" else mp.make_grid_mesh(arg, arg)
+
+
+def load_graph(name):
+    import paper_2602_00898_b200 as mp
+    return mp.mesh_to_graph(load_mesh(name))
 
 
 def golden(name):
@@ -305,6 +308,32 @@ def run_ours(args):
     h2d = 4 * (n + 1) + 4 * m2
     d2h = sum(v.numel() * v.element_size() for v in h_outs.values())
 
+    # the CSR build from device-resident triangles (mesh_to_graph
+    # on the GPU), timed separately; HBM-bound, so its roofline is meaningful
+    csr_build = None
+    if args.workload in ("c2", "c1", "ico158", "grid1000", "c5"):
+        mesh = load_mesh(args.workload)
+        tri_d = torch.from_numpy(np.ascontiguousarray(mesh.triangles, np.int32).reshape(-1)).to(dev)
+        ntri = tri_d.numel() // 3
+        off_d = torch.empty(n + 1, dtype=torch.int32, device=dev)
+        nbr_d = torch.empty(max(6 * ntri, 1), dtype=torch.int32, device=dev)
+        nnz = api.mesh_to_graph_device_ptr(ctx, n, ntri, tri_d.data_ptr(), off_d.data_ptr(), nbr_d.data_ptr())
+        ok = (nnz == m2 and torch.equal(off_d.cpu(), torch.from_numpy(g.offsets))
+              and torch.equal(nbr_d[:nnz].cpu(), torch.from_numpy(g.neighbors)))
+        cms = []
+        for _ in range(5):
+            with torch.cuda.stream(stream):
+                flush.fill_(1)
+            ev0.record(stream)
+            api.mesh_to_graph_device_ptr(ctx, n, ntri, tri_d.data_ptr(), off_d.data_ptr(), nbr_d.data_ptr())
+            ev1.record(stream)
+            ev1.synchronize()
+            cms.append(ev0.elapsed_time(ev1))
+        cms_v = float(np.median(cms))
+        cab = 12 * ntri + 4 * (n + 1) + 4 * nnz
+        csr_build = {"ms": round(cms_v, 4), "triangles": ntri, "nnz": nnz, "matches_host_csr": bool(ok),
+                     "alg_bytes": int(cab), "gbs": round(cab / (cms_v * 1e-3) / 1e9, 1)}
+
     line = None
     if rank == 0:
         names = ["fps", "lloyd", "fm", "refine", "md", "symbolic"]
@@ -375,6 +404,10 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
         }
+        if csr_build:
+            csr_build["peak_gbs"] = peak
+            csr_build["frac"] = round(csr_build["gbs"] / peak, 4)
+            line["csr_build"] = csr_build
         print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist

@@ -173,7 +173,15 @@ int mp_make_torus_mesh(int32_t rows, int32_t cols, int32_t* tris);
 int64_t mp_icosphere_vertices(int32_t f);
 int64_t mp_icosphere_triangles(int32_t f);
 int mp_make_icosphere_mesh(int32_t f, int32_t* tris);
-/* graph.hpp:56 mesh_to_graph; nbr NULL = count only */
+/* graph.hpp:51 mesh_to_graph on the device (graph.cpp:14-75,
+ * validate_mesh types.cpp:20-33).  tris (3 * ntri corners) in host or device
+ * memory per tris_on_device; off (nv + 1) and nbr (capacity >= nnz = 2|E|;
+ * NULL = offsets and *nnz only) in host or device memory per out_on_device.
+ * MP_EINVAL with the reference's message for a bad triangle. */
+int mp_mesh_to_graph_device(mp_context* ctx, int32_t nv, int64_t ntri, const int32_t* tris,
+                            int32_t tris_on_device, int32_t* off, int32_t* nbr, int32_t out_on_device,
+                            int64_t* nnz);
+/* graph.hpp:56 mesh_to_graph on the host (input generation); nbr NULL = count only */
 int mp_mesh_to_graph(int32_t nv, int64_t ntri, const int32_t* tris, int32_t* off, int32_t* nbr,
                      int64_t* nnz);
 

@@ -185,6 +185,31 @@ def mesh_to_graph(mesh: TriangleMesh) -> AdjacencyGraph:  # graph.hpp:56
     return AdjacencyGraph(n, off, nbr)
 
 
+def mesh_to_graph_device(mesh: TriangleMesh, ctx: Context | None = None) -> AdjacencyGraph:
+    """graph.hpp:51 mesh_to_graph computed on the GPU; same
+    AdjacencyGraph as the reference (sorted, deduplicated, symmetric lists)."""
+    ctx = ctx or default_context()
+    tris = _i32(mesh.triangles).reshape(-1, 3)
+    n = int(mesh.vertex_count)
+    off = np.zeros(n + 1, np.int32)
+    nnz = C.c_int64()
+    check(lib().mp_mesh_to_graph_device(ctx.handle, n, len(tris), _ptr(tris), 0, _ptr(off), C.c_void_p(0), 0,
+                                        C.byref(nnz)))
+    nbr = np.zeros(nnz.value, np.int32)
+    check(lib().mp_mesh_to_graph_device(ctx.handle, n, len(tris), _ptr(tris), 0, _ptr(off), _ptr(nbr), 0,
+                                        C.byref(nnz)))
+    return AdjacencyGraph(n, off, nbr)
+
+
+def mesh_to_graph_device_ptr(ctx: Context, nv: int, ntri: int, tris_ptr: int, off_ptr: int, nbr_ptr: int) -> int:
+    """Device-pointer form (tris, off, nbr all device memory; nbr capacity
+    >= 6 * ntri or the nnz of an earlier call).  Returns nnz."""
+    nnz = C.c_int64()
+    check(lib().mp_mesh_to_graph_device(ctx.handle, nv, ntri, C.c_void_p(tris_ptr), 1, C.c_void_p(off_ptr),
+                                        C.c_void_p(nbr_ptr), 1, C.byref(nnz)))
+    return int(nnz.value)
+
+
 def default_nd_level(n: int) -> int:  # etree.hpp:35-36
     return int(lib().mp_default_nd_level(n))
 

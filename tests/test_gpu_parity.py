@@ -317,3 +317,56 @@ def test_order_subtrees_shards_merge_to_full_order(world):
             merged[s:s + n] = pm[s:s + n]
         assert np.all(pm[~inside] == -7)
     assert np.array_equal(merged, full.perm.perm)
+
+
+# ---------------------------------------------------------------- §8 f1: device CSR build
+def _same_graph(a, b):
+    return a.n == b.n and np.array_equal(a.offsets, b.offsets) and np.array_equal(a.neighbors, b.neighbors)
+
+
+def test_mesh_to_graph_device_known_answer():
+    """tests/graph_test.cpp:44-51: a shared edge is counted once."""
+    g = mp.mesh_to_graph_device(mp.TriangleMesh(4, np.array([[0, 1, 2], [1, 2, 3]], np.int32)))
+    assert g.edge_count() == 5
+    assert 2 in g.neighbors_of(1).tolist() and 3 not in g.neighbors_of(0).tolist()
+    # an isolated vertex keeps an empty list; an empty mesh is all isolated
+    g = mp.mesh_to_graph_device(mp.TriangleMesh(5, np.array([[0, 1, 2]], np.int32)))
+    assert g.offsets.tolist() == [0, 2, 4, 6, 6, 6]
+    g = mp.mesh_to_graph_device(mp.TriangleMesh(3, np.zeros((0, 3), np.int32)))
+    assert g.offsets.tolist() == [0, 0, 0, 0] and g.neighbors.size == 0
+
+
+@pytest.mark.parametrize("mesh", ["random", "grid", "torus", "icosphere", "fan"])
+def test_mesh_to_graph_device_matches_reference(mesh):
+    from oracle.oracle import Reference
+    if mesh == "random":
+        m = mp.make_random_mesh(37, 53, 9)
+    elif mesh == "grid":
+        m = mp.make_grid_mesh(64, 64)
+    elif mesh == "torus":
+        m = mp.make_torus_mesh(40, 70)
+    elif mesh == "icosphere":
+        m = mp.make_icosphere_mesh(25)
+    else:  # a hub in 200 triangles: the long-list (warp) sort path
+        k = 200
+        tris = np.array([[0, 1 + i, 1 + (i + 1) % k] for i in range(k)], np.int32)
+        m = mp.TriangleMesh(k + 1, tris)
+    off, nbr = Reference().mesh_to_graph(m.vertex_count, np.asarray(m.triangles, np.int32).reshape(-1, 3))
+    g = mp.mesh_to_graph_device(m)
+    assert np.array_equal(g.offsets, off) and np.array_equal(g.neighbors, nbr)
+
+
+def test_mesh_to_graph_device_errors_match_reference():
+    with pytest.raises(ValueError, match=r"triangle 1 references vertex 3 outside \[0, 3\)"):
+        mp.mesh_to_graph_device(mp.TriangleMesh(3, np.array([[0, 1, 2], [0, 1, 3]], np.int32)))
+    with pytest.raises(ValueError, match="triangle 0 has repeated corners"):
+        mp.mesh_to_graph_device(mp.TriangleMesh(3, np.array([[0, 1, 1], [0, 1, 3]], np.int32)))
+
+
+def test_mesh_to_graph_device_c2():
+    """BASELINE configs[1] (1M icosphere): device CSR == host restatement
+    (itself pinned to the reference on the small cases above)."""
+    m = mp.make_icosphere_mesh(316)
+    g = mp.mesh_to_graph_device(m)
+    h = mp.mesh_to_graph(m)
+    assert _same_graph(g, h) and g.edge_count() == 2995680
