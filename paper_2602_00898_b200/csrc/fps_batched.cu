@@ -75,6 +75,7 @@ struct BatchArgs {
   int32_t grid_radius;     // candidates farther than this use the grid-mode regions
   int32_t grid_cands;      // candidates per grid-mode batch
   int32_t sub_region;      // largest region (last batch) that still runs kMaxSub groups per CTA
+  int32_t resume;          // 1: fps_cluster_phase ran the large-radius seeds; continue from its state
   int32_t* seeds;          // output, k
   unsigned long long* work;
 };
@@ -308,14 +309,18 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
   __shared__ int32_t s_wcnt[kMaxSub][3], s_wn[kMaxSub], s_wnlev[kMaxSub];
   __shared__ int32_t s_wlstart[kMaxSub][kMaxDepth + 2];  // region-list offset of each BFS level
 
-  for (int64_t v = gtid; v < a.n; v += gthreads) a.dist[v] = kUnreached;
-  if (gtid == 0) {
-    a.ctl[0] = 0, a.ctl[2] = 0, a.ctl[1] = 1, a.ctl[3] = 1;  // batch 0: the start vertex, grid mode
-    a.ctl[9] = 1, a.ctl[10] = 0, a.ctl[11] = 0;
-    a.cand[0] = static_cast<int32_t>(splitmix64(a.seed) % static_cast<uint64_t>(a.n));  // patching.cpp:32
-    a.ckey[0] = ~0ull;
+  if (a.resume) {  // seeds so far, dist, tiles and the next candidates come from fps_cluster_phase
+    if (__ldcg(&a.ctl[0]) >= a.k) return;
+  } else {
+    for (int64_t v = gtid; v < a.n; v += gthreads) a.dist[v] = kUnreached;
+    if (gtid == 0) {
+      a.ctl[0] = 0, a.ctl[2] = 0, a.ctl[1] = 1, a.ctl[3] = 1;  // batch 0: the start vertex, grid mode
+      a.ctl[9] = 1, a.ctl[10] = 0, a.ctl[11] = 0;
+      a.cand[0] = static_cast<int32_t>(splitmix64(a.seed) % static_cast<uint64_t>(a.n));  // patching.cpp:32
+      a.ckey[0] = ~0ull;
+    }
+    grid.sync();
   }
-  grid.sync();
   for (int32_t batch = 0;; ++batch) {
     // ---- 2. regions.  Large radii: all candidates advance together over the
     // whole grid (one grid barrier per level, entries (cand, vertex) appended
@@ -637,6 +642,178 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
   }
 }
 
+// Large-radius seeds, one at a time, on one thread-block cluster.  While the
+// farthest vertex is farther than grid_radius the candidate list is the single
+// argmax (a batch of one is always accepted), so its BFS writes dist directly:
+// a claim is atomicMin(dist[w], d + 1) returning a larger value (the region
+// R(c) = {v : d(c, v) < dist(v)}, patching.cpp:35-49).  Levels are separated by
+// the hardware cluster barrier instead of a grid-wide one.  At the end the
+// cluster's CTA 0 selects the first candidate batch for fps_batched_kernel.
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) fps_cluster_phase(BatchArgs a, int32_t w_main) {
+  extern __shared__ uint64_t bsm[];
+  __shared__ int32_t shi[32];
+  __shared__ uint64_t s_red[32];
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int64_t ctid = static_cast<int64_t>(rank) * blockDim.x + threadIdx.x;
+  const int64_t cthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;  // the grid is one cluster
+  // Each CTA keeps the frontier vertices it claims in its shared memory
+  // (double-buffered by level parity; the other CTAs read them through
+  // distributed shared memory) and appends every claimed vertex to its region
+  // list, a row of the a.reg slab (overflowing frontier entries are read from
+  // there).  After the cluster barrier every CTA reads the 16 level counts.
+  constexpr int32_t kCF = 4096;
+  __shared__ int32_t s_front[2][kCF], s_fcnt[2], s_fbeg[2];
+  __shared__ int32_t s_len, s_pre[33], s_rbeg[32];
+  cg::cluster_group cl = cg::this_cluster();
+  int32_t* const myl = a.reg + static_cast<int64_t>(rank) * a.n;
+  unsigned long long scans = 0, levels = 0;
+  const int32_t tsize = 1 << a.tile_shift;
+  const int32_t ncta = static_cast<int32_t>(gridDim.x);
+
+  for (int64_t v = ctid; v < a.n; v += cthreads) a.dist[v] = kUnreached;
+  if (ctid == 0) a.ctl[2] = 0;  // touched tiles
+  cluster_barrier();
+  int32_t c = static_cast<int32_t>(splitmix64(a.seed) % static_cast<uint64_t>(a.n));  // patching.cpp:32
+  int32_t done = 0;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      s_fcnt[0] = 0, s_fbeg[0] = 0, s_len = 0;
+      if (rank == 0) {
+        a.seeds[done] = c;
+        a.dist[c] = 0;
+        myl[0] = c;
+        s_front[0][0] = c;
+        s_fcnt[0] = 1, s_len = 1;
+      }
+    }
+    ++done;
+    __syncthreads();
+    for (int32_t d = 0;; ++d) {  // level-synchronous BFS of the new seed's region
+      const int p = d & 1, q = p ^ 1;
+      cluster_barrier();  // every CTA's level-d frontier is complete
+      if (threadIdx.x < 32) {  // prefix of the CTAs' level counts (DSMEM reads)
+        const int32_t r = threadIdx.x;
+        const int32_t cnt = r < ncta ? *cl.map_shared_rank(&s_fcnt[p], r) : 0;
+        int32_t inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+          if (r >= o) inc += y;
+        }
+        s_pre[r + 1] = inc;
+        if (r == 0) s_pre[0] = 0, s_fcnt[q] = 0;
+        s_rbeg[r] = r < ncta ? *cl.map_shared_rank(&s_fbeg[p], r) : 0;
+      }
+      __syncthreads();
+      const int32_t nf = s_pre[ncta];
+      if (nf == 0) break;
+      const int32_t len0 = s_len;  // this level's claims go to myl[len0 ...]
+      const int64_t items = static_cast<int64_t>(nf) * 8;
+      for (int64_t base = ctid - lane; base < items; base += cthreads) {
+        const int64_t it = base + lane;
+        int32_t x = -1, u = 0;
+        if (it < items) {
+          const int32_t i = static_cast<int32_t>(it >> 3);
+          int32_t r = 0;
+#pragma unroll
+          for (int k = 16; k > 0; k >>= 1)
+            if (r + k < ncta && s_pre[r + k] <= i) r += k;
+          const int32_t j = i - s_pre[r];
+          u = j < kCF ? *cl.map_shared_rank(&s_front[p][j], r)
+                      : __ldcg(&a.reg[static_cast<int64_t>(r) * a.n + s_rbeg[r] + j]);
+          x = a.ell[static_cast<int64_t>(u) * 8 + (it & 7)];
+        }
+        const bool push = x >= 0 && atomicMin(&a.dist[x], d + 1) > d + 1;
+        const int32_t slot = warp_append(&s_fcnt[q], push);
+        if (push) {
+          if (slot < kCF) s_front[q][slot] = x;
+          myl[len0 + slot] = x;
+        }
+        if (x < -1)  // CSR tail of a vertex with more than 8 neighbours
+          for (int32_t k = -x - 2; k < a.g.off[u + 1]; ++k) {
+            const int32_t w = a.g.nbr[k];
+            if (atomicMin(&a.dist[w], d + 1) > d + 1) {
+              const int32_t sl = atomicAdd(&s_fcnt[q], 1);
+              if (sl < kCF) s_front[q][sl] = w;
+              myl[len0 + sl] = w;
+            }
+          }
+      }
+      ++levels;
+      __syncthreads();
+      if (threadIdx.x == 0) s_fbeg[q] = len0, s_len = len0 + s_fcnt[q];
+      __syncthreads();
+    }
+    // mark the tiles of this CTA's region vertices
+    for (int32_t i = threadIdx.x; i < s_len; i += blockDim.x) {
+      const int32_t w = myl[i];
+      const int32_t t = w >> a.tile_shift;
+      const uint32_t bit = 1u << (t & 31);
+      if (!(atomicOr(&a.tbits[t >> 5], bit) & bit)) a.tlist[atomicAdd(&a.ctl[2], 1)] = t;
+      scans += a.g.off[w + 1] - a.g.off[w];
+    }
+    cluster_barrier();
+    // refresh the touched tile and subtile maxima
+    {
+      const int64_t gw = ctid >> 5, nwarps = cthreads >> 5;
+      const int32_t nt = __ldcg(&a.ctl[2]);
+      for (int64_t i = gw; i < nt; i += nwarps) {
+        const int32_t t = __ldcg(&a.tlist[i]);
+        uint64_t best = 0;
+        const int32_t lo = t * tsize, hi = min(a.n, lo + tsize);
+        for (int32_t v0 = lo; v0 < hi; v0 += 32) {
+          const int32_t v = v0 + lane;
+          const int32_t dv = v < hi ? __ldcg(&a.dist[v]) : -1;
+          if (v < hi) best = max(best, vkey(dv, v));
+          const int32_t sm = __reduce_max_sync(0xffffffffu, dv);
+          if (lane == 0) a.smax[v0 >> 5] = sm;
+        }
+        best = warp_max_u64(best);
+        if (lane == 0) {
+          a.tkey[t] = best;
+          a.tbits[t >> 5] = 0;
+        }
+      }
+    }
+    cluster_barrier();
+    if (done >= a.k) break;
+    // the next seed: argmax (dist desc, id asc) over the tile maxima (every CTA)
+    uint64_t best = 0;
+    for (int32_t t = threadIdx.x; t < a.ntile; t += blockDim.x) best = max(best, __ldcg(&a.tkey[t]));
+    best = block_max_u64(best, s_red);
+    if (static_cast<int32_t>(best >> 32) <= a.grid_radius) break;
+    c = static_cast<int32_t>(key_max_id(best));
+    if (ctid == 0) a.ctl[2] = 0;  // every CTA has read the touched count (refresh, barrier above)
+    cluster_barrier();
+  }
+  // hand over: seeds done, no touched tiles, the first candidate batch
+  if (rank == 0) {
+    if (threadIdx.x == 0) {
+      a.ctl[0] = done, a.ctl[2] = 0, a.ctl[3] = 0, a.ctl[9] = 1, a.ctl[10] = 0, a.ctl[11] = 0;
+      if (a.work) {
+        atomicAdd(&a.work[4], static_cast<unsigned long long>(done));
+        atomicAdd(&a.work[5], levels);
+      }
+    }
+    __syncthreads();
+    if (done < a.k) select_candidates(a, w_main, bsm, reinterpret_cast<int32_t*>(bsm + kSCap), shi);
+  }
+  if (a.work) {
+    const uint64_t tot = block_sum_i64(static_cast<int64_t>(scans), reinterpret_cast<int64_t*>(s_red));
+    if (threadIdx.x == 0 && tot) atomicAdd(&a.work[0], static_cast<unsigned long long>(tot));
+  }
+}
+
 }  // namespace
 
 // Seeds of one component spanning the whole graph (positions = vertex ids).
@@ -695,8 +872,42 @@ void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32
   a.grid_cands = grid_cands;
   const char* sr = getenv("MP_FPS_SUB_REGION");
   a.sub_region = sr ? atoi(sr) : kSubRegion;
-  void* args[] = {&a};
   const int kt = ctx.ktime_begin(kKFps);
+  // large-radius seeds on one cluster (16 CTAs where the device allows, else 8)
+  a.resume = 0;
+  if (!getenv("MP_FPS_NO_CLUSTER")) {
+    static int cluster_ctas = -1;  // decided once per process
+    if (cluster_ctas < 0) {
+      cluster_ctas = 0;
+      allow_max_smem(fps_cluster_phase, ctx.device);
+      cudaFuncSetAttribute(fps_cluster_phase, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      for (int cs : {16, 8}) {
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cs, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(cs), cfg.blockDim = dim3(kThreads), cfg.dynamicSmemBytes = smem;
+        cfg.attrs = at, cfg.numAttrs = 1;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, fps_cluster_phase, &cfg) == cudaSuccess && ncl > 0) {
+          cluster_ctas = cs;
+          break;
+        }
+        cudaGetLastError();
+      }
+    }
+    if (cluster_ctas > 0) {
+      cudaLaunchConfig_t cfg{};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cluster_ctas, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(cluster_ctas), cfg.blockDim = dim3(kThreads), cfg.dynamicSmemBytes = smem;
+      cfg.stream = s, cfg.attrs = at, cfg.numAttrs = 1;
+      MP_KERNEL(ctx, MP_CUDA(cudaLaunchKernelEx(&cfg, fps_cluster_phase, a, static_cast<int32_t>(W))));
+      a.resume = 1;
+    }
+  }
+  void* args[] = {&a};
   MP_KERNEL(ctx, MP_CUDA(cudaLaunchCooperativeKernel((void*)fps_batched_kernel, W, kThreads, args, smem, s)));
   ctx.ktime_end(kt);
 }
