@@ -9,7 +9,7 @@
 //   2. scan         raw list offsets
 //   3. tri_scatter: each corner appends its two opposite corners
 //   4. list_sort:   one thread per vertex sorts + dedups its raw list in shared
-//                   memory (lists longer than kSortCap: one warp in global)
+//                   memory (lists longer than kSortCap: listed, one warp each)
 //   5. scan         CSR offsets of the deduplicated lengths
 //   6. list_copy:   compact the sorted lists into neighbors[]
 // Algorithmic bytes: 12 per triangle read + 4 (n + 1) + 4 nnz written.
@@ -40,10 +40,11 @@ __global__ void tri_count(int64_t ntri, int32_t nv, const int32_t* __restrict__ 
   }
 }
 
-__global__ void tri_scatter(int64_t ntri, const int32_t* __restrict__ tris, int32_t* cur, int32_t* raw) {
+__global__ void tri_scatter(int64_t ntri, int32_t nv, const int32_t* __restrict__ tris, int32_t* cur, int32_t* raw) {
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < ntri;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int32_t a = __ldg(&tris[3 * t]), b = __ldg(&tris[3 * t + 1]), c = __ldg(&tris[3 * t + 2]);
+    if (a < 0 || a >= nv || b < 0 || b >= nv || c < 0 || c >= nv || a == b || b == c || a == c) continue;
     int32_t p = atomicAdd(&cur[a], 2);
     raw[p] = b, raw[p + 1] = c;
     p = atomicAdd(&cur[b], 2);
@@ -54,14 +55,15 @@ __global__ void tri_scatter(int64_t ntri, const int32_t* __restrict__ tris, int3
 }
 
 // Sort + dedup each raw list in place; deg[v] = unique length.  Long lists are
-// left for list_sort_long (flagged with -1).
-__global__ void __launch_bounds__(kSortThreads) list_sort(int32_t nv, const int32_t* ro, int32_t* raw, int32_t* deg) {
+// left for list_sort_long (appended to `longv`, counted in longv[-1]).
+__global__ void __launch_bounds__(kSortThreads) list_sort(int32_t nv, const int32_t* ro, int32_t* raw, int32_t* deg,
+                                                         int32_t* nlong, int32_t* longv) {
   __shared__ int32_t sm[kSortThreads * kSortCap];
   int32_t* my = sm + threadIdx.x;  // strided: entry k at my[k * kSortThreads] (bank-conflict free)
   for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
     const int32_t b = ro[v], len = ro[v + 1] - b;
     if (len > kSortCap) {
-      deg[v] = -1;
+      longv[atomicAdd(nlong, 1)] = v;
       continue;
     }
     for (int32_t k = 0; k < len; ++k) {  // insertion sort while loading
@@ -84,12 +86,13 @@ __global__ void __launch_bounds__(kSortThreads) list_sort(int32_t nv, const int3
 
 // One warp per long list: odd-even transposition in global memory (rare: a
 // vertex in more than kSortCap / 2 triangles).
-__global__ void list_sort_long(int32_t nv, const int32_t* ro, int32_t* raw, int32_t* deg) {
+__global__ void list_sort_long(const int32_t* nlong, const int32_t* longv, const int32_t* ro, int32_t* raw,
+                               int32_t* deg) {
   const int lane = threadIdx.x & 31;
-  for (int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; w < nv;
+  const int32_t nl = *nlong;
+  for (int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; w < nl;
        w += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
-    const int32_t v = static_cast<int32_t>(w);
-    if (deg[v] != -1) continue;
+    const int32_t v = longv[w];
     const int32_t b = ro[v], len = ro[v + 1] - b;
     for (int32_t r = 0; r < len; ++r) {
       for (int32_t i = 2 * lane + (r & 1); i + 1 < len; i += 64) {
@@ -137,9 +140,8 @@ int64_t mesh_to_graph_dev(mp_context& ctx, int32_t nv, int64_t ntri, const int32
   MP_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nv + 1), s));
   MP_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s));
   if (ntri > 0) MP_KERNEL(ctx, tri_count<<<grid, 256, 0, s>>>(ntri, nv, tris, cnt, bad));
-  unsigned long long hbad = 0;
-  MP_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof hbad, cudaMemcpyDeviceToHost, s));
-  MP_CUDA(cudaStreamSynchronize(s));
+  // (bad triangles are skipped by the scatter; the verdict is read with nnz)
+  auto check_bad = [&](unsigned long long hbad) {
   if (hbad != ~0ull) {  // validate_mesh's message for the first bad triangle (types.cpp:20-33)
     const int64_t t = static_cast<int64_t>(hbad >> 1);
     int32_t c[3];
@@ -152,26 +154,31 @@ int64_t mesh_to_graph_dev(mp_context& ctx, int32_t nv, int64_t ntri, const int32
     }
     throw Error(MP_EINVAL, "triangle " + std::to_string(t) + " has repeated corners");
   }
+  };
   size_t tmp = 0;
   MP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.get(), ro.get(), nv + 1, s));
   DevBuf<char> t1(tmp, s);
   MP_CUDA(cub::DeviceScan::ExclusiveSum(t1.get(), tmp, cnt.get(), ro.get(), nv + 1, s));
   MP_CUDA(cudaMemcpyAsync(cnt.get(), ro.get(), sizeof(int32_t) * nv, cudaMemcpyDeviceToDevice, s));  // cursors
-  if (ntri > 0) MP_KERNEL(ctx, tri_scatter<<<grid, 256, 0, s>>>(ntri, tris, cnt, raw));
-  DevBuf<int32_t> deg(static_cast<size_t>(nv) + 1, s);
+  if (ntri > 0) MP_KERNEL(ctx, tri_scatter<<<grid, 256, 0, s>>>(ntri, nv, tris, cnt, raw));
+  DevBuf<int32_t> deg(static_cast<size_t>(nv) + 1, s), longv(static_cast<size_t>(nv) + 1, s);
   MP_CUDA(cudaMemsetAsync(deg.get() + nv, 0, sizeof(int32_t), s));
+  MP_CUDA(cudaMemsetAsync(longv.get() + nv, 0, sizeof(int32_t), s));  // long-list count
   if (nv > 0) {
     const int sg = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nv, kSortThreads), ctx.num_sms * 8LL)));
-    MP_KERNEL(ctx, list_sort<<<sg, kSortThreads, 0, s>>>(nv, ro, raw, deg));
-    MP_KERNEL(ctx, list_sort_long<<<ctx.num_sms, 256, 0, s>>>(nv, ro, raw, deg));
+    MP_KERNEL(ctx, list_sort<<<sg, kSortThreads, 0, s>>>(nv, ro, raw, deg, longv.get() + nv, longv));
+    MP_KERNEL(ctx, list_sort_long<<<ctx.num_sms, 256, 0, s>>>(longv.get() + nv, longv, ro, raw, deg));
   }
   MP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, deg.get(), off, nv + 1, s));
   DevBuf<char> t2(tmp, s);
   MP_CUDA(cub::DeviceScan::ExclusiveSum(t2.get(), tmp, deg.get(), off, nv + 1, s));
   int32_t nnz = 0;
+  unsigned long long hbad = 0;
   MP_CUDA(cudaMemcpyAsync(&nnz, off + nv, sizeof nnz, cudaMemcpyDeviceToHost, s));
+  MP_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof hbad, cudaMemcpyDeviceToHost, s));
   if (!nbr && alloc) {
     MP_CUDA(cudaStreamSynchronize(s));
+    check_bad(hbad);
     alloc->alloc(std::max(nnz, 1), s);
     nbr = alloc->get();
   }
@@ -181,6 +188,7 @@ int64_t mesh_to_graph_dev(mp_context& ctx, int32_t nv, int64_t ntri, const int32
     MP_KERNEL(ctx, list_copy<<<cg, 256, 0, s>>>(nv, ro, raw, off, nbr));
   }
   MP_CUDA(cudaStreamSynchronize(s));
+  check_bad(hbad);
   return nnz;
 }
 
