@@ -789,7 +789,7 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
   __shared__ RefKey sred[32];
   __shared__ int64_t s_rw[2], s_size;
   __shared__ double s_imb, s_ni[2][kRefTab];
-  __shared__ int32_t s_list, s_mv, s_moves;
+  __shared__ int32_t s_list, s_mv, s_moves, s_pw[32];
   extern __shared__ int32_t ref_sm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int32_t lc = 2 * li, rc = 2 * li + 1;  // children, local to the next level
@@ -902,12 +902,99 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
       const int32_t mv = k.hi == ~0ull ? -1 : static_cast<int32_t>(k.lo & 0xffffffffu);
       if (lane == 0) s_mv = mv;
       if (mv >= 0) {
+        // mv's slot, its ELL row and its degree are independent loads
+        const int32_t e_mv = lane < 8 ? ell[static_cast<int64_t>(mv) * 8 + lane] : -1;
         const int32_t im = a.slot_of[mv];
+        const int32_t e7 = __shfl_sync(0xffffffffu, e_mv, 7);
+        const int32_t dmv = e7 < -1 ? degree(mv) : 0;  // CSR tail: exact degree needed
         const int8_t own = static_cast<int8_t>(lown[im]), opp = 1 - own;
-        // 1. pull mv's opposite-region neighbours into the separator
-        const int32_t dmv = degree(mv);
-        int32_t tail = s_list, np = 0;
+        int32_t np = 0;
         int32_t* pulled = a.ref_pulled + s0;
+        if (e7 >= -1 || dmv <= 32) {
+          // ---- fast path (degree <= 32): one neighbour per lane, three
+          // dependent L2 round trips in all (mv's row; the neighbours' region /
+          // slot / side / rows; the pulled vertices' neighbours' region / slot)
+          int32_t w = -1;
+          if (e7 >= -1) w = lane < 8 ? e_mv : -1;
+          else if (lane < 7) w = e_mv;
+          else {
+            const int32_t j = -e7 - 2 + (lane - 7);
+            w = j < a.g.off[mv + 1] ? a.g.nbr[j] : -1;
+          }
+          int32_t rw = 3, sw = -1;
+          uint8_t vs = 0;
+          int4 r0 = make_int4(-1, -1, -1, -1), r1 = r0;  // w's ELL row (used if w is pulled)
+          if (w >= 0) {
+            rw = region[w], sw = a.slot_of[w], vs = a.vside[w];
+            const int4* row = reinterpret_cast<const int4*>(ell + static_cast<int64_t>(w) * 8);
+            r0 = row[0], r1 = row[1];
+          }
+          const bool pull = rw == opp;
+          const uint32_t m = __ballot_sync(0xffffffffu, pull);
+          const bool fresh = pull && sw < 0;
+          const uint32_t mf = __ballot_sync(0xffffffffu, fresh);
+          np = __popc(m);
+          // mv: 2 -> own raises the pull of separator neighbours whose opposite is own
+          if (rw == 2 && lin[sw] == 1 && lown[sw] == opp) atomicAdd(&lpull[sw], 1);
+          const int32_t tail = s_list;
+          int32_t ws = sw;
+          if (pull) s_pw[__popc(m & ((1u << lane) - 1))] = w;
+          __syncwarp();
+          if (pull) {
+            region[w] = 2;
+            if (fresh) {
+              ws = tail + __popc(mf & ((1u << lane) - 1));
+              lv[ws] = w;
+              lown[ws] = vs;
+              a.slot_of[w] = ws;
+            }
+            lin[ws] = 2;  // 2 = pulled by this move
+          }
+          // pulled w (opp -> 2): its own pull count and the separator neighbours
+          // on side `own` it no longer pulls.  Region values are as after this
+          // move: mv is `own`, every pulled vertex is 2 (corrected in registers).
+          int32_t cntp = 0;
+          if (pull) {
+            const int8_t wopp = static_cast<int8_t>(1 - vs);
+            const int32_t xs[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+            int8_t rx[8];
+            int32_t ix[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int32_t x = xs[k];
+              rx[k] = x >= 0 ? region[x] : int8_t(3);
+              ix[k] = x >= 0 ? a.slot_of[x] : -1;
+            }
+            auto visit = [&](int32_t x, int8_t r, int32_t slot) {
+              if (x == mv) r = own;
+              else if (r == opp)  // was it pulled by this move? (then it is 2 now)
+                for (int32_t t = 0; t < np; ++t)
+                  if (s_pw[t] == x) r = 2, slot = -1;
+              cntp += r == wopp;
+              if (r == 2 && slot >= 0 && lin[slot] == 1 && lown[slot] == own) atomicSub(&lpull[slot], 1);
+            };
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (k < 7 || xs[7] >= -1)
+                if (xs[k] >= 0) visit(xs[k], rx[k], ix[k]);
+            if (xs[7] < -1)  // CSR tail of a pulled vertex with more than 8 neighbours
+              for (int32_t j = -xs[7] - 2; j < a.g.off[w + 1]; ++j) {
+                const int32_t x = a.g.nbr[j];
+                visit(x, region[x], a.slot_of[x]);
+              }
+            lpull[ws] = cntp;
+          }
+          __syncwarp();
+          if (pull) lin[ws] = 1;
+          if (lane == 0) {
+            region[mv] = own;
+            lin[im] = 0;
+            s_list = tail + __popc(mf);
+          }
+        } else {
+        // ---- general path (degree > 32)
+        // 1. pull mv's opposite-region neighbours into the separator
+        int32_t tail = s_list;
         for (int32_t k0 = 0; k0 < dmv; k0 += 32) {
           const int32_t w = k0 + lane < dmv ? nbr_at(mv, k0 + lane) : -1;
           const bool pull = w >= 0 && region[w] == opp;
@@ -968,6 +1055,7 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
         }
         __syncwarp();
         for (int32_t t = lane; t < np; t += 32) lin[a.slot_of[pulled[t]]] = 1;
+        }
         const int64_t nrw0 = s_rw[0] + (own == 0 ? 1 : -np), nrw1 = s_rw[1] + (own == 1 ? 1 : -np);
         // imbalance table of the next move
         {
