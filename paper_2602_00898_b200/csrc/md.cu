@@ -278,7 +278,8 @@ __global__ void __launch_bounds__(kMdThreads) md_fast_kernel(MdArgs a) {
   int32_t* mark = reinterpret_cast<int32_t*>(deg + nv);
   int32_t* bsz = mark + nv;
   int32_t* st = bsz + nv;
-  uint32_t* dirty = reinterpret_cast<uint32_t*>(st + nv);  // nb bits
+  int32_t* loff = st + nv;  // CSR offset of each local vertex (its list slots)
+  uint32_t* dirty = reinterpret_cast<uint32_t*>(loff + nv);  // nb bits
   __shared__ int32_t s_nb, s_cursor, s_half, s_need, s_p, s_dcnt;
   __shared__ int32_t s_dlist[kMdThreads];  // dirty blocks of this pivot (<= reach + 1 distinct)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
@@ -296,6 +297,7 @@ __global__ void __launch_bounds__(kMdThreads) md_fast_kernel(MdArgs a) {
     }
     if (c > 0x7fff) atomicExch(a.overflow, 2);  // packed list lengths: the general kernel redoes it
     st[k] = c;
+    loff[k] = o;
     deg[k] = static_cast<uint32_t>(c);
     mark[k] = 0;
     bsz[k] = 0;
@@ -325,8 +327,7 @@ __global__ void __launch_bounds__(kMdThreads) md_fast_kernel(MdArgs a) {
     __syncthreads();  // B1
     const int32_t p = s_p;
     const int32_t tok = k + 1;
-    const int32_t gp = verts[p];
-    const int32_t po = a.g.off[gp];
+    const int32_t po = loff[p];
     const int32_t pst = st[p];
     const int32_t np_adj = pst & 0xffff, np_el = pst >> 16;
     if (s_need) {  // compact live boundaries into the other half
@@ -391,7 +392,7 @@ __global__ void __launch_bounds__(kMdThreads) md_fast_kernel(MdArgs a) {
     // ---- member updates (elimination.cpp:75-83) and their approx degrees
     for (int32_t i = threadIdx.x; i < nbd; i += blockDim.x) {
       const int32_t w = out[i];
-      const int32_t o = a.g.off[verts[w]];
+      const int32_t o = loff[w];
       const int32_t wst = st[w];
       int32_t* wa = a.adj + o;
       int32_t c = 0;
@@ -511,7 +512,7 @@ void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t L, const int
     for (int32_t i = 0; i < nn; ++i) maxnv = std::max(maxnv, hoff[i + 1] - hoff[i]);
     const int32_t fast_nv = std::min(maxnv, kMdFastCap);
     const int32_t fnb = (fast_nv + 31) / 32;
-    const size_t fsmem = sizeof(uint64_t) * fnb + sizeof(int32_t) * 4 * fast_nv + sizeof(uint32_t) * ((fnb + 31) / 32 + 1);
+    const size_t fsmem = sizeof(uint64_t) * fnb + sizeof(int32_t) * 5 * fast_nv + sizeof(uint32_t) * ((fnb + 31) / 32 + 1);
     allow_max_smem(md_fast_kernel, ctx.device);
     MP_KERNEL(ctx, md_fast_kernel<<<nn, kMdThreads, fsmem, s>>>(a));
     int32_t h_flag = 0;
