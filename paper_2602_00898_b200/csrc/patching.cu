@@ -429,8 +429,38 @@ __device__ __forceinline__ bool lloyd_active(const LloydArgs& a, int32_t v) {
   return a.comp_mode[c] == kModeFps && __ldcg(&a.comp_active[c]) != 0;
 }
 
+// One BFS level over `items` (frontier vertex, ELL slot) pairs in CTA-sized
+// chunks: a chunk's pushes gather in shared memory and reserve their range of
+// the next frontier with ONE global atomic (a per-warp atomic on the shared
+// counter serialises ~15K warps per level at C2).  item(it, push) handles one
+// pair and calls push(w) for every newly reached vertex.
+constexpr int kLvlPer = 4;                 // items per thread per chunk
+constexpr int kLvlBuf = 256 * kLvlPer * 2; // shared push buffer (pairs + CSR tails)
+template <class F>
+__device__ __forceinline__ void chunked_level(int64_t items, int32_t* gcount, int32_t* next, int32_t* sbuf,
+                                              int32_t* sh, F&& item) {
+  const int64_t chunk = static_cast<int64_t>(blockDim.x) * kLvlPer;
+  for (int64_t c0 = static_cast<int64_t>(blockIdx.x) * chunk; c0 < items; c0 += static_cast<int64_t>(gridDim.x) * chunk) {
+    if (threadIdx.x == 0) sh[0] = 0;
+    __syncthreads();
+    auto push = [&](int32_t w) {
+      const int32_t slot = atomicAdd(&sh[0], 1);
+      if (slot < kLvlBuf) sbuf[slot] = w;
+      else next[atomicAdd(gcount, 1)] = w;  // overflow (high-degree tails): direct
+    };
+#pragma unroll
+    for (int q = 0; q < kLvlPer; ++q) item(c0 + q * static_cast<int64_t>(blockDim.x) + threadIdx.x, push);
+    __syncthreads();
+    const int32_t cnt = min(sh[0], kLvlBuf);
+    if (threadIdx.x == 0 && cnt) sh[1] = atomicAdd(gcount, cnt);
+    __syncthreads();
+    for (int32_t i = threadIdx.x; i < cnt; i += blockDim.x) next[sh[1] + i] = sbuf[i];
+  }
+}
+
 __global__ void lloyd_kernel(LloydArgs a) {
   cg::grid_group grid = cg::this_grid();
+  __shared__ int32_t s_lbuf[kLvlBuf], s_lsh[2];
   const int lane = threadIdx.x & 31;
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -459,37 +489,32 @@ __global__ void lloyd_kernel(LloydArgs a) {
         const int32_t nf = __ldcg(&a.counters[cin]);
         if (nf == 0) break;
         if (tid == 0) a.counters[cclr] = 0;
-        // edge parallel over (frontier vertex, ELL slot); warp-aggregated appends
+        // edge parallel over (frontier vertex, ELL slot), CTA-aggregated appends
         const int64_t items = static_cast<int64_t>(nf) * 8;
-        for (int64_t base = tid - lane; base < items; base += nthreads) {
-          const int64_t it = base + lane;
-          int32_t u = -1, x = -1;
-          if (it < items) {
-            u = front[it >> 3];
-            x = a.ell[static_cast<int64_t>(u) * 8 + (it & 7)];
+        auto visit = [&](int32_t w, int32_t lu) -> bool {
+          int32_t dw = __ldcg(&a.dist[w]);
+          bool fresh = false;
+          if (dw == kUnreached) {
+            dw = atomicCAS(&a.dist[w], kUnreached, d + 1);
+            if (dw == kUnreached) fresh = true, dw = d + 1;
           }
-          auto visit = [&](int32_t w, int32_t lu) -> bool {
-            int32_t dw = __ldcg(&a.dist[w]);
-            bool fresh = false;
-            if (dw == kUnreached) {
-              dw = atomicCAS(&a.dist[w], kUnreached, d + 1);
-              if (dw == kUnreached) fresh = true, dw = d + 1;
-            }
-            if (dw == d + 1) atomicMin(&a.label[w], lu);
-            return fresh;
-          };
-          bool push = false;
-          if (x >= 0) push = visit(x, __ldcg(&a.label[u]));
-          const int32_t slot = warp_append(&a.counters[cout], push);
-          if (push) next[slot] = x;
-          if (x < -1) {  // degree > 8: CSR tail
+          if (dw == d + 1) atomicMin(&a.label[w], lu);
+          return fresh;
+        };
+        chunked_level(items, &a.counters[cout], next, s_lbuf, s_lsh, [&](int64_t it, auto&& push) {
+          if (it >= items) return;
+          const int32_t u = front[it >> 3];
+          const int32_t x = a.ell[static_cast<int64_t>(u) * 8 + (it & 7)];
+          if (x >= 0) {
+            if (visit(x, __ldcg(&a.label[u]))) push(x);
+          } else if (x < -1) {  // degree > 8: CSR tail
             const int32_t lu = __ldcg(&a.label[u]);
             for (int32_t j = -x - 2; j < a.g.off[u + 1]; ++j) {
               const int32_t w = a.g.nbr[j];
-              if (visit(w, lu)) next[atomicAdd(&a.counters[cout], 1)] = w;
+              if (visit(w, lu)) push(w);
             }
           }
-        }
+        });
         grid.sync();
         if (tid == 0 && a.work) atomicAdd(&a.work[3], 1ull);
         int32_t* t = front;
@@ -540,29 +565,24 @@ __global__ void lloyd_kernel(LloydArgs a) {
         if (nf == 0) break;
         if (tid == 0) a.counters[cclr] = 0;
         const int64_t items = static_cast<int64_t>(nf) * 8;
-        for (int64_t base = tid - lane; base < items; base += nthreads) {
-          const int64_t it = base + lane;
-          int32_t u = -1, x = -1;
-          if (it < items) {
-            u = front[it >> 3];
-            x = a.ell[static_cast<int64_t>(u) * 8 + (it & 7)];
-          }
-          auto visit = [&](int32_t w, int32_t lu) -> bool {
-            if (__ldcg(&a.label[w]) != lu || __ldcg(&a.dist[w]) != kUnreached) return false;
-            return atomicCAS(&a.dist[w], kUnreached, d + 1) == kUnreached;
-          };
-          bool push = false;
-          if (x >= 0) push = visit(x, __ldcg(&a.label[u]));
-          const int32_t slot = warp_append(&a.counters[cout], push);
-          if (push) next[slot] = x;
-          if (x < -1) {
+        auto visit = [&](int32_t w, int32_t lu) -> bool {
+          if (__ldcg(&a.label[w]) != lu || __ldcg(&a.dist[w]) != kUnreached) return false;
+          return atomicCAS(&a.dist[w], kUnreached, d + 1) == kUnreached;
+        };
+        chunked_level(items, &a.counters[cout], next, s_lbuf, s_lsh, [&](int64_t it, auto&& push) {
+          if (it >= items) return;
+          const int32_t u = front[it >> 3];
+          const int32_t x = a.ell[static_cast<int64_t>(u) * 8 + (it & 7)];
+          if (x >= 0) {
+            if (visit(x, __ldcg(&a.label[u]))) push(x);
+          } else if (x < -1) {
             const int32_t lu = __ldcg(&a.label[u]);
             for (int32_t j = -x - 2; j < a.g.off[u + 1]; ++j) {
               const int32_t w = a.g.nbr[j];
-              if (visit(w, lu)) next[atomicAdd(&a.counters[cout], 1)] = w;
+              if (visit(w, lu)) push(w);
             }
           }
-        }
+        });
         grid.sync();
         int32_t* t = front;
         front = next;
