@@ -173,6 +173,17 @@ int mp_make_torus_mesh(int32_t rows, int32_t cols, int32_t* tris);
 int64_t mp_icosphere_vertices(int32_t f);
 int64_t mp_icosphere_triangles(int32_t f);
 int mp_make_icosphere_mesh(int32_t f, int32_t* tris);
+/* the pipeline's separation self-check (pipeline.cpp:141-142;
+ * cross_block_fill, symbolic.hpp:37) in edge-locality form: *violations =
+ * number of edges whose endpoints lie in tree nodes that are neither equal
+ * nor ancestor-related (tests/etree_test.cpp:171-179).  Zero implies
+ * cross_block_fill == 0 for the postorder and levelorder schedules.  The
+ * tree arrays are host or device memory per on_device; g per g->on_device.
+ * mp_order runs this check after its timed stages and fails with MP_ELOGIC
+ * ("separator failed to disconnect its sides") like run_pipeline. */
+int mp_tree_separation_check(mp_context* ctx, const mp_csr* g, int32_t nd_level,
+                             const int32_t* node_offsets, const int32_t* node_vertices,
+                             int32_t on_device, int64_t* violations);
 /* graph.hpp:51 mesh_to_graph on the device (graph.cpp:14-75,
  * validate_mesh types.cpp:20-33).  tris (3 * ntri corners) in host or device
  * memory per tris_on_device; off (nv + 1) and nbr (capacity >= nnz = 2|E|;

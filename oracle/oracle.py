@@ -190,6 +190,14 @@ class Reference(_Base):
                                              C.byref(nnz)))
         return off, nbr
 
+    def cross_block_fill(self, g, perm, nd_level, node_offsets, node_vertices):
+        """symbolic.cpp:98-119 (the pipeline self-check, pipeline.cpp:141)."""
+        c = C.c_int64()
+        self._check(self._f("cross_block_fill")(C.c_int32(g.n), _p(_i32(g.offsets)), _p(_i32(g.neighbors)),
+                                                _p(_i32(perm)), C.c_int32(nd_level), _p(_i32(node_offsets)),
+                                                _p(_i32(node_vertices)), C.byref(c)))
+        return int(c.value)
+
     def order_timed(self, g, patch_size=256, nd_level=-1, seed=0, mode=0, levelorder=0, threads=1):
         """ref_order: run_pipeline's ordering stages with time_stage timers (ms per stage)."""
         n = g.n

@@ -318,6 +318,17 @@ def compute_perm(tree: EliminationTree, g: AdjacencyGraph, schedule: str = "post
     return Permutation(pm[:g.n], inv[:g.n])
 
 
+def tree_separation_violations(g: AdjacencyGraph, tree: EliminationTree, ctx: Context | None = None) -> int:
+    """edges joining tree nodes that are neither equal nor
+    ancestor-related (tests/etree_test.cpp:171-179).  0 implies the
+    reference's pipeline self-check cross_block_fill == 0 (pipeline.cpp:141)."""
+    ctx = ctx or default_context()
+    v = C.c_int64()
+    check(lib().mp_tree_separation_check(ctx.handle, C.byref(_csr(g)), tree.nd_level, _ptr(_i32(tree.node_offsets)),
+                                         _ptr(_i32(tree.vertices)), 0, C.byref(v)))
+    return int(v.value)
+
+
 def tree_fill(g: AdjacencyGraph, tree: EliminationTree, schedule: str = "postorder",
               ctx: Context | None = None) -> FillReport:  # symbolic.hpp:23 + :31
     ctx = ctx or default_context()

@@ -41,6 +41,7 @@ int set_error(int code, const std::string& msg) {
 }
 
 std::vector<int32_t> make_schedule(int32_t L, int32_t kind);
+int64_t unrelated_edges_dev(mp_context& ctx, const DGraph& g, const int32_t* node_of);
 void compute_perm_blocks_dev(mp_context& ctx, int32_t n, int32_t L, const int32_t* node_offsets,
                              const int32_t* node_vertices, const int32_t* local_perm, int32_t schedule,
                              int32_t b, int32_t* perm, int32_t* inverse, int32_t* node_pos_dev);
@@ -499,6 +500,9 @@ int mp_order(mp_context* ctx, const mp_csr* g, const mp_config* cfg, mp_result* 
       }
     }
     MP_CUDA(cudaEventRecord(ctx->ev[7], s));
+    // the pipeline's self-check (pipeline.cpp:141-142), untimed like the reference's
+    if (unrelated_edges_dev(*ctx, gv.g, node_of) != 0)
+      throw Error(MP_ELOGIC, "separator failed to disconnect its sides");
     // outputs
     const bool od = out->on_device != 0;
     output_copy(*ctx, out->patch_of, asg.get(), n, od);

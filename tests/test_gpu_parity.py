@@ -370,3 +370,45 @@ def test_mesh_to_graph_device_c2():
     g = mp.mesh_to_graph_device(m)
     h = mp.mesh_to_graph(m)
     assert _same_graph(g, h) and g.edge_count() == 2995680
+
+
+# ---------------------------------------------------------------- §8 f2: separation self-check
+def test_separation_check_known_answers():
+    """tests/symbolic_test.cpp:104-129: sibling leaves joined by edges ->
+    cross_block_fill 3 (here: 2 unrelated edges); a proper dissection -> 0."""
+    from oracle.oracle import Reference
+    cycle = graph(4, [(0, 1), (1, 2), (2, 3), (3, 0)])
+    bad = mp.EliminationTree(4, 1, np.array([0, 0, 2, 4], np.int32), np.array([0, 1, 2, 3], np.int32))
+    good = mp.EliminationTree(4, 1, np.array([0, 2, 3, 4], np.int32), np.array([0, 2, 1, 3], np.int32))
+    assert mp.tree_separation_violations(cycle, bad) == 2
+    assert Reference().cross_block_fill(cycle, [0, 1, 2, 3], 1, bad.node_offsets, bad.vertices) == 3
+    assert mp.tree_separation_violations(cycle, good) == 0
+    assert Reference().cross_block_fill(cycle, [1, 3, 0, 2], 1, good.node_offsets, good.vertices) == 0
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_separation_check_agrees_with_cross_block_fill(seed):
+    """Zero violations <=> the reference's cross_block_fill == 0, on our trees
+    and on trees broken by moving one separator vertex into a leaf."""
+    from oracle.oracle import Reference
+    R = Reference()
+    g = mp.mesh_to_graph(mp.make_random_mesh(20, 24, seed))
+    res = mp.order(g, patch_size=12, nd_level=3)
+    t = res.tree
+    assert mp.tree_separation_violations(g, t) == 0
+    assert R.cross_block_fill(g, res.perm.perm, 3, t.node_offsets, t.vertices) == 0
+    # move the root separator's first vertex into the first non-empty leaf
+    off, verts = t.node_offsets.copy(), t.vertices.copy()
+    if off[1] > off[0]:
+        leaf = next(i for i in range(7, 15) if off[i + 1] > off[i])
+        v = verts[off[0]]
+        nv = np.concatenate([verts[off[0] + 1:off[leaf]], [v], verts[off[leaf]:]]).astype(np.int32)
+        new_off = off.copy()
+        new_off[1:leaf + 1] -= 1
+        nv[new_off[leaf]:new_off[leaf + 1]].sort()  # node lists stay ascending
+        lp = np.concatenate([np.arange(new_off[i + 1] - new_off[i]) for i in range(15)]).astype(np.int32)
+        broken = mp.EliminationTree(g.n, 3, new_off, nv, lp)
+        viol = mp.tree_separation_violations(g, broken)
+        perm = mp.compute_perm(broken, g).perm
+        cbf = R.cross_block_fill(g, perm, 3, new_off, nv)
+        assert (viol > 0) == (cbf > 0)
