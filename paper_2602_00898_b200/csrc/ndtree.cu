@@ -767,7 +767,61 @@ __device__ __forceinline__ bool ref_less(const RefKey& x, const RefKey& y) {
 // Per-vertex state is one byte of region (0/1 sides, 2 separator, 3 gone --
 // dead vertices never count as neighbours) plus the vertex's patch side, so
 // no node-membership lookups are needed; adjacency comes from the ELL copy.
-constexpr int32_t kRefSmemList = 6 * 1024;
+constexpr int32_t kRefSmemList = 12 * 1024;  // candidate entries kept in shared memory (10 B each)
+
+// Ordered compaction of [0, cnt) by the whole block: warp w owns the
+// contiguous range [w * per, (w + 1) * per); pass 1 counts, pass 2 emits with
+// ballot ranks.  One block-wide exchange instead of a block scan per 1024
+// items (a 1M-vertex node is 1,000 scans).  classify(i) returns -1 (skip), 0
+// or 1; emit(i, cls, rank within its class).  Returns the two class counts.
+template <class Cls, class Emit>
+__device__ __forceinline__ int2 block_ordered_split(int32_t cnt, int32_t* sh64, Cls classify, Emit emit) {
+  constexpr int U = 8;  // 32-element groups per step: their loads are in flight together
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int32_t per = (cnt + nw - 1) / nw;
+  const int32_t lo = min(cnt, wid * per), hi = min(cnt, lo + per);
+  int32_t c0 = 0, c1 = 0;
+  for (int32_t i0 = lo; i0 < hi; i0 += 32 * U) {
+    int c[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int32_t i = i0 + 32 * q + lane;
+      c[q] = i < hi ? classify(i) : -1;
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      c0 += __popc(__ballot_sync(0xffffffffu, c[q] == 0));
+      c1 += __popc(__ballot_sync(0xffffffffu, c[q] == 1));
+    }
+  }
+  if (lane == 0) sh64[wid] = c0, sh64[32 + wid] = c1;
+  __syncthreads();
+  int32_t b0 = 0, b1 = 0, t0 = 0, t1 = 0;
+  for (int32_t w = 0; w < nw; ++w) {
+    const int32_t x0 = sh64[w], x1 = sh64[32 + w];
+    if (w < wid) b0 += x0, b1 += x1;
+    t0 += x0, t1 += x1;
+  }
+  const uint32_t below = (1u << lane) - 1;
+  for (int32_t i0 = lo; i0 < hi; i0 += 32 * U) {
+    int c[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int32_t i = i0 + 32 * q + lane;
+      c[q] = i < hi ? classify(i) : -1;
+    }
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int32_t i = i0 + 32 * q + lane;
+      const uint32_t m0 = __ballot_sync(0xffffffffu, c[q] == 0), m1 = __ballot_sync(0xffffffffu, c[q] == 1);
+      if (c[q] == 0) emit(i, 0, b0 + __popc(m0 & below));
+      if (c[q] == 1) emit(i, 1, b1 + __popc(m1 & below));
+      b0 += __popc(m0), b1 += __popc(m1);
+    }
+  }
+  __syncthreads();
+  return make_int2(t0, t1);
+}
 constexpr int kRefTab = 16;  // pulls tabulated per side
 
 __device__ __forceinline__ RefKey warp_min_ref(RefKey k) {
@@ -802,11 +856,19 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
     return;
   }
   const int32_t* seg = a.vlist + s0;
-  const bool in_smem = cnt <= kRefSmemList;
-  int32_t* lv = in_smem ? ref_sm : a.sep_list + s0;
-  int32_t* lpull = in_smem ? ref_sm + kRefSmemList : a.ref_pull + s0;
-  uint8_t* lown = in_smem ? reinterpret_cast<uint8_t*>(ref_sm + 2 * kRefSmemList) : a.ref_own + s0;
-  uint8_t* lin = in_smem ? lown + kRefSmemList : a.ref_in + s0;
+  __shared__ int32_t sh64[64];
+  // candidate list: shared memory while it fits (checked before every move;
+  // a move adds at most one entry), the global scratch of the node otherwise
+  bool in_smem;
+  int32_t *lv, *lpull;
+  uint8_t *lown, *lin;
+  auto use_lists = [&](bool sm) {
+    in_smem = sm;
+    lv = sm ? ref_sm : a.sep_list + s0;
+    lpull = sm ? ref_sm + kRefSmemList : a.ref_pull + s0;
+    lown = sm ? reinterpret_cast<uint8_t*>(ref_sm + 2 * kRefSmemList) : a.ref_own + s0;
+    lin = sm ? reinterpret_cast<uint8_t*>(ref_sm + 2 * kRefSmemList) + kRefSmemList : a.ref_in + s0;
+  };
   int8_t* region = a.region;
   const int32_t* ell = a.ell;
 
@@ -824,28 +886,37 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
   // initial separator: the smaller boundary, ties to the left (partition.cpp:212-222)
   const int8_t take = a.bcount[2 * li] <= a.bcount[2 * li + 1] ? 0 : 1;
   {
-    int32_t run = 0, c0 = 0, c1 = 0;
-    for (int32_t i0 = 0; i0 < cnt; i0 += blockDim.x) {
-      const int32_t i = i0 + threadIdx.x;
-      int32_t v = -1, in = 0;
-      if (i < cnt) {
-        v = seg[i];
-        in = a.in_super[v] && region[v] == take;
+    // counts: separator entries, and the remaining vertices per region
+    int32_t nin = 0, c0 = 0, c1 = 0;
+    for (int32_t i0 = 0; i0 < cnt; i0 += 8 * blockDim.x) {
+      int8_t rr[8];
+      bool su[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {  // eight loads in flight per thread
+        const int32_t i = i0 + q * blockDim.x + threadIdx.x;
+        const int32_t v = i < cnt ? seg[i] : -1;
+        rr[q] = v >= 0 ? region[v] : int8_t(-1);
+        su[q] = v >= 0 && a.in_super[v];
       }
-      int32_t tot;
-      const int32_t e = block_excl_scan(in, shi, &tot);
-      if (in) {
-        const int32_t k = run + e;
-        lv[k] = v;
-        lown[k] = static_cast<uint8_t>(take);
-        lin[k] = 1;
-        a.slot_of[v] = k;
-        region[v] = 2;
-      } else if (i < cnt) {
-        (region[v] == 0 ? c0 : c1)++;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (rr[q] < 0) continue;
+        if (su[q] && rr[q] == take) ++nin;
+        else (rr[q] == 0 ? c0 : c1)++;
       }
-      run += tot;
     }
+    const int32_t run = static_cast<int32_t>(block_sum_i64(nin, reinterpret_cast<int64_t*>(sred)));
+    use_lists(run < kRefSmemList / 2);
+    block_ordered_split(
+        cnt, sh64, [&](int32_t i) { const int32_t v = seg[i]; return (a.in_super[v] && region[v] == take) ? 0 : -1; },
+        [&](int32_t i, int, int32_t k) {
+          const int32_t v = seg[i];
+          lv[k] = v;
+          lown[k] = static_cast<uint8_t>(take);
+          lin[k] = 1;
+          a.slot_of[v] = k;
+          region[v] = 2;
+        });
     const int64_t r0 = block_sum_i64(c0, reinterpret_cast<int64_t*>(sred));
     const int64_t r1 = block_sum_i64(c1, reinterpret_cast<int64_t*>(sred));
     if (threadIdx.x == 0) {
@@ -872,6 +943,15 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
   }
   // greedy moves (partition.cpp:235-274)
   for (;;) {
+    if (in_smem && s_list >= kRefSmemList) {  // the list outgrew shared memory: move it to global
+      int32_t* gv = a.sep_list + s0;
+      int32_t* gp = a.ref_pull + s0;
+      uint8_t* go = a.ref_own + s0;
+      uint8_t* gi = a.ref_in + s0;
+      for (int32_t i = threadIdx.x; i < s_list; i += blockDim.x) gv[i] = lv[i], gp[i] = lpull[i], go[i] = lown[i], gi[i] = lin[i];
+      use_lists(false);
+      __syncthreads();
+    }
     const int64_t cur = s_size;
     const double cimb = s_imb;
     const double thr = kBalanceTol > cimb ? kBalanceTol : cimb;
@@ -1077,33 +1157,18 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
   // split the node: separator stays at `node` (and leaves play: region 3),
   // sides go to the children (stable, so each child's list stays ascending)
   int32_t* out = a.next_vlist + s0;
-  int32_t nleft_total;
-  {
-    int32_t c = 0;
-    for (int32_t i = threadIdx.x; i < cnt; i += blockDim.x) c += region[seg[i]] == 0;
-    nleft_total = static_cast<int32_t>(block_sum_i64(c, reinterpret_cast<int64_t*>(sred)));
-  }
-  int32_t runl = 0, runr = 0;
-  for (int32_t i0 = 0; i0 < cnt; i0 += blockDim.x) {
-    const int32_t i = i0 + threadIdx.x;
-    int32_t v = -1;
-    int8_t r = 3;
-    if (i < cnt) {
-      v = seg[i];
-      r = region[v];
-    }
-    int32_t tl, tr;
-    const int32_t el = block_excl_scan(r == 0 ? 1 : 0, shi, &tl);
-    const int32_t er = block_excl_scan(r == 1 ? 1 : 0, shi, &tr);
-    if (r == 0) {
-      out[runl + el] = v;
-      a.node_of[v] = 2 * node + 1;
-    } else if (r == 1) {
-      out[nleft_total + runr + er] = v;
-      a.node_of[v] = 2 * node + 2;
-    }
-    runl += tl, runr += tr;
-  }
+  // left then right, each stable (ascending): two ordered passes, the second
+  // offset by the left count
+  const int2 lr = block_ordered_split(cnt, sh64, [&](int32_t i) { const int8_t r = region[seg[i]]; return r <= 1 ? r : -1; },
+                                      [&](int32_t, int, int32_t) {});
+  const int32_t runl = lr.x, runr = lr.y;
+  block_ordered_split(
+      cnt, sh64, [&](int32_t i) { const int8_t r = region[seg[i]]; return r <= 1 ? r : -1; },
+      [&](int32_t i, int c, int32_t k) {
+        const int32_t v = seg[i];
+        out[c ? runl + k : k] = v;
+        a.node_of[v] = 2 * node + 1 + c;
+      });
   __syncthreads();
   for (int32_t i = threadIdx.x; i < s_list; i += blockDim.x) {
     const int32_t v = lv[i];
@@ -1433,7 +1498,7 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     else exact ? launch_fm(fm_kernel<uint64_t, true>) : launch_fm(fm_kernel<uint64_t, false>);
     st.mark("level/fm");
     MP_KERNEL(ctx, super_pass<<<lgrid, 256, 0, s>>>(a));
-    const size_t ref_smem = static_cast<size_t>(kRefSmemList) * 10;
+    const size_t ref_smem = static_cast<size_t>(kRefSmemList) * 10;  // 120 KB
     allow_max_smem(refine_kernel, ctx.device);
     { const int kt__ = ctx.ktime_begin(kKRefine); MP_KERNEL(ctx, refine_kernel<<<width, kNodeThreads, ref_smem, s>>>(a)); ctx.ktime_end(kt__); }
     st.mark("level/super+refine");
