@@ -352,7 +352,10 @@ def run_ours(args):
         traffic = None
         tp = ROOT / "profiles" / "traffic.json"
         if tp.exists():
-            traffic = json.loads(tp.read_text()).get(dom_name)
+            tj = json.loads(tp.read_text())
+            traffic = tj.get(dom_name)
+            if dom_name == "fps" and traffic is not None:  # the kernel-time slot covers both FPS kernels
+                traffic += tj.get("fps_cluster_phase", 0)
         cpu = None
         if not args.no_cpu and ws >= 1:
             threads = os.cpu_count() or 1
