@@ -881,7 +881,10 @@ void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32
       cluster_ctas = 0;
       allow_max_smem(fps_cluster_phase, ctx.device);
       cudaFuncSetAttribute(fps_cluster_phase, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      for (int cs : {16, 8}) {
+      const char* ce = getenv("MP_FPS_CLUSTER");  // tuning knob: cluster size to try first
+      const int first = ce ? atoi(ce) : 16;
+      for (int cs : {first, 16, 8}) {
+        if (cs < 1 || cs > 16) continue;
         cudaLaunchConfig_t cfg{};
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
