@@ -76,6 +76,9 @@ struct BatchArgs {
   int32_t grid_cands;      // candidates per grid-mode batch
   int32_t sub_region;      // largest region (last batch) that still runs kMaxSub groups per CTA
   int32_t resume;          // 1: fps_cluster_phase ran the large-radius seeds; continue from its state
+  int32_t* queue;          // cluster phase work queue (qcap slots, -1 = empty)
+  int32_t* qctl;           // [0] head [1] tail [2] pending
+  int64_t qcap;
   int32_t* seeds;          // output, k
   unsigned long long* work;
 };
@@ -309,9 +312,13 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
   __shared__ int32_t s_wcnt[kMaxSub][3], s_wn[kMaxSub], s_wnlev[kMaxSub];
   __shared__ int32_t s_wlstart[kMaxSub][kMaxDepth + 2];  // region-list offset of each BFS level
 
-  if (a.resume) {  // seeds so far, dist, tiles and the next candidates come from fps_cluster_phase
+  if (a.resume && __ldcg(&a.ctl[12]) == 0) {  // seeds, dist, tiles and the next candidates from fps_cluster_phase
     if (__ldcg(&a.ctl[0]) >= a.k) return;
-  } else {
+  } else {  // (no cluster phase, or its queue overflowed: start over here)
+    if (a.resume) {
+      const int32_t nt = a.ntile / 32 + 1;
+      for (int64_t i = gtid; i < nt; i += gthreads) a.tbits[i] = 0;
+    }
     for (int64_t v = gtid; v < a.n; v += gthreads) a.dist[v] = kUnreached;
     if (gtid == 0) {
       a.ctl[0] = 0, a.ctl[2] = 0, a.ctl[1] = 1, a.ctl[3] = 1;  // batch 0: the start vertex, grid mode
@@ -666,101 +673,135 @@ __global__ void __launch_bounds__(kThreads, 1) fps_cluster_phase(BatchArgs a, in
   const uint32_t rank = cluster_rank();
   const int64_t ctid = static_cast<int64_t>(rank) * blockDim.x + threadIdx.x;
   const int64_t cthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;  // the grid is one cluster
-  // Each CTA keeps the frontier vertices it claims in its shared memory
-  // (double-buffered by level parity; the other CTAs read them through
-  // distributed shared memory) and appends every claimed vertex to its region
-  // list, a row of the a.reg slab (overflowing frontier entries are read from
-  // there).  After the cluster barrier every CTA reads the 16 level counts.
-  constexpr int32_t kCF = 4096;
-  __shared__ int32_t s_front[2][kCF], s_fcnt[2], s_fbeg[2];
-  __shared__ int32_t s_len, s_pre[33], s_rbeg[32];
-  cg::cluster_group cl = cg::this_cluster();
+  // Asynchronous label-correcting BFS (no level barriers): a global work
+  // queue of vertices whose dist just dropped; a warp reserves 32 slots, waits
+  // for their items, relaxes their neighbours with atomicMin(dist, dist[u]+1)
+  // and queues every vertex it lowers.  The fixed point is the exact BFS
+  // distance min'd with the previous dist (relaxations commute), i.e. the
+  // same result as level-synchronous BFS.  `pending` counts queued but
+  // unfinished items (raised before a push is published, lowered after the
+  // item is done), so pending == 0 means no work is left anywhere.  Each CTA
+  // appends the vertices it lowers to its region list for the tile refresh.
   int32_t* const myl = a.reg + static_cast<int64_t>(rank) * a.n;
+  __shared__ int32_t s_len;
   unsigned long long scans = 0, levels = 0;
   const int32_t tsize = 1 << a.tile_shift;
-  const int32_t ncta = static_cast<int32_t>(gridDim.x);
+  int32_t* q = a.queue;
+  int32_t* qc = a.qctl;  // [0] head [1] tail [2] pending [3] overflow
+  const int64_t qcap = a.qcap;
 
   for (int64_t v = ctid; v < a.n; v += cthreads) a.dist[v] = kUnreached;
-  if (ctid == 0) a.ctl[2] = 0;  // touched tiles
+  if (ctid == 0) a.ctl[2] = 0, a.ctl[12] = 0;  // touched tiles, overflow
   cluster_barrier();
   int32_t c = static_cast<int32_t>(splitmix64(a.seed) % static_cast<uint64_t>(a.n));  // patching.cpp:32
   int32_t done = 0;
   for (;;) {
-    if (threadIdx.x == 0) {
-      s_fcnt[0] = 0, s_fbeg[0] = 0, s_len = 0;
-      if (rank == 0) {
-        a.seeds[done] = c;
-        a.dist[c] = 0;
-        myl[0] = c;
-        s_front[0][0] = c;
-        s_fcnt[0] = 1, s_len = 1;
-      }
+    if (threadIdx.x == 0) s_len = 0;
+    if (ctid == 0) {
+      const int32_t t = *reinterpret_cast<volatile int32_t*>(&qc[1]);
+      a.seeds[done] = c;
+      a.dist[c] = 0;
+      myl[0] = c;
+      s_len = 1;
+      q[t] = c;
+      qc[0] = t, qc[1] = t + 1, qc[2] = 1;
     }
     ++done;
-    __syncthreads();
-    for (int32_t d = 0;; ++d) {  // level-synchronous BFS of the new seed's region
-      const int p = d & 1, q = p ^ 1;
-      cluster_barrier();  // every CTA's level-d frontier is complete
-      if (threadIdx.x < 32) {  // prefix of the CTAs' level counts (DSMEM reads)
-        const int32_t r = threadIdx.x;
-        const int32_t cnt = r < ncta ? *cl.map_shared_rank(&s_fcnt[p], r) : 0;
-        int32_t inc = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-          if (r >= o) inc += y;
-        }
-        s_pre[r + 1] = inc;
-        if (r == 0) s_pre[0] = 0, s_fcnt[q] = 0;
-        s_rbeg[r] = r < ncta ? *cl.map_shared_rank(&s_fbeg[p], r) : 0;
+    cluster_barrier();
+    int64_t my_slot = -1;  // this lane's reserved queue slot (kept until its item arrives)
+    for (int idle = 0;;) {
+      const uint32_t needy = __ballot_sync(0xffffffffu, my_slot < 0);
+      if (needy) {
+        int32_t h0 = 0;
+        if (lane == 0) h0 = atomicAdd(&qc[0], __popc(needy));
+        h0 = __shfl_sync(0xffffffffu, h0, 0);
+        if (my_slot < 0) my_slot = static_cast<int64_t>(h0) + __popc(needy & ((1u << lane) - 1));
       }
-      __syncthreads();
-      const int32_t nf = s_pre[ncta];
-      if (nf == 0) break;
-      const int32_t len0 = s_len;  // this level's claims go to myl[len0 ...]
-      const int64_t items = static_cast<int64_t>(nf) * 8;
-      for (int64_t base = ctid - lane; base < items; base += cthreads) {
-        const int64_t it = base + lane;
-        int32_t x = -1, u = 0;
-        if (it < items) {
-          const int32_t i = static_cast<int32_t>(it >> 3);
-          int32_t r = 0;
+      if (__any_sync(0xffffffffu, my_slot >= qcap)) {
+        if (lane == 0) atomicExch(&a.ctl[12], 1), atomicExch(&qc[2], 0);  // abort: the main kernel redoes FPS
+        break;
+      }
+      // one poll per round: a lane never blocks the others of its warp
+      const int32_t u = *reinterpret_cast<volatile int32_t*>(&q[my_slot]);
+      const bool have = u >= 0;
+      if (have) my_slot = -1;
+      if (!__any_sync(0xffffffffu, have)) {
+        int32_t pend = lane == 0 ? *reinterpret_cast<volatile int32_t*>(&qc[2]) : 0;
+        pend = __shfl_sync(0xffffffffu, pend, 0);  // one verdict per warp
+        if (pend == 0) break;                       // no work anywhere: region complete
+        if (++idle > (1 << 22)) {                   // watchdog (never expected): fall back
+          if (lane == 0) atomicExch(&a.ctl[12], 1), atomicExch(&qc[2], 0);
+          break;
+        }
+        if (idle > 4) __nanosleep(64);
+        continue;
+      }
+      idle = 0;
+      // relax u's neighbours
+      int32_t np = 0, xs[8];
+      if (have) {
+        const int32_t nd = __ldcg(&a.dist[u]) + 1;
+        const int4* row = reinterpret_cast<const int4*>(a.ell + static_cast<int64_t>(u) * 8);
+        const int4 r0 = row[0], r1 = row[1];
+        const int32_t cand[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+        int32_t old[8];
 #pragma unroll
-          for (int k = 16; k > 0; k >>= 1)
-            if (r + k < ncta && s_pre[r + k] <= i) r += k;
-          const int32_t j = i - s_pre[r];
-          u = j < kCF ? *cl.map_shared_rank(&s_front[p][j], r)
-                      : __ldcg(&a.reg[static_cast<int64_t>(r) * a.n + s_rbeg[r] + j]);
-          x = a.ell[static_cast<int64_t>(u) * 8 + (it & 7)];
-        }
-        const bool push = x >= 0 && atomicMin(&a.dist[x], d + 1) > d + 1;
-        const int32_t slot = warp_append(&s_fcnt[q], push);
-        if (push) {
-          if (slot < kCF) s_front[q][slot] = x;
-          myl[len0 + slot] = x;
-        }
-        if (x < -1)  // CSR tail of a vertex with more than 8 neighbours
-          for (int32_t k = -x - 2; k < a.g.off[u + 1]; ++k) {
-            const int32_t w = a.g.nbr[k];
-            if (atomicMin(&a.dist[w], d + 1) > d + 1) {
-              const int32_t sl = atomicAdd(&s_fcnt[q], 1);
-              if (sl < kCF) s_front[q][sl] = w;
-              myl[len0 + sl] = w;
+        for (int k = 0; k < 8; ++k) old[k] = cand[k] >= 0 ? atomicMin(&a.dist[cand[k]], nd) : 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (cand[k] >= 0 && old[k] > nd) xs[np++] = cand[k];
+        scans += a.g.off[u + 1] - a.g.off[u];
+        if (cand[7] < -1)  // CSR tail of a vertex with more than 8 neighbours: queued one by one
+          for (int32_t j = -cand[7] - 2; j < a.g.off[u + 1]; ++j) {
+            const int32_t w = a.g.nbr[j];
+            if (atomicMin(&a.dist[w], nd) > nd) {
+              atomicAdd(&qc[2], 1);
+              const int32_t t = atomicAdd(&qc[1], 1);
+              if (t < qcap) q[t] = w;
+              else atomicExch(&a.ctl[12], 1);
+              const int32_t li = atomicAdd(&s_len, 1);
+              if (li < a.n) myl[li] = w;
+              else atomicExch(&a.ctl[12], 1);
             }
           }
       }
+      // publish the pushes: pending first, then the slots, then retire the items
+      int32_t inc = np;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+      }
+      const int32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+      const int32_t nproc = __popc(__ballot_sync(0xffffffffu, have));
+      int32_t base = 0, lbase = 0;
+      if (lane == 0 && tot) {
+        atomicAdd(&qc[2], tot);
+        base = atomicAdd(&qc[1], tot);
+        lbase = atomicAdd(&s_len, tot);
+      }
+      base = __shfl_sync(0xffffffffu, base, 0);
+      lbase = __shfl_sync(0xffffffffu, lbase, 0);
+      const int32_t my0 = inc - np;
+      for (int k = 0; k < np; ++k) {
+        const int64_t t = static_cast<int64_t>(base) + my0 + k;
+        if (t < qcap) q[t] = xs[k];
+        else atomicExch(&a.ctl[12], 1);
+        if (lbase + my0 + k < a.n) myl[lbase + my0 + k] = xs[k];
+        else atomicExch(&a.ctl[12], 1);
+      }
+      __threadfence();
+      if (lane == 0 && nproc) atomicSub(&qc[2], nproc);
       ++levels;
-      __syncthreads();
-      if (threadIdx.x == 0) s_fbeg[q] = len0, s_len = len0 + s_fcnt[q];
-      __syncthreads();
     }
+    cluster_barrier();
+    if (__ldcg(&a.ctl[12])) break;  // queue or list overflow: fps_batched_kernel starts over
     // mark the tiles of this CTA's region vertices
-    for (int32_t i = threadIdx.x; i < s_len; i += blockDim.x) {
+    for (int32_t i = threadIdx.x; i < min(s_len, a.n); i += blockDim.x) {
       const int32_t w = myl[i];
       const int32_t t = w >> a.tile_shift;
       const uint32_t bit = 1u << (t & 31);
       if (!(atomicOr(&a.tbits[t >> 5], bit) & bit)) a.tlist[atomicAdd(&a.ctl[2], 1)] = t;
-      scans += a.g.off[w + 1] - a.g.off[w];
     }
     cluster_barrier();
     // refresh the touched tile and subtile maxima
@@ -806,7 +847,7 @@ __global__ void __launch_bounds__(kThreads, 1) fps_cluster_phase(BatchArgs a, in
       }
     }
     __syncthreads();
-    if (done < a.k) select_candidates(a, w_main, bsm, reinterpret_cast<int32_t*>(bsm + kSCap), shi);
+    if (done < a.k && !__ldcg(&a.ctl[12])) select_candidates(a, w_main, bsm, reinterpret_cast<int32_t*>(bsm + kSCap), shi);
   }
   if (a.work) {
     const uint64_t tot = block_sum_i64(static_cast<int64_t>(scans), reinterpret_cast<int64_t*>(s_red));
@@ -875,6 +916,12 @@ void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32
   const int kt = ctx.ktime_begin(kKFps);
   // large-radius seeds on one cluster (16 CTAs where the device allows, else 8)
   a.resume = 0;
+  a.qcap = 8LL * n + 1024;
+  a.queue = static_cast<int32_t*>(ctx.slab(4, sizeof(int32_t) * a.qcap));
+  DevBuf<int32_t> qctl(4, s);
+  a.qctl = qctl;
+  MP_CUDA(cudaMemsetAsync(a.queue, 0xff, sizeof(int32_t) * a.qcap, s));
+  MP_CUDA(cudaMemsetAsync(qctl, 0, sizeof(int32_t) * 4, s));
   if (!getenv("MP_FPS_NO_CLUSTER")) {
     static int cluster_ctas = -1;  // decided once per process
     if (cluster_ctas < 0) {
