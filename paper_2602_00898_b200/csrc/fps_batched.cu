@@ -40,6 +40,7 @@ constexpr int kMaxSub = 4;        // worker groups per CTA when regions are smal
 constexpr int kSubRegion = 4096;  // ... i.e. when the last batch's largest region was below this
 constexpr int kMaskWords = kMaxWorkers / 32;
 constexpr int kGridCands = 64;    // candidates per grid-mode batch
+constexpr int kQHead = 0, kQTail = 32, kQPend = 64;  // cluster-queue control words, 128 B apart
 constexpr int kMaxDepth = 250;    // worker BFS depth bound (< the grid radius, clamped to it)
 
 __host__ __device__ inline uint64_t splitmix64(uint64_t x) {  // patching.cpp:17-22
@@ -673,22 +674,26 @@ __global__ void __launch_bounds__(kThreads, 1) fps_cluster_phase(BatchArgs a, in
   const uint32_t rank = cluster_rank();
   const int64_t ctid = static_cast<int64_t>(rank) * blockDim.x + threadIdx.x;
   const int64_t cthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;  // the grid is one cluster
-  // Asynchronous label-correcting BFS (no level barriers): a global work
-  // queue of vertices whose dist just dropped; a warp reserves 32 slots, waits
-  // for their items, relaxes their neighbours with atomicMin(dist, dist[u]+1)
-  // and queues every vertex it lowers.  The fixed point is the exact BFS
-  // distance min'd with the previous dist (relaxations commute), i.e. the
-  // same result as level-synchronous BFS.  `pending` counts queued but
-  // unfinished items (raised before a push is published, lowered after the
-  // item is done), so pending == 0 means no work is left anywhere.  Each CTA
-  // appends the vertices it lowers to its region list for the tile refresh.
+  // Asynchronous label-correcting BFS (no level barriers).  Every lane holds
+  // at most one work item (vertex, dist); a warp relaxes its items' neighbours
+  // with atomicMin(dist, d + 1), keeps the vertices it lowered as its next items
+  // (one per free lane: the front stays with the warp that reached it, so a hop
+  // costs an ELL row load and the atomics) and spills the rest to a global
+  // queue that idle lanes poll.  The fixed point is the exact BFS distance
+  // min'd with the previous dist (relaxations commute): the level-synchronous
+  // result.  `pending` counts existing unprocessed items (raised before a new
+  // item is published, lowered after an item is done), so pending == 0 means
+  // no work is left anywhere.  Each CTA appends the vertices it lowers to its
+  // region list for the tile refresh.
   int32_t* const myl = a.reg + static_cast<int64_t>(rank) * a.n;
   __shared__ int32_t s_len;
   unsigned long long scans = 0, levels = 0;
   const int32_t tsize = 1 << a.tile_shift;
-  int32_t* q = a.queue;
-  int32_t* qc = a.qctl;  // [0] head [1] tail [2] pending [3] overflow
+  uint64_t* q = reinterpret_cast<uint64_t*>(a.queue);  // items dist << 32 | vertex, ~0 = empty
+  int32_t* qc = a.qctl;  // head, tail, pending: one 128-byte line each (no shared hot spot)
   const int64_t qcap = a.qcap;
+  const int wid = threadIdx.x >> 5;
+  uint64_t* stage = bsm + 256 * wid;  // per warp: this step's lowered (dist, vertex) (dynamic smem)
 
   for (int64_t v = ctid; v < a.n; v += cthreads) a.dist[v] = kUnreached;
   if (ctid == 0) a.ctl[2] = 0, a.ctl[12] = 0;  // touched tiles, overflow
@@ -698,66 +703,71 @@ __global__ void __launch_bounds__(kThreads, 1) fps_cluster_phase(BatchArgs a, in
   for (;;) {
     if (threadIdx.x == 0) s_len = 0;
     if (ctid == 0) {
-      const int32_t t = *reinterpret_cast<volatile int32_t*>(&qc[1]);
+      const int32_t t = *reinterpret_cast<volatile int32_t*>(&qc[kQTail]);
       a.seeds[done] = c;
       a.dist[c] = 0;
       myl[0] = c;
       s_len = 1;
-      q[t] = c;
-      qc[0] = t, qc[1] = t + 1, qc[2] = 1;
+      q[t] = static_cast<uint32_t>(c);  // dist 0
+      qc[kQHead] = t, qc[kQTail] = t + 1, qc[kQPend] = 1;
     }
     ++done;
     cluster_barrier();
     int64_t my_slot = -1;  // this lane's reserved queue slot (kept until its item arrives)
+    int32_t u = -1, du = 0;  // this lane's item
     for (int idle = 0;;) {
-      const uint32_t needy = __ballot_sync(0xffffffffu, my_slot < 0);
+      // idle lanes reserve a queue slot (once) and poll it without blocking
+      const uint32_t needy = __ballot_sync(0xffffffffu, u < 0 && my_slot < 0);
       if (needy) {
         int32_t h0 = 0;
-        if (lane == 0) h0 = atomicAdd(&qc[0], __popc(needy));
+        if (lane == 0) h0 = atomicAdd(&qc[kQHead], __popc(needy));
         h0 = __shfl_sync(0xffffffffu, h0, 0);
-        if (my_slot < 0) my_slot = static_cast<int64_t>(h0) + __popc(needy & ((1u << lane) - 1));
+        if (u < 0 && my_slot < 0) my_slot = static_cast<int64_t>(h0) + __popc(needy & ((1u << lane) - 1));
       }
       if (__any_sync(0xffffffffu, my_slot >= qcap)) {
-        if (lane == 0) atomicExch(&a.ctl[12], 1), atomicExch(&qc[2], 0);  // abort: the main kernel redoes FPS
+        if (lane == 0) atomicExch(&a.ctl[12], 1), atomicExch(&qc[kQPend], 0);  // abort: the main kernel redoes FPS
         break;
       }
-      // one poll per round: a lane never blocks the others of its warp
-      const int32_t u = *reinterpret_cast<volatile int32_t*>(&q[my_slot]);
+      if (u < 0 && my_slot >= 0) {
+        const uint64_t it = *reinterpret_cast<volatile uint64_t*>(&q[my_slot]);
+        if (it != ~0ull) u = static_cast<int32_t>(static_cast<uint32_t>(it)), du = static_cast<int32_t>(it >> 32), my_slot = -1;
+      }
       const bool have = u >= 0;
-      if (have) my_slot = -1;
       if (!__any_sync(0xffffffffu, have)) {
-        int32_t pend = lane == 0 ? *reinterpret_cast<volatile int32_t*>(&qc[2]) : 0;
+        int32_t pend = lane == 0 ? *reinterpret_cast<volatile int32_t*>(&qc[kQPend]) : 0;
         pend = __shfl_sync(0xffffffffu, pend, 0);  // one verdict per warp
         if (pend == 0) break;                       // no work anywhere: region complete
         if (++idle > (1 << 22)) {                   // watchdog (never expected): fall back
-          if (lane == 0) atomicExch(&a.ctl[12], 1), atomicExch(&qc[2], 0);
+          if (lane == 0) atomicExch(&a.ctl[12], 1), atomicExch(&qc[kQPend], 0);
           break;
         }
-        if (idle > 4) __nanosleep(64);
+        if (idle > 2) __nanosleep(idle < 32 ? 64 * idle : 2048);  // back off: idle polls must not starve the atomics
         continue;
       }
       idle = 0;
-      // relax u's neighbours
-      int32_t np = 0, xs[8];
+      // relax the items' neighbours
+      int32_t np = 0;
+      uint64_t mine[8];
       if (have) {
-        const int32_t nd = __ldcg(&a.dist[u]) + 1;
+        const int32_t nd = du + 1;
         const int4* row = reinterpret_cast<const int4*>(a.ell + static_cast<int64_t>(u) * 8);
         const int4 r0 = row[0], r1 = row[1];
         const int32_t cand[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
         int32_t old[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) old[k] = cand[k] >= 0 ? atomicMin(&a.dist[cand[k]], nd) : 0;
+        const uint64_t hi = static_cast<uint64_t>(nd) << 32;
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-          if (cand[k] >= 0 && old[k] > nd) xs[np++] = cand[k];
+          if (cand[k] >= 0 && old[k] > nd) mine[np++] = hi | static_cast<uint32_t>(cand[k]);
         scans += a.g.off[u + 1] - a.g.off[u];
-        if (cand[7] < -1)  // CSR tail of a vertex with more than 8 neighbours: queued one by one
+        if (cand[7] < -1)  // CSR tail of a vertex with more than 8 neighbours: straight to the queue
           for (int32_t j = -cand[7] - 2; j < a.g.off[u + 1]; ++j) {
             const int32_t w = a.g.nbr[j];
             if (atomicMin(&a.dist[w], nd) > nd) {
-              atomicAdd(&qc[2], 1);
-              const int32_t t = atomicAdd(&qc[1], 1);
-              if (t < qcap) q[t] = w;
+              atomicAdd(&qc[kQPend], 1);
+              const int32_t t = atomicAdd(&qc[kQTail], 1);
+              if (t < qcap) q[t] = hi | static_cast<uint32_t>(w);
               else atomicExch(&a.ctl[12], 1);
               const int32_t li = atomicAdd(&s_len, 1);
               if (li < a.n) myl[li] = w;
@@ -765,7 +775,7 @@ __global__ void __launch_bounds__(kThreads, 1) fps_cluster_phase(BatchArgs a, in
             }
           }
       }
-      // publish the pushes: pending first, then the slots, then retire the items
+      // stage the lowered vertices warp-wide
       int32_t inc = np;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -774,24 +784,42 @@ __global__ void __launch_bounds__(kThreads, 1) fps_cluster_phase(BatchArgs a, in
       }
       const int32_t tot = __shfl_sync(0xffffffffu, inc, 31);
       const int32_t nproc = __popc(__ballot_sync(0xffffffffu, have));
+      for (int k = 0; k < np; ++k) stage[inc - np + k] = mine[k];
+      u = -1;
+      // lanes without a reservation take the first items; the rest is spilled
+      const uint32_t freel = __ballot_sync(0xffffffffu, my_slot < 0);
+      const int32_t nfree = __popc(freel);
+      const int32_t keep = min(tot, nfree), spill = tot - keep;
       int32_t base = 0, lbase = 0;
       if (lane == 0 && tot) {
-        atomicAdd(&qc[2], tot);
-        base = atomicAdd(&qc[1], tot);
+        atomicAdd(&qc[kQPend], tot);  // before any of them can be retired
+        if (spill) base = atomicAdd(&qc[kQTail], spill);
         lbase = atomicAdd(&s_len, tot);
       }
       base = __shfl_sync(0xffffffffu, base, 0);
       lbase = __shfl_sync(0xffffffffu, lbase, 0);
-      const int32_t my0 = inc - np;
-      for (int k = 0; k < np; ++k) {
-        const int64_t t = static_cast<int64_t>(base) + my0 + k;
-        if (t < qcap) q[t] = xs[k];
-        else atomicExch(&a.ctl[12], 1);
-        if (lbase + my0 + k < a.n) myl[lbase + my0 + k] = xs[k];
-        else atomicExch(&a.ctl[12], 1);
+      __syncwarp();
+      if (my_slot < 0) {
+        const int32_t r = __popc(freel & ((1u << lane) - 1));
+        if (r < keep) {
+          const uint64_t it = stage[r];
+          u = static_cast<int32_t>(static_cast<uint32_t>(it)), du = static_cast<int32_t>(it >> 32);
+        }
       }
-      __threadfence();
-      if (lane == 0 && nproc) atomicSub(&qc[2], nproc);
+      for (int32_t i = lane; i < tot; i += 32) {
+        const uint64_t it = stage[i];
+        if (lbase + i < a.n) myl[lbase + i] = static_cast<int32_t>(static_cast<uint32_t>(it));
+        else atomicExch(&a.ctl[12], 1);
+        if (i >= keep) {
+          const int64_t t = static_cast<int64_t>(base) + (i - keep);
+          if (t < qcap) q[t] = it;
+          else atomicExch(&a.ctl[12], 1);
+        }
+      }
+      // (same-address atomics of one thread are ordered: the increment above
+      //  lands before this decrement, so pending never reads 0 early)
+      if (lane == 0 && nproc) atomicSub(&qc[kQPend], nproc);
+      __syncwarp();
       ++levels;
     }
     cluster_barrier();
@@ -916,12 +944,14 @@ void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32
   const int kt = ctx.ktime_begin(kKFps);
   // large-radius seeds on one cluster (16 CTAs where the device allows, else 8)
   a.resume = 0;
-  a.qcap = 8LL * n + 1024;
-  a.queue = static_cast<int32_t*>(ctx.slab(4, sizeof(int32_t) * a.qcap));
-  DevBuf<int32_t> qctl(4, s);
+  // the cluster kernel's dynamic smem: the select scratch, or 256 staged items per warp
+  const size_t cl_smem = std::max(smem, sizeof(uint64_t) * 256 * (kThreads / 32));
+  a.qcap = 8LL * n + 1024;  // uint64 items
+  a.queue = static_cast<int32_t*>(ctx.slab(4, sizeof(uint64_t) * a.qcap));
+  DevBuf<int32_t> qctl(96, s);
   a.qctl = qctl;
-  MP_CUDA(cudaMemsetAsync(a.queue, 0xff, sizeof(int32_t) * a.qcap, s));
-  MP_CUDA(cudaMemsetAsync(qctl, 0, sizeof(int32_t) * 4, s));
+  MP_CUDA(cudaMemsetAsync(a.queue, 0xff, sizeof(uint64_t) * a.qcap, s));
+  MP_CUDA(cudaMemsetAsync(qctl, 0, sizeof(int32_t) * 96, s));
   if (!getenv("MP_FPS_NO_CLUSTER")) {
     static int cluster_ctas = -1;  // decided once per process
     if (cluster_ctas < 0) {
@@ -936,7 +966,7 @@ void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
         at[0].val.clusterDim.x = cs, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
-        cfg.gridDim = dim3(cs), cfg.blockDim = dim3(kThreads), cfg.dynamicSmemBytes = smem;
+        cfg.gridDim = dim3(cs), cfg.blockDim = dim3(kThreads), cfg.dynamicSmemBytes = cl_smem;
         cfg.attrs = at, cfg.numAttrs = 1;
         int ncl = 0;
         if (cudaOccupancyMaxActiveClusters(&ncl, fps_cluster_phase, &cfg) == cudaSuccess && ncl > 0) {
@@ -951,7 +981,7 @@ void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeClusterDimension;
       at[0].val.clusterDim.x = cluster_ctas, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
-      cfg.gridDim = dim3(cluster_ctas), cfg.blockDim = dim3(kThreads), cfg.dynamicSmemBytes = smem;
+      cfg.gridDim = dim3(cluster_ctas), cfg.blockDim = dim3(kThreads), cfg.dynamicSmemBytes = cl_smem;
       cfg.stream = s, cfg.attrs = at, cfg.numAttrs = 1;
       MP_KERNEL(ctx, MP_CUDA(cudaLaunchKernelEx(&cfg, fps_cluster_phase, a, static_cast<int32_t>(W))));
       a.resume = 1;
