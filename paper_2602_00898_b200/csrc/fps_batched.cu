@@ -60,7 +60,8 @@ struct BatchArgs {
   int32_t* smax;           // n/32 subtile maximum distances (refreshed with the tiles)
   uint32_t* tbits;         // touched tiles
   int32_t* tlist;          // ntile
-  uint32_t* vm;            // n * kMaskWords visit bits: bit j of vertex v = v is in region j this batch
+  uint32_t* vm;            // visit bits, one plane of vwords words per worker: bit v of plane j = v in region j
+  int64_t vwords;
   int32_t* dw;             // grid-mode distances, grid_cands * n
   int32_t* reg;            // W * n worker region lists (level-ordered)
   int32_t* cand;           // kSCap
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
     const bool gridmode = __ldcg(&a.ctl[3]) != 0;
     int32_t nc, nsub, G, sub, gt, wk, my_word;
     uint32_t my_bit;
-    int64_t reg_cap;
+    int64_t reg_cap, my_plane;
     int32_t* my_reg;
     long long t_reg0 = clock64();
     for (;;) {  // a worker whose region outgrows its list share: redo with one group per CTA
@@ -347,6 +348,7 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
     wk = static_cast<int32_t>(blockIdx.x) * nsub + sub;  // candidate of this group
     my_word = wk >> 5;
     my_bit = 1u << (wk & 31);
+    my_plane = static_cast<int64_t>(wk) * a.vwords;
     reg_cap = a.n / nsub;
     my_reg = a.reg + static_cast<int64_t>(blockIdx.x) * a.n + static_cast<int64_t>(sub) * reg_cap;
     auto gsync = [&]() {
@@ -356,7 +358,7 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
     if (gridmode) {
       for (int32_t j = static_cast<int32_t>(gtid); j < nc; j += static_cast<int32_t>(gthreads)) {
         const int32_t c = __ldcg(&a.cand[j]);
-        atomicOr(&a.vm[static_cast<int64_t>(c) * kMaskWords + (j >> 5)], 1u << (j & 31));
+        atomicOr(&a.vm[static_cast<int64_t>(j) * a.vwords + (c >> 5)], 1u << (c & 31));
         a.dw[static_cast<int64_t>(j) * a.n + c] = 0;
         a.glist[j] = (static_cast<uint64_t>(j) << 32) | static_cast<uint32_t>(c);
         a.mkey[j] = vkey(0, c);
@@ -385,7 +387,8 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
           const uint32_t jbit = 1u << (j & 31);
           uint64_t mk = 0;  // largest key this lane claims (the region's max key, mkey)
           auto claim = [&](int32_t w) -> bool {
-            if (d + 1 < __ldcg(&a.dist[w]) && !(atomicOr(&a.vm[static_cast<int64_t>(w) * kMaskWords + jword], jbit) & jbit)) {
+            const uint32_t wb = 1u << (w & 31);
+            if (d + 1 < __ldcg(&a.dist[w]) && !(atomicOr(&a.vm[static_cast<int64_t>(j) * a.vwords + (w >> 5)], wb) & wb)) {
               jdw[w] = d + 1;
               mk = max(mk, vkey(d + 1, w));
               return true;
@@ -417,7 +420,8 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
       if (gtid == 0) a.ctl[8] = lbeg;  // entries in glist
       for (int32_t q = static_cast<int32_t>(gtid); q < nc * nc; q += static_cast<int32_t>(gthreads)) {
         const int32_t i = q / nc, j = q % nc;
-        if ((__ldcg(&a.vm[static_cast<int64_t>(__ldcg(&a.cand[j])) * kMaskWords + (i >> 5)]) >> (i & 31)) & 1u)
+        const int32_t cj = __ldcg(&a.cand[j]);
+        if ((__ldcg(&a.vm[static_cast<int64_t>(i) * a.vwords + (cj >> 5)]) >> (cj & 31)) & 1u)
           atomicOr(&a.inm[i * kMaskWords + (j >> 5)], 1u << (j & 31));
       }
     } else if (wk < nc) {
@@ -429,7 +433,7 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
       int32_t* cnt3 = s_wcnt[sub];
       int32_t* lstart = s_wlstart[sub];
       if (gt == 0) {
-        atomicOr(&a.vm[static_cast<int64_t>(c) * kMaskWords + my_word], my_bit);
+        atomicOr(&a.vm[my_plane + (c >> 5)], 1u << (c & 31));
         my_reg[0] = c;
         lstart[0] = 0;
         sf0[0] = c;
@@ -454,7 +458,7 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
         const int32_t items = nf * 8;
         auto relax = [&](int32_t w) {
           if (d + 1 < __ldcg(&a.dist[w]) &&
-              !(atomicOr(&a.vm[static_cast<int64_t>(w) * kMaskWords + my_word], my_bit) & my_bit)) {
+              !(atomicOr(&a.vm[my_plane + (w >> 5)], 1u << (w & 31)) & (1u << (w & 31)))) {
             const int32_t slot = atomicAdd(cout, 1);
             if (slot < fcap) fout[slot] = w;
             if (rtop + slot < reg_cap) my_reg[rtop + slot] = w;
@@ -477,15 +481,15 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
           }
 #pragma unroll
           for (int q = 0; q < kUnroll; ++q) ds[q] = xs[q] >= 0 ? __ldcg(&a.dist[xs[q]]) : 0;
-          uint32_t old[kUnroll];
+          uint32_t old[kUnroll];  // the claimed vertex's previous visit bit (1: already ours)
 #pragma unroll
           for (int q = 0; q < kUnroll; ++q)
             old[q] = (xs[q] >= 0 && d + 1 < ds[q])
-                         ? atomicOr(&a.vm[static_cast<int64_t>(xs[q]) * kMaskWords + my_word], my_bit)
-                         : my_bit;
+                         ? atomicOr(&a.vm[my_plane + (xs[q] >> 5)], 1u << (xs[q] & 31)) >> (xs[q] & 31) & 1u
+                         : 1u;
 #pragma unroll
           for (int q = 0; q < kUnroll; ++q) {
-            if (!(old[q] & my_bit)) {
+            if (!old[q]) {
               const int32_t w = xs[q];
               const int32_t slot = atomicAdd(cout, 1);
               if (slot < fcap) fout[slot] = w;
@@ -524,14 +528,16 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
       }
       for (int32_t j0 = 0; j0 < nc; j0 += G) {  // which candidates lie in this region
         const int32_t j = j0 + gt;
-        const bool in = j < nc && (__ldcg(&a.vm[static_cast<int64_t>(__ldcg(&a.cand[j])) * kMaskWords + my_word]) & my_bit);
+        int32_t cj = 0;
+        if (j < nc) cj = __ldcg(&a.cand[j]);
+        const bool in = j < nc && ((__ldcg(&a.vm[my_plane + (cj >> 5)]) >> (cj & 31)) & 1u);
         const uint32_t bits = __ballot_sync(0xffffffffu, in);
         if (lane == 0 && j < kMaxWorkers) a.inm[wk * kMaskWords + (j >> 5)] = bits;
       }
     }
     grid.sync();
     if (__ldcg(&a.ctl[10]) == 0) break;
-    for (int64_t q = gtid; q < static_cast<int64_t>(a.n) * kMaskWords; q += gthreads) a.vm[q] = 0;
+    for (int64_t q = gtid; q < static_cast<int64_t>(kMaxWorkers) * a.vwords; q += gthreads) a.vm[q] = 0;
     grid.sync();
     if (gtid == 0) a.ctl[10] = 0, a.ctl[9] = 1, a.ctl[1] = min(nc, static_cast<int32_t>(gridDim.x));
     grid.sync();
@@ -564,7 +570,7 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
       for (int32_t q = static_cast<int32_t>(gtid); q < ne; q += static_cast<int32_t>(gthreads)) {
         const uint64_t e = __ldcg(&a.glist[q]);
         const int32_t j = static_cast<int32_t>(e >> 32), w = static_cast<int32_t>(static_cast<uint32_t>(e));
-        a.vm[static_cast<int64_t>(w) * kMaskWords + (j >> 5)] = 0;  // every region is finished: clear its bits
+        a.vm[static_cast<int64_t>(j) * a.vwords + (w >> 5)] = 0;  // every region is finished: clear its bits
         if (!s_acc[j]) continue;
         atomicMin(&a.dist[w], __ldcg(&a.dw[static_cast<int64_t>(j) * a.n + w]));
         const int32_t t = w >> a.tile_shift;
@@ -579,7 +585,7 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
       const int32_t* lstart = s_wlstart[sub];
       for (int32_t i = gt; i < rn; i += G) {
         const int32_t w = __ldcg(&my_reg[i]);
-        a.vm[static_cast<int64_t>(w) * kMaskWords + my_word] = 0;  // clear (every worker's region is finished)
+        a.vm[my_plane + (w >> 5)] = 0;  // clear (every worker's region is finished)
         if (!acc) continue;
         int32_t lo = 0, hi = nlev - 1;  // depth of entry i: last level starting at or before i
         while (lo < hi) {
@@ -916,7 +922,8 @@ void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32
   const int W = ctx.fps_workers;
   const int64_t wn = static_cast<int64_t>(W) * n;
   // visit bits: 32 bytes per vertex, shared by all regions (L2-resident at 1M)
-  uint32_t* vm = static_cast<uint32_t*>(ctx.slab(0, sizeof(uint32_t) * kMaskWords * static_cast<int64_t>(n)));
+  const int64_t vwords = (static_cast<int64_t>(n) + 31) / 32;  // one bit plane of n bits per worker
+  uint32_t* vm = static_cast<uint32_t*>(ctx.slab(0, sizeof(uint32_t) * kMaxWorkers * vwords));
   int32_t* dw = static_cast<int32_t*>(ctx.slab(1, sizeof(int32_t) * static_cast<int64_t>(grid_cands) * n));
   int32_t* reg = static_cast<int32_t*>(ctx.slab(2, sizeof(int32_t) * wn));
   uint64_t* glist = static_cast<uint64_t*>(ctx.slab(3, sizeof(uint64_t) * (static_cast<int64_t>(grid_cands) * n + 64)));
@@ -926,11 +933,11 @@ void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32
   DevBuf<int32_t> tscratch(ntile, s), bar(1, s), smax(n / 32 + 1, s);
   MP_CUDA(cudaMemsetAsync(bar, 0, sizeof(int32_t), s));
   MP_CUDA(cudaMemsetAsync(inm, 0, sizeof(uint32_t) * inm.n, s));
-  MP_CUDA(cudaMemsetAsync(vm, 0, sizeof(uint32_t) * kMaskWords * static_cast<int64_t>(n), s));
+  MP_CUDA(cudaMemsetAsync(vm, 0, sizeof(uint32_t) * kMaxWorkers * vwords, s));
   MP_CUDA(cudaMemsetAsync(tbits, 0, sizeof(uint32_t) * tbits.n, s));
   BatchArgs a{};
   a.g = g, a.ell = ell, a.n = n, a.k = k, a.tile_shift = tile_shift, a.ntile = ntile, a.seed = seed;
-  a.dist = dist, a.tkey = tkey, a.tbits = tbits, a.tlist = tlist, a.vm = vm, a.dw = dw, a.reg = reg;
+  a.dist = dist, a.tkey = tkey, a.tbits = tbits, a.tlist = tlist, a.vm = vm, a.vwords = vwords, a.dw = dw, a.reg = reg;
   a.cand = cand, a.ckey = ckey, a.mkey = mkey, a.inm = inm, a.regn = regn, a.ctl = ctl, a.seeds = seeds;
   a.work = ctx.dwork;
   a.glist = glist;
