@@ -190,21 +190,36 @@ __global__ void __launch_bounds__(kMdThreads) md_kernel(MdArgs a) {
       int32_t* wa = a.adj + o;
       int32_t c = 0;
       const int32_t na = a.nadj[w];
-      for (int32_t j = 0; j < na; ++j) {
-        const int32_t x = wa[j];
-        if (a.vmark[x] != tok) wa[c++] = x;
+      // in-place compaction with 8 reads in flight ahead of the writes
+      for (int32_t j0 = 0; j0 < na; j0 += 8) {
+        int32_t xs[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) xs[q] = j0 + q < na ? wa[j0 + q] : -1;
+        int32_t mk[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mk[q] = xs[q] >= 0 ? a.vmark[xs[q]] : tok;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (mk[q] != tok) wa[c++] = xs[q];
       }
       a.nadj[w] = c;
       int32_t* we = a.el + o;
       int32_t ce = 0;
       const int32_t ne = a.nel[w];
       int64_t d = c;
-      for (int32_t j = 0; j < ne; ++j) {
-        const int32_t e = we[j];
-        if (a.emark[e] != tok) {
-          we[ce++] = e;
-          d += a.bsz[e];
-        }
+      for (int32_t j0 = 0; j0 < ne; j0 += 8) {
+        int32_t es[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) es[q] = j0 + q < ne ? we[j0 + q] : -1;
+        int32_t mk[8], bs[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mk[q] = es[q] >= 0 ? a.emark[es[q]] : tok, bs[q] = es[q] >= 0 ? a.bsz[es[q]] : 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (mk[q] != tok) {
+            we[ce++] = es[q];
+            d += bs[q];
+          }
       }
       we[ce++] = p;
       d += nb;
@@ -397,19 +412,30 @@ __global__ void __launch_bounds__(kMdThreads) md_fast_kernel(MdArgs a) {
       int32_t* wa = a.adj + o;
       int32_t c = 0;
       const int32_t na = wst & 0xffff, ne = wst >> 16;
-      for (int32_t j = 0; j < na; ++j) {
-        const int32_t x = wa[j];
-        if (mark[x] != tok) wa[c++] = x;
+      // lists are compacted in place: read 8 entries ahead of the writes so the
+      // loads are in flight together (the compiler cannot reorder across the
+      // possibly-aliasing stores)
+      for (int32_t j0 = 0; j0 < na; j0 += 8) {
+        int32_t xs[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) xs[q] = j0 + q < na ? wa[j0 + q] : -1;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (xs[q] >= 0 && mark[xs[q]] != tok) wa[c++] = xs[q];
       }
       int32_t* we = a.el + o;
       int32_t ce = 0;
       int64_t d = c + nbd;
-      for (int32_t j = 0; j < ne; ++j) {
-        const int32_t e = we[j];
-        if (mark[e] != tok) {
-          we[ce++] = e;
-          d += bsz[e];
-        }
+      for (int32_t j0 = 0; j0 < ne; j0 += 8) {
+        int32_t es[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) es[q] = j0 + q < ne ? we[j0 + q] : -1;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (es[q] >= 0 && mark[es[q]] != tok) {
+            we[ce++] = es[q];
+            d += bsz[es[q]];
+          }
       }
       we[ce++] = p;
       st[w] = c | (ce << 16);
