@@ -548,6 +548,19 @@ def run_c3(args):
     gold = golden("c3")
     import hashlib
     sha = hashlib.sha256(perm.cpu().numpy().tobytes()).hexdigest()[:16]
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        # the reference on all 10M vertices takes ~15 min (FPS is O(k n)); bounded sample: 1000x1000 torus
+        threads = os.cpu_count() or 1
+        try:
+            gs = mp.mesh_to_graph(mp.make_torus_mesh(1000, 1000))
+            cms, cstage, _ = cpu_reference(gs, 1, 0, threads)
+            cpu = {"value": round(cms, 3), "unit": "ms", "cores": threads, "kind": "reference",
+                   "sample": f"one full torus 1000x1000 (n=1M) ordering, a bounded sample of c3 (stages 1-5), "
+                             f"order_tree_nodes threads={threads}",
+                   "stage_ms": {k: round(v, 2) for k, v in zip(["patch", "quotient", "etree", "local", "assemble"], cstage)}}
+        except Exception as e:  # reference .so missing on this box
+            cpu = {"value": None, "unit": "ms", "cores": None, "kind": "reference", "sample": f"unavailable: {e}"}
     if rank == 0:
         sizes = np.diff(node_off.cpu().numpy())
         line = {
@@ -564,6 +577,7 @@ def run_c3(args):
             "rank0_vertices_owned": int(sizes[own == 0].sum()),
             "parity": {"sha_perm": sha, "golden": gold.get("sha_perm") if gold else None,
                        "match": bool(gold and sha == gold["sha_perm"])},
+            "cpu_baseline": cpu,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
