@@ -595,7 +595,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS) + ["c4"])
     ap.add_argument("--c3-unsharded", action="store_true", help="c3 through mp_order (stats, fill) instead")
-    ap.add_argument("--c4-workers", type=int, default=8, help="concurrent contexts per GPU for c4")
+    ap.add_argument("--c4-workers", type=int, default=4, help="concurrent contexts per GPU for c4")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
     if args.impl == "reference":

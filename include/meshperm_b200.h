@@ -106,6 +106,12 @@ const char* mp_version(void);
  * pinned staging buffers, a stream and the timing events. */
 int mp_context_create(mp_context** ctx, int32_t device);
 void mp_context_destroy(mp_context* ctx);
+/* Number of contexts the caller runs concurrently on this device (default 1):
+ * the persistent grid-wide kernels (farthest-point seeding, Lloyd rounds)
+ * size their grids to 1/share of the SMs so that concurrent contexts overlap
+ * instead of queueing behind each other's whole-GPU launches.  Results do not
+ * depend on it. */
+int mp_context_set_sm_share(mp_context* ctx, int32_t share);
 /* cudaStream_t to run on; NULL restores the context's own stream. */
 int mp_context_set_stream(mp_context* ctx, void* stream);
 

@@ -32,7 +32,10 @@ class FramePool:
     def __init__(self, device: int = 0, workers: int = 4):
         from .api import Context
         self.device = device
+        from ._lib import check, lib
         self.ctx = [Context(device) for _ in range(workers)]
+        for c in self.ctx:  # concurrent contexts: grid-wide kernels take 1/workers of the SMs each
+            check(lib().mp_context_set_sm_share(c.handle, workers))
         self.free = list(range(workers))
         self.lock = threading.Lock()
         self.ex = cf.ThreadPoolExecutor(max_workers=workers)

@@ -231,6 +231,15 @@ void mp_context_destroy(mp_context* ctx) {
   delete ctx;
 }
 
+int mp_context_set_sm_share(mp_context* ctx, int32_t share) {
+  return guarded([&] {
+    if (!ctx) throw Error(MP_EINVAL, "null context");
+    if (share < 1) throw Error(MP_EINVAL, "share must be positive");
+    ctx->sm_share = share;
+    ctx->fps_workers = 0;  // re-decided on the next call
+  });
+}
+
 int mp_context_set_stream(mp_context* ctx, void* stream) {
   return guarded([&] {
     if (!ctx) throw Error(MP_EINVAL, "null context");

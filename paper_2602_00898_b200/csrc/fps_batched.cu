@@ -913,7 +913,7 @@ void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32
   // workers: one per SM, bounded by the bit-matrix width and by memory
   // (a 4-byte region list per vertex each); decided once per context
   if (ctx.fps_workers == 0) {
-    int W0 = std::min(ctx.num_sms, kMaxWorkers);
+    int W0 = std::min(std::max(ctx.num_sms / std::max(ctx.sm_share, 1), 4), kMaxWorkers);
     size_t free_b = 0, total_b = 0;
     MP_CUDA(cudaMemGetInfo(&free_b, &total_b));
     while (W0 > 1 && 4ull * n * W0 > free_b / 2) W0 /= 2;
@@ -925,7 +925,8 @@ void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32
   const int64_t vwords = (static_cast<int64_t>(n) + 31) / 32;  // one bit plane of n bits per worker
   uint32_t* vm = static_cast<uint32_t*>(ctx.slab(0, sizeof(uint32_t) * kMaxWorkers * vwords));
   int32_t* dw = static_cast<int32_t*>(ctx.slab(1, sizeof(int32_t) * static_cast<int64_t>(grid_cands) * n));
-  int32_t* reg = static_cast<int32_t*>(ctx.slab(2, sizeof(int32_t) * wn));
+  // region lists: one row of n per worker CTA, and per cluster CTA of fps_cluster_phase (up to 16)
+  int32_t* reg = static_cast<int32_t*>(ctx.slab(2, sizeof(int32_t) * std::max<int64_t>(W, 16) * n));
   uint64_t* glist = static_cast<uint64_t*>(ctx.slab(3, sizeof(uint64_t) * (static_cast<int64_t>(grid_cands) * n + 64)));
   DevBuf<int32_t> tlist(ntile, s), cand(kSCap, s), regn(kMaxWorkers, s), ctl(16, s);
   DevBuf<uint64_t> tkey(ntile, s), ckey(kSCap, s), mkey(kMaxWorkers, s);

@@ -37,6 +37,7 @@ struct mp_context {
   std::vector<std::pair<void*, size_t>> slabs;
   void* slab(int id, size_t bytes);
   int fps_workers = 0;  // worker CTAs of the batched FPS (decided once)
+  int sm_share = 1;     // contexts expected to run concurrently on the device (grid sizing)
 };
 
 namespace mp {

@@ -1165,7 +1165,7 @@ int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, ui
     la.work = ctx.dwork;
     int bpsm = 0;
     MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, lloyd_kernel, 256, 0));
-    int blocks = std::max(1, std::min(bpsm, 4)) * ctx.num_sms;
+    int blocks = std::max(1, std::min(bpsm, 4)) * std::max(ctx.num_sms / std::max(ctx.sm_share, 1), 1);
     void* args[] = {&la};
     { const int kt__ = ctx.ktime_begin(kKLloyd); MP_KERNEL(ctx, MP_CUDA(cudaLaunchCooperativeKernel((void*)lloyd_kernel, blocks, 256, args, 0, s))); ctx.ktime_end(kt__); }
     MP_KERNEL(ctx, lloyd_finish<<<grid_for(ctx, n), 256, 0, s>>>(n, comp_of.get(), comp_mode, prev, assignment));
