@@ -412,3 +412,18 @@ def test_separation_check_agrees_with_cross_block_fill(seed):
         perm = mp.compute_perm(broken, g).perm
         cbf = R.cross_block_fill(g, perm, 3, new_off, nv)
         assert (viol > 0) == (cbf > 0)
+
+
+@pytest.mark.parametrize("share", [16, 3])
+def test_sm_share_does_not_change_results(share):
+    """mp_context_set_sm_share (concurrent frame contexts) shrinks the grid-wide
+    FPS / Lloyd kernels; results must stay the reference's (ico158 digests)."""
+    from paper_2602_00898_b200._lib import check, lib
+    gold = json.loads((GOLDEN / "bench_golden.json").read_text())["ico158"]
+    ctx = mp.Context(0)
+    check(lib().mp_context_set_sm_share(ctx.handle, share))
+    g = mp.mesh_to_graph(mp.make_icosphere_mesh(158))
+    res = mp.order(g, ctx=ctx)
+    assert res.patch.patch_count == gold["patch_count"]
+    assert digest(res.perm.perm) == gold["sha_perm"]
+    assert res.fill.nnz_L == gold["nnz_L"]
