@@ -458,6 +458,27 @@ __device__ __forceinline__ void chunked_level(int64_t items, int32_t* gcount, in
   }
 }
 
+// Small levels (few items): grid-stride over items with one warp-aggregated
+// global append per warp -- cheaper than chunked_level's three barriers when
+// only a handful of CTAs have work.
+constexpr int64_t kChunkMinItems = 65536;
+template <class F>
+__device__ __forceinline__ void warp_level(int64_t items, int32_t* gcount, int32_t* next, F&& item) {
+  const int lane = threadIdx.x & 31;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t base = tid - lane; base < items; base += nthreads) {
+    int32_t pw = -1;  // the ELL item's push; CSR-tail extras go straight out
+    item(base + lane, [&](int32_t w) {
+      if (pw < 0) pw = w;
+      else next[atomicAdd(gcount, 1)] = w;
+    });
+    const bool push = pw >= 0;
+    const int32_t slot = warp_append(gcount, push);
+    if (push) next[slot] = pw;
+  }
+}
+
 __global__ void lloyd_kernel(LloydArgs a) {
   cg::grid_group grid = cg::this_grid();
   __shared__ int32_t s_lbuf[kLvlBuf], s_lsh[2];
@@ -501,7 +522,7 @@ __global__ void lloyd_kernel(LloydArgs a) {
           if (dw == d + 1) atomicMin(&a.label[w], lu);
           return fresh;
         };
-        chunked_level(items, &a.counters[cout], next, s_lbuf, s_lsh, [&](int64_t it, auto&& push) {
+        auto body = [&](int64_t it, auto&& push) {
           if (it >= items) return;
           const int32_t u = front[it >> 3];
           const int32_t x = a.ell[static_cast<int64_t>(u) * 8 + (it & 7)];
@@ -514,7 +535,9 @@ __global__ void lloyd_kernel(LloydArgs a) {
               if (visit(w, lu)) push(w);
             }
           }
-        });
+        };
+        if (items >= kChunkMinItems) chunked_level(items, &a.counters[cout], next, s_lbuf, s_lsh, body);
+        else warp_level(items, &a.counters[cout], next, body);
         grid.sync();
         if (tid == 0 && a.work) atomicAdd(&a.work[3], 1ull);
         int32_t* t = front;
@@ -569,7 +592,7 @@ __global__ void lloyd_kernel(LloydArgs a) {
           if (__ldcg(&a.label[w]) != lu || __ldcg(&a.dist[w]) != kUnreached) return false;
           return atomicCAS(&a.dist[w], kUnreached, d + 1) == kUnreached;
         };
-        chunked_level(items, &a.counters[cout], next, s_lbuf, s_lsh, [&](int64_t it, auto&& push) {
+        auto body = [&](int64_t it, auto&& push) {
           if (it >= items) return;
           const int32_t u = front[it >> 3];
           const int32_t x = a.ell[static_cast<int64_t>(u) * 8 + (it & 7)];
@@ -582,7 +605,9 @@ __global__ void lloyd_kernel(LloydArgs a) {
               if (visit(w, lu)) push(w);
             }
           }
-        });
+        };
+        if (items >= kChunkMinItems) chunked_level(items, &a.counters[cout], next, s_lbuf, s_lsh, body);
+        else warp_level(items, &a.counters[cout], next, body);
         grid.sync();
         int32_t* t = front;
         front = next;
