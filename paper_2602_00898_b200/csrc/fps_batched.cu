@@ -23,6 +23,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <mutex>
 #include <cstdlib>
 
 #include "mp_context.h"
@@ -955,33 +956,43 @@ void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32
   // the cluster kernel's dynamic smem: the select scratch, or 256 staged items per warp
   const size_t cl_smem = std::max(smem, sizeof(uint64_t) * 256 * (kThreads / 32));
   a.qcap = 8LL * n + 1024;  // uint64 items
+  if (const char* qc = getenv("MP_FPS_QCAP")) a.qcap = std::max<int64_t>(64, std::min<int64_t>(a.qcap, atoll(qc)));  // test knob
   a.queue = static_cast<int32_t*>(ctx.slab(4, sizeof(uint64_t) * a.qcap));
   DevBuf<int32_t> qctl(96, s);
   a.qctl = qctl;
   MP_CUDA(cudaMemsetAsync(a.queue, 0xff, sizeof(uint64_t) * a.qcap, s));
   MP_CUDA(cudaMemsetAsync(qctl, 0, sizeof(int32_t) * 96, s));
   if (!getenv("MP_FPS_NO_CLUSTER")) {
-    static int cluster_ctas = -1;  // decided once per process
-    if (cluster_ctas < 0) {
-      cluster_ctas = 0;
-      allow_max_smem(fps_cluster_phase, ctx.device);
-      cudaFuncSetAttribute(fps_cluster_phase, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      const char* ce = getenv("MP_FPS_CLUSTER");  // tuning knob: cluster size to try first
-      const int first = ce ? atoi(ce) : 16;
-      for (int cs : {first, 16, 8}) {
-        if (cs < 1 || cs > 16) continue;
-        cudaLaunchConfig_t cfg{};
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = cs, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
-        cfg.gridDim = dim3(cs), cfg.blockDim = dim3(kThreads), cfg.dynamicSmemBytes = cl_smem;
-        cfg.attrs = at, cfg.numAttrs = 1;
-        int ncl = 0;
-        if (cudaOccupancyMaxActiveClusters(&ncl, fps_cluster_phase, &cfg) == cudaSuccess && ncl > 0) {
-          cluster_ctas = cs;
-          break;
+    // cluster size: 16 CTAs (non-portable) where the device allows, else 8;
+    // probed once per process (MP_FPS_CLUSTER overrides and is re-read)
+    static std::mutex mu;
+    static int cached = -1;
+    const char* ce = getenv("MP_FPS_CLUSTER");
+    int cluster_ctas = 0;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      if (ce || cached < 0) {
+        allow_max_smem(fps_cluster_phase, ctx.device);
+        cudaFuncSetAttribute(fps_cluster_phase, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        const int first = ce ? atoi(ce) : 16;
+        for (int cs : {first, 16, 8}) {
+          if (cs < 1 || cs > 16) continue;
+          cudaLaunchConfig_t cfg{};
+          cudaLaunchAttribute at[1];
+          at[0].id = cudaLaunchAttributeClusterDimension;
+          at[0].val.clusterDim.x = cs, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
+          cfg.gridDim = dim3(cs), cfg.blockDim = dim3(kThreads), cfg.dynamicSmemBytes = cl_smem;
+          cfg.attrs = at, cfg.numAttrs = 1;
+          int ncl = 0;
+          if (cudaOccupancyMaxActiveClusters(&ncl, fps_cluster_phase, &cfg) == cudaSuccess && ncl > 0) {
+            cluster_ctas = cs;
+            break;
+          }
+          cudaGetLastError();
         }
-        cudaGetLastError();
+        if (!ce) cached = cluster_ctas;
+      } else {
+        cluster_ctas = cached;
       }
     }
     if (cluster_ctas > 0) {
