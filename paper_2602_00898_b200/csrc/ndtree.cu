@@ -546,6 +546,7 @@ __device__ __forceinline__ void fm_node(const LevelArgs& a, int32_t li, int32_t 
         K ck0 = cp0 >= 0 ? FmKey<K>::make(gain[cp0], cp0) : K(0);
         K ck1 = cp1 >= 0 ? FmKey<K>::make(gain[cp1], cp1) : K(0);
         int32_t cw0 = cp0 >= 0 ? w[cp0] : 0, cw1 = cp1 >= 0 ? w[cp1] : 0;
+        __syncwarp();  // every lane has read the shared state before lane 0 rewrites it
         uint32_t refilled = static_cast<uint32_t>(need & 3);
         // one move: lock ch, flip it, update the neighbours' gains and the caches
         auto apply = [&](K kbest, int32_t sd) {
@@ -1143,6 +1144,7 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
           const int64_t ro = o2 ? nrw1 : nrw0, rp = o2 ? nrw0 : nrw1;
           s_ni[o2][pull] = imbalance_of(ro + 1, rp - pull);
         }
+        __syncwarp();  // every lane has read s_rw / s_size
         if (lane == 0) {
           s_rw[0] = nrw0, s_rw[1] = nrw1;
           s_size = s_size - 1 + np;
