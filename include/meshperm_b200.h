@@ -198,6 +198,20 @@ int mp_tree_separation_check(mp_context* ctx, const mp_csr* g, int32_t nd_level,
 int mp_mesh_to_graph_device(mp_context* ctx, int32_t nv, int64_t ntri, const int32_t* tris,
                             int32_t tris_on_device, int32_t* off, int32_t* nbr, int32_t out_on_device,
                             int64_t* nnz);
+/* the matrix input path on the device.  A SparsePattern
+ * {n, entries (rows[k], cols[k])} becomes the ordering graph: build_graph
+ * (graph.hpp:48, graph.cpp:53-61) for block_size 1, compress_blocks
+ * (graph.hpp:59, graph.cpp:77-94) for block_size > 1 (n / block_size nodes,
+ * an edge between blocks joined by any entry).  Array placement and the
+ * nbr == NULL count-only call as in mp_mesh_to_graph_device; MP_EINVAL with
+ * the reference's messages ("pattern entry out of range", "matrix size N is
+ * not a multiple of block size B", "block size must be positive"). */
+int mp_pattern_to_graph_device(mp_context* ctx, int32_t n, int64_t nnz, const int32_t* rows,
+                               const int32_t* cols, int32_t in_on_device, int32_t block_size,
+                               int32_t* off, int32_t* nbr, int32_t out_on_device, int64_t* nnz_out);
+/* graph.hpp:62 lift_patches: out[v * b + t] = assignment[v] (n * b entries). */
+int mp_lift_patches(mp_context* ctx, int32_t n, const int32_t* assignment, int32_t block_size,
+                    int32_t* out, int32_t on_device);
 /* graph.hpp:56 mesh_to_graph on the host (input generation); nbr NULL = count only */
 int mp_mesh_to_graph(int32_t nv, int64_t ntri, const int32_t* tris, int32_t* off, int32_t* nbr,
                      int64_t* nnz);

@@ -190,6 +190,20 @@ class Reference(_Base):
                                              C.byref(nnz)))
         return off, nbr
 
+    def pattern_to_graph(self, n, rows, cols, block_size=1):
+        """graph.cpp:53-61 build_graph / :77-94 compress_blocks."""
+        rows, cols = _i32(rows), _i32(cols)
+        nodes = n // block_size if block_size > 0 else 0
+        off = np.zeros(nodes + 1, np.int32)
+        nnz = C.c_int64()
+        f = self._f("pattern_to_graph")
+        self._check(f(C.c_int32(n), C.c_int64(len(rows)), _p(rows), _p(cols), C.c_int32(block_size), _p(off), None,
+                      C.byref(nnz)))
+        nbr = np.zeros(nnz.value, np.int32)
+        self._check(f(C.c_int32(n), C.c_int64(len(rows)), _p(rows), _p(cols), C.c_int32(block_size), _p(off),
+                      _p(nbr), C.byref(nnz)))
+        return off, nbr
+
     def cross_block_fill(self, g, perm, nd_level, node_offsets, node_vertices):
         """symbolic.cpp:98-119 (the pipeline self-check, pipeline.cpp:141)."""
         c = C.c_int64()

@@ -116,6 +116,23 @@ int ref_mesh_to_graph(int32_t nv, int64_t ntri, const int32_t* tris, int32_t* of
   });
 }
 
+// graph.cpp:53-61 build_graph (block_size 1) / graph.cpp:77-94 compress_blocks
+// (block_size > 1) of a SparsePattern{n, entries (rows[k], cols[k])}.
+// Two-call like ref_mesh_to_graph; off_out holds n / block_size + 1 ints.
+int ref_pattern_to_graph(int32_t n, int64_t nnz, const int32_t* rows, const int32_t* cols, int32_t block_size,
+                         int32_t* off_out, int32_t* nbr_out, int64_t* nnz_out) {
+  return guarded([&] {
+    SparsePattern pattern;
+    pattern.n = n;
+    pattern.entries.resize(nnz);
+    for (int64_t k = 0; k < nnz; ++k) pattern.entries[k] = {rows[k], cols[k]};
+    AdjacencyGraph g = block_size == 1 ? build_graph(pattern) : compress_blocks(pattern, block_size);
+    *nnz_out = static_cast<int64_t>(g.neighbors.size());
+    if (off_out) std::memcpy(off_out, g.offsets.data(), sizeof(int32_t) * (g.n + 1));
+    if (nbr_out) std::memcpy(nbr_out, g.neighbors.data(), sizeof(int32_t) * g.neighbors.size());
+  });
+}
+
 // pipeline.cpp:38-55 make_grid_mesh.  tris_out holds 2*(r-1)*(c-1)*3 ints.
 int ref_make_grid_mesh(int32_t rows, int32_t cols, int32_t* tris_out) {
   return guarded([&] {

@@ -9,5 +9,6 @@ from .api import (  # noqa: F401
     AdjacencyGraph, Context, EliminationTree, FillReport, PatchPartition, Permutation, PipelineResult,
     QuotientGraph, TriangleMesh, build_etree, build_quotient, compute_patches, compute_perm, default_context,
     default_nd_level, enforce_connectivity, make_grid_mesh, make_icosphere_mesh, make_random_mesh,
-    make_torus_mesh, mesh_to_graph, mesh_to_graph_device, order, order_device, order_subtrees, order_tree_nodes, tree_fill, tree_separation_violations,
+    make_torus_mesh, mesh_to_graph, mesh_to_graph_device, pattern_to_graph_device, lift_patches, run_baseline,
+    BASELINES, order, order_device, order_subtrees, order_tree_nodes, tree_fill, tree_separation_violations,
 )

@@ -201,6 +201,51 @@ def mesh_to_graph_device(mesh: TriangleMesh, ctx: Context | None = None) -> Adja
     return AdjacencyGraph(n, off, nbr)
 
 
+def pattern_to_graph_device(n: int, rows, cols, block_size: int = 1, ctx: Context | None = None) -> AdjacencyGraph:
+    """graph.hpp:48 build_graph (block_size 1) / graph.hpp:59 compress_blocks on
+    the GPU: a SparsePattern's entries -> the ordering graph."""
+    ctx = ctx or default_context()
+    rows, cols = _i32(rows), _i32(cols)
+    if len(rows) != len(cols):
+        raise ValueError("rows and cols differ in length")
+    nodes = n // block_size if block_size > 0 and n >= 0 and n % block_size == 0 else 0
+    off = np.zeros(nodes + 1, np.int32)
+    nnz = C.c_int64()
+    f = lib().mp_pattern_to_graph_device
+    check(f(ctx.handle, n, len(rows), _ptr(rows), _ptr(cols), 0, block_size, _ptr(off), C.c_void_p(0), 0, C.byref(nnz)))
+    nbr = np.zeros(nnz.value, np.int32)
+    check(f(ctx.handle, n, len(rows), _ptr(rows), _ptr(cols), 0, block_size, _ptr(off), _ptr(nbr), 0, C.byref(nnz)))
+    return AdjacencyGraph(nodes, off, nbr)
+
+
+def lift_patches(partition: PatchPartition, block_size: int, ctx: Context | None = None) -> PatchPartition:
+    """graph.hpp:62 lift_patches: every block row inherits its node's patch."""
+    ctx = ctx or default_context()
+    a = _i32(partition.assignment)
+    out = np.zeros(max(len(a) * block_size, 1), np.int32)
+    check(lib().mp_lift_patches(ctx.handle, len(a), _ptr(a), block_size, _ptr(out), 0))
+    return PatchPartition(out[:len(a) * block_size], partition.patch_count)
+
+
+# run_baselines (pipeline.cpp:162-186): the comparison orderings as configs of
+# the same path.
+BASELINES = {
+    "natural": dict(nd_level=0, local_mode="natural"),
+    "md": dict(nd_level=0, local_mode="approx_md"),
+    "nd-vertex": dict(patch_size=1),
+}
+
+
+def run_baseline(g: AdjacencyGraph, name: str, ctx: Context | None = None, **kw) -> PipelineResult:
+    """One run_baselines row: `natural` (identity order), `md` (approximate
+    minimum degree on the whole graph) or `nd-vertex` (patch size 1)."""
+    if name not in BASELINES:
+        raise ValueError("unknown baseline: " + name)
+    cfg = dict(kw)
+    cfg.update(BASELINES[name])
+    return order(g, ctx=ctx, **cfg)
+
+
 def mesh_to_graph_device_ptr(ctx: Context, nv: int, ntri: int, tris_ptr: int, off_ptr: int, nbr_ptr: int) -> int:
     """Device-pointer form (tris, off, nbr all device memory; nbr capacity
     >= 6 * ntri or the nnz of an earlier call).  Returns nnz."""

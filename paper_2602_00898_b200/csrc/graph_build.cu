@@ -54,6 +54,35 @@ __global__ void tri_scatter(int64_t ntri, int32_t nv, const int32_t* __restrict_
   }
 }
 
+// SparsePattern entries (rows[k], cols[k]) -> edges between blocks
+// (i / b, j / b), diagonal blocks dropped: build_graph (b = 1, graph.cpp:53-61)
+// and compress_blocks (graph.cpp:77-94).  The first out-of-range entry wins.
+__global__ void pair_count(int64_t nnz, int32_t n, int32_t b, const int32_t* __restrict__ rows,
+                           const int32_t* __restrict__ cols, int32_t* cnt, unsigned long long* bad) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < nnz;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t i = __ldg(&rows[k]), j = __ldg(&cols[k]);
+    if (i < 0 || i >= n || j < 0 || j >= n) {
+      atomicMin(bad, static_cast<unsigned long long>(k));
+      continue;
+    }
+    const int32_t u = i / b, v = j / b;
+    if (u != v) atomicAdd(&cnt[u], 1), atomicAdd(&cnt[v], 1);
+  }
+}
+__global__ void pair_scatter(int64_t nnz, int32_t n, int32_t b, const int32_t* __restrict__ rows,
+                             const int32_t* __restrict__ cols, int32_t* cur, int32_t* raw) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < nnz;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t i = __ldg(&rows[k]), j = __ldg(&cols[k]);
+    if (i < 0 || i >= n || j < 0 || j >= n) continue;
+    const int32_t u = i / b, v = j / b;
+    if (u == v) continue;
+    raw[atomicAdd(&cur[u], 1)] = v;
+    raw[atomicAdd(&cur[v], 1)] = u;
+  }
+}
+
 // Sort + dedup each raw list in place; deg[v] = unique length.  Long lists are
 // left for list_sort_long (appended to `longv`, counted in longv[-1]).
 __global__ void __launch_bounds__(kSortThreads) list_sort(int32_t nv, const int32_t* ro, int32_t* raw, int32_t* deg,
@@ -127,40 +156,24 @@ __global__ void list_copy(int32_t nv, const int32_t* ro, const int32_t* raw, con
 // is non-null, else into *alloc (sized here) when that is non-null, else
 // offsets only.  Returns nnz = 2|E|.  Throws MP_EINVAL with the reference's
 // messages.
-int64_t mesh_to_graph_dev(mp_context& ctx, int32_t nv, int64_t ntri, const int32_t* tris, int32_t* off,
-                          int32_t* nbr, DevBuf<int32_t>* alloc) {
+// Shared back half: raw lists (counted in cnt, appended by scatter(cursors,
+// raw)) -> sorted, deduplicated CSR.  check_bad(verdict) throws for invalid
+// input after the one host synchronisation.
+template <class Count, class Scatter, class Check>
+int64_t csr_from_raw(mp_context& ctx, int32_t nv, int64_t nraw, int32_t* off, int32_t* nbr, DevBuf<int32_t>* alloc,
+                     Count count, Scatter scatter, unsigned long long* bad, Check check_bad) {
   cudaStream_t s = ctx.stream;
-  if (nv < 0) throw Error(MP_EINVAL, "negative vertex count");
-  const int64_t nraw = 6 * ntri;
-  if (nraw > 0x7fffffffLL) throw Error(MP_EINVAL, "mesh too large for int32 offsets");
-  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(std::max<int64_t>(ntri, nv), 256),
-                                                                          ctx.num_sms * 16LL)));
+  if (nraw > 0x7fffffffLL) throw Error(MP_EINVAL, "input too large for int32 offsets");
   DevBuf<int32_t> cnt(static_cast<size_t>(nv) + 1, s), ro(static_cast<size_t>(nv) + 1, s), raw(std::max<int64_t>(nraw, 1), s);
-  DevBuf<unsigned long long> bad(1, s);
   MP_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nv + 1), s));
   MP_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s));
-  if (ntri > 0) MP_KERNEL(ctx, tri_count<<<grid, 256, 0, s>>>(ntri, nv, tris, cnt, bad));
-  // (bad triangles are skipped by the scatter; the verdict is read with nnz)
-  auto check_bad = [&](unsigned long long hbad) {
-  if (hbad != ~0ull) {  // validate_mesh's message for the first bad triangle (types.cpp:20-33)
-    const int64_t t = static_cast<int64_t>(hbad >> 1);
-    int32_t c[3];
-    MP_CUDA(cudaMemcpy(c, tris + 3 * t, sizeof c, cudaMemcpyDeviceToHost));
-    if (!(hbad & 1ull)) {
-      for (int k = 0; k < 3; ++k)
-        if (c[k] < 0 || c[k] >= nv)
-          throw Error(MP_EINVAL, "triangle " + std::to_string(t) + " references vertex " + std::to_string(c[k]) +
-                                     " outside [0, " + std::to_string(nv) + ")");
-    }
-    throw Error(MP_EINVAL, "triangle " + std::to_string(t) + " has repeated corners");
-  }
-  };
+  count(cnt.get());
   size_t tmp = 0;
   MP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt.get(), ro.get(), nv + 1, s));
   DevBuf<char> t1(tmp, s);
   MP_CUDA(cub::DeviceScan::ExclusiveSum(t1.get(), tmp, cnt.get(), ro.get(), nv + 1, s));
   MP_CUDA(cudaMemcpyAsync(cnt.get(), ro.get(), sizeof(int32_t) * nv, cudaMemcpyDeviceToDevice, s));  // cursors
-  if (ntri > 0) MP_KERNEL(ctx, tri_scatter<<<grid, 256, 0, s>>>(ntri, nv, tris, cnt, raw));
+  scatter(cnt.get(), raw.get());
   DevBuf<int32_t> deg(static_cast<size_t>(nv) + 1, s), longv(static_cast<size_t>(nv) + 1, s);
   MP_CUDA(cudaMemsetAsync(deg.get() + nv, 0, sizeof(int32_t), s));
   MP_CUDA(cudaMemsetAsync(longv.get() + nv, 0, sizeof(int32_t), s));  // long-list count
@@ -175,7 +188,7 @@ int64_t mesh_to_graph_dev(mp_context& ctx, int32_t nv, int64_t ntri, const int32
   int32_t nnz = 0;
   unsigned long long hbad = 0;
   MP_CUDA(cudaMemcpyAsync(&nnz, off + nv, sizeof nnz, cudaMemcpyDeviceToHost, s));
-  MP_CUDA(cudaMemcpyAsync(&hbad, bad.get(), sizeof hbad, cudaMemcpyDeviceToHost, s));
+  MP_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost, s));
   if (!nbr && alloc) {
     MP_CUDA(cudaStreamSynchronize(s));
     check_bad(hbad);
@@ -190,6 +203,67 @@ int64_t mesh_to_graph_dev(mp_context& ctx, int32_t nv, int64_t ntri, const int32
   MP_CUDA(cudaStreamSynchronize(s));
   check_bad(hbad);
   return nnz;
+}
+
+int grid_for_items(const mp_context& ctx, int64_t items) {
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, 256), ctx.num_sms * 16LL)));
+}
+
+// Builds off (nv + 1) and the neighbours (device pointers): into nbr when it
+// is non-null, else into *alloc (sized here) when that is non-null, else
+// offsets only.  Returns nnz = 2|E|.  Throws MP_EINVAL with the reference's
+// messages.
+int64_t mesh_to_graph_dev(mp_context& ctx, int32_t nv, int64_t ntri, const int32_t* tris, int32_t* off,
+                          int32_t* nbr, DevBuf<int32_t>* alloc) {
+  cudaStream_t s = ctx.stream;
+  if (nv < 0) throw Error(MP_EINVAL, "negative vertex count");
+  const int grid = grid_for_items(ctx, std::max<int64_t>(ntri, nv));
+  DevBuf<unsigned long long> bad(1, s);
+  return csr_from_raw(
+      ctx, nv, 6 * ntri, off, nbr, alloc,
+      [&](int32_t* cnt) { if (ntri > 0) MP_KERNEL(ctx, tri_count<<<grid, 256, 0, s>>>(ntri, nv, tris, cnt, bad)); },
+      [&](int32_t* cur, int32_t* raw) { if (ntri > 0) MP_KERNEL(ctx, tri_scatter<<<grid, 256, 0, s>>>(ntri, nv, tris, cur, raw)); },
+      bad.get(),
+      [&](unsigned long long hbad) {  // validate_mesh's message for the first bad triangle (types.cpp:20-33)
+        if (hbad == ~0ull) return;
+        const int64_t t = static_cast<int64_t>(hbad >> 1);
+        int32_t c[3];
+        MP_CUDA(cudaMemcpy(c, tris + 3 * t, sizeof c, cudaMemcpyDeviceToHost));
+        if (!(hbad & 1ull)) {
+          for (int k = 0; k < 3; ++k)
+            if (c[k] < 0 || c[k] >= nv)
+              throw Error(MP_EINVAL, "triangle " + std::to_string(t) + " references vertex " + std::to_string(c[k]) +
+                                         " outside [0, " + std::to_string(nv) + ")");
+        }
+        throw Error(MP_EINVAL, "triangle " + std::to_string(t) + " has repeated corners");
+      });
+}
+
+// build_graph (b = 1) / compress_blocks (b > 1) of a SparsePattern on the device.
+int64_t pattern_to_graph_dev(mp_context& ctx, int32_t n, int64_t nnz, const int32_t* rows, const int32_t* cols,
+                             int32_t b, int32_t* off, int32_t* nbr, DevBuf<int32_t>* alloc) {
+  cudaStream_t s = ctx.stream;
+  if (b < 1) throw Error(MP_EINVAL, "block size must be positive");
+  if (n < 0) throw Error(MP_EINVAL, "negative matrix size");
+  if (n % b != 0)
+    throw Error(MP_EINVAL, "matrix size " + std::to_string(n) + " is not a multiple of block size " + std::to_string(b));
+  const int32_t nodes = n / b;
+  const int grid = grid_for_items(ctx, std::max<int64_t>(nnz, nodes));
+  DevBuf<unsigned long long> bad(1, s);
+  return csr_from_raw(
+      ctx, nodes, 2 * nnz, off, nbr, alloc,
+      [&](int32_t* cnt) { if (nnz > 0) MP_KERNEL(ctx, pair_count<<<grid, 256, 0, s>>>(nnz, n, b, rows, cols, cnt, bad)); },
+      [&](int32_t* cur, int32_t* raw) { if (nnz > 0) MP_KERNEL(ctx, pair_scatter<<<grid, 256, 0, s>>>(nnz, n, b, rows, cols, cur, raw)); },
+      bad.get(),
+      [&](unsigned long long hbad) {
+        if (hbad != ~0ull) throw Error(MP_EINVAL, "pattern entry out of range");
+      });
+}
+
+__global__ void lift_kernel(int64_t n, int32_t b, const int32_t* in, int32_t* out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n * b;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = in[i / b];
 }
 
 }  // namespace mp
@@ -230,3 +304,63 @@ extern "C" int mp_mesh_to_graph_device(mp_context* ctx, int32_t nv, int64_t ntri
     if (prev != ctx->device) cudaSetDevice(prev);
   });
 }
+
+extern "C" int mp_pattern_to_graph_device(mp_context* ctx, int32_t n, int64_t nnz, const int32_t* rows,
+                                         const int32_t* cols, int32_t in_on_device, int32_t block_size, int32_t* off,
+                                         int32_t* nbr, int32_t out_on_device, int64_t* nnz_out) {
+  return guarded([&] {
+    if (!ctx || (nnz > 0 && (!rows || !cols)) || !off) throw Error(MP_EINVAL, "null argument");
+    if (nnz < 0) throw Error(MP_EINVAL, "negative entry count");
+    if (block_size < 1) throw Error(MP_EINVAL, "block size must be positive");
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != ctx->device) cudaSetDevice(ctx->device);
+    cudaStream_t s = ctx->stream;
+    DevBuf<int32_t> dr, dc, doff, dnbr;
+    const int32_t *r = rows, *c = cols;
+    if (!in_on_device && nnz > 0) {
+      dr.alloc(nnz, s), dc.alloc(nnz, s);
+      MP_CUDA(cudaMemcpyAsync(dr.get(), rows, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s));
+      MP_CUDA(cudaMemcpyAsync(dc.get(), cols, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s));
+      r = dr.get(), c = dc.get();
+    }
+    const int32_t nodes = n >= 0 && n % block_size == 0 ? n / block_size : 0;
+    int32_t* o = off;
+    if (!out_on_device) {
+      doff.alloc(static_cast<size_t>(nodes) + 1, s);
+      o = doff.get();
+    }
+    const bool want = nbr != nullptr;
+    const int64_t m = pattern_to_graph_dev(*ctx, n, nnz, r, c, block_size, o, out_on_device ? nbr : nullptr,
+                                           (!out_on_device && want) ? &dnbr : nullptr);
+    if (!out_on_device) {
+      MP_CUDA(cudaMemcpyAsync(off, o, sizeof(int32_t) * (static_cast<size_t>(nodes) + 1), cudaMemcpyDeviceToHost, s));
+      if (want && m > 0) MP_CUDA(cudaMemcpyAsync(nbr, dnbr.get(), sizeof(int32_t) * m, cudaMemcpyDeviceToHost, s));
+      MP_CUDA(cudaStreamSynchronize(s));
+    }
+    if (nnz_out) *nnz_out = m;
+    if (prev != ctx->device) cudaSetDevice(prev);
+  });
+}
+
+extern "C" int mp_lift_patches(mp_context* ctx, int32_t n, const int32_t* assignment, int32_t block_size,
+                               int32_t* out, int32_t on_device) {
+  return guarded([&] {
+    if (!ctx || (n > 0 && (!assignment || !out))) throw Error(MP_EINVAL, "null argument");
+    if (block_size < 1) throw Error(MP_EINVAL, "block size must be positive");
+    if (!on_device) {  // host arrays: nothing to gain from a device round trip
+      for (int64_t v = 0; v < n; ++v)
+        for (int32_t t = 0; t < block_size; ++t) out[v * block_size + t] = assignment[v];
+      return;
+    }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != ctx->device) cudaSetDevice(ctx->device);
+    if (n > 0)
+      MP_KERNEL(*ctx, lift_kernel<<<grid_for_items(*ctx, static_cast<int64_t>(n) * block_size), 256, 0, ctx->stream>>>(
+                          n, block_size, assignment, out));
+    MP_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (prev != ctx->device) cudaSetDevice(prev);
+  });
+}
+

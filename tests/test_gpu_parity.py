@@ -443,3 +443,64 @@ def test_fps_fallbacks_match_reference(env, monkeypatch):
     assert res.patch.patch_count == gold["patch_count"]
     assert digest(res.patch.assignment) == gold["sha_assignment"]
     assert digest(res.perm.perm) == gold["sha_perm"]
+
+
+# ---------------------------------------------------------------- §8 f4: matrix input path, baselines
+def _pattern_of(g, b=1):
+    """Entries of the b-expanded pattern of g (both triangles, the diagonal included)."""
+    rows, cols = [], []
+    for u in range(g.n):
+        for v in list(g.neighbors_of(u)) + [u]:
+            for s in range(b):
+                for t in range(b):
+                    rows.append(u * b + s), cols.append(v * b + t)
+    return np.array(rows, np.int32), np.array(cols, np.int32)
+
+
+@pytest.mark.parametrize("b", [1, 2, 3])
+def test_pattern_to_graph_matches_reference(b):
+    from oracle.oracle import Reference
+    R = Reference()
+    g = mp.mesh_to_graph(mp.make_random_mesh(13, 17, 5))
+    rows, cols = _pattern_of(g, b)
+    rng = np.random.default_rng(b)
+    perm = rng.permutation(len(rows))  # entry order must not matter
+    rows, cols = rows[perm], cols[perm]
+    off, nbr = R.pattern_to_graph(g.n * b, rows, cols, b)
+    d = mp.pattern_to_graph_device(g.n * b, rows, cols, b)
+    assert np.array_equal(d.offsets, off) and np.array_equal(d.neighbors, nbr)
+    if b > 1:  # compressing the expanded pattern gives the mesh graph back
+        assert np.array_equal(d.offsets, g.offsets) and np.array_equal(d.neighbors, g.neighbors)
+    # unsymmetric entries and duplicates (build_graph symmetrises, dedups)
+    rr = rng.integers(0, g.n * b, 500).astype(np.int32)
+    cc = rng.integers(0, g.n * b, 500).astype(np.int32)
+    off, nbr = R.pattern_to_graph(g.n * b, rr, cc, b)
+    d = mp.pattern_to_graph_device(g.n * b, rr, cc, b)
+    assert np.array_equal(d.offsets, off) and np.array_equal(d.neighbors, nbr)
+
+
+def test_pattern_to_graph_errors_and_lift():
+    with pytest.raises(ValueError, match="matrix size 5 is not a multiple of block size 2"):
+        mp.pattern_to_graph_device(5, [0], [1], 2)
+    with pytest.raises(ValueError, match="pattern entry out of range"):
+        mp.pattern_to_graph_device(4, [0, 4], [1, 1], 1)
+    with pytest.raises(ValueError, match="block size must be positive"):
+        mp.pattern_to_graph_device(4, [0], [1], 0)
+    # tests/graph_test.cpp:34-42: symmetrises and drops the diagonal
+    g = mp.pattern_to_graph_device(3, [2, 1], [0, 1])
+    assert g.edge_count() == 1 and g.neighbors_of(0).tolist() == [2] and g.neighbors_of(1).size == 0
+    lifted = mp.lift_patches(mp.PatchPartition(np.array([1, 0, 2], np.int32), 3), 2)
+    assert lifted.assignment.tolist() == [1, 1, 0, 0, 2, 2] and lifted.patch_count == 3
+
+
+@pytest.mark.parametrize("name", ["natural", "md", "nd-vertex"])
+def test_baselines_match_reference(name):
+    """run_baselines (pipeline.cpp:162-186) configurations vs the reference."""
+    from oracle.oracle import Reference
+    g = mp.mesh_to_graph(mp.make_random_mesh(24, 21, 7))
+    res = mp.run_baseline(g, name)
+    cfg = {"natural": dict(nd_level=0, mode=2), "md": dict(nd_level=0, mode=0), "nd-vertex": dict(patch_size=1)}[name]
+    o = Reference().order(g, **cfg)
+    assert np.array_equal(res.perm.perm, o["perm"])
+    if name == "natural":
+        assert res.perm.perm.tolist() == list(range(g.n))
