@@ -39,7 +39,8 @@ enum {
   MP_EINVAL = 1,  /* std::invalid_argument in the reference */
   MP_ECUDA = 2,   /* CUDA runtime / launch failure */
   MP_ENOMEM = 3,  /* device or pinned allocation failed */
-  MP_ELOGIC = 4   /* std::logic_error in the reference (self-check) */
+  MP_ELOGIC = 4,  /* std::logic_error in the reference (self-check) */
+  MP_EIO = 5      /* std::runtime_error from the reference's file I/O (io.cpp) */
 };
 
 enum { MP_LOCAL_APPROX = 0, MP_LOCAL_EXACT = 1, MP_LOCAL_NATURAL = 2 }; /* local_order.hpp:10 OrderMode */
@@ -215,6 +216,25 @@ int mp_lift_patches(mp_context* ctx, int32_t n, const int32_t* assignment, int32
 /* graph.hpp:56 mesh_to_graph on the host (input generation); nbr NULL = count only */
 int mp_mesh_to_graph(int32_t nv, int64_t ntri, const int32_t* tris, int32_t* off, int32_t* nbr,
                      int64_t* nnz);
+
+/* ---- On-disk formats (io.hpp / io.cpp): host-only text I/O.
+ * Accepted syntax, error texts ("path:line: msg") and written bytes follow the
+ * reference; its std::runtime_error becomes MP_EIO, validate_mesh's
+ * std::invalid_argument stays MP_EINVAL.  Two-call convention: a NULL output
+ * array returns only the counts. */
+/* io.cpp:178 parse_mesh (.off / .obj by extension, polygons fan-triangulated) */
+int mp_read_mesh(const char* path, int32_t format /* 0 by extension, 1 OFF, 2 OBJ */, int32_t* vertex_count,
+                 int64_t* triangle_count, int32_t* tris);
+/* io.cpp:186 parse_matrix_market + types.cpp:9 symmetrize: 0-based, sorted, unique */
+int mp_read_matrix_market(const char* path, int32_t* n, int64_t* nnz, int32_t* rows, int32_t* cols);
+/* io.cpp:242 read_patch_file: exactly n nonnegative ids; patch_count = max + 1 */
+int mp_read_patch_file(const char* path, int32_t n, int32_t* assignment, int32_t* patch_count);
+/* io.cpp:264 write_permutation / io.cpp:270 read_permutation: one index per line */
+int mp_write_permutation(const char* path, int32_t n, const int32_t* perm);
+int mp_read_permutation(const char* path, int32_t* n, int32_t* perm);
+/* io.cpp:283 write_etree: "idx level count v..." per node of the 2^(L+1)-1 tree */
+int mp_write_etree(const char* path, int32_t nd_level, const int32_t* node_offsets,
+                   const int32_t* node_vertices);
 
 #ifdef __cplusplus
 }

@@ -12,6 +12,7 @@ __graft_entry__.smoke() and bench.py's CPU-baseline legs may import this.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import subprocess
 import time
 from pathlib import Path
@@ -203,6 +204,50 @@ class Reference(_Base):
         self._check(f(C.c_int32(n), C.c_int64(len(rows)), _p(rows), _p(cols), C.c_int32(block_size), _p(off),
                       _p(nbr), C.byref(nnz)))
         return off, nbr
+
+    # --- on-disk formats (io.cpp) -------------------------------------------
+    def parse_mesh(self, path, fmt=0):
+        """io.cpp:88-184 parse_off (fmt 1) / parse_obj (2) / parse_mesh (0) -> (nv, tris)."""
+        nv, nt = C.c_int32(), C.c_int64()
+        f = self._f("parse_mesh")
+        self._check(f(os.fsencode(path), C.c_int32(fmt), C.byref(nv), C.byref(nt), None))
+        tris = np.zeros((nt.value, 3), np.int32)
+        self._check(f(os.fsencode(path), C.c_int32(fmt), C.byref(nv), C.byref(nt), _p(tris)))
+        return nv.value, tris
+
+    def parse_matrix_market(self, path):
+        """io.cpp:186-240 -> (n, rows, cols) of the symmetrized pattern."""
+        n, nnz = C.c_int32(), C.c_int64()
+        f = self._f("parse_matrix_market")
+        self._check(f(os.fsencode(path), C.byref(n), C.byref(nnz), None, None))
+        rows, cols = np.zeros(max(nnz.value, 1), np.int32), np.zeros(max(nnz.value, 1), np.int32)
+        self._check(f(os.fsencode(path), C.byref(n), C.byref(nnz), _p(rows), _p(cols)))
+        return n.value, rows[:nnz.value], cols[:nnz.value]
+
+    def read_patch_file(self, path, n):
+        """io.cpp:242-262 -> (assignment, patch_count)."""
+        a, pc = np.zeros(max(n, 1), np.int32), C.c_int32()
+        self._check(self._f("read_patch_file")(os.fsencode(path), C.c_int32(n), _p(a), C.byref(pc)))
+        return a[:n], pc.value
+
+    def write_permutation(self, path, perm):
+        """io.cpp:264-268."""
+        perm = _i32(perm)
+        self._check(self._f("write_permutation")(os.fsencode(path), C.c_int32(len(perm)), _p(perm)))
+
+    def read_permutation(self, path):
+        """io.cpp:270-281."""
+        n = C.c_int32()
+        f = self._f("read_permutation")
+        self._check(f(os.fsencode(path), C.byref(n), None))
+        p = np.zeros(max(n.value, 1), np.int32)
+        self._check(f(os.fsencode(path), C.byref(n), _p(p)))
+        return p[:n.value]
+
+    def write_etree(self, path, n, nd_level, node_offsets, node_vertices):
+        """io.cpp:283-293."""
+        self._check(self._f("write_etree")(os.fsencode(path), C.c_int32(n), C.c_int32(nd_level),
+                                           _p(_i32(node_offsets)), _p(_i32(node_vertices))))
 
     def cross_block_fill(self, g, perm, nd_level, node_offsets, node_vertices):
         """symbolic.cpp:98-119 (the pipeline self-check, pipeline.cpp:141)."""

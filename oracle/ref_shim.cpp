@@ -7,6 +7,7 @@
 // path, and bench.py's reference arm / cpu_baseline leg time it on the GPU
 // box's host cores.  Every entry point forwards to the reference stage
 // function named in its comment; nothing here re-implements an algorithm.
+#include <algorithm>
 #include <bit>
 #include <chrono>
 #include <cstdint>
@@ -18,6 +19,7 @@
 #include "meshperm/assemble.hpp"
 #include "meshperm/etree.hpp"
 #include "meshperm/graph.hpp"
+#include "meshperm/io.hpp"
 #include "meshperm/local_order.hpp"
 #include "meshperm/patching.hpp"
 #include "meshperm/pipeline.hpp"
@@ -315,6 +317,68 @@ int ref_order(int32_t n, const int32_t* off, const int32_t* nbr, int32_t patch_s
     if (node_offsets) flatten_tree(tree, node_offsets, node_vertices, local_perm);
     if (perm) std::memcpy(perm, p.perm.data(), sizeof(int32_t) * n);
     if (inverse) std::memcpy(inverse, p.inverse.data(), sizeof(int32_t) * n);
+  });
+}
+
+// io.cpp:88-184 parse_off / parse_obj / parse_mesh.  format 0 by extension,
+// 1 OFF, 2 OBJ; tris_out NULL = counts only.
+int ref_parse_mesh(const char* path, int32_t format, int32_t* nv, int64_t* ntri, int32_t* tris_out) {
+  return guarded([&] {
+    TriangleMesh m = format == 1 ? parse_off(path) : format == 2 ? parse_obj(path) : parse_mesh(path);
+    *nv = m.vertex_count;
+    *ntri = static_cast<int64_t>(m.triangles.size());
+    if (tris_out)
+      for (std::size_t t = 0; t < m.triangles.size(); ++t)
+        for (int k = 0; k < 3; ++k) tris_out[3 * t + k] = m.triangles[t][k];
+  });
+}
+
+// io.cpp:186-240 parse_matrix_market (symmetrized pattern).
+int ref_parse_matrix_market(const char* path, int32_t* n, int64_t* nnz, int32_t* rows, int32_t* cols) {
+  return guarded([&] {
+    SparsePattern p = parse_matrix_market(path);
+    *n = p.n;
+    *nnz = static_cast<int64_t>(p.entries.size());
+    if (rows && cols)
+      for (std::size_t k = 0; k < p.entries.size(); ++k) rows[k] = p.entries[k].first, cols[k] = p.entries[k].second;
+  });
+}
+
+// io.cpp:242-262 read_patch_file.
+int ref_read_patch_file(const char* path, int32_t n, int32_t* assignment, int32_t* patch_count) {
+  return guarded([&] {
+    GroupMap g = read_patch_file(path, n);
+    std::copy(g.assignment.begin(), g.assignment.end(), assignment);
+    *patch_count = g.patch_count;
+  });
+}
+
+// io.cpp:264-268 write_permutation (inverse filled for completeness).
+int ref_write_permutation(const char* path, int32_t n, const int32_t* perm) {
+  return guarded([&] {
+    Permutation p;
+    p.perm.assign(perm, perm + n);
+    p.inverse.assign(n, 0);
+    for (int32_t k = 0; k < n; ++k)
+      if (perm[k] >= 0 && perm[k] < n) p.inverse[perm[k]] = k;
+    write_permutation(p, path);
+  });
+}
+
+// io.cpp:270-281 read_permutation; perm NULL = count only.
+int ref_read_permutation(const char* path, int32_t* n, int32_t* perm) {
+  return guarded([&] {
+    std::vector<index_t> p = read_permutation(path);
+    *n = static_cast<int32_t>(p.size());
+    if (perm) std::copy(p.begin(), p.end(), perm);
+  });
+}
+
+// io.cpp:283-293 write_etree of a flattened tree.
+int ref_write_etree(const char* path, int32_t n, int32_t nd_level, const int32_t* node_offsets,
+                    const int32_t* node_vertices) {
+  return guarded([&] {
+    write_etree(unflatten_tree(n, nd_level, node_offsets, node_vertices, nullptr), path);
   });
 }
 

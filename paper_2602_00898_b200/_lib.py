@@ -10,7 +10,7 @@ from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libmeshperm_b200.so"
 
-MP_OK, MP_EINVAL, MP_ECUDA, MP_ENOMEM, MP_ELOGIC = 0, 1, 2, 3, 4
+MP_OK, MP_EINVAL, MP_ECUDA, MP_ENOMEM, MP_ELOGIC, MP_EIO = 0, 1, 2, 3, 4, 5
 LOCAL_MODES = {"approx_md": 0, "exact_md": 1, "natural": 2}
 SCHEDULES = {"postorder": 0, "levelorder": 1}
 
@@ -105,6 +105,12 @@ SIGNATURES = [
     ("mp_lift_patches", C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32]),
     ("mp_mesh_to_graph_device", C.c_int,
      [C.c_void_p, C.c_int32, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, i64p]),
+    ("mp_read_mesh", C.c_int, [C.c_char_p, C.c_int32, i32p, i64p, C.c_void_p]),
+    ("mp_read_matrix_market", C.c_int, [C.c_char_p, i32p, i64p, C.c_void_p, C.c_void_p]),
+    ("mp_read_patch_file", C.c_int, [C.c_char_p, C.c_int32, C.c_void_p, i32p]),
+    ("mp_write_permutation", C.c_int, [C.c_char_p, C.c_int32, C.c_void_p]),
+    ("mp_read_permutation", C.c_int, [C.c_char_p, i32p, C.c_void_p]),
+    ("mp_write_etree", C.c_int, [C.c_char_p, C.c_int32, C.c_void_p, C.c_void_p]),
 ]
 
 _lib = None
