@@ -29,6 +29,8 @@ namespace mp {
 namespace {
 
 constexpr int kSymThreads = 512;
+constexpr int kSymWide = 1024;  // block size for levels narrower than half the SMs
+constexpr int kU = 4;  // reach entries per thread per sweep step
 
 int grid_for(const mp_context& ctx, int64_t n, int threads = 256) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), ctx.num_sms * 16LL)));
@@ -63,6 +65,7 @@ struct SymArgs {
   int64_t* column_counts;    // by position
   int32_t* parent;           // by position
   int32_t* overflow;
+  int32_t smem_path;         // path sizes up to this use shared-memory marks
 };
 
 // private index of w (in node A, an ancestor-or-self of the CTA's node)
@@ -70,7 +73,15 @@ __device__ __forceinline__ int32_t priv_idx(const SymArgs& a, const int32_t* aba
   return abase[tree_level(a.node_of[w])] + a.local_of[w];
 }
 
-__global__ void __launch_bounds__(kSymThreads) sym_kernel(SymArgs a) {
+// Pool space is taken from the global cursor in per-CTA chunks that double
+// from kChunk0 to kChunkMax ints (the unused tail of a CTA's last chunk is at
+// most what it used); every thread tracks the chunk identically (all inputs
+// to the bookkeeping are block-uniform), so only a refill needs a broadcast.
+constexpr unsigned long long kChunk0 = 2048, kChunkMax = 1 << 20;
+
+extern __shared__ int32_t sym_dyn[];
+
+__global__ void __launch_bounds__(kSymWide) sym_kernel(SymArgs a) {
   const int32_t first = (1 << a.level) - 1;
   const int32_t X = first + blockIdx.x;
   if (X >= a.nn) return;
@@ -80,13 +91,14 @@ __global__ void __launch_bounds__(kSymThreads) sym_kernel(SymArgs a) {
   const bool has_children = lc < a.nn;
   const int64_t lslab = a.left_off[X];
   int32_t* myleft = a.left_list + lslab;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   __shared__ int32_t abase[32];
-  __shared__ int32_t s_cnt, s_nleft, s_abort;
-  __shared__ unsigned long long s_at;
+  __shared__ int32_t s_cnt[2], s_nleft;
+  __shared__ unsigned long long s_chunk;
   __shared__ uint64_t red[32];
   if (threadIdx.x == 0) {
     s_nleft = 0;
-    s_abort = 0;
+    s_cnt[0] = s_cnt[1] = 0;
     // ancestor sizes along the path: abase[level] = sum of the sizes above
     int32_t path[32];
     int32_t depth = 0;
@@ -104,7 +116,10 @@ __global__ void __launch_bounds__(kSymThreads) sym_kernel(SymArgs a) {
   }
   __syncthreads();
   const int32_t path_size = abase[a.level + 1];
-  int32_t* marks = a.ws + a.ws_off[blockIdx.x];
+  // marks + scratch: shared memory when the launch provided room for this
+  // level's longest path, else this node's global workspace.  A reach lies
+  // inside the path (node + ancestors), so scratch needs path_size entries.
+  int32_t* marks = a.smem_path >= path_size ? sym_dyn : a.ws + a.ws_off[blockIdx.x];
   int32_t* scratch = marks + path_size;
   for (int32_t i = threadIdx.x; i < path_size; i += blockDim.x) marks[i] = 0;
   const int32_t* verts = a.node_vertices + xb;
@@ -124,7 +139,6 @@ __global__ void __launch_bounds__(kSymThreads) sym_kernel(SymArgs a) {
   __syncthreads();
   // ---- inherited elements (warp per element)
   if (has_children) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int side = 0; side < 2; ++side) {
       const int32_t c = side ? rc : lc;
       const int32_t* cl = a.left_list + a.left_off[c];
@@ -146,83 +160,143 @@ __global__ void __launch_bounds__(kSymThreads) sym_kernel(SymArgs a) {
     }
   }
   __syncthreads();
-  // ---- the game on X, pivots in local_perm order
+  // ---- the game on X, pivots in local_perm order; two barriers per pivot
   const int32_t pos0 = a.node_pos[X];
+  unsigned long long cur = 0, cend = 0, chunk = kChunk0;  // this CTA's pool chunk (block-uniform)
+  // the pivot sequence and CSR offsets are static: the next pivot's are
+  // loaded while this one runs
+  int32_t p_next = nx ? verts[a.local_perm[xb]] : 0;
+  int32_t o_next = nx ? a.g.off[p_next] : 0;
   for (int32_t k = 0; k < nx; ++k) {
-    const int32_t p = verts[a.local_perm[xb + k]];
+    const int32_t p = p_next, po = o_next;
+    if (k + 1 < nx) {
+      p_next = verts[a.local_perm[xb + k + 1]];
+      o_next = a.g.off[p_next];
+    }
     const int32_t tok = k + 1;
-    if (threadIdx.x == 0) {
-      s_cnt = 0;
-      marks[priv_idx(a, abase, p)] = tok;
-    }
-    __syncthreads();
+    int32_t* cnt = &s_cnt[k & 1];
     const int32_t np_adj = a.nadj[p], np_el = a.nel[p];
-    const int32_t* padj = a.adj + a.g.off[p];
-    const int32_t* pel = a.el + a.g.off[p];
-    for (int32_t i = threadIdx.x; i < np_adj; i += blockDim.x) {
-      const int32_t w = padj[i];
-      if (atomicExch(&marks[priv_idx(a, abase, w)], tok) != tok) scratch[atomicAdd(&s_cnt, 1)] = w;
-    }
-    for (int32_t ei = 0; ei < np_el; ++ei) {
-      const int32_t e = pel[ei];
-      const int32_t* bd = a.pool + a.bptr[e];
-      const int32_t sz = a.bsz[e];
-      for (int32_t i = threadIdx.x; i < sz; i += blockDim.x) {
-        const int32_t w = bd[i];
-        if (atomicExch(&marks[priv_idx(a, abase, w)], tok) != tok) scratch[atomicAdd(&s_cnt, 1)] = w;
+    const int32_t* padj = a.adj + po;
+    const int32_t* pel = a.el + po;
+    // reach = adj(p) + the boundaries of p's elements, minus p; the smallest
+    // permutation position in it is folded in on the way.  Each thread takes
+    // kU entries at a time so their dependent loads are in flight together.
+    uint64_t mn = ~0ull;
+    auto sweep = [&](const int32_t* list, int32_t len) {
+      for (int32_t i0 = threadIdx.x; i0 < len; i0 += kU * blockDim.x) {
+        int32_t w[kU], pi[kU];
+        uint32_t inv[kU];
+#pragma unroll
+        for (int q = 0; q < kU; ++q) {
+          const int32_t i = i0 + q * blockDim.x;
+          w[q] = i < len ? list[i] : p;
+        }
+#pragma unroll
+        for (int q = 0; q < kU; ++q)
+          if (w[q] != p) pi[q] = priv_idx(a, abase, w[q]), inv[q] = static_cast<uint32_t>(a.inverse[w[q]]);
+#pragma unroll
+        for (int q = 0; q < kU; ++q)
+          if (w[q] != p && atomicExch(&marks[pi[q]], tok) != tok) {
+            scratch[atomicAdd(cnt, 1)] = w[q];
+            mn = min(mn, static_cast<uint64_t>(inv[q]));
+          }
+      }
+    };
+    sweep(padj, np_adj);
+    // elements: each warp loads up to 32 (boundary, size) pairs at once, then
+    // the whole block sweeps each boundary (a root-separator element can hold
+    // thousands of vertices)
+    for (int32_t e0 = 0; e0 < np_el; e0 += 32) {
+      const int32_t ne = min(32, np_el - e0);
+      int32_t my_e = -1, my_sz = 0;
+      int64_t my_bp = 0;
+      if (lane < ne) {
+        my_e = pel[e0 + lane];
+        my_bp = a.bptr[my_e];
+        my_sz = a.bsz[my_e];
+        if (wid == 0) a.emark[my_e] = p + 1;
+      }
+      for (int32_t j = 0; j < ne; ++j) {
+        const int32_t sz = __shfl_sync(0xffffffffu, my_sz, j);
+        sweep(a.pool + __shfl_sync(0xffffffffu, my_bp, j), sz);
       }
     }
-    for (int32_t ei = threadIdx.x; ei < np_el; ei += blockDim.x) a.emark[pel[ei]] = p + 1;
+    mn = warp_min_u64(mn);
+    if (lane == 0) red[wid] = mn;
     __syncthreads();
-    const int32_t nb = s_cnt;
-    // column count and etree parent (symbolic.cpp:40-43, :86-93)
-    uint64_t mn = ~0ull;
-    for (int32_t i = threadIdx.x; i < nb; i += blockDim.x) mn = min(mn, static_cast<uint64_t>(a.inverse[scratch[i]]));
-    mn = block_min_u64(mn, red);
+    const int32_t nb = *cnt;
+    mn = lane < nw ? red[lane] : ~0ull;
+    mn = warp_min_u64(mn);
+    if (cur + nb > cend) {  // block-uniform: refill the chunk
+      const unsigned long long take = max(static_cast<unsigned long long>(nb), chunk);
+      chunk = min(2 * chunk, kChunkMax);
+      if (threadIdx.x == 0) {
+        const unsigned long long at = atomicAdd(a.pool_cursor, take);
+        if (static_cast<int64_t>(at + take) > a.pool_cap) {
+          atomicExch(a.overflow, 1);
+          s_chunk = ~0ull;
+        } else {
+          s_chunk = at;
+        }
+      }
+      __syncthreads();
+      cur = s_chunk;
+      if (cur == ~0ull) return;  // host retries with a larger pool
+      cend = cur + take;
+    }
+    const unsigned long long at = cur;
+    cur += nb;
     if (threadIdx.x == 0) {
+      // column count and etree parent (symbolic.cpp:40-43, :86-93)
       a.column_counts[pos0 + k] = static_cast<int64_t>(nb) + 1;
       a.parent[pos0 + k] = nb ? static_cast<int32_t>(mn) : -1;
-      unsigned long long at = atomicAdd(a.pool_cursor, static_cast<unsigned long long>(nb));
-      s_at = at;
-      if (static_cast<int64_t>(at + nb) > a.pool_cap) {
-        s_abort = 1;
-        atomicExch(a.overflow, 1);
-      }
+      a.bptr[p] = static_cast<int64_t>(at);
+      a.bsz[p] = nb;
+      a.nadj[p] = 0;
+      a.nel[p] = 0;
+      s_cnt[(k + 1) & 1] = 0;
     }
-    __syncthreads();
-    if (s_abort) return;  // host retries with a larger pool
-    int32_t* dst = a.pool + s_at;
+    int32_t* dst = a.pool + at;
     for (int32_t i = threadIdx.x; i < nb; i += blockDim.x) dst[i] = scratch[i];
-    // update the node's own boundary members (elimination.cpp:75-83)
+    for (int32_t ei = threadIdx.x; ei < np_el; ei += blockDim.x) a.bsz[pel[ei]] = 0;
+    // update the node's own boundary members (elimination.cpp:75-83): drop
+    // reach members and p from adj, absorbed elements from el, append p.
+    // Lists are read ahead in chunks of 8 before the in-place compaction
+    // writes (the aliasing would otherwise serialise every load).
     for (int32_t i = threadIdx.x; i < nb; i += blockDim.x) {
       const int32_t w = scratch[i];
-      if (a.node_of[w] != X) continue;
-      const int32_t o = a.g.off[w];
+      // membership and the list heads are loaded together
+      const int32_t xw = a.node_of[w], o = a.g.off[w], na = a.nadj[w], ne = a.nel[w];
+      if (xw != X) continue;
       int32_t* wa = a.adj + o;
       int32_t c = 0;
-      const int32_t na = a.nadj[w];
-      for (int32_t j = 0; j < na; ++j) {
-        const int32_t x = wa[j];
-        if (marks[priv_idx(a, abase, x)] != tok) wa[c++] = x;
+      for (int32_t j0 = 0; j0 < na; j0 += 8) {
+        int32_t x[8];
+        bool keep[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) x[q] = j0 + q < na ? wa[j0 + q] : p;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) keep[q] = x[q] != p && marks[priv_idx(a, abase, x[q])] != tok;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (keep[q]) wa[c++] = x[q];
       }
       a.nadj[w] = c;
       int32_t* we = a.el + o;
       int32_t ce = 0;
-      const int32_t ne = a.nel[w];
-      for (int32_t j = 0; j < ne; ++j) {
-        const int32_t e = we[j];
-        if (a.emark[e] != p + 1) we[ce++] = e;
+      for (int32_t j0 = 0; j0 < ne; j0 += 8) {
+        int32_t e[8];
+        bool keep[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) e[q] = j0 + q < ne ? we[j0 + q] : -1;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) keep[q] = e[q] >= 0 && a.emark[e[q]] != p + 1;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (keep[q]) we[ce++] = e[q];
       }
       we[ce++] = p;
       a.nel[w] = ce;
-    }
-    __syncthreads();
-    for (int32_t ei = threadIdx.x; ei < np_el; ei += blockDim.x) a.bsz[pel[ei]] = 0;
-    if (threadIdx.x == 0) {
-      a.bptr[p] = static_cast<int64_t>(s_at);
-      a.bsz[p] = nb;
-      a.nadj[p] = 0;
-      a.nel[p] = 0;
     }
     __syncthreads();
   }
@@ -289,13 +363,23 @@ void tree_fill_dev(mp_context& ctx, const DGraph& g, int32_t L, const int32_t* n
   // path sizes (node + ancestors), per level workspace offsets
   std::vector<int64_t> path(nn, 0);
   for (int32_t i = 0; i < nn; ++i) path[i] = size_of(i) + (i ? path[(i - 1) / 2] : 0);
+  // marks + scratch (8 B per path vertex) live in shared
+  // memory for nodes whose path fits kSymSmem (keeps 2 CTAs per SM); longer
+  // paths use a per-node global workspace
+  constexpr int64_t kSymSmem = 100 * 1024;
+  allow_max_smem(sym_kernel, ctx.device);
   int64_t ws_max = 0;
   std::vector<std::vector<int64_t>> ws_offs(L + 1);
+  std::vector<int32_t> smem_path(L + 1, 0);
   for (int32_t l = 0; l <= L; ++l) {
     const int32_t first = (1 << l) - 1, width = 1 << l;
     auto& wo = ws_offs[l];
     wo.assign(width + 1, 0);
-    for (int32_t j = 0; j < width; ++j) wo[j + 1] = wo[j] + 2 * path[first + j] + 2;
+    int64_t longest = 0;
+    for (int32_t j = 0; j < width; ++j) longest = std::max(longest, path[first + j]);
+    smem_path[l] = static_cast<int32_t>(std::min<int64_t>(longest, kSymSmem / 8));
+    for (int32_t j = 0; j < width; ++j)
+      wo[j + 1] = wo[j] + (path[first + j] > smem_path[l] ? 2 * path[first + j] + 2 : 0);
     ws_max = std::max(ws_max, wo[width]);
   }
   DevBuf<int32_t> local_of(n, s), nadj(n, s), nel(n, s), bsz(n, s), emark(n, s), ws(std::max<int64_t>(ws_max, 1), s),
@@ -326,7 +410,9 @@ void tree_fill_dev(mp_context& ctx, const DGraph& g, int32_t L, const int32_t* n
       MP_CUDA(cudaMemcpyAsync(d_ws_off, ws_offs[l].data(), sizeof(int64_t) * (width + 1), cudaMemcpyHostToDevice, s));
       a.level = l;
       a.ws_off = d_ws_off;
-      { const int kt__ = ctx.ktime_begin(kKSym); MP_KERNEL(ctx, sym_kernel<<<width, kSymThreads, 0, s>>>(a)); ctx.ktime_end(kt__); }
+      a.smem_path = smem_path[l];
+      const size_t dyn = 8 * static_cast<size_t>(smem_path[l]);
+      { const int kt__ = ctx.ktime_begin(kKSym); MP_KERNEL(ctx, sym_kernel<<<width, 2 * width <= ctx.num_sms ? kSymWide : kSymThreads, dyn, s>>>(a)); ctx.ktime_end(kt__); }
     }
     int32_t h_over = 0;
     unsigned long long used = 0;
