@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kMdThreads) md_kernel(MdArgs a) {
 //   bsz[e]  = boundary size of element e (0 = absorbed / empty)
 //   blk[b]  = min (degree, id) key of the 32 vertices of block b
 // Per pivot: argmin over blk (every warp, redundantly), reach collection,
-// member updates, dirty-block refresh: three barriers.
+// member updates, dirty-block refresh: three barriers (B2, B3, B4).
 constexpr int32_t kMdFastCap = 6 * 1024;  // nodes up to this size use the fast kernel
 
 __global__ void __launch_bounds__(kMdThreads) md_fast_kernel(MdArgs a) {
@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(kMdThreads) md_fast_kernel(MdArgs a) {
   int32_t* st = bsz + nv;
   int32_t* loff = st + nv;  // CSR offset of each local vertex (its list slots)
   uint32_t* dirty = reinterpret_cast<uint32_t*>(loff + nv);  // nb bits
-  __shared__ int32_t s_nb, s_cursor, s_half, s_need, s_p, s_dcnt;
+  __shared__ int32_t s_nbc[2], s_cursor, s_half, s_dcnt;
   __shared__ int32_t s_dlist[kMdThreads];  // dirty blocks of this pivot (<= reach + 1 distinct)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int64_t pbase = a.pool_off[node];
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(kMdThreads) md_fast_kernel(MdArgs a) {
     bsz[k] = 0;
   }
   for (int32_t b = threadIdx.x; b < (nb + 31) / 32; b += blockDim.x) dirty[b] = 0;
-  if (threadIdx.x == 0) s_cursor = 0, s_half = 0, s_dcnt = 0;
+  if (threadIdx.x == 0) s_cursor = 0, s_half = 0, s_dcnt = 0, s_nbc[0] = s_nbc[1] = 0;
   __syncthreads();
   for (int32_t b = wid; b < nb; b += nwarp) {
     const int32_t i = b * 32 + lane;
@@ -328,24 +328,18 @@ __global__ void __launch_bounds__(kMdThreads) md_fast_kernel(MdArgs a) {
   __syncthreads();
 
   for (int32_t k = 0; k < nv; ++k) {
-    // ---- pivot: min (degree, local id), warp 0
-    if (wid == 0) {
-      uint64_t best = ~0ull;
-      for (int32_t b = lane; b < nb; b += 32) best = min(best, blk[b]);
-      best = warp_min_u64(best);
-      if (lane == 0) {
-        s_p = static_cast<int32_t>(best & 0xffffffffu);
-        s_need = (s_cursor + (nv - k)) > pcap;
-        s_nb = 0;
-      }
-    }
-    __syncthreads();  // B1
-    const int32_t p = s_p;
+    // ---- pivot: min (degree, local id), computed by every warp (no barrier
+    // to broadcast it; blk is stable since the previous B4)
+    uint64_t best = ~0ull;
+    for (int32_t b = lane; b < nb; b += 32) best = min(best, blk[b]);
+    best = warp_min_u64(best);
+    const int32_t p = static_cast<int32_t>(best & 0xffffffffu);
     const int32_t tok = k + 1;
+    int32_t* cnt = &s_nbc[k & 1];
     const int32_t po = loff[p];
     const int32_t pst = st[p];
     const int32_t np_adj = pst & 0xffff, np_el = pst >> 16;
-    if (s_need) {  // compact live boundaries into the other half
+    if (s_cursor + (nv - k) > pcap) {  // block-uniform: compact live boundaries into the other half
       int32_t* src = a.pool + pbase + (s_half ? pcap : 0);
       int32_t* dst = a.pool + pbase + (s_half ? 0 : pcap);
       int32_t run = 0;
@@ -372,15 +366,15 @@ __global__ void __launch_bounds__(kMdThreads) md_fast_kernel(MdArgs a) {
       __syncthreads();
     }
     int32_t* half = a.pool + pbase + (s_half ? pcap : 0);
-    int32_t* out = half + s_cursor;
-    if (threadIdx.x == 0) mark[p] = tok;
-    __syncthreads();
-    // ---- reach set: variables of p plus boundaries of p's elements
+    const int32_t cur0 = s_cursor;
+    int32_t* out = half + cur0;
+    // ---- reach set: variables of p plus boundaries of p's elements (p itself
+    // is skipped explicitly; its mark is set for the member updates below)
     const int32_t* padj = a.adj + po;
     const int32_t* pel = a.el + po;
     for (int32_t i = threadIdx.x; i < np_adj; i += blockDim.x) {
       const int32_t w = padj[i];
-      if (atomicExch(&mark[w], tok) != tok) out[atomicAdd(&s_nb, 1)] = w;
+      if (atomicExch(&mark[w], tok) != tok) out[atomicAdd(cnt, 1)] = w;
     }
     for (int32_t ei = 0; ei < np_el; ++ei) {
       const int32_t e = pel[ei];
@@ -388,22 +382,23 @@ __global__ void __launch_bounds__(kMdThreads) md_fast_kernel(MdArgs a) {
       const int32_t sz = bsz[e];
       for (int32_t i = threadIdx.x; i < sz; i += blockDim.x) {
         const int32_t w = bd[i];
-        if (atomicExch(&mark[w], tok) != tok) out[atomicAdd(&s_nb, 1)] = w;
+        if (w != p && atomicExch(&mark[w], tok) != tok) out[atomicAdd(cnt, 1)] = w;
       }
     }
-    __syncthreads();  // B2
-    const int32_t nbd = s_nb;
-    // absorbed elements get the pivot's token (their own vertex marks are dead)
+    // absorbed elements get the pivot's token (element ids are dead vertices,
+    // disjoint from the live vertices marked above)
     for (int32_t ei = threadIdx.x; ei < np_el; ei += blockDim.x) mark[pel[ei]] = tok;
     if (threadIdx.x == 0) {
-      bp[p] = s_cursor;
+      mark[p] = tok;
+      bp[p] = cur0;
       order[k] = p;
       lperm[k] = p;
       deg[p] = 0xffffffffu;
       if (!(atomicOr(&dirty[(p >> 5) >> 5], 1u << ((p >> 5) & 31)) & (1u << ((p >> 5) & 31))))
         s_dlist[atomicAdd(&s_dcnt, 1)] = p >> 5;
     }
-    __syncthreads();  // B2b: absorption marks visible
+    __syncthreads();  // B2: reach, marks and absorption marks visible
+    const int32_t nbd = *cnt;
     // ---- member updates (elimination.cpp:75-83) and their approx degrees
     for (int32_t i = threadIdx.x; i < nbd; i += blockDim.x) {
       const int32_t w = out[i];
@@ -449,6 +444,7 @@ __global__ void __launch_bounds__(kMdThreads) md_fast_kernel(MdArgs a) {
       bsz[p] = nbd;
       st[p] = 0;
       s_cursor += nbd;
+      s_nbc[(k + 1) & 1] = 0;  // its last reader was the previous pivot, before this B2
     }
     // ---- refresh dirty blocks
     const int32_t ndirty = s_dcnt;
