@@ -118,6 +118,13 @@ int mp_context_set_stream(mp_context* ctx, void* stream);
 
 /* ---- whole path: run_pipeline's ordering stages (pipeline.cpp:100-140) ---- */
 int mp_order(mp_context* ctx, const mp_csr* g, const mp_config* cfg, mp_result* out);
+/* Batch of independent graphs (C4): frame f is
+ * mp_order(ctx, &graphs[f], &cfgs[f], &results[f]) on one of the nctx contexts
+ * (one host thread each, all on their own streams, sm_share = nctx for the
+ * call).  status[f] (optional) gets each frame's code; the return value is the
+ * code of the lowest failing frame, its message prefixed "frame f: ". */
+int mp_order_batch(mp_context* const* ctxs, int32_t nctx, int32_t count, const mp_csr* graphs,
+                   const mp_config* cfgs, mp_result* results, int32_t* status);
 
 /* ---- stage entry points (reference free functions) ---- */
 /* etree.hpp:35-36 default_nd_level */

@@ -67,6 +67,9 @@ SIGNATURES = [
     ("mp_context_destroy", None, [C.c_void_p]),
     ("mp_context_set_stream", C.c_int, [C.c_void_p, C.c_void_p]),
     ("mp_order", C.c_int, [C.c_void_p, C.POINTER(MpCsr), C.POINTER(MpConfig), C.POINTER(MpResult)]),
+    ("mp_order_batch", C.c_int,
+     [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, C.POINTER(MpCsr), C.POINTER(MpConfig), C.POINTER(MpResult),
+      C.c_void_p]),
     ("mp_default_nd_level", C.c_int32, [C.c_int32]),
     ("mp_compute_patches", C.c_int,
      [C.c_void_p, C.POINTER(MpCsr), C.c_int32, C.c_uint64, C.c_void_p, C.c_int32, i32p]),

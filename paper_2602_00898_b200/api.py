@@ -394,12 +394,7 @@ def make_config(patch_size=256, nd_level=-1, seed=0, local_mode="approx_md", sch
                     1 if want_fill else 0)
 
 
-def order(g: AdjacencyGraph, patch_size: int = 256, nd_level: int = -1, seed: int = 0, local_mode="approx_md",
-          schedule="postorder", block_size: int = 1, want_fill: bool = True,
-          ctx: Context | None = None) -> PipelineResult:
-    """run_pipeline's ordering stages (pipeline.cpp:100-140) on host arrays."""
-    ctx = ctx or default_context()
-    cfg = make_config(patch_size, nd_level, seed, local_mode, schedule, block_size, want_fill)
+def _prepare(g: AdjacencyGraph, nd_level: int, block_size: int, want_fill: bool):
     L = nd_level if nd_level >= 0 else default_nd_level(g.n)
     nn = (1 << (L + 1)) - 1
     N = block_size * g.n
@@ -420,7 +415,11 @@ def order(g: AdjacencyGraph, patch_size: int = 256, nd_level: int = -1, seed: in
     if not want_fill:
         res.etree_parent = None
         res.column_counts = None
-    check(lib().mp_order(ctx.handle, C.byref(_csr(g)), C.byref(cfg), C.byref(res)))
+    return bufs, res
+
+
+def _finish(g: AdjacencyGraph, bufs, res: MpResult, patch_size: int, block_size: int, want_fill: bool):
+    N = block_size * g.n
     tree = EliminationTree(N, res.nd_level, bufs["tree_node_offsets"], bufs["tree_vertices"][:N],
                            bufs["tree_local_perm"][:N])
     fill = None
@@ -431,6 +430,37 @@ def order(g: AdjacencyGraph, patch_size: int = 256, nd_level: int = -1, seed: in
     return PipelineResult(PatchPartition(bufs["patch_of"][:g.n], res.patch_count, patch_size), tree,
                           Permutation(bufs["perm"][:N], bufs["inverse"][:N]), fill,
                           {k: float(res.stage_ms[i]) for i, k in enumerate(names)}, int(res.kernel_launches))
+
+
+def order(g: AdjacencyGraph, patch_size: int = 256, nd_level: int = -1, seed: int = 0, local_mode="approx_md",
+          schedule="postorder", block_size: int = 1, want_fill: bool = True,
+          ctx: Context | None = None) -> PipelineResult:
+    """run_pipeline's ordering stages (pipeline.cpp:100-140) on host arrays."""
+    ctx = ctx or default_context()
+    cfg = make_config(patch_size, nd_level, seed, local_mode, schedule, block_size, want_fill)
+    bufs, res = _prepare(g, nd_level, block_size, want_fill)
+    check(lib().mp_order(ctx.handle, C.byref(_csr(g)), C.byref(cfg), C.byref(res)))
+    return _finish(g, bufs, res, patch_size, block_size, want_fill)
+
+
+def order_batch(graphs, contexts, patch_size: int = 256, nd_level: int = -1, seed: int = 0,
+                local_mode="approx_md", schedule="postorder", block_size: int = 1,
+                want_fill: bool = True) -> list[PipelineResult]:
+    """mp_order_batch: every graph ordered (same config), frames spread over
+    `contexts` (host threads + streams inside the library); results equal
+    sequential order() calls, in input order."""
+    graphs = list(graphs)
+    cfg = make_config(patch_size, nd_level, seed, local_mode, schedule, block_size, want_fill)
+    preps = [_prepare(g, nd_level, block_size, want_fill) for g in graphs]
+    keep = [_csr(g) for g in graphs]  # the struct copies below do not own the arrays
+    csrs = (MpCsr * max(len(graphs), 1))(*keep)
+    cfgs = (MpConfig * max(len(graphs), 1))(*[cfg for _ in graphs])
+    ress = (MpResult * max(len(graphs), 1))(*[r for _, r in preps])
+    handles = (C.c_void_p * len(contexts))(*[c.handle for c in contexts])
+    status = np.zeros(max(len(graphs), 1), np.int32)
+    check(lib().mp_order_batch(handles, len(contexts), len(graphs), csrs, cfgs, ress, _ptr(status)))
+    return [_finish(g, bufs, ress[i], patch_size, block_size, want_fill)
+            for i, (g, (bufs, _)) in enumerate(zip(graphs, preps))]
 
 
 def order_device(ctx: Context, n: int, offsets_ptr: int, neighbors_ptr: int, out: dict, patch_size=256,

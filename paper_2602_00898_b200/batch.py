@@ -56,10 +56,11 @@ class FramePool:
             self._give(i)
 
     def order_all(self, graphs, **kw):
-        """mp_order for every graph (host arrays in and out), concurrently."""
-        from .api import order
-        futs = [self.ex.submit(self._run, order, g, **kw) for g in graphs]
-        return [f.result() for f in futs]
+        """Every graph ordered concurrently over the pool's contexts (host
+        arrays in and out) through the native mp_order_batch: the library's
+        own host threads, one per context."""
+        from .api import order_batch
+        return order_batch(graphs, self.ctx, **kw)
 
     def close(self):
         self.ex.shutdown()

@@ -279,6 +279,44 @@ def test_frame_pool_concurrent_frames_match():
         assert r.fill.nnz_L == R.elimination_fill(g, o["perm"])["nnz_L"]
 
 
+def test_order_batch_errors_and_status():
+    """mp_order_batch reports the lowest failing frame with its message and
+    per-frame codes; the good frames are still ordered."""
+    good = mp.mesh_to_graph(mp.make_grid_mesh(30, 30))
+    ctxs = [mp.Context(0) for _ in range(3)]
+    try:
+        ok = mp.order_batch([good, good], ctxs, patch_size=32)
+        ref = mp.order(good, patch_size=32)
+        assert all(np.array_equal(r.perm.perm, ref.perm.perm) for r in ok)
+        with pytest.raises(ValueError, match="^frame 1: nd_level out of range"):
+            _batch_with_bad(good, ctxs)
+    finally:
+        for c in ctxs:
+            c.close()
+
+
+def _batch_with_bad(good, ctxs):
+    """Frames 0 and 2 valid, frame 1 with nd_level 30 (rejected)."""
+    import ctypes as C
+    from paper_2602_00898_b200 import api
+    from paper_2602_00898_b200._lib import MpConfig, MpCsr, MpResult, check, lib
+    cfg_ok = api.make_config(patch_size=32)
+    cfg_bad = api.make_config(patch_size=32, nd_level=30)
+    preps = [api._prepare(good, -1, 1, True) for _ in range(3)]
+    keep = [api._csr(good) for _ in range(3)]
+    csrs = (MpCsr * 3)(*keep)
+    cfgs = (MpConfig * 3)(cfg_ok, cfg_bad, cfg_ok)
+    ress = (MpResult * 3)(*[r for _, r in preps])
+    handles = (C.c_void_p * len(ctxs))(*[c.handle for c in ctxs])
+    status = np.full(3, -1, np.int32)
+    try:
+        check(lib().mp_order_batch(handles, len(ctxs), 3, csrs, cfgs, ress, api._ptr(status)))
+    finally:
+        assert status.tolist() == [0, 1, 0]
+        ref = mp.order(good, patch_size=32)
+        assert np.array_equal(preps[2][0]["perm"][:good.n], ref.perm.perm)
+
+
 @pytest.mark.parametrize("rows,patch", [(240, 4), (150, 2)])
 def test_fm_large_nodes_global_state(rows, patch):
     """Root quotients beyond the shared-memory FM capacity (>10,240 patches,
