@@ -243,6 +243,21 @@ int mp_read_permutation(const char* path, int32_t* n, int32_t* perm);
 int mp_write_etree(const char* path, int32_t nd_level, const int32_t* node_offsets,
                    const int32_t* node_vertices);
 
+/* pipeline.hpp:39-54 BenchRow and pipeline.cpp:188-205 csv_header / write_csv
+ * (the reference writes to a stream; here to a file path). */
+typedef struct {
+  const char* input;
+  int64_t n, nnz_A;
+  const char* method;
+  int32_t patch_size, nd_level;
+  double t_patch_ms, t_quotient_ms, t_etree_ms, t_local_ms, t_assemble_ms;
+  int64_t nnz_L;
+  double fill_ratio;
+  int64_t cost;
+} mp_bench_row;
+const char* mp_csv_header(void);
+int mp_write_csv(const char* path, const mp_bench_row* rows, int32_t count);
+
 #ifdef __cplusplus
 }
 #endif

@@ -249,6 +249,17 @@ class Reference(_Base):
         self._check(self._f("write_etree")(os.fsencode(path), C.c_int32(n), C.c_int32(nd_level),
                                            _p(_i32(node_offsets)), _p(_i32(node_vertices))))
 
+    def write_csv(self, path, rows):
+        """pipeline.cpp:193-205 write_csv; rows = dicts with BenchRow fields."""
+        k = len(rows)
+        inp = (C.c_char_p * max(k, 1))(*[r["input"].encode() for r in rows])
+        meth = (C.c_char_p * max(k, 1))(*[r["method"].encode() for r in rows])
+        ints = np.array([[r[f] for f in ("n", "nnz_A", "patch_size", "nd_level", "nnz_L", "cost")] for r in rows],
+                        np.int64).reshape(-1)
+        dbl = np.array([[r[f] for f in ("t_patch_ms", "t_quotient_ms", "t_etree_ms", "t_local_ms", "t_assemble_ms",
+                                         "fill_ratio")] for r in rows], np.float64).reshape(-1)
+        self._check(self._f("write_csv")(os.fsencode(path), C.c_int32(k), inp, meth, _p(ints), _p(dbl)))
+
     def cross_block_fill(self, g, perm, nd_level, node_offsets, node_vertices):
         """symbolic.cpp:98-119 (the pipeline self-check, pipeline.cpp:141)."""
         c = C.c_int64()

@@ -19,6 +19,7 @@
 #include "meshperm/assemble.hpp"
 #include "meshperm/etree.hpp"
 #include "meshperm/graph.hpp"
+#include <fstream>
 #include "meshperm/io.hpp"
 #include "meshperm/local_order.hpp"
 #include "meshperm/patching.hpp"
@@ -379,6 +380,28 @@ int ref_write_etree(const char* path, int32_t n, int32_t nd_level, const int32_t
                     const int32_t* node_vertices) {
   return guarded([&] {
     write_etree(unflatten_tree(n, nd_level, node_offsets, node_vertices, nullptr), path);
+  });
+}
+
+// pipeline.cpp:193-205 write_csv of rows given field by field (strings as
+// '\n'-free C strings; doubles as given).
+int ref_write_csv(const char* path, int32_t count, const char* const* input, const char* const* method,
+                  const int64_t* ints /* n, nnz_A, patch_size, nd_level, nnz_L, cost per row */,
+                  const double* dbl /* t_patch .. t_assemble, fill_ratio per row */) {
+  return guarded([&] {
+    std::vector<BenchRow> rows(count);
+    for (int32_t i = 0; i < count; ++i) {
+      BenchRow& r = rows[i];
+      r.input = input[i];
+      r.method = method[i];
+      r.n = ints[6 * i], r.nnz_A = ints[6 * i + 1];
+      r.patch_size = static_cast<index_t>(ints[6 * i + 2]), r.nd_level = static_cast<index_t>(ints[6 * i + 3]);
+      r.nnz_L = ints[6 * i + 4], r.cost = ints[6 * i + 5];
+      r.t_patch_ms = dbl[6 * i], r.t_quotient_ms = dbl[6 * i + 1], r.t_etree_ms = dbl[6 * i + 2];
+      r.t_local_ms = dbl[6 * i + 3], r.t_assemble_ms = dbl[6 * i + 4], r.fill_ratio = dbl[6 * i + 5];
+    }
+    std::ofstream out(path);
+    write_csv(out, rows);
   });
 }
 

@@ -13,6 +13,6 @@ from .api import (  # noqa: F401
     BASELINES, order, order_batch, order_device, order_subtrees, order_tree_nodes, tree_fill, tree_separation_violations,
 )
 from .formats import (  # noqa: F401
-    parse_matrix_market, parse_mesh, parse_obj, parse_off, read_patch_file, read_permutation, write_etree,
+    BenchRow, bench_row, csv_header, run_baselines, write_csv, parse_matrix_market, parse_mesh, parse_obj, parse_off, read_patch_file, read_permutation, write_etree,
     write_permutation,
 )

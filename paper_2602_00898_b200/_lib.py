@@ -58,6 +58,25 @@ class MpResult(C.Structure):
     ]
 
 
+class MpBenchRow(C.Structure):  # pipeline.hpp:39-54 BenchRow
+    _fields_ = [
+        ("input", C.c_char_p),
+        ("n", C.c_int64),
+        ("nnz_A", C.c_int64),
+        ("method", C.c_char_p),
+        ("patch_size", C.c_int32),
+        ("nd_level", C.c_int32),
+        ("t_patch_ms", C.c_double),
+        ("t_quotient_ms", C.c_double),
+        ("t_etree_ms", C.c_double),
+        ("t_local_ms", C.c_double),
+        ("t_assemble_ms", C.c_double),
+        ("nnz_L", C.c_int64),
+        ("fill_ratio", C.c_double),
+        ("cost", C.c_int64),
+    ]
+
+
 # (name, restype, argtypes) of every exported entry point; tests check that the
 # library exports exactly these.
 SIGNATURES = [
@@ -114,6 +133,8 @@ SIGNATURES = [
     ("mp_write_permutation", C.c_int, [C.c_char_p, C.c_int32, C.c_void_p]),
     ("mp_read_permutation", C.c_int, [C.c_char_p, i32p, C.c_void_p]),
     ("mp_write_etree", C.c_int, [C.c_char_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    ("mp_csv_header", C.c_char_p, []),
+    ("mp_write_csv", C.c_int, [C.c_char_p, C.POINTER(MpBenchRow), C.c_int32]),
 ]
 
 _lib = None

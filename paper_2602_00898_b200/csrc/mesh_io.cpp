@@ -467,3 +467,30 @@ int mp_write_etree(const char* path, int32_t nd_level, const int32_t* node_offse
 }
 
 }  // extern "C"
+
+// ---- benchmark CSV (pipeline.cpp:188-205 csv_header / write_csv) ----------
+extern "C" const char* mp_csv_header(void) {
+  return "input,n,nnz_A,method,patch_size,nd_level,t_patch_ms,t_quotient_ms,"
+         "t_etree_ms,t_local_ms,t_assemble_ms,nnz_L,fill_ratio,cost";
+}
+
+extern "C" int mp_write_csv(const char* path, const mp_bench_row* rows, int32_t count) {
+  return io_guarded([&] {
+    if (!path || (count > 0 && !rows)) throw Error(MP_EINVAL, "null argument");
+    std::string text = std::string(mp_csv_header()) + "\n";
+    char buf[192];
+    for (int32_t i = 0; i < count; ++i) {
+      const mp_bench_row& r = rows[i];
+      std::snprintf(buf, sizeof buf, "%lld,%lld,", static_cast<long long>(r.n), static_cast<long long>(r.nnz_A));
+      text += std::string(r.input ? r.input : "") + "," + buf + (r.method ? r.method : "") + ",";
+      std::snprintf(buf, sizeof buf, "%d,%d,%.3f,%.3f,%.3f,%.3f,%.3f,%lld,%.6f,%lld\n", r.patch_size, r.nd_level,
+                    r.t_patch_ms, r.t_quotient_ms, r.t_etree_ms, r.t_local_ms, r.t_assemble_ms,
+                    static_cast<long long>(r.nnz_L), r.fill_ratio, static_cast<long long>(r.cost));
+      text += buf;
+    }
+    FILE* f = std::fopen(path, "wb");
+    if (!f) throw IoError{std::string("cannot open ") + path + " for writing"};
+    const bool ok = std::fwrite(text.data(), 1, text.size(), f) == text.size();
+    if (std::fclose(f) != 0 || !ok) throw IoError{std::string("write failed: ") + path};
+  });
+}

@@ -11,11 +11,13 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+from dataclasses import dataclass
 
 import numpy as np
 
-from ._lib import check, lib
-from .api import EliminationTree, PatchPartition, Permutation, TriangleMesh, _i32, _ptr
+from ._lib import MpBenchRow, check, lib
+from .api import (AdjacencyGraph, EliminationTree, PatchPartition, Permutation, PipelineResult, TriangleMesh,
+                  _i32, _ptr)
 
 _FORMAT = {"auto": 0, "off": 1, "obj": 2}
 
@@ -78,3 +80,62 @@ def read_permutation(path) -> np.ndarray:  # io.hpp:34
 def write_etree(tree: EliminationTree, path) -> None:  # io.hpp:37
     off, verts = _i32(tree.node_offsets), _i32(tree.vertices)
     check(lib().mp_write_etree(_path(path), int(tree.nd_level), _ptr(off), _ptr(verts)))
+
+
+# ---------------------------------------------------------------- bench CSV
+@dataclass
+class BenchRow:  # pipeline.hpp:39-54
+    input: str = ""
+    n: int = 0
+    nnz_A: int = 0
+    method: str = ""
+    patch_size: int = 0
+    nd_level: int = 0
+    t_patch_ms: float = 0.0
+    t_quotient_ms: float = 0.0
+    t_etree_ms: float = 0.0
+    t_local_ms: float = 0.0
+    t_assemble_ms: float = 0.0
+    nnz_L: int = 0
+    fill_ratio: float = 0.0
+    cost: int = 0
+
+
+def csv_header() -> str:  # pipeline.cpp:188-191
+    return lib().mp_csv_header().decode()
+
+
+def write_csv(rows, path) -> None:  # pipeline.cpp:193-205 (to a file)
+    rows = list(rows)
+    arr = (MpBenchRow * max(len(rows), 1))()
+    for i, r in enumerate(rows):
+        vals = dict(vars(r))
+        vals["input"], vals["method"] = r.input.encode(), r.method.encode()
+        for k, v in vals.items():
+            setattr(arr[i], k, v)
+    check(lib().mp_write_csv(_path(path), arr, len(rows)))
+
+
+def bench_row(result: PipelineResult, g: AdjacencyGraph, input: str, method: str | None = None) -> BenchRow:
+    """The BenchRow run_pipeline fills (pipeline.cpp:88-148): device stage
+    times, n / nnz_A of the measured graph, method "ours-<patch size>"."""
+    st = result.stage_ms
+    fill = result.fill
+    n = len(result.perm.perm)
+    return BenchRow(input, n, fill.nnz_A if fill else n + int(g.offsets[-1]),
+                    method or f"ours-{result.patch.target_size}", result.patch.target_size, result.tree.nd_level,
+                    st["patch"], st["quotient"], st["etree"], st["local"], st["assemble"],
+                    fill.nnz_L if fill else 0, fill.fill_ratio if fill else 0.0, fill.cost if fill else 0)
+
+
+def run_baselines(g: AdjacencyGraph, names, input: str = "graph", ctx=None, **kw) -> list[BenchRow]:
+    """run_baselines (pipeline.cpp:162-186): one row per baseline, `md` reported
+    as "md-only"; unknown names raise ValueError like the reference."""
+    from .api import BASELINES, run_baseline
+    rows = []
+    for name in names:
+        if name not in BASELINES:
+            raise ValueError("unknown baseline: " + name)
+        r = run_baseline(g, name, ctx=ctx, **kw)
+        rows.append(bench_row(r, g, input, "md-only" if name == "md" else name))
+    return rows

@@ -316,3 +316,35 @@ def test_writers_byte_identical(tmp_path, L):
     mp.write_etree(tree, tmp_path / "t1.txt")
     Reference().write_etree(str(tmp_path / "t2.txt"), n, L, node_offsets, perm)
     assert (tmp_path / "t1.txt").read_bytes() == (tmp_path / "t2.txt").read_bytes()
+
+
+# ------------------------------------------------------------------ bench CSV
+def _rows(k, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(k):
+        out.append(mp.BenchRow(
+            input=["grid-64x64", "mesh.off", "a,b"][i % 3], n=int(rng.integers(0, 10**7)),
+            nnz_A=int(rng.integers(0, 10**9)), method=["ours-256", "natural", "md-only", "nd-vertex"][i % 4],
+            patch_size=int(rng.integers(1, 1000)), nd_level=int(rng.integers(0, 12)),
+            t_patch_ms=float(rng.choice([0.0, 0.0005, 0.0015, 2.5e-4, 1234.56789, 1e12])),
+            t_quotient_ms=float(rng.random() * 10), t_etree_ms=float(rng.random() * 1e4), t_local_ms=0.0125,
+            t_assemble_ms=float(rng.random()), nnz_L=int(rng.integers(0, 2**40)),
+            fill_ratio=float(rng.random() * 30), cost=int(rng.integers(0, 2**62))))
+    return out
+
+
+@needs_ref
+@pytest.mark.parametrize("k", [0, 1, 7])
+def test_csv_byte_identical(tmp_path, k):
+    """pipeline.cpp:188-205: header and %.3f / %.6f formatting, byte for byte."""
+    rows = _rows(k, k)
+    mp.write_csv(rows, tmp_path / "a.csv")
+    Reference().write_csv(str(tmp_path / "b.csv"), [vars(r) for r in rows])
+    assert (tmp_path / "a.csv").read_bytes() == (tmp_path / "b.csv").read_bytes()
+    assert (tmp_path / "a.csv").read_text().splitlines()[0] == mp.csv_header()
+
+
+def test_run_baselines_unknown_name():
+    with pytest.raises(ValueError, match="unknown baseline: foo"):
+        mp.run_baselines(None, ["foo"])

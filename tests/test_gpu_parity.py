@@ -542,3 +542,23 @@ def test_baselines_match_reference(name):
     assert np.array_equal(res.perm.perm, o["perm"])
     if name == "natural":
         assert res.perm.perm.tolist() == list(range(g.n))
+
+
+def test_run_baselines_rows_and_csv(tmp_path):
+    """run_baselines rows (methods, n, nnz_A, nnz_L) and the CSV round trip of
+    a pipeline row; nnz_L of each row equals the reference's elimination_fill
+    of the same permutation."""
+    from oracle.oracle import Reference
+    g = mp.mesh_to_graph(mp.make_grid_mesh(20, 20))
+    rows = mp.run_baselines(g, ["natural", "md", "nd-vertex"], input="grid-20x20")
+    assert [r.method for r in rows] == ["natural", "md-only", "nd-vertex"]
+    R = Reference()
+    for r, name in zip(rows, ["natural", "md", "nd-vertex"]):
+        assert r.n == g.n and r.nnz_A == g.n + int(g.offsets[-1]) and r.input == "grid-20x20"
+        assert r.nnz_L == R.elimination_fill(g, mp.run_baseline(g, name).perm.perm)["nnz_L"]
+    main = mp.bench_row(mp.order(g), g, "grid-20x20")
+    assert main.method == "ours-256" and main.patch_size == 256
+    mp.write_csv([main] + rows, tmp_path / "rows.csv")
+    lines = (tmp_path / "rows.csv").read_text().splitlines()
+    assert lines[0] == mp.csv_header() and len(lines) == 5
+    assert lines[1].startswith("grid-20x20,400,") and ",ours-256,256," in lines[1]
