@@ -64,6 +64,12 @@ typedef struct {
   int32_t schedule;     /* MP_SCHEDULE_* (postorder) */
   int32_t block_size;   /* 1; >1 expands perm/tree by b (assemble.hpp:43) */
   int32_t want_fill;    /* 1: factor etree + column counts + nnz(L) (symbolic.hpp:23-31) */
+  /* RunConfig.patch_file path (pipeline.cpp:101-111): NULL = compute_patches;
+   * else a user GroupMap (n ids in [0, user_patch_count), host or device as
+   * the csr) that is validated and, if a patch is disconnected, split by
+   * enforce_connectivity before the ND tree. */
+  const int32_t* user_patches;
+  int32_t user_patch_count;
 } mp_config;
 
 /* PipelineResult (pipeline.hpp:56-61) flattened.  Array pointers may be
@@ -138,6 +144,14 @@ int mp_compute_patches(mp_context* ctx, const mp_csr* g, int32_t target_size, ui
 int mp_enforce_connectivity(mp_context* ctx, const mp_csr* g, const int32_t* assignment,
                             int32_t patch_count, int32_t* out, int32_t on_device,
                             int32_t* out_count);
+/* patching.hpp:44-45 validate_user_patches: PatchReport of a user
+ * assignment (on_device as the csr).  patch_sizes (patch_count int64),
+ * disconnected / unused (patch_count ints each, ascending ids) may be NULL;
+ * the counts are always written.  MP_EINVAL "patch id P out of range at
+ * vertex v" for the first bad vertex, as the reference throws. */
+int mp_validate_user_patches(mp_context* ctx, const mp_csr* g, const int32_t* assignment, int32_t patch_count,
+                             int64_t* patch_sizes, int32_t* disconnected, int32_t* n_disconnected,
+                             int32_t* unused, int32_t* n_unused);
 
 /* quotient.hpp:41 build_quotient + QuotientGraph::positive_edges (quotient.hpp:36).
  * Two-call: edge arrays NULL returns only *n_edges. Host outputs. */

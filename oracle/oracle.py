@@ -260,6 +260,29 @@ class Reference(_Base):
                                          "fill_ratio")] for r in rows], np.float64).reshape(-1)
         self._check(self._f("write_csv")(os.fsencode(path), C.c_int32(k), inp, meth, _p(ints), _p(dbl)))
 
+    def validate_user_patches(self, g, assignment, patch_count):
+        """patching.cpp:386-433 -> (sizes, disconnected, unused)."""
+        a = _i32(assignment)
+        P = max(patch_count, 1)
+        sizes, dis, unu = np.zeros(P, np.int64), np.zeros(P, np.int32), np.zeros(P, np.int32)
+        nd, nu = C.c_int32(), C.c_int32()
+        self._check(self._f("validate_user_patches")(C.c_int32(g.n), _p(_i32(g.offsets)), _p(_i32(g.neighbors)),
+                                                     _p(a), C.c_int32(len(a)), C.c_int32(patch_count), _p(sizes),
+                                                     _p(dis), C.byref(nd), _p(unu), C.byref(nu)))
+        return sizes[:patch_count].tolist(), dis[:nd.value].tolist(), unu[:nu.value].tolist()
+
+    def run_pipeline(self, n_rows_out, mesh_path="", rows=0, cols=0, patch_file="", patch_size=256, nd_level=-1,
+                     seed=0, block_size=1):
+        """pipeline.cpp:57-160 run_pipeline (timing off) -> dict(perm, nnz_L, cost, method)."""
+        perm = np.zeros(max(n_rows_out, 1), np.int32)
+        nnz, cost = C.c_int64(), C.c_int64()
+        method = C.create_string_buffer(64)
+        self._check(self._f("run_pipeline")(os.fsencode(str(mesh_path)), C.c_int32(rows), C.c_int32(cols),
+                                            os.fsencode(str(patch_file)), C.c_int32(patch_size),
+                                            C.c_int32(nd_level), C.c_uint64(seed), C.c_int32(block_size), _p(perm),
+                                            C.byref(nnz), C.byref(cost), method))
+        return dict(perm=perm[:n_rows_out], nnz_L=nnz.value, cost=cost.value, method=method.value.decode())
+
     def cross_block_fill(self, g, perm, nd_level, node_offsets, node_vertices):
         """symbolic.cpp:98-119 (the pipeline self-check, pipeline.cpp:141)."""
         c = C.c_int64()

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <bit>
 #include <chrono>
+#include <cstdio>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -402,6 +403,43 @@ int ref_write_csv(const char* path, int32_t count, const char* const* input, con
     }
     std::ofstream out(path);
     write_csv(out, rows);
+  });
+}
+
+// patching.cpp:386-433 validate_user_patches.  sizes / disconnected / unused
+// hold patch_count entries each.
+int ref_validate_user_patches(int32_t n, const int32_t* off, const int32_t* nbr, const int32_t* assignment,
+                              int32_t assignment_len, int32_t patch_count, int64_t* sizes, int32_t* disconnected,
+                              int32_t* n_disconnected, int32_t* unused, int32_t* n_unused) {
+  return guarded([&] {
+    AdjacencyGraph g = make_graph(n, off, nbr);
+    GroupMap gm{std::vector<index_t>(assignment, assignment + assignment_len), patch_count};
+    PatchReport r = validate_user_patches(gm, g);
+    std::copy(r.patch_sizes.begin(), r.patch_sizes.end(), sizes);
+    std::copy(r.disconnected_patches.begin(), r.disconnected_patches.end(), disconnected);
+    std::copy(r.unused_patches.begin(), r.unused_patches.end(), unused);
+    *n_disconnected = static_cast<int32_t>(r.disconnected_patches.size());
+    *n_unused = static_cast<int32_t>(r.unused_patches.size());
+  });
+}
+
+// pipeline.cpp:57-160 run_pipeline itself on a mesh file or a grid, with an
+// optional patch file: perm (bn ints), nnz_L, cost and the CSV method label.
+int ref_run_pipeline(const char* mesh_path, int32_t rows, int32_t cols, const char* patch_file, int32_t patch_size,
+                     int32_t nd_level, uint64_t seed, int32_t block_size, int32_t* perm_out, int64_t* nnz_L,
+                     int64_t* cost, char* method_out /* 64 bytes */) {
+  return guarded([&] {
+    RunConfig c;
+    if (mesh_path && *mesh_path) c.mesh_path = mesh_path;
+    c.grid_rows = rows, c.grid_cols = cols;
+    if (patch_file && *patch_file) c.patch_file = patch_file;
+    c.patch_size = patch_size, c.nd_level = nd_level, c.seed = seed, c.block_size = block_size;
+    c.collect_timing = false;
+    PipelineResult r = run_pipeline(c);
+    std::copy(r.perm.perm.begin(), r.perm.perm.end(), perm_out);
+    *nnz_L = r.row.nnz_L;
+    *cost = r.row.cost;
+    std::snprintf(method_out, 64, "%s", r.row.method.c_str());
   });
 }
 

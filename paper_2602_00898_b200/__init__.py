@@ -10,7 +10,7 @@ from .api import (  # noqa: F401
     QuotientGraph, TriangleMesh, build_etree, build_quotient, compute_patches, compute_perm, default_context,
     default_nd_level, enforce_connectivity, make_grid_mesh, make_icosphere_mesh, make_random_mesh,
     make_torus_mesh, mesh_to_graph, mesh_to_graph_device, pattern_to_graph_device, lift_patches, run_baseline,
-    BASELINES, order, order_batch, order_device, order_subtrees, order_tree_nodes, tree_fill, tree_separation_violations,
+    BASELINES, PatchReport, validate_user_patches, order, order_batch, order_device, order_subtrees, order_tree_nodes, tree_fill, tree_separation_violations,
 )
 from .formats import (  # noqa: F401
     BenchRow, bench_row, csv_header, run_baselines, write_csv, parse_matrix_market, parse_mesh, parse_obj, parse_off, read_patch_file, read_permutation, write_etree,

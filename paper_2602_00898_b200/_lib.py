@@ -31,6 +31,8 @@ class MpConfig(C.Structure):
         ("schedule", C.c_int32),
         ("block_size", C.c_int32),
         ("want_fill", C.c_int32),
+        ("user_patches", C.c_void_p),
+        ("user_patch_count", C.c_int32),
     ]
 
 
@@ -94,6 +96,8 @@ SIGNATURES = [
      [C.c_void_p, C.POINTER(MpCsr), C.c_int32, C.c_uint64, C.c_void_p, C.c_int32, i32p]),
     ("mp_enforce_connectivity", C.c_int,
      [C.c_void_p, C.POINTER(MpCsr), C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, i32p]),
+    ("mp_validate_user_patches", C.c_int,
+     [C.c_void_p, C.POINTER(MpCsr), C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, i32p, C.c_void_p, i32p]),
     ("mp_build_quotient", C.c_int,
      [C.c_void_p, C.POINTER(MpCsr), C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, i64p]),
     ("mp_build_etree", C.c_int,

@@ -283,6 +283,36 @@ def enforce_connectivity(partition: PatchPartition, g: AdjacencyGraph,
     return PatchPartition(out[:g.n], pc.value, partition.target_size)
 
 
+@dataclass
+class PatchReport:  # patching.hpp:35-42
+    patch_sizes: np.ndarray
+    disconnected_patches: list
+    unused_patches: list
+
+    def all_connected(self) -> bool:
+        return not self.disconnected_patches
+
+    def clean(self) -> bool:
+        return not self.disconnected_patches and not self.unused_patches
+
+
+def validate_user_patches(partition: PatchPartition, g: AdjacencyGraph,
+                          ctx: Context | None = None) -> PatchReport:  # patching.hpp:44-45
+    """Diagnostics of a user assignment, computed on the GPU; ValueError with
+    the reference's messages for a wrong length or an out-of-range id."""
+    ctx = ctx or default_context()
+    a = _i32(partition.assignment)
+    if len(a) != g.n:
+        raise ValueError(f"assignment covers {len(a)} vertices, graph has {g.n}")
+    P = int(partition.patch_count)
+    sizes = np.zeros(max(P, 1), np.int64)
+    dis, unu = np.zeros(max(P, 1), np.int32), np.zeros(max(P, 1), np.int32)
+    nd, nu = C.c_int32(), C.c_int32()
+    check(lib().mp_validate_user_patches(ctx.handle, C.byref(_csr(g)), _ptr(a), P, _ptr(sizes), _ptr(dis),
+                                         C.byref(nd), _ptr(unu), C.byref(nu)))
+    return PatchReport(sizes[:P], dis[:nd.value].tolist(), unu[:nu.value].tolist())
+
+
 def build_quotient(g: AdjacencyGraph, assignment, patch_count: int,
                    ctx: Context | None = None) -> QuotientGraph:  # quotient.hpp:41
     ctx = ctx or default_context()
@@ -434,10 +464,19 @@ def _finish(g: AdjacencyGraph, bufs, res: MpResult, patch_size: int, block_size:
 
 def order(g: AdjacencyGraph, patch_size: int = 256, nd_level: int = -1, seed: int = 0, local_mode="approx_md",
           schedule="postorder", block_size: int = 1, want_fill: bool = True,
-          ctx: Context | None = None) -> PipelineResult:
-    """run_pipeline's ordering stages (pipeline.cpp:100-140) on host arrays."""
+          ctx: Context | None = None, user_patches: PatchPartition | None = None) -> PipelineResult:
+    """run_pipeline's ordering stages (pipeline.cpp:100-140) on host arrays.
+    `user_patches` is the RunConfig.patch_file path (pipeline.cpp:102-111): the
+    given GroupMap is validated and its disconnected patches split instead of
+    computing patches."""
     ctx = ctx or default_context()
     cfg = make_config(patch_size, nd_level, seed, local_mode, schedule, block_size, want_fill)
+    if user_patches is not None:
+        up = _i32(user_patches.assignment)
+        if len(up) != g.n:  # patching.cpp:387-390
+            raise ValueError(f"assignment covers {len(up)} vertices, graph has {g.n}")
+        cfg.user_patches = _ptr(up)
+        cfg.user_patch_count = int(user_patches.patch_count)
     bufs, res = _prepare(g, nd_level, block_size, want_fill)
     check(lib().mp_order(ctx.handle, C.byref(_csr(g)), C.byref(cfg), C.byref(res)))
     return _finish(g, bufs, res, patch_size, block_size, want_fill)

@@ -278,6 +278,25 @@ int mp_enforce_connectivity(mp_context* ctx, const mp_csr* g, const int32_t* ass
   });
 }
 
+int mp_validate_user_patches(mp_context* ctx, const mp_csr* g, const int32_t* assignment, int32_t patch_count,
+                             int64_t* patch_sizes, int32_t* disconnected, int32_t* n_disconnected,
+                             int32_t* unused, int32_t* n_unused) {
+  return guarded([&] {
+    if (!ctx || !g || !n_disconnected || !n_unused || (g->n > 0 && !assignment)) throw Error(MP_EINVAL, "null argument");
+    ScopedDevice sd(ctx->device);
+    GraphView gv;
+    make_view(*ctx, g, gv);
+    DevBuf<int32_t> hold;
+    const int32_t* in = input_ptr(*ctx, assignment, g->n, g->on_device != 0, hold);
+    const UserPatchReport r = validate_user_patches_dev(*ctx, gv.g, in, patch_count);
+    if (patch_sizes) std::copy(r.sizes.begin(), r.sizes.end(), patch_sizes);
+    if (disconnected) std::copy(r.disconnected.begin(), r.disconnected.end(), disconnected);
+    if (unused) std::copy(r.unused.begin(), r.unused.end(), unused);
+    *n_disconnected = static_cast<int32_t>(r.disconnected.size());
+    *n_unused = static_cast<int32_t>(r.unused.size());
+  });
+}
+
 int mp_build_quotient(mp_context* ctx, const mp_csr* g, const int32_t* assignment, int32_t patch_count,
                       int64_t* node_weight, int32_t* edge_p, int32_t* edge_q, int64_t* edge_w, int64_t* n_edges) {
   return guarded([&] {
@@ -466,7 +485,20 @@ int mp_order(mp_context* ctx, const mp_csr* g, const mp_config* cfg, mp_result* 
     DevBuf<int32_t> asg(std::max(n, 1), s), node_of(std::max(n, 1), s), off(nn + 1, s), verts(std::max(n, 1), s),
         lp(std::max(n, 1), s), pm(std::max<int64_t>(N, 1), s), inv(std::max<int64_t>(N, 1), s), pos(nn + 1, s);
     MP_CUDA(cudaEventRecord(ctx->ev[1], s));
-    const int32_t pc = compute_patches_dev(*ctx, gv.g, cfg->patch_size, cfg->seed, asg);
+    int32_t pc = 0;
+    if (cfg->user_patches) {  // pipeline.cpp:102-111: validate, split disconnected patches
+      DevBuf<int32_t> hold;
+      const int32_t* user = input_ptr(*ctx, cfg->user_patches, n, g->on_device != 0, hold);
+      const UserPatchReport rep = validate_user_patches_dev(*ctx, gv.g, user, cfg->user_patch_count);
+      if (!rep.disconnected.empty()) {
+        pc = enforce_connectivity_dev(*ctx, gv.g, user, cfg->user_patch_count, asg);
+      } else {
+        pc = cfg->user_patch_count;
+        if (n > 0) MP_CUDA(cudaMemcpyAsync(asg, user, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
+      }
+    } else {
+      pc = compute_patches_dev(*ctx, gv.g, cfg->patch_size, cfg->seed, asg);
+    }
     MP_CUDA(cudaEventRecord(ctx->ev[2], s));
     // the per-level quotient is rebuilt inside the level loop (ndtree.cu), so
     // the quotient stage has no separate launch; its time is part of etree

@@ -76,6 +76,13 @@ int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, ui
 // patching.cu: enforce_connectivity on a device assignment; returns the new patch count.
 int32_t enforce_connectivity_dev(mp_context& ctx, const DGraph& g, const int32_t* in,
                                  int32_t patch_count, int32_t* out);
+// patching.cu: validate_user_patches (patching.cpp:386-433); throws MP_EINVAL
+// with the reference's message for an out-of-range id.
+struct UserPatchReport {
+  std::vector<int64_t> sizes;
+  std::vector<int32_t> disconnected, unused;
+};
+UserPatchReport validate_user_patches_dev(mp_context& ctx, const DGraph& g, const int32_t* in, int32_t patch_count);
 
 // ND tree (ndtree.cu).  node_of[v] receives the tree node of every vertex;
 // node_offsets (nn+1) / node_vertices (n) the flattened EliminationTree.

@@ -1072,6 +1072,57 @@ int32_t enforce_connectivity_dev(mp_context& ctx, const DGraph& g, const int32_t
   return P + E;
 }
 
+// ------------------------------------------------------------ validate_user_patches
+// patching.cpp:386-433: sizes, patches with more than one component (union-
+// find restricted to same-patch edges, one root per component), unused ids.
+__global__ void patch_stats(int32_t n, const int32_t* assignment, const int32_t* par,
+                            unsigned long long* size, int32_t* ncomp) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    const int32_t p = assignment[v];
+    atomicAdd(&size[p], 1ull);
+    if (par[v] == v) atomicAdd(&ncomp[p], 1);
+  }
+}
+
+UserPatchReport validate_user_patches_dev(mp_context& ctx, const DGraph& g, const int32_t* in, int32_t P) {
+  cudaStream_t s = ctx.stream;
+  const int32_t n = g.n;
+  if (P < 0) throw Error(MP_EINVAL, "patch count must be nonnegative");
+  UserPatchReport r;
+  r.sizes.assign(P, 0);
+  if (n > 0) {
+    DevBuf<int32_t> bad(1, s);
+    MP_KERNEL(ctx, fill_i32<<<1, 32, 0, s>>>(1, bad, 0x7fffffff));
+    MP_KERNEL(ctx, check_range<<<grid_for(ctx, n), 256, 0, s>>>(n, in, P, bad));
+    int32_t h_bad;
+    MP_CUDA(cudaMemcpyAsync(&h_bad, bad, sizeof h_bad, cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+    if (h_bad != 0x7fffffff) {  // the first offending vertex, as the sequential scan reports it
+      int32_t p = 0;
+      MP_CUDA(cudaMemcpyAsync(&p, in + h_bad, sizeof p, cudaMemcpyDeviceToHost, s));
+      MP_CUDA(cudaStreamSynchronize(s));
+      throw Error(MP_EINVAL, "patch id " + std::to_string(p) + " out of range at vertex " + std::to_string(h_bad));
+    }
+  }
+  std::vector<int32_t> ncomp(P, 0);
+  if (n > 0 && P > 0) {
+    DevBuf<int32_t> par(n, s), d_ncomp(P, s);
+    DevBuf<unsigned long long> d_size(P, s);
+    union_find(ctx, g, in, par);
+    MP_CUDA(cudaMemsetAsync(d_size, 0, sizeof(unsigned long long) * P, s));
+    MP_CUDA(cudaMemsetAsync(d_ncomp, 0, sizeof(int32_t) * P, s));
+    MP_KERNEL(ctx, patch_stats<<<grid_for(ctx, n), 256, 0, s>>>(n, in, par, d_size, d_ncomp));
+    MP_CUDA(cudaMemcpyAsync(r.sizes.data(), d_size, sizeof(int64_t) * P, cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaMemcpyAsync(ncomp.data(), d_ncomp, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+  }
+  for (int32_t p = 0; p < P; ++p) {
+    if (ncomp[p] > 1) r.disconnected.push_back(p);
+    if (r.sizes[p] == 0) r.unused.push_back(p);
+  }
+  return r;
+}
+
 int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, uint64_t seed,
                             int32_t* assignment) {
   if (target < 1) throw Error(MP_EINVAL, "target patch size must be positive");

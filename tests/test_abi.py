@@ -5,6 +5,8 @@ import ctypes as C
 import re
 import subprocess
 
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -81,4 +83,32 @@ def test_result_struct_layout():
     # mp_result as declared: 8 pointers + scalars + float[6] + int64 + float[6] + int64[16]
     assert C.sizeof(_lib.MpResult) >= 8 * 8 + 8 + 3 * 8 + 8 + 24 + 8 + 24 + 128
     assert [f[0] for f in _lib.MpConfig._fields_] == ["patch_size", "nd_level", "seed", "local_mode", "schedule",
-                                                      "block_size", "want_fill"]
+                                                      "block_size", "want_fill", "user_patches", "user_patch_count"]
+
+
+def test_struct_offsets_match_header(tmp_path):
+    """ctypes mirrors of mp_csr / mp_config / mp_result / mp_bench_row have the
+    offsets and sizes the C compiler gives the header's declarations."""
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        pytest.skip("no gcc")
+    structs = {"mp_csr": _lib.MpCsr, "mp_config": _lib.MpConfig, "mp_result": _lib.MpResult,
+               "mp_bench_row": _lib.MpBenchRow}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "meshperm_b200.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'  printf("{cname} sizeof %zu\\n", sizeof({cname}));')
+        for f in py._fields_:
+            lines.append(f'  printf("{cname} {f[0]} %zu\\n", offsetof({cname}, {f[0]}));')
+    lines.append("  return 0;\n}")
+    src = tmp_path / "abi.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "abi"
+    subprocess.run(["gcc", "-I", str(Path(__file__).resolve().parents[1] / "include"), str(src), "-o", str(exe)],
+                   check=True)
+    got = dict(l.rsplit(" ", 1) for l in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                         check=True).stdout.splitlines())
+    for cname, py in structs.items():
+        assert int(got[f"{cname} sizeof"]) == C.sizeof(py), cname
+        for f in py._fields_:
+            assert int(got[f"{cname} {f[0]}"]) == getattr(py, f[0]).offset, (cname, f[0])

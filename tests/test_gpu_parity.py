@@ -562,3 +562,72 @@ def test_run_baselines_rows_and_csv(tmp_path):
     lines = (tmp_path / "rows.csv").read_text().splitlines()
     assert lines[0] == mp.csv_header() and len(lines) == 5
     assert lines[1].startswith("grid-20x20,400,") and ",ours-256,256," in lines[1]
+
+
+def _path_graph(n):
+    off = np.array([0] + [min(v, 1) + min(n - 1 - v, 1) for v in range(n)], np.int64).cumsum().astype(np.int32)
+    nbr = np.array([w for v in range(n) for w in (v - 1, v + 1) if 0 <= w < n], np.int32)
+    return mp.AdjacencyGraph(n, off, nbr)
+
+
+def test_validate_user_patches_known_answer():
+    """patching_test.cpp:121-133."""
+    path = _path_graph(5)
+    r = mp.validate_user_patches(mp.PatchPartition(np.array([0, 0, 1, 0, 1], np.int32), 3), path)
+    assert r.patch_sizes.tolist() == [3, 2, 0]
+    assert r.disconnected_patches == [0, 1] and r.unused_patches == [2]
+    assert not r.all_connected() and not r.clean()
+    with pytest.raises(ValueError, match="^patch id 9 out of range at vertex 4$"):
+        mp.validate_user_patches(mp.PatchPartition(np.array([0, 0, 1, 0, 9], np.int32), 3), path)
+    with pytest.raises(ValueError, match="^assignment covers 4 vertices, graph has 5$"):
+        mp.validate_user_patches(mp.PatchPartition(np.array([0, 0, 1, 0], np.int32), 3), path)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_validate_user_patches_matches_reference(seed):
+    from oracle.oracle import Reference
+    rng = np.random.default_rng(seed)
+    g = mp.mesh_to_graph(mp.make_random_mesh(30, 41, seed))
+    r, c = np.divmod(np.arange(g.n), 41)
+    blocks = (r // 6) * 7 + c // 6
+    ids = rng.permutation(blocks.max() + 1 + 5)[blocks]  # 5 unused ids, shuffled
+    ids[rng.integers(0, g.n, 20)] = rng.integers(0, ids.max() + 1, 20)  # stray vertices: disconnected patches
+    P = int(ids.max()) + 3
+    got = mp.validate_user_patches(mp.PatchPartition(ids.astype(np.int32), P), g)
+    sizes, dis, unu = Reference().validate_user_patches(g, ids, P)
+    assert got.patch_sizes.tolist() == sizes and got.disconnected_patches == dis and got.unused_patches == unu
+    assert dis and unu
+
+
+def test_user_patches_stripes_match_run_pipeline(tmp_path):
+    """pipeline_test.cpp:190-205: stripes c % 2 on a 3x4 grid (two disconnected
+    ids) give the reference run_pipeline's permutation."""
+    from oracle.oracle import Reference
+    f = tmp_path / "stripes.patches"
+    f.write_text("".join(f"{c % 2}\n" for r in range(3) for c in range(4)))
+    g = mp.mesh_to_graph(mp.make_grid_mesh(3, 4))
+    up = mp.read_patch_file(f, g.n)
+    res = mp.order(g, patch_size=4, nd_level=1, user_patches=up)
+    ref = Reference().run_pipeline(12, rows=3, cols=4, patch_file=f, patch_size=4, nd_level=1)
+    assert ref["method"] == "user-patches"
+    assert np.array_equal(res.perm.perm, ref["perm"]) and res.fill.nnz_L == ref["nnz_L"]
+    assert mp.tree_separation_violations(g, res.tree) == 0
+
+
+@pytest.mark.parametrize("rows,cols,bs,L", [(40, 37, 7, 3), (64, 64, 9, 4)])
+def test_user_patches_blocks_match_run_pipeline(tmp_path, rows, cols, bs, L):
+    """Block patches with unused ids and split (disconnected) ids through
+    mp_order's user-patch path against the reference run_pipeline."""
+    from oracle.oracle import Reference
+    r, c = np.divmod(np.arange(rows * cols), cols)
+    nbc = (cols + bs - 1) // bs
+    ids = 2 * ((r // bs) * nbc + c // bs)  # every odd id unused
+    ids[(r // bs == 0) & (c // bs == 2)] = 0  # block (0, 2) shares id 0 with block (0, 0): disconnected
+    f = tmp_path / "blocks.patches"
+    f.write_text("".join(f"{x}\n" for x in ids))
+    g = mp.mesh_to_graph(mp.make_grid_mesh(rows, cols))
+    up = mp.read_patch_file(f, g.n)
+    res = mp.order(g, nd_level=L, user_patches=up)
+    ref = Reference().run_pipeline(g.n, rows=rows, cols=cols, patch_file=f, nd_level=L)
+    assert np.array_equal(res.perm.perm, ref["perm"])
+    assert res.fill.nnz_L == ref["nnz_L"] and res.fill.cost == ref["cost"]
