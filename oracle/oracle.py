@@ -271,16 +271,17 @@ class Reference(_Base):
                                                      _p(dis), C.byref(nd), _p(unu), C.byref(nu)))
         return sizes[:patch_count].tolist(), dis[:nd.value].tolist(), unu[:nu.value].tolist()
 
-    def run_pipeline(self, n_rows_out, mesh_path="", rows=0, cols=0, patch_file="", patch_size=256, nd_level=-1,
-                     seed=0, block_size=1):
+    def run_pipeline(self, n_rows_out, mesh_path="", matrix_path="", rows=0, cols=0, patch_file="", patch_size=256,
+                     nd_level=-1, seed=0, block_size=1, out_perm="", out_etree=""):
         """pipeline.cpp:57-160 run_pipeline (timing off) -> dict(perm, nnz_L, cost, method)."""
         perm = np.zeros(max(n_rows_out, 1), np.int32)
         nnz, cost = C.c_int64(), C.c_int64()
         method = C.create_string_buffer(64)
-        self._check(self._f("run_pipeline")(os.fsencode(str(mesh_path)), C.c_int32(rows), C.c_int32(cols),
-                                            os.fsencode(str(patch_file)), C.c_int32(patch_size),
-                                            C.c_int32(nd_level), C.c_uint64(seed), C.c_int32(block_size), _p(perm),
-                                            C.byref(nnz), C.byref(cost), method))
+        e = lambda x: os.fsencode(str(x))
+        self._check(self._f("run_pipeline")(e(mesh_path), e(matrix_path), C.c_int32(rows), C.c_int32(cols),
+                                            e(patch_file), C.c_int32(patch_size), C.c_int32(nd_level),
+                                            C.c_uint64(seed), C.c_int32(block_size), e(out_perm), e(out_etree),
+                                            _p(perm), C.byref(nnz), C.byref(cost), method))
         return dict(perm=perm[:n_rows_out], nnz_L=nnz.value, cost=cost.value, method=method.value.decode())
 
     def cross_block_fill(self, g, perm, nd_level, node_offsets, node_vertices):

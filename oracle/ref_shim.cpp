@@ -423,16 +423,21 @@ int ref_validate_user_patches(int32_t n, const int32_t* off, const int32_t* nbr,
   });
 }
 
-// pipeline.cpp:57-160 run_pipeline itself on a mesh file or a grid, with an
-// optional patch file: perm (bn ints), nnz_L, cost and the CSV method label.
-int ref_run_pipeline(const char* mesh_path, int32_t rows, int32_t cols, const char* patch_file, int32_t patch_size,
-                     int32_t nd_level, uint64_t seed, int32_t block_size, int32_t* perm_out, int64_t* nnz_L,
-                     int64_t* cost, char* method_out /* 64 bytes */) {
+// pipeline.cpp:57-160 run_pipeline itself (mesh file, matrix file or grid;
+// optional patch file and output files): perm (rows out), nnz_L, cost, the
+// CSV method label.
+int ref_run_pipeline(const char* mesh_path, const char* matrix_path, int32_t rows, int32_t cols,
+                     const char* patch_file, int32_t patch_size, int32_t nd_level, uint64_t seed,
+                     int32_t block_size, const char* out_perm, const char* out_etree, int32_t* perm_out,
+                     int64_t* nnz_L, int64_t* cost, char* method_out /* 64 bytes */) {
   return guarded([&] {
     RunConfig c;
     if (mesh_path && *mesh_path) c.mesh_path = mesh_path;
+    if (matrix_path && *matrix_path) c.matrix_path = matrix_path;
     c.grid_rows = rows, c.grid_cols = cols;
     if (patch_file && *patch_file) c.patch_file = patch_file;
+    if (out_perm && *out_perm) c.out_perm = out_perm;
+    if (out_etree && *out_etree) c.out_etree = out_etree;
     c.patch_size = patch_size, c.nd_level = nd_level, c.seed = seed, c.block_size = block_size;
     c.collect_timing = false;
     PipelineResult r = run_pipeline(c);

@@ -16,3 +16,4 @@ from .formats import (  # noqa: F401
     BenchRow, bench_row, csv_header, run_baselines, write_csv, parse_matrix_market, parse_mesh, parse_obj, parse_off, read_patch_file, read_permutation, write_etree,
     write_permutation,
 )
+from .pipeline import PipelineRun, RunConfig, default_input_id, run_pipeline  # noqa: F401,E402

@@ -631,3 +631,75 @@ def test_user_patches_blocks_match_run_pipeline(tmp_path, rows, cols, bs, L):
     ref = Reference().run_pipeline(g.n, rows=rows, cols=cols, patch_file=f, nd_level=L)
     assert np.array_equal(res.perm.perm, ref["perm"])
     assert res.fill.nnz_L == ref["nnz_L"] and res.fill.cost == ref["cost"]
+
+
+def _write_block_matrix(path, g, b, drop=0):
+    """MatrixMarket 'pattern symmetric' of the row graph of g with b x b blocks
+    (lower triangle + diagonal); `drop` removes that many off-block-diagonal
+    entries so the row graph is not exactly expand_graph."""
+    ent = set()
+    for v in range(g.n):
+        for w in list(g.neighbors_of(v)) + [v]:
+            for s in range(b):
+                for t in range(b):
+                    i, j = v * b + s, w * b + t
+                    if i >= j:
+                        ent.add((i, j))
+    ent = sorted(ent)
+    if drop:
+        rng = np.random.default_rng(drop)
+        off = [k for k, (i, j) in enumerate(ent) if i // b != j // b]
+        gone = set(rng.choice(off, drop, replace=False).tolist())
+        ent = [e for k, e in enumerate(ent) if k not in gone]
+    with open(path, "w") as f:
+        f.write("%%MatrixMarket matrix coordinate pattern symmetric\n")
+        f.write(f"{g.n * b} {g.n * b} {len(ent)}\n")
+        f.write("".join(f"{i + 1} {j + 1}\n" for i, j in ent))
+
+
+@pytest.mark.parametrize("case", ["grid", "off", "mesh_block3", "matrix", "matrix_block3", "patches"])
+def test_run_pipeline_matches_reference(tmp_path, case):
+    """run_pipeline (pipeline.cpp:57-160) end to end against the reference's
+    own run_pipeline: permutation, nnz(L), cost, CSV method, and the written
+    permutation / etree files byte for byte."""
+    from oracle.oracle import Reference
+    g0 = mp.mesh_to_graph(mp.make_random_mesh(18, 23, 5))
+    kw = dict(nd_level=3, patch_size=24)
+    if case == "grid":
+        cfg, rkw, rows_out = mp.RunConfig(grid_rows=30, grid_cols=27, **kw), dict(rows=30, cols=27), 30 * 27
+    elif case in ("off", "mesh_block3"):
+        m = mp.make_random_mesh(18, 23, 5)
+        f = tmp_path / "m.off"
+        f.write_text(f"OFF\n{m.vertex_count} {len(m.triangles)} 0\n" + "0 0 0\n" * m.vertex_count
+                     + "".join(f"3 {a} {b} {c}\n" for a, b, c in m.triangles))
+        b = 3 if case == "mesh_block3" else 1
+        cfg, rkw, rows_out = mp.RunConfig(mesh_path=str(f), block_size=b, **kw), dict(mesh_path=f, block_size=b), \
+            m.vertex_count * b
+    elif case in ("matrix", "matrix_block3"):
+        b = 3 if case == "matrix_block3" else 1
+        f = tmp_path / "a.mtx"
+        _write_block_matrix(f, g0, b, drop=40 if b > 1 else 0)
+        cfg, rkw, rows_out = mp.RunConfig(matrix_path=str(f), block_size=b, **kw), dict(matrix_path=f, block_size=b), \
+            g0.n * b
+    else:
+        f = tmp_path / "p.txt"
+        r, c = np.divmod(np.arange(30 * 27), 27)
+        f.write_text("".join(f"{2 * ((rr // 6) * 5 + cc // 6)}\n" for rr, cc in zip(r, c)))
+        cfg = mp.RunConfig(grid_rows=30, grid_cols=27, patch_file=str(f), **kw)
+        rkw, rows_out = dict(rows=30, cols=27, patch_file=f), 30 * 27
+    cfg.out_perm, cfg.out_etree = str(tmp_path / "p1"), str(tmp_path / "e1")
+    run = mp.run_pipeline(cfg)
+    ref = Reference().run_pipeline(rows_out, out_perm=tmp_path / "p2", out_etree=tmp_path / "e2", **kw, **rkw)
+    assert np.array_equal(run.perm.perm, ref["perm"])
+    assert run.row.nnz_L == ref["nnz_L"] and run.row.cost == ref["cost"] and run.row.method == ref["method"]
+    assert (tmp_path / "p1").read_bytes() == (tmp_path / "p2").read_bytes()
+    assert (tmp_path / "e1").read_bytes() == (tmp_path / "e2").read_bytes()
+
+
+def test_run_pipeline_config_validation():  # pipeline_test.cpp:207-217
+    with pytest.raises(ValueError, match="exactly one input source"):
+        mp.run_pipeline(mp.RunConfig())
+    with pytest.raises(ValueError, match="exactly one input source"):
+        mp.run_pipeline(mp.RunConfig(grid_rows=4, grid_cols=4, matrix_path="whatever.mtx"))
+    with pytest.raises(ValueError, match="block size must be positive"):
+        mp.run_pipeline(mp.RunConfig(grid_rows=4, grid_cols=4, block_size=0))
