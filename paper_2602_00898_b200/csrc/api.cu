@@ -235,6 +235,7 @@ int mp_context_set_sm_share(mp_context* ctx, int32_t share) {
   return guarded([&] {
     if (!ctx) throw Error(MP_EINVAL, "null context");
     if (share < 1) throw Error(MP_EINVAL, "share must be positive");
+    if (ctx->sm_share == share) return;  // keep the sizing decided for it
     ctx->sm_share = share;
     ctx->fps_workers = 0;  // re-decided on the next call
   });
