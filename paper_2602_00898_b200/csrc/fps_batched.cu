@@ -443,6 +443,10 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
       }
       gsync();
       uint64_t mk = vkey(0, c);
+      // region size, tracked identically by every thread of the group (all
+      // inputs are group-uniform), so one barrier per level suffices: the
+      // level counters rotate over three slots (read / written / cleared)
+      int32_t wn = 1;
       for (int32_t d = 0;; ++d) {
         const int32_t nf = cnt3[d % 3];
         if (nf == 0) {
@@ -452,8 +456,8 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
         if (gt == 0) cnt3[(d + 2) % 3] = 0;
         const int32_t* fin = (d & 1) ? sf1 : sf0;
         int32_t* fout = (d & 1) ? sf0 : sf1;
-        const int32_t rbase = s_wn[sub] - nf;  // this level's vertices end the region list
-        const int32_t rtop = s_wn[sub];
+        const int32_t rbase = wn - nf;  // this level's vertices end the region list
+        const int32_t rtop = wn;
         if (gt == 0) lstart[d + 1] = rtop;  // depth d+1 entries start here
         int32_t* cout = &cnt3[(d + 1) % 3];
         const int32_t items = nf * 8;
@@ -502,17 +506,14 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
           }
         }
         gsync();
-        if (s_wn[sub] + *cout > reg_cap) {  // the region outgrew this group's list share
+        if (wn + *cout > reg_cap) {  // the region outgrew this group's list share
           if (gt == 0) s_wnlev[sub] = 0, atomicExch(&a.ctl[10], 1);
           break;
         }
-        gsync();
-        if (gt == 0) {
-          s_wn[sub] += *cout;
-          if (a.work && wk == 0) atomicAdd(&a.work[7], 1ull);
-        }
-        gsync();
+        wn += *cout;
+        if (gt == 0 && a.work && wk == 0) atomicAdd(&a.work[7], 1ull);
       }
+      if (gt == 0) s_wn[sub] = wn;
       // group max of mk
       mk = warp_max_u64(mk);
       if (lane == 0) s_red[wid] = mk;
