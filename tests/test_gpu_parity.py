@@ -703,3 +703,20 @@ def test_run_pipeline_config_validation():  # pipeline_test.cpp:207-217
         mp.run_pipeline(mp.RunConfig(grid_rows=4, grid_cols=4, matrix_path="whatever.mtx"))
     with pytest.raises(ValueError, match="block size must be positive"):
         mp.run_pipeline(mp.RunConfig(grid_rows=4, grid_cols=4, block_size=0))
+
+
+def test_cpp_adapter_with_reference_core(tmp_path):
+    """include/meshperm_b200_adapter.hpp used by the reference's own C++ code
+    (oracle/_ref/adapter_test, built from tests/cpp/adapter_main.cpp against the
+    unmodified reference core): stage outputs equal, and the reference's
+    elimination_fill / factor_etree_parents / cross_block_fill / write_etree
+    accept the GPU results unchanged."""
+    import subprocess
+    from pathlib import Path
+    exe = Path(__file__).resolve().parents[1] / "oracle" / "_ref" / "adapter_test"
+    if not exe.exists():
+        pytest.skip("adapter_test not built (needs the reference sources at build time)")
+    r = subprocess.run([str(exe), str(tmp_path)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    assert "adapter ok" in r.stdout
+    assert (tmp_path / "adapter_etree_2.txt").read_text().count("\n") == (1 << 6) - 1
