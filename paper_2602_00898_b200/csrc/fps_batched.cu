@@ -111,9 +111,60 @@ __device__ __forceinline__ uint64_t vkey(int32_t d, int32_t v) {
 }
 
 // Block-wide bitonic sort (descending) of m = power-of-two keys in smem.
+// Compare-exchange stages with a partner less than 64 elements away run in
+// registers: a warp owns 64 consecutive keys (two per lane; partners at
+// distance 1 in the same thread, 2..32 one shuffle away), so only the stages
+// with stride >= 64 go through shared memory and a block barrier (15 of the
+// 66 stages at m = 2048).
+__device__ __forceinline__ void bitonic_reg_stages(uint64_t& x0, uint64_t& x1, int32_t base, int32_t size,
+                                                   int32_t top_stride) {
+  const int lane = threadIdx.x & 31;
+  for (int32_t stride = top_stride; stride > 0; stride >>= 1) {
+    if (stride == 1) {
+      const bool desc = ((base + 2 * lane) & size) == 0;
+      const uint64_t hi = max(x0, x1), lo = min(x0, x1);
+      x0 = desc ? hi : lo;
+      x1 = desc ? lo : hi;
+    } else {
+      const int32_t pl = stride >> 1;  // partner lane distance
+      const bool lower = ((2 * lane) & stride) == 0;
+      const bool desc = ((base + 2 * lane) & size) == 0;
+      const bool keep_max = lower == desc;
+      const uint64_t y0 = __shfl_xor_sync(0xffffffffu, x0, pl), y1 = __shfl_xor_sync(0xffffffffu, x1, pl);
+      x0 = keep_max ? max(x0, y0) : min(x0, y0);
+      x1 = keep_max ? max(x1, y1) : min(x1, y1);
+    }
+  }
+}
+
 __device__ void bitonic_desc(uint64_t* s, int32_t m) {
-  for (int32_t size = 2; size <= m; size <<= 1) {
-    for (int32_t stride = size >> 1; stride > 0; stride >>= 1) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (m < 64) {  // tiny lists: plain shared-memory network
+    for (int32_t size = 2; size <= m; size <<= 1) {
+      for (int32_t stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int32_t t = threadIdx.x; t < m / 2; t += blockDim.x) {
+          const int32_t i = 2 * t - (t & (stride - 1));
+          const int32_t j = i + stride;
+          const bool up = (i & size) == 0;
+          const uint64_t x = s[i], y = s[j];
+          if ((x < y) == up) s[i] = y, s[j] = x;
+        }
+        __syncthreads();
+      }
+    }
+    return;
+  }
+  const int32_t nchunk = m >> 6;
+  // sizes 2..64: every 64-key chunk sorted in registers (alternating directions)
+  for (int32_t c = wid; c < nchunk; c += nw) {
+    const int32_t base = c << 6;
+    uint64_t x0 = s[base + 2 * lane], x1 = s[base + 2 * lane + 1];
+    for (int32_t size = 2; size <= 64; size <<= 1) bitonic_reg_stages(x0, x1, base, size, size >> 1);
+    s[base + 2 * lane] = x0, s[base + 2 * lane + 1] = x1;
+  }
+  __syncthreads();
+  for (int32_t size = 128; size <= m; size <<= 1) {
+    for (int32_t stride = size >> 1; stride >= 64; stride >>= 1) {
       for (int32_t t = threadIdx.x; t < m / 2; t += blockDim.x) {
         const int32_t i = 2 * t - (t & (stride - 1));
         const int32_t j = i + stride;
@@ -123,6 +174,13 @@ __device__ void bitonic_desc(uint64_t* s, int32_t m) {
       }
       __syncthreads();
     }
+    for (int32_t c = wid; c < nchunk; c += nw) {
+      const int32_t base = c << 6;
+      uint64_t x0 = s[base + 2 * lane], x1 = s[base + 2 * lane + 1];
+      bitonic_reg_stages(x0, x1, base, size, 32);
+      s[base + 2 * lane] = x0, s[base + 2 * lane + 1] = x1;
+    }
+    __syncthreads();
   }
 }
 
