@@ -603,26 +603,37 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
     grid.sync();
     }
     if (blockIdx.x == 0 && threadIdx.x == 0 && a.work) atomicAdd(&a.work[9], static_cast<unsigned long long>(clock64() - t_reg0));
-    // ---- 3. the walk, every CTA redundantly (exact sequential argmax semantics)
-    if (wid == 0) {
-      uint32_t U = 0;  // lane w: bits [32w, 32w+32) of the accepted-region union
-      uint64_t Mx = 0;
-      int32_t done = __ldcg(&a.ctl[0]);
-      for (int32_t j = lane; j < kMaxWorkers; j += 32) s_acc[j] = 0;
-      __syncwarp();
-      for (int32_t j = 0; j < nc; ++j) {
-        const uint32_t uw = __shfl_sync(0xffffffffu, U, j >> 5);
-        if ((uw >> (j & 31)) & 1u) continue;  // inside an accepted region: not a seed
-        if (done >= a.k || !(__ldcg(&a.ckey[j]) > Mx)) break;
-        if (lane == 0) s_acc[j] = 1;
-        if (lane < kMaskWords) U |= __ldcg(&a.inm[j * kMaskWords + lane]);
-        Mx = max(Mx, __ldcg(&a.mkey[j]));
-        if (blockIdx.x == 0 && lane == 0) a.seeds[done] = __ldcg(&a.cand[j]);
-        ++done;
+    // ---- 3. the walk, every CTA redundantly (exact sequential argmax semantics).
+    // The candidates' keys, region maxima and in-region masks are staged in
+    // shared memory by the whole CTA first (one parallel L2 round), so each
+    // accepted candidate costs shared-memory reads instead of dependent L2 loads.
+    {
+      uint64_t* s_ck = bsm;                                                   // nc keys
+      uint64_t* s_mk = bsm + kMaxWorkers;                                     // nc region maxima
+      uint32_t* s_in = reinterpret_cast<uint32_t*>(bsm + 2 * kMaxWorkers);    // nc x kMaskWords
+      for (int32_t j = threadIdx.x; j < nc; j += blockDim.x) s_ck[j] = __ldcg(&a.ckey[j]), s_mk[j] = __ldcg(&a.mkey[j]);
+      for (int32_t q = threadIdx.x; q < nc * kMaskWords; q += blockDim.x) s_in[q] = __ldcg(&a.inm[q]);
+      __syncthreads();
+      if (wid == 0) {
+        uint32_t U = 0;  // lane w: bits [32w, 32w+32) of the accepted-region union
+        uint64_t Mx = 0;
+        int32_t done = __ldcg(&a.ctl[0]);
+        for (int32_t j = lane; j < kMaxWorkers; j += 32) s_acc[j] = 0;
+        __syncwarp();
+        for (int32_t j = 0; j < nc; ++j) {
+          const uint32_t uw = __shfl_sync(0xffffffffu, U, j >> 5);
+          if ((uw >> (j & 31)) & 1u) continue;  // inside an accepted region: not a seed
+          if (done >= a.k || !(s_ck[j] > Mx)) break;
+          if (lane == 0) s_acc[j] = 1;
+          if (lane < kMaskWords) U |= s_in[j * kMaskWords + lane];
+          Mx = max(Mx, s_mk[j]);
+          if (blockIdx.x == 0 && lane == 0) a.seeds[done] = __ldcg(&a.cand[j]);
+          ++done;
+        }
+        if (lane == 0) s_done = done;
       }
-      if (lane == 0) s_done = done;
+      __syncthreads();
     }
-    __syncthreads();
     // ---- 4. commit the accepted regions
     long long t_c0 = clock64();
     if (gridmode) {
@@ -966,7 +977,10 @@ void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32
   while ((static_cast<int64_t>(n) + (1 << tile_shift) - 1) >> tile_shift > 65536) ++tile_shift;
   const int32_t ntile = static_cast<int32_t>((static_cast<int64_t>(n) + (1 << tile_shift) - 1) >> tile_shift);
   int bpsm = 0;
-  const size_t smem = sizeof(uint64_t) * kSCap + sizeof(int32_t) * kBins;
+  // candidate selection (kSCap keys + kBins histogram) or the walk's staging
+  // (keys, region maxima, in-region masks of kMaxWorkers candidates)
+  const size_t smem = std::max(sizeof(uint64_t) * kSCap + sizeof(int32_t) * kBins,
+                               sizeof(uint64_t) * 2 * kMaxWorkers + sizeof(uint32_t) * kMaxWorkers * kMaskWords);
   allow_max_smem(fps_batched_kernel, ctx.device);
   MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, fps_batched_kernel, kThreads, smem));
   if (bpsm < 1) throw Error(MP_ECUDA, "fps_batched_kernel does not fit on an SM");
