@@ -295,6 +295,9 @@ __global__ void __launch_bounds__(kMdThreads) md_fast_kernel(MdArgs a) {
   int32_t* st = bsz + nv;
   int32_t* loff = st + nv;  // CSR offset of each local vertex (its list slots)
   uint32_t* dirty = reinterpret_cast<uint32_t*>(loff + nv);  // nb bits
+  // this pivot's reach (local ids < kMdFastCap fit 16 bits), read back by the
+  // member updates without a trip through the global pool
+  int16_t* sreach = reinterpret_cast<int16_t*>(dirty + (nb + 31) / 32 + 1);
   __shared__ int32_t s_nbc[2], s_cursor, s_half, s_dcnt;
   __shared__ int32_t s_dlist[kMdThreads];  // dirty blocks of this pivot (<= reach + 1 distinct)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
@@ -374,7 +377,11 @@ __global__ void __launch_bounds__(kMdThreads) md_fast_kernel(MdArgs a) {
     const int32_t* pel = a.el + po;
     for (int32_t i = threadIdx.x; i < np_adj; i += blockDim.x) {
       const int32_t w = padj[i];
-      if (atomicExch(&mark[w], tok) != tok) out[atomicAdd(cnt, 1)] = w;
+      if (atomicExch(&mark[w], tok) != tok) {
+        const int32_t at = atomicAdd(cnt, 1);
+        out[at] = w;
+        sreach[at] = static_cast<int16_t>(w);
+      }
     }
     for (int32_t ei = 0; ei < np_el; ++ei) {
       const int32_t e = pel[ei];
@@ -382,7 +389,11 @@ __global__ void __launch_bounds__(kMdThreads) md_fast_kernel(MdArgs a) {
       const int32_t sz = bsz[e];
       for (int32_t i = threadIdx.x; i < sz; i += blockDim.x) {
         const int32_t w = bd[i];
-        if (w != p && atomicExch(&mark[w], tok) != tok) out[atomicAdd(cnt, 1)] = w;
+        if (w != p && atomicExch(&mark[w], tok) != tok) {
+          const int32_t at = atomicAdd(cnt, 1);
+          out[at] = w;
+          sreach[at] = static_cast<int16_t>(w);
+        }
       }
     }
     // absorbed elements get the pivot's token (element ids are dead vertices,
@@ -401,7 +412,7 @@ __global__ void __launch_bounds__(kMdThreads) md_fast_kernel(MdArgs a) {
     const int32_t nbd = *cnt;
     // ---- member updates (elimination.cpp:75-83) and their approx degrees
     for (int32_t i = threadIdx.x; i < nbd; i += blockDim.x) {
-      const int32_t w = out[i];
+      const int32_t w = sreach[i];
       const int32_t o = loff[w];
       const int32_t wst = st[w];
       int32_t* wa = a.adj + o;
@@ -534,7 +545,8 @@ void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t L, const int
     for (int32_t i = 0; i < nn; ++i) maxnv = std::max(maxnv, hoff[i + 1] - hoff[i]);
     const int32_t fast_nv = std::min(maxnv, kMdFastCap);
     const int32_t fnb = (fast_nv + 31) / 32;
-    const size_t fsmem = sizeof(uint64_t) * fnb + sizeof(int32_t) * 5 * fast_nv + sizeof(uint32_t) * ((fnb + 31) / 32 + 1);
+    const size_t fsmem = sizeof(uint64_t) * fnb + sizeof(int32_t) * 5 * fast_nv + sizeof(uint32_t) * ((fnb + 31) / 32 + 1) +
+                         sizeof(int16_t) * (fast_nv + 2);
     allow_max_smem(md_fast_kernel, ctx.device);
     MP_KERNEL(ctx, md_fast_kernel<<<nn, kMdThreads, fsmem, s>>>(a));
     int32_t h_flag = 0;
