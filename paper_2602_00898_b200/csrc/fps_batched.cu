@@ -186,7 +186,7 @@ __device__ void bitonic_desc(uint64_t* s, int32_t m) {
 
 // Leader: the downward-closed candidate list of this batch.
 __device__ void select_candidates(const BatchArgs& a, int32_t W, uint64_t* sS, int32_t* hist, int32_t* shi) {
-  __shared__ int32_t s_n, s_thr;
+  __shared__ int32_t s_n, s_thr, s_gq, s_gs;
   int32_t* ssub = hist;                   // subtile list (reuses the histogram, kBins >= kSCap)
   __shared__ int32_t scnt[kMaxWorkers];   // exact mode: per-subtile counts / offsets
   __shared__ uint64_t red[32];
@@ -250,38 +250,76 @@ __device__ void select_candidates(const BatchArgs& a, int32_t W, uint64_t* sS, i
   for (int pass = 0; pass < 2; ++pass) {
     const bool ex = exact;
     int32_t* tl = a.tscratch;
-    int32_t nq = 0;
-    for (int32_t t0 = 0; t0 < a.ntile; t0 += blockDim.x) {
-      const int32_t t = t0 + threadIdx.x;
-      int32_t f = 0;
-      if (t < a.ntile) {
-        const int64_t td = static_cast<int64_t>(__ldcg(&a.tkey[t]) >> 32);
-        f = ex ? td == thr_d : td >= thr_d;
-      }
-      int32_t tt;
-      const int32_t e = block_excl_scan(f, shi, &tt);
-      if (f) tl[nq + e] = t;
-      nq += tt;
-    }
-    __syncthreads();
-    // qualifying subtiles, in order (capacity: kSCap; exact mode needs only W)
     const int32_t spt = tsize >> 5;  // subtiles per tile
     const int32_t cap_sub = ex ? min(W, kSCap) : kSCap;
-    int32_t nsub = 0;
-    for (int64_t q0 = 0; q0 < static_cast<int64_t>(nq) * spt && nsub < cap_sub; q0 += blockDim.x) {
-      const int64_t q = q0 + threadIdx.x;
-      int32_t f = 0, sub = 0;
-      if (q < static_cast<int64_t>(nq) * spt) {
-        sub = __ldcg(&tl[q / spt]) * spt + static_cast<int32_t>(q % spt);
-        if ((static_cast<int64_t>(sub) << 5) < a.n) {
-          const int64_t sd = __ldcg(&a.smax[sub]);
-          f = ex ? sd == thr_d : sd >= thr_d;
+    int32_t nq = 0, nsub = 0;
+    if (!ex) {
+      // every vertex above the threshold is taken and the list is sorted by
+      // key afterwards, so tiles and subtiles are gathered unordered: shared
+      // counters, kG items per thread with their loads in flight together
+      constexpr int kG = 4;
+      if (threadIdx.x == 0) s_gq = 0, s_gs = 0;
+      __syncthreads();
+      for (int32_t t0 = threadIdx.x; t0 < a.ntile; t0 += kG * blockDim.x) {
+        uint64_t tk[kG];
+#pragma unroll
+        for (int g = 0; g < kG; ++g) {
+          const int32_t t = t0 + g * blockDim.x;
+          tk[g] = t < a.ntile ? __ldcg(&a.tkey[t]) : 0;
+        }
+#pragma unroll
+        for (int g = 0; g < kG; ++g) {
+          const int32_t t = t0 + g * blockDim.x;
+          if (t < a.ntile && static_cast<int64_t>(tk[g] >> 32) >= thr_d) tl[atomicAdd(&s_gq, 1)] = t;
         }
       }
-      int32_t tt;
-      const int32_t e = block_excl_scan(f, shi, &tt);
-      if (f && nsub + e < cap_sub) ssub[nsub + e] = sub;
-      nsub += tt;
+      __syncthreads();
+      nq = s_gq;
+      const int64_t total = static_cast<int64_t>(nq) * spt;
+      for (int64_t q0 = threadIdx.x; q0 < total; q0 += kG * blockDim.x) {
+        int32_t sub[kG];
+        int64_t sd[kG];
+#pragma unroll
+        for (int g = 0; g < kG; ++g) {
+          const int64_t q = q0 + static_cast<int64_t>(g) * blockDim.x;
+          sub[g] = q < total ? __ldcg(&tl[q / spt]) * spt + static_cast<int32_t>(q % spt) : -1;
+        }
+#pragma unroll
+        for (int g = 0; g < kG; ++g)
+          sd[g] = sub[g] >= 0 && (static_cast<int64_t>(sub[g]) << 5) < a.n ? static_cast<int64_t>(__ldcg(&a.smax[sub[g]])) : -1;
+#pragma unroll
+        for (int g = 0; g < kG; ++g)
+          if (sd[g] >= thr_d && sd[g] >= 0) {
+            const int32_t at = atomicAdd(&s_gs, 1);
+            if (at < cap_sub) ssub[at] = sub[g];
+          }
+      }
+      __syncthreads();
+      nsub = s_gs;
+    } else {
+      for (int32_t t0 = 0; t0 < a.ntile; t0 += blockDim.x) {
+        const int32_t t = t0 + threadIdx.x;
+        int32_t f = 0;
+        if (t < a.ntile) f = static_cast<int64_t>(__ldcg(&a.tkey[t]) >> 32) == thr_d;
+        int32_t tt;
+        const int32_t e = block_excl_scan(f, shi, &tt);
+        if (f) tl[nq + e] = t;
+        nq += tt;
+      }
+      __syncthreads();
+      // qualifying subtiles, in id order (exact mode truncates ties by id)
+      for (int64_t q0 = 0; q0 < static_cast<int64_t>(nq) * spt && nsub < cap_sub; q0 += blockDim.x) {
+        const int64_t q = q0 + threadIdx.x;
+        int32_t f = 0, sub = 0;
+        if (q < static_cast<int64_t>(nq) * spt) {
+          sub = __ldcg(&tl[q / spt]) * spt + static_cast<int32_t>(q % spt);
+          if ((static_cast<int64_t>(sub) << 5) < a.n) f = static_cast<int64_t>(__ldcg(&a.smax[sub])) == thr_d;
+        }
+        int32_t tt;
+        const int32_t e = block_excl_scan(f, shi, &tt);
+        if (f && nsub + e < cap_sub) ssub[nsub + e] = sub;
+        nsub += tt;
+      }
     }
     if (!ex && nsub > cap_sub) {  // more than kSCap candidates: the exact-max rule instead
       __syncthreads();
