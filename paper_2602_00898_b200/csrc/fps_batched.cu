@@ -965,12 +965,22 @@ __global__ void __launch_bounds__(kThreads, 1) fps_cluster_phase(BatchArgs a, in
         const int32_t t = __ldcg(&a.tlist[i]);
         uint64_t best = 0;
         const int32_t lo = t * tsize, hi = min(a.n, lo + tsize);
-        for (int32_t v0 = lo; v0 < hi; v0 += 32) {
-          const int32_t v = v0 + lane;
-          const int32_t dv = v < hi ? __ldcg(&a.dist[v]) : -1;
-          if (v < hi) best = max(best, vkey(dv, v));
-          const int32_t sm = __reduce_max_sync(0xffffffffu, dv);
-          if (lane == 0) a.smax[v0 >> 5] = sm;
+        // eight 32-vertex subtiles per step, their loads in flight together
+        for (int32_t b0 = lo; b0 < hi; b0 += 8 * 32) {
+          int32_t dv[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int32_t v = b0 + 32 * q + lane;
+            dv[q] = v < hi ? __ldcg(&a.dist[v]) : -1;
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int32_t v0 = b0 + 32 * q;
+            if (v0 >= hi) break;
+            if (v0 + lane < hi) best = max(best, vkey(dv[q], v0 + lane));
+            const int32_t sm = __reduce_max_sync(0xffffffffu, dv[q]);
+            if (lane == 0) a.smax[v0 >> 5] = sm;
+          }
         }
         best = warp_max_u64(best);
         if (lane == 0) {
