@@ -720,3 +720,20 @@ def test_cpp_adapter_with_reference_core(tmp_path):
     assert r.returncode == 0, r.stderr
     assert "adapter ok" in r.stdout
     assert (tmp_path / "adapter_etree_2.txt").read_text().count("\n") == (1 << 6) - 1
+
+
+def test_run_pipeline_row_fields(tmp_path):
+    """BenchRow fields of run_pipeline (pipeline.cpp:88-98, :147-152): input id
+    override, collect_timing=False zeroes the stage times, the row writes as
+    one CSV line."""
+    cfg = mp.RunConfig(grid_rows=12, grid_cols=9, patch_size=8, nd_level=2, input_id="tiny", collect_timing=False)
+    run = mp.run_pipeline(cfg)
+    r = run.row
+    assert r.input == "tiny" and r.n == 108 and r.method == "ours-8" and r.nd_level == 2
+    assert (r.t_patch_ms, r.t_quotient_ms, r.t_etree_ms, r.t_local_ms, r.t_assemble_ms) == (0, 0, 0, 0, 0)
+    assert r.nnz_A == 108 + int(mp.mesh_to_graph(mp.make_grid_mesh(12, 9)).offsets[-1])
+    mp.write_csv([r], tmp_path / "r.csv")
+    line = (tmp_path / "r.csv").read_text().splitlines()[1]
+    assert line.startswith("tiny,108,") and ",ours-8,8,2,0.000,0.000,0.000,0.000,0.000," in line
+    assert mp.default_input_id(mp.RunConfig(mesh_path="/a/b/mesh.off")) == "mesh.off"
+    assert mp.default_input_id(mp.RunConfig(grid_rows=3, grid_cols=4)) == "grid-3x4"
