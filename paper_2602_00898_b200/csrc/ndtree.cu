@@ -357,11 +357,14 @@ __device__ __forceinline__ void fm_refill(int32_t t, int32_t np, G gain, W st, K
   __syncthreads();
 }
 
-// One node's bipartition.  SM: the patch state and the packed adjacency
-// (local id << 16 | weight) live in shared memory; otherwise in global
-// scratch (plist layout) with the adjacency read from qloc / qw.
-template <class K, bool EXACT, bool SM>
+// One node's bipartition.  SM: the patch state (20 B per patch) lives in
+// shared memory, else in global scratch (plist layout).  SMA: the packed
+// adjacency (local id << 16 | weight) is in shared memory too, else it is
+// read from qloc / qw (read-only, L2) -- the middle case keeps nodes whose
+// adjacency does not fit (C5 root) on shared-memory state.
+template <class K, bool EXACT, bool SM, bool SMA = SM>
 __device__ __forceinline__ void fm_node(const LevelArgs& a, int32_t li, int32_t pbeg, int32_t np) {
+  static_assert(SM || !SMA, "packed adjacency in shared memory needs the shared state layout");
   const int32_t* pl = a.plist + pbeg;
   int32_t* fifo = a.fm_fifo + a.fm_fifo_off[li];
   int32_t* moves = a.fm_moves + pbeg;
@@ -377,7 +380,7 @@ __device__ __forceinline__ void fm_node(const LevelArgs& a, int32_t li, int32_t 
     gain = w + np;
     abe = reinterpret_cast<int2*>(base + 8LL * np);
     st = reinterpret_cast<uint32_t*>(base + 16LL * np);
-    packed = reinterpret_cast<uint32_t*>(base + ((20LL * np + 15) & ~15LL));
+    if constexpr (SMA) packed = reinterpret_cast<uint32_t*>(base + ((20LL * np + 15) & ~15LL));
   } else {
     w = a.fm_w + pbeg;
     gain = a.fm_gain + pbeg;
@@ -388,11 +391,11 @@ __device__ __forceinline__ void fm_node(const LevelArgs& a, int32_t li, int32_t 
   auto side = [&](int32_t i) -> uint32_t { return stb[4 * i]; };
   auto flag = [&](int32_t i) -> uint32_t { return stb[4 * i + 1]; };
   auto A_nb = [&](int32_t j) -> int32_t {
-    if constexpr (SM) return static_cast<int32_t>(packed[j] >> 16);
+    if constexpr (SMA) return static_cast<int32_t>(packed[j] >> 16);
     else return __ldg(&a.qloc[j]);
   };
   auto A_w = [&](int32_t j) -> int32_t {
-    if constexpr (SM) return static_cast<int32_t>(packed[j] & 0xffffu);
+    if constexpr (SMA) return static_cast<int32_t>(packed[j] & 0xffffu);
     else return __ldg(&a.qw[j]);
   };
 
@@ -413,7 +416,7 @@ __device__ __forceinline__ void fm_node(const LevelArgs& a, int32_t li, int32_t 
     tot += w[i];
   }
   tot = block_sum_i64(tot, reinterpret_cast<int64_t*>(red));
-  if constexpr (SM) {  // node-local packed adjacency
+  if constexpr (SMA) {  // node-local packed adjacency
     int32_t run = 0;
     for (int32_t i0 = 0; i0 < np; i0 += blockDim.x) {
       const int32_t i = i0 + threadIdx.x;
@@ -697,7 +700,10 @@ __host__ __device__ inline int64_t fm_node_smem(int64_t np, int64_t entries) {
 // EXACT: integer feasibility (n < 2^26).  32-bit keys imply < 65536 patches
 // and edge weights < 32768, so a node whose state fits uses the packed
 // shared-memory layout; 64-bit-key nodes always use the global layout.
-template <class K, bool EXACT>
+// HYB: the level has a node whose adjacency does not fit but whose state
+// does (a separate instantiation, so levels without one keep the smaller
+// kernel).
+template <class K, bool EXACT, bool HYB = false>
 __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
   const int32_t li = blockIdx.x;
   if (!a.active[li]) return;
@@ -707,6 +713,12 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
     if (fm_node_smem(np, e_node) <= a.fm_smem_bytes) {
       fm_node<K, EXACT, true>(a, li, pbeg, np);
       return;
+    }
+    if constexpr (HYB) {
+      if (fm_node_smem(np, 0) <= a.fm_smem_bytes) {  // state only; adjacency from L2
+        fm_node<K, EXACT, true, false>(a, li, pbeg, np);
+        return;
+      }
     }
   }
   fm_node<K, EXACT, false>(a, li, pbeg, np);
@@ -1458,6 +1470,7 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     if (U > 0) MP_KERNEL(ctx, local_adjacency<<<grid_for(ctx, U), 256, 0, s>>>(static_cast<int32_t>(U), qnbr, lidx, qloc));
     a.qloc = qloc;
     size_t fm_smem = 1024;
+    bool fm_hybrid = false;  // a node whose state fits shared memory but whose adjacency does not
     {
       // room for the packed adjacency of the largest node that fits
       std::vector<int64_t> hfo(width + 1);
@@ -1465,18 +1478,22 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
       MP_CUDA(cudaMemcpyAsync(hfo.data(), fifo_off.get(), sizeof(int64_t) * (width + 1), cudaMemcpyDeviceToHost, s));
       MP_CUDA(cudaMemcpyAsync(hpo.data(), poff.get(), sizeof(int32_t) * (width + 1), cudaMemcpyDeviceToHost, s));
       MP_CUDA(cudaStreamSynchronize(s));
-      size_t need = 0;
+      size_t need = 0, need_state = 0;
       for (int32_t i = 0; i < width; ++i) {
         const int64_t np_i = hpo[i + 1] - hpo[i];
         if (np_i == 0) continue;
         need = std::max<size_t>(need, static_cast<size_t>(fm_node_smem(np_i, (hfo[i + 1] - hfo[i]) - np_i)));
+        need_state = std::max<size_t>(need_state, static_cast<size_t>(fm_node_smem(np_i, 0)));
       }
       // opt-in limit minus the kernels' static shared memory
-      cudaFuncAttributes fa32{}, fa64{};
+      cudaFuncAttributes fa32{}, fa64{}, fah{};
       MP_CUDA(cudaFuncGetAttributes(&fa32, fm_kernel<uint32_t, true>));
       MP_CUDA(cudaFuncGetAttributes(&fa64, fm_kernel<uint64_t, false>));
-      const size_t cap = static_cast<size_t>(ctx.smem_optin) - std::max(fa32.sharedSizeBytes, fa64.sharedSizeBytes);
+      MP_CUDA(cudaFuncGetAttributes(&fah, fm_kernel<uint32_t, true, true>));
+      const size_t cap = static_cast<size_t>(ctx.smem_optin) -
+                         std::max({fa32.sharedSizeBytes, fa64.sharedSizeBytes, fah.sharedSizeBytes});
       fm_smem = std::min<size_t>(std::max(fm_smem, need), cap);
+      fm_hybrid = need > cap && need_state <= cap;
     }
     a.fm_smem_bytes = static_cast<int64_t>(fm_smem);
     // 32-bit move keys when every node fits (patch count and gain range)
@@ -1496,7 +1513,8 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
       MP_KERNEL(ctx, kernel<<<width, kFmThreads, fm_smem, s>>>(a));
       ctx.ktime_end(kt__);
     };
-    if (k32) exact ? launch_fm(fm_kernel<uint32_t, true>) : launch_fm(fm_kernel<uint32_t, false>);
+    if (k32 && fm_hybrid) exact ? launch_fm(fm_kernel<uint32_t, true, true>) : launch_fm(fm_kernel<uint32_t, false, true>);
+    else if (k32) exact ? launch_fm(fm_kernel<uint32_t, true>) : launch_fm(fm_kernel<uint32_t, false>);
     else exact ? launch_fm(fm_kernel<uint64_t, true>) : launch_fm(fm_kernel<uint64_t, false>);
     st.mark("level/fm");
     MP_KERNEL(ctx, super_pass<<<lgrid, 256, 0, s>>>(a));

@@ -317,6 +317,21 @@ def _batch_with_bad(good, ctxs):
         assert np.array_equal(preps[2][0]["perm"][:good.n], ref.perm.perm)
 
 
+@pytest.mark.parametrize("rows,patch", [(200, 5), (170, 4)])
+def test_fm_state_in_smem_adjacency_in_l2(rows, patch):
+    """Root quotients of ~7-8K patches (C5's root has 7,805): the per-patch FM
+    state fits shared memory but the packed adjacency does not, so FM runs
+    with state in shared memory and adjacency from L2."""
+    from oracle.oracle import Reference
+    g = mp.mesh_to_graph(mp.make_grid_mesh(rows, rows))
+    o = Reference().order(g, patch_size=patch, nd_level=2)
+    res = mp.order(g, patch_size=patch, nd_level=2)
+    assert 5500 < o["patch_count"] < 10240 and res.patch.patch_count == o["patch_count"]
+    assert np.array_equal(res.tree.node_offsets, o["node_offsets"])
+    assert np.array_equal(res.tree.vertices, o["node_vertices"])
+    assert np.array_equal(res.perm.perm, o["perm"])
+
+
 @pytest.mark.parametrize("rows,patch", [(240, 4), (150, 2)])
 def test_fm_large_nodes_global_state(rows, patch):
     """Root quotients beyond the shared-memory FM capacity (>10,240 patches,
