@@ -70,6 +70,12 @@ typedef struct {
    * enforce_connectivity before the ND tree. */
   const int32_t* user_patches;
   int32_t user_patch_count;
+  /* compute_perm(tree, g, schedule) with an arbitrary node sequence
+   * (assemble.hpp:37): NULL = the `schedule` enum; else schedule_len host
+   * ints, validated like validate_schedule (MP_EINVAL "invalid schedule at
+   * position N", assemble.cpp:71-72). */
+  const int32_t* schedule_nodes;
+  int64_t schedule_len;
 } mp_config;
 
 /* PipelineResult (pipeline.hpp:56-61) flattened.  Array pointers may be
@@ -128,7 +134,9 @@ int mp_order(mp_context* ctx, const mp_csr* g, const mp_config* cfg, mp_result* 
  * mp_order(ctx, &graphs[f], &cfgs[f], &results[f]) on one of the nctx contexts
  * (one host thread each, all on their own streams, sm_share = nctx for the
  * call).  status[f] (optional) gets each frame's code; the return value is the
- * code of the lowest failing frame, its message prefixed "frame f: ". */
+ * code of the lowest failing frame, its message prefixed "frame f: ".  The
+ * contexts must be distinct (MP_EINVAL otherwise): a context is never used by
+ * two host threads at once. */
 int mp_order_batch(mp_context* const* ctxs, int32_t nctx, int32_t count, const mp_csr* graphs,
                    const mp_config* cfgs, mp_result* results, int32_t* status);
 
@@ -184,6 +192,16 @@ int mp_compute_perm(mp_context* ctx, int32_t n, int32_t nd_level, const int32_t*
                     const int32_t* node_vertices, const int32_t* local_perm, int32_t schedule,
                     int32_t* perm, int32_t* inverse, int32_t on_device);
 
+/* assemble.hpp:35 validate_schedule: *first_violation = the first position
+ * that lists a node out of range, twice, or before one of its children (a
+ * short sequence reports `length`), or -1 when the sequence is valid. */
+int mp_validate_schedule(int32_t nd_level, const int32_t* sequence, int64_t length, int64_t* first_violation);
+/* assemble.hpp:37 compute_perm(tree, g, schedule) with any valid node
+ * sequence (schedule_nodes: schedule_len host ints). */
+int mp_compute_perm_schedule(mp_context* ctx, int32_t n, int32_t nd_level, const int32_t* node_offsets,
+                             const int32_t* node_vertices, const int32_t* local_perm, const int32_t* schedule_nodes,
+                             int64_t schedule_len, int32_t* perm, int32_t* inverse, int32_t on_device);
+
 /* symbolic.hpp:23 elimination_fill + :31 factor_etree_parents for a
  * permutation produced from an ND tree (perm = compute_perm(tree, ...)).
  * Requires the tree because the device game runs subtree by subtree. */
@@ -191,6 +209,27 @@ int mp_tree_fill(mp_context* ctx, const mp_csr* g, int32_t nd_level, const int32
                  const int32_t* node_vertices, const int32_t* local_perm, int32_t schedule,
                  int64_t* column_counts, int32_t* etree_parent, int32_t on_device,
                  int64_t* nnz_A, int64_t* nnz_L, int64_t* cost, double* fill_ratio);
+/* The same for compute_perm(tree, g, schedule) with any valid node sequence. */
+int mp_tree_fill_schedule(mp_context* ctx, const mp_csr* g, int32_t nd_level, const int32_t* node_offsets,
+                          const int32_t* node_vertices, const int32_t* local_perm, const int32_t* schedule_nodes,
+                          int64_t schedule_len, int64_t* column_counts, int32_t* etree_parent, int32_t on_device,
+                          int64_t* nnz_A, int64_t* nnz_L, int64_t* cost, double* fill_ratio);
+
+/* symbolic.hpp:23 elimination_fill + :31 factor_etree_parents for ANY
+ * permutation perm[n] (new position -> old index; host or device per
+ * on_device): the elimination game played on the device in permutation order
+ * (one CTA; the ND-structured mp_tree_fill is the fast path for ND trees).
+ * MP_EINVAL "permutation is not a bijection" as symbolic.cpp:16-18. */
+int mp_elimination_fill(mp_context* ctx, const mp_csr* g, const int32_t* perm, int64_t* column_counts,
+                        int32_t* etree_parent, int32_t on_device, int64_t* nnz_A, int64_t* nnz_L, int64_t* cost,
+                        double* fill_ratio);
+/* symbolic.hpp:37 cross_block_fill(g, perm, tree): the number of factor
+ * entries joining vertices whose tree nodes are neither equal nor ancestor-
+ * related, for any permutation and tree (the exact value; the pipeline's
+ * self-check only needs zero / non-zero, see mp_tree_separation_check). */
+int mp_cross_block_fill(mp_context* ctx, const mp_csr* g, const int32_t* perm, int32_t nd_level,
+                        const int32_t* node_offsets, const int32_t* node_vertices, int32_t on_device,
+                        int64_t* crossing);
 
 /* ---- synthetic inputs and host CSR build (outside the timed path) ---- */
 int64_t mp_grid_mesh_triangles(int32_t rows, int32_t cols);

@@ -191,6 +191,18 @@ class Reference(_Base):
                                              C.byref(nnz)))
         return off, nbr
 
+    def make_grid_mesh(self, rows, cols):
+        """pipeline.cpp:38-55 -> (T, 3) int32 triangles."""
+        tris = np.zeros((max(2 * (rows - 1) * (cols - 1), 1), 3), np.int32)
+        self._check(self._f("make_grid_mesh")(C.c_int32(rows), C.c_int32(cols), _p(tris)))
+        return tris[:2 * (rows - 1) * (cols - 1)]
+
+    def random_mesh(self, rows, cols, seed):
+        """tests/test_support.hpp:66-86 mtest::random_mesh -> (T, 3) int32 triangles."""
+        tris = np.zeros((max(2 * (rows - 1) * (cols - 1), 1), 3), np.int32)
+        self._check(self._f("random_mesh")(C.c_int32(rows), C.c_int32(cols), C.c_uint64(seed), _p(tris)))
+        return tris[:2 * (rows - 1) * (cols - 1)]
+
     def pattern_to_graph(self, n, rows, cols, block_size=1):
         """graph.cpp:53-61 build_graph / :77-94 compress_blocks."""
         rows, cols = _i32(rows), _i32(cols)
@@ -291,6 +303,22 @@ class Reference(_Base):
                                                 _p(_i32(perm)), C.c_int32(nd_level), _p(_i32(node_offsets)),
                                                 _p(_i32(node_vertices)), C.byref(c)))
         return int(c.value)
+
+    def compute_perm_schedule(self, g, nd_level, node_offsets, node_vertices, local_perm, schedule):
+        """assemble.cpp:65-85 compute_perm(tree, g, schedule) with any node sequence."""
+        pm, inv = np.zeros(max(g.n, 1), np.int32), np.zeros(max(g.n, 1), np.int32)
+        sched = _i32(schedule)
+        self._check(self._f("compute_perm_schedule")(
+            C.c_int32(g.n), _p(_i32(g.offsets)), _p(_i32(g.neighbors)), C.c_int32(nd_level), _p(_i32(node_offsets)),
+            _p(_i32(node_vertices)), _p(_i32(local_perm)), _p(sched), C.c_int64(len(sched)), _p(pm), _p(inv)))
+        return pm[:g.n], inv[:g.n]
+
+    def validate_schedule(self, nd_level, sequence):
+        """assemble.cpp:48-63: first violating position or None."""
+        seq = _i32(sequence)
+        bad = C.c_int64()
+        self._check(self._f("validate_schedule")(C.c_int32(nd_level), _p(seq), C.c_int64(len(seq)), C.byref(bad)))
+        return None if bad.value < 0 else bad.value
 
     def order_timed(self, g, patch_size=256, nd_level=-1, seed=0, mode=0, levelorder=0, threads=1):
         """ref_order: run_pipeline's ordering stages with time_stage timers (ms per stage)."""

@@ -27,6 +27,7 @@
 #include "meshperm/pipeline.hpp"
 #include "meshperm/quotient.hpp"
 #include "meshperm/symbolic.hpp"
+#include "test_support.hpp"  // the reference test suite's generators (tests/)
 
 using namespace meshperm;
 
@@ -146,6 +147,16 @@ int ref_make_grid_mesh(int32_t rows, int32_t cols, int32_t* tris_out) {
   });
 }
 
+// tests/test_support.hpp:66-86 mtest::random_mesh (the reference's own
+// generator: std::mt19937_64 picks each cell's diagonal).
+int ref_random_mesh(int32_t rows, int32_t cols, uint64_t seed, int32_t* tris_out) {
+  return guarded([&] {
+    TriangleMesh m = mtest::random_mesh(rows, cols, seed);
+    for (std::size_t t = 0; t < m.triangles.size(); ++t)
+      for (int c = 0; c < 3; ++c) tris_out[3 * t + c] = m.triangles[t][c];
+  });
+}
+
 // etree.cpp:42-46
 int32_t ref_default_nd_level(int32_t n) { return default_nd_level(n); }
 
@@ -244,6 +255,33 @@ int ref_compute_perm(int32_t n, const int32_t* off, const int32_t* nbr, int32_t 
     Permutation p = compute_perm(t, g, s);
     std::memcpy(perm, p.perm.data(), sizeof(int32_t) * n);
     std::memcpy(inverse, p.inverse.data(), sizeof(int32_t) * n);
+  });
+}
+
+// assemble.cpp:65-85 compute_perm with a caller schedule (any node sequence;
+// invalid ones throw from validate_schedule).
+int ref_compute_perm_schedule(int32_t n, const int32_t* off, const int32_t* nbr, int32_t nd_level,
+                              const int32_t* node_offsets, const int32_t* node_vertices,
+                              const int32_t* local_perm, const int32_t* sched, int64_t len, int32_t* perm,
+                              int32_t* inverse) {
+  return guarded([&] {
+    AdjacencyGraph g = make_graph(n, off, nbr);
+    EliminationTree t = unflatten_tree(n, nd_level, node_offsets, node_vertices, local_perm);
+    Schedule s(sched, sched + len);
+    Permutation p = compute_perm(t, g, s);
+    std::memcpy(perm, p.perm.data(), sizeof(int32_t) * n);
+    std::memcpy(inverse, p.inverse.data(), sizeof(int32_t) * n);
+  });
+}
+
+// assemble.cpp:48-63 validate_schedule: *bad = first violation or -1.
+int ref_validate_schedule(int32_t nd_level, const int32_t* seq, int64_t len, int64_t* bad) {
+  return guarded([&] {
+    EliminationTree t;
+    t.nd_level = nd_level;
+    t.nodes.resize((std::size_t{1} << (nd_level + 1)) - 1);
+    auto r = validate_schedule(t, std::span<const index_t>(seq, static_cast<std::size_t>(len)));
+    *bad = r ? static_cast<int64_t>(*r) : -1;
   });
 }
 

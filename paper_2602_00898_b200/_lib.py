@@ -33,6 +33,8 @@ class MpConfig(C.Structure):
         ("want_fill", C.c_int32),
         ("user_patches", C.c_void_p),
         ("user_patch_count", C.c_int32),
+        ("schedule_nodes", C.c_void_p),
+        ("schedule_len", C.c_int64),
     ]
 
 
@@ -113,6 +115,18 @@ SIGNATURES = [
     ("mp_tree_fill", C.c_int,
      [C.c_void_p, C.POINTER(MpCsr), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p,
       C.c_void_p, C.c_int32, i64p, i64p, i64p, C.POINTER(C.c_double)]),
+    ("mp_validate_schedule", C.c_int, [C.c_int32, C.c_void_p, C.c_int64, i64p]),
+    ("mp_compute_perm_schedule", C.c_int,
+     [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+      C.c_void_p, C.c_int32]),
+    ("mp_tree_fill_schedule", C.c_int,
+     [C.c_void_p, C.POINTER(MpCsr), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+      C.c_void_p, C.c_void_p, C.c_int32, i64p, i64p, i64p, C.POINTER(C.c_double)]),
+    ("mp_elimination_fill", C.c_int,
+     [C.c_void_p, C.POINTER(MpCsr), C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, i64p, i64p, i64p,
+      C.POINTER(C.c_double)]),
+    ("mp_cross_block_fill", C.c_int,
+     [C.c_void_p, C.POINTER(MpCsr), C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, i64p]),
     ("mp_grid_mesh_triangles", C.c_int64, [C.c_int32, C.c_int32]),
     ("mp_make_grid_mesh", C.c_int, [C.c_int32, C.c_int32, C.c_void_p]),
     ("mp_make_random_mesh", C.c_int, [C.c_int32, C.c_int32, C.c_uint64, C.c_void_p]),

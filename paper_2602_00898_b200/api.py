@@ -378,8 +378,53 @@ def order_subtrees(tree: EliminationTree, g: AdjacencyGraph, node_mask, local_pe
                                   LOCAL_MODES[mode], SCHEDULES[schedule], _ptr(mask), _ptr(local_perm), _ptr(perm), 0))
 
 
-def compute_perm(tree: EliminationTree, g: AdjacencyGraph, schedule: str = "postorder",
+def _schedule_nodes(tree: EliminationTree, schedule) -> np.ndarray:
+    """A named schedule (schedule_postorder / schedule_levelorder,
+    assemble.hpp:25-29) or any node sequence, as int32 node ids."""
+    if isinstance(schedule, str):
+        if schedule not in SCHEDULES:
+            raise ValueError("unknown schedule: " + schedule)
+        return _i32(schedule_nodes(tree.nd_level, schedule))
+    return _i32(schedule)
+
+
+def _nonempty(a: np.ndarray) -> np.ndarray:
+    return a if a.size else np.zeros(1, np.int32)
+
+
+def schedule_nodes(nd_level: int, kind: str = "postorder") -> list[int]:
+    """schedule_postorder (left, right, node) / schedule_levelorder (deepest
+    level first), assemble.cpp:24-46."""
+    nn = (1 << (nd_level + 1)) - 1
+    if kind == "levelorder":
+        return [i for lev in range(nd_level, -1, -1) for i in range((1 << lev) - 1, (1 << (lev + 1)) - 1)]
+    out, st = [], [(0, 0)]
+    while st:
+        i, state = st.pop()
+        if i >= nn:
+            continue
+        if state == 0:
+            st += [(i, 1), (2 * i + 1, 0)]
+        elif state == 1:
+            st += [(i, 2), (2 * i + 2, 0)]
+        else:
+            out.append(i)
+    return out
+
+
+def validate_schedule(tree: EliminationTree, sequence) -> int | None:
+    """assemble.hpp:35 validate_schedule: the first violating position, or None."""
+    seq = _i32(sequence)
+    bad = C.c_int64()
+    check(lib().mp_validate_schedule(tree.nd_level, C.c_void_p(_nonempty(seq).ctypes.data), len(seq), C.byref(bad)))
+    return None if bad.value < 0 else int(bad.value)
+
+
+def compute_perm(tree: EliminationTree, g: AdjacencyGraph, schedule="postorder",
                  ctx: Context | None = None) -> Permutation:  # assemble.hpp:25-38
+    """compute_perm(tree, g, schedule): `schedule` is "postorder",
+    "levelorder" or any node sequence (validated like validate_schedule;
+    ValueError "invalid schedule at position N")."""
     ctx = ctx or default_context()
     if tree.n != g.n:
         raise ValueError("tree was built for a different graph")
@@ -387,9 +432,10 @@ def compute_perm(tree: EliminationTree, g: AdjacencyGraph, schedule: str = "post
         raise ValueError("tree nodes have no local order")
     pm = np.zeros(max(g.n, 1), np.int32)
     inv = np.zeros(max(g.n, 1), np.int32)
-    check(lib().mp_compute_perm(ctx.handle, g.n, tree.nd_level, _ptr(_i32(tree.node_offsets)),
-                                _ptr(_i32(tree.vertices)), _ptr(_i32(tree.local_perm)), SCHEDULES[schedule], _ptr(pm),
-                                _ptr(inv), 0))
+    sched = _schedule_nodes(tree, schedule)
+    check(lib().mp_compute_perm_schedule(ctx.handle, g.n, tree.nd_level, _ptr(_i32(tree.node_offsets)),
+                                         _ptr(_i32(tree.vertices)), _ptr(_i32(tree.local_perm)),
+                                         C.c_void_p(_nonempty(sched).ctypes.data), len(sched), _ptr(pm), _ptr(inv), 0))
     return Permutation(pm[:g.n], inv[:g.n])
 
 
@@ -404,17 +450,59 @@ def tree_separation_violations(g: AdjacencyGraph, tree: EliminationTree, ctx: Co
     return int(v.value)
 
 
-def tree_fill(g: AdjacencyGraph, tree: EliminationTree, schedule: str = "postorder",
+def tree_fill(g: AdjacencyGraph, tree: EliminationTree, schedule="postorder",
               ctx: Context | None = None) -> FillReport:  # symbolic.hpp:23 + :31
+    """elimination_fill + factor_etree_parents of compute_perm(tree, g,
+    schedule), played subtree by subtree on the device (any valid schedule)."""
     ctx = ctx or default_context()
     cc = np.zeros(max(g.n, 1), np.int64)
     par = np.zeros(max(g.n, 1), np.int32)
     a, l, c = C.c_int64(), C.c_int64(), C.c_int64()
     r = C.c_double()
-    check(lib().mp_tree_fill(ctx.handle, C.byref(_csr(g)), tree.nd_level, _ptr(_i32(tree.node_offsets)),
-                             _ptr(_i32(tree.vertices)), _ptr(_i32(tree.local_perm)), SCHEDULES[schedule], _ptr(cc),
-                             _ptr(par), 0, C.byref(a), C.byref(l), C.byref(c), C.byref(r)))
+    sched = _schedule_nodes(tree, schedule)
+    check(lib().mp_tree_fill_schedule(ctx.handle, C.byref(_csr(g)), tree.nd_level, _ptr(_i32(tree.node_offsets)),
+                                      _ptr(_i32(tree.vertices)), _ptr(_i32(tree.local_perm)),
+                                      C.c_void_p(_nonempty(sched).ctypes.data), len(sched), _ptr(cc), _ptr(par), 0,
+                                      C.byref(a),
+                                      C.byref(l), C.byref(c), C.byref(r)))
     return FillReport(a.value, l.value, r.value, cc[:g.n], c.value, par[:g.n])
+
+
+def _perm_array(g: AdjacencyGraph, perm) -> np.ndarray:
+    p = _i32(perm.perm if isinstance(perm, Permutation) else perm)
+    if len(p) != g.n:  # symbolic.cpp:12-14
+        raise ValueError("permutation does not match the graph")
+    return p
+
+
+def elimination_fill(g: AdjacencyGraph, perm, ctx: Context | None = None) -> FillReport:  # symbolic.hpp:23
+    """The elimination game for ANY permutation (new position -> old index),
+    on the device; FillReport.parents = factor_etree_parents (symbolic.hpp:31)."""
+    ctx = ctx or default_context()
+    p = _perm_array(g, perm)
+    cc = np.zeros(max(g.n, 1), np.int64)
+    par = np.zeros(max(g.n, 1), np.int32)
+    a, l, c = C.c_int64(), C.c_int64(), C.c_int64()
+    r = C.c_double()
+    check(lib().mp_elimination_fill(ctx.handle, C.byref(_csr(g)), _ptr(p), _ptr(cc), _ptr(par), 0, C.byref(a),
+                                    C.byref(l), C.byref(c), C.byref(r)))
+    return FillReport(a.value, l.value, r.value, cc[:g.n], c.value, par[:g.n])
+
+
+def factor_etree_parents(g: AdjacencyGraph, perm, ctx: Context | None = None) -> np.ndarray:  # symbolic.hpp:31
+    return elimination_fill(g, perm, ctx).parents
+
+
+def cross_block_fill(g: AdjacencyGraph, perm, tree: EliminationTree, ctx: Context | None = None) -> int:
+    """symbolic.hpp:37: factor entries joining unrelated tree nodes (exact count)."""
+    ctx = ctx or default_context()
+    p = _perm_array(g, perm)
+    if tree.n != g.n:
+        raise ValueError("tree was built for a different graph")
+    v = C.c_int64()
+    check(lib().mp_cross_block_fill(ctx.handle, C.byref(_csr(g)), _ptr(p), tree.nd_level,
+                                    _ptr(_i32(tree.node_offsets)), _ptr(_i32(tree.vertices)), 0, C.byref(v)))
+    return int(v.value)
 
 
 # ----------------------------------------------------------------- whole path
@@ -470,7 +558,13 @@ def order(g: AdjacencyGraph, patch_size: int = 256, nd_level: int = -1, seed: in
     given GroupMap is validated and its disconnected patches split instead of
     computing patches."""
     ctx = ctx or default_context()
-    cfg = make_config(patch_size, nd_level, seed, local_mode, schedule, block_size, want_fill)
+    custom = None if isinstance(schedule, str) else _i32(schedule)
+    cfg = make_config(patch_size, nd_level, seed, local_mode, "postorder" if custom is not None else schedule,
+                      block_size, want_fill)
+    if custom is not None:  # compute_perm(tree, g, schedule) with a caller sequence (assemble.hpp:37)
+        buf = custom if custom.size else np.zeros(1, np.int32)  # non-NULL even when empty
+        cfg.schedule_nodes = C.c_void_p(buf.ctypes.data)
+        cfg.schedule_len = len(custom)
     if user_patches is not None:
         up = _i32(user_patches.assignment)
         if len(up) != g.n:  # patching.cpp:387-390

@@ -9,9 +9,6 @@ collective, and off the timed path.
 """
 from __future__ import annotations
 
-import concurrent.futures as cf
-import threading
-
 import numpy as np
 
 
@@ -27,43 +24,24 @@ def owner(frame: int, world: int) -> int:
 
 
 class FramePool:
-    """`workers` contexts on one device; order() is thread-safe per worker."""
+    """`workers` contexts on one device, driven by the native mp_order_batch
+    (one library host thread per context)."""
 
     def __init__(self, device: int = 0, workers: int = 4):
         from .api import Context
-        self.device = device
         from ._lib import check, lib
+        self.device = device
         self.ctx = [Context(device) for _ in range(workers)]
         for c in self.ctx:  # concurrent contexts: grid-wide kernels take 1/workers of the SMs each
             check(lib().mp_context_set_sm_share(c.handle, workers))
-        self.free = list(range(workers))
-        self.lock = threading.Lock()
-        self.ex = cf.ThreadPoolExecutor(max_workers=workers)
-
-    def _take(self):
-        with self.lock:
-            return self.free.pop()
-
-    def _give(self, i):
-        with self.lock:
-            self.free.append(i)
-
-    def _run(self, fn, *args, **kw):
-        i = self._take()
-        try:
-            return fn(*args, ctx=self.ctx[i], **kw)
-        finally:
-            self._give(i)
 
     def order_all(self, graphs, **kw):
         """Every graph ordered concurrently over the pool's contexts (host
-        arrays in and out) through the native mp_order_batch: the library's
-        own host threads, one per context."""
+        arrays in and out) through the native mp_order_batch."""
         from .api import order_batch
         return order_batch(graphs, self.ctx, **kw)
 
     def close(self):
-        self.ex.shutdown()
         for c in self.ctx:
             c.close()
 

@@ -2,6 +2,7 @@
 // marshalling and the mp_order pipeline (reference run_pipeline ordering
 // stages, core/src/pipeline.cpp:100-140).
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -34,19 +35,41 @@ void SectionTimer::mark(const char* what) {
 }
 
 thread_local std::string g_last_error;
+thread_local cudaMemPool_t tl_pool = nullptr;
+
+cudaError_t dev_malloc_async(void** p, size_t bytes, cudaStream_t s) {
+  return tl_pool ? cudaMallocFromPoolAsync(p, bytes, tl_pool, s) : cudaMallocAsync(p, bytes, s);
+}
 
 int set_error(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
 }
 
-std::vector<int32_t> make_schedule(int32_t L, int32_t kind);
 int64_t unrelated_edges_dev(mp_context& ctx, const DGraph& g, const int32_t* node_of);
-void compute_perm_blocks_dev(mp_context& ctx, int32_t n, int32_t L, const int32_t* node_offsets,
-                             const int32_t* node_vertices, const int32_t* local_perm, int32_t schedule,
-                             int32_t b, int32_t* perm, int32_t* inverse, int32_t* node_pos_dev);
 
 namespace {
+
+// NVTX ranges (SURVEY §5 tracing): one per mp_order call plus one per stage,
+// visible in Nsight Systems / ncu --nvtx; no-ops when no tool is attached.
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+};
+// Consecutive stage ranges inside a call; balanced on every exit path.
+struct NvtxStages {
+  bool open = false;
+  void next(const char* name) {
+    end();
+    nvtxRangePushA(name);
+    open = true;
+  }
+  void end() {
+    if (open) nvtxRangePop();
+    open = false;
+  }
+  ~NvtxStages() { end(); }
+};
 
 int32_t default_nd_level_host(int32_t n) {  // etree.cpp:42-46
   int32_t level = 0;
@@ -139,18 +162,6 @@ int grid_for(const mp_context& ctx, int64_t n) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), ctx.num_sms * 16LL)));
 }
 
-struct ScopedDevice {
-  int prev = 0;
-  explicit ScopedDevice(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) cudaSetDevice(dev);
-  }
-  ~ScopedDevice() {
-    int cur = 0;
-    cudaGetDevice(&cur);
-    if (cur != prev) cudaSetDevice(prev);
-  }
-};
 
 }  // namespace
 }  // namespace mp
@@ -200,7 +211,7 @@ int mp_context_create(mp_context** out, int32_t device) {
     if (device < 0 || device >= count) throw Error(MP_EINVAL, "no CUDA device " + std::to_string(device));
     auto* ctx = new mp_context();
     ctx->device = device;
-    ScopedDevice sd(device);
+    ContextScope sd(*ctx);
     MP_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
     ctx->stream = ctx->own_stream;
     MP_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
@@ -208,18 +219,22 @@ int mp_context_create(mp_context** out, int32_t device) {
     for (auto& e : ctx->ev) MP_CUDA(cudaEventCreate(&e));
     MP_CUDA(cudaMalloc(reinterpret_cast<void**>(&ctx->dwork), 16 * sizeof(unsigned long long)));
     MP_CUDA(cudaMemset(ctx->dwork, 0, 16 * sizeof(unsigned long long)));
-    // keep freed scratch in the pool between calls (stream-ordered allocator)
-    cudaMemPool_t pool;
-    MP_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    // a private stream-ordered pool that keeps freed scratch between calls;
+    // the device's default pool (shared with the host application) is untouched
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    MP_CUDA(cudaMemPoolCreate(&ctx->pool, &props));
     uint64_t thr = UINT64_MAX;
-    MP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    MP_CUDA(cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &thr));
     *out = ctx;
   });
 }
 
 void mp_context_destroy(mp_context* ctx) {
   if (!ctx) return;
-  ScopedDevice sd(ctx->device);
+  ContextScope sd(*ctx);
   cudaStreamSynchronize(ctx->stream);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
@@ -228,6 +243,7 @@ void mp_context_destroy(mp_context* ctx) {
     if (sl.first) cudaFree(sl.first);
   if (ctx->dwork) cudaFree(ctx->dwork);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
   delete ctx;
 }
 
@@ -252,7 +268,7 @@ int mp_compute_patches(mp_context* ctx, const mp_csr* g, int32_t target, uint64_
                        int32_t on_device, int32_t* patch_count) {
   return guarded([&] {
     if (!ctx) throw Error(MP_EINVAL, "null context");
-    ScopedDevice sd(ctx->device);
+    ContextScope sd(*ctx);
     GraphView gv;
     make_view(*ctx, g, gv);
     DevBuf<int32_t> asg(std::max(g->n, 1), ctx->stream);
@@ -267,7 +283,7 @@ int mp_enforce_connectivity(mp_context* ctx, const mp_csr* g, const int32_t* ass
                             int32_t* out, int32_t on_device, int32_t* out_count) {
   return guarded([&] {
     if (!ctx) throw Error(MP_EINVAL, "null context");
-    ScopedDevice sd(ctx->device);
+    ContextScope sd(*ctx);
     GraphView gv;
     make_view(*ctx, g, gv);
     DevBuf<int32_t> hold, res(std::max(g->n, 1), ctx->stream);
@@ -284,7 +300,7 @@ int mp_validate_user_patches(mp_context* ctx, const mp_csr* g, const int32_t* as
                              int32_t* unused, int32_t* n_unused) {
   return guarded([&] {
     if (!ctx || !g || !n_disconnected || !n_unused || (g->n > 0 && !assignment)) throw Error(MP_EINVAL, "null argument");
-    ScopedDevice sd(ctx->device);
+    ContextScope sd(*ctx);
     GraphView gv;
     make_view(*ctx, g, gv);
     DevBuf<int32_t> hold;
@@ -302,7 +318,7 @@ int mp_build_quotient(mp_context* ctx, const mp_csr* g, const int32_t* assignmen
                       int64_t* node_weight, int32_t* edge_p, int32_t* edge_q, int64_t* edge_w, int64_t* n_edges) {
   return guarded([&] {
     if (!ctx) throw Error(MP_EINVAL, "null context");
-    ScopedDevice sd(ctx->device);
+    ContextScope sd(*ctx);
     cudaStream_t s = ctx->stream;
     GraphView gv;
     make_view(*ctx, g, gv);
@@ -330,7 +346,7 @@ int mp_build_etree(mp_context* ctx, const mp_csr* g, const int32_t* assignment, 
   return guarded([&] {
     if (!ctx) throw Error(MP_EINVAL, "null context");
     if (nd_level < 0 || nd_level > 24) throw Error(MP_EINVAL, "nd_level out of range");
-    ScopedDevice sd(ctx->device);
+    ContextScope sd(*ctx);
     cudaStream_t s = ctx->stream;
     GraphView gv;
     make_view(*ctx, g, gv);
@@ -351,7 +367,7 @@ int mp_order_tree_nodes(mp_context* ctx, const mp_csr* g, int32_t nd_level, cons
     if (!ctx) throw Error(MP_EINVAL, "null context");
     if (nd_level < 0 || nd_level > 24) throw Error(MP_EINVAL, "nd_level out of range");
     if (mode < 0 || mode > 2) throw Error(MP_EINVAL, "unknown local ordering mode");
-    ScopedDevice sd(ctx->device);
+    ContextScope sd(*ctx);
     cudaStream_t s = ctx->stream;
     GraphView gv;
     make_view(*ctx, g, gv);
@@ -374,7 +390,7 @@ int mp_order_subtrees(mp_context* ctx, const mp_csr* g, int32_t nd_level, const 
     if (nd_level < 0 || nd_level > 24) throw Error(MP_EINVAL, "nd_level out of range");
     if (mode < 0 || mode > 2) throw Error(MP_EINVAL, "unknown local ordering mode");
     if (!node_mask || !local_perm || !perm) throw Error(MP_EINVAL, "null node_mask / local_perm / perm");
-    ScopedDevice sd(ctx->device);
+    ContextScope sd(*ctx);
     cudaStream_t s = ctx->stream;
     GraphView gv;
     make_view(*ctx, g, gv);
@@ -398,7 +414,7 @@ int mp_order_subtrees(mp_context* ctx, const mp_csr* g, int32_t nd_level, const 
     }
     node_of_from_tree_dev(*ctx, n, nn, off, verts, node_of);
     order_tree_nodes_dev(*ctx, gv.g, nd_level, node_of, off, verts, mode, lp, mask);
-    compute_perm_partial_dev(*ctx, n, nd_level, off, verts, lp, schedule, mask, pm);
+    compute_perm_partial_dev(*ctx, n, nd_level, off, verts, lp, resolve_schedule(nd_level, schedule, nullptr, 0), mask, pm);
     if (!on_device) {
       MP_CUDA(cudaMemcpyAsync(local_perm, lp, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
       MP_CUDA(cudaMemcpyAsync(perm, pm, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
@@ -407,34 +423,57 @@ int mp_order_subtrees(mp_context* ctx, const mp_csr* g, int32_t nd_level, const 
   });
 }
 
-int mp_compute_perm(mp_context* ctx, int32_t n, int32_t nd_level, const int32_t* node_offsets,
-                    const int32_t* node_vertices, const int32_t* local_perm, int32_t schedule, int32_t* perm,
-                    int32_t* inverse, int32_t on_device) {
+int mp_compute_perm_schedule(mp_context* ctx, int32_t n, int32_t nd_level, const int32_t* node_offsets,
+                             const int32_t* node_vertices, const int32_t* local_perm, const int32_t* schedule_nodes,
+                             int64_t schedule_len, int32_t* perm, int32_t* inverse, int32_t on_device) {
   return guarded([&] {
     if (!ctx) throw Error(MP_EINVAL, "null context");
     if (nd_level < 0 || nd_level > 24) throw Error(MP_EINVAL, "nd_level out of range");
-    ScopedDevice sd(ctx->device);
+    if (!schedule_nodes) throw Error(MP_EINVAL, "null schedule");
+    ContextScope sd(*ctx);
+    const Schedule sched = resolve_schedule(nd_level, 0, schedule_nodes, schedule_len);
     cudaStream_t s = ctx->stream;
     const int32_t nn = static_cast<int32_t>((1LL << (nd_level + 1)) - 1);
     DevBuf<int32_t> h1, h2, h3, pm(std::max(n, 1), s), inv(std::max(n, 1), s), pos(nn + 1, s);
     const int32_t* off = input_ptr(*ctx, node_offsets, nn + 1, on_device != 0, h1);
     const int32_t* verts = input_ptr(*ctx, node_vertices, n, on_device != 0, h2);
     const int32_t* lp = input_ptr(*ctx, local_perm, n, on_device != 0, h3);
-    compute_perm_dev(*ctx, n, nd_level, off, verts, lp, schedule, pm, inv, pos);
+    compute_perm_dev(*ctx, n, nd_level, off, verts, lp, sched, pm, inv, pos);
     output_copy(*ctx, perm, pm.get(), n, on_device);
     output_copy(*ctx, inverse, inv.get(), n, on_device);
     MP_CUDA(cudaStreamSynchronize(s));
   });
 }
 
-int mp_tree_fill(mp_context* ctx, const mp_csr* g, int32_t nd_level, const int32_t* node_offsets,
-                 const int32_t* node_vertices, const int32_t* local_perm, int32_t schedule, int64_t* column_counts,
-                 int32_t* etree_parent, int32_t on_device, int64_t* nnz_A, int64_t* nnz_L, int64_t* cost,
-                 double* fill_ratio) {
+int mp_compute_perm(mp_context* ctx, int32_t n, int32_t nd_level, const int32_t* node_offsets,
+                    const int32_t* node_vertices, const int32_t* local_perm, int32_t schedule, int32_t* perm,
+                    int32_t* inverse, int32_t on_device) {
+  if (nd_level < 0 || nd_level > 24) return set_error(MP_EINVAL, "nd_level out of range");
+  if (schedule != MP_SCHEDULE_POSTORDER && schedule != MP_SCHEDULE_LEVELORDER)
+    return set_error(MP_EINVAL, "unknown schedule");
+  const Schedule sched = make_schedule(nd_level, schedule);
+  return mp_compute_perm_schedule(ctx, n, nd_level, node_offsets, node_vertices, local_perm, sched.data(),
+                                  static_cast<int64_t>(sched.size()), perm, inverse, on_device);
+}
+
+int mp_validate_schedule(int32_t nd_level, const int32_t* sequence, int64_t length, int64_t* first_violation) {
   return guarded([&] {
-    if (!ctx) throw Error(MP_EINVAL, "null context");
     if (nd_level < 0 || nd_level > 24) throw Error(MP_EINVAL, "nd_level out of range");
-    ScopedDevice sd(ctx->device);
+    if (!first_violation || (length > 0 && !sequence) || length < 0) throw Error(MP_EINVAL, "null argument");
+    *first_violation = validate_schedule_host(nd_level, sequence, length);
+  });
+}
+
+int mp_tree_fill_schedule(mp_context* ctx, const mp_csr* g, int32_t nd_level, const int32_t* node_offsets,
+                          const int32_t* node_vertices, const int32_t* local_perm, const int32_t* schedule_nodes,
+                          int64_t schedule_len, int64_t* column_counts, int32_t* etree_parent, int32_t on_device,
+                          int64_t* nnz_A, int64_t* nnz_L, int64_t* cost, double* fill_ratio) {
+  return guarded([&] {
+    if (!ctx || !g) throw Error(MP_EINVAL, "null argument");
+    if (nd_level < 0 || nd_level > 24) throw Error(MP_EINVAL, "nd_level out of range");
+    if (!schedule_nodes) throw Error(MP_EINVAL, "null schedule");
+    ContextScope sd(*ctx);
+    const Schedule sched = resolve_schedule(nd_level, 0, schedule_nodes, schedule_len);
     cudaStream_t s = ctx->stream;
     GraphView gv;
     make_view(*ctx, g, gv);
@@ -446,7 +485,7 @@ int mp_tree_fill(mp_context* ctx, const mp_csr* g, int32_t nd_level, const int32
     const int32_t* off = input_ptr(*ctx, node_offsets, nn + 1, on_device != 0, h1);
     const int32_t* verts = input_ptr(*ctx, node_vertices, n, on_device != 0, h2);
     const int32_t* lp = input_ptr(*ctx, local_perm, n, on_device != 0, h3);
-    compute_perm_dev(*ctx, n, nd_level, off, verts, lp, schedule, pm, inv, pos);
+    compute_perm_dev(*ctx, n, nd_level, off, verts, lp, sched, pm, inv, pos);
     node_of_from_tree_dev(*ctx, n, nn, off, verts, node_of);
     int64_t L = 0, C = 0;
     tree_fill_dev(*ctx, gv.g, nd_level, node_of, off, verts, lp, pos, inv, cc, par, &L, &C);
@@ -461,6 +500,70 @@ int mp_tree_fill(mp_context* ctx, const mp_csr* g, int32_t nd_level, const int32
   });
 }
 
+int mp_tree_fill(mp_context* ctx, const mp_csr* g, int32_t nd_level, const int32_t* node_offsets,
+                 const int32_t* node_vertices, const int32_t* local_perm, int32_t schedule, int64_t* column_counts,
+                 int32_t* etree_parent, int32_t on_device, int64_t* nnz_A, int64_t* nnz_L, int64_t* cost,
+                 double* fill_ratio) {
+  if (nd_level < 0 || nd_level > 24) return set_error(MP_EINVAL, "nd_level out of range");
+  if (schedule != MP_SCHEDULE_POSTORDER && schedule != MP_SCHEDULE_LEVELORDER)
+    return set_error(MP_EINVAL, "unknown schedule");
+  const Schedule sched = make_schedule(nd_level, schedule);
+  return mp_tree_fill_schedule(ctx, g, nd_level, node_offsets, node_vertices, local_perm, sched.data(),
+                               static_cast<int64_t>(sched.size()), column_counts, etree_parent, on_device, nnz_A,
+                               nnz_L, cost, fill_ratio);
+}
+
+int mp_elimination_fill(mp_context* ctx, const mp_csr* g, const int32_t* perm, int64_t* column_counts,
+                        int32_t* etree_parent, int32_t on_device, int64_t* nnz_A, int64_t* nnz_L, int64_t* cost,
+                        double* fill_ratio) {
+  return guarded([&] {
+    if (!ctx || !g || (g->n > 0 && !perm)) throw Error(MP_EINVAL, "null argument");
+    ContextScope sd(*ctx);
+    cudaStream_t s = ctx->stream;
+    GraphView gv;
+    make_view(*ctx, g, gv);
+    const int32_t n = g->n;
+    DevBuf<int32_t> hp, par(std::max(n, 1), s);
+    DevBuf<int64_t> cc(std::max(n, 1), s);
+    const int32_t* pm = input_ptr(*ctx, perm, n, on_device != 0, hp);
+    int64_t L = 0, C = 0;
+    elimination_game_dev(*ctx, gv.g, pm, cc, par, &L, &C, nullptr, nullptr);
+    output_copy(*ctx, column_counts, cc.get(), n, on_device);
+    output_copy(*ctx, etree_parent, par.get(), n, on_device);
+    MP_CUDA(cudaStreamSynchronize(s));
+    const int64_t A = static_cast<int64_t>(n) + gv.m2;  // symbolic.cpp:22-29 finish
+    if (nnz_A) *nnz_A = A;
+    if (nnz_L) *nnz_L = L;
+    if (cost) *cost = C;
+    if (fill_ratio) *fill_ratio = A > 0 ? static_cast<double>(L) / static_cast<double>(A) : 0.0;
+  });
+}
+
+int mp_cross_block_fill(mp_context* ctx, const mp_csr* g, const int32_t* perm, int32_t nd_level,
+                        const int32_t* node_offsets, const int32_t* node_vertices, int32_t on_device,
+                        int64_t* crossing) {
+  return guarded([&] {
+    if (!ctx || !g || !crossing || (g->n > 0 && !perm) || !node_offsets) throw Error(MP_EINVAL, "null argument");
+    if (nd_level < 0 || nd_level > 24) throw Error(MP_EINVAL, "nd_level out of range");
+    ContextScope sd(*ctx);
+    cudaStream_t s = ctx->stream;
+    GraphView gv;
+    make_view(*ctx, g, gv);
+    const int32_t n = g->n;
+    const int32_t nn = static_cast<int32_t>((1LL << (nd_level + 1)) - 1);
+    DevBuf<int32_t> hp, h1, h2, owner(std::max(n, 1), s), par(std::max(n, 1), s);
+    DevBuf<int64_t> cc(std::max(n, 1), s);
+    const int32_t* pm = input_ptr(*ctx, perm, n, on_device != 0, hp);
+    const int32_t* off = input_ptr(*ctx, node_offsets, nn + 1, on_device != 0, h1);
+    const int32_t* verts = input_ptr(*ctx, node_vertices, n, on_device != 0, h2);
+    // tree.n != g.n (symbolic.cpp:102-103) shows up as offsets not covering n
+    node_of_from_tree_dev(*ctx, n, nn, off, verts, owner);
+    int64_t L = 0, C = 0, X = 0;
+    elimination_game_dev(*ctx, gv.g, pm, cc, par, &L, &C, owner, &X);
+    *crossing = X;
+  });
+}
+
 // run_pipeline's ordering stages (pipeline.cpp:100-140) on a device CSR.
 int mp_order(mp_context* ctx, const mp_csr* g, const mp_config* cfg, mp_result* out) {
   return guarded([&] {
@@ -468,8 +571,8 @@ int mp_order(mp_context* ctx, const mp_csr* g, const mp_config* cfg, mp_result* 
     if (cfg->block_size < 1) throw Error(MP_EINVAL, "block size must be positive");
     if (cfg->patch_size < 1) throw Error(MP_EINVAL, "patch size must be positive");
     if (cfg->local_mode < 0 || cfg->local_mode > 2) throw Error(MP_EINVAL, "unknown local ordering mode");
-    if (cfg->schedule < 0 || cfg->schedule > 1) throw Error(MP_EINVAL, "unknown schedule");
-    ScopedDevice sd(ctx->device);
+    if (!cfg->schedule_nodes && (cfg->schedule < 0 || cfg->schedule > 1)) throw Error(MP_EINVAL, "unknown schedule");
+    ContextScope sd(*ctx);
     cudaStream_t s = ctx->stream;
     const int64_t launches0 = ctx->launches;
     const int32_t n = g->n, b = cfg->block_size;
@@ -477,15 +580,21 @@ int mp_order(mp_context* ctx, const mp_csr* g, const mp_config* cfg, mp_result* 
     if (L > 24) throw Error(MP_EINVAL, "nd_level out of range");
     const int32_t nn = static_cast<int32_t>((1LL << (L + 1)) - 1);
     const int64_t N = static_cast<int64_t>(b) * n;
+    // schedule_postorder / schedule_levelorder, or the caller's node sequence
+    // validated up front like compute_perm does (assemble.cpp:71-72)
+    const Schedule sched = resolve_schedule(L, cfg->schedule, cfg->schedule_nodes, cfg->schedule_len);
 
     ctx->ktime_reset();
     MP_CUDA(cudaMemsetAsync(ctx->dwork, 0, 16 * sizeof(unsigned long long), s));
+    NvtxScope call_range("mp_order");
+    NvtxStages stage;
     MP_CUDA(cudaEventRecord(ctx->ev[0], s));
     GraphView gv;
     make_view(*ctx, g, gv);
     DevBuf<int32_t> asg(std::max(n, 1), s), node_of(std::max(n, 1), s), off(nn + 1, s), verts(std::max(n, 1), s),
         lp(std::max(n, 1), s), pm(std::max<int64_t>(N, 1), s), inv(std::max<int64_t>(N, 1), s), pos(nn + 1, s);
     MP_CUDA(cudaEventRecord(ctx->ev[1], s));
+    stage.next("mp_order/patch");
     int32_t pc = 0;
     if (cfg->user_patches) {  // pipeline.cpp:102-111: validate, split disconnected patches
       DevBuf<int32_t> hold;
@@ -501,23 +610,28 @@ int mp_order(mp_context* ctx, const mp_csr* g, const mp_config* cfg, mp_result* 
       pc = compute_patches_dev(*ctx, gv.g, cfg->patch_size, cfg->seed, asg);
     }
     MP_CUDA(cudaEventRecord(ctx->ev[2], s));
+    stage.next("mp_order/quotient");
     // the per-level quotient is rebuilt inside the level loop (ndtree.cu), so
     // the quotient stage has no separate launch; its time is part of etree
     MP_CUDA(cudaEventRecord(ctx->ev[3], s));
+    stage.next("mp_order/etree");
     build_etree_dev(*ctx, gv.g, asg, pc, L, node_of, off, verts);
     MP_CUDA(cudaEventRecord(ctx->ev[4], s));
+    stage.next("mp_order/local");
     order_tree_nodes_dev(*ctx, gv.g, L, node_of, off, verts, cfg->local_mode, lp);
     MP_CUDA(cudaEventRecord(ctx->ev[5], s));
+    stage.next("mp_order/assemble");
     DevBuf<int32_t> pm1, inv1;
     if (b == 1) {
-      compute_perm_blocks_dev(*ctx, n, L, off, verts, lp, cfg->schedule, 1, pm, inv, pos);
+      compute_perm_blocks_dev(*ctx, n, L, off, verts, lp, sched, 1, pm, inv, pos);
     } else {
       pm1.alloc(std::max(n, 1), s);
       inv1.alloc(std::max(n, 1), s);
-      compute_perm_blocks_dev(*ctx, n, L, off, verts, lp, cfg->schedule, 1, pm1, inv1, pos);
-      compute_perm_blocks_dev(*ctx, n, L, off, verts, lp, cfg->schedule, b, pm, inv, pos);
+      compute_perm_blocks_dev(*ctx, n, L, off, verts, lp, sched, 1, pm1, inv1, pos);
+      compute_perm_blocks_dev(*ctx, n, L, off, verts, lp, sched, b, pm, inv, pos);
     }
     MP_CUDA(cudaEventRecord(ctx->ev[6], s));
+    stage.next("mp_order/symbolic");
     int64_t nnzL = 0, cost = 0;
     DevBuf<int64_t> cc;
     DevBuf<int32_t> par;
@@ -542,6 +656,7 @@ int mp_order(mp_context* ctx, const mp_csr* g, const mp_config* cfg, mp_result* 
       }
     }
     MP_CUDA(cudaEventRecord(ctx->ev[7], s));
+    stage.end();
     // the pipeline's self-check (pipeline.cpp:141-142), untimed like the reference's
     if (unrelated_edges_dev(*ctx, gv.g, node_of) != 0)
       throw Error(MP_ELOGIC, "separator failed to disconnect its sides");

@@ -24,8 +24,12 @@ extern "C" int mp_order_batch(mp_context* const* ctxs, int32_t nctx, int32_t cou
                               const mp_config* cfgs, mp_result* results, int32_t* status) {
   if (!ctxs || nctx < 1 || count < 0 || (count > 0 && (!graphs || !cfgs || !results)))
     return set_error(MP_EINVAL, "null or empty batch argument");
-  for (int32_t c = 0; c < nctx; ++c)
+  for (int32_t c = 0; c < nctx; ++c) {
     if (!ctxs[c]) return set_error(MP_EINVAL, "null context");
+    // a context (stream, scratch, timers) serves one host thread at a time
+    for (int32_t d = 0; d < c; ++d)
+      if (ctxs[d] == ctxs[c]) return set_error(MP_EINVAL, "context listed twice in the batch");
+  }
   std::vector<int32_t> share(nctx);
   for (int32_t c = 0; c < nctx; ++c) {
     share[c] = ctxs[c]->sm_share;

@@ -23,6 +23,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <map>
 #include <mutex>
 #include <cstdlib>
 
@@ -1095,19 +1096,24 @@ void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32
   MP_CUDA(cudaMemsetAsync(qctl, 0, sizeof(int32_t) * 96, s));
   if (!getenv("MP_FPS_NO_CLUSTER")) {
     // cluster size: 16 CTAs (non-portable) where the device allows, else 8;
-    // probed once per process (MP_FPS_CLUSTER overrides and is re-read)
+    // probed once per device (MP_FPS_CLUSTER overrides and is re-read).  The
+    // function attributes are per device too, so they are set for every
+    // device this process launches on, not only the first one probed.
     static std::mutex mu;
-    static int cached = -1;
+    static std::map<int, int> cached;  // device -> cluster CTAs (0: no cluster launch)
     const char* ce = getenv("MP_FPS_CLUSTER");
     int cluster_ctas = 0;
     {
       std::lock_guard<std::mutex> lk(mu);
-      if (ce || cached < 0) {
+      auto it = cached.find(ctx.device);
+      if (ce || it == cached.end()) {
         allow_max_smem(fps_cluster_phase, ctx.device);
-        cudaFuncSetAttribute(fps_cluster_phase, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        const bool nonportable =
+            cudaFuncSetAttribute(fps_cluster_phase, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+        cudaGetLastError();
         const int first = ce ? atoi(ce) : 16;
         for (int cs : {first, 16, 8}) {
-          if (cs < 1 || cs > 16) continue;
+          if (cs < 1 || cs > 16 || (cs > 8 && !nonportable)) continue;
           cudaLaunchConfig_t cfg{};
           cudaLaunchAttribute at[1];
           at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1121,9 +1127,9 @@ void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32
           }
           cudaGetLastError();
         }
-        if (!ce) cached = cluster_ctas;
+        if (!ce) cached[ctx.device] = cluster_ctas;
       } else {
-        cluster_ctas = cached;
+        cluster_ctas = it->second;
       }
     }
     if (cluster_ctas > 0) {

@@ -276,9 +276,7 @@ extern "C" int mp_mesh_to_graph_device(mp_context* ctx, int32_t nv, int64_t ntri
   return guarded([&] {
     if (!ctx || (!tris && ntri > 0) || !off) throw Error(MP_EINVAL, "null argument");
     if (ntri < 0) throw Error(MP_EINVAL, "negative triangle count");
-    int prev = 0;
-    cudaGetDevice(&prev);
-    if (prev != ctx->device) cudaSetDevice(ctx->device);
+    ContextScope scope(*ctx);
     cudaStream_t s = ctx->stream;
     DevBuf<int32_t> dtris, doff, dnbr;
     const int32_t* t = tris;
@@ -301,7 +299,6 @@ extern "C" int mp_mesh_to_graph_device(mp_context* ctx, int32_t nv, int64_t ntri
       MP_CUDA(cudaStreamSynchronize(s));
     }
     if (nnz) *nnz = m;
-    if (prev != ctx->device) cudaSetDevice(prev);
   });
 }
 
@@ -312,9 +309,7 @@ extern "C" int mp_pattern_to_graph_device(mp_context* ctx, int32_t n, int64_t nn
     if (!ctx || (nnz > 0 && (!rows || !cols)) || !off) throw Error(MP_EINVAL, "null argument");
     if (nnz < 0) throw Error(MP_EINVAL, "negative entry count");
     if (block_size < 1) throw Error(MP_EINVAL, "block size must be positive");
-    int prev = 0;
-    cudaGetDevice(&prev);
-    if (prev != ctx->device) cudaSetDevice(ctx->device);
+    ContextScope scope(*ctx);
     cudaStream_t s = ctx->stream;
     DevBuf<int32_t> dr, dc, doff, dnbr;
     const int32_t *r = rows, *c = cols;
@@ -339,7 +334,6 @@ extern "C" int mp_pattern_to_graph_device(mp_context* ctx, int32_t n, int64_t nn
       MP_CUDA(cudaStreamSynchronize(s));
     }
     if (nnz_out) *nnz_out = m;
-    if (prev != ctx->device) cudaSetDevice(prev);
   });
 }
 
@@ -353,14 +347,11 @@ extern "C" int mp_lift_patches(mp_context* ctx, int32_t n, const int32_t* assign
         for (int32_t t = 0; t < block_size; ++t) out[v * block_size + t] = assignment[v];
       return;
     }
-    int prev = 0;
-    cudaGetDevice(&prev);
-    if (prev != ctx->device) cudaSetDevice(ctx->device);
+    ContextScope scope(*ctx);
     if (n > 0)
       MP_KERNEL(*ctx, lift_kernel<<<grid_for_items(*ctx, static_cast<int64_t>(n) * block_size), 256, 0, ctx->stream>>>(
                           n, block_size, assignment, out));
     MP_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (prev != ctx->device) cudaSetDevice(prev);
   });
 }
 

@@ -38,9 +38,34 @@ struct mp_context {
   void* slab(int id, size_t bytes);
   int fps_workers = 0;  // worker CTAs of the batched FPS (decided once)
   int sm_share = 1;     // contexts expected to run concurrently on the device (grid sizing)
+  // private stream-ordered pool for the per-call scratch (release threshold
+  // raised on this pool only, never on the device's default pool)
+  cudaMemPool_t pool = nullptr;
 };
 
 namespace mp {
+
+// The pool DevBuf allocates from on this thread (set by ContextScope).
+extern thread_local cudaMemPool_t tl_pool;
+
+// Entry-point scope: the context's device is current and its private pool
+// serves DevBuf allocations; both are restored on exit.
+struct ContextScope {
+  int prev = 0;
+  int dev = 0;
+  cudaMemPool_t prev_pool = nullptr;
+  explicit ContextScope(const mp_context& ctx) : dev(ctx.device), prev_pool(tl_pool) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+    tl_pool = ctx.pool;
+  }
+  ~ContextScope() {
+    tl_pool = prev_pool;
+    if (prev != dev) cudaSetDevice(prev);
+  }
+  ContextScope(const ContextScope&) = delete;
+  ContextScope& operator=(const ContextScope&) = delete;
+};
 
 // Debug section timer: with MP_PROFILE=1 in the environment, synchronises the
 // stream at every mark and prints host wall time between marks to stderr.
@@ -101,22 +126,40 @@ void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t nd_level,
                           const int32_t* node_vertices, int32_t mode, int32_t* local_perm,
                           const uint8_t* node_mask = nullptr);
 
+// Node schedules (assemble.cu): schedule_postorder / schedule_levelorder
+// (assemble.cpp:24-46), or a caller sequence checked like validate_schedule
+// (assemble.cpp:48-63; MP_EINVAL "invalid schedule at position N").
+using Schedule = std::vector<int32_t>;
+Schedule make_schedule(int32_t L, int32_t kind);
+int64_t validate_schedule_host(int32_t L, const int32_t* seq, int64_t len);
+Schedule resolve_schedule(int32_t L, int32_t kind, const int32_t* nodes, int64_t len);
+std::vector<int32_t> node_positions(const std::vector<int32_t>& node_offsets, int32_t L, const Schedule& sched);
+
 // Assembly (assemble.cu): schedule + perm/inverse.  node_pos (nn+1) receives
 // the first permutation position of every node.
 void compute_perm_dev(mp_context& ctx, int32_t n, int32_t nd_level, const int32_t* node_offsets,
-                      const int32_t* node_vertices, const int32_t* local_perm, int32_t schedule,
+                      const int32_t* node_vertices, const int32_t* local_perm, const Schedule& schedule,
                       int32_t* perm, int32_t* inverse, int32_t* node_pos);
+void compute_perm_blocks_dev(mp_context& ctx, int32_t n, int32_t L, const int32_t* node_offsets,
+                             const int32_t* node_vertices, const int32_t* local_perm, const Schedule& schedule,
+                             int32_t b, int32_t* perm, int32_t* inverse, int32_t* node_pos_dev);
 // Sharded assembly: perm entries of the masked nodes only (no inverse, no
 // bijection check -- the other ranks own the remaining positions).
 void compute_perm_partial_dev(mp_context& ctx, int32_t n, int32_t nd_level, const int32_t* node_offsets,
-                              const int32_t* node_vertices, const int32_t* local_perm, int32_t schedule,
+                              const int32_t* node_vertices, const int32_t* local_perm, const Schedule& schedule,
                               const uint8_t* node_mask, int32_t* perm);
 
 // Symbolic (symbolic.cu): column counts (by position) and factor etree parents.
 void tree_fill_dev(mp_context& ctx, const DGraph& g, int32_t nd_level, const int32_t* node_of,
                    const int32_t* node_offsets, const int32_t* node_vertices,
                    const int32_t* local_perm, const int32_t* node_pos, const int32_t* inverse,
-                   int64_t* column_counts, int32_t* etree_parent, int64_t* nnz_L, int64_t* cost);
+                   int64_t* column_counts, int32_t* etree_parent, int64_t* nnz_L, int64_t* cost,
+                   const int32_t* cross_owner = nullptr, int64_t* crossing = nullptr);
+// The same game for any permutation (one-node tree): elimination_fill,
+// factor_etree_parents and, with cross_owner, cross_block_fill's count.
+void elimination_game_dev(mp_context& ctx, const DGraph& g, const int32_t* perm, int64_t* column_counts,
+                          int32_t* etree_parent, int64_t* nnz_L, int64_t* cost, const int32_t* cross_owner,
+                          int64_t* crossing);
 
 // node_of[v] from the flattened tree (assemble.cu).
 void node_of_from_tree_dev(mp_context& ctx, int32_t n, int32_t nn, const int32_t* node_offsets,

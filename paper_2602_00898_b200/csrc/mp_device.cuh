@@ -175,6 +175,10 @@ inline void allow_max_smem(K* kernel, int device) {
   done.insert(key);
 }
 
+// Stream-ordered allocation from the calling entry point's context pool
+// (ContextScope), else from the device's current pool.
+cudaError_t dev_malloc_async(void** p, size_t bytes, cudaStream_t s);
+
 // Stream-ordered scratch buffer (cudaMallocAsync from the context pool).
 template <class T>
 struct DevBuf {
@@ -187,7 +191,7 @@ struct DevBuf {
     release();
     s = st;
     n = count;
-    if (count) MP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(T) * count, st));
+    if (count) MP_CUDA(dev_malloc_async(reinterpret_cast<void**>(&p), sizeof(T) * count, st));
   }
   void release() {
     if (p) cudaFreeAsync(p, s);

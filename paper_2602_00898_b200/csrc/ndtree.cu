@@ -1327,9 +1327,9 @@ int64_t build_quotient_dev(mp_context& ctx, const DGraph& g, const int32_t* assi
     MP_CUDA(cudaStreamSynchronize(s));
   }
   if (edge_p) {
-    MP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(edge_p), sizeof(int32_t) * std::max(U, 1), s));
-    MP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(edge_q), sizeof(int32_t) * std::max(U, 1), s));
-    MP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(edge_w), sizeof(int64_t) * std::max(U, 1), s));
+    MP_CUDA(dev_malloc_async(reinterpret_cast<void**>(edge_p), sizeof(int32_t) * std::max(U, 1), s));
+    MP_CUDA(dev_malloc_async(reinterpret_cast<void**>(edge_q), sizeof(int32_t) * std::max(U, 1), s));
+    MP_CUDA(dev_malloc_async(reinterpret_cast<void**>(edge_w), sizeof(int64_t) * std::max(U, 1), s));
     if (U > 0) MP_KERNEL(ctx, split_keys<<<grid_for(ctx, U), 256, 0, s>>>(U, uk, uc, *edge_p, *edge_q, *edge_w));
   }
   return U;

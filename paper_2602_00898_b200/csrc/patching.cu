@@ -705,6 +705,7 @@ struct RepairArgs {
   int32_t* seg_len;
   int32_t* seg_next;
   int32_t* pool;       // cap_pool
+  int32_t* pool2;      // cap_pool: compaction target (the two pools swap)
   int32_t* dist;       // n, kUnreached outside the current patch work
   int32_t* lab;        // n
   int32_t* fa;         // n
@@ -729,12 +730,63 @@ __global__ void __launch_bounds__(1024) repair_kernel(RepairArgs a) {
   __syncthreads();
   const int64_t max_iter = 4LL * a.P0 + 64;
 
+  int32_t* pool = a.pool;  // member storage; splits append to it, compaction swaps it
+  int32_t* spare = a.pool2;
   // iterate the member chain of patch p: f(v) for every member, block-parallel
   auto for_members = [&](int32_t p, auto&& f) {
     for (int32_t sgi = a.head[p]; sgi >= 0; sgi = a.seg_next[sgi]) {
       const int32_t st = a.seg_start[sgi], len = a.seg_len[sgi];
-      for (int32_t i = threadIdx.x; i < len; i += blockDim.x) f(a.pool[st + i]);
+      for (int32_t i = threadIdx.x; i < len; i += blockDim.x) f(pool[st + i]);
     }
+  };
+  // Splits append 2 x |patch| ints to the pool and 2 segments; when either
+  // runs out, every live patch's chain is copied into one contiguous segment
+  // of the spare pool (a warp per patch, bases from a block scan of the
+  // sizes) and the pools swap.  Member order inside a patch never affects a
+  // result (every choice is a min / max by id), so this is invisible.
+  auto compact = [&](int32_t P) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __shared__ int32_t s_base[1024];
+    int64_t run = 0;
+    for (int32_t p0 = 0; p0 < P; p0 += blockDim.x) {
+      const int32_t p = p0 + threadIdx.x;
+      const int32_t sz = p < P ? max(a.size[p], 0) : 0;
+      int32_t tot;
+      const int32_t e = block_excl_scan(sz, shi, &tot);
+      s_base[threadIdx.x] = static_cast<int32_t>(run) + e;
+      __syncthreads();
+      for (int32_t k = wid; k < static_cast<int32_t>(blockDim.x) && p0 + k < P; k += nw) {
+        const int32_t q = p0 + k;
+        if (a.size[q] <= 0) continue;
+        int32_t at = s_base[k];
+        for (int32_t sgi = a.head[q]; sgi >= 0; sgi = a.seg_next[sgi]) {
+          const int32_t st = a.seg_start[sgi], len = a.seg_len[sgi];
+          for (int32_t i = lane; i < len; i += 32) spare[at + i] = pool[st + i];
+          at += len;
+        }
+      }
+      __syncthreads();
+      for (int32_t q = p0 + threadIdx.x; q < P && q < p0 + static_cast<int32_t>(blockDim.x); q += blockDim.x) {
+        if (a.size[q] > 0) {
+          a.seg_start[q] = s_base[q - p0];
+          a.seg_len[q] = a.size[q];
+          a.seg_next[q] = -1;
+          a.head[q] = a.tail[q] = q;
+        } else {
+          a.head[q] = a.tail[q] = -1;
+        }
+      }
+      run += tot;
+      __syncthreads();
+    }
+    int32_t* t = pool;
+    pool = spare;
+    spare = t;
+    if (threadIdx.x == 0) {
+      s_nseg = P;
+      s_pool = run;
+    }
+    __syncthreads();
   };
 
   for (int64_t iter = 0; iter < max_iter; ++iter) {
@@ -790,6 +842,7 @@ __global__ void __launch_bounds__(1024) repair_kernel(RepairArgs a) {
     if (big == 0) break;
     const int32_t sp = static_cast<int32_t>(key_max_id(big));
     const int32_t spsize = a.size[sp];
+    if (s_nseg + 2 > a.cap_seg || s_pool + 2LL * spsize > a.cap_pool) compact(P);
     if (P >= a.cap_p || s_nseg + 2 > a.cap_seg || s_pool + 2LL * spsize > a.cap_pool) {
       if (threadIdx.x == 0) s_err = 1;
       __syncthreads();
@@ -800,9 +853,9 @@ __global__ void __launch_bounds__(1024) repair_kernel(RepairArgs a) {
     __syncthreads();
     if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
-    for_members(sp, [&](int32_t v) { a.pool[gbase + atomicAdd(&s_cnt, 1)] = v; });
+    for_members(sp, [&](int32_t v) { pool[gbase + atomicAdd(&s_cnt, 1)] = v; });
     __syncthreads();
-    const int32_t* mem = a.pool + gbase;
+    const int32_t* mem = pool + gbase;
     // farthest-vertex sweeps (patching.cpp:165-185, 231-233)
     uint64_t mn = ~0ull;
     for (int32_t i = threadIdx.x; i < spsize; i += blockDim.x)
@@ -911,9 +964,9 @@ __global__ void __launch_bounds__(1024) repair_kernel(RepairArgs a) {
         int32_t tk, tf;
         int32_t ek = block_excl_scan(isk, shi, &tk);
         int32_t ef = block_excl_scan(isf, shi, &tf);
-        if (isk) a.pool[kbase + run_keep + ek] = v;
+        if (isk) pool[kbase + run_keep + ek] = v;
         if (isf) {
-          a.pool[kbase + nkeep_total + run_fresh + ef] = v;
+          pool[kbase + nkeep_total + run_fresh + ef] = v;
           a.assignment[v] = fresh;
         }
         run_keep += tk, run_fresh += tf;
@@ -1009,18 +1062,22 @@ int32_t repair_sizes_dev(mp_context& ctx, const DGraph& g, int32_t* assignment, 
   a.g = g;
   a.assignment = assignment;
   a.P0 = P;
-  a.cap_p = P + std::max<int32_t>(1024, P);
+  // every split takes one of the 4P+64 iterations (patching.cpp:187): ids
+  // are never reused, so P0 + 4P0 + 64 bounds them; segments and pool space
+  // are recycled by the in-kernel compaction
+  a.cap_p = 5 * P + 65;
   a.cap_seg = 2 * a.cap_p + 16;
   a.cap_pool = 3LL * n + 1024;
   a.target = target;
   DevBuf<int32_t> size(a.cap_p, s), exempt(a.cap_p, s), head(a.cap_p, s), tail(a.cap_p, s),
       seg_start(a.cap_seg, s), seg_len(a.cap_seg, s), seg_next(a.cap_seg, s), pool(a.cap_pool, s),
+      pool2(a.cap_pool, s),
       dist(n, s), lab(n, s), fa(n, s), fb(n, s), remap(a.cap_p, s), out(2, s), cnt(P, s), st(P, s);
   bucket_by_patch(ctx, n, assignment, P, st, cnt, pool);
   MP_KERNEL(ctx, seg_init<<<grid_for(ctx, P), 256, 0, s>>>(P, st, cnt, head, tail, seg_start, seg_len,
                                                           seg_next, size, exempt));
   a.size = size, a.exempt = exempt, a.head = head, a.tail = tail, a.seg_start = seg_start;
-  a.seg_len = seg_len, a.seg_next = seg_next, a.pool = pool, a.dist = dist, a.lab = lab;
+  a.seg_len = seg_len, a.seg_next = seg_next, a.pool = pool, a.pool2 = pool2, a.dist = dist, a.lab = lab;
   a.fa = fa, a.fb = fb, a.remap = remap, a.out = out;
   MP_KERNEL(ctx, repair_kernel<<<1, 1024, 0, s>>>(a));
   int32_t h_out[2];

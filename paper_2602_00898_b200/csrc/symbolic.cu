@@ -66,6 +66,11 @@ struct SymArgs {
   int32_t* parent;           // by position
   int32_t* overflow;
   int32_t smem_path;         // path sizes up to this use shared-memory marks
+  // cross_block_fill (symbolic.cpp:98-119): tree node of every vertex in the
+  // caller's tree, and the count of reach members whose node is unrelated to
+  // the pivot's (NULL: not counted)
+  const int32_t* cross_owner;
+  unsigned long long* cross_count;
 };
 
 // private index of w (in node A, an ancestor-or-self of the CTA's node)
@@ -182,6 +187,8 @@ __global__ void __launch_bounds__(kSymWide) sym_kernel(SymArgs a) {
     // permutation position in it is folded in on the way.  Each thread takes
     // kU entries at a time so their dependent loads are in flight together.
     uint64_t mn = ~0ull;
+    const int32_t powner = a.cross_owner ? a.cross_owner[p] : 0;
+    uint32_t ncross = 0;
     auto sweep = [&](const int32_t* list, int32_t len) {
       for (int32_t i0 = threadIdx.x; i0 < len; i0 += kU * blockDim.x) {
         int32_t w[kU], pi[kU];
@@ -199,6 +206,10 @@ __global__ void __launch_bounds__(kSymWide) sym_kernel(SymArgs a) {
           if (w[q] != p && atomicExch(&marks[pi[q]], tok) != tok) {
             scratch[atomicAdd(cnt, 1)] = w[q];
             mn = min(mn, static_cast<uint64_t>(inv[q]));
+            if (a.cross_owner) {
+              const int32_t wo = a.cross_owner[w[q]];
+              ncross += wo != powner && !is_ancestor_or_self(wo, powner) && !is_ancestor_or_self(powner, wo);
+            }
           }
       }
     };
@@ -220,6 +231,10 @@ __global__ void __launch_bounds__(kSymWide) sym_kernel(SymArgs a) {
         const int32_t sz = __shfl_sync(0xffffffffu, my_sz, j);
         sweep(a.pool + __shfl_sync(0xffffffffu, my_bp, j), sz);
       }
+    }
+    if (a.cross_owner) {
+      ncross = __reduce_add_sync(0xffffffffu, ncross);
+      if (lane == 0 && ncross) atomicAdd(a.cross_count, static_cast<unsigned long long>(ncross));
     }
     mn = warp_min_u64(mn);
     if (lane == 0) red[wid] = mn;
@@ -339,7 +354,8 @@ __global__ void clear_bsz(int32_t n, int32_t* bsz) {
 void tree_fill_dev(mp_context& ctx, const DGraph& g, int32_t L, const int32_t* node_of,
                    const int32_t* node_offsets, const int32_t* node_vertices, const int32_t* local_perm,
                    const int32_t* node_pos, const int32_t* inverse, int64_t* column_counts,
-                   int32_t* etree_parent, int64_t* nnz_L, int64_t* cost) {
+                   int32_t* etree_parent, int64_t* nnz_L, int64_t* cost, const int32_t* cross_owner,
+                   int64_t* crossing) {
   cudaStream_t s = ctx.stream;
   const int32_t n = g.n;
   const int32_t nn = static_cast<int32_t>((1LL << (L + 1)) - 1);
@@ -386,7 +402,7 @@ void tree_fill_dev(mp_context& ctx, const DGraph& g, int32_t L, const int32_t* n
       left_cnt(nn, s), left_list(std::max<int64_t>(left_off[nn], 1), s), overflow(1, s);
   DevBuf<int64_t> bptr(n, s), d_left_off(nn + 1, s), d_ws_off((static_cast<size_t>(1) << L) + 1, s);
   DevBuf<int32_t> adj(std::max(m2, 1), s), el(std::max(m2, 1), s);
-  DevBuf<unsigned long long> cursor(1, s), sums(2, s);
+  DevBuf<unsigned long long> cursor(1, s), sums(2, s), cross(1, s);
   MP_KERNEL(ctx, local_of_kernel<<<grid_for(ctx, n), 256, 0, s>>>(n, node_of, node_offsets, node_vertices, local_of));
   MP_CUDA(cudaMemcpyAsync(d_left_off, left_off.data(), sizeof(int64_t) * (nn + 1), cudaMemcpyHostToDevice, s));
   // boundary pool: sum of reach sizes = nnz(L) - n; start from the ratio seen
@@ -405,6 +421,8 @@ void tree_fill_dev(mp_context& ctx, const DGraph& g, int32_t L, const int32_t* n
     a.pool = pool, a.pool_cap = cap, a.pool_cursor = cursor, a.ws = ws, a.left_off = d_left_off;
     a.left_cnt = left_cnt, a.left_list = left_list, a.column_counts = column_counts, a.parent = etree_parent;
     a.overflow = overflow;
+    a.cross_owner = cross_owner, a.cross_count = cross;
+    MP_CUDA(cudaMemsetAsync(cross, 0, sizeof(unsigned long long), s));
     for (int32_t l = L; l >= 0; --l) {
       const int32_t width = 1 << l;
       MP_CUDA(cudaMemcpyAsync(d_ws_off, ws_offs[l].data(), sizeof(int64_t) * (width + 1), cudaMemcpyHostToDevice, s));
@@ -433,6 +451,55 @@ void tree_fill_dev(mp_context& ctx, const DGraph& g, int32_t L, const int32_t* n
   MP_CUDA(cudaStreamSynchronize(s));
   *nnz_L = static_cast<int64_t>(h[0]);
   *cost = static_cast<int64_t>(h[1]);
+  if (crossing) {
+    unsigned long long hc = 0;
+    MP_CUDA(cudaMemcpyAsync(&hc, cross, 8, cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+    *crossing = static_cast<int64_t>(hc);
+  }
+}
+
+namespace {
+__global__ void game_tree(int32_t n, const int32_t* perm, int32_t* verts, int32_t* inverse, int32_t* node_of,
+                          int32_t* bad) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    verts[i] = i;
+    node_of[i] = 0;
+    const int32_t v = perm[i];
+    if (v < 0 || v >= n) {
+      atomicExch(bad, 1);
+      continue;
+    }
+    if (atomicExch(&inverse[v], i) != -1) atomicExch(bad, 1);
+  }
+}
+}  // namespace
+
+// elimination_fill / factor_etree_parents / cross_block_fill for an arbitrary
+// permutation (symbolic.cpp:33-45, :82-96, :98-119): the game on a one-node
+// tree whose local order is the permutation itself (one CTA plays every pivot).
+void elimination_game_dev(mp_context& ctx, const DGraph& g, const int32_t* perm, int64_t* column_counts,
+                          int32_t* etree_parent, int64_t* nnz_L, int64_t* cost, const int32_t* cross_owner,
+                          int64_t* crossing) {
+  cudaStream_t s = ctx.stream;
+  const int32_t n = g.n;
+  *nnz_L = 0, *cost = 0;
+  if (crossing) *crossing = 0;
+  if (n == 0) return;
+  DevBuf<int32_t> off(2, s), verts(n, s), inv(n, s), node_of(n, s), pos(2, s), bad(1, s);
+  const int32_t hoff[2] = {0, n};
+  MP_CUDA(cudaMemcpyAsync(off, hoff, sizeof hoff, cudaMemcpyHostToDevice, s));
+  MP_CUDA(cudaMemcpyAsync(pos, hoff, sizeof hoff, cudaMemcpyHostToDevice, s));
+  MP_CUDA(cudaMemsetAsync(inv, 0xff, sizeof(int32_t) * n, s));
+  MP_CUDA(cudaMemsetAsync(bad, 0, 4, s));
+  MP_KERNEL(ctx, game_tree<<<grid_for(ctx, n), 256, 0, s>>>(n, perm, verts, inv, node_of, bad));
+  int32_t hb = 0;
+  MP_CUDA(cudaMemcpyAsync(&hb, bad, 4, cudaMemcpyDeviceToHost, s));
+  MP_CUDA(cudaStreamSynchronize(s));
+  if (hb) throw Error(MP_EINVAL, "permutation is not a bijection");  // symbolic.cpp:16-18
+  // local_perm of the single node = positions into its iota vertex list = perm
+  tree_fill_dev(ctx, g, 0, node_of, off, verts, perm, pos, inv, column_counts, etree_parent, nnz_L, cost,
+                cross_owner, crossing);
 }
 
 }  // namespace mp

@@ -71,9 +71,7 @@ extern "C" int mp_tree_separation_check(mp_context* ctx, const mp_csr* g, int32_
   return guarded([&] {
     if (!ctx || !g || !node_offsets || !node_vertices || !violations) throw Error(MP_EINVAL, "null argument");
     if (nd_level < 0 || nd_level > 24) throw Error(MP_EINVAL, "nd_level out of range");
-    int prev = 0;
-    cudaGetDevice(&prev);
-    if (prev != ctx->device) cudaSetDevice(ctx->device);
+    ContextScope scope(*ctx);
     cudaStream_t s = ctx->stream;
     const int32_t n = g->n, nn = (1 << (nd_level + 1)) - 1;
     DevBuf<int32_t> doff, dnbr, toff, tv, node_of(std::max(n, 1), s), bad(1, s);
@@ -100,6 +98,5 @@ extern "C" int mp_tree_separation_check(mp_context* ctx, const mp_csr* g, int32_
     MP_CUDA(cudaStreamSynchronize(s));
     if (hb) throw Error(MP_EINVAL, "tree vertex out of range");
     *violations = unrelated_edges_dev(*ctx, DGraph{n, off, nbr}, node_of);
-    if (prev != ctx->device) cudaSetDevice(prev);
   });
 }

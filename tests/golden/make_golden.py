@@ -86,10 +86,13 @@ def main():
     ap.add_argument("--big", action="store_true", help="also the 1M-vertex C2 golden (~1 min)")
     ap.add_argument("--c5", action="store_true", help="only the 2M-vertex C5 golden (3x3 blocks)")
     ap.add_argument("--c3", action="store_true", help="only the 10M-vertex C3 torus golden (~15 min)")
+    ap.add_argument("--c4", action="store_true", help="only the 64 C4 frames random_mesh(500,500,seed=f)")
     args = ap.parse_args()
     R = Reference()
     if args.c5:
         return make_c5(R)
+    if args.c4:
+        return make_c4(R)
     if args.c3:
         return make_big(R, "c3", lambda: mp.mesh_to_graph(mp.make_torus_mesh(2000, 5000)))
     arrays = {}
@@ -154,14 +157,49 @@ def make_c5(R, b=3):
     cc = r["column_counts"].astype(np.int64)
     cols = (b * cc[:, None] - np.arange(b)[None, :]).reshape(-1)
     pb = (b * r["perm"].astype(np.int64)[:, None] + np.arange(b)[None, :]).reshape(-1).astype(np.int32)
+    # expanded factor etree: inside a block row b*k+t -> b*k+t+1, the block's
+    # last row -> the first row of the parent block (or -1)
+    par = r["parents"].astype(np.int64)
+    parb = (b * np.arange(g.n, dtype=np.int64)[:, None] + np.arange(b)[None, :] + 1)
+    parb[:, b - 1] = np.where(par < 0, -1, b * par)
+    parb = parb.reshape(-1).astype(np.int32)
     gold_path = HERE / "bench_golden.json"
     gold = json.loads(gold_path.read_text())
     gold["c5"] = {"n": g.n, "edges": g.edge_count(), "block_size": b, "patch_count": r["patch_count"],
                   "nd_level": r["nd_level"], "base_nnz_L": r["nnz_L"], "sha_base_perm": digest(r["perm"]),
                   "nnz_A": int(b * b * r["nnz_A"]),
                   "nnz_L": int(cols.sum()), "cost": int((cols * cols).sum()), "sha_perm": digest(pb),
+                  "sha_base_column_counts": digest(r["column_counts"]), "sha_base_parents": digest(r["parents"]),
+                  "sha_column_counts": digest(cols), "sha_parents": digest(parb),
                   "reference_s": round(time.time() - t0, 1)}
     print("c5", gold["c5"])
+    gold_path.write_text(json.dumps(gold, indent=1) + "\n")
+
+
+def make_c4(R, frames=64, threads=None):
+    """configs[3]: 64 frames random_mesh(500, 500, seed=f) (the reference's own
+    generator, tests/test_support.hpp:66-86), each ordered, filled and
+    etree'd by the reference core; frames run concurrently (one per core)."""
+    import concurrent.futures as cf
+    import os
+    from oracle import meshgen
+    threads = threads or os.cpu_count()
+
+    def one(f):
+        n, off, nbr = meshgen.graph("random", (500, 500, f), R)
+        g = mp.AdjacencyGraph(n, off, nbr)
+        r = run_case(R, g, 256, -1, 0, 0, threads=1)
+        return {"frame": f, "n": n, "sha_csr": meshgen.csr_digest(off, nbr), "patch_count": r["patch_count"],
+                "nnz_L": r["nnz_L"], "cost": r["cost"], "sha_perm": digest(r["perm"]),
+                "sha_column_counts": digest(r["column_counts"]), "sha_parents": digest(r["parents"])}
+
+    t0 = time.time()
+    with cf.ThreadPoolExecutor(threads) as ex:
+        rows = list(ex.map(one, range(frames)))
+    gold_path = HERE / "bench_golden.json"
+    gold = json.loads(gold_path.read_text())
+    gold["c4"] = {"frames": rows, "reference_s": round(time.time() - t0, 1), "threads": threads}
+    print("c4", rows[:2], gold["c4"]["reference_s"])
     gold_path.write_text(json.dumps(gold, indent=1) + "\n")
 
 

@@ -83,7 +83,8 @@ def test_result_struct_layout():
     # mp_result as declared: 8 pointers + scalars + float[6] + int64 + float[6] + int64[16]
     assert C.sizeof(_lib.MpResult) >= 8 * 8 + 8 + 3 * 8 + 8 + 24 + 8 + 24 + 128
     assert [f[0] for f in _lib.MpConfig._fields_] == ["patch_size", "nd_level", "seed", "local_mode", "schedule",
-                                                      "block_size", "want_fill", "user_patches", "user_patch_count"]
+                                                      "block_size", "want_fill", "user_patches", "user_patch_count",
+                                                      "schedule_nodes", "schedule_len"]
 
 
 def test_struct_offsets_match_header(tmp_path):

@@ -248,6 +248,30 @@ def test_c5_blocks_match_reference():
     assert res.patch.patch_count == gold["patch_count"]
     assert digest(res.perm.perm) == gold["sha_perm"]
     assert (res.fill.nnz_A, res.fill.nnz_L, res.fill.cost) == (gold["nnz_A"], gold["nnz_L"], gold["cost"])
+    # "permutation + etree + nnz(L)": the expanded factor's column counts and
+    # etree parents, digested from the reference's base outputs
+    assert digest(res.fill.column_counts) == gold["sha_column_counts"]
+    assert digest(res.fill.parents) == gold["sha_parents"]
+
+
+def test_c4_all_frames_match_reference():
+    """configs[3]: all 64 frames random_mesh(500, 500, seed=f) ordered through
+    mp_order_batch on 4 concurrent contexts with the fill on; perm, nnz(L),
+    cost, column counts and factor etree of every frame against the reference
+    (tests/golden/make_golden.py --c4)."""
+    gold = json.loads((GOLDEN / "bench_golden.json").read_text())["c4"]["frames"]
+    frames = [mp.mesh_to_graph(mp.make_random_mesh(500, 500, seed=f)) for f in range(len(gold))]
+    ctxs = [mp.Context(0) for _ in range(4)]
+    try:
+        res = mp.order_batch(frames, ctxs, want_fill=True)
+    finally:
+        for c in ctxs:
+            c.close()
+    for f, (g, r, want) in enumerate(zip(frames, res, gold)):
+        got = {"patch_count": r.patch.patch_count, "nnz_L": r.fill.nnz_L, "cost": r.fill.cost,
+               "sha_perm": digest(r.perm.perm), "sha_column_counts": digest(r.fill.column_counts),
+               "sha_parents": digest(r.fill.parents)}
+        assert got == {k: want[k] for k in got}, f
 
 
 def test_deterministic_across_calls_and_contexts():
@@ -752,3 +776,35 @@ def test_run_pipeline_row_fields(tmp_path):
     assert line.startswith("tiny,108,") and ",ours-8,8,2,0.000,0.000,0.000,0.000,0.000," in line
     assert mp.default_input_id(mp.RunConfig(mesh_path="/a/b/mesh.off")) == "mesh.off"
     assert mp.default_input_id(mp.RunConfig(grid_rows=3, grid_cols=4)) == "grid-3x4"
+
+
+def _star_like(kind):
+    if kind == "star":  # hub 0 + 1000 leaves
+        return graph(1001, [(0, i) for i in range(1, 1001)]), 100
+    if kind == "star_mid":  # hub in the middle of the id range
+        return graph(2001, [(1000, i) for i in range(2001) if i != 1000]), 64
+    if kind == "broom":  # a 100-vertex path ending in a 500-leaf star
+        return graph(600, [(i, i + 1) for i in range(99)] + [(99, j) for j in range(100, 600)]), 50
+    # two grids joined by a 30-vertex path
+    a = mp.mesh_to_graph(mp.make_grid_mesh(20, 20))
+    e = [(u, int(w)) for u in range(a.n) for w in a.neighbors_of(u) if u < w]
+    e += [(u + 400, w + 400) for u, w in e[:]]
+    e += [(399, 800)] + [(800 + i, 801 + i) for i in range(29)] + [(829, 400)]
+    return graph(830, e), 48
+
+
+@pytest.mark.parametrize("kind", ["star", "star_mid", "broom", "dumbbell"])
+def test_repair_sizes_merge_and_split_match_reference(kind):
+    """repair_sizes (patching.cpp:149-291): on a star the Lloyd regions leave a
+    1,000-vertex patch (> 2t, split branch) and singleton seed patches
+    (< (t+1)/2, merge branch); the two alternate until the 4P+64 iteration cap.
+    Patch ids, tree and permutation must equal the reference's."""
+    from oracle.oracle import Reference
+    R = Reference()
+    g, t = _star_like(kind)
+    a, pc = R.compute_patches(g, t, 0)
+    p = mp.compute_patches(g, t, 0)
+    assert p.patch_count == pc and np.array_equal(p.assignment, a)
+    o = R.order(g, patch_size=t, nd_level=2)
+    r = mp.order(g, patch_size=t, nd_level=2)
+    assert np.array_equal(r.perm.perm, o["perm"]) and np.array_equal(r.tree.vertices, o["node_vertices"])
