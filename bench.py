@@ -692,100 +692,99 @@ def run_c4(args):
 
 # ------------------------------------------------------------------ our arm: C3 subtrees
 def run_c3(args):
-    """configs[2]: 10M-vertex torus, subtrees sharded across ranks
-    (paper_2602_00898_b200/subtree.py).  value = device ms of the whole step,
-    max over ranks."""
-    import ctypes as C
-
+    """configs[2]: the 10M-vertex torus ordered by all ranks together through
+    the native mp_order_sharded: patches and the top
+    ceil(log2 N) ND levels on every rank, the level-k subtrees dealt to ranks,
+    NCCL all-gathers of sizes, tree lists, subtree-root elements and column
+    counts.  value = permutation ms (stages 1-5, CUDA events in the library),
+    device-resident CSR and outputs, max over ranks; fill reported beside."""
     import torch
 
     import paper_2602_00898_b200 as mp
-    from paper_2602_00898_b200 import subtree as st
-    from paper_2602_00898_b200._lib import MpCsr, check, lib
+    from paper_2602_00898_b200 import api
 
     ws, rank, local = dist_setup()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     _, g = product_graph("c3")
-    n = g.n
+    n, m2 = g.n, int(g.offsets[-1])
     L = mp.default_nd_level(n)
     nn = (1 << (L + 1)) - 1
     ctx = mp.Context(local)
     stream = torch.cuda.Stream(device=dev)
     ctx.set_stream(stream.cuda_stream)
+    if ws > 1:
+        import torch.distributed as dist
+        uid = [mp.Comm.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = mp.Comm.nccl(rank, ws, local, uid[0])
+    else:
+        comm = mp.Comm.from_allgather(0, 1, lambda b: b)
     d_off = torch.from_numpy(g.offsets).to(dev)
     d_nbr = torch.from_numpy(g.neighbors).to(dev)
-    patch_of = torch.empty(n, dtype=torch.int32, device=dev)
-    node_off = torch.empty(nn + 1, dtype=torch.int32, device=dev)
-    node_verts = torch.empty(n, dtype=torch.int32, device=dev)
-    lp = torch.zeros(n, dtype=torch.int32, device=dev)
-    perm = torch.zeros(n, dtype=torch.int32, device=dev)
-    inv = torch.empty(n, dtype=torch.int32, device=dev)
-    mask = torch.empty(nn, dtype=torch.uint8, device=dev)
+    outs = {k: torch.empty(nn + 1 if k == "tree_node_offsets" else n, dtype=torch.int32, device=dev)
+            for k in ("patch_of", "tree_node_offsets", "tree_vertices", "tree_local_perm", "perm", "inverse",
+                      "etree_parent")}
+    outs["column_counts"] = torch.empty(n, dtype=torch.int64, device=dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    csr = MpCsr(n, C.c_void_p(d_off.data_ptr()), C.c_void_p(d_nbr.data_ptr()), 1)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    import ctypes as C
+    from paper_2602_00898_b200._lib import MpCsr, MpResult, check, lib
 
-    def step():
+    def call(want_fill):
+        cfg = api.make_config(want_fill=want_fill)
+        csr = MpCsr(n, C.c_void_p(d_off.data_ptr()), C.c_void_p(d_nbr.data_ptr()), 1)
+        r = MpResult()
+        r.on_device = 1
+        for k, v in outs.items():
+            setattr(r, k, C.c_void_p(v.data_ptr()))
         with torch.cuda.stream(stream):
             flush.fill_(1)
-            ev[0].record(stream)
-            pc = C.c_int32()
-            check(lib().mp_compute_patches(ctx.handle, C.byref(csr), 256, C.c_uint64(0),
-                                           C.c_void_p(patch_of.data_ptr()), 1, C.byref(pc)))
-            ev[1].record(stream)
-            check(lib().mp_build_etree(ctx.handle, C.byref(csr), C.c_void_p(patch_of.data_ptr()), pc.value, L,
-                                       C.c_uint64(0), C.c_void_p(node_off.data_ptr()),
-                                       C.c_void_p(node_verts.data_ptr()), 1))
-            ev[2].record(stream)
-            h_off = node_off.cpu().numpy()
-            own = st.owners(h_off, L, ws)
-            mask.copy_(torch.from_numpy((own == rank).astype(np.uint8)))
-            st.order_subtrees_device(ctx, n, d_off.data_ptr(), d_nbr.data_ptr(), L, node_off.data_ptr(),
-                                     node_verts.data_ptr(), mask.data_ptr(), lp.data_ptr(), perm.data_ptr())
-            ev[3].record(stream)
-            st.gather_perm(perm, h_off, L, own, ws, rank)
-            inv.scatter_(0, perm.long(), torch.arange(n, dtype=torch.int32, device=dev))
-            ev[4].record(stream)
-        stream.synchronize()
-        return [ev[i].elapsed_time(ev[i + 1]) for i in range(4)], own
+        check(lib().mp_order_sharded(ctx.handle, C.byref(csr), C.byref(cfg), C.byref(comm.struct), C.byref(r)))
+        return r
 
     for _ in range(args.warmup):
-        step()
+        call(False)
     barrier(ws)
-    rows = []
+    rows, launches = [], 0
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
-            parts, own = step()
-            rows.append(parts)
+            r = call(False)
+            rows.append([r.stage_ms[i] for i in range(5)])
+            launches += r.kernel_launches
     barrier(ws)
     rows = np.array(rows)
     ms = max_over_ranks(float(rows.sum(1).mean()), ws)
     parts = [max_over_ranks(float(x), ws) for x in rows.mean(0)]
+    owned = int(r.work[15])
+    perm_sha = digest(outs["perm"].cpu().numpy())
+    # one call with the fill on: nnz(L), column counts and parents vs the golden
+    rf = call(True)
+    fill_ms = max_over_ranks(float(rf.stage_ms[5]), ws)
     gold = golden("c3")
-    sha = digest(perm.cpu().numpy())
+    parity = {"sha_perm": perm_sha, "nnz_L": int(rf.nnz_L), "sha_column_counts": digest(outs["column_counts"].cpu().numpy()),
+              "sha_parents": digest(outs["etree_parent"].cpu().numpy())}
+    if gold:
+        parity["match"] = bool(perm_sha == gold["sha_perm"] and parity["nnz_L"] == gold["nnz_L"]
+                               and parity["sha_column_counts"] == gold["sha_column_counts"]
+                               and parity["sha_parents"] == gold["sha_parents"])
+    comm.close()
     if rank == 0:
-        sizes = np.diff(node_off.cpu().numpy())
         peak, peak_src = peaks()
-        m = int(g.offsets[-1]) // 2
-        path_bytes = alg_bytes(n, m, L, 0, "path")
+        path_bytes = alg_bytes(n, m2 // 2, L, 0, "path")
         cpu = {"value": round(gold["reference_s"] * 1e3, 1) if gold else None, "unit": "ms", "cores": 8,
                "kind": "reference",
-               "sample": "recorded, not re-run per session: the full 10M ordering + fill by the reference core "
-                         "(tests/golden/make_golden.py --c3, 8-core build container, order_tree_nodes threads=16)"}
+               "sample": "recorded, not re-run per session (12.6 min): the full 10M ordering + fill by the reference "
+                         "core (tests/golden/make_golden.py --c3, 8-core build container, order_tree_nodes threads=16)"}
         line = {
             "metric": METRIC_C3, "value": round(ms, 3), "unit": "ms", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 3), "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": WORKLOADS["c3"][2], "n": n, "nd_level": L, "parallelism": f"subtrees{ws}",
-                       "l2_flush": "512 MiB write before every step"},
-            "vertices_per_s": round(n / (ms * 1e-3), 1),
-            "stage_ms_max_over_ranks": {"patch": round(parts[0], 3), "etree": round(parts[1], 3),
-                                        "local+assemble (own subtrees)": round(parts[2], 3),
-                                        "gather+inverse": round(parts[3], 3)},
-            "rank0_vertices_owned": int(sizes[own == 0].sum()),
-            "parity": {"sha_perm": sha, "golden": gold.get("sha_perm") if gold else None,
-                       "match": bool(gold and sha == gold["sha_perm"])},
+                       "shard_level": int(np.ceil(np.log2(ws))) if ws > 1 else 0,
+                       "l2_flush": "512 MiB write before every step", "csr_sha256": csr_sha(g)},
+            "vertices_per_s": round(n / (ms * 1e-3), 1), "fill_ms": round(fill_ms, 3),
+            "stage_ms_max_over_ranks": dict(zip(STAGES, [round(x, 3) for x in parts])),
+            "rank0_vertices_ordered": owned, "gpu_launches": int(launches), "parity": parity,
             "roofline": {"bound": "hbm", "kernel": "path", "achieved": round(path_bytes / (ms * 1e-3) / 1e9, 2),
                          "peak": peak, "peak_source": peak_src, "unit": "GB/s",
                          "frac": round(path_bytes / (ms * 1e-3) / 1e9 / peak, 6), "traffic": None,

@@ -140,6 +140,41 @@ int mp_order(mp_context* ctx, const mp_csr* g, const mp_config* cfg, mp_result* 
 int mp_order_batch(mp_context* const* ctxs, int32_t nctx, int32_t count, const mp_csr* graphs,
                    const mp_config* cfgs, mp_result* results, int32_t* status);
 
+/* ---- multi-GPU: one very large mesh sharded over ranks (C3) ----
+ * One process (or host thread) per GPU, each with its own context, calls
+ * mp_order_sharded with the same graph and config.  Every rank computes the
+ * patches and the top k = ceil(log2 world) ND levels (sequential chains:
+ * replicated, not shipped); the level-k subtrees are then dealt to ranks by
+ * size (largest first, least-loaded rank), each rank splits, orders (MD) and
+ * plays the fill game on its own subtrees only, and three all-gathers
+ * exchange (1) node sizes, (2) the owned nodes' vertex lists + local orders,
+ * (3) the subtree roots' live elements and the owned column counts /
+ * parents.  Every rank returns the complete, rank-count-independent
+ * mp_result -- bit-identical to mp_order.
+ *
+ * The all-gather is the caller's or the library's NCCL one: recv receives
+ * world * bytes, rank r's contribution at r * bytes.  device_buffers = 1:
+ * send / recv are device memory of the context's GPU and the collective is
+ * enqueued on `stream` (NCCL); 0: host memory (e.g. an MPI or gloo
+ * all-gather), stream unused. */
+typedef struct {
+  int32_t rank, world;
+  int32_t device_buffers;
+  int (*allgather)(void* user, const void* send, void* recv, int64_t bytes, void* stream);
+  void* user;
+} mp_comm;
+
+int mp_order_sharded(mp_context* ctx, const mp_csr* g, const mp_config* cfg, const mp_comm* comm, mp_result* out);
+
+/* NCCL plumbing for mp_comm (libnccl.so.2 is loaded on first use, so the
+ * library has no link-time NCCL dependency).  Rank 0 creates the unique id
+ * and ships its 128 bytes to the other ranks out of band; every rank then
+ * creates its communicator on its GPU.  mp_nccl_comm_init fills comm with
+ * the library's ncclAllGather (device_buffers = 1). */
+int mp_nccl_get_unique_id(uint8_t id[128]);
+int mp_nccl_comm_init(mp_comm* comm, const uint8_t id[128], int32_t world, int32_t rank, int32_t device);
+void mp_nccl_comm_destroy(mp_comm* comm);
+
 /* ---- stage entry points (reference free functions) ---- */
 /* etree.hpp:35-36 default_nd_level */
 int32_t mp_default_nd_level(int32_t n);

@@ -12,6 +12,7 @@ from .api import (  # noqa: F401
     make_torus_mesh, mesh_to_graph, mesh_to_graph_device, pattern_to_graph_device, lift_patches, run_baseline,
     BASELINES, PatchReport, validate_user_patches, order, order_batch, order_device, order_subtrees, order_tree_nodes, tree_fill, tree_separation_violations,
     elimination_fill, factor_etree_parents, cross_block_fill, validate_schedule, schedule_nodes,
+    Comm, order_sharded,
 )
 from .formats import (  # noqa: F401
     BenchRow, bench_row, csv_header, run_baselines, write_csv, parse_matrix_market, parse_mesh, parse_obj, parse_off, read_patch_file, read_permutation, write_etree,

@@ -62,6 +62,20 @@ class MpResult(C.Structure):
     ]
 
 
+# int allgather(void* user, const void* send, void* recv, int64_t bytes, void* stream)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+
+
+class MpComm(C.Structure):  # mp_comm (include/meshperm_b200.h)
+    _fields_ = [
+        ("rank", C.c_int32),
+        ("world", C.c_int32),
+        ("device_buffers", C.c_int32),
+        ("allgather", C.c_void_p),
+        ("user", C.c_void_p),
+    ]
+
+
 class MpBenchRow(C.Structure):  # pipeline.hpp:39-54 BenchRow
     _fields_ = [
         ("input", C.c_char_p),
@@ -127,6 +141,11 @@ SIGNATURES = [
       C.POINTER(C.c_double)]),
     ("mp_cross_block_fill", C.c_int,
      [C.c_void_p, C.POINTER(MpCsr), C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, i64p]),
+    ("mp_order_sharded", C.c_int,
+     [C.c_void_p, C.POINTER(MpCsr), C.POINTER(MpConfig), C.POINTER(MpComm), C.POINTER(MpResult)]),
+    ("mp_nccl_get_unique_id", C.c_int, [C.c_void_p]),
+    ("mp_nccl_comm_init", C.c_int, [C.POINTER(MpComm), C.c_void_p, C.c_int32, C.c_int32, C.c_int32]),
+    ("mp_nccl_comm_destroy", None, [C.POINTER(MpComm)]),
     ("mp_grid_mesh_triangles", C.c_int64, [C.c_int32, C.c_int32]),
     ("mp_make_grid_mesh", C.c_int, [C.c_int32, C.c_int32, C.c_void_p]),
     ("mp_make_random_mesh", C.c_int, [C.c_int32, C.c_int32, C.c_uint64, C.c_void_p]),

@@ -13,7 +13,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import LOCAL_MODES, SCHEDULES, MpConfig, MpCsr, MpResult, check, lib
+from ._lib import ALLGATHER_FN, LOCAL_MODES, SCHEDULES, MpComm, MpConfig, MpCsr, MpResult, check, lib
 
 
 # ----------------------------------------------------------------- data model
@@ -608,3 +608,97 @@ def order_device(ctx: Context, n: int, offsets_ptr: int, neighbors_ptr: int, out
         setattr(res, k, C.c_void_p(v))
     check(lib().mp_order(ctx.handle, C.byref(csr), C.byref(cfg), C.byref(res)))
     return res
+
+
+# ----------------------------------------------------------------- multi-GPU (C3)
+class Comm:
+    """mp_comm: this rank, the world size and an all-gather.
+
+    * Comm.nccl(rank, world, device, unique_id): the library's own NCCL
+      communicator (device buffers on the context's stream); rank 0 makes
+      the id with Comm.nccl_unique_id() and ships it to the others.
+    * Comm.from_allgather(rank, world, fn): fn(send: bytes) -> bytes of
+      world * len(send), rank-major (host buffers: gloo, MPI, threads ...).
+    * Comm.torch_distributed(): from_allgather over the current
+      torch.distributed group (CPU tensors, e.g. the gloo backend).
+    """
+
+    def __init__(self):
+        self.struct = MpComm()
+        self._fn = None
+        self._nccl = False
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(lib().mp_nccl_get_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def nccl(cls, rank: int, world: int, device: int, unique_id: bytes) -> "Comm":
+        c = cls()
+        uid = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        check(lib().mp_nccl_comm_init(C.byref(c.struct), uid, world, rank, device))
+        c._nccl = True
+        return c
+
+    @classmethod
+    def from_allgather(cls, rank: int, world: int, fn) -> "Comm":
+        c = cls()
+
+        def trampoline(user, send, recv, nbytes, stream):
+            try:
+                data = C.string_at(send, nbytes) if nbytes else b""
+                got = fn(data)
+                if len(got) != world * nbytes:
+                    return 1
+                if got:
+                    C.memmove(recv, got, len(got))
+                return 0
+            except Exception:  # never raise across the C boundary
+                return 2
+
+        c._fn = ALLGATHER_FN(trampoline)
+        c.struct.rank, c.struct.world, c.struct.device_buffers = rank, world, 0
+        c.struct.allgather = C.cast(c._fn, C.c_void_p)
+        c.struct.user = None
+        return c
+
+    @classmethod
+    def torch_distributed(cls, group=None) -> "Comm":
+        import torch
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+
+        def fn(data: bytes) -> bytes:
+            t = torch.frombuffer(bytearray(data), dtype=torch.uint8) if data else torch.empty(0, dtype=torch.uint8)
+            out = torch.empty(world * len(data), dtype=torch.uint8)
+            dist.all_gather_into_tensor(out, t, group=group)
+            return out.numpy().tobytes()
+
+        return cls.from_allgather(rank, world, fn)
+
+    def close(self):
+        if self._nccl:
+            lib().mp_nccl_comm_destroy(C.byref(self.struct))
+            self._nccl = False
+
+
+def order_sharded(g: AdjacencyGraph, comm: Comm, patch_size: int = 256, nd_level: int = -1, seed: int = 0,
+                  local_mode="approx_md", schedule="postorder", want_fill: bool = True,
+                  ctx: Context | None = None) -> PipelineResult:
+    """mp_order_sharded: one mesh ordered by `comm.world` ranks together (each
+    calls this with the same graph); every rank returns the complete result,
+    identical to order()."""
+    ctx = ctx or default_context()
+    cfg = make_config(patch_size, nd_level, seed, local_mode, schedule if isinstance(schedule, str) else "postorder",
+                      1, want_fill)
+    custom = None if isinstance(schedule, str) else _nonempty(_i32(schedule))
+    if custom is not None:
+        cfg.schedule_nodes = C.c_void_p(custom.ctypes.data)
+        cfg.schedule_len = len(schedule)
+    bufs, res = _prepare(g, nd_level, 1, want_fill)
+    check(lib().mp_order_sharded(ctx.handle, C.byref(_csr(g)), C.byref(cfg), C.byref(comm.struct), C.byref(res)))
+    r = _finish(g, bufs, res, patch_size, 1, want_fill)
+    r.work = [int(res.work[i]) for i in range(16)]
+    return r

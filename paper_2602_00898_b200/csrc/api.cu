@@ -14,6 +14,7 @@
 
 #include "mp_context.h"
 #include "mp_device.cuh"
+#include "mp_host.h"
 
 namespace mp {
 
@@ -70,57 +71,6 @@ struct NvtxStages {
   }
   ~NvtxStages() { end(); }
 };
-
-int32_t default_nd_level_host(int32_t n) {  // etree.cpp:42-46
-  int32_t level = 0;
-  for (int32_t x = n / 512; x > 1; x >>= 1) ++level;
-  return std::min<int32_t>(8, level);
-}
-
-// Device view of a caller CSR (copied when it is host memory).
-struct GraphView {
-  DevBuf<int32_t> off, nbr;
-  DGraph g{};
-  int64_t m2 = 0;
-};
-
-void make_view(mp_context& ctx, const mp_csr* c, GraphView& gv) {
-  if (!c) throw Error(MP_EINVAL, "null graph");
-  if (c->n < 0) throw Error(MP_EINVAL, "negative vertex count");
-  cudaStream_t s = ctx.stream;
-  const int32_t n = c->n;
-  if (c->on_device) {
-    int32_t m2 = 0;
-    MP_CUDA(cudaMemcpyAsync(&m2, c->offsets + n, 4, cudaMemcpyDeviceToHost, s));
-    MP_CUDA(cudaStreamSynchronize(s));
-    gv.g = {n, c->offsets, c->neighbors};
-    gv.m2 = m2;
-  } else {
-    gv.m2 = c->offsets[n];
-    gv.off.alloc(n + 1, s);
-    gv.nbr.alloc(std::max<int64_t>(gv.m2, 1), s);
-    MP_CUDA(cudaMemcpyAsync(gv.off.get(), c->offsets, sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice, s));
-    if (gv.m2)
-      MP_CUDA(cudaMemcpyAsync(gv.nbr.get(), c->neighbors, sizeof(int32_t) * gv.m2, cudaMemcpyHostToDevice, s));
-    gv.g = {n, gv.off.get(), gv.nbr.get()};
-  }
-}
-
-// Input array: device pointer as-is, or a device copy of host memory.
-template <class T>
-const T* input_ptr(mp_context& ctx, const T* p, int64_t count, bool on_device, DevBuf<T>& hold) {
-  if (on_device || !p) return p;
-  hold.alloc(std::max<int64_t>(count, 1), ctx.stream);
-  if (count) MP_CUDA(cudaMemcpyAsync(hold.get(), p, sizeof(T) * count, cudaMemcpyHostToDevice, ctx.stream));
-  return hold.get();
-}
-
-template <class T>
-void output_copy(mp_context& ctx, T* dst, const T* src, int64_t count, bool on_device) {
-  if (!dst || count == 0) return;
-  MP_CUDA(cudaMemcpyAsync(dst, src, sizeof(T) * count,
-                          on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, ctx.stream));
-}
 
 // expand_blocks (assemble.cpp:87-114) for the tree, and the closed-form
 // expansion of column counts / parents.
@@ -595,20 +545,7 @@ int mp_order(mp_context* ctx, const mp_csr* g, const mp_config* cfg, mp_result* 
         lp(std::max(n, 1), s), pm(std::max<int64_t>(N, 1), s), inv(std::max<int64_t>(N, 1), s), pos(nn + 1, s);
     MP_CUDA(cudaEventRecord(ctx->ev[1], s));
     stage.next("mp_order/patch");
-    int32_t pc = 0;
-    if (cfg->user_patches) {  // pipeline.cpp:102-111: validate, split disconnected patches
-      DevBuf<int32_t> hold;
-      const int32_t* user = input_ptr(*ctx, cfg->user_patches, n, g->on_device != 0, hold);
-      const UserPatchReport rep = validate_user_patches_dev(*ctx, gv.g, user, cfg->user_patch_count);
-      if (!rep.disconnected.empty()) {
-        pc = enforce_connectivity_dev(*ctx, gv.g, user, cfg->user_patch_count, asg);
-      } else {
-        pc = cfg->user_patch_count;
-        if (n > 0) MP_CUDA(cudaMemcpyAsync(asg, user, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
-      }
-    } else {
-      pc = compute_patches_dev(*ctx, gv.g, cfg->patch_size, cfg->seed, asg);
-    }
+    const int32_t pc = patch_stage(*ctx, gv, cfg, g->on_device != 0, asg);
     MP_CUDA(cudaEventRecord(ctx->ev[2], s));
     stage.next("mp_order/quotient");
     // the per-level quotient is rebuilt inside the level loop (ndtree.cu), so

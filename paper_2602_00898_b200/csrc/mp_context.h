@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <vector>
 
 #include "mp_internal.h"
@@ -109,11 +110,21 @@ struct UserPatchReport {
 };
 UserPatchReport validate_user_patches_dev(mp_context& ctx, const DGraph& g, const int32_t* in, int32_t patch_count);
 
+// Sharded ND (mp_order_sharded): every rank splits the top k
+// levels; at level k the subtrees are dealt to ranks (owner[i] = rank for
+// nodes of level >= k, -1 above) and a rank splits only its own subtrees
+// further -- the others stay whole in their level-k root in its local tree.
+struct ShardSpec {
+  int32_t rank = 0, world = 1, k = 0;
+  std::vector<int32_t> owner;  // out: nn entries
+};
+std::vector<int32_t> deal_subtrees(const std::vector<int64_t>& root_size, int32_t k, int32_t L, int32_t world);
+
 // ND tree (ndtree.cu).  node_of[v] receives the tree node of every vertex;
 // node_offsets (nn+1) / node_vertices (n) the flattened EliminationTree.
 void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assignment,
                      int32_t patch_count, int32_t nd_level, int32_t* node_of,
-                     int32_t* node_offsets, int32_t* node_vertices);
+                     int32_t* node_offsets, int32_t* node_vertices, ShardSpec* shard = nullptr);
 
 // Quotient (ndtree.cu): node weights (P) + positive edges, device outputs; returns #edges.
 int64_t build_quotient_dev(mp_context& ctx, const DGraph& g, const int32_t* assignment,
@@ -149,12 +160,25 @@ void compute_perm_partial_dev(mp_context& ctx, int32_t n, int32_t nd_level, cons
                               const int32_t* node_vertices, const int32_t* local_perm, const Schedule& schedule,
                               const uint8_t* node_mask, int32_t* perm);
 
+// Sharded game (mp_order_sharded): this rank plays the nodes of its own
+// subtrees below level k (owner[i] == rank), hands their level-k roots' live
+// elements to `exchange` (an all-gather returning every rank's buffer,
+// concatenated), imports the others', then plays levels k-1..0 itself.
+// Column counts / parents are then valid at the positions of its own nodes
+// and of the top nodes; nnz_L / cost are left to the caller's gather.
+struct FillShard {
+  int32_t rank = 0, k = 0;
+  std::vector<int32_t> owner;
+  std::function<std::vector<int32_t>(const std::vector<int32_t>&)> exchange;
+};
 // Symbolic (symbolic.cu): column counts (by position) and factor etree parents.
 void tree_fill_dev(mp_context& ctx, const DGraph& g, int32_t nd_level, const int32_t* node_of,
                    const int32_t* node_offsets, const int32_t* node_vertices,
                    const int32_t* local_perm, const int32_t* node_pos, const int32_t* inverse,
                    int64_t* column_counts, int32_t* etree_parent, int64_t* nnz_L, int64_t* cost,
-                   const int32_t* cross_owner = nullptr, int64_t* crossing = nullptr);
+                   const int32_t* cross_owner = nullptr, int64_t* crossing = nullptr,
+                   const FillShard* shard = nullptr);
+void sum_counts_dev(mp_context& ctx, int64_t n, const int64_t* column_counts, int64_t* nnz_L, int64_t* cost);
 // The same game for any permutation (one-node tree): elimination_fill,
 // factor_etree_parents and, with cross_owner, cross_block_fill's count.
 void elimination_game_dev(mp_context& ctx, const DGraph& g, const int32_t* perm, int64_t* column_counts,

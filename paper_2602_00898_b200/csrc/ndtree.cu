@@ -91,6 +91,7 @@ struct LevelArgs {
   const int32_t* ell;      // n * 8 ELL adjacency
   int64_t fm_smem_bytes;   // dynamic shared memory of the FM launch
   int32_t* fm_moves;
+  const uint8_t* own_mask; // sharded build (mp_order_sharded): nodes this rank splits; NULL = all
 };
 
 __global__ void level_weights(LevelArgs a) {
@@ -110,6 +111,9 @@ __global__ void level_activity(LevelArgs a, int32_t nd_level, int32_t level, int
   for (int32_t li = blockIdx.x * blockDim.x + threadIdx.x; li < a.width; li += gridDim.x * blockDim.x) {
     // etree.cpp:123-131: leaf at nd_level, below 2 vertices, or <= 1 alive patch
     bool act = level < nd_level && a.seg_cnt[li] >= 2 && a.np_node[li] >= 2;
+    // sharded build: subtrees below the shard level that another rank owns
+    // stay whole in their level-k root here (that rank splits them)
+    if (a.own_mask && !a.own_mask[a.first + li]) act = false;
     a.active[li] = act ? 1 : 0;
     if (act) atomicAdd(n_active, 1);
   }
@@ -1335,8 +1339,34 @@ int64_t build_quotient_dev(mp_context& ctx, const DGraph& g, const int32_t* assi
   return U;
 }
 
+// Level-k subtrees dealt to ranks: largest first (vertex count of the
+// level-k node = the whole subtree), each to the least-loaded rank (ties:
+// lower rank, then lower node id).  Deterministic from the tree alone.
+std::vector<int32_t> deal_subtrees(const std::vector<int64_t>& root_size, int32_t k, int32_t L, int32_t world) {
+  const int32_t nn = static_cast<int32_t>((1LL << (L + 1)) - 1);
+  const int32_t first = (1 << k) - 1, width = 1 << k;
+  std::vector<int32_t> owner(nn, -1), order(width);
+  for (int32_t j = 0; j < width; ++j) order[j] = j;
+  std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return root_size[x] > root_size[y]; });
+  std::vector<int64_t> load(world, 0);
+  for (int32_t j : order) {
+    const int32_t dst = static_cast<int32_t>(std::min_element(load.begin(), load.end()) - load.begin());
+    load[dst] += root_size[j];
+    // the whole subtree of root first+j
+    std::vector<int32_t> st{first + j};
+    while (!st.empty()) {
+      const int32_t i = st.back();
+      st.pop_back();
+      if (i >= nn) continue;
+      owner[i] = dst;
+      st.push_back(2 * i + 1), st.push_back(2 * i + 2);
+    }
+  }
+  return owner;
+}
+
 void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, int32_t P, int32_t L,
-                     int32_t* node_of, int32_t* node_offsets, int32_t* node_vertices) {
+                     int32_t* node_of, int32_t* node_offsets, int32_t* node_vertices, ShardSpec* shard) {
   if (L < 0 || L > kMaxNdLevel) throw Error(MP_EINVAL, "nd_level out of range");
   cudaStream_t s = ctx.stream;
   const int32_t n = g.n;
@@ -1376,6 +1406,8 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
   MP_CUDA(cudaMemcpyAsync(seg_cnt.get(), &n, 4, cudaMemcpyHostToDevice, s));
   int32_t* cur_list = vl_a.get();
   int32_t* nxt_list = vl_b.get();
+  DevBuf<uint8_t> own_mask;  // sharded build: set at the shard level
+  if (shard) shard->owner.assign(nn, -1);
 
   SectionTimer st(s, "etree");
   st.mark("setup");
@@ -1400,6 +1432,19 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     a.vside = vside, a.ell = ell;
     a.stats = ctx.dwork ? ctx.dwork + 1 : stats.get(), a.fm_gain = fm_gain, a.fm_moves = fm_moves;
     const dim3 lgrid(std::max(1, grid_for(ctx, n) / std::max(1, width)), std::min(width, 65535));
+    if (shard && level == shard->k && shard->world > 1) {
+      // the shard level: deal the level-k subtrees by their vertex counts
+      std::vector<int32_t> hc(width);
+      MP_CUDA(cudaMemcpyAsync(hc.data(), seg_cnt.get(), sizeof(int32_t) * width, cudaMemcpyDeviceToHost, s));
+      MP_CUDA(cudaStreamSynchronize(s));
+      shard->owner = deal_subtrees(std::vector<int64_t>(hc.begin(), hc.end()), level, L, shard->world);
+      std::vector<uint8_t> hm(nn);
+      for (int64_t i = 0; i < nn; ++i) hm[i] = shard->owner[i] < 0 || shard->owner[i] == shard->rank;
+      own_mask.alloc(nn, s);
+      MP_CUDA(cudaMemcpyAsync(own_mask.get(), hm.data(), nn, cudaMemcpyHostToDevice, s));
+      MP_CUDA(cudaStreamSynchronize(s));
+    }
+    a.own_mask = own_mask.get();
     MP_KERNEL(ctx, level_weights<<<lgrid, 256, 0, s>>>(a));
     MP_KERNEL(ctx, level_patch_counts<<<grid_for(ctx, P), 256, 0, s>>>(a));
     MP_KERNEL(ctx, level_activity<<<grid_for(ctx, width), 256, 0, s>>>(a, L, level, cnt.get()));

@@ -20,6 +20,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <functional>
+#include <utility>
 #include <vector>
 
 #include "mp_context.h"
@@ -71,6 +73,7 @@ struct SymArgs {
   // the pivot's (NULL: not counted)
   const int32_t* cross_owner;
   unsigned long long* cross_count;
+  const uint8_t* play_mask;  // sharded game: nodes this rank plays (NULL = all)
 };
 
 // private index of w (in node A, an ancestor-or-self of the CTA's node)
@@ -90,6 +93,7 @@ __global__ void __launch_bounds__(kSymWide) sym_kernel(SymArgs a) {
   const int32_t first = (1 << a.level) - 1;
   const int32_t X = first + blockIdx.x;
   if (X >= a.nn) return;
+  if (a.play_mask && !a.play_mask[X]) return;  // another rank plays this node
   if (*static_cast<volatile int32_t*>(a.overflow)) return;  // an earlier node ran out of pool
   const int32_t xb = a.node_offsets[X], nx = a.node_offsets[X + 1] - xb;
   const int32_t lc = 2 * X + 1, rc = 2 * X + 2;
@@ -345,17 +349,55 @@ __global__ void sum_counts(int32_t n, const int64_t* cc, unsigned long long* out
     atomicAdd(&out[1], static_cast<unsigned long long>(q));
   }
 }
+// element records [e, |boundary|, boundary...] at rec_off[i] (export of a
+// subtree root's live elements, mp_order_sharded)
+__global__ void pack_elements(int32_t ne, const int32_t* elems, const int64_t* rec_off, const int64_t* bptr,
+                              const int32_t* bsz, const int32_t* pool, int32_t* out) {
+  const int lane = threadIdx.x & 31;
+  for (int32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < ne; i += (gridDim.x * blockDim.x) >> 5) {
+    const int32_t e = elems[i], sz = bsz[e];
+    int32_t* o = out + rec_off[i];
+    if (lane == 0) o[0] = e, o[1] = sz;
+    const int32_t* src = pool + bptr[e];
+    for (int32_t j = lane; j < sz; j += 32) o[2 + j] = src[j];
+  }
+}
+__global__ void gather_bsz(int32_t ne, const int32_t* elems, const int32_t* bsz, int32_t* out) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ne; i += gridDim.x * blockDim.x) out[i] = bsz[elems[i]];
+}
+// import: element i gets boundary pool[base + off[i] ..) of size sz[i]
+__global__ void set_elements(int32_t ne, const int32_t* elems, const int32_t* sz, const int64_t* off, int64_t base,
+                             int64_t* bptr, int32_t* bsz) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ne; i += gridDim.x * blockDim.x) {
+    bptr[elems[i]] = base + off[i];
+    bsz[elems[i]] = sz[i];
+  }
+}
 __global__ void clear_bsz(int32_t n, int32_t* bsz) {
   for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) bsz[i] = 0;
 }
 
 }  // namespace
 
+void sum_counts_dev(mp_context& ctx, int64_t n, const int64_t* column_counts, int64_t* nnz_L, int64_t* cost) {
+  cudaStream_t s = ctx.stream;
+  *nnz_L = 0, *cost = 0;
+  if (n == 0) return;
+  DevBuf<unsigned long long> sums(2, s);
+  MP_CUDA(cudaMemsetAsync(sums, 0, 16, s));
+  MP_KERNEL(ctx, sum_counts<<<grid_for(ctx, n), 256, 0, s>>>(static_cast<int32_t>(n), column_counts, sums));
+  unsigned long long h[2];
+  MP_CUDA(cudaMemcpyAsync(h, sums, 16, cudaMemcpyDeviceToHost, s));
+  MP_CUDA(cudaStreamSynchronize(s));
+  *nnz_L = static_cast<int64_t>(h[0]);
+  *cost = static_cast<int64_t>(h[1]);
+}
+
 void tree_fill_dev(mp_context& ctx, const DGraph& g, int32_t L, const int32_t* node_of,
                    const int32_t* node_offsets, const int32_t* node_vertices, const int32_t* local_perm,
                    const int32_t* node_pos, const int32_t* inverse, int64_t* column_counts,
                    int32_t* etree_parent, int64_t* nnz_L, int64_t* cost, const int32_t* cross_owner,
-                   int64_t* crossing) {
+                   int64_t* crossing, const FillShard* shard) {
   cudaStream_t s = ctx.stream;
   const int32_t n = g.n;
   const int32_t nn = static_cast<int32_t>((1LL << (L + 1)) - 1);
@@ -402,9 +444,23 @@ void tree_fill_dev(mp_context& ctx, const DGraph& g, int32_t L, const int32_t* n
       left_cnt(nn, s), left_list(std::max<int64_t>(left_off[nn], 1), s), overflow(1, s);
   DevBuf<int64_t> bptr(n, s), d_left_off(nn + 1, s), d_ws_off((static_cast<size_t>(1) << L) + 1, s);
   DevBuf<int32_t> adj(std::max(m2, 1), s), el(std::max(m2, 1), s);
-  DevBuf<unsigned long long> cursor(1, s), sums(2, s), cross(1, s);
+  DevBuf<unsigned long long> cursor(1, s), cross(1, s);
+  DevBuf<uint8_t> play_mask;
   MP_KERNEL(ctx, local_of_kernel<<<grid_for(ctx, n), 256, 0, s>>>(n, node_of, node_offsets, node_vertices, local_of));
   MP_CUDA(cudaMemcpyAsync(d_left_off, left_off.data(), sizeof(int64_t) * (nn + 1), cudaMemcpyHostToDevice, s));
+  // sharded game (mp_order_sharded): this rank plays its own subtrees below
+  // the shard level, exchanges their roots' live elements, then every rank
+  // plays the top levels
+  const bool sharded = shard && shard->k > 0 && shard->k <= L;
+  const int32_t k = sharded ? shard->k : 0;
+  if (sharded) {
+    std::vector<uint8_t> hm(nn);
+    for (int32_t i = 0; i < nn; ++i) hm[i] = shard->owner[i] < 0 || shard->owner[i] == shard->rank;
+    play_mask.alloc(nn, s);
+    MP_CUDA(cudaMemcpyAsync(play_mask.get(), hm.data(), nn, cudaMemcpyHostToDevice, s));
+  }
+  std::vector<int32_t> received;  // all ranks' exported roots (the collective runs once)
+  bool exchanged = false;
   // boundary pool: sum of reach sizes = nnz(L) - n; start from the ratio seen
   // on earlier calls of this context, grow and replay on overflow
   int64_t cap = std::max<int64_t>(48LL * n, static_cast<int64_t>(ctx.sym_pool_ratio * 1.25 * n)) + 4096;
@@ -423,34 +479,156 @@ void tree_fill_dev(mp_context& ctx, const DGraph& g, int32_t L, const int32_t* n
     a.overflow = overflow;
     a.cross_owner = cross_owner, a.cross_count = cross;
     MP_CUDA(cudaMemsetAsync(cross, 0, sizeof(unsigned long long), s));
-    for (int32_t l = L; l >= 0; --l) {
-      const int32_t width = 1 << l;
-      MP_CUDA(cudaMemcpyAsync(d_ws_off, ws_offs[l].data(), sizeof(int64_t) * (width + 1), cudaMemcpyHostToDevice, s));
-      a.level = l;
-      a.ws_off = d_ws_off;
-      a.smem_path = smem_path[l];
-      const size_t dyn = 8 * static_cast<size_t>(smem_path[l]);
-      { const int kt__ = ctx.ktime_begin(kKSym); MP_KERNEL(ctx, sym_kernel<<<width, 2 * width <= ctx.num_sms ? kSymWide : kSymThreads, dyn, s>>>(a)); ctx.ktime_end(kt__); }
-    }
-    int32_t h_over = 0;
+    auto play = [&](int32_t hi, int32_t lo, const uint8_t* mask) {
+      a.play_mask = mask;
+      for (int32_t l = hi; l >= lo; --l) {
+        const int32_t width = 1 << l;
+        MP_CUDA(cudaMemcpyAsync(d_ws_off, ws_offs[l].data(), sizeof(int64_t) * (width + 1), cudaMemcpyHostToDevice, s));
+        a.level = l;
+        a.ws_off = d_ws_off;
+        a.smem_path = smem_path[l];
+        const size_t dyn = 8 * static_cast<size_t>(smem_path[l]);
+        const int kt = ctx.ktime_begin(kKSym);
+        MP_KERNEL(ctx, sym_kernel<<<width, 2 * width <= ctx.num_sms ? kSymWide : kSymThreads, dyn, s>>>(a));
+        ctx.ktime_end(kt);
+      }
+    };
+    auto overflowed = [&](unsigned long long* used) {
+      int32_t h_over = 0;
+      MP_CUDA(cudaMemcpyAsync(&h_over, overflow, 4, cudaMemcpyDeviceToHost, s));
+      MP_CUDA(cudaMemcpyAsync(used, cursor, 8, cudaMemcpyDeviceToHost, s));
+      MP_CUDA(cudaStreamSynchronize(s));
+      return h_over != 0;
+    };
     unsigned long long used = 0;
-    MP_CUDA(cudaMemcpyAsync(&h_over, overflow, 4, cudaMemcpyDeviceToHost, s));
-    MP_CUDA(cudaMemcpyAsync(&used, cursor, 8, cudaMemcpyDeviceToHost, s));
-    MP_CUDA(cudaStreamSynchronize(s));
-    if (!h_over) {
+    play(L, k, sharded ? play_mask.get() : nullptr);
+    bool over = overflowed(&used);
+    if (sharded && !over) {
+      // ---- export: [root, count, (element, |boundary|, boundary...)...] per own level-k root
+      const int32_t first = (1 << k) - 1, width = 1 << k;
+      std::vector<int32_t> hcnt(nn);
+      MP_CUDA(cudaMemcpyAsync(hcnt.data(), left_cnt.get(), sizeof(int32_t) * nn, cudaMemcpyDeviceToHost, s));
+      MP_CUDA(cudaStreamSynchronize(s));
+      std::vector<int32_t> roots, elems;
+      for (int32_t j = 0; j < width; ++j)
+        if (shard->owner[first + j] == shard->rank) roots.push_back(first + j);
+      std::vector<size_t> root_at;
+      for (int32_t X : roots) {
+        root_at.push_back(elems.size());
+        const size_t at = elems.size();
+        elems.resize(at + hcnt[X]);
+        if (hcnt[X])
+          MP_CUDA(cudaMemcpyAsync(elems.data() + at, left_list.get() + left_off[X], sizeof(int32_t) * hcnt[X],
+                                  cudaMemcpyDeviceToHost, s));
+      }
+      MP_CUDA(cudaStreamSynchronize(s));
+      const int32_t ne = static_cast<int32_t>(elems.size());
+      std::vector<int32_t> esz(ne);
+      std::vector<int64_t> rec_off(ne);
+      DevBuf<int32_t> d_elems(std::max(ne, 1), s), d_esz(std::max(ne, 1), s);
+      if (ne) {
+        MP_CUDA(cudaMemcpyAsync(d_elems, elems.data(), sizeof(int32_t) * ne, cudaMemcpyHostToDevice, s));
+        MP_KERNEL(ctx, gather_bsz<<<grid_for(ctx, ne), 256, 0, s>>>(ne, d_elems, bsz, d_esz));
+        MP_CUDA(cudaMemcpyAsync(esz.data(), d_esz.get(), sizeof(int32_t) * ne, cudaMemcpyDeviceToHost, s));
+        MP_CUDA(cudaStreamSynchronize(s));
+      }
+      // layout: [nroots] then per root [X, cnt, records...]
+      std::vector<int32_t> buf(1, static_cast<int32_t>(roots.size()));
+      int64_t total = 1;
+      for (size_t r = 0; r < roots.size(); ++r) {
+        total += 2;
+        const size_t e0 = root_at[r], e1 = r + 1 < roots.size() ? root_at[r + 1] : elems.size();
+        for (size_t i = e0; i < e1; ++i) rec_off[i] = total, total += 2 + esz[i];
+      }
+      buf.resize(total);
+      if (ne) {
+        DevBuf<int64_t> d_off(ne, s);
+        DevBuf<int32_t> d_buf(total, s);
+        MP_CUDA(cudaMemcpyAsync(d_off, rec_off.data(), sizeof(int64_t) * ne, cudaMemcpyHostToDevice, s));
+        MP_KERNEL(ctx, pack_elements<<<grid_for(ctx, 32LL * ne), 256, 0, s>>>(ne, d_elems, d_off, bptr, bsz, pool,
+                                                                             d_buf));
+        MP_CUDA(cudaMemcpyAsync(buf.data(), d_buf.get(), sizeof(int32_t) * total, cudaMemcpyDeviceToHost, s));
+        MP_CUDA(cudaStreamSynchronize(s));
+      }
+      {
+        int64_t at = 1;
+        for (size_t r = 0; r < roots.size(); ++r) {
+          buf[at] = roots[r], buf[at + 1] = hcnt[roots[r]];
+          at += 2;
+          const size_t e0 = root_at[r], e1 = r + 1 < roots.size() ? root_at[r + 1] : elems.size();
+          for (size_t i = e0; i < e1; ++i) at += 2 + esz[i];
+        }
+        buf[0] = static_cast<int32_t>(roots.size());
+      }
+      if (!exchanged) {
+        received = shard->exchange(buf);
+        exchanged = true;
+      }
+      // ---- import the other ranks' roots: their live elements join this pool
+      std::vector<int32_t> ie, isz, blob;
+      std::vector<int64_t> ioff;
+      std::vector<std::pair<int32_t, std::vector<int32_t>>> lists;
+      for (size_t at = 0; at < received.size();) {
+        const int32_t nr = received[at++];
+        for (int32_t r = 0; r < nr; ++r) {
+          const int32_t X = received[at], cnt = received[at + 1];
+          at += 2;
+          const bool mine = shard->owner[X] == shard->rank;
+          std::vector<int32_t> lst;
+          for (int32_t i = 0; i < cnt; ++i) {
+            const int32_t e = received[at], sz = received[at + 1];
+            if (!mine) {
+              ie.push_back(e), isz.push_back(sz), ioff.push_back(static_cast<int64_t>(blob.size()));
+              blob.insert(blob.end(), received.begin() + at + 2, received.begin() + at + 2 + sz);
+              lst.push_back(e);
+            }
+            at += 2 + sz;
+          }
+          if (!mine) lists.emplace_back(X, std::move(lst));
+        }
+      }
+      const int64_t base = static_cast<int64_t>(used);
+      if (base + static_cast<int64_t>(blob.size()) > cap) {
+        over = true;  // no room for the imported boundaries: grow and replay
+        used += blob.size();
+      } else {
+        const int32_t ni = static_cast<int32_t>(ie.size());
+        if (!blob.empty())
+          MP_CUDA(cudaMemcpyAsync(pool.get() + base, blob.data(), sizeof(int32_t) * blob.size(),
+                                  cudaMemcpyHostToDevice, s));
+        DevBuf<int32_t> d_ie(std::max(ni, 1), s), d_isz(std::max(ni, 1), s);
+        DevBuf<int64_t> d_ioff(std::max(ni, 1), s);
+        if (ni) {
+          MP_CUDA(cudaMemcpyAsync(d_ie, ie.data(), sizeof(int32_t) * ni, cudaMemcpyHostToDevice, s));
+          MP_CUDA(cudaMemcpyAsync(d_isz, isz.data(), sizeof(int32_t) * ni, cudaMemcpyHostToDevice, s));
+          MP_CUDA(cudaMemcpyAsync(d_ioff, ioff.data(), sizeof(int64_t) * ni, cudaMemcpyHostToDevice, s));
+          MP_KERNEL(ctx, set_elements<<<grid_for(ctx, ni), 256, 0, s>>>(ni, d_ie, d_isz, d_ioff, base, bptr, bsz));
+        }
+        for (auto& [X, lst] : lists) {
+          const int32_t c = static_cast<int32_t>(lst.size());
+          if (c)
+            MP_CUDA(cudaMemcpyAsync(left_list.get() + left_off[X], lst.data(), sizeof(int32_t) * c,
+                                    cudaMemcpyHostToDevice, s));
+          MP_CUDA(cudaMemcpyAsync(left_cnt.get() + X, &c, 4,
+                                  cudaMemcpyHostToDevice, s));
+          MP_CUDA(cudaStreamSynchronize(s));  // the host copies live in this loop iteration
+        }
+        const unsigned long long nc = static_cast<unsigned long long>(base + blob.size());
+        MP_CUDA(cudaMemcpyAsync(cursor, &nc, 8, cudaMemcpyHostToDevice, s));
+        MP_CUDA(cudaStreamSynchronize(s));
+        // ---- the top levels, replicated on every rank
+        play(k - 1, 0, nullptr);
+        over = overflowed(&used);
+      }
+    }
+    if (!over) {
       ctx.sym_pool_ratio = std::max(ctx.sym_pool_ratio, static_cast<double>(used) / std::max(n, 1));
       break;
     }
     cap = std::max<int64_t>(2 * cap, static_cast<int64_t>(used) * 2);
     if (attempt == 7) throw Error(MP_ENOMEM, "symbolic: element pool exhausted");
   }
-  MP_CUDA(cudaMemsetAsync(sums, 0, 16, s));
-  MP_KERNEL(ctx, sum_counts<<<grid_for(ctx, n), 256, 0, s>>>(n, column_counts, sums));
-  unsigned long long h[2];
-  MP_CUDA(cudaMemcpyAsync(h, sums, 16, cudaMemcpyDeviceToHost, s));
-  MP_CUDA(cudaStreamSynchronize(s));
-  *nnz_L = static_cast<int64_t>(h[0]);
-  *cost = static_cast<int64_t>(h[1]);
+  if (!sharded) sum_counts_dev(ctx, n, column_counts, nnz_L, cost);  // sharded: the caller sums after its gather
   if (crossing) {
     unsigned long long hc = 0;
     MP_CUDA(cudaMemcpyAsync(&hc, cross, 8, cudaMemcpyDeviceToHost, s));

@@ -95,7 +95,7 @@ def test_struct_offsets_match_header(tmp_path):
     if not shutil.which("gcc"):
         pytest.skip("no gcc")
     structs = {"mp_csr": _lib.MpCsr, "mp_config": _lib.MpConfig, "mp_result": _lib.MpResult,
-               "mp_bench_row": _lib.MpBenchRow}
+               "mp_bench_row": _lib.MpBenchRow, "mp_comm": _lib.MpComm}
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "meshperm_b200.h"', "int main(void) {"]
     for cname, py in structs.items():
         lines.append(f'  printf("{cname} sizeof %zu\\n", sizeof({cname}));')
