@@ -125,6 +125,13 @@ void mp_context_destroy(mp_context* ctx);
  * instead of queueing behind each other's whole-GPU launches.  Results do not
  * depend on it. */
 int mp_context_set_sm_share(mp_context* ctx, int32_t share);
+/* How mp_order / mp_tree_fill compute column counts, parents and nnz(L):
+ * 0 (default) the factor's elimination tree + Gilbert-Ng-Peyton column counts
+ * split by the ND tree; 1 the elimination game of symbolic.cpp:33-45 played
+ * node by node.  Both give identical outputs; 1 is kept as a cross-check.
+ * cross_block_fill, elimination_fill of an arbitrary permutation and trees
+ * whose separators leak always use the game. */
+int mp_context_set_fill_algorithm(mp_context* ctx, int32_t algo);
 /* cudaStream_t to run on; NULL restores the context's own stream. */
 int mp_context_set_stream(mp_context* ctx, void* stream);
 

@@ -129,6 +129,11 @@ class Context:
     def set_stream(self, stream_ptr: int | None):
         check(lib().mp_context_set_stream(self.handle, C.c_void_p(stream_ptr or 0)))
 
+    def set_fill_algorithm(self, algo: str):
+        """'etree' (default: elimination tree + column counts) or 'game' (the
+        elimination game of symbolic.cpp:33-45); identical outputs."""
+        check(lib().mp_context_set_fill_algorithm(self.handle, {"etree": 0, "game": 1}[algo]))
+
 
 _default: dict[int, Context] = {}
 

@@ -207,6 +207,14 @@ int mp_context_set_sm_share(mp_context* ctx, int32_t share) {
   });
 }
 
+int mp_context_set_fill_algorithm(mp_context* ctx, int32_t algo) {
+  return guarded([&] {
+    if (!ctx) throw Error(MP_EINVAL, "null context");
+    if (algo != 0 && algo != 1) throw Error(MP_EINVAL, "fill algorithm must be 0 or 1");
+    ctx->fill_algo = algo;
+  });
+}
+
 int mp_context_set_stream(mp_context* ctx, void* stream) {
   return guarded([&] {
     if (!ctx) throw Error(MP_EINVAL, "null context");
@@ -438,7 +446,12 @@ int mp_tree_fill_schedule(mp_context* ctx, const mp_csr* g, int32_t nd_level, co
     compute_perm_dev(*ctx, n, nd_level, off, verts, lp, sched, pm, inv, pos);
     node_of_from_tree_dev(*ctx, n, nn, off, verts, node_of);
     int64_t L = 0, C = 0;
-    tree_fill_dev(*ctx, gv.g, nd_level, node_of, off, verts, lp, pos, inv, cc, par, &L, &C);
+    // a caller's tree whose separators leak: the game on the permutation itself
+    // (the node-by-node split needs separated subtrees)
+    if (unrelated_edges_dev(*ctx, gv.g, node_of) == 0)
+      tree_fill_dev(*ctx, gv.g, nd_level, node_of, off, verts, lp, pos, inv, cc, par, &L, &C);
+    else
+      elimination_game_dev(*ctx, gv.g, pm, cc, par, &L, &C, nullptr, nullptr);
     output_copy(*ctx, column_counts, cc.get(), n, on_device);
     output_copy(*ctx, etree_parent, par.get(), n, on_device);
     MP_CUDA(cudaStreamSynchronize(s));

@@ -512,7 +512,6 @@ void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t L, const int
   int32_t m2 = 0;
   MP_CUDA(cudaMemcpyAsync(&m2, g.off + n, 4, cudaMemcpyDeviceToHost, s));
   MP_CUDA(cudaStreamSynchronize(s));
-  DevBuf<int32_t> adj(std::max(m2, 1), s), el(std::max(m2, 1), s);
   MP_KERNEL(ctx, local_of_kernel<<<grid_for(ctx, n), 256, 0, s>>>(n, node_of, node_offsets, node_vertices, local_of));
   MP_CUDA(cudaMemsetAsync(need, 0, sizeof(int64_t) * (nn + 1), s));
   MP_KERNEL(ctx, node_pool_need<<<std::min(nn, 4096), 256, 0, s>>>(nn, node_offsets, node_vertices, g.off, node_mask, need));
@@ -526,7 +525,14 @@ void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t L, const int
   MP_CUDA(cudaMemcpyAsync(&pool_total, pool_off.get() + nn, 8, cudaMemcpyDeviceToHost, s));
   MP_CUDA(cudaMemsetAsync(overflow, 0, 4, s));
   MP_CUDA(cudaStreamSynchronize(s));
-  DevBuf<int32_t> pool(std::max<int64_t>(pool_total, 1), s);
+  // slot lists and the element-boundary pool: one persistent context slab
+  SlabCarve sc;
+  const size_t o_adj = sc.add(sizeof(int32_t) * std::max(m2, 1)), o_el = sc.add(sizeof(int32_t) * std::max(m2, 1)),
+               o_pool = sc.add(sizeof(int32_t) * std::max<int64_t>(pool_total, 1));
+  void* slab = ctx.slab(kSlabMd, sc.total);
+  int32_t* adj = SlabCarve::at<int32_t>(slab, o_adj);
+  int32_t* el = SlabCarve::at<int32_t>(slab, o_el);
+  int32_t* pool = SlabCarve::at<int32_t>(slab, o_pool);
   MdArgs a{};
   a.g = g, a.nn = nn, a.node_of = node_of, a.node_offsets = node_offsets, a.node_vertices = node_vertices;
   a.local_of = local_of, a.mode = mode, a.adj = adj, a.el = el, a.nadj = nadj, a.nel = nel;

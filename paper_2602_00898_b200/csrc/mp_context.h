@@ -39,6 +39,7 @@ struct mp_context {
   void* slab(int id, size_t bytes);
   int fps_workers = 0;  // worker CTAs of the batched FPS (decided once)
   int sm_share = 1;     // contexts expected to run concurrently on the device (grid sizing)
+  int fill_algo = 0;    // 0: etree + column counts (colcount.cu), 1: the elimination game (symbolic.cu)
   // private stream-ordered pool for the per-call scratch (release threshold
   // raised on this pool only, never on the device's default pool)
   cudaMemPool_t pool = nullptr;
@@ -84,6 +85,9 @@ struct DGraph {
   const int32_t* off;
   const int32_t* nbr;
 };
+
+// Persistent context slab ids (mp_context::slab): 0-4 farthest-point seeding.
+enum SlabId { kSlabMd = 5, kSlabFill = 6 };
 
 // Kernel-time slots reported in mp_result.kernel_ms.
 enum KernelSlot { kKFps = 0, kKLloyd = 1, kKFm = 2, kKRefine = 3, kKMd = 4, kKSym = 5, kKSlots = 6 };
@@ -178,6 +182,13 @@ void tree_fill_dev(mp_context& ctx, const DGraph& g, int32_t nd_level, const int
                    int64_t* column_counts, int32_t* etree_parent, int64_t* nnz_L, int64_t* cost,
                    const int32_t* cross_owner = nullptr, int64_t* crossing = nullptr,
                    const FillShard* shard = nullptr);
+// The same outputs from the factor's elimination tree (colcount.cu): Liu's
+// etree split by the ND tree, a postorder, Gilbert-Ng-Peyton column counts.
+// Needs a tree whose separators separate (no edge between unrelated nodes).
+void tree_fill_fast_dev(mp_context& ctx, const DGraph& g, int32_t nd_level, const int32_t* node_of,
+                        const int32_t* node_offsets, const int32_t* node_vertices, const int32_t* local_perm,
+                        const int32_t* node_pos, const int32_t* inverse, int64_t* column_counts,
+                        int32_t* etree_parent, int64_t* nnz_L, int64_t* cost);
 void sum_counts_dev(mp_context& ctx, int64_t n, const int64_t* column_counts, int64_t* nnz_L, int64_t* cost);
 // The same game for any permutation (one-node tree): elimination_fill,
 // factor_etree_parents and, with cross_owner, cross_block_fill's count.

@@ -212,4 +212,20 @@ struct DevBuf {
   operator T*() const { return p; }
 };
 
+// Several arrays carved out of one persistent context slab (mp_context::slab):
+// the large per-call scratch of a stage lives there, so repeated calls neither
+// allocate nor fragment the stream-ordered pool.
+struct SlabCarve {
+  size_t total = 0;
+  size_t add(size_t bytes) {
+    const size_t at = total;
+    total += (bytes + 255) & ~size_t(255);
+    return at;
+  }
+  template <class T>
+  static T* at(void* base, size_t off) {
+    return reinterpret_cast<T*>(static_cast<char*>(base) + off);
+  }
+};
+
 }  // namespace mp

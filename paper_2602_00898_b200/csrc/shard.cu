@@ -342,9 +342,12 @@ int mp_order_sharded(mp_context* ctx, const mp_csr* g, const mp_config* cfg, con
         for (auto& part : ex.hostv(buf)) cat.insert(cat.end(), part.begin(), part.end());
         return cat;
       };
+      // the etree / column-count fill (colcount.cu) is replicated on every
+      // rank; the game (fill_algo 1) plays its own subtrees and exchanges
+      const bool shard_game = sharded && ctx->fill_algo == 1;
       tree_fill_dev(*ctx, gv.g, L, node_of_g, off_g, verts_g, lp_g, pos, inv, cc, par, &nnzL, &cost, nullptr,
-                    nullptr, sharded ? &fs : nullptr);
-      if (sharded) {
+                    nullptr, shard_game ? &fs : nullptr);
+      if (shard_game) {
         // all-gather 4: column counts and parents at the own nodes' positions
         std::vector<int32_t> hpos(nn + 1);
         MP_CUDA(cudaMemcpyAsync(hpos.data(), pos.get(), sizeof(int32_t) * (nn + 1), cudaMemcpyDeviceToHost, s));

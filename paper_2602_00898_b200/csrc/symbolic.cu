@@ -398,6 +398,12 @@ void tree_fill_dev(mp_context& ctx, const DGraph& g, int32_t L, const int32_t* n
                    const int32_t* node_pos, const int32_t* inverse, int64_t* column_counts,
                    int32_t* etree_parent, int64_t* nnz_L, int64_t* cost, const int32_t* cross_owner,
                    int64_t* crossing, const FillShard* shard) {
+  const bool sharded_game = shard && shard->k > 0 && shard->k <= L;
+  if (!cross_owner && !crossing && !sharded_game && ctx.fill_algo == 0) {
+    tree_fill_fast_dev(ctx, g, L, node_of, node_offsets, node_vertices, local_perm, node_pos, inverse, column_counts,
+                       etree_parent, nnz_L, cost);
+    return;
+  }
   cudaStream_t s = ctx.stream;
   const int32_t n = g.n;
   const int32_t nn = static_cast<int32_t>((1LL << (L + 1)) - 1);
