@@ -163,10 +163,12 @@ int mp_context_create(mp_context** out, int32_t device) {
     ctx->device = device;
     ContextScope sd(*ctx);
     MP_CUDA(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+    MP_CUDA(cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
     ctx->stream = ctx->own_stream;
     MP_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
     MP_CUDA(cudaDeviceGetAttribute(&ctx->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
     for (auto& e : ctx->ev) MP_CUDA(cudaEventCreate(&e));
+    for (auto& e : ctx->fork_ev) MP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     MP_CUDA(cudaMalloc(reinterpret_cast<void**>(&ctx->dwork), 16 * sizeof(unsigned long long)));
     MP_CUDA(cudaMemset(ctx->dwork, 0, 16 * sizeof(unsigned long long)));
     // a private stream-ordered pool that keeps freed scratch between calls;
@@ -189,10 +191,13 @@ void mp_context_destroy(mp_context* ctx) {
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : ctx->kev) cudaEventDestroy(e);
+  for (auto& e : ctx->fork_ev)
+    if (e) cudaEventDestroy(e);
   for (auto& sl : ctx->slabs)
     if (sl.first) cudaFree(sl.first);
   if (ctx->dwork) cudaFree(ctx->dwork);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
   if (ctx->pool) cudaMemPoolDestroy(ctx->pool);
   delete ctx;
 }

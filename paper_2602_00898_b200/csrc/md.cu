@@ -27,6 +27,7 @@ namespace {
 constexpr int kMdThreads = 512;
 constexpr int32_t kSmemDegCap = 12 * 1024;  // nodes up to this size keep degrees in smem
 constexpr uint32_t kInfDeg = 0xffffffffu;
+constexpr int32_t kMdDirtyCap = 1024;  // dirty blocks listed per pivot (more: recompute all)
 
 int grid_for(const mp_context& ctx, int64_t n, int threads = 256) {
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), ctx.num_sms * 16LL)));
@@ -54,7 +55,11 @@ struct MdArgs {
   int32_t* order_ws;         // per vertex scratch: pivots in order (node_vertices layout)
   int32_t* local_perm;       // output, node_vertices layout
   int32_t* overflow;         // set on pool exhaustion
-  int32_t min_nv;            // md_kernel: only nodes with at least this many vertices
+  const int32_t* sched;      // md_smem_kernel: node per CTA, largest first
+  uint64_t* gblk;            // md_node_global: block minima when shared memory is short
+  uint32_t* gdbits;          // md_node_global: dirty-block bits when shared memory is short
+  int64_t gsmem_bytes;       // md_node_global: dynamic shared memory of the launch
+  int64_t smem_bytes;        // md_smem_kernel: dynamic shared memory per CTA
   const uint8_t* node_mask;  // non-null: order only nodes with mask != 0 (sharded C3 path)
 };
 
@@ -62,10 +67,12 @@ __device__ __forceinline__ uint32_t md_key_deg(int64_t d) {
   return d >= static_cast<int64_t>(kInfDeg) ? kInfDeg - 1 : static_cast<uint32_t>(d);
 }
 
-__global__ void __launch_bounds__(kMdThreads) md_kernel(MdArgs a) {
-  const int32_t node = blockIdx.x;
+// One node with its lists, pool and (above kSmemDegCap) degrees in global
+// memory: exact mode, natural mode, and approximate-mode nodes too large for
+// md_smem_kernel.
+__device__ __forceinline__ void md_node_global(const MdArgs& a, int32_t node) {
   const int32_t vb = a.node_offsets[node], nv = a.node_offsets[node + 1] - vb;
-  if (nv == 0 || nv < a.min_nv || (a.node_mask && !a.node_mask[node])) return;
+  if (nv == 0 || (a.node_mask && !a.node_mask[node])) return;
   const int32_t* verts = a.node_vertices + vb;
   int32_t* lperm = a.local_perm + vb;
   int32_t* order = a.order_ws + vb;
@@ -78,7 +85,7 @@ __global__ void __launch_bounds__(kMdThreads) md_kernel(MdArgs a) {
   uint32_t* deg = smem_deg ? sdeg_dyn : a.gdeg + vb;  // indexed by local id
 
   __shared__ uint64_t red[32];
-  __shared__ int32_t s_nb, s_cursor, s_half, s_need_compact;
+  __shared__ int32_t s_nb, s_cursor, s_half, s_need_compact, s_ndirty, s_dlist[kMdDirtyCap];
   const int64_t pbase = a.pool_off[node];
   const int64_t pcap = (a.pool_off[node + 1] - pbase) / 2;
 
@@ -98,21 +105,49 @@ __global__ void __launch_bounds__(kMdThreads) md_kernel(MdArgs a) {
     a.emark[v] = 0;
     deg[k] = static_cast<uint32_t>(c);  // approx degree with no elements = |adj|
   }
-  if (threadIdx.x == 0) s_cursor = 0, s_half = 0;
+  if (threadIdx.x == 0) s_cursor = 0, s_half = 0, s_ndirty = 0;
   __syncthreads();
   int32_t xcount = 0;  // exact mode: running token counter (same in every thread)
+  // (degree, id) block minima: the argmin reads nbk entries, not nv; a lowered
+  // key lowers its block's minimum at once, a block whose minimum rose is
+  // recomputed at the end of the pivot (blk / dirty bits in shared memory
+  // after the degrees when they fit, else in the node's global slab)
+  const int32_t nbk = (nv + 31) / 32, lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int64_t deg_bytes = smem_deg ? 4LL * kSmemDegCap : 0;
+  const bool blk_sm = deg_bytes + 8LL * nbk + 4LL * (nbk / 32 + 1) <= a.gsmem_bytes;
+  uint64_t* blk = blk_sm ? reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(sdeg_dyn) + deg_bytes)
+                         : a.gblk + (vb >> 5) + node;
+  uint32_t* dbits = blk_sm ? reinterpret_cast<uint32_t*>(blk + nbk) : a.gdbits + (vb >> 10) + 2 * node;
+  auto key_of = [&](int32_t i) -> uint64_t {
+    const uint32_t d = i < nv ? deg[i] : kInfDeg;
+    return d != kInfDeg ? key_min(d, static_cast<uint32_t>(i)) : ~0ull;
+  };
+  auto mark_dirty = [&](int32_t b) {
+    const uint32_t bit = 1u << (b & 31);
+    if (!(atomicOr(&dbits[b >> 5], bit) & bit)) {
+      const int32_t at = atomicAdd(&s_ndirty, 1);
+      if (at < kMdDirtyCap) s_dlist[at] = b;
+    }
+  };
+  // a member's degree changed from od to nd
+  auto rekey = [&](int32_t lw, uint32_t od, uint32_t nd) {
+    const uint64_t ok = key_min(od, static_cast<uint32_t>(lw)), nk = key_min(nd, static_cast<uint32_t>(lw));
+    if (nk < ok) atomicMin(reinterpret_cast<unsigned long long*>(&blk[lw >> 5]), nk);
+    else if (nk > ok && ok == blk[lw >> 5]) mark_dirty(lw >> 5);
+  };
+  for (int32_t b = threadIdx.x; b <= nbk / 32; b += blockDim.x) dbits[b] = 0;
+  for (int32_t b = wid; b < nbk; b += nwarp) {
+    const uint64_t m = warp_min_u64(key_of(b * 32 + lane));
+    if (lane == 0) blk[b] = m;
+  }
+  __syncthreads();
 
   for (int32_t k = 0; k < nv; ++k) {
-    // ---- pivot: min (degree, local id)
+    // ---- pivot: min (degree, local id) over the block minima
     uint64_t best = ~0ull;
-    for (int32_t i = threadIdx.x; i < nv; i += blockDim.x) {
-      const uint32_t d = deg[i];
-      if (d != kInfDeg) {
-        const uint64_t kk = key_min(d, static_cast<uint32_t>(i));
-        best = kk < best ? kk : best;
-      }
-    }
+    for (int32_t b = threadIdx.x; b < nbk; b += blockDim.x) best = min(best, blk[b]);
     best = block_min_u64(best, red);
+    if (threadIdx.x == 0) s_ndirty = 0;  // every reader of the last pivot's count is past its barrier
     const int32_t kp = static_cast<int32_t>(best & 0xffffffffu);
     const int32_t p = verts[kp];
     const int32_t tok = p + 1;
@@ -180,6 +215,7 @@ __global__ void __launch_bounds__(kMdThreads) md_kernel(MdArgs a) {
       order[k] = p;
       lperm[k] = kp;
       deg[kp] = kInfDeg;
+      mark_dirty(kp >> 5);  // the pivot was its block's minimum
     }
     // absorbed elements' boundaries are dropped after the member updates
     __syncthreads();
@@ -224,7 +260,12 @@ __global__ void __launch_bounds__(kMdThreads) md_kernel(MdArgs a) {
       we[ce++] = p;
       d += nb;
       a.nel[w] = ce;
-      if (a.mode == 0) deg[a.local_of[w]] = md_key_deg(d);
+      if (a.mode == 0) {
+        const int32_t lw = a.local_of[w];
+        const uint32_t od = deg[lw], nd = md_key_deg(d);
+        deg[lw] = nd;
+        rekey(lw, od, nd);
+      }
     }
     __syncthreads();
     for (int32_t ei = threadIdx.x; ei < np_el; ei += blockDim.x) a.bsz[pel[ei]] = 0;
@@ -258,218 +299,322 @@ __global__ void __launch_bounds__(kMdThreads) md_kernel(MdArgs a) {
           }
         }
         __syncthreads();
-        if (threadIdx.x == 0) deg[a.local_of[w]] = static_cast<uint32_t>(s_cnt);
+        if (threadIdx.x == 0) {
+          const int32_t lw = a.local_of[w];
+          const uint32_t od = deg[lw], nd = static_cast<uint32_t>(s_cnt);
+          deg[lw] = nd;
+          rekey(lw, od, nd);
+        }
         __syncthreads();
+      }
+    }
+    __syncthreads();
+    const int32_t ndirty = s_ndirty;
+    if (ndirty > kMdDirtyCap) {  // list overflow: every block
+      for (int32_t b = wid; b < nbk; b += nwarp) {
+        const uint64_t m = warp_min_u64(key_of(b * 32 + lane));
+        if (lane == 0) blk[b] = m;
+      }
+      for (int32_t b = threadIdx.x; b <= nbk / 32; b += blockDim.x) dbits[b] = 0;
+    } else {
+      for (int32_t q = wid; q < ndirty; q += nwarp) {
+        const int32_t b = s_dlist[q];
+        const uint64_t m = warp_min_u64(key_of(b * 32 + lane));
+        if (lane == 0) {
+          blk[b] = m;
+          atomicAnd(&dbits[b >> 5], ~(1u << (b & 31)));
+        }
       }
     }
     __syncthreads();
   }
 }
 
-// Fast approximate-MD kernel (the default mode).  Node-local ids throughout:
-// variable and element lists hold local ids (an element is named by its
-// pivot's local id), and the per-vertex state lives in shared memory:
-//   st[v]   = |adj| | |elems| << 16    deg[v] = approx degree (INF once gone)
-//   mark[v] = token: a vertex mark while v is alive, the absorption mark of
-//             element v once v is eliminated (the two uses never overlap)
-//   bsz[e]  = boundary size of element e (0 = absorbed / empty)
-//   blk[b]  = min (degree, id) key of the 32 vertices of block b
-// Per pivot: argmin over blk (every warp, redundantly), reach collection,
-// member updates, dirty-block refresh: three barriers (B2, B3, B4).
-constexpr int32_t kMdFastCap = 6 * 1024;  // nodes up to this size use the fast kernel
+__global__ void __launch_bounds__(kMdThreads) md_kernel(MdArgs a) {
+  md_node_global(a, a.sched ? a.sched[blockIdx.x] : static_cast<int32_t>(blockIdx.x));
+}
 
-__global__ void __launch_bounds__(kMdThreads) md_fast_kernel(MdArgs a) {
-  const int32_t node = a.nn - 1 - static_cast<int32_t>(blockIdx.x);  // leaves (the big nodes) first
+// Shared-memory approximate-MD kernel (the default mode).  The whole
+// elimination state of a node lives in one CTA's shared memory, in node-local
+// ids, so a pivot's dependent chain never leaves the SM; four warps run it
+// (cheap barriers, one reach member per thread):
+//   kd[v]   32-bit key (approx degree << 13 | v), ~0 once eliminated
+//   blk[b]  min key of the 32 vertices of block b (the argmin is a min over
+//           blk); a lowered key lowers it at once (atomicMin), a block whose
+//           minimum rose (the pivot's, a member that was its block minimum)
+//           is recomputed after the member updates
+//   st[v]   live: |adj| | |elems| << 16; element: |boundary| (0 = absorbed)
+//   ebp[e]  boundary offset of element e in the current pool half
+//   L[loff[v] .. loff[v+1])  v's list slots: variables from the front, elements
+//           from the back (|adj| + |elems| never exceeds the initial degree)
+//   pool    element boundaries, two halves (compaction copies the live ones)
+//   inr / absb  bit sets: this pivot's reach, the elements it absorbs
+// The approx degree of a member is |adj| + sum of its elements' boundaries <=
+// deg0 * nv, so keys are exact while max local degree * nv < 2^19.  A node
+// whose boundaries outgrow the shared halves continues with halves in its
+// global pool slab; a node whose lists or keys do not fit is ordered by
+// md_node_global in the same CTA.
+constexpr int32_t kMdSmemMaxNv = 8192;  // local ids in 13 bits
+constexpr int32_t kMdMinHalf = 1024;    // smallest shared pool half worth running with
+constexpr uint32_t kKeyInf = 0xffffffffu;
+constexpr int kMdSmemThreads = 128;  // four warps: cheap barriers, one member per thread
+
+__host__ __device__ inline int64_t md_smem_fixed(int32_t nv) {
+  const int64_t nb = (nv + 31) / 32;
+  return 4 * nb + 4 * (4LL * nv + 1) + 4 * (2 * nb + (nb + 31) / 32 + 1) + 16;
+}
+
+__global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
+  const int32_t node = a.sched[blockIdx.x];  // largest nodes first
   const int32_t vb = a.node_offsets[node], nv = a.node_offsets[node + 1] - vb;
-  if (nv == 0 || nv > kMdFastCap || (a.node_mask && !a.node_mask[node])) return;
+  if (nv == 0 || (a.node_mask && !a.node_mask[node])) return;
   const int32_t* verts = a.node_vertices + vb;
   int32_t* lperm = a.local_perm + vb;
-  int32_t* order = a.order_ws + vb;
-  int32_t* bp = a.bptr + vb;  // element boundary offsets, local ids (node slab)
   extern __shared__ uint64_t md_sm[];
   const int32_t nb = (nv + 31) / 32;
-  uint64_t* blk = md_sm;
-  uint32_t* deg = reinterpret_cast<uint32_t*>(blk + nb);
-  int32_t* mark = reinterpret_cast<int32_t*>(deg + nv);
-  int32_t* bsz = mark + nv;
-  int32_t* st = bsz + nv;
-  int32_t* loff = st + nv;  // CSR offset of each local vertex (its list slots)
-  uint32_t* dirty = reinterpret_cast<uint32_t*>(loff + nv);  // nb bits
-  // this pivot's reach (local ids < kMdFastCap fit 16 bits), read back by the
-  // member updates without a trip through the global pool
-  int16_t* sreach = reinterpret_cast<int16_t*>(dirty + (nb + 31) / 32 + 1);
-  __shared__ int32_t s_nbc[2], s_cursor, s_half, s_dcnt;
-  __shared__ int32_t s_dlist[kMdThreads];  // dirty blocks of this pivot (<= reach + 1 distinct)
+  uint32_t* blk = reinterpret_cast<uint32_t*>(md_sm);
+  uint32_t* kd = blk + nb;
+  uint32_t* st = kd + nv;
+  uint32_t* ebp = st + nv;
+  uint32_t* loff = ebp + nv;  // nv + 1
+  uint32_t* inr = loff + nv + 1;
+  uint32_t* absb = inr + nb;
+  uint32_t* dbits = absb + nb;  // dirty blocks (nb bits)
+  uint16_t* L = reinterpret_cast<uint16_t*>(dbits + (nb + 31) / 32 + 1);
+  __shared__ int32_t s_cursor, s_cap, s_inglobal, s_maxdeg, s_nbd[2], s_ndirty, sh[32];
+  __shared__ int32_t s_dlist[kMdSmemMaxNv / 32];
+  __shared__ int64_t s_red64[32];
+  __shared__ uint16_t* s_cur;
+  __shared__ uint16_t* s_other;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  const int64_t pbase = a.pool_off[node];
-  const int64_t pcap = (a.pool_off[node + 1] - pbase) / 2;
 
-  // induced subgraph in local ids; list slots at the vertex's CSR range
+  // ---- local degrees -> list slot offsets
+  if (threadIdx.x == 0) s_maxdeg = 0;
+  __syncthreads();
+  int32_t mymax = 0;
   for (int32_t k = threadIdx.x; k < nv; k += blockDim.x) {
     const int32_t v = verts[k];
-    const int32_t o = a.g.off[v];
     int32_t c = 0;
-    for (int32_t j = o; j < a.g.off[v + 1]; ++j) {
-      const int32_t w = a.g.nbr[j];
-      if (a.node_of[w] == node) a.adj[o + c++] = a.local_of[w];
-    }
-    if (c > 0x7fff) atomicExch(a.overflow, 2);  // packed list lengths: the general kernel redoes it
+    for (int32_t j = a.g.off[v]; j < a.g.off[v + 1]; ++j) c += a.node_of[a.g.nbr[j]] == node;
     st[k] = c;
-    loff[k] = o;
-    deg[k] = static_cast<uint32_t>(c);
-    mark[k] = 0;
-    bsz[k] = 0;
+    mymax = max(mymax, c);
   }
-  for (int32_t b = threadIdx.x; b < (nb + 31) / 32; b += blockDim.x) dirty[b] = 0;
-  if (threadIdx.x == 0) s_cursor = 0, s_half = 0, s_dcnt = 0, s_nbc[0] = s_nbc[1] = 0;
+  atomicMax(&s_maxdeg, mymax);
+  __syncthreads();
+  int32_t run = 0;
+  for (int32_t b0 = 0; b0 < nv; b0 += blockDim.x) {
+    const int32_t k = b0 + threadIdx.x;
+    int32_t tot;
+    const int32_t ex = block_excl_scan(k < nv ? static_cast<int32_t>(st[k]) : 0, sh, &tot);
+    if (k < nv) loff[k] = run + ex;
+    run += tot;
+  }
+  const int64_t D = run;
+  const int64_t half = (a.smem_bytes - md_smem_fixed(nv) - 2 * D) / 4;  // u16 entries per pool half
+  if (half < kMdMinHalf || static_cast<int64_t>(s_maxdeg) * nv >= (1LL << 19)) {
+    __syncthreads();
+    md_node_global(a, node);  // lists or keys do not fit: global state
+    return;
+  }
+  if (threadIdx.x == 0) {
+    loff[nv] = static_cast<uint32_t>(D);
+    s_cursor = 0, s_inglobal = 0;
+    s_cap = static_cast<int32_t>(half);
+    s_cur = L + D;
+    s_other = L + D + half;
+  }
+  for (int32_t b = threadIdx.x; b < nb; b += blockDim.x) inr[b] = 0, absb[b] = 0;
+  for (int32_t b = threadIdx.x; b <= (nb + 31) / 32; b += blockDim.x) dbits[b] = 0;
+  if (threadIdx.x == 0) s_nbd[0] = s_nbd[1] = 0, s_ndirty = 0;
+  // induced subgraph in local ids
+  for (int32_t k = threadIdx.x; k < nv; k += blockDim.x) {
+    const int32_t v = verts[k];
+    const uint32_t o = loff[k];
+    int32_t c = 0;
+    for (int32_t j = a.g.off[v]; j < a.g.off[v + 1]; ++j) {
+      const int32_t w = a.g.nbr[j];
+      if (a.node_of[w] == node) L[o + c++] = static_cast<uint16_t>(a.local_of[w]);
+    }
+    st[k] = static_cast<uint32_t>(c);
+    kd[k] = (static_cast<uint32_t>(c) << 13) | static_cast<uint32_t>(k);
+  }
   __syncthreads();
   for (int32_t b = wid; b < nb; b += nwarp) {
     const int32_t i = b * 32 + lane;
-    const uint64_t m = warp_min_u64(i < nv ? key_min(deg[i], static_cast<uint32_t>(i)) : ~0ull);
+    const uint32_t m = __reduce_min_sync(0xffffffffu, i < nv ? kd[i] : kKeyInf);
     if (lane == 0) blk[b] = m;
   }
   __syncthreads();
 
+  // ---- the pivots
+  const uint32_t below = (1u << lane) - 1;
+  // a block whose minimum may have risen is recomputed after the member updates
+  auto mark_dirty = [&](int32_t b) {
+    const uint32_t bit = 1u << (b & 31);
+    if (!(atomicOr(&dbits[b >> 5], bit) & bit)) s_dlist[atomicAdd(&s_ndirty, 1)] = b;
+  };
   for (int32_t k = 0; k < nv; ++k) {
-    // ---- pivot: min (degree, local id), computed by every warp (no barrier
-    // to broadcast it; blk is stable since the previous B4)
-    uint64_t best = ~0ull;
+    // pivot: min key over the block minima (every warp; blk is stable since B4)
+    uint32_t best = kKeyInf;
     for (int32_t b = lane; b < nb; b += 32) best = min(best, blk[b]);
-    best = warp_min_u64(best);
-    const int32_t p = static_cast<int32_t>(best & 0xffffffffu);
-    const int32_t tok = k + 1;
-    int32_t* cnt = &s_nbc[k & 1];
-    const int32_t po = loff[p];
-    const int32_t pst = st[p];
-    const int32_t np_adj = pst & 0xffff, np_el = pst >> 16;
-    if (s_cursor + (nv - k) > pcap) {  // block-uniform: compact live boundaries into the other half
-      int32_t* src = a.pool + pbase + (s_half ? pcap : 0);
-      int32_t* dst = a.pool + pbase + (s_half ? 0 : pcap);
-      int32_t run = 0;
-      for (int32_t i0 = 0; i0 < k; i0 += blockDim.x) {
-        const int32_t i = i0 + threadIdx.x;
-        const int32_t e = i < k ? order[i] : -1;
-        const int32_t sz = e >= 0 ? bsz[e] : 0;
-        int32_t tot;
-        __shared__ int32_t shs[32];
-        const int32_t off = block_excl_scan(sz, shs, &tot);
-        if (sz > 0) {
-          const int32_t from = bp[e];
-          for (int32_t t = 0; t < sz; ++t) dst[run + off + t] = src[from + t];
-          bp[e] = run + off;
-        }
-        run += tot;
-        __syncthreads();
+    best = __reduce_min_sync(0xffffffffu, best);
+    const int32_t p = static_cast<int32_t>(best & 0x1fffu);
+    int32_t* cnt = &s_nbd[k & 1];
+    if (s_cursor + (nv - k) > s_cap) {  // block-uniform: compact the live boundaries
+      int64_t live = 0;
+      for (int32_t e = threadIdx.x; e < nv; e += blockDim.x)
+        if (kd[e] == kKeyInf) live += st[e];
+      live = block_sum_i64(live, s_red64);
+      uint16_t* src = s_cur;
+      uint16_t* dst;
+      int64_t cap;
+      bool to_global = false;
+      if (!s_inglobal && live + (nv - k) <= half) {
+        dst = s_other, cap = half;
+      } else {
+        // global halves: the node's slab of the int32 pool, as u16 entries
+        const int64_t pb = a.pool_off[node], gcap = a.pool_off[node + 1] - pb;  // u16 entries per half
+        uint16_t* g0 = reinterpret_cast<uint16_t*>(a.pool + pb);
+        dst = (s_inglobal && src == g0) ? g0 + gcap : g0;
+        cap = gcap;
+        to_global = true;
       }
+      int32_t crun = 0;
+      for (int32_t b0 = 0; b0 < nv; b0 += blockDim.x) {
+        const int32_t e = b0 + threadIdx.x;
+        const int32_t sz = (e < nv && kd[e] == kKeyInf) ? static_cast<int32_t>(st[e]) : 0;
+        int32_t tot;
+        const int32_t ex = block_excl_scan(sz, sh, &tot);
+        const uint32_t from = sz > 0 ? ebp[e] : 0;
+        if (sz > 0) ebp[e] = static_cast<uint32_t>(crun + ex);
+        // each warp copies its live boundaries one element at a time
+        uint32_t live_m = __ballot_sync(0xffffffffu, sz > 0);
+        while (live_m) {
+          const int l = __ffs(live_m) - 1;
+          live_m &= live_m - 1;
+          const int32_t szl = __shfl_sync(0xffffffffu, sz, l);
+          const uint32_t fl = __shfl_sync(0xffffffffu, from, l);
+          const int32_t tl = crun + __shfl_sync(0xffffffffu, ex, l);
+          for (int32_t t = lane; t < szl; t += 32) dst[tl + t] = src[fl + t];
+        }
+        crun += tot;
+      }
+      __syncthreads();
       if (threadIdx.x == 0) {
-        s_half ^= 1;
-        s_cursor = run;
-        if (run + (nv - k) > pcap) atomicExch(a.overflow, 1);
+        if (!to_global) s_other = src;
+        s_cur = dst;
+        s_cap = static_cast<int32_t>(cap);
+        s_inglobal = to_global ? 1 : 0;
+        s_cursor = crun;
+        if (crun + (nv - k) > cap) atomicExch(a.overflow, 1);
       }
       __syncthreads();
     }
-    int32_t* half = a.pool + pbase + (s_half ? pcap : 0);
+    uint16_t* cur = s_cur;
     const int32_t cur0 = s_cursor;
-    int32_t* out = half + cur0;
-    // ---- reach set: variables of p plus boundaries of p's elements (p itself
-    // is skipped explicitly; its mark is set for the member updates below)
-    const int32_t* padj = a.adj + po;
-    const int32_t* pel = a.el + po;
-    for (int32_t i = threadIdx.x; i < np_adj; i += blockDim.x) {
-      const int32_t w = padj[i];
-      if (atomicExch(&mark[w], tok) != tok) {
-        const int32_t at = atomicAdd(cnt, 1);
-        out[at] = w;
-        sreach[at] = static_cast<int16_t>(w);
+    uint16_t* out = cur + cur0;
+    const uint32_t pst = st[p];
+    const int32_t np_adj = pst & 0xffff, np_el = pst >> 16;
+    const uint32_t po = loff[p], pe = loff[p + 1];
+    // ---- reach: variables of p plus the boundaries of p's elements
+    // (warp-aggregated appends)
+    for (int32_t i0 = 0; i0 < np_adj; i0 += blockDim.x) {
+      const int32_t i = i0 + threadIdx.x;
+      bool fresh = false;
+      int32_t w = 0;
+      if (i < np_adj) {
+        w = L[po + i];
+        const uint32_t bit = 1u << (w & 31);
+        fresh = !(atomicOr(&inr[w >> 5], bit) & bit);
       }
+      const int32_t at = warp_append(cnt, fresh);
+      if (fresh) out[at] = static_cast<uint16_t>(w);
     }
     for (int32_t ei = 0; ei < np_el; ++ei) {
-      const int32_t e = pel[ei];
-      const int32_t* bd = half + bp[e];
-      const int32_t sz = bsz[e];
-      for (int32_t i = threadIdx.x; i < sz; i += blockDim.x) {
-        const int32_t w = bd[i];
-        if (w != p && atomicExch(&mark[w], tok) != tok) {
-          const int32_t at = atomicAdd(cnt, 1);
-          out[at] = w;
-          sreach[at] = static_cast<int16_t>(w);
+      const int32_t e = L[pe - 1 - ei];
+      const uint16_t* bd = cur + ebp[e];
+      const int32_t sz = static_cast<int32_t>(st[e]);
+      if (threadIdx.x == 0) atomicOr(&absb[e >> 5], 1u << (e & 31));
+      for (int32_t i0 = 0; i0 < sz; i0 += blockDim.x) {
+        const int32_t i = i0 + threadIdx.x;
+        bool fresh = false;
+        int32_t w = 0;
+        if (i < sz) {
+          w = bd[i];
+          const uint32_t bit = 1u << (w & 31);
+          fresh = w != p && !(atomicOr(&inr[w >> 5], bit) & bit);
+        }
+        const int32_t at = warp_append(cnt, fresh);
+        if (fresh) out[at] = static_cast<uint16_t>(w);
+      }
+    }
+    if (threadIdx.x == 0) {
+      ebp[p] = static_cast<uint32_t>(cur0);
+      lperm[k] = p;
+      kd[p] = kKeyInf;
+      mark_dirty(p >> 5);  // p was its block's minimum
+    }
+    __syncthreads();  // B2
+    const int32_t nbd = *cnt;
+    // ---- member updates (elimination.cpp:75-83), one member per thread; a
+    // lowered key lowers its block's minimum at once, a raised block minimum
+    // is recomputed below
+    for (int32_t i = threadIdx.x; i < nbd; i += blockDim.x) {
+      const int32_t w = out[i];
+      const uint32_t o = loff[w], oe = loff[w + 1];
+      const uint32_t wst = st[w];
+      const int32_t na = wst & 0xffff, ne = wst >> 16;
+      int32_t c = 0;
+      for (int32_t j = 0; j < na; j += 2) {  // two reads ahead of the writes
+        const int32_t x0 = L[o + j], x1 = j + 1 < na ? L[o + j + 1] : p;
+        const uint32_t i0 = inr[x0 >> 5], i1 = inr[x1 >> 5];
+        if (x0 != p && !((i0 >> (x0 & 31)) & 1u)) L[o + c++] = static_cast<uint16_t>(x0);
+        if (x1 != p && !((i1 >> (x1 & 31)) & 1u)) L[o + c++] = static_cast<uint16_t>(x1);
+      }
+      int32_t ce = 0;
+      uint32_t d = static_cast<uint32_t>(c + nbd);
+      for (int32_t j = 0; j < ne; ++j) {
+        const int32_t e = L[oe - 1 - j];
+        if (!((absb[e >> 5] >> (e & 31)) & 1u)) {
+          L[oe - 1 - ce++] = static_cast<uint16_t>(e);
+          d += st[e];
         }
       }
-    }
-    // absorbed elements get the pivot's token (element ids are dead vertices,
-    // disjoint from the live vertices marked above)
-    for (int32_t ei = threadIdx.x; ei < np_el; ei += blockDim.x) mark[pel[ei]] = tok;
-    if (threadIdx.x == 0) {
-      mark[p] = tok;
-      bp[p] = cur0;
-      order[k] = p;
-      lperm[k] = p;
-      deg[p] = 0xffffffffu;
-      if (!(atomicOr(&dirty[(p >> 5) >> 5], 1u << ((p >> 5) & 31)) & (1u << ((p >> 5) & 31))))
-        s_dlist[atomicAdd(&s_dcnt, 1)] = p >> 5;
-    }
-    __syncthreads();  // B2: reach, marks and absorption marks visible
-    const int32_t nbd = *cnt;
-    // ---- member updates (elimination.cpp:75-83) and their approx degrees
-    for (int32_t i = threadIdx.x; i < nbd; i += blockDim.x) {
-      const int32_t w = sreach[i];
-      const int32_t o = loff[w];
-      const int32_t wst = st[w];
-      int32_t* wa = a.adj + o;
-      int32_t c = 0;
-      const int32_t na = wst & 0xffff, ne = wst >> 16;
-      // lists are compacted in place: read 8 entries ahead of the writes so the
-      // loads are in flight together (the compiler cannot reorder across the
-      // possibly-aliasing stores)
-      for (int32_t j0 = 0; j0 < na; j0 += 8) {
-        int32_t xs[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) xs[q] = j0 + q < na ? wa[j0 + q] : -1;
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (xs[q] >= 0 && mark[xs[q]] != tok) wa[c++] = xs[q];
-      }
-      int32_t* we = a.el + o;
-      int32_t ce = 0;
-      int64_t d = c + nbd;
-      for (int32_t j0 = 0; j0 < ne; j0 += 8) {
-        int32_t es[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) es[q] = j0 + q < ne ? we[j0 + q] : -1;
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (es[q] >= 0 && mark[es[q]] != tok) {
-            we[ce++] = es[q];
-            d += bsz[es[q]];
-          }
-      }
-      we[ce++] = p;
-      st[w] = c | (ce << 16);
-      deg[w] = md_key_deg(d);
-      const uint32_t bit = 1u << ((w >> 5) & 31);
-      if (!(atomicOr(&dirty[(w >> 5) >> 5], bit) & bit)) s_dlist[atomicAdd(&s_dcnt, 1)] = w >> 5;
+      L[oe - 1 - ce++] = static_cast<uint16_t>(p);
+      st[w] = static_cast<uint32_t>(c) | (static_cast<uint32_t>(ce) << 16);
+      const uint32_t nk = (d << 13) | static_cast<uint32_t>(w), ok = kd[w];
+      kd[w] = nk;
+      const int32_t b = w >> 5;
+      if (nk < ok) atomicMin(&blk[b], nk);
+      else if (nk > ok && ok == blk[b]) mark_dirty(b);
     }
     __syncthreads();  // B3
-    for (int32_t ei = threadIdx.x; ei < np_el; ei += blockDim.x) bsz[pel[ei]] = 0;
-    if (threadIdx.x == 0) {
-      bsz[p] = nbd;
-      st[p] = 0;
-      s_cursor += nbd;
-      s_nbc[(k + 1) & 1] = 0;  // its last reader was the previous pivot, before this B2
+    for (int32_t i = threadIdx.x; i < nbd; i += blockDim.x) {
+      const int32_t w = out[i];
+      atomicAnd(&inr[w >> 5], ~(1u << (w & 31)));
     }
-    // ---- refresh dirty blocks
-    const int32_t ndirty = s_dcnt;
+    for (int32_t ei = threadIdx.x; ei < np_el; ei += blockDim.x) {
+      const int32_t e = L[pe - 1 - ei];
+      atomicAnd(&absb[e >> 5], ~(1u << (e & 31)));
+      st[e] = 0;  // absorbed
+    }
+    const int32_t ndirty = s_ndirty;
     for (int32_t q = wid; q < ndirty; q += nwarp) {
       const int32_t b = s_dlist[q];
-      const int32_t i = b * 32 + lane;
-      const uint64_t m = warp_min_u64(i < nv ? key_min(deg[i], static_cast<uint32_t>(i)) : ~0ull);
+      const int32_t v = b * 32 + lane;
+      const uint32_t m = __reduce_min_sync(0xffffffffu, v < nv ? kd[v] : kKeyInf);
       if (lane == 0) {
         blk[b] = m;
-        dirty[b >> 5] = 0;  // every set bit of the word is in the list
+        atomicAnd(&dbits[b >> 5], ~(1u << (b & 31)));
       }
     }
+    if (threadIdx.x == 0) {
+      st[p] = static_cast<uint32_t>(nbd);
+      s_cursor = cur0 + nbd;
+      s_nbd[(k + 1) & 1] = 0;  // its last reader was the previous pivot, before this B2
+    }
     __syncthreads();  // B4
-    if (threadIdx.x == 0) s_dcnt = 0;
+    if (threadIdx.x == 0) s_ndirty = 0;
   }
 }
 
@@ -539,32 +684,53 @@ void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t L, const int
   a.bptr = bptr, a.bsz = bsz, a.vmark = vmark, a.emark = emark, a.gdeg = gdeg, a.pool = pool;
   a.pool_off = pool_off, a.order_ws = order, a.local_perm = local_perm, a.overflow = overflow;
   a.node_mask = node_mask;
-  const size_t smem = sizeof(uint32_t) * kSmemDegCap;
+  // md_kernel: degrees (kSmemDegCap) + block minima / dirty bits of nodes up to 64K vertices
+  const size_t smem = sizeof(uint32_t) * kSmemDegCap + 16384 + 512;
+  DevBuf<uint64_t> gblk(static_cast<size_t>(n >> 5) + nn + 1, s);
+  DevBuf<uint32_t> gdbits(static_cast<size_t>(n >> 10) + 2LL * nn + 2, s);
+  a.gblk = gblk, a.gdbits = gdbits;
+  a.gsmem_bytes = static_cast<int64_t>(smem);
   allow_max_smem(md_kernel, ctx.device);
   const int kt__ = ctx.ktime_begin(kKMd);
   if (mode == 0) {
-    // largest node decides the shared-memory footprint of the fast kernel
+    // one CTA per non-empty node, largest first: shared-memory state where it
+    // fits, global lists (md_node_global) for the rest, in the same launch
     std::vector<int32_t> hoff(nn + 1);
+    std::vector<uint8_t> hmask(node_mask ? nn : 0);
     MP_CUDA(cudaMemcpyAsync(hoff.data(), node_offsets, sizeof(int32_t) * (nn + 1), cudaMemcpyDeviceToHost, s));
+    if (node_mask) MP_CUDA(cudaMemcpyAsync(hmask.data(), node_mask, nn, cudaMemcpyDeviceToHost, s));
     MP_CUDA(cudaStreamSynchronize(s));
-    int32_t maxnv = 0;
-    for (int32_t i = 0; i < nn; ++i) maxnv = std::max(maxnv, hoff[i + 1] - hoff[i]);
-    const int32_t fast_nv = std::min(maxnv, kMdFastCap);
-    const int32_t fnb = (fast_nv + 31) / 32;
-    const size_t fsmem = sizeof(uint64_t) * fnb + sizeof(int32_t) * 5 * fast_nv + sizeof(uint32_t) * ((fnb + 31) / 32 + 1) +
-                         sizeof(int16_t) * (fast_nv + 2);
-    allow_max_smem(md_fast_kernel, ctx.device);
-    MP_KERNEL(ctx, md_fast_kernel<<<nn, kMdThreads, fsmem, s>>>(a));
-    int32_t h_flag = 0;
-    MP_CUDA(cudaMemcpyAsync(&h_flag, overflow.get(), 4, cudaMemcpyDeviceToHost, s));
-    MP_CUDA(cudaStreamSynchronize(s));
-    if (h_flag == 2) {  // a vertex of degree > 32767: the general kernel orders every node
-      MP_CUDA(cudaMemsetAsync(overflow, 0, 4, s));
-      MP_KERNEL(ctx, md_kernel<<<nn, kMdThreads, smem, s>>>(a));
-    } else if (maxnv > kMdFastCap) {
-      a.min_nv = kMdFastCap + 1;  // the general kernel takes the remaining (large) nodes
-      MP_KERNEL(ctx, md_kernel<<<nn, kMdThreads, smem, s>>>(a));
+    std::vector<int32_t> sched;
+    for (int32_t i = 0; i < nn; ++i)
+      if (hoff[i + 1] > hoff[i] && (!node_mask || hmask[i])) sched.push_back(i);
+    std::stable_sort(sched.begin(), sched.end(), [&](int32_t x, int32_t y) {
+      return hoff[x + 1] - hoff[x] > hoff[y + 1] - hoff[y];
+    });
+    const int32_t ns = static_cast<int32_t>(sched.size());
+    int32_t big = 0;
+    while (big < ns && hoff[sched[big] + 1] - hoff[sched[big]] > kMdSmemMaxNv) ++big;
+    DevBuf<int32_t> dsched(std::max(ns, 1), s);
+    if (ns > 0) MP_CUDA(cudaMemcpyAsync(dsched, sched.data(), sizeof(int32_t) * ns, cudaMemcpyHostToDevice, s));
+    if (big > 0) {
+      // nodes above kMdSmemMaxNv: 512-thread CTAs with global lists, on the
+      // auxiliary stream so they overlap the shared-memory kernel
+      MP_CUDA(cudaEventRecord(ctx.fork_ev[0], s));
+      MP_CUDA(cudaStreamWaitEvent(ctx.aux_stream, ctx.fork_ev[0], 0));
+      MdArgs ab = a;
+      ab.sched = dsched;
+      MP_KERNEL(ctx, md_kernel<<<big, kMdThreads, smem, ctx.aux_stream>>>(ab));
+      MP_CUDA(cudaEventRecord(ctx.fork_ev[1], ctx.aux_stream));
     }
+    if (ns > big) {
+      a.sched = dsched.get() + big;
+      allow_max_smem(md_smem_kernel, ctx.device);
+      cudaFuncAttributes fa{};
+      MP_CUDA(cudaFuncGetAttributes(&fa, md_smem_kernel));
+      a.smem_bytes = static_cast<int64_t>(ctx.smem_optin) - static_cast<int64_t>(fa.sharedSizeBytes);
+      a.gsmem_bytes = a.smem_bytes;
+      MP_KERNEL(ctx, md_smem_kernel<<<ns - big, kMdSmemThreads, static_cast<size_t>(a.smem_bytes), s>>>(a));
+    }
+    if (big > 0) MP_CUDA(cudaStreamWaitEvent(s, ctx.fork_ev[1], 0));
   } else {
     MP_KERNEL(ctx, md_kernel<<<nn, kMdThreads, smem, s>>>(a));
   }

@@ -12,6 +12,10 @@ struct mp_context {
   int device = 0;
   cudaStream_t own_stream = nullptr;
   cudaStream_t stream = nullptr;
+  // second stream for work that overlaps the main one inside a stage (forked
+  // from and joined back into `stream` with fork_ev)
+  cudaStream_t aux_stream = nullptr;
+  cudaEvent_t fork_ev[2] = {};
   int num_sms = 148;
   int smem_optin = 232448;  // cudaDevAttrMaxSharedMemoryPerBlockOptin
   int64_t launches = 0;  // kernels launched through this context (cumulative)
