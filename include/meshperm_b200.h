@@ -132,6 +132,26 @@ int mp_context_set_sm_share(mp_context* ctx, int32_t share);
  * cross_block_fill, elimination_fill of an arbitrary permutation and trees
  * whose separators leak always use the game. */
 int mp_context_set_fill_algorithm(mp_context* ctx, int32_t algo);
+/* Internal tuning / fallback selection of one context (defaults: 0 = the
+ * library's own choice).  Results never depend on these; they exist so that
+ * tests can force the fallback paths and so that the sizing can be studied.
+ *   MP_TUNE_FPS_CLUSTER      farthest-point cluster phase: 8 or 16 CTAs, -1 off
+ *   MP_TUNE_FPS_QCAP         cluster-phase queue slots (small: forces overflow)
+ *   MP_TUNE_FPS_GRID_RADIUS  cluster / grid mode while the radius exceeds it
+ *   MP_TUNE_FPS_GRID_CANDS   grid-mode candidates per batch
+ *   MP_TUNE_FPS_SUB_REGION   largest region of the four-group worker mode
+ *   MP_TUNE_LLOYD_BLOCKS     CTAs of the Lloyd kernel
+ * MP_EINVAL for an unknown key. */
+enum {
+  MP_TUNE_FPS_CLUSTER = 0,
+  MP_TUNE_FPS_QCAP = 1,
+  MP_TUNE_FPS_GRID_RADIUS = 2,
+  MP_TUNE_FPS_GRID_CANDS = 3,
+  MP_TUNE_FPS_SUB_REGION = 4,
+  MP_TUNE_LLOYD_BLOCKS = 5,
+  MP_TUNE_COUNT = 6
+};
+int mp_context_set_tuning(mp_context* ctx, int32_t key, int64_t value);
 /* cudaStream_t to run on; NULL restores the context's own stream. */
 int mp_context_set_stream(mp_context* ctx, void* stream);
 
@@ -152,12 +172,15 @@ int mp_order_batch(mp_context* const* ctxs, int32_t nctx, int32_t count, const m
  * mp_order_sharded with the same graph and config.  Every rank computes the
  * patches and the top k = ceil(log2 world) ND levels (sequential chains:
  * replicated, not shipped); the level-k subtrees are then dealt to ranks by
- * size (largest first, least-loaded rank), each rank splits, orders (MD) and
- * plays the fill game on its own subtrees only, and three all-gathers
- * exchange (1) node sizes, (2) the owned nodes' vertex lists + local orders,
- * (3) the subtree roots' live elements and the owned column counts /
- * parents.  Every rank returns the complete, rank-count-independent
- * mp_result -- bit-identical to mp_order.
+ * size (largest first, least-loaded rank), each rank splits and orders (MD)
+ * its own subtrees only, and two all-gathers exchange (1) node sizes and
+ * (2) the owned nodes' vertex lists + local orders.  The fill (etree +
+ * column counts, a few percent of the path) then runs on every rank over the
+ * assembled tree.  With mp_context_set_fill_algorithm(ctx, 1) each rank plays
+ * the elimination game on its own subtrees and a third all-gather exchanges
+ * the subtree roots' live elements and the owned column counts / parents.
+ * Every rank returns the complete, rank-count-independent mp_result --
+ * bit-identical to mp_order.
  *
  * The all-gather is the caller's or the library's NCCL one: recv receives
  * world * bytes, rank r's contribution at r * bytes.  device_buffers = 1:
@@ -245,8 +268,11 @@ int mp_compute_perm_schedule(mp_context* ctx, int32_t n, int32_t nd_level, const
                              int64_t schedule_len, int32_t* perm, int32_t* inverse, int32_t on_device);
 
 /* symbolic.hpp:23 elimination_fill + :31 factor_etree_parents for a
- * permutation produced from an ND tree (perm = compute_perm(tree, ...)).
- * Requires the tree because the device game runs subtree by subtree. */
+ * permutation produced from an ND tree (perm = compute_perm(tree, ...)):
+ * the factor's elimination tree built subtree by subtree (Liu's algorithm,
+ * one CTA per tree node and level) and Gilbert-Ng-Peyton column counts.  A
+ * tree whose separators do not separate (edges between unrelated nodes) is
+ * handled as an arbitrary permutation (mp_elimination_fill). */
 int mp_tree_fill(mp_context* ctx, const mp_csr* g, int32_t nd_level, const int32_t* node_offsets,
                  const int32_t* node_vertices, const int32_t* local_perm, int32_t schedule,
                  int64_t* column_counts, int32_t* etree_parent, int32_t on_device,
@@ -259,8 +285,9 @@ int mp_tree_fill_schedule(mp_context* ctx, const mp_csr* g, int32_t nd_level, co
 
 /* symbolic.hpp:23 elimination_fill + :31 factor_etree_parents for ANY
  * permutation perm[n] (new position -> old index; host or device per
- * on_device): the elimination game played on the device in permutation order
- * (one CTA; the ND-structured mp_tree_fill is the fast path for ND trees).
+ * on_device): the same etree + column-count computation on a one-node tree
+ * (the etree is then one CTA's serial pass; the ND-structured mp_tree_fill
+ * splits it over tree nodes).  With fill algorithm 1 the elimination game.
  * MP_EINVAL "permutation is not a bijection" as symbolic.cpp:16-18. */
 int mp_elimination_fill(mp_context* ctx, const mp_csr* g, const int32_t* perm, int64_t* column_counts,
                         int32_t* etree_parent, int32_t on_device, int64_t* nnz_A, int64_t* nnz_L, int64_t* cost,

@@ -159,6 +159,7 @@ SIGNATURES = [
      [C.c_void_p, C.POINTER(MpCsr), C.c_int32, C.c_void_p, C.c_void_p, C.c_int32, i64p]),
     ("mp_context_set_sm_share", C.c_int, [C.c_void_p, C.c_int32]),
     ("mp_context_set_fill_algorithm", C.c_int, [C.c_void_p, C.c_int32]),
+    ("mp_context_set_tuning", C.c_int, [C.c_void_p, C.c_int32, C.c_int64]),
     ("mp_pattern_to_graph_device", C.c_int,
      [C.c_void_p, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
       C.c_int32, i64p]),

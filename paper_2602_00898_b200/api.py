@@ -129,6 +129,13 @@ class Context:
     def set_stream(self, stream_ptr: int | None):
         check(lib().mp_context_set_stream(self.handle, C.c_void_p(stream_ptr or 0)))
 
+    TUNING = {"fps_cluster": 0, "fps_qcap": 1, "fps_grid_radius": 2, "fps_grid_cands": 3,
+              "fps_sub_region": 4, "lloyd_blocks": 5}
+
+    def set_tuning(self, key: str, value: int):
+        """mp_context_set_tuning: force a fallback path or a sizing (results unchanged)."""
+        check(lib().mp_context_set_tuning(self.handle, self.TUNING[key], int(value)))
+
     def set_fill_algorithm(self, algo: str):
         """'etree' (default: elimination tree + column counts) or 'game' (the
         elimination game of symbolic.cpp:33-45); identical outputs."""

@@ -220,6 +220,14 @@ int mp_context_set_fill_algorithm(mp_context* ctx, int32_t algo) {
   });
 }
 
+int mp_context_set_tuning(mp_context* ctx, int32_t key, int64_t value) {
+  return guarded([&] {
+    if (!ctx) throw Error(MP_EINVAL, "null context");
+    if (key < 0 || key >= MP_TUNE_COUNT) throw Error(MP_EINVAL, "unknown tuning key");
+    ctx->tune[key] = value;
+  });
+}
+
 int mp_context_set_stream(mp_context* ctx, void* stream) {
   return guarded([&] {
     if (!ctx) throw Error(MP_EINVAL, "null context");

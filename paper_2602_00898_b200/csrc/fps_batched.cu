@@ -1024,12 +1024,11 @@ __global__ void __launch_bounds__(kThreads, 1) fps_cluster_phase(BatchArgs a, in
 // Seeds of one component spanning the whole graph (positions = vertex ids).
 void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32_t k, uint64_t seed, int32_t* seeds,
                      int32_t* dist) {
-  const char* gr = getenv("MP_FPS_GRID_RADIUS");  // tuning knobs
   // worker-mode regions are shallower than the grid radius (their depth is
   // below the candidate's distance): kMaxDepth bounds the per-level offsets
-  const int32_t grid_radius = std::min(gr ? atoi(gr) : 200, kMaxDepth);
-  const char* gc = getenv("MP_FPS_GRID_CANDS");
-  const int32_t grid_cands = std::max(1, std::min(gc ? atoi(gc) : 1, kGridCands));
+  const int64_t gr = ctx.tune[MP_TUNE_FPS_GRID_RADIUS], gc = ctx.tune[MP_TUNE_FPS_GRID_CANDS];
+  const int32_t grid_radius = static_cast<int32_t>(std::min<int64_t>(gr > 0 ? gr : 200, kMaxDepth));
+  const int32_t grid_cands = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(gc > 0 ? gc : 1, kGridCands)));
   cudaStream_t s = ctx.stream;
   const int32_t n = g.n;
   int tile_shift = 8;
@@ -1080,28 +1079,27 @@ void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32
   a.bar = reinterpret_cast<unsigned int*>(bar.get());
   a.grid_radius = grid_radius;
   a.grid_cands = grid_cands;
-  const char* sr = getenv("MP_FPS_SUB_REGION");
-  a.sub_region = sr ? atoi(sr) : kSubRegion;
+  a.sub_region = ctx.tune[MP_TUNE_FPS_SUB_REGION] > 0 ? static_cast<int32_t>(ctx.tune[MP_TUNE_FPS_SUB_REGION]) : kSubRegion;
   const int kt = ctx.ktime_begin(kKFps);
   // large-radius seeds on one cluster (16 CTAs where the device allows, else 8)
   a.resume = 0;
   // the cluster kernel's dynamic smem: the select scratch, or 256 staged items per warp
   const size_t cl_smem = std::max(smem, sizeof(uint64_t) * 256 * (kThreads / 32));
   a.qcap = 8LL * n + 1024;  // uint64 items
-  if (const char* qc = getenv("MP_FPS_QCAP")) a.qcap = std::max<int64_t>(64, std::min<int64_t>(a.qcap, atoll(qc)));  // test knob
+  if (ctx.tune[MP_TUNE_FPS_QCAP] > 0) a.qcap = std::max<int64_t>(64, std::min<int64_t>(a.qcap, ctx.tune[MP_TUNE_FPS_QCAP]));
   a.queue = static_cast<int32_t*>(ctx.slab(4, sizeof(uint64_t) * a.qcap));
   DevBuf<int32_t> qctl(96, s);
   a.qctl = qctl;
   MP_CUDA(cudaMemsetAsync(a.queue, 0xff, sizeof(uint64_t) * a.qcap, s));
   MP_CUDA(cudaMemsetAsync(qctl, 0, sizeof(int32_t) * 96, s));
-  if (!getenv("MP_FPS_NO_CLUSTER")) {
+  if (ctx.tune[MP_TUNE_FPS_CLUSTER] >= 0) {
     // cluster size: 16 CTAs (non-portable) where the device allows, else 8;
-    // probed once per device (MP_FPS_CLUSTER overrides and is re-read).  The
-    // function attributes are per device too, so they are set for every
+    // probed once per device (MP_TUNE_FPS_CLUSTER overrides and is re-probed).
+    // The function attributes are per device too, so they are set for every
     // device this process launches on, not only the first one probed.
     static std::mutex mu;
     static std::map<int, int> cached;  // device -> cluster CTAs (0: no cluster launch)
-    const char* ce = getenv("MP_FPS_CLUSTER");
+    const bool ce = ctx.tune[MP_TUNE_FPS_CLUSTER] > 0;
     int cluster_ctas = 0;
     {
       std::lock_guard<std::mutex> lk(mu);
@@ -1111,7 +1109,7 @@ void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32
         const bool nonportable =
             cudaFuncSetAttribute(fps_cluster_phase, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
         cudaGetLastError();
-        const int first = ce ? atoi(ce) : 16;
+        const int first = ce ? static_cast<int>(ctx.tune[MP_TUNE_FPS_CLUSTER]) : 16;
         for (int cs : {first, 16, 8}) {
           if (cs < 1 || cs > 16 || (cs > 8 && !nonportable)) continue;
           cudaLaunchConfig_t cfg{};

@@ -8,10 +8,14 @@
 //   1. tri_count:   validate every triangle, 2 raw entries per corner (atomics)
 //   2. scan         raw list offsets
 //   3. tri_scatter: each corner appends its two opposite corners
-//   4. list_sort:   one thread per vertex sorts + dedups its raw list in shared
-//                   memory (lists longer than kSortCap: listed, one warp each)
-//   5. scan         CSR offsets of the deduplicated lengths
-//   6. list_copy:   compact the sorted lists into neighbors[]
+//   4. list_mark / list_sort_long: lists longer than kSortCap (a vertex in
+//                   more than kSortCap / 2 triangles; block patterns) are
+//                   sorted + deduplicated in place, one warp each
+//   5. list_finish: one thread per vertex sorts + dedups its raw list in
+//                   shared memory, a block scan of the unique lengths plus a
+//                   decoupled look-back across tiles gives the CSR offsets, and
+//                   the thread writes its offset and neighbours directly (no
+//                   separate scan or compaction pass)
 // Algorithmic bytes: 12 per triangle read + 4 (n + 1) + 4 nnz written.
 #include <cub/cub.cuh>
 
@@ -23,7 +27,7 @@
 namespace mp {
 namespace {
 
-constexpr int kSortThreads = 128;
+constexpr int kSortThreads = 256;
 constexpr int kSortCap = 48;  // raw entries per vertex sorted in shared memory
 
 __global__ void tri_count(int64_t ntri, int32_t nv, const int32_t* __restrict__ tris, int32_t* cnt,
@@ -83,34 +87,10 @@ __global__ void pair_scatter(int64_t nnz, int32_t n, int32_t b, const int32_t* _
   }
 }
 
-// Sort + dedup each raw list in place; deg[v] = unique length.  Long lists are
-// left for list_sort_long (appended to `longv`, counted in longv[-1]).
-__global__ void __launch_bounds__(kSortThreads) list_sort(int32_t nv, const int32_t* ro, int32_t* raw, int32_t* deg,
-                                                         int32_t* nlong, int32_t* longv) {
-  __shared__ int32_t sm[kSortThreads * kSortCap];
-  int32_t* my = sm + threadIdx.x;  // strided: entry k at my[k * kSortThreads] (bank-conflict free)
-  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
-    const int32_t b = ro[v], len = ro[v + 1] - b;
-    if (len > kSortCap) {
-      longv[atomicAdd(nlong, 1)] = v;
-      continue;
-    }
-    for (int32_t k = 0; k < len; ++k) {  // insertion sort while loading
-      const int32_t x = raw[b + k];
-      int32_t j = k;
-      while (j > 0 && my[(j - 1) * kSortThreads] > x) {
-        my[j * kSortThreads] = my[(j - 1) * kSortThreads];
-        --j;
-      }
-      my[j * kSortThreads] = x;
-    }
-    int32_t u = 0;
-    for (int32_t k = 0; k < len; ++k) {
-      const int32_t x = my[k * kSortThreads];
-      if (k == 0 || my[(k - 1) * kSortThreads] != x) raw[b + u++] = x;
-    }
-    deg[v] = u;
-  }
+// Lists longer than kSortCap, for list_sort_long.
+__global__ void list_mark(int32_t nv, const int32_t* ro, int32_t* nlong, int32_t* longv) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x)
+    if (ro[v + 1] - ro[v] > kSortCap) longv[atomicAdd(nlong, 1)] = v;
 }
 
 // One warp per long list: odd-even transposition in global memory (rare: a
@@ -139,23 +119,161 @@ __global__ void list_sort_long(const int32_t* nlong, const int32_t* longv, const
   }
 }
 
-__global__ void list_copy(int32_t nv, const int32_t* ro, const int32_t* raw, const int32_t* off, int32_t* nbr) {
-  // one warp per vertex: lists are short, lanes copy consecutive entries
-  const int lane = threadIdx.x & 31;
-  for (int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; w < nv;
-       w += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
-    const int32_t v = static_cast<int32_t>(w);
-    const int32_t b = ro[v], o = off[v], d = off[v + 1] - o;
-    for (int32_t k = lane; k < d; k += 32) nbr[o + k] = raw[b + k];
+// 1D bulk copy global -> shared (TMA, cp.async.bulk) completing on an mbarrier.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra WAIT_%=;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+constexpr int32_t kStage = kSortThreads * 16;  // staged raw entries per tile (16 KB; larger tiles read global)
+
+// Tiles of kSortThreads vertices, taken in order from a counter.  The tile's
+// raw lists are one contiguous range of raw: a bulk copy (TMA) stages it in
+// shared memory, each thread sorts + dedups its list there (long lists are
+// already sorted in place, their unique length in deg), the block scans the
+// unique lengths, thread 0 resolves the tile's offset by decoupled look-back
+// over the earlier tiles' published sums (tstate[t] = flag << 32 | value,
+// 1 aggregate, 2 inclusive), the lists are packed into an output stage and
+// the CTA writes offsets and neighbours with coalesced stores.  A tile whose
+// range does not fit the stage sorts from global memory.
+__global__ void __launch_bounds__(kSortThreads) list_finish(int32_t nv, const int32_t* ro, const int32_t* raw,
+                                                           const int32_t* deg, int32_t* off, int32_t* nbr,
+                                                           unsigned long long* tstate, int32_t* tcounter) {
+  extern __shared__ __align__(128) int32_t lf_stage[];  // in[kStage] | outs[kStage]
+  int32_t* in = lf_stage;
+  int32_t* outs = lf_stage + kStage;
+  __shared__ uint64_t bar;
+  __shared__ int32_t sh[32], s_tile, s_prefix, s_a0, s_staged;
+  volatile unsigned long long* vs = tstate;
+  if (threadIdx.x == 0) mbar_init(&bar);
+  uint32_t phase = 0;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      const int32_t tile = atomicAdd(tcounter, 1);
+      s_tile = tile;
+      s_staged = 0;
+      const int64_t v0 = static_cast<int64_t>(tile) * kSortThreads;
+      if (v0 < nv) {
+        const int32_t v1 = static_cast<int32_t>(v0 + kSortThreads < nv ? v0 + kSortThreads : nv);
+        const int32_t a0 = ro[v0] & ~3, a1 = (ro[v1] + 3) & ~3;  // 16-byte aligned superset
+        s_a0 = a0;
+        if (a1 - a0 <= kStage && a1 > a0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic use of `in`
+          bulk_load(in, raw + a0, static_cast<uint32_t>(a1 - a0) * 4u, &bar);
+          s_staged = 1;
+        }
+      }
+    }
+    __syncthreads();
+    const int32_t tile = s_tile;
+    if (static_cast<int64_t>(tile) * kSortThreads >= nv) break;
+    const bool staged = s_staged;
+    if (staged) {
+      mbar_wait(&bar, phase);
+      phase ^= 1;
+    }
+    const int32_t v = tile * kSortThreads + threadIdx.x;
+    int32_t u = 0, b = 0, len = 0;
+    int32_t* my = nullptr;
+    int32_t loc[kSortCap];  // unstaged tiles only
+    if (v < nv) {
+      b = ro[v], len = ro[v + 1] - b;
+      if (len > kSortCap) {
+        u = deg[v];  // sorted in place by list_sort_long
+      } else {
+        if (staged) {
+          my = in + (b - s_a0);
+        } else {
+          my = loc;
+          for (int32_t k = 0; k < len; ++k) loc[k] = raw[b + k];
+        }
+        for (int32_t k = 1; k < len; ++k) {  // insertion sort
+          const int32_t x = my[k];
+          int32_t j = k;
+          while (j > 0 && my[j - 1] > x) my[j] = my[j - 1], --j;
+          my[j] = x;
+        }
+        for (int32_t k = 0; k < len; ++k)
+          if (u == 0 || my[u - 1] != my[k]) my[u++] = my[k];
+      }
+    }
+    int32_t tot = 0;
+    const int32_t ex = block_excl_scan(u, sh, &tot);
+    // decoupled look-back, one warp: 32 predecessors per step, stop at the
+    // nearest published inclusive prefix
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      if (tile == 0) {
+        if (lane == 0) vs[0] = (2ull << 32) | static_cast<uint32_t>(tot), s_prefix = 0;
+      } else {
+        if (lane == 0) vs[tile] = (1ull << 32) | static_cast<uint32_t>(tot);
+        int32_t prefix = 0;
+        for (int32_t hi = tile - 1;;) {
+          const int32_t t = hi - lane;  // lane 0 nearest
+          unsigned long long x = 0;
+          uint32_t fl = 2;
+          if (t >= 0) {
+            do {
+              x = vs[t];
+              fl = static_cast<uint32_t>(x >> 32);
+            } while (fl == 0);
+          }
+          const uint32_t incl = __ballot_sync(0xffffffffu, t >= 0 && fl == 2);
+          const int stop = incl ? __ffs(incl) - 1 : 32;  // nearest inclusive (or none in the window)
+          int32_t val = (t >= 0 && lane <= stop) ? static_cast<int32_t>(static_cast<uint32_t>(x)) : 0;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+          prefix += val;
+          if (incl || hi - 32 < 0) break;
+          hi -= 32;
+        }
+        if (lane == 0) {
+          vs[tile] = (2ull << 32) | static_cast<uint32_t>(prefix + tot);
+          s_prefix = prefix;
+        }
+      }
+    }
+    // pack the deduplicated lists (never more than the staged input)
+    const int32_t* src = len > kSortCap ? (staged ? in + (b - s_a0) : raw + b) : my;
+    if (staged && v < nv)
+      for (int32_t k = 0; k < u; ++k) outs[ex + k] = src[k];
+    __syncthreads();
+    const int32_t P = s_prefix;
+    if (v < nv) {
+      off[v] = P + ex;
+      if (v == nv - 1) off[nv] = P + ex + u;
+      if (nbr && !staged)
+        for (int32_t k = 0; k < u; ++k) nbr[P + ex + k] = src[k];
+    }
+    if (nbr && staged)
+      for (int32_t i = threadIdx.x; i < tot; i += blockDim.x) nbr[P + i] = outs[i];
+    __syncthreads();  // the stages are consumed before the next tile
   }
 }
 
 }  // namespace
 
-// Builds off (nv + 1) and the neighbours (device pointers): into nbr when it
-// is non-null, else into *alloc (sized here) when that is non-null, else
-// offsets only.  Returns nnz = 2|E|.  Throws MP_EINVAL with the reference's
-// messages.
+int grid_for_items(const mp_context& ctx, int64_t items) {
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, 256), ctx.num_sms * 16LL)));
+}
+
 // Shared back half: raw lists (counted in cnt, appended by scatter(cursors,
 // raw)) -> sorted, deduplicated CSR.  check_bad(verdict) throws for invalid
 // input after the one host synchronisation.
@@ -164,7 +282,7 @@ int64_t csr_from_raw(mp_context& ctx, int32_t nv, int64_t nraw, int32_t* off, in
                      Count count, Scatter scatter, unsigned long long* bad, Check check_bad) {
   cudaStream_t s = ctx.stream;
   if (nraw > 0x7fffffffLL) throw Error(MP_EINVAL, "input too large for int32 offsets");
-  DevBuf<int32_t> cnt(static_cast<size_t>(nv) + 1, s), ro(static_cast<size_t>(nv) + 1, s), raw(std::max<int64_t>(nraw, 1), s);
+  DevBuf<int32_t> cnt(static_cast<size_t>(nv) + 1, s), ro(static_cast<size_t>(nv) + 1, s), raw(std::max<int64_t>(nraw, 1) + 4, s);  // +4: bulk copies read whole 16-byte groups
   MP_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nv + 1), s));
   MP_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s));
   count(cnt.get());
@@ -175,38 +293,35 @@ int64_t csr_from_raw(mp_context& ctx, int32_t nv, int64_t nraw, int32_t* off, in
   MP_CUDA(cudaMemcpyAsync(cnt.get(), ro.get(), sizeof(int32_t) * nv, cudaMemcpyDeviceToDevice, s));  // cursors
   scatter(cnt.get(), raw.get());
   DevBuf<int32_t> deg(static_cast<size_t>(nv) + 1, s), longv(static_cast<size_t>(nv) + 1, s);
-  MP_CUDA(cudaMemsetAsync(deg.get() + nv, 0, sizeof(int32_t), s));
   MP_CUDA(cudaMemsetAsync(longv.get() + nv, 0, sizeof(int32_t), s));  // long-list count
-  if (nv > 0) {
-    const int sg = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(nv, kSortThreads), ctx.num_sms * 8LL)));
-    MP_KERNEL(ctx, list_sort<<<sg, kSortThreads, 0, s>>>(nv, ro, raw, deg, longv.get() + nv, longv));
-    MP_KERNEL(ctx, list_sort_long<<<ctx.num_sms, 256, 0, s>>>(longv.get() + nv, longv, ro, raw, deg));
+  // neighbours: the caller's array, or one sized by the raw count (an upper
+  // bound of nnz, so no host round trip before the finish)
+  if (!nbr && alloc) {
+    alloc->alloc(std::max<int64_t>(nraw, 1), s);
+    nbr = alloc->get();
   }
-  MP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, deg.get(), off, nv + 1, s));
-  DevBuf<char> t2(tmp, s);
-  MP_CUDA(cub::DeviceScan::ExclusiveSum(t2.get(), tmp, deg.get(), off, nv + 1, s));
+  const int64_t tiles = ceil_div(std::max(nv, 1), kSortThreads);
+  DevBuf<unsigned long long> tstate(tiles, s);
+  DevBuf<int32_t> tcounter(1, s);
+  MP_CUDA(cudaMemsetAsync(tstate, 0, sizeof(unsigned long long) * tiles, s));
+  MP_CUDA(cudaMemsetAsync(tcounter, 0, sizeof(int32_t), s));
+  if (nv > 0) {
+    MP_KERNEL(ctx, list_mark<<<grid_for_items(ctx, nv), 256, 0, s>>>(nv, ro, longv.get() + nv, longv));
+    MP_KERNEL(ctx, list_sort_long<<<ctx.num_sms, 256, 0, s>>>(longv.get() + nv, longv, ro, raw, deg));
+    const int fg = static_cast<int>(std::min<int64_t>(tiles, ctx.num_sms * 8LL));
+    allow_max_smem(list_finish, ctx.device);
+    MP_KERNEL(ctx, list_finish<<<fg, kSortThreads, 2 * kStage * sizeof(int32_t), s>>>(nv, ro, raw, deg, off, nbr, tstate,
+                                                                                      tcounter));
+  } else {
+    MP_CUDA(cudaMemsetAsync(off, 0, sizeof(int32_t), s));
+  }
   int32_t nnz = 0;
   unsigned long long hbad = 0;
   MP_CUDA(cudaMemcpyAsync(&nnz, off + nv, sizeof nnz, cudaMemcpyDeviceToHost, s));
   MP_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost, s));
-  if (!nbr && alloc) {
-    MP_CUDA(cudaStreamSynchronize(s));
-    check_bad(hbad);
-    alloc->alloc(std::max(nnz, 1), s);
-    nbr = alloc->get();
-  }
-  if (nbr && nv > 0) {
-    const int cg = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(static_cast<int64_t>(nv) * 32, 256),
-                                                                            ctx.num_sms * 16LL)));
-    MP_KERNEL(ctx, list_copy<<<cg, 256, 0, s>>>(nv, ro, raw, off, nbr));
-  }
   MP_CUDA(cudaStreamSynchronize(s));
   check_bad(hbad);
   return nnz;
-}
-
-int grid_for_items(const mp_context& ctx, int64_t items) {
-  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, 256), ctx.num_sms * 16LL)));
 }
 
 // Builds off (nv + 1) and the neighbours (device pointers): into nbr when it

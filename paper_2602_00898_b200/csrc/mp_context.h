@@ -44,6 +44,7 @@ struct mp_context {
   int fps_workers = 0;  // worker CTAs of the batched FPS (decided once)
   int sm_share = 1;     // contexts expected to run concurrently on the device (grid sizing)
   int fill_algo = 0;    // 0: etree + column counts (colcount.cu), 1: the elimination game (symbolic.cu)
+  int64_t tune[8] = {};  // mp_context_set_tuning (MP_TUNE_*), 0 = default
   // private stream-ordered pool for the per-call scratch (release threshold
   // raised on this pool only, never on the device's default pool)
   cudaMemPool_t pool = nullptr;

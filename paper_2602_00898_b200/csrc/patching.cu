@@ -1301,7 +1301,8 @@ int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, ui
     int blocks = std::max(1, std::min(bpsm, 4)) * std::max(ctx.num_sms / std::max(ctx.sm_share, 1), 1);
     // small meshes: one CTA per SM is enough and makes the grid barriers cheaper
     blocks = static_cast<int>(std::min<int64_t>(blocks, std::max<int64_t>(ctx.num_sms / std::max(ctx.sm_share, 1), ceil_div(n, 512))));
-    if (const char* lb = getenv("MP_LLOYD_BLOCKS")) blocks = std::max(1, std::min(blocks, atoi(lb)));  // tuning knob
+    if (ctx.tune[MP_TUNE_LLOYD_BLOCKS] > 0)
+      blocks = std::max(1, std::min<int>(blocks, static_cast<int>(ctx.tune[MP_TUNE_LLOYD_BLOCKS])));
     void* args[] = {&la};
     { const int kt__ = ctx.ktime_begin(kKLloyd); MP_KERNEL(ctx, MP_CUDA(cudaLaunchCooperativeKernel((void*)lloyd_kernel, blocks, 256, args, 0, s))); ctx.ktime_end(kt__); }
     MP_KERNEL(ctx, lloyd_finish<<<grid_for(ctx, n), 256, 0, s>>>(n, comp_of.get(), comp_mode, prev, assignment));

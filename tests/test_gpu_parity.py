@@ -506,17 +506,18 @@ def test_sm_share_does_not_change_results(share):
     assert res.fill.nnz_L == gold["nnz_L"]
 
 
-@pytest.mark.parametrize("env", [{"MP_FPS_QCAP": "64"}, {"MP_FPS_NO_CLUSTER": "1"}, {"MP_FPS_CLUSTER": "8"}])
-def test_fps_fallbacks_match_reference(env, monkeypatch):
+@pytest.mark.parametrize("tune", [{"fps_qcap": 64}, {"fps_cluster": -1}, {"fps_cluster": 8}, {"lloyd_blocks": 3}])
+def test_fps_fallbacks_match_reference(tune):
     """The cluster phase's queue overflow (forced with a 64-slot queue) hands
     FPS to the batched kernel from scratch; without the cluster phase the
     batched kernel's grid mode runs the large radii; an 8-CTA cluster is the
     portable fallback.  All must reproduce the reference (ico158 digests)."""
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
+    ctx = mp.Context(0)
+    for k, v in tune.items():
+        ctx.set_tuning(k, v)
     gold = json.loads((GOLDEN / "bench_golden.json").read_text())["ico158"]
     g = mp.mesh_to_graph(mp.make_icosphere_mesh(158))
-    res = mp.order(g, ctx=mp.Context(0))
+    res = mp.order(g, ctx=ctx)
     assert res.patch.patch_count == gold["patch_count"]
     assert digest(res.patch.assignment) == gold["sha_assignment"]
     assert digest(res.perm.perm) == gold["sha_perm"]
