@@ -95,6 +95,7 @@ class PipelineResult:  # pipeline.hpp:56-61
     fill: FillReport | None
     stage_ms: dict = field(default_factory=dict)
     kernel_launches: int = 0
+    kernel_ms: dict = field(default_factory=dict)  # per kernel family (mp_result.kernel_ms)
 
 
 def _i32(a) -> np.ndarray:
@@ -548,6 +549,9 @@ def _prepare(g: AdjacencyGraph, nd_level: int, block_size: int, want_fill: bool)
     return bufs, res
 
 
+KERNEL_NAMES = ["fps", "lloyd", "fm", "refine", "md", "symbolic"]
+
+
 def _finish(g: AdjacencyGraph, bufs, res: MpResult, patch_size: int, block_size: int, want_fill: bool):
     N = block_size * g.n
     tree = EliminationTree(N, res.nd_level, bufs["tree_node_offsets"], bufs["tree_vertices"][:N],
@@ -559,7 +563,8 @@ def _finish(g: AdjacencyGraph, bufs, res: MpResult, patch_size: int, block_size:
     names = ["patch", "quotient", "etree", "local", "assemble", "symbolic"]
     return PipelineResult(PatchPartition(bufs["patch_of"][:g.n], res.patch_count, patch_size), tree,
                           Permutation(bufs["perm"][:N], bufs["inverse"][:N]), fill,
-                          {k: float(res.stage_ms[i]) for i, k in enumerate(names)}, int(res.kernel_launches))
+                          {k: float(res.stage_ms[i]) for i, k in enumerate(names)}, int(res.kernel_launches),
+                          {k: float(res.kernel_ms[i]) for i, k in enumerate(KERNEL_NAMES)})
 
 
 def order(g: AdjacencyGraph, patch_size: int = 256, nd_level: int = -1, seed: int = 0, local_mode="approx_md",

@@ -92,6 +92,8 @@ struct LevelArgs {
   int64_t fm_smem_bytes;   // dynamic shared memory of the FM launch
   int32_t* fm_moves;
   const uint8_t* own_mask; // sharded build (mp_order_sharded): nodes this rank splits; NULL = all
+  int32_t* ref_cnt;        // per level node: initial separator size (ref_init)
+  int32_t* ref_rw;         // per level node: [2*i] / [2*i+1] remaining vertices per side
 };
 
 __global__ void level_weights(LevelArgs a) {
@@ -853,6 +855,76 @@ __device__ __forceinline__ RefKey warp_min_ref(RefKey k) {
   return RefKey{(static_cast<uint64_t>(m1) << 32) | m0, (static_cast<uint64_t>(n1) << 32) | n0};
 }
 
+// Initial separator of every active node (partition.cpp:212-222: the smaller
+// boundary, ties to the left), grid-wide over the level's vertices: members
+// join the node's candidate list (global, slot order arbitrary -- the moves
+// pick by key) and leave their region; the rest is counted per side.
+__global__ void ref_init(LevelArgs a) {
+  __shared__ int64_t red[32];
+  const int lane = threadIdx.x & 31;
+  for (int32_t li = blockIdx.y; li < a.width; li += gridDim.y) {
+    if (!a.active[li]) continue;
+    const int32_t s0 = a.seg_start[li], cnt = a.seg_cnt[li];
+    const int8_t take = a.bcount[2 * li] <= a.bcount[2 * li + 1] ? 0 : 1;
+    int32_t c0 = 0, c1 = 0;
+    const int32_t w0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+    for (int32_t i0 = w0; i0 < cnt; i0 += gridDim.x * blockDim.x) {
+      const int32_t i = i0 + lane;
+      const int32_t v = i < cnt ? a.vlist[s0 + i] : -1;
+      const int8_t r = v >= 0 ? a.region[v] : int8_t(-1);
+      const bool mem = v >= 0 && a.in_super[v] && r == take;
+      const int32_t slot = warp_append(&a.ref_cnt[li], mem);
+      if (mem) {
+        a.sep_list[s0 + slot] = v;
+        a.ref_own[s0 + slot] = static_cast<uint8_t>(take);
+        a.ref_in[s0 + slot] = 1;
+        a.slot_of[v] = slot;
+        a.region[v] = 2;
+      } else if (v >= 0) {
+        (r == 0 ? c0 : c1)++;
+      }
+    }
+    const int64_t t0 = block_sum_i64(c0, red), t1 = block_sum_i64(c1, red);
+    if (threadIdx.x == 0) {
+      if (t0) atomicAdd(&a.ref_rw[2 * li], static_cast<int32_t>(t0));
+      if (t1) atomicAdd(&a.ref_rw[2 * li + 1], static_cast<int32_t>(t1));
+    }
+  }
+}
+
+// Split after refine: every vertex of an active node left in region 0 / 1
+// moves to the left / right child (node_of, child counts); the stable radix
+// sort that follows on key (node << 1 | side) packs the children's vertex
+// lists in node order, ascending inside each (separator and leaf vertices
+// get the drop key and sort past the end).
+__global__ void split_classify(LevelArgs a, uint32_t* keys, uint32_t drop_key, int32_t* next_cnt) {
+  __shared__ int64_t red[32];
+  for (int32_t li = blockIdx.y; li < a.width; li += gridDim.y) {
+    const int32_t s0 = a.seg_start[li], cnt = a.seg_cnt[li];
+    const bool act = a.active[li] != 0;
+    const int32_t node = a.first + li;
+    int32_t c0 = 0, c1 = 0;
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+      const int32_t v = a.vlist[s0 + i];
+      const int8_t r = act ? a.region[v] : int8_t(3);
+      if (r == 0 || r == 1) {
+        keys[s0 + i] = (static_cast<uint32_t>(li) << 1) | static_cast<uint32_t>(r);
+        a.node_of[v] = 2 * node + 1 + r;
+        (r ? c1 : c0)++;
+      } else {
+        keys[s0 + i] = drop_key;
+      }
+    }
+    if (act) {
+      const int64_t t0 = block_sum_i64(c0, red), t1 = block_sum_i64(c1, red);
+      if (threadIdx.x == 0) {
+        if (t0) atomicAdd(&next_cnt[2 * li], static_cast<int32_t>(t0));
+        if (t1) atomicAdd(&next_cnt[2 * li + 1], static_cast<int32_t>(t1));
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
   const int32_t li = blockIdx.x;
   const int32_t s0 = a.seg_start[li], cnt = a.seg_cnt[li];
@@ -863,17 +935,7 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
   __shared__ int32_t s_list, s_mv, s_moves, s_pw[32];
   extern __shared__ int32_t ref_sm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  const int32_t lc = 2 * li, rc = 2 * li + 1;  // children, local to the next level
-  const int32_t node = a.first + li;
-  if (!a.active[li]) {
-    if (threadIdx.x == 0) {
-      a.next_start[lc] = s0, a.next_cnt[lc] = 0;
-      a.next_start[rc] = s0, a.next_cnt[rc] = 0;
-    }
-    return;
-  }
-  const int32_t* seg = a.vlist + s0;
-  __shared__ int32_t sh64[64];
+  if (!a.active[li]) return;  // no split (split_classify drops its vertices)
   // candidate list: shared memory while it fits (checked before every move;
   // a move adds at most one entry), the global scratch of the node otherwise
   bool in_smem;
@@ -900,42 +962,18 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
   };
   auto degree = [&](int32_t v) { return a.g.off[v + 1] - a.g.off[v]; };
 
-  // initial separator: the smaller boundary, ties to the left (partition.cpp:212-222)
-  const int8_t take = a.bcount[2 * li] <= a.bcount[2 * li + 1] ? 0 : 1;
+  // initial separator (ref_init): the list in the node's global scratch,
+  // moved into shared memory when it fits
   {
-    // counts: separator entries, and the remaining vertices per region
-    int32_t nin = 0, c0 = 0, c1 = 0;
-    for (int32_t i0 = 0; i0 < cnt; i0 += 8 * blockDim.x) {
-      int8_t rr[8];
-      bool su[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {  // eight loads in flight per thread
-        const int32_t i = i0 + q * blockDim.x + threadIdx.x;
-        const int32_t v = i < cnt ? seg[i] : -1;
-        rr[q] = v >= 0 ? region[v] : int8_t(-1);
-        su[q] = v >= 0 && a.in_super[v];
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        if (rr[q] < 0) continue;
-        if (su[q] && rr[q] == take) ++nin;
-        else (rr[q] == 0 ? c0 : c1)++;
-      }
-    }
-    const int32_t run = static_cast<int32_t>(block_sum_i64(nin, reinterpret_cast<int64_t*>(sred)));
+    const int32_t run = a.ref_cnt[li];
+    const int64_t r0 = a.ref_rw[2 * li], r1 = a.ref_rw[2 * li + 1];
     use_lists(run < kRefSmemList / 2);
-    block_ordered_split(
-        cnt, sh64, [&](int32_t i) { const int32_t v = seg[i]; return (a.in_super[v] && region[v] == take) ? 0 : -1; },
-        [&](int32_t i, int, int32_t k) {
-          const int32_t v = seg[i];
-          lv[k] = v;
-          lown[k] = static_cast<uint8_t>(take);
-          lin[k] = 1;
-          a.slot_of[v] = k;
-          region[v] = 2;
-        });
-    const int64_t r0 = block_sum_i64(c0, reinterpret_cast<int64_t*>(sred));
-    const int64_t r1 = block_sum_i64(c1, reinterpret_cast<int64_t*>(sred));
+    if (in_smem)
+      for (int32_t k = threadIdx.x; k < run; k += blockDim.x) {
+        lv[k] = a.sep_list[s0 + k];
+        lown[k] = a.ref_own[s0 + k];
+        lin[k] = 1;
+      }
     if (threadIdx.x == 0) {
       s_list = run;
       s_size = run;
@@ -1172,32 +1210,14 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
     __syncthreads();
     if (s_mv < 0) break;
   }
-  // split the node: separator stays at `node` (and leaves play: region 3),
-  // sides go to the children (stable, so each child's list stays ascending)
-  int32_t* out = a.next_vlist + s0;
-  // left then right, each stable (ascending): two ordered passes, the second
-  // offset by the left count
-  const int2 lr = block_ordered_split(cnt, sh64, [&](int32_t i) { const int8_t r = region[seg[i]]; return r <= 1 ? r : -1; },
-                                      [&](int32_t, int, int32_t) {});
-  const int32_t runl = lr.x, runr = lr.y;
-  block_ordered_split(
-      cnt, sh64, [&](int32_t i) { const int8_t r = region[seg[i]]; return r <= 1 ? r : -1; },
-      [&](int32_t i, int c, int32_t k) {
-        const int32_t v = seg[i];
-        out[c ? runl + k : k] = v;
-        a.node_of[v] = 2 * node + 1 + c;
-      });
-  __syncthreads();
+  // the separator stays at `node` and leaves play (region 3); split_classify
+  // moves the sides to the children
   for (int32_t i = threadIdx.x; i < s_list; i += blockDim.x) {
     const int32_t v = lv[i];
     a.slot_of[v] = -1;
     if (region[v] == 2) region[v] = 3;  // the separator leaves the game
   }
-  if (threadIdx.x == 0) {
-    a.next_start[lc] = s0, a.next_cnt[lc] = runl;
-    a.next_start[rc] = s0 + runl, a.next_cnt[rc] = runr;
-    atomicAdd(&a.stats[1], static_cast<unsigned long long>(s_moves));
-  }
+  if (threadIdx.x == 0) atomicAdd(&a.stats[1], static_cast<unsigned long long>(s_moves));
 }
 
 template <class T>
@@ -1392,6 +1412,7 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
   MP_CUDA(cudaMemsetAsync(in_list, 0, std::max(n, 1), s));
   MP_CUDA(cudaMemsetAsync(region, 3, std::max(n, 1), s));  // 3 = not in play
   DevBuf<uint8_t> vside(std::max(n, 1), s);
+  DevBuf<uint32_t> split_keys(std::max(n, 1), s), split_keys_out(std::max(n, 1), s);
   DevBuf<int32_t> ell(8LL * std::max(n, 1), s);
   if (n > 0) MP_KERNEL(ctx, build_ell_nd<<<grid_for(ctx, n), 256, 0, s>>>(g, ell));
   MP_CUDA(cudaMemsetAsync(stats, 0, 16, s));
@@ -1563,10 +1584,40 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     else exact ? launch_fm(fm_kernel<uint64_t, true>) : launch_fm(fm_kernel<uint64_t, false>);
     st.mark("level/fm");
     MP_KERNEL(ctx, super_pass<<<lgrid, 256, 0, s>>>(a));
+    DevBuf<int32_t> ref_cnt(width, s), ref_rw(2 * width, s);
+    MP_CUDA(cudaMemsetAsync(ref_cnt, 0, sizeof(int32_t) * width, s));
+    MP_CUDA(cudaMemsetAsync(ref_rw, 0, sizeof(int32_t) * 2 * width, s));
+    a.ref_cnt = ref_cnt, a.ref_rw = ref_rw;
     const size_t ref_smem = static_cast<size_t>(kRefSmemList) * 10;  // 120 KB
     allow_max_smem(refine_kernel, ctx.device);
-    { const int kt__ = ctx.ktime_begin(kKRefine); MP_KERNEL(ctx, refine_kernel<<<width, kNodeThreads, ref_smem, s>>>(a)); ctx.ktime_end(kt__); }
+    {
+      const int kt__ = ctx.ktime_begin(kKRefine);
+      MP_KERNEL(ctx, ref_init<<<lgrid, 256, 0, s>>>(a));
+      MP_KERNEL(ctx, refine_kernel<<<width, kNodeThreads, ref_smem, s>>>(a));
+      ctx.ktime_end(kt__);
+    }
     st.mark("level/super+refine");
+    // split: children's vertex lists packed in node order by a stable radix
+    // sort on (node << 1 | side); the rest gets drop_key and sorts past the end
+    {
+      const uint32_t drop_key = static_cast<uint32_t>(2 * width);
+      MP_KERNEL(ctx, fill32<<<grid_for(ctx, n), 256, 0, s>>>(n, reinterpret_cast<int32_t*>(split_keys.get()),
+                                                               static_cast<int32_t>(drop_key)));
+      MP_CUDA(cudaMemsetAsync(next_cnt, 0, sizeof(int32_t) * 2 * width, s));
+      MP_KERNEL(ctx, split_classify<<<lgrid, 256, 0, s>>>(a, split_keys, drop_key, next_cnt));
+      const int nb = bits_for(drop_key);
+      size_t tmp = 0;
+      MP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, split_keys.get(), split_keys_out.get(), cur_list, nxt_list,
+                                              n, 0, nb, s));
+      DevBuf<char> t(tmp, s);
+      MP_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, split_keys.get(), split_keys_out.get(), cur_list, nxt_list,
+                                              n, 0, nb, s));
+      size_t tmp2 = 0;
+      MP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp2, next_cnt.get(), next_start.get(), 2 * width, s));
+      DevBuf<char> t2(tmp2, s);
+      MP_CUDA(cub::DeviceScan::ExclusiveSum(t2.get(), tmp2, next_cnt.get(), next_start.get(), 2 * width, s));
+    }
+    st.mark("level/split");
     // next level
     seg_start = std::move(next_start);
     seg_cnt = std::move(next_cnt);
