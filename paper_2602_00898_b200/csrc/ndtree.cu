@@ -1267,9 +1267,15 @@ int64_t quotient_from_keys(mp_context& ctx, uint64_t* keys, int64_t nkeys, int32
   return U;
 }
 
-__global__ void node_hist(int32_t n, const int32_t* node_of, int32_t* cnt) {
-  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
-    atomicAdd(&cnt[node_of[v]], 1);
+// node_offsets from the node-sorted keys: the run boundary between keys
+// kout[i-1] < kout[i] starts every node in (kout[i-1], kout[i]] at i (empty
+// nodes included); the ends of the key range fill the rest.
+__global__ void node_bounds(int32_t n, int64_t nn, const int32_t* kout, int32_t* node_offsets) {
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x) {
+    const int64_t lo = i == 0 ? 0 : static_cast<int64_t>(kout[i - 1]) + 1;
+    const int64_t hi = i == n ? nn : static_cast<int64_t>(kout[i]);
+    for (int64_t x = lo; x <= hi; ++x) node_offsets[x] = i;
+  }
 }
 
 __global__ void count_weights_all(int32_t n, const int32_t* assign, int32_t* pw) {
@@ -1626,19 +1632,14 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
   }
   // flatten: stable sort of vertices by node id (ascending vertex inside a node)
   if (n > 0) {
-    DevBuf<int32_t> ids(n, s), kout(n, s), hist(nn + 1, s);
+    DevBuf<int32_t> ids(n, s), kout(n, s);
     MP_KERNEL(ctx, iota32<<<grid_for(ctx, n), 256, 0, s>>>(n, ids));
     size_t tmp = 0;
     const int nb = bits_for(nn);
     MP_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, node_of, kout.get(), ids.get(), node_vertices, n, 0, nb, s));
     DevBuf<char> t(tmp, s);
     MP_CUDA(cub::DeviceRadixSort::SortPairs(t.get(), tmp, node_of, kout.get(), ids.get(), node_vertices, n, 0, nb, s));
-    MP_CUDA(cudaMemsetAsync(hist, 0, sizeof(int32_t) * (nn + 1), s));
-    MP_KERNEL(ctx, node_hist<<<grid_for(ctx, n), 256, 0, s>>>(n, node_of, hist));
-    size_t tmp2 = 0;
-    MP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp2, hist.get(), node_offsets, nn + 1, s));
-    DevBuf<char> t2(tmp2, s);
-    MP_CUDA(cub::DeviceScan::ExclusiveSum(t2.get(), tmp2, hist.get(), node_offsets, nn + 1, s));
+    MP_KERNEL(ctx, node_bounds<<<grid_for(ctx, n + 1), 256, 0, s>>>(n, nn, kout, node_offsets));
   } else {
     MP_CUDA(cudaMemsetAsync(node_offsets, 0, sizeof(int32_t) * (nn + 1), s));
   }

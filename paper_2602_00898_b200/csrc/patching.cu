@@ -50,9 +50,19 @@ __device__ __forceinline__ int32_t uf_find(int32_t* par, int32_t x) {
   }
 }
 
-__global__ void uf_init(int32_t n, int32_t* par) {
-  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
-    par[v] = v;
+// Start every vertex at its smallest neighbour in the same label class (or
+// itself): chains strictly decrease, so they end at set roots, and most hooks
+// below find their endpoints already joined.
+__global__ void uf_init(DGraph g, int32_t* par, const int32_t* label) {
+  for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < g.n; v += gridDim.x * blockDim.x) {
+    const int32_t lv = label ? label[v] : 0;
+    int32_t m = v;
+    for (int32_t j = g.off[v]; j < g.off[v + 1]; ++j) {
+      const int32_t w = g.nbr[j];
+      if (w < m && (!label || label[w] == lv)) m = w;
+    }
+    par[v] = m;
+  }
 }
 
 // Hook the larger root under the smaller one, so every root is the minimum
@@ -94,7 +104,7 @@ __global__ void uf_roots(int32_t n, const int32_t* par, int32_t* root) {
 void union_find(mp_context& ctx, const DGraph& g, const int32_t* label, int32_t* par) {
   const int blocks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(g.n, 256), ctx.num_sms * 8));
   DevBuf<int32_t> work(std::max(g.n, 1), ctx.stream);
-  MP_KERNEL(ctx, uf_init<<<blocks, 256, 0, ctx.stream>>>(g.n, work));
+  MP_KERNEL(ctx, uf_init<<<blocks, 256, 0, ctx.stream>>>(g, work, label));
   MP_KERNEL(ctx, uf_hook<<<blocks, 256, 0, ctx.stream>>>(g, work, label));
   MP_KERNEL(ctx, uf_roots<<<blocks, 256, 0, ctx.stream>>>(g.n, work, par));
 }
