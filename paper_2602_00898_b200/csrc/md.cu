@@ -667,6 +667,8 @@ void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t L, const int
     MP_CUDA(cub::DeviceScan::ExclusiveSum(t.get(), tmp, need.get(), pool_off.get(), nn + 1, s));
   }
   int64_t pool_total = 0;
+  std::vector<int64_t> hneed(mode == 0 ? nn : 0);  // per node: 2 (4 deg sum + 2 nv + 64)
+  if (mode == 0) MP_CUDA(cudaMemcpyAsync(hneed.data(), need.get(), sizeof(int64_t) * nn, cudaMemcpyDeviceToHost, s));
   MP_CUDA(cudaMemcpyAsync(&pool_total, pool_off.get() + nn, 8, cudaMemcpyDeviceToHost, s));
   MP_CUDA(cudaMemsetAsync(overflow, 0, 4, s));
   MP_CUDA(cudaStreamSynchronize(s));
@@ -726,7 +728,19 @@ void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t L, const int
       allow_max_smem(md_smem_kernel, ctx.device);
       cudaFuncAttributes fa{};
       MP_CUDA(cudaFuncGetAttributes(&fa, md_smem_kernel));
-      a.smem_bytes = static_cast<int64_t>(ctx.smem_optin) - static_cast<int64_t>(fa.sharedSizeBytes);
+      // dynamic shared memory: what the largest shared-memory node needs
+      // (state + lists from its degree sum + pool halves of 2 nv entries), so
+      // small nodes (C4 frames) keep several CTAs per SM and leave room for
+      // the other contexts' kernels
+      const int64_t cap = static_cast<int64_t>(ctx.smem_optin) - static_cast<int64_t>(fa.sharedSizeBytes);
+      int64_t want = 0;
+      for (int32_t i = big; i < ns; ++i) {
+        const int32_t node = sched[i];
+        const int64_t nv = hoff[node + 1] - hoff[node];
+        const int64_t dsum = (hneed[node] / 2 - 64 - 2 * nv) / 4;
+        want = std::max(want, md_smem_fixed(static_cast<int32_t>(nv)) + 2 * dsum + 4 * std::max<int64_t>(kMdMinHalf, 2 * nv));
+      }
+      a.smem_bytes = std::min(cap, (want + 1023) & ~int64_t(1023));
       a.gsmem_bytes = a.smem_bytes;
       MP_KERNEL(ctx, md_smem_kernel<<<ns - big, kMdSmemThreads, static_cast<size_t>(a.smem_bytes), s>>>(a));
     }
