@@ -51,8 +51,8 @@ for rep in sorted(glob.glob(f"gpurun_out/{R}_ncu_*.ncu-rep")):
             return f * scale
         rb, wb = num("dram__bytes_read.sum"), num("dram__bytes_write.sum")
         vals["DRAM read+write"] = f"{(rb + wb)/1e6:.2f} MB"
-        traffic[kname.replace("_kernel", "").replace("fps_batched", "fps").replace("md_fast", "md").replace("sym", "symbolic")] = int(rb + wb)
-        if kname in ("tri_scatter", "list_sort"):
+        traffic[kname.replace("_kernel", "").replace("fps_batched", "fps").replace("md_smem", "md")] = int(rb + wb)
+        if kname in ("tri_scatter", "list_finish"):
             traffic["csr_build"] = traffic.get("csr_build", 0) + int(rb + wb)
     out.append(f"## `{kname}`\n")
     out.append("| metric | value |\n|---|---|")
