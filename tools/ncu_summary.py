@@ -10,13 +10,15 @@ out = [f"# ncu summary, round {R}\n", "Captured on one B200 with `tools/profile_
 rows = [r for r in csv.reader(open(f"gpurun_out/{R}_launches.csv")) if len(r) > 10]
 h = rows[0]; ki = h.index("Kernel Name"); vi = h.index("Metric Value")
 data = [(r[ki], float(r[vi].replace(",", ""))) for r in rows[1:]]
-half = data[len(data) // 2:]  # the timed (second) call
+# one whole mp_order call: from the last-but-one fps_cluster_phase launch to the last
+starts = [i for i, (k, _) in enumerate(data) if "fps_cluster_phase" in k]
+half = data[starts[-2]:starts[-1]] if len(starts) >= 2 else data[len(data) // 2:]
 tot = defaultdict(float); cnt = defaultdict(int)
 for k, v in half:
     name = k.split("(")[0].replace("mp::<unnamed>::", "").replace("void ", "")[:60]
     tot[name] += v; cnt[name] += 1
 T = sum(tot.values())
-out.append("## Launch list (second bench call; gpu__time_duration.sum)\n")
+out.append("## Launch list (one mp_order call of the C2 bench; gpu__time_duration.sum)\n")
 out.append("| kernel | launches | ms | share |\n|---|---|---|---|")
 for k, v in sorted(tot.items(), key=lambda x: -x[1])[:20]:
     out.append(f"| `{k}` | {cnt[k]} | {v/1e6:.3f} | {100*v/T:.1f}% |")
