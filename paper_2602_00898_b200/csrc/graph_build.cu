@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(kSortThreads) list_finish(int32_t nv, const in
   __shared__ int32_t sh[32], s_tile, s_prefix, s_a0, s_staged;
   volatile unsigned long long* vs = tstate;
   if (threadIdx.x == 0) mbar_init(&bar);
+  __syncthreads();  // the barrier is initialised before any thread can observe it
   uint32_t phase = 0;
   for (;;) {
     if (threadIdx.x == 0) {

@@ -17,3 +17,29 @@ assert mp.tree_separation_violations(g2, r2.tree) == 0
 g3 = mp.mesh_to_graph(mp.make_icosphere_mesh(int(sys.argv[1]) if len(sys.argv) > 1 else 60))
 r3 = mp.order(g3)
 print("sanitize ok", r.fill.nnz_L, r2.fill.nnz_L, m.edge_count(), g3.n, r3.patch.patch_count, r3.fill.nnz_L)
+# round 2 paths: the game fill (fill algorithm 1) against the etree + counts
+# fill, the fill of an arbitrary permutation, a block pattern (rows with more
+# than 32 lower neighbours), and a node large enough to compact its MD pool
+ctx = mp.Context(0)
+ctx.set_fill_algorithm("game")
+rg = mp.order(g2, patch_size=16, nd_level=4, ctx=ctx)
+assert np.array_equal(rg.fill.column_counts, r2.fill.column_counts)
+perm = np.random.default_rng(1).permutation(g2.n).astype(np.int32)
+fe = mp.elimination_fill(g2, perm)
+rows, offs = [], [0]
+b = 12
+for v in range(g.n if False else 300):
+    pass
+g4 = mp.mesh_to_graph(mp.make_grid_mesh(12, 9))
+blk_rows, blk_off = [], [0]
+for v in range(g4.n):
+    blocks = np.sort(np.concatenate([[v], g4.neighbors[g4.offsets[v]:g4.offsets[v + 1]]]))
+    cols = (blocks[:, None] * b + np.arange(b)[None, :]).ravel()
+    for i in range(b):
+        row = cols[cols != v * b + i]
+        blk_rows.append(row)
+        blk_off.append(blk_off[-1] + len(row))
+g5 = mp.AdjacencyGraph(g4.n * b, np.asarray(blk_off, np.int32), np.concatenate(blk_rows).astype(np.int32))
+r5 = mp.order(g5, patch_size=64, nd_level=2)
+r6 = mp.order(mp.mesh_to_graph(mp.make_grid_mesh(90, 90)), patch_size=2000, nd_level=1)
+print("round2 paths ok", rg.fill.nnz_L, fe.nnz_L, r5.fill.nnz_L, r6.fill.nnz_L)
