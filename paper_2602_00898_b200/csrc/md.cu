@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
   uint32_t* absb = inr + nb;
   uint32_t* dbits = absb + nb;  // dirty blocks (nb bits)
   uint16_t* L = reinterpret_cast<uint16_t*>(dbits + (nb + 31) / 32 + 1);
-  __shared__ int32_t s_cursor, s_cap, s_inglobal, s_maxdeg, s_nbd[2], s_ndirty, sh[32];
+  __shared__ int32_t s_cursor, s_cap, s_inglobal, s_maxdeg, s_nbd[2], s_ndirty, s_ip, sh[32];
   __shared__ int32_t s_dlist[kMdSmemMaxNv / 32];
   __shared__ int64_t s_red64[32];
   __shared__ uint16_t* s_cur;
@@ -516,36 +516,57 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
     const uint32_t pst = st[p];
     const int32_t np_adj = pst & 0xffff, np_el = pst >> 16;
     const uint32_t po = loff[p], pe = loff[p + 1];
-    // ---- reach: variables of p plus the boundaries of p's elements
-    // (warp-aggregated appends)
-    for (int32_t i0 = 0; i0 < np_adj; i0 += blockDim.x) {
-      const int32_t i = i0 + threadIdx.x;
-      bool fresh = false;
-      int32_t w = 0;
-      if (i < np_adj) {
-        w = L[po + i];
-        const uint32_t bit = 1u << (w & 31);
-        fresh = !(atomicOr(&inr[w >> 5], bit) & bit);
+    // ---- reach: variables of p plus the boundaries of p's elements.  With at
+    // most one element the parts need no deduplication: adj(p) lost every
+    // member of that element's boundary when the element formed (and lists
+    // only shrink), the boundary holds distinct live vertices, p among them
+    // once.  So they are copied as they are (p's entry is swapped out after
+    // the member updates) and the count is known without a barrier.
+    int32_t nbd = 0, ptotal = 0;
+    const bool simple = np_el <= 1;
+    if (simple) {
+      const int32_t e1 = np_el ? L[pe - 1] : 0;
+      const uint16_t* bd = cur + (np_el ? ebp[e1] : 0);
+      const int32_t sz = np_el ? static_cast<int32_t>(st[e1]) : 0;
+      ptotal = np_adj + sz;
+      nbd = ptotal - np_el;
+      if (np_el && threadIdx.x == 0) atomicOr(&absb[e1 >> 5], 1u << (e1 & 31));
+      for (int32_t i = threadIdx.x; i < ptotal; i += blockDim.x) {
+        const int32_t w = i < np_adj ? L[po + i] : bd[i - np_adj];
+        out[i] = static_cast<uint16_t>(w);
+        if (w == p) s_ip = i;
+        else atomicOr(&inr[w >> 5], 1u << (w & 31));
       }
-      const int32_t at = warp_append(cnt, fresh);
-      if (fresh) out[at] = static_cast<uint16_t>(w);
-    }
-    for (int32_t ei = 0; ei < np_el; ++ei) {
-      const int32_t e = L[pe - 1 - ei];
-      const uint16_t* bd = cur + ebp[e];
-      const int32_t sz = static_cast<int32_t>(st[e]);
-      if (threadIdx.x == 0) atomicOr(&absb[e >> 5], 1u << (e & 31));
-      for (int32_t i0 = 0; i0 < sz; i0 += blockDim.x) {
+    } else {  // several elements: deduplicate (warp-aggregated appends)
+      for (int32_t i0 = 0; i0 < np_adj; i0 += blockDim.x) {
         const int32_t i = i0 + threadIdx.x;
         bool fresh = false;
         int32_t w = 0;
-        if (i < sz) {
-          w = bd[i];
+        if (i < np_adj) {
+          w = L[po + i];
           const uint32_t bit = 1u << (w & 31);
-          fresh = w != p && !(atomicOr(&inr[w >> 5], bit) & bit);
+          fresh = !(atomicOr(&inr[w >> 5], bit) & bit);
         }
         const int32_t at = warp_append(cnt, fresh);
         if (fresh) out[at] = static_cast<uint16_t>(w);
+      }
+      for (int32_t ei = 0; ei < np_el; ++ei) {
+        const int32_t e = L[pe - 1 - ei];
+        const uint16_t* bd = cur + ebp[e];
+        const int32_t sz = static_cast<int32_t>(st[e]);
+        if (threadIdx.x == 0) atomicOr(&absb[e >> 5], 1u << (e & 31));
+        for (int32_t i0 = 0; i0 < sz; i0 += blockDim.x) {
+          const int32_t i = i0 + threadIdx.x;
+          bool fresh = false;
+          int32_t w = 0;
+          if (i < sz) {
+            w = bd[i];
+            const uint32_t bit = 1u << (w & 31);
+            fresh = w != p && !(atomicOr(&inr[w >> 5], bit) & bit);
+          }
+          const int32_t at = warp_append(cnt, fresh);
+          if (fresh) out[at] = static_cast<uint16_t>(w);
+        }
       }
     }
     if (threadIdx.x == 0) {
@@ -555,12 +576,13 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
       mark_dirty(p >> 5);  // p was its block's minimum
     }
     __syncthreads();  // B2
-    const int32_t nbd = *cnt;
+    if (!simple) nbd = ptotal = *cnt;
     // ---- member updates (elimination.cpp:75-83), one member per thread; a
     // lowered key lowers its block's minimum at once, a raised block minimum
     // is recomputed below
-    for (int32_t i = threadIdx.x; i < nbd; i += blockDim.x) {
+    for (int32_t i = threadIdx.x; i < ptotal; i += blockDim.x) {
       const int32_t w = out[i];
+      if (w == p) continue;
       const uint32_t o = loff[w], oe = loff[w + 1];
       const uint32_t wst = st[w];
       const int32_t na = wst & 0xffff, ne = wst >> 16;
@@ -589,9 +611,9 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
       else if (nk > ok && ok == blk[b]) mark_dirty(b);
     }
     __syncthreads();  // B3
-    for (int32_t i = threadIdx.x; i < nbd; i += blockDim.x) {
+    for (int32_t i = threadIdx.x; i < ptotal; i += blockDim.x) {
       const int32_t w = out[i];
-      atomicAnd(&inr[w >> 5], ~(1u << (w & 31)));
+      if (w != p) atomicAnd(&inr[w >> 5], ~(1u << (w & 31)));
     }
     for (int32_t ei = threadIdx.x; ei < np_el; ei += blockDim.x) {
       const int32_t e = L[pe - 1 - ei];
@@ -609,6 +631,7 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
       }
     }
     if (threadIdx.x == 0) {
+      if (simple && np_el && s_ip != ptotal - 1) out[s_ip] = out[ptotal - 1];  // the boundary without p
       st[p] = static_cast<uint32_t>(nbd);
       s_cursor = cur0 + nbd;
       s_nbd[(k + 1) & 1] = 0;  // its last reader was the previous pivot, before this B2
@@ -729,7 +752,7 @@ void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t L, const int
       cudaFuncAttributes fa{};
       MP_CUDA(cudaFuncGetAttributes(&fa, md_smem_kernel));
       // dynamic shared memory: what the largest shared-memory node needs
-      // (state + lists from its degree sum + pool halves of 2 nv entries), so
+      // (state + lists from its degree sum + pool halves of 4 nv entries), so
       // small nodes (C4 frames) keep several CTAs per SM and leave room for
       // the other contexts' kernels
       const int64_t cap = static_cast<int64_t>(ctx.smem_optin) - static_cast<int64_t>(fa.sharedSizeBytes);
@@ -738,7 +761,7 @@ void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t L, const int
         const int32_t node = sched[i];
         const int64_t nv = hoff[node + 1] - hoff[node];
         const int64_t dsum = (hneed[node] / 2 - 64 - 2 * nv) / 4;
-        want = std::max(want, md_smem_fixed(static_cast<int32_t>(nv)) + 2 * dsum + 4 * std::max<int64_t>(kMdMinHalf, 2 * nv));
+        want = std::max(want, md_smem_fixed(static_cast<int32_t>(nv)) + 2 * dsum + 4 * std::max<int64_t>(kMdMinHalf, 4 * nv));
       }
       a.smem_bytes = std::min(cap, (want + 1023) & ~int64_t(1023));
       a.gsmem_bytes = a.smem_bytes;
