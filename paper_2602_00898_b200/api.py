@@ -131,7 +131,8 @@ class Context:
         check(lib().mp_context_set_stream(self.handle, C.c_void_p(stream_ptr or 0)))
 
     TUNING = {"fps_cluster": 0, "fps_qcap": 1, "fps_grid_radius": 2, "fps_grid_cands": 3,
-              "fps_sub_region": 4, "lloyd_blocks": 5}
+              "fps_sub_region": 4, "lloyd_blocks": 5,
+              "lloyd_cluster_n": 6, "fps_backoff_ns": 7}
 
     def set_tuning(self, key: str, value: int):
         """mp_context_set_tuning: force a fallback path or a sizing (results unchanged)."""

@@ -14,6 +14,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "mp_context.h"
@@ -489,8 +491,21 @@ __device__ __forceinline__ void warp_level(int64_t items, int32_t* gcount, int32
   }
 }
 
-__global__ void lloyd_kernel(LloydArgs a) {
-  cg::grid_group grid = cg::this_grid();
+// The rounds' barriers: the whole cooperative grid, or -- for small meshes,
+// whose BFS levels hold a few hundred vertices -- one thread-block cluster
+// that IS the grid (barrier.cluster ~ 400 cycles instead of a grid barrier's
+// several microseconds over 148 CTAs; C1's 300 barriers dominate Lloyd).
+struct GridBarrier {
+  cg::grid_group g = cg::this_grid();
+  __device__ void sync() { g.sync(); }
+};
+struct ClusterBarrier {
+  __device__ void sync() { cg::this_cluster().sync(); }
+};
+
+template <class Barrier>
+__global__ void __launch_bounds__(512) lloyd_kernel(LloydArgs a) {
+  Barrier grid;
   __shared__ int32_t s_lbuf[kLvlBuf], s_lsh[2];
   const int lane = threadIdx.x & 31;
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -640,6 +655,40 @@ __global__ void lloyd_kernel(LloydArgs a) {
     }
     grid.sync();
   }
+}
+
+// Meshes up to this many vertices run the Lloyd rounds on one cluster.
+constexpr int64_t kLloydClusterN = 12288;
+constexpr int kLloydClusterThreads = 512;
+
+// Cluster size for the one-cluster Lloyd: 16 CTAs where the device allows a
+// non-portable cluster, else 8; probed once per device.
+int lloyd_cluster_ctas(int device) {
+  static std::mutex mu;
+  static std::map<int, int> cached;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cached.find(device);
+  if (it != cached.end()) return it->second;
+  const bool nonportable = cudaFuncSetAttribute(lloyd_kernel<ClusterBarrier>,
+                                                cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+  cudaGetLastError();
+  int found = 0;
+  for (int cs : {16, 8}) {
+    if (cs > 8 && !nonportable) continue;
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(cs), cfg.blockDim = dim3(kLloydClusterThreads), cfg.attrs = at, cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, lloyd_kernel<ClusterBarrier>, &cfg) == cudaSuccess && ncl > 0) {
+      found = cs;
+      break;
+    }
+    cudaGetLastError();
+  }
+  cached[device] = found;
+  return found;
 }
 
 __global__ void lloyd_finish(int32_t n, const int32_t* comp_of, const int32_t* comp_mode,
@@ -1306,15 +1355,29 @@ int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, ui
     la.counters = counters;
     la.ell = ell;
     la.work = ctx.dwork;
+    void* args[] = {&la};
+    const int64_t cl_max = ctx.tune[MP_TUNE_LLOYD_CLUSTER_N] != 0 ? ctx.tune[MP_TUNE_LLOYD_CLUSTER_N] : kLloydClusterN;
+    const int cl = n <= cl_max ? lloyd_cluster_ctas(ctx.device) : 0;
+    if (cl > 0) {
+      cudaLaunchConfig_t cfg{};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cl, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(cl), cfg.blockDim = dim3(kLloydClusterThreads), cfg.dynamicSmemBytes = 0;
+      cfg.stream = s, cfg.attrs = at, cfg.numAttrs = 1;
+      const int kt__ = ctx.ktime_begin(kKLloyd);
+      MP_KERNEL(ctx, MP_CUDA(cudaLaunchKernelEx(&cfg, lloyd_kernel<ClusterBarrier>, la)));
+      ctx.ktime_end(kt__);
+    } else {
     int bpsm = 0;
-    MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, lloyd_kernel, 256, 0));
+    MP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, lloyd_kernel<GridBarrier>, 256, 0));
     int blocks = std::max(1, std::min(bpsm, 4)) * std::max(ctx.num_sms / std::max(ctx.sm_share, 1), 1);
     // small meshes: one CTA per SM is enough and makes the grid barriers cheaper
     blocks = static_cast<int>(std::min<int64_t>(blocks, std::max<int64_t>(ctx.num_sms / std::max(ctx.sm_share, 1), ceil_div(n, 512))));
     if (ctx.tune[MP_TUNE_LLOYD_BLOCKS] > 0)
       blocks = std::max(1, std::min<int>(blocks, static_cast<int>(ctx.tune[MP_TUNE_LLOYD_BLOCKS])));
-    void* args[] = {&la};
-    { const int kt__ = ctx.ktime_begin(kKLloyd); MP_KERNEL(ctx, MP_CUDA(cudaLaunchCooperativeKernel((void*)lloyd_kernel, blocks, 256, args, 0, s))); ctx.ktime_end(kt__); }
+    { const int kt__ = ctx.ktime_begin(kKLloyd); MP_KERNEL(ctx, MP_CUDA(cudaLaunchCooperativeKernel((void*)lloyd_kernel<GridBarrier>, blocks, 256, args, 0, s))); ctx.ktime_end(kt__); }
+    }
     MP_KERNEL(ctx, lloyd_finish<<<grid_for(ctx, n), 256, 0, s>>>(n, comp_of.get(), comp_mode, prev, assignment));
   }
   st.mark("lloyd");

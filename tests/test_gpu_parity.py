@@ -506,12 +506,14 @@ def test_sm_share_does_not_change_results(share):
     assert res.fill.nnz_L == gold["nnz_L"]
 
 
-@pytest.mark.parametrize("tune", [{"fps_qcap": 64}, {"fps_cluster": -1}, {"fps_cluster": 8}, {"lloyd_blocks": 3}])
+@pytest.mark.parametrize("tune", [{"fps_qcap": 64}, {"fps_cluster": -1}, {"fps_cluster": 8}, {"lloyd_blocks": 3},
+                                  {"lloyd_cluster_n": 1 << 20}])
 def test_fps_fallbacks_match_reference(tune):
     """The cluster phase's queue overflow (forced with a 64-slot queue) hands
     FPS to the batched kernel from scratch; without the cluster phase the
     batched kernel's grid mode runs the large radii; an 8-CTA cluster is the
-    portable fallback.  All must reproduce the reference (ico158 digests)."""
+    portable fallback; the one-cluster Lloyd (small meshes) is forced on a
+    250K-vertex mesh.  All must reproduce the reference (ico158 digests)."""
     ctx = mp.Context(0)
     for k, v in tune.items():
         ctx.set_tuning(k, v)

@@ -10,7 +10,10 @@ import paper_2602_00898_b200 as mp  # noqa: E402
 f = int(sys.argv[1]) if len(sys.argv) > 1 else 316
 g = mp.mesh_to_graph(mp.make_icosphere_mesh(f))
 base = None
-for tune in [{}, {"fps_cluster": 8}, {"fps_grid_radius": 100}, {"fps_grid_radius": 400}]:
+import json
+tunes = json.loads(sys.argv[2]) if len(sys.argv) > 2 else [{}, {"fps_cluster": 8}, {"fps_grid_radius": 100},
+                                                         {"fps_grid_radius": 400}]
+for tune in tunes:
     ctx = mp.Context(0)
     for k, v in tune.items():
         ctx.set_tuning(k, v)
@@ -20,5 +23,6 @@ for tune in [{}, {"fps_cluster": 8}, {"fps_grid_radius": 100}, {"fps_grid_radius
         ts.append(r.kernel_ms["fps"])
     same = base is None or np.array_equal(base, r.perm.perm)
     base = r.perm.perm if base is None else base
-    print(tune, "same" if same else "DIFF", [round(t, 2) for t in ts], round(r.stage_ms["patch"], 2))
+    print(tune, "same" if same else "DIFF", [round(t, 2) for t in ts], round(r.stage_ms["patch"], 2),
+          [int(x) for x in r.work[8:13]], flush=True)
     ctx.close()
