@@ -132,7 +132,7 @@ class Context:
 
     TUNING = {"fps_cluster": 0, "fps_qcap": 1, "fps_grid_radius": 2, "fps_grid_cands": 3,
               "fps_sub_region": 4, "lloyd_blocks": 5,
-              "lloyd_cluster_n": 6, "fps_backoff_ns": 7}
+              "lloyd_cluster_n": 6}
 
     def set_tuning(self, key: str, value: int):
         """mp_context_set_tuning: force a fallback path or a sizing (results unchanged)."""
@@ -591,7 +591,9 @@ def order(g: AdjacencyGraph, patch_size: int = 256, nd_level: int = -1, seed: in
         cfg.user_patch_count = int(user_patches.patch_count)
     bufs, res = _prepare(g, nd_level, block_size, want_fill)
     check(lib().mp_order(ctx.handle, C.byref(_csr(g)), C.byref(cfg), C.byref(res)))
-    return _finish(g, bufs, res, patch_size, block_size, want_fill)
+    r = _finish(g, bufs, res, patch_size, block_size, want_fill)
+    r.work = [int(res.work[i]) for i in range(16)]
+    return r
 
 
 def order_batch(graphs, contexts, patch_size: int = 256, nd_level: int = -1, seed: int = 0,

@@ -79,7 +79,6 @@ struct BatchArgs {
   int32_t grid_radius;     // candidates farther than this use the grid-mode regions
   int32_t grid_cands;      // candidates per grid-mode batch
   int32_t sub_region;      // largest region (last batch) that still runs kMaxSub groups per CTA
-  int32_t backoff_ns;      // cluster phase: longest idle-poll back-off
   int32_t resume;          // 1: fps_cluster_phase ran the large-radius seeds; continue from its state
   int32_t* queue;          // cluster phase work queue (qcap slots, -1 = empty)
   int32_t* qctl;           // [0] head [1] tail [2] pending
@@ -784,7 +783,7 @@ __global__ void __launch_bounds__(kThreads) fps_batched_kernel(BatchArgs a) {
 // R(c) = {v : d(c, v) < dist(v)}, patching.cpp:35-49).  Levels are separated by
 // the hardware cluster barrier instead of a grid-wide one.  At the end the
 // cluster's CTA 0 selects the first candidate batch for fps_batched_kernel.
-constexpr int32_t kBackoffNs = 2048;
+constexpr int32_t kBackoffNs = 2048;  // longest idle-poll back-off (64 ns steps)
 __device__ __forceinline__ void cluster_barrier() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -869,7 +868,7 @@ __global__ void __launch_bounds__(kThreads, 1) fps_cluster_phase(BatchArgs a, in
           if (lane == 0) atomicExch(&a.ctl[12], 1), atomicExch(&qc[kQPend], 0);
           break;
         }
-        if (idle > 2) __nanosleep(min(64 * idle, a.backoff_ns));  // back off: idle polls must not starve the atomics
+        if (idle > 2) __nanosleep(min(64 * idle, kBackoffNs));  // back off: idle polls must not starve the atomics
         continue;
       }
       idle = 0;
@@ -1081,7 +1080,6 @@ void fps_batched_dev(mp_context& ctx, const DGraph& g, const int32_t* ell, int32
   a.bar = reinterpret_cast<unsigned int*>(bar.get());
   a.grid_radius = grid_radius;
   a.grid_cands = grid_cands;
-  a.backoff_ns = ctx.tune[MP_TUNE_FPS_BACKOFF_NS] > 0 ? static_cast<int32_t>(ctx.tune[MP_TUNE_FPS_BACKOFF_NS]) : kBackoffNs;
   a.sub_region = ctx.tune[MP_TUNE_FPS_SUB_REGION] > 0 ? static_cast<int32_t>(ctx.tune[MP_TUNE_FPS_SUB_REGION]) : kSubRegion;
   const int kt = ctx.ktime_begin(kKFps);
   // large-radius seeds on one cluster (16 CTAs where the device allows, else 8)

@@ -771,9 +771,11 @@ struct RepairArgs {
   int32_t* fb;         // n
   int32_t* remap;      // cap_p
   int32_t* out;        // [0] patch count, [1] error
+  int32_t smem_words;  // dynamic shared memory of the split's local graph (32-bit words)
 };
 
 __global__ void __launch_bounds__(1024) repair_kernel(RepairArgs a) {
+  extern __shared__ uint32_t rsm[];
   __shared__ uint64_t red[32];
   __shared__ int32_t shi[32];
   __shared__ int32_t s_P, s_nseg, s_cnt, s_err;
@@ -915,93 +917,201 @@ __global__ void __launch_bounds__(1024) repair_kernel(RepairArgs a) {
     for_members(sp, [&](int32_t v) { pool[gbase + atomicAdd(&s_cnt, 1)] = v; });
     __syncthreads();
     const int32_t* mem = pool + gbase;
-    // farthest-vertex sweeps (patching.cpp:165-185, 231-233)
-    uint64_t mn = ~0ull;
-    for (int32_t i = threadIdx.x; i < spsize; i += blockDim.x)
-      mn = min(mn, static_cast<uint64_t>(mem[i]));
-    mn = block_min_u64(mn, red);
-    int32_t ends[3];
-    ends[0] = static_cast<int32_t>(mn);
-    for (int sweep = 1; sweep <= 2; ++sweep) {
-      for (int32_t i = threadIdx.x; i < spsize; i += blockDim.x) a.dist[mem[i]] = kUnreached;
+    // The split's three BFS runs (two farthest-vertex sweeps, the two-source
+    // competition) on the patch's induced subgraph staged in shared memory
+    // (local ids; dist and label packed in one word so the competition is one
+    // atomicMin): each level is shared-memory work between two barriers
+    // instead of a chain of L2 round trips.  Patches whose subgraph does not
+    // fit take the global-memory BFS below.
+    bool local = false;
+    if (a.smem_words > 0) {
+      for (int32_t i = threadIdx.x; i < spsize; i += blockDim.x) a.dist[mem[i]] = i;  // global -> local id
       __syncthreads();
-      const int32_t from = ends[sweep - 1];
+      int64_t dsum = 0;
+      for (int32_t i = threadIdx.x; i < spsize; i += blockDim.x) {
+        const int32_t u = mem[i];
+        for (int32_t j = a.g.off[u]; j < a.g.off[u + 1]; ++j) dsum += a.assignment[a.g.nbr[j]] == sp;
+      }
+      dsum = block_sum_i64(dsum, reinterpret_cast<int64_t*>(red));
+      // sd, lm, off (spsize + 1), two u16 frontiers, u16 adjacency
+      local = spsize < 65536 && 3LL * spsize + 1 + spsize + (dsum + 1) / 2 <= a.smem_words;
+    }
+    if (local) {
+      uint32_t* sd = rsm;                      // spsize: dist << 1 | label, ~0 unreached
+      int32_t* lm = reinterpret_cast<int32_t*>(sd + spsize);  // local -> global id
+      int32_t* lo = lm + spsize;               // spsize + 1 adjacency offsets
+      uint16_t* fr0 = reinterpret_cast<uint16_t*>(lo + spsize + 1);
+      uint16_t* fr1 = fr0 + spsize;
+      uint16_t* la = fr1 + spsize;             // local adjacency
+      int32_t run = 0;
+      for (int32_t i0 = 0; i0 < spsize; i0 += blockDim.x) {
+        const int32_t i = i0 + threadIdx.x;
+        int32_t c = 0;
+        if (i < spsize) {
+          const int32_t u = mem[i];
+          lm[i] = u;
+          for (int32_t j = a.g.off[u]; j < a.g.off[u + 1]; ++j) c += a.assignment[a.g.nbr[j]] == sp;
+        }
+        int32_t tot;
+        const int32_t e = block_excl_scan(c, shi, &tot);
+        if (i < spsize) lo[i] = run + e;
+        run += tot;
+      }
+      if (threadIdx.x == 0) lo[spsize] = run;
+      __syncthreads();
+      for (int32_t i = threadIdx.x; i < spsize; i += blockDim.x) {
+        const int32_t u = lm[i];
+        int32_t o = lo[i];
+        for (int32_t j = a.g.off[u]; j < a.g.off[u + 1]; ++j) {
+          const int32_t w = a.g.nbr[j];
+          if (a.assignment[w] == sp) la[o++] = static_cast<uint16_t>(__ldcg(&a.dist[w]));
+        }
+      }
+      __syncthreads();
+      // level-synchronous BFS from the given local sources; packed values
+      // (d << 1 | label) with atomicMin keep the smallest label among a
+      // vertex's same-level predecessors (patching.cpp:246-252); returns the
+      // farthest vertex (dist desc, global id asc) (patching.cpp:165-185)
+      auto bfs = [&](int32_t ns, const int32_t* src, const uint32_t* lab) -> int32_t {
+        for (int32_t i = threadIdx.x; i < spsize; i += blockDim.x) sd[i] = ~0u;
+        __syncthreads();
+        uint64_t far = 0;
+        if (threadIdx.x == 0) {
+          for (int32_t q = 0; q < ns; ++q) sd[src[q]] = lab[q], fr0[q] = static_cast<uint16_t>(src[q]);
+          s_cnt = 0;
+        }
+        if (threadIdx.x == 0) far = key_max(0u, static_cast<uint32_t>(lm[src[0]]));
+        __syncthreads();
+        int32_t nf = ns;
+        uint16_t *front = fr0, *next = fr1;
+        for (uint32_t d = 1; nf > 0; ++d) {
+          for (int32_t i = threadIdx.x; i < nf; i += blockDim.x) {
+            const int32_t u = front[i];
+            const uint32_t lu = sd[u] & 1u;
+            for (int32_t j = lo[u]; j < lo[u + 1]; ++j) {
+              const int32_t w = la[j];
+              if (sd[w] <= (d << 1)) continue;  // settled at an earlier level (or this one with label 0)
+              if (atomicMin(&sd[w], (d << 1) | lu) == ~0u) {
+                next[atomicAdd(&s_cnt, 1)] = static_cast<uint16_t>(w);
+                far = max(far, key_max(d, static_cast<uint32_t>(lm[w])));
+              }
+            }
+          }
+          __syncthreads();
+          nf = s_cnt;
+          __syncthreads();
+          if (threadIdx.x == 0) s_cnt = 0;
+          uint16_t* t = front;
+          front = next;
+          next = t;
+        }
+        __syncthreads();
+        far = block_max_u64(far, red);
+        return static_cast<int32_t>(key_max_id(far));
+      };
+      uint64_t mn = ~0ull;
+      for (int32_t i = threadIdx.x; i < spsize; i += blockDim.x) mn = min(mn, static_cast<uint64_t>(lm[i]));
+      mn = block_min_u64(mn, red);
+      const uint32_t zero[2] = {0u, 1u};
+      int32_t src[2];
+      src[0] = __ldcg(&a.dist[static_cast<int32_t>(mn)]);
+      const int32_t b_g = bfs(1, src, zero);
+      src[0] = __ldcg(&a.dist[b_g]);
+      const int32_t c_g = bfs(1, src, zero);
+      src[0] = __ldcg(&a.dist[b_g]), src[1] = __ldcg(&a.dist[c_g]);
+      bfs(2, src, zero);  // labels 0 (b) and 1 (c)
+      for (int32_t i = threadIdx.x; i < spsize; i += blockDim.x)
+        a.lab[lm[i]] = (sd[i] != ~0u && (sd[i] & 1u)) ? 1 : 0;
+      __syncthreads();
+    } else {
+      // farthest-vertex sweeps (patching.cpp:165-185, 231-233)
+      uint64_t mn = ~0ull;
+      for (int32_t i = threadIdx.x; i < spsize; i += blockDim.x)
+        mn = min(mn, static_cast<uint64_t>(mem[i]));
+      mn = block_min_u64(mn, red);
+      int32_t ends[3];
+      ends[0] = static_cast<int32_t>(mn);
+      for (int sweep = 1; sweep <= 2; ++sweep) {
+        for (int32_t i = threadIdx.x; i < spsize; i += blockDim.x) a.dist[mem[i]] = kUnreached;
+        __syncthreads();
+        const int32_t from = ends[sweep - 1];
+        if (threadIdx.x == 0) {
+          a.dist[from] = 0;
+          a.fa[0] = from;
+          s_cnt = 0;
+        }
+        __syncthreads();
+        int32_t nf = 1, d = 0;
+        int32_t *front = a.fa, *next = a.fb;
+        uint64_t far = key_max(0u, static_cast<uint32_t>(from));
+        while (nf > 0) {
+          for (int32_t i = threadIdx.x; i < nf; i += blockDim.x) {
+            const int32_t u = front[i];
+            for (int32_t j = a.g.off[u]; j < a.g.off[u + 1]; ++j) {
+              const int32_t w = a.g.nbr[j];
+              if (a.assignment[w] != sp) continue;
+              if (atomicCAS(&a.dist[w], kUnreached, d + 1) == kUnreached) {
+                next[atomicAdd(&s_cnt, 1)] = w;
+                uint64_t kk = key_max(static_cast<uint32_t>(d + 1), static_cast<uint32_t>(w));
+                far = kk > far ? kk : far;
+              }
+            }
+          }
+          __syncthreads();
+          nf = s_cnt;
+          __syncthreads();
+          if (threadIdx.x == 0) s_cnt = 0;
+          int32_t* t = front;
+          front = next;
+          next = t;
+          ++d;
+          __syncthreads();
+        }
+        far = block_max_u64(far, red);
+        ends[sweep] = static_cast<int32_t>(key_max_id(far));
+      }
+      // two-source competition, ties to b's half (patching.cpp:234-261)
+      const int32_t b = ends[1], cc = ends[2];
+      for (int32_t i = threadIdx.x; i < spsize; i += blockDim.x) {
+        a.dist[mem[i]] = kUnreached;
+        a.lab[mem[i]] = 0x7fffffff;
+      }
+      __syncthreads();
       if (threadIdx.x == 0) {
-        a.dist[from] = 0;
-        a.fa[0] = from;
+        a.dist[b] = 0, a.lab[b] = 0;
+        a.dist[cc] = 0, a.lab[cc] = 1;
+        a.fa[0] = b, a.fa[1] = cc;
         s_cnt = 0;
       }
       __syncthreads();
-      int32_t nf = 1, d = 0;
-      int32_t *front = a.fa, *next = a.fb;
-      uint64_t far = key_max(0u, static_cast<uint32_t>(from));
-      while (nf > 0) {
-        for (int32_t i = threadIdx.x; i < nf; i += blockDim.x) {
-          const int32_t u = front[i];
-          for (int32_t j = a.g.off[u]; j < a.g.off[u + 1]; ++j) {
-            const int32_t w = a.g.nbr[j];
-            if (a.assignment[w] != sp) continue;
-            if (atomicCAS(&a.dist[w], kUnreached, d + 1) == kUnreached) {
-              next[atomicAdd(&s_cnt, 1)] = w;
-              uint64_t kk = key_max(static_cast<uint32_t>(d + 1), static_cast<uint32_t>(w));
-              far = kk > far ? kk : far;
+      {
+        int32_t nf = 2, d = 0;
+        int32_t *front = a.fa, *next = a.fb;
+        while (nf > 0) {
+          for (int32_t i = threadIdx.x; i < nf; i += blockDim.x) {
+            const int32_t u = front[i];
+            const int32_t lu = a.lab[u];
+            for (int32_t j = a.g.off[u]; j < a.g.off[u + 1]; ++j) {
+              const int32_t w = a.g.nbr[j];
+              if (a.assignment[w] != sp) continue;
+              int32_t dw = atomicCAS(&a.dist[w], kUnreached, d + 1);
+              if (dw == kUnreached) {
+                next[atomicAdd(&s_cnt, 1)] = w;
+                dw = d + 1;
+              }
+              if (dw == d + 1) atomicMin(&a.lab[w], lu);
             }
           }
+          __syncthreads();
+          nf = s_cnt;
+          __syncthreads();
+          if (threadIdx.x == 0) s_cnt = 0;
+          int32_t* t = front;
+          front = next;
+          next = t;
+          ++d;
+          __syncthreads();
         }
-        __syncthreads();
-        nf = s_cnt;
-        __syncthreads();
-        if (threadIdx.x == 0) s_cnt = 0;
-        int32_t* t = front;
-        front = next;
-        next = t;
-        ++d;
-        __syncthreads();
-      }
-      far = block_max_u64(far, red);
-      ends[sweep] = static_cast<int32_t>(key_max_id(far));
-    }
-    // two-source competition, ties to b's half (patching.cpp:234-261)
-    const int32_t b = ends[1], cc = ends[2];
-    for (int32_t i = threadIdx.x; i < spsize; i += blockDim.x) {
-      a.dist[mem[i]] = kUnreached;
-      a.lab[mem[i]] = 0x7fffffff;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      a.dist[b] = 0, a.lab[b] = 0;
-      a.dist[cc] = 0, a.lab[cc] = 1;
-      a.fa[0] = b, a.fa[1] = cc;
-      s_cnt = 0;
-    }
-    __syncthreads();
-    {
-      int32_t nf = 2, d = 0;
-      int32_t *front = a.fa, *next = a.fb;
-      while (nf > 0) {
-        for (int32_t i = threadIdx.x; i < nf; i += blockDim.x) {
-          const int32_t u = front[i];
-          const int32_t lu = a.lab[u];
-          for (int32_t j = a.g.off[u]; j < a.g.off[u + 1]; ++j) {
-            const int32_t w = a.g.nbr[j];
-            if (a.assignment[w] != sp) continue;
-            int32_t dw = atomicCAS(&a.dist[w], kUnreached, d + 1);
-            if (dw == kUnreached) {
-              next[atomicAdd(&s_cnt, 1)] = w;
-              dw = d + 1;
-            }
-            if (dw == d + 1) atomicMin(&a.lab[w], lu);
-          }
-        }
-        __syncthreads();
-        nf = s_cnt;
-        __syncthreads();
-        if (threadIdx.x == 0) s_cnt = 0;
-        int32_t* t = front;
-        front = next;
-        next = t;
-        ++d;
-        __syncthreads();
       }
     }
     // split members stably: keep (label != 1) then fresh (label == 1)
@@ -1113,6 +1223,8 @@ void bucket_by_patch(mp_context& ctx, int32_t n, const int32_t* assignment, int3
                                           list, n, 0, end_bit, s));
 }
 
+constexpr int kRepairSmemBytes = 96 * 1024;  // the split's local graph (patches up to ~3.5K vertices)
+
 int32_t repair_sizes_dev(mp_context& ctx, const DGraph& g, int32_t* assignment, int32_t P,
                          int32_t target) {
   cudaStream_t s = ctx.stream;
@@ -1138,7 +1250,9 @@ int32_t repair_sizes_dev(mp_context& ctx, const DGraph& g, int32_t* assignment, 
   a.size = size, a.exempt = exempt, a.head = head, a.tail = tail, a.seg_start = seg_start;
   a.seg_len = seg_len, a.seg_next = seg_next, a.pool = pool, a.pool2 = pool2, a.dist = dist, a.lab = lab;
   a.fa = fa, a.fb = fb, a.remap = remap, a.out = out;
-  MP_KERNEL(ctx, repair_kernel<<<1, 1024, 0, s>>>(a));
+  allow_max_smem(repair_kernel, ctx.device);
+  a.smem_words = kRepairSmemBytes / 4;
+  MP_KERNEL(ctx, repair_kernel<<<1, 1024, kRepairSmemBytes, s>>>(a));
   int32_t h_out[2];
   MP_CUDA(cudaMemcpyAsync(h_out, out, sizeof h_out, cudaMemcpyDeviceToHost, s));
   MP_CUDA(cudaStreamSynchronize(s));

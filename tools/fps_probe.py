@@ -24,5 +24,5 @@ for tune in tunes:
     same = base is None or np.array_equal(base, r.perm.perm)
     base = r.perm.perm if base is None else base
     print(tune, "same" if same else "DIFF", [round(t, 2) for t in ts], round(r.stage_ms["patch"], 2),
-          [int(x) for x in r.work[8:13]], flush=True)
+          [int(x) for x in r.work[4:16]], flush=True)
     ctx.close()
