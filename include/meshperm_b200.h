@@ -143,6 +143,7 @@ int mp_context_set_fill_algorithm(mp_context* ctx, int32_t algo);
  *   MP_TUNE_LLOYD_BLOCKS     CTAs of the Lloyd kernel
  *   MP_TUNE_LLOYD_CLUSTER_N  meshes up to this many vertices run Lloyd on one
  *                            thread-block cluster (default 12288; -1 never)
+ *   MP_TUNE_MD_THREADS       threads of the shared-memory minimum-degree CTAs
  * MP_EINVAL for an unknown key. */
 enum {
   MP_TUNE_FPS_CLUSTER = 0,
@@ -152,7 +153,8 @@ enum {
   MP_TUNE_FPS_SUB_REGION = 4,
   MP_TUNE_LLOYD_BLOCKS = 5,
   MP_TUNE_LLOYD_CLUSTER_N = 6,
-  MP_TUNE_COUNT = 7
+  MP_TUNE_MD_THREADS = 7,
+  MP_TUNE_COUNT = 8
 };
 int mp_context_set_tuning(mp_context* ctx, int32_t key, int64_t value);
 /* cudaStream_t to run on; NULL restores the context's own stream. */

@@ -132,7 +132,7 @@ class Context:
 
     TUNING = {"fps_cluster": 0, "fps_qcap": 1, "fps_grid_radius": 2, "fps_grid_cands": 3,
               "fps_sub_region": 4, "lloyd_blocks": 5,
-              "lloyd_cluster_n": 6}
+              "lloyd_cluster_n": 6, "md_threads": 7}
 
     def set_tuning(self, key: str, value: int):
         """mp_context_set_tuning: force a fallback path or a sizing (results unchanged)."""

@@ -765,7 +765,10 @@ void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t L, const int
       }
       a.smem_bytes = std::min(cap, (want + 1023) & ~int64_t(1023));
       a.gsmem_bytes = a.smem_bytes;
-      MP_KERNEL(ctx, md_smem_kernel<<<ns - big, kMdSmemThreads, static_cast<size_t>(a.smem_bytes), s>>>(a));
+      const int threads = ctx.tune[MP_TUNE_MD_THREADS] > 0
+                              ? static_cast<int>(std::min<int64_t>(kMdSmemThreads, ctx.tune[MP_TUNE_MD_THREADS]) & ~31)
+                              : kMdSmemThreads;
+      MP_KERNEL(ctx, md_smem_kernel<<<ns - big, std::max(threads, 32), static_cast<size_t>(a.smem_bytes), s>>>(a));
     }
     if (big > 0) MP_CUDA(cudaStreamWaitEvent(s, ctx.fork_ev[1], 0));
   } else {

@@ -15,7 +15,10 @@ meshes = {
     "ico50": mp.make_icosphere_mesh(50),
     "ico100": mp.make_icosphere_mesh(100),
 }
-tunes = [{}, {"lloyd_cluster_n": -1}, {"lloyd_cluster_n": 1 << 20}]
+import json
+tunes = json.loads(sys.argv[1]) if len(sys.argv) > 1 else [{}, {"lloyd_cluster_n": -1}]
+if len(sys.argv) > 2:
+    meshes["ico316"] = mp.make_icosphere_mesh(316)
 for name, mesh in meshes.items():
     g = mp.mesh_to_graph(mesh)
     base = None
