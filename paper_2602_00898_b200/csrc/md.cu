@@ -456,6 +456,7 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
   for (int32_t k = 0; k < nv; ++k) {
     // pivot: min key over the block minima (every warp; blk is stable since B4)
     uint32_t best = kKeyInf;
+#pragma unroll 4
     for (int32_t b = lane; b < nb; b += 32) best = min(best, blk[b]);
     best = __reduce_min_sync(0xffffffffu, best);
     const int32_t p = static_cast<int32_t>(best & 0x1fffu);
@@ -569,11 +570,13 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
         }
       }
     }
-    if (threadIdx.x == 0) {
+    // the pivot's own bookkeeping on the last thread (thread 0 leads the
+    // reach copy); its block, whose minimum p was, is refreshed after the
+    // member updates by the last warp without going through the dirty list
+    if (threadIdx.x == blockDim.x - 1) {
       ebp[p] = static_cast<uint32_t>(cur0);
       lperm[k] = p;
       kd[p] = kKeyInf;
-      mark_dirty(p >> 5);  // p was its block's minimum
     }
     __syncthreads();  // B2
     if (!simple) nbd = ptotal = *cnt;
@@ -586,21 +589,38 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
       const uint32_t o = loff[w], oe = loff[w + 1];
       const uint32_t wst = st[w];
       const int32_t na = wst & 0xffff, ne = wst >> 16;
+      // both lists in chunks of four: the chunk's slots, then their bit-set
+      // words and sizes, are independent loads in flight together (a chunk's
+      // compacting writes land at or below its reads)
       int32_t c = 0;
-      for (int32_t j = 0; j < na; j += 2) {  // two reads ahead of the writes
-        const int32_t x0 = L[o + j], x1 = j + 1 < na ? L[o + j + 1] : p;
-        const uint32_t i0 = inr[x0 >> 5], i1 = inr[x1 >> 5];
-        if (x0 != p && !((i0 >> (x0 & 31)) & 1u)) L[o + c++] = static_cast<uint16_t>(x0);
-        if (x1 != p && !((i1 >> (x1 & 31)) & 1u)) L[o + c++] = static_cast<uint16_t>(x1);
+      for (int32_t j0 = 0; j0 < na; j0 += 4) {
+        int32_t x[4];
+        uint32_t iw[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x[q] = j0 + q < na ? L[o + j0 + q] : p;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) iw[q] = inr[x[q] >> 5];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (x[q] != p && !((iw[q] >> (x[q] & 31)) & 1u)) L[o + c++] = static_cast<uint16_t>(x[q]);
       }
       int32_t ce = 0;
       uint32_t d = static_cast<uint32_t>(c + nbd);
-      for (int32_t j = 0; j < ne; ++j) {
-        const int32_t e = L[oe - 1 - j];
-        if (!((absb[e >> 5] >> (e & 31)) & 1u)) {
-          L[oe - 1 - ce++] = static_cast<uint16_t>(e);
-          d += st[e];
-        }
+      for (int32_t j0 = 0; j0 < ne; j0 += 4) {
+        int32_t e[4];
+        uint32_t ab[4], sz[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) e[q] = j0 + q < ne ? L[oe - 1 - (j0 + q)] : -1;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ab[q] = e[q] >= 0 ? absb[e[q] >> 5] : ~0u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sz[q] = e[q] >= 0 ? st[e[q]] : 0u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (e[q] >= 0 && !((ab[q] >> (e[q] & 31)) & 1u)) {
+            L[oe - 1 - ce++] = static_cast<uint16_t>(e[q]);
+            d += sz[q];
+          }
       }
       L[oe - 1 - ce++] = static_cast<uint16_t>(p);
       st[w] = static_cast<uint32_t>(c) | (static_cast<uint32_t>(ce) << 16);
@@ -630,6 +650,11 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
         atomicAnd(&dbits[b >> 5], ~(1u << (b & 31)));
       }
     }
+    if (wid == nwarp - 1) {  // the pivot's block (a second refresh of it via the list is identical)
+      const int32_t v = (p & ~31) + lane;
+      const uint32_t m = __reduce_min_sync(0xffffffffu, v < nv ? kd[v] : kKeyInf);
+      if (lane == 0) blk[p >> 5] = m;
+    }
     if (threadIdx.x == 0) {
       if (simple && np_el && s_ip != ptotal - 1) out[s_ip] = out[ptotal - 1];  // the boundary without p
       st[p] = static_cast<uint32_t>(nbd);
@@ -639,6 +664,7 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
     __syncthreads();  // B4
     if (threadIdx.x == 0) s_ndirty = 0;
   }
+
 }
 
 __global__ void local_of_kernel(int32_t n, const int32_t* node_of, const int32_t* node_offsets,
