@@ -361,7 +361,7 @@ constexpr int kMdSmemThreads = 128;  // four warps: cheap barriers, one member p
 
 __host__ __device__ inline int64_t md_smem_fixed(int32_t nv) {
   const int64_t nb = (nv + 31) / 32;
-  return 4 * nb + 4 * (4LL * nv + 1) + 4 * (2 * nb + (nb + 31) / 32 + 1) + 16;
+  return 4 * nb + 4 * (4LL * nv + 1) + 4 * (2 * nb + (nb + 31) / 32 + 1) + 2 * ((nv + 1) & ~1) + 16;
 }
 
 __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
@@ -380,7 +380,8 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
   uint32_t* inr = loff + nv + 1;
   uint32_t* absb = inr + nb;
   uint32_t* dbits = absb + nb;  // dirty blocks (nb bits)
-  uint16_t* L = reinterpret_cast<uint16_t*>(dbits + (nb + 31) / 32 + 1);
+  uint16_t* mk = reinterpret_cast<uint16_t*>(dbits + (nb + 31) / 32 + 1);  // reach stamp: k + 1 = in pivot k's reach
+  uint16_t* L = mk + ((nv + 1) & ~1);
   __shared__ int32_t s_cursor, s_cap, s_inglobal, s_maxdeg, s_nbd[2], s_ndirty, s_ip, sh[32];
   __shared__ int32_t s_dlist[kMdSmemMaxNv / 32];
   __shared__ int64_t s_red64[32];
@@ -424,6 +425,7 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
     s_other = L + D + half;
   }
   for (int32_t b = threadIdx.x; b < nb; b += blockDim.x) inr[b] = 0, absb[b] = 0;
+  for (int32_t i = threadIdx.x; i < nv; i += blockDim.x) mk[i] = 0;
   for (int32_t b = threadIdx.x; b <= (nb + 31) / 32; b += blockDim.x) dbits[b] = 0;
   if (threadIdx.x == 0) s_nbd[0] = s_nbd[1] = 0, s_ndirty = 0;
   // induced subgraph in local ids
@@ -454,6 +456,7 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
     if (!(atomicOr(&dbits[b >> 5], bit) & bit)) s_dlist[atomicAdd(&s_ndirty, 1)] = b;
   };
   for (int32_t k = 0; k < nv; ++k) {
+    const uint16_t stamp = static_cast<uint16_t>(k + 1);  // nv <= kMdSmemMaxNv < 65536
     // pivot: min key over the block minima (every warp; blk is stable since B4)
     uint32_t best = kKeyInf;
 #pragma unroll 4
@@ -536,7 +539,7 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
         const int32_t w = i < np_adj ? L[po + i] : bd[i - np_adj];
         out[i] = static_cast<uint16_t>(w);
         if (w == p) s_ip = i;
-        else atomicOr(&inr[w >> 5], 1u << (w & 31));
+        else mk[w] = stamp;
       }
     } else {  // several elements: deduplicate (warp-aggregated appends)
       for (int32_t i0 = 0; i0 < np_adj; i0 += blockDim.x) {
@@ -549,7 +552,7 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
           fresh = !(atomicOr(&inr[w >> 5], bit) & bit);
         }
         const int32_t at = warp_append(cnt, fresh);
-        if (fresh) out[at] = static_cast<uint16_t>(w);
+        if (fresh) out[at] = static_cast<uint16_t>(w), mk[w] = stamp;
       }
       for (int32_t ei = 0; ei < np_el; ++ei) {
         const int32_t e = L[pe - 1 - ei];
@@ -566,7 +569,7 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
             fresh = w != p && !(atomicOr(&inr[w >> 5], bit) & bit);
           }
           const int32_t at = warp_append(cnt, fresh);
-          if (fresh) out[at] = static_cast<uint16_t>(w);
+          if (fresh) out[at] = static_cast<uint16_t>(w), mk[w] = stamp;
         }
       }
     }
@@ -595,14 +598,14 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
       int32_t c = 0;
       for (int32_t j0 = 0; j0 < na; j0 += 4) {
         int32_t x[4];
-        uint32_t iw[4];
+        uint16_t iw[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) x[q] = j0 + q < na ? L[o + j0 + q] : p;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) iw[q] = inr[x[q] >> 5];
+        for (int q = 0; q < 4; ++q) iw[q] = mk[x[q]];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          if (x[q] != p && !((iw[q] >> (x[q] & 31)) & 1u)) L[o + c++] = static_cast<uint16_t>(x[q]);
+          if (x[q] != p && iw[q] != stamp) L[o + c++] = static_cast<uint16_t>(x[q]);
       }
       int32_t ce = 0;
       uint32_t d = static_cast<uint32_t>(c + nbd);
@@ -631,10 +634,11 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
       else if (nk > ok && ok == blk[b]) mark_dirty(b);
     }
     __syncthreads();  // B3
-    for (int32_t i = threadIdx.x; i < ptotal; i += blockDim.x) {
-      const int32_t w = out[i];
-      if (w != p) atomicAnd(&inr[w >> 5], ~(1u << (w & 31)));
-    }
+    if (!simple)  // the deduplication bits (simple reaches only stamp)
+      for (int32_t i = threadIdx.x; i < ptotal; i += blockDim.x) {
+        const int32_t w = out[i];
+        if (w != p) atomicAnd(&inr[w >> 5], ~(1u << (w & 31)));
+      }
     for (int32_t ei = threadIdx.x; ei < np_el; ei += blockDim.x) {
       const int32_t e = L[pe - 1 - ei];
       atomicAnd(&absb[e >> 5], ~(1u << (e & 31)));
