@@ -361,7 +361,7 @@ constexpr int kMdSmemThreads = 128;  // four warps: cheap barriers, one member p
 
 __host__ __device__ inline int64_t md_smem_fixed(int32_t nv) {
   const int64_t nb = (nv + 31) / 32;
-  return 4 * nb + 4 * (4LL * nv + 1) + 4 * (2 * nb + (nb + 31) / 32 + 1) + 2 * ((nv + 1) & ~1) + 16;
+  return 4 * nb + 4 * (4LL * nv + 1) + 8 * nb + 4 * ((nv + 1) & ~1) + 16;
 }
 
 __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
@@ -378,10 +378,10 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
   uint32_t* ebp = st + nv;
   uint32_t* loff = ebp + nv;  // nv + 1
   uint32_t* inr = loff + nv + 1;
-  uint32_t* absb = inr + nb;
-  uint32_t* dbits = absb + nb;  // dirty blocks (nb bits)
-  uint16_t* mk = reinterpret_cast<uint16_t*>(dbits + (nb + 31) / 32 + 1);  // reach stamp: k + 1 = in pivot k's reach
-  uint16_t* L = mk + ((nv + 1) & ~1);
+  uint32_t* dst = inr + nb;  // dirty-block stamp: k + 1 = listed for refresh after pivot k
+  uint16_t* mk = reinterpret_cast<uint16_t*>(dst + nb);  // reach stamp: k + 1 = in pivot k's reach
+  uint16_t* ea = mk + ((nv + 1) & ~1);                   // absorbed stamp: k + 1 = absorbed by pivot k
+  uint16_t* L = ea + ((nv + 1) & ~1);
   __shared__ int32_t s_cursor, s_cap, s_inglobal, s_maxdeg, s_nbd[2], s_ndirty, s_ip, sh[32];
   __shared__ int32_t s_dlist[kMdSmemMaxNv / 32];
   __shared__ int64_t s_red64[32];
@@ -424,9 +424,8 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
     s_cur = L + D;
     s_other = L + D + half;
   }
-  for (int32_t b = threadIdx.x; b < nb; b += blockDim.x) inr[b] = 0, absb[b] = 0;
-  for (int32_t i = threadIdx.x; i < nv; i += blockDim.x) mk[i] = 0;
-  for (int32_t b = threadIdx.x; b <= (nb + 31) / 32; b += blockDim.x) dbits[b] = 0;
+  for (int32_t b = threadIdx.x; b < nb; b += blockDim.x) inr[b] = 0, dst[b] = 0;
+  for (int32_t i = threadIdx.x; i < nv; i += blockDim.x) mk[i] = 0, ea[i] = 0;
   if (threadIdx.x == 0) s_nbd[0] = s_nbd[1] = 0, s_ndirty = 0;
   // induced subgraph in local ids
   for (int32_t k = threadIdx.x; k < nv; k += blockDim.x) {
@@ -451,9 +450,8 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
   // ---- the pivots
   const uint32_t below = (1u << lane) - 1;
   // a block whose minimum may have risen is recomputed after the member updates
-  auto mark_dirty = [&](int32_t b) {
-    const uint32_t bit = 1u << (b & 31);
-    if (!(atomicOr(&dbits[b >> 5], bit) & bit)) s_dlist[atomicAdd(&s_ndirty, 1)] = b;
+  auto mark_dirty = [&](int32_t b, uint32_t sp) {
+    if (atomicExch(&dst[b], sp) != sp) s_dlist[atomicAdd(&s_ndirty, 1)] = b;
   };
   for (int32_t k = 0; k < nv; ++k) {
     const uint16_t stamp = static_cast<uint16_t>(k + 1);  // nv <= kMdSmemMaxNv < 65536
@@ -534,7 +532,7 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
       const int32_t sz = np_el ? static_cast<int32_t>(st[e1]) : 0;
       ptotal = np_adj + sz;
       nbd = ptotal - np_el;
-      if (np_el && threadIdx.x == 0) atomicOr(&absb[e1 >> 5], 1u << (e1 & 31));
+      if (np_el && threadIdx.x == 0) ea[e1] = stamp;
       for (int32_t i = threadIdx.x; i < ptotal; i += blockDim.x) {
         const int32_t w = i < np_adj ? L[po + i] : bd[i - np_adj];
         out[i] = static_cast<uint16_t>(w);
@@ -558,7 +556,7 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
         const int32_t e = L[pe - 1 - ei];
         const uint16_t* bd = cur + ebp[e];
         const int32_t sz = static_cast<int32_t>(st[e]);
-        if (threadIdx.x == 0) atomicOr(&absb[e >> 5], 1u << (e & 31));
+        if (threadIdx.x == 0) ea[e] = stamp;
         for (int32_t i0 = 0; i0 < sz; i0 += blockDim.x) {
           const int32_t i = i0 + threadIdx.x;
           bool fresh = false;
@@ -611,16 +609,17 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
       uint32_t d = static_cast<uint32_t>(c + nbd);
       for (int32_t j0 = 0; j0 < ne; j0 += 4) {
         int32_t e[4];
-        uint32_t ab[4], sz[4];
+        uint16_t ab[4];
+        uint32_t sz[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) e[q] = j0 + q < ne ? L[oe - 1 - (j0 + q)] : -1;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) ab[q] = e[q] >= 0 ? absb[e[q] >> 5] : ~0u;
+        for (int q = 0; q < 4; ++q) ab[q] = e[q] >= 0 ? ea[e[q]] : stamp;
 #pragma unroll
         for (int q = 0; q < 4; ++q) sz[q] = e[q] >= 0 ? st[e[q]] : 0u;
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          if (e[q] >= 0 && !((ab[q] >> (e[q] & 31)) & 1u)) {
+          if (ab[q] != stamp) {
             L[oe - 1 - ce++] = static_cast<uint16_t>(e[q]);
             d += sz[q];
           }
@@ -631,7 +630,7 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
       kd[w] = nk;
       const int32_t b = w >> 5;
       if (nk < ok) atomicMin(&blk[b], nk);
-      else if (nk > ok && ok == blk[b]) mark_dirty(b);
+      else if (nk > ok && ok == blk[b]) mark_dirty(b, stamp);
     }
     __syncthreads();  // B3
     if (!simple)  // the deduplication bits (simple reaches only stamp)
@@ -641,7 +640,6 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
       }
     for (int32_t ei = threadIdx.x; ei < np_el; ei += blockDim.x) {
       const int32_t e = L[pe - 1 - ei];
-      atomicAnd(&absb[e >> 5], ~(1u << (e & 31)));
       st[e] = 0;  // absorbed
     }
     const int32_t ndirty = s_ndirty;
@@ -651,7 +649,6 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
       const uint32_t m = __reduce_min_sync(0xffffffffu, v < nv ? kd[v] : kKeyInf);
       if (lane == 0) {
         blk[b] = m;
-        atomicAnd(&dbits[b >> 5], ~(1u << (b & 31)));
       }
     }
     if (wid == nwarp - 1) {  // the pivot's block (a second refresh of it via the list is identical)
