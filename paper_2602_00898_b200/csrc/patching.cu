@@ -138,8 +138,11 @@ __global__ void scatter_pos(int32_t n, const int32_t* list, int32_t* pos_of) {
 __global__ void plan_components(int32_t C, const int32_t* comp_size, int32_t target,
                                 int32_t* comp_start, int32_t* comp_k, int32_t* comp_mode,
                                 int32_t* comp_base, int32_t* tile_base, int32_t* super_base,
-                                int32_t* totals /* [0]=patches [1]=tiles [2]=supers */) {
+                                int32_t* totals /* [0]=patches [1]=tiles [2]=supers [3]=largest FPS component */) {
   __shared__ int32_t sh[32];
+  __shared__ int32_t s_max;
+  if (threadIdx.x == 0) s_max = 0;
+  __syncthreads();
   int32_t run_start = 0, run_base = 0, run_tile = 0, run_super = 0;
   for (int32_t c0 = 0; c0 < C; c0 += blockDim.x) {
     int32_t c = c0 + threadIdx.x;
@@ -156,6 +159,7 @@ __global__ void plan_components(int32_t C, const int32_t* comp_size, int32_t tar
         ns = static_cast<int32_t>(ceil_div(nt, kTile));
       }
     }
+    if (mode == kModeFps) atomicMax(&s_max, sz);
     int32_t tot;
     int32_t es = block_excl_scan(sz, sh, &tot);
     int32_t add_s = tot;
@@ -175,7 +179,8 @@ __global__ void plan_components(int32_t C, const int32_t* comp_size, int32_t tar
     }
     run_start += add_s, run_base += add_b, run_tile += add_t, run_super += add_u;
   }
-  if (threadIdx.x == 0) totals[0] = run_base, totals[1] = run_tile, totals[2] = run_super;
+  __syncthreads();
+  if (threadIdx.x == 0) totals[0] = run_base, totals[1] = run_tile, totals[2] = run_super, totals[3] = s_max;
 }
 
 // Assignments of singleton / one-patch components (patching.cpp:313-322).
@@ -223,6 +228,7 @@ struct FpsArgs {
   int32_t* seeds;        // by global patch id
   uint64_t seed;
   unsigned long long* work;  // [0] += adjacency scans of the relaxations (R_fps)
+  int32_t smem_n;            // components up to this size keep dist + ELL in shared memory
 };
 
 __device__ __forceinline__ int32_t vtx_at(const FpsArgs& a, int32_t pos) {
@@ -259,12 +265,34 @@ __global__ void __launch_bounds__(kFpsThreads) fps_kernel(FpsArgs a) {
   uint32_t* sbits = reinterpret_cast<uint32_t*>(fsm + 2 * kFrontCap);
   const int32_t nwords = (ntile + 31) / 32;
   uint32_t* tbits = nwords <= kSmemTileWords ? sbits : a.tile_bits + (a.tile_base[c] + 31) / 32 + c;
+  // Small components (a.smem_n): the distances and the adjacency (ELL rows in
+  // component-local 16-bit ids) live in shared memory, so a BFS level is
+  // shared-memory work between two barriers instead of L2 round trips;
+  // frontiers then hold local ids.  A vertex of degree > 8 keeps the
+  // component on the global path.
+  int32_t* sdist = fsm + 2 * kFrontCap + kSmemTileWords;
+  uint16_t* sell = reinterpret_cast<uint16_t*>(sdist + a.smem_n);
 
   __shared__ int32_t touched[kTouchCap];
   __shared__ int32_t n_touched, overflow, cnt[3], s_cur;
   __shared__ uint32_t super_bits[64];  // up to 2048 supertiles (524M vertices)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
 
+  bool sm = size <= a.smem_n;
+  if (sm) {
+    bool tail = false;
+    for (int32_t i = threadIdx.x; i < size; i += blockDim.x) {
+      const int32_t v = vtx_at(a, start + i);
+#pragma unroll
+      for (int k = 0; k < kEll; ++k) {
+        const int32_t x = a.ell[static_cast<int64_t>(v) * kEll + k];
+        tail |= x < -1;
+        sell[i * kEll + k] = x >= 0 ? static_cast<uint16_t>(pos_in(a, x) - start) : uint16_t(0xffff);
+      }
+      sdist[i] = kUnreached;
+    }
+    sm = !__syncthreads_or(tail);
+  }
   for (int32_t i = threadIdx.x; i < size; i += blockDim.x) a.dist[vtx_at(a, start + i)] = kUnreached;
   for (int32_t i = threadIdx.x; i < 64; i += blockDim.x) super_bits[i] = 0;
   for (int32_t i = threadIdx.x; i < nwords; i += blockDim.x) tbits[i] = 0;
@@ -274,6 +302,15 @@ __global__ void __launch_bounds__(kFpsThreads) fps_kernel(FpsArgs a) {
   }
   __syncthreads();
 
+  auto mark_tile_pos = [&](int32_t p) {  // p: position in the component
+    const int32_t t = p / kTile;
+    const uint32_t bit = 1u << (t & 31);
+    if (!(atomicOr(&tbits[t >> 5], bit) & bit)) {
+      const int32_t slot = atomicAdd(&n_touched, 1);
+      if (slot < kTouchCap) touched[slot] = t;
+      else overflow = 1;
+    }
+  };
   auto mark_tile = [&](int32_t v) {
     const int32_t t = (pos_in(a, v) - start) / kTile;
     const uint32_t bit = 1u << (t & 31);
@@ -288,7 +325,7 @@ __global__ void __launch_bounds__(kFpsThreads) fps_kernel(FpsArgs a) {
     const int32_t lo = t * kTile, hi = min(size, lo + kTile);
     for (int32_t p = lo + lane; p < hi; p += 32) {
       const int32_t v = vtx_at(a, start + p);
-      const int32_t dv = __ldcg(&a.dist[v]);
+      const int32_t dv = sm ? sdist[p] : __ldcg(&a.dist[v]);
       const uint64_t kk = key_max(static_cast<uint32_t>(dv), static_cast<uint32_t>(v));
       best = kk > best ? kk : best;
     }
@@ -309,12 +346,41 @@ __global__ void __launch_bounds__(kFpsThreads) fps_kernel(FpsArgs a) {
     const int32_t cur = s_cur;
     if (threadIdx.x == 0) {
       a.seeds[a.comp_base[c] + s] = cur;
-      a.dist[cur] = 0;
-      sfront0[0] = cur;
+      if (sm) {
+        const int32_t lc = pos_in(a, cur) - start;
+        sdist[lc] = 0;
+        sfront0[0] = lc;
+        mark_tile_pos(lc);
+      } else {
+        a.dist[cur] = 0;
+        sfront0[0] = cur;
+        mark_tile(cur);
+      }
       cnt[0] = 1, cnt[1] = 0, cnt[2] = 0;
-      mark_tile(cur);
     }
     __syncthreads();
+    if (sm) {  // relax_from (patching.cpp:35-49) on the shared-memory field
+      for (int32_t d = 0;; ++d) {
+        const int32_t nf = cnt[d % 3];
+        if (nf == 0) break;
+        if (threadIdx.x == 0) cnt[(d + 2) % 3] = 0;
+        const int32_t* sin = (d & 1) ? sfront1 : sfront0;
+        int32_t* sout = (d & 1) ? sfront0 : sfront1;
+        int32_t* cout = &cnt[(d + 1) % 3];
+        const int32_t items = nf * kEll;
+        for (int32_t it = threadIdx.x; it < items; it += blockDim.x) {
+          const int32_t u = sin[it >> 3];
+          const uint16_t x = sell[u * kEll + (it & (kEll - 1))];
+          if (x == 0xffff) continue;
+          ++scans;
+          if (d + 1 < sdist[x] && atomicMin(&sdist[x], d + 1) > d + 1) {
+            sout[atomicAdd(cout, 1)] = x;  // a vertex enters a frontier once: nf <= size <= kFrontCap
+            mark_tile_pos(x);
+          }
+        }
+        __syncthreads();
+      }
+    } else {
     // relax_from (patching.cpp:35-49)
     for (int32_t d = 0;; ++d) {
       const int32_t nf = cnt[d % 3];
@@ -353,6 +419,7 @@ __global__ void __launch_bounds__(kFpsThreads) fps_kernel(FpsArgs a) {
       }
       __syncthreads();
     }
+    }  // sm / global
     // refresh touched tiles, then touched supertiles, then the top
     if (overflow) {
       for (int32_t t = wid; t < ntile; t += nwarp) {
@@ -411,6 +478,8 @@ __global__ void __launch_bounds__(kFpsThreads) fps_kernel(FpsArgs a) {
     }
     __syncthreads();
   }
+  if (sm)
+    for (int32_t i = threadIdx.x; i < size; i += blockDim.x) a.dist[vtx_at(a, start + i)] = sdist[i];
   if (a.work && scans) atomicAdd(&a.work[0], scans);
 }
 
@@ -1379,7 +1448,7 @@ int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, ui
 
   DevBuf<int32_t> comp_of, comp_list, pos_of;
   DevBuf<int32_t> comp_size(C, s), comp_start(C, s), comp_k(C, s), comp_mode(C, s), comp_base(C, s),
-      tile_base(C, s), super_base(C, s), totals(3, s);
+      tile_base(C, s), super_base(C, s), totals(4, s);
   if (C == 1) {
     int32_t hn = n;
     MP_CUDA(cudaMemcpyAsync(comp_size.get(), &hn, 4, cudaMemcpyHostToDevice, s));
@@ -1404,7 +1473,7 @@ int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, ui
   st.mark("components");
   MP_KERNEL(ctx, plan_components<<<1, 1024, 0, s>>>(C, comp_size, target, comp_start, comp_k, comp_mode,
                                                    comp_base, tile_base, super_base, totals));
-  int32_t h_tot[3];
+  int32_t h_tot[4];
   MP_CUDA(cudaMemcpyAsync(h_tot, totals, sizeof h_tot, cudaMemcpyDeviceToHost, s));
   MP_CUDA(cudaStreamSynchronize(s));
   const int32_t P0 = h_tot[0];
@@ -1431,7 +1500,12 @@ int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, ui
       fps_batched_dev(ctx, g, ell, P0, seed, seeds, dist);
     } else {
       fa.ell = ell;
-      const size_t fps_smem = sizeof(int32_t) * (2 * kFrontCap + kSmemTileWords);
+      // shared-memory components: 4 B distance + 16 B local ELL row per vertex
+      const int32_t max_size = h_tot[3];
+      const int64_t base_b = sizeof(int32_t) * (2 * kFrontCap + kSmemTileWords);
+      const int64_t room = (static_cast<int64_t>(ctx.smem_optin) - 16 * 1024 - base_b) / 20;
+      fa.smem_n = static_cast<int32_t>(std::min<int64_t>({room, kFrontCap, 65535, max_size}));
+      const size_t fps_smem = static_cast<size_t>(base_b + 20LL * fa.smem_n);
       allow_max_smem(fps_kernel, ctx.device);
       { const int kt__ = ctx.ktime_begin(kKFps); MP_KERNEL(ctx, fps_kernel<<<C, kFpsThreads, fps_smem, s>>>(fa)); ctx.ktime_end(kt__); }
     }
