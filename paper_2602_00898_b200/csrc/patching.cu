@@ -506,7 +506,9 @@ struct LloydArgs {
 };
 
 __device__ __forceinline__ bool lloyd_active(const LloydArgs& a, int32_t v) {
-  int32_t c = a.comp_of ? a.comp_of[v] : 0;
+  // one component: active for as long as the rounds run (they end when it settles)
+  if (!a.comp_of) return true;
+  int32_t c = a.comp_of[v];
   return a.comp_mode[c] == kModeFps && __ldcg(&a.comp_active[c]) != 0;
 }
 
@@ -572,10 +574,93 @@ struct ClusterBarrier {
   __device__ void sync() { cg::this_cluster().sync(); }
 };
 
-template <class Barrier>
-__global__ void __launch_bounds__(512) lloyd_kernel(LloydArgs a) {
+constexpr int32_t kLloydSmemBest = 512;  // patches whose recenter keys the shared-memory Lloyd keeps on chip
+
+struct BlockBarrier {
+  __device__ void sync() { __syncthreads(); }
+};
+
+// SM variant's BFS level: one frontier vertex per thread, its eight ELL slots'
+// loads and claims in flight together, warp-aggregated appends (shared-memory
+// counter).  visit(w, label(u)) claims w; a CSR tail (degree > 8) is walked
+// by the owning thread.
+template <class V>
+__device__ __forceinline__ void vertex_level(int32_t nf, const int32_t* front, const int32_t* ell, const int32_t* label,
+                                             const DGraph& g, int32_t* gcount, int32_t* next, V&& visit) {
+  const int lane = threadIdx.x & 31;
+  for (int32_t i0 = 0; i0 < nf; i0 += blockDim.x) {
+    const int32_t i = i0 + threadIdx.x;
+    uint32_t got = 0;
+    int32_t xs[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) xs[k] = -1;
+    int32_t u = -1, lu = 0;
+    if (i < nf) {
+      u = front[i];
+      lu = label[u];
+      const int4 r0 = reinterpret_cast<const int4*>(ell)[2 * u], r1 = reinterpret_cast<const int4*>(ell)[2 * u + 1];
+      xs[0] = r0.x, xs[1] = r0.y, xs[2] = r0.z, xs[3] = r0.w, xs[4] = r1.x, xs[5] = r1.y, xs[6] = r1.z, xs[7] = r1.w;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (xs[k] >= 0 && visit(xs[k], lu)) got |= 1u << k;
+    }
+    const int32_t np = __popc(got);
+    int32_t inc = np;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    const int32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+    int32_t base = 0;
+    if (lane == 31 && tot) base = atomicAdd(gcount, tot);
+    base = __shfl_sync(0xffffffffu, base, 31);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if ((got >> k) & 1u) next[base + inc - np + __popc(got & ((1u << k) - 1))] = xs[k];
+    if (u >= 0 && xs[7] < -1)  // CSR tail of a vertex with more than 8 neighbours
+      for (int32_t j = -xs[7] - 2; j < g.off[u + 1]; ++j) {
+        const int32_t w = g.nbr[j];
+        if (visit(w, lu)) next[atomicAdd(gcount, 1)] = w;
+      }
+  }
+}
+
+// SM: one CTA with the per-vertex state (distances, labels, previous labels,
+// both frontiers, the ELL rows) in shared memory -- small meshes (C1), whose
+// BFS levels are then shared-memory work between two CTA barriers.
+template <class Barrier, bool SM = false>
+__global__ void __launch_bounds__(512) lloyd_kernel(LloydArgs a_in) {
   Barrier grid;
-  __shared__ int32_t s_lbuf[kLvlBuf], s_lsh[2];
+  __shared__ int32_t s_lbuf[kLvlBuf], s_lsh[2], s_cnt[4];
+  __shared__ LloydArgs a_sm;  // SM: the arguments with the per-vertex arrays rebound to shared memory
+  __shared__ uint64_t s_best[SM ? kLloydSmemBest : 1];
+  if constexpr (SM) {
+    extern __shared__ int32_t lsm[];
+    const int32_t n0 = a_in.g.n;
+    int32_t* ell = lsm;
+    for (int32_t i = threadIdx.x; i < 8 * n0; i += blockDim.x) ell[i] = a_in.ell[i];
+    if (threadIdx.x == 0) {
+      a_sm = a_in;
+      a_sm.ell = ell;
+      a_sm.dist = ell + 8 * n0;
+      a_sm.label = a_sm.dist + n0;
+      a_sm.prev = a_sm.label + n0;
+      a_sm.fa = a_sm.prev + n0;
+      a_sm.fb = a_sm.fa + n0;
+      a_sm.counters = s_cnt;
+      if (a_in.P <= kLloydSmemBest) a_sm.best = s_best;  // the recenter argmax keys in shared memory
+    }
+    int32_t* prev = ell + 10 * n0;
+    for (int32_t i = threadIdx.x; i < n0; i += blockDim.x) prev[i] = a_in.prev[i];
+    __syncthreads();
+  }
+  const LloydArgs& a = SM ? a_sm : a_in;
+  // per-vertex state loads: shared memory, or L2 (__ldcg) on the grid
+  auto ld = [](const int32_t* p) -> int32_t {
+    if constexpr (SM) return *p;
+    else return __ldcg(p);
+  };
   const int lane = threadIdx.x & 31;
   const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -601,13 +686,13 @@ __global__ void __launch_bounds__(512) lloyd_kernel(LloydArgs a) {
       int32_t* next = a.fb;
       for (int32_t d = 0;; ++d) {
         const int32_t cin = d % 3, cout = (d + 1) % 3, cclr = (d + 2) % 3;
-        const int32_t nf = __ldcg(&a.counters[cin]);
+        const int32_t nf = ld(&a.counters[cin]);
         if (nf == 0) break;
         if (tid == 0) a.counters[cclr] = 0;
         // edge parallel over (frontier vertex, ELL slot), CTA-aggregated appends
         const int64_t items = static_cast<int64_t>(nf) * 8;
         auto visit = [&](int32_t w, int32_t lu) -> bool {
-          int32_t dw = __ldcg(&a.dist[w]);
+          int32_t dw = ld(&a.dist[w]);
           bool fresh = false;
           if (dw == kUnreached) {
             dw = atomicCAS(&a.dist[w], kUnreached, d + 1);
@@ -621,16 +706,17 @@ __global__ void __launch_bounds__(512) lloyd_kernel(LloydArgs a) {
           const int32_t u = front[it >> 3];
           const int32_t x = a.ell[static_cast<int64_t>(u) * 8 + (it & 7)];
           if (x >= 0) {
-            if (visit(x, __ldcg(&a.label[u]))) push(x);
+            if (visit(x, ld(&a.label[u]))) push(x);
           } else if (x < -1) {  // degree > 8: CSR tail
-            const int32_t lu = __ldcg(&a.label[u]);
+            const int32_t lu = ld(&a.label[u]);
             for (int32_t j = -x - 2; j < a.g.off[u + 1]; ++j) {
               const int32_t w = a.g.nbr[j];
               if (visit(w, lu)) push(w);
             }
           }
         };
-        if (items >= kChunkMinItems) chunked_level(items, &a.counters[cout], next, s_lbuf, s_lsh, body);
+        if constexpr (SM) vertex_level(nf, front, a.ell, a.label, a.g, &a.counters[cout], next, visit);
+        else if (items >= kChunkMinItems) chunked_level(items, &a.counters[cout], next, s_lbuf, s_lsh, body);
         else warp_level(items, &a.counters[cout], next, body);
         grid.sync();
         if (tid == 0 && a.work) atomicAdd(&a.work[3], 1ull);
@@ -642,13 +728,13 @@ __global__ void __launch_bounds__(512) lloyd_kernel(LloydArgs a) {
     // ---- stability test (patching.cpp:327-334) per component
     int32_t* chg = a.changed + static_cast<int64_t>(round) * a.C;
     for (int64_t v = tid; v < n; v += nthreads)
-      if (lloyd_active(a, v) && __ldcg(&a.label[v]) != a.prev[v]) chg[a.comp_of ? a.comp_of[v] : 0] = 1;
+      if (lloyd_active(a, v) && ld(&a.label[v]) != a.prev[v]) chg[a.comp_of ? a.comp_of[v] : 0] = 1;
     grid.sync();
     if (tid == 0) a.counters[3] = 0;
     for (int64_t v = tid; v < n; v += nthreads) {
       if (!lloyd_active(a, v)) continue;
       int32_t c = a.comp_of ? a.comp_of[v] : 0;
-      if (__ldcg(&chg[c])) a.prev[v] = __ldcg(&a.label[v]);
+      if (__ldcg(&chg[c])) a.prev[v] = ld(&a.label[v]);
     }
     grid.sync();
     for (int64_t c = tid; c < a.C; c += nthreads) {
@@ -657,7 +743,7 @@ __global__ void __launch_bounds__(512) lloyd_kernel(LloydArgs a) {
       else atomicAdd(&a.counters[3], 1);
     }
     grid.sync();
-    if (__ldcg(&a.counters[3]) == 0 || round == kLloydRounds - 1) break;
+    if (ld(&a.counters[3]) == 0 || round == kLloydRounds - 1) break;
 
     // ---- recenter_seeds (patching.cpp:103-139); dist is reused as depth
     if (tid == 0) a.counters[0] = 0, a.counters[1] = 0, a.counters[2] = 0;
@@ -665,10 +751,19 @@ __global__ void __launch_bounds__(512) lloyd_kernel(LloydArgs a) {
     grid.sync();
     for (int64_t v = tid; v < n; v += nthreads) {
       if (!lloyd_active(a, v)) continue;
-      const int32_t lv = __ldcg(&a.label[v]);
+      const int32_t lv = ld(&a.label[v]);
       bool boundary = false;
-      for (int32_t j = a.g.off[v]; j < a.g.off[v + 1] && !boundary; ++j)
-        boundary = __ldcg(&a.label[a.g.nbr[j]]) != lv;
+      if constexpr (SM) {  // the neighbours from the shared-memory ELL rows (a CSR tail from global)
+        const int4 r0 = reinterpret_cast<const int4*>(a.ell)[2 * v], r1 = reinterpret_cast<const int4*>(a.ell)[2 * v + 1];
+        const int32_t xs[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) boundary |= xs[k] >= 0 && a.label[xs[k]] != lv;
+        if (xs[7] < -1)
+          for (int32_t j = -xs[7] - 2; j < a.g.off[v + 1] && !boundary; ++j) boundary = a.label[a.g.nbr[j]] != lv;
+      } else {
+        for (int32_t j = a.g.off[v]; j < a.g.off[v + 1] && !boundary; ++j)
+          boundary = ld(&a.label[a.g.nbr[j]]) != lv;
+      }
       a.dist[v] = boundary ? 0 : kUnreached;
       if (boundary) a.fa[atomicAdd(&a.counters[0], 1)] = static_cast<int32_t>(v);
     }
@@ -678,12 +773,12 @@ __global__ void __launch_bounds__(512) lloyd_kernel(LloydArgs a) {
       int32_t* next = a.fb;
       for (int32_t d = 0;; ++d) {
         const int32_t cin = d % 3, cout = (d + 1) % 3, cclr = (d + 2) % 3;
-        const int32_t nf = __ldcg(&a.counters[cin]);
+        const int32_t nf = ld(&a.counters[cin]);
         if (nf == 0) break;
         if (tid == 0) a.counters[cclr] = 0;
         const int64_t items = static_cast<int64_t>(nf) * 8;
         auto visit = [&](int32_t w, int32_t lu) -> bool {
-          if (__ldcg(&a.label[w]) != lu || __ldcg(&a.dist[w]) != kUnreached) return false;
+          if (ld(&a.label[w]) != lu || ld(&a.dist[w]) != kUnreached) return false;
           return atomicCAS(&a.dist[w], kUnreached, d + 1) == kUnreached;
         };
         auto body = [&](int64_t it, auto&& push) {
@@ -691,16 +786,17 @@ __global__ void __launch_bounds__(512) lloyd_kernel(LloydArgs a) {
           const int32_t u = front[it >> 3];
           const int32_t x = a.ell[static_cast<int64_t>(u) * 8 + (it & 7)];
           if (x >= 0) {
-            if (visit(x, __ldcg(&a.label[u]))) push(x);
+            if (visit(x, ld(&a.label[u]))) push(x);
           } else if (x < -1) {
-            const int32_t lu = __ldcg(&a.label[u]);
+            const int32_t lu = ld(&a.label[u]);
             for (int32_t j = -x - 2; j < a.g.off[u + 1]; ++j) {
               const int32_t w = a.g.nbr[j];
               if (visit(w, lu)) push(w);
             }
           }
         };
-        if (items >= kChunkMinItems) chunked_level(items, &a.counters[cout], next, s_lbuf, s_lsh, body);
+        if constexpr (SM) vertex_level(nf, front, a.ell, a.label, a.g, &a.counters[cout], next, visit);
+        else if (items >= kChunkMinItems) chunked_level(items, &a.counters[cout], next, s_lbuf, s_lsh, body);
         else warp_level(items, &a.counters[cout], next, body);
         grid.sync();
         int32_t* t = front;
@@ -710,24 +806,29 @@ __global__ void __launch_bounds__(512) lloyd_kernel(LloydArgs a) {
     }
     for (int64_t v = tid; v < n; v += nthreads) {
       if (!lloyd_active(a, v)) continue;
-      const int32_t dv = __ldcg(&a.dist[v]);
+      const int32_t dv = ld(&a.dist[v]);
       if (dv == kUnreached) continue;
-      atomicMax(reinterpret_cast<unsigned long long*>(&a.best[__ldcg(&a.label[v])]),
+      atomicMax(reinterpret_cast<unsigned long long*>(&a.best[ld(&a.label[v])]),
                 static_cast<unsigned long long>(key_max(static_cast<uint32_t>(dv) + 1u, static_cast<uint32_t>(v))));
     }
     grid.sync();
     for (int64_t p = tid; p < a.P; p += nthreads) {
       int32_t c = a.patch_comp ? a.patch_comp[p] : 0;
       if (c < 0 || a.comp_mode[c] != kModeFps || !__ldcg(&a.comp_active[c])) continue;
-      uint64_t b = __ldcg(&a.best[p]);
+      uint64_t b = (SM && a.P <= kLloydSmemBest) ? a.best[p] : __ldcg(&a.best[p]);
       if (b != 0) a.seeds[p] = static_cast<int32_t>(key_max_id(b));
     }
     grid.sync();
+  }
+  if constexpr (SM) {
+    __syncthreads();
+    for (int32_t i = threadIdx.x; i < a.g.n; i += blockDim.x) a_in.prev[i] = a.prev[i];
   }
 }
 
 // Meshes up to this many vertices run the Lloyd rounds on one cluster.
 constexpr int64_t kLloydClusterN = 12288;
+constexpr int64_t kLloydSmemN = 4096;  // ... and up to this many on one CTA with the state in shared memory
 constexpr int kLloydClusterThreads = 512;
 
 // Cluster size for the one-cluster Lloyd: 16 CTAs where the device allows a
@@ -1546,7 +1647,16 @@ int32_t compute_patches_dev(mp_context& ctx, const DGraph& g, int32_t target, ui
     void* args[] = {&la};
     const int64_t cl_max = ctx.tune[MP_TUNE_LLOYD_CLUSTER_N] != 0 ? ctx.tune[MP_TUNE_LLOYD_CLUSTER_N] : kLloydClusterN;
     const int cl = n <= cl_max ? lloyd_cluster_ctas(ctx.device) : 0;
-    if (cl > 0) {
+    const size_t lsm_bytes = sizeof(int32_t) * 13 * static_cast<size_t>(n);  // ELL (8) + dist, label, prev, two frontiers
+    cudaFuncAttributes lfa{};
+    MP_CUDA(cudaFuncGetAttributes(&lfa, lloyd_kernel<BlockBarrier, true>));
+    if (n <= kLloydSmemN && ctx.tune[MP_TUNE_LLOYD_CLUSTER_N] >= 0 &&
+        lsm_bytes + lfa.sharedSizeBytes <= static_cast<size_t>(ctx.smem_optin)) {
+      allow_max_smem(lloyd_kernel<BlockBarrier, true>, ctx.device);
+      const int kt__ = ctx.ktime_begin(kKLloyd);
+      MP_KERNEL(ctx, lloyd_kernel<BlockBarrier, true><<<1, kLloydClusterThreads, lsm_bytes, s>>>(la));
+      ctx.ktime_end(kt__);
+    } else if (cl > 0) {
       cudaLaunchConfig_t cfg{};
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeClusterDimension;
