@@ -359,12 +359,38 @@ constexpr int32_t kMdMinHalf = 1024;    // smallest shared pool half worth runni
 constexpr uint32_t kKeyInf = 0xffffffffu;
 constexpr int kMdSmemThreads = 128;  // four warps: cheap barriers, one member per thread
 
+// Two layouts of the per-vertex state.  Wide: u32 list state / offsets and
+// u16 stamps (k + 1, unique for the whole node).  Compact (nodes that do not
+// fit wide, C5's 8K-vertex leaves): u16 state / offsets (degree < 256, degree
+// sum < 2^16) and u8 stamps unique inside windows of 255 pivots.
+struct MdWide {
+  using S = uint32_t;
+  using T = uint16_t;
+  static constexpr int kShift = 16;
+  static constexpr uint32_t kMask = 0xffffu;
+  static constexpr int32_t kWindow = 1 << 30;
+};
+struct MdCompact {
+  using S = uint16_t;
+  using T = uint8_t;
+  static constexpr int kShift = 8;
+  static constexpr uint32_t kMask = 0xffu;
+  static constexpr int32_t kWindow = 255;
+};
+
+template <class Lay>
 __host__ __device__ inline int64_t md_smem_fixed(int32_t nv) {
   const int64_t nb = (nv + 31) / 32;
-  return 4 * nb + 4 * (4LL * nv + 1) + 8 * nb + 4 * ((nv + 1) & ~1) + 16;
+  const int64_t sw = sizeof(typename Lay::S), tw = sizeof(typename Lay::T);
+  // u32: block minima, keys, boundary offsets, dedup bits, dirty stamps; then
+  // list state, list offsets (S) and the reach / absorbed stamps (T), 4-byte padded
+  return 4 * nb + 8LL * nv + 8 * nb + ((sw * nv + 3) & ~3) + ((sw * (nv + 1) + 3) & ~3) + 2 * ((tw * nv + 3) & ~3) + 16;
 }
 
+template <class Lay>
 __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
+  using S = typename Lay::S;
+  using T = typename Lay::T;
   const int32_t node = a.sched[blockIdx.x];  // largest nodes first
   const int32_t vb = a.node_offsets[node], nv = a.node_offsets[node + 1] - vb;
   if (nv == 0 || (a.node_mask && !a.node_mask[node])) return;
@@ -374,14 +400,19 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
   const int32_t nb = (nv + 31) / 32;
   uint32_t* blk = reinterpret_cast<uint32_t*>(md_sm);
   uint32_t* kd = blk + nb;
-  uint32_t* st = kd + nv;
-  uint32_t* ebp = st + nv;
-  uint32_t* loff = ebp + nv;  // nv + 1
-  uint32_t* inr = loff + nv + 1;
-  uint32_t* dst = inr + nb;  // dirty-block stamp: k + 1 = listed for refresh after pivot k
-  uint16_t* mk = reinterpret_cast<uint16_t*>(dst + nb);  // reach stamp: k + 1 = in pivot k's reach
-  uint16_t* ea = mk + ((nv + 1) & ~1);                   // absorbed stamp: k + 1 = absorbed by pivot k
-  uint16_t* L = ea + ((nv + 1) & ~1);
+  uint32_t* ebp = kd + nv;
+  uint32_t* inr = ebp + nv;
+  uint32_t* dstp = inr + nb;  // dirty-block stamp: k + 1 = listed for refresh after pivot k
+  char* cb = reinterpret_cast<char*>(dstp + nb);
+  S* st = reinterpret_cast<S*>(cb);  // live: |adj| | |elems| << kShift; element: |boundary|
+  cb += (sizeof(S) * nv + 3) & ~3;
+  S* loff = reinterpret_cast<S*>(cb);  // nv + 1 list offsets
+  cb += (sizeof(S) * (nv + 1) + 3) & ~3;
+  T* mk = reinterpret_cast<T*>(cb);  // reach stamp
+  cb += (sizeof(T) * nv + 3) & ~3;
+  T* ea = reinterpret_cast<T*>(cb);  // absorbed stamp
+  cb += (sizeof(T) * nv + 3) & ~3;
+  uint16_t* L = reinterpret_cast<uint16_t*>(cb);
   __shared__ int32_t s_cursor, s_cap, s_inglobal, s_maxdeg, s_nbd[2], s_ndirty, s_ip, sh[32];
   __shared__ int32_t s_dlist[kMdSmemMaxNv / 32];
   __shared__ int64_t s_red64[32];
@@ -407,24 +438,25 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
     const int32_t k = b0 + threadIdx.x;
     int32_t tot;
     const int32_t ex = block_excl_scan(k < nv ? static_cast<int32_t>(st[k]) : 0, sh, &tot);
-    if (k < nv) loff[k] = run + ex;
+    if (k < nv) loff[k] = static_cast<S>(run + ex);
     run += tot;
   }
   const int64_t D = run;
-  const int64_t half = (a.smem_bytes - md_smem_fixed(nv) - 2 * D) / 4;  // u16 entries per pool half
-  if (half < kMdMinHalf || static_cast<int64_t>(s_maxdeg) * nv >= (1LL << 19)) {
+  const int64_t half = (a.smem_bytes - md_smem_fixed<Lay>(nv) - 2 * D) / 4;  // u16 entries per pool half
+  if (half < kMdMinHalf || static_cast<int64_t>(s_maxdeg) * nv >= (1LL << 19) ||
+      static_cast<uint32_t>(s_maxdeg) > Lay::kMask || static_cast<uint64_t>(D) > static_cast<uint64_t>(S(~S(0)))) {
     __syncthreads();
     md_node_global(a, node);  // lists or keys do not fit: global state
     return;
   }
   if (threadIdx.x == 0) {
-    loff[nv] = static_cast<uint32_t>(D);
+    loff[nv] = static_cast<S>(D);
     s_cursor = 0, s_inglobal = 0;
     s_cap = static_cast<int32_t>(half);
     s_cur = L + D;
     s_other = L + D + half;
   }
-  for (int32_t b = threadIdx.x; b < nb; b += blockDim.x) inr[b] = 0, dst[b] = 0;
+  for (int32_t b = threadIdx.x; b < nb; b += blockDim.x) inr[b] = 0, dstp[b] = 0;
   for (int32_t i = threadIdx.x; i < nv; i += blockDim.x) mk[i] = 0, ea[i] = 0;
   if (threadIdx.x == 0) s_nbd[0] = s_nbd[1] = 0, s_ndirty = 0;
   // induced subgraph in local ids
@@ -436,7 +468,7 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
       const int32_t w = a.g.nbr[j];
       if (a.node_of[w] == node) L[o + c++] = static_cast<uint16_t>(a.local_of[w]);
     }
-    st[k] = static_cast<uint32_t>(c);
+    st[k] = static_cast<S>(c);
     kd[k] = (static_cast<uint32_t>(c) << 13) | static_cast<uint32_t>(k);
   }
   __syncthreads();
@@ -451,10 +483,17 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
   const uint32_t below = (1u << lane) - 1;
   // a block whose minimum may have risen is recomputed after the member updates
   auto mark_dirty = [&](int32_t b, uint32_t sp) {
-    if (atomicExch(&dst[b], sp) != sp) s_dlist[atomicAdd(&s_ndirty, 1)] = b;
+    if (atomicExch(&dstp[b], sp) != sp) s_dlist[atomicAdd(&s_ndirty, 1)] = b;
   };
   for (int32_t k = 0; k < nv; ++k) {
-    const uint16_t stamp = static_cast<uint16_t>(k + 1);  // nv <= kMdSmemMaxNv < 65536
+    // 8-bit stamps: unique inside a window of 255 pivots; the arrays are
+    // cleared when a window starts (every user of the old stamps is behind B4)
+    if (Lay::kWindow < kMdSmemMaxNv && k > 0 && k % Lay::kWindow == 0) {
+      for (int32_t i = threadIdx.x; i < nv; i += blockDim.x) mk[i] = 0, ea[i] = 0;
+      __syncthreads();
+    }
+    const T stamp = static_cast<T>(k % Lay::kWindow + 1);
+    const uint32_t dstamp = static_cast<uint32_t>(k + 1);
     // pivot: min key over the block minima (every warp; blk is stable since B4)
     uint32_t best = kKeyInf;
 #pragma unroll 4
@@ -516,7 +555,7 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
     const int32_t cur0 = s_cursor;
     uint16_t* out = cur + cur0;
     const uint32_t pst = st[p];
-    const int32_t np_adj = pst & 0xffff, np_el = pst >> 16;
+    const int32_t np_adj = pst & Lay::kMask, np_el = pst >> Lay::kShift;
     const uint32_t po = loff[p], pe = loff[p + 1];
     // ---- reach: variables of p plus the boundaries of p's elements.  With at
     // most one element the parts need no deduplication: adj(p) lost every
@@ -589,14 +628,14 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
       if (w == p) continue;
       const uint32_t o = loff[w], oe = loff[w + 1];
       const uint32_t wst = st[w];
-      const int32_t na = wst & 0xffff, ne = wst >> 16;
+      const int32_t na = wst & Lay::kMask, ne = wst >> Lay::kShift;
       // both lists in chunks of four: the chunk's slots, then their bit-set
       // words and sizes, are independent loads in flight together (a chunk's
       // compacting writes land at or below its reads)
       int32_t c = 0;
       for (int32_t j0 = 0; j0 < na; j0 += 4) {
         int32_t x[4];
-        uint16_t iw[4];
+        T iw[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) x[q] = j0 + q < na ? L[o + j0 + q] : p;
 #pragma unroll
@@ -609,7 +648,7 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
       uint32_t d = static_cast<uint32_t>(c + nbd);
       for (int32_t j0 = 0; j0 < ne; j0 += 4) {
         int32_t e[4];
-        uint16_t ab[4];
+        T ab[4];
         uint32_t sz[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) e[q] = j0 + q < ne ? L[oe - 1 - (j0 + q)] : -1;
@@ -625,12 +664,12 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
           }
       }
       L[oe - 1 - ce++] = static_cast<uint16_t>(p);
-      st[w] = static_cast<uint32_t>(c) | (static_cast<uint32_t>(ce) << 16);
+      st[w] = static_cast<S>(c | (ce << Lay::kShift));
       const uint32_t nk = (d << 13) | static_cast<uint32_t>(w), ok = kd[w];
       kd[w] = nk;
       const int32_t b = w >> 5;
       if (nk < ok) atomicMin(&blk[b], nk);
-      else if (nk > ok && ok == blk[b]) mark_dirty(b, stamp);
+      else if (nk > ok && ok == blk[b]) mark_dirty(b, dstamp);
     }
     __syncthreads();  // B3
     if (!simple)  // the deduplication bits (simple reaches only stamp)
@@ -658,7 +697,7 @@ __global__ void __launch_bounds__(kMdSmemThreads) md_smem_kernel(MdArgs a) {
     }
     if (threadIdx.x == 0) {
       if (simple && np_el && s_ip != ptotal - 1) out[s_ip] = out[ptotal - 1];  // the boundary without p
-      st[p] = static_cast<uint32_t>(nbd);
+      st[p] = static_cast<S>(nbd);
       s_cursor = cur0 + nbd;
       s_nbd[(k + 1) & 1] = 0;  // its last reader was the previous pivot, before this B2
     }
@@ -775,27 +814,39 @@ void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t L, const int
     }
     if (ns > big) {
       a.sched = dsched.get() + big;
-      allow_max_smem(md_smem_kernel, ctx.device);
-      cudaFuncAttributes fa{};
-      MP_CUDA(cudaFuncGetAttributes(&fa, md_smem_kernel));
+      allow_max_smem(md_smem_kernel<MdWide>, ctx.device);
+      allow_max_smem(md_smem_kernel<MdCompact>, ctx.device);
+      cudaFuncAttributes fw{}, fc{};
+      MP_CUDA(cudaFuncGetAttributes(&fw, md_smem_kernel<MdWide>));
+      MP_CUDA(cudaFuncGetAttributes(&fc, md_smem_kernel<MdCompact>));
       // dynamic shared memory: what the largest shared-memory node needs
       // (state + lists from its degree sum + pool halves of 4 nv entries), so
       // small nodes (C4 frames) keep several CTAs per SM and leave room for
-      // the other contexts' kernels
-      const int64_t cap = static_cast<int64_t>(ctx.smem_optin) - static_cast<int64_t>(fa.sharedSizeBytes);
-      int64_t want = 0;
+      // the other contexts' kernels.  The compact layout when some node fits
+      // only that way (its lists plus the smallest pool halves).
+      const int64_t cap = static_cast<int64_t>(ctx.smem_optin) -
+                          static_cast<int64_t>(std::max(fw.sharedSizeBytes, fc.sharedSizeBytes));
+      int64_t want_w = 0, want_c = 0;
+      bool compact = false;
       for (int32_t i = big; i < ns; ++i) {
         const int32_t node = sched[i];
         const int64_t nv = hoff[node + 1] - hoff[node];
         const int64_t dsum = (hneed[node] / 2 - 64 - 2 * nv) / 4;
-        want = std::max(want, md_smem_fixed(static_cast<int32_t>(nv)) + 2 * dsum + 4 * std::max<int64_t>(kMdMinHalf, 4 * nv));
+        const int64_t fw_n = md_smem_fixed<MdWide>(static_cast<int32_t>(nv)) + 2 * dsum;
+        const int64_t fc_n = md_smem_fixed<MdCompact>(static_cast<int32_t>(nv)) + 2 * dsum;
+        want_w = std::max(want_w, fw_n + 4 * std::max<int64_t>(kMdMinHalf, 4 * nv));
+        want_c = std::max(want_c, fc_n + 4 * std::max<int64_t>(kMdMinHalf, 4 * nv));
+        if (fw_n + 4 * kMdMinHalf > cap && fc_n + 4 * kMdMinHalf <= cap) compact = true;
       }
-      a.smem_bytes = std::min(cap, (want + 1023) & ~int64_t(1023));
+      a.smem_bytes = std::min(cap, ((compact ? want_c : want_w) + 1023) & ~int64_t(1023));
       a.gsmem_bytes = a.smem_bytes;
       const int threads = ctx.tune[MP_TUNE_MD_THREADS] > 0
                               ? static_cast<int>(std::min<int64_t>(kMdSmemThreads, ctx.tune[MP_TUNE_MD_THREADS]) & ~31)
                               : kMdSmemThreads;
-      MP_KERNEL(ctx, md_smem_kernel<<<ns - big, std::max(threads, 32), static_cast<size_t>(a.smem_bytes), s>>>(a));
+      if (compact)
+        MP_KERNEL(ctx, md_smem_kernel<MdCompact><<<ns - big, std::max(threads, 32), static_cast<size_t>(a.smem_bytes), s>>>(a));
+      else
+        MP_KERNEL(ctx, md_smem_kernel<MdWide><<<ns - big, std::max(threads, 32), static_cast<size_t>(a.smem_bytes), s>>>(a));
     }
     if (big > 0) MP_CUDA(cudaStreamWaitEvent(s, ctx.fork_ev[1], 0));
   } else {
