@@ -26,7 +26,8 @@ out.append(f"\nTotal kernel time {T/1e6:.1f} ms over {len(half)} launches.\n")
 want = ["Duration", "Elapsed Cycles", "SM Frequency", "DRAM Throughput", "L2 Hit Rate", "L1/TEX Hit Rate",
         "Achieved Occupancy", "Registers Per Thread", "Block Size", "Grid Size", "Executed Ipc Active",
         "Warp Cycles Per Issued Instruction"]
-traffic = {}
+import os
+traffic = json.load(open("profiles/traffic.json")) if os.path.exists("profiles/traffic.json") else {}  # kernels not re-captured keep their entry
 for rep in sorted(glob.glob(f"gpurun_out/{R}_ncu_*.ncu-rep")):
     kname = rep.split(f"{R}_ncu_")[1].replace(".ncu-rep", "")
     det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
