@@ -787,6 +787,7 @@ __device__ __forceinline__ bool ref_less(const RefKey& x, const RefKey& y) {
 // dead vertices never count as neighbours) plus the vertex's patch side, so
 // no node-membership lookups are needed; adjacency comes from the ELL copy.
 constexpr int32_t kRefSmemList = 12 * 1024;  // candidate entries kept in shared memory (10 B each)
+constexpr int32_t kRefSmemN = 4096;          // graphs up to this size refine with their state in shared memory
 
 // Ordered compaction of [0, cnt) by the whole block: warp w owns the
 // contiguous range [w * per, (w + 1) * per); pass 1 counts, pass 2 emits with
@@ -925,7 +926,14 @@ __global__ void split_classify(LevelArgs a, uint32_t* keys, uint32_t drop_key, i
   }
 }
 
+// SM: small graphs (n <= kRefSmemN) copy the per-vertex state the moves read
+// -- ELL rows, list slots, regions, patch sides -- into shared memory, so a
+// move's dependent loads are shared-memory round trips instead of L2 ones;
+// the regions and slots of the list entries (every vertex a move touches)
+// are written back at the end.
+template <bool SM>
 __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
+  constexpr int32_t kCap = SM ? kRefSmemN : kRefSmemList;  // candidate entries kept in shared memory
   const int32_t li = blockIdx.x;
   const int32_t s0 = a.seg_start[li], cnt = a.seg_cnt[li];
   __shared__ int32_t shi[32];
@@ -944,12 +952,29 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
   auto use_lists = [&](bool sm) {
     in_smem = sm;
     lv = sm ? ref_sm : a.sep_list + s0;
-    lpull = sm ? ref_sm + kRefSmemList : a.ref_pull + s0;
-    lown = sm ? reinterpret_cast<uint8_t*>(ref_sm + 2 * kRefSmemList) : a.ref_own + s0;
-    lin = sm ? reinterpret_cast<uint8_t*>(ref_sm + 2 * kRefSmemList) + kRefSmemList : a.ref_in + s0;
+    lpull = sm ? ref_sm + kCap : a.ref_pull + s0;
+    lown = sm ? reinterpret_cast<uint8_t*>(ref_sm + 2 * kCap) : a.ref_own + s0;
+    lin = sm ? reinterpret_cast<uint8_t*>(ref_sm + 2 * kCap) + kCap : a.ref_in + s0;
   };
   int8_t* region = a.region;
   const int32_t* ell = a.ell;
+  int32_t* slot_of = a.slot_of;
+  const uint8_t* vside = a.vside;
+  if constexpr (SM) {
+    const int32_t n = a.g.n;
+    int32_t* sell = ref_sm + (10 * kCap) / 4;  // after the candidate lists
+    int32_t* sslot = sell + 8 * n;
+    int8_t* sreg = reinterpret_cast<int8_t*>(sslot + n);
+    uint8_t* sside = reinterpret_cast<uint8_t*>(sreg + n);
+    for (int32_t i = threadIdx.x; i < 8 * n; i += blockDim.x) sell[i] = a.ell[i];
+    for (int32_t i = threadIdx.x; i < n; i += blockDim.x) {
+      sslot[i] = a.slot_of[i];
+      sreg[i] = a.region[i];
+      sside[i] = a.vside[i];
+    }
+    ell = sell, slot_of = sslot, region = sreg, vside = sside;
+    __syncthreads();
+  }
 
   // neighbour w of v through the ELL copy, slot k of a warp-uniform walk;
   // returns -1 past the end (the CSR tail serves vertices of degree > 8)
@@ -967,7 +992,7 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
   {
     const int32_t run = a.ref_cnt[li];
     const int64_t r0 = a.ref_rw[2 * li], r1 = a.ref_rw[2 * li + 1];
-    use_lists(run < kRefSmemList / 2);
+    use_lists(run < kCap / 2);
     if (in_smem)
       for (int32_t k = threadIdx.x; k < run; k += blockDim.x) {
         lv[k] = a.sep_list[s0 + k];
@@ -998,7 +1023,7 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
   }
   // greedy moves (partition.cpp:235-274)
   for (;;) {
-    if (in_smem && s_list >= kRefSmemList) {  // the list outgrew shared memory: move it to global
+    if (in_smem && s_list >= kCap) {  // the list outgrew shared memory: move it to global
       int32_t* gv = a.sep_list + s0;
       int32_t* gp = a.ref_pull + s0;
       uint8_t* go = a.ref_own + s0;
@@ -1039,7 +1064,7 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
       if (mv >= 0) {
         // mv's slot, its ELL row and its degree are independent loads
         const int32_t e_mv = lane < 8 ? ell[static_cast<int64_t>(mv) * 8 + lane] : -1;
-        const int32_t im = a.slot_of[mv];
+        const int32_t im = slot_of[mv];
         const int32_t e7 = __shfl_sync(0xffffffffu, e_mv, 7);
         const int32_t dmv = e7 < -1 ? degree(mv) : 0;  // CSR tail: exact degree needed
         const int8_t own = static_cast<int8_t>(lown[im]), opp = 1 - own;
@@ -1060,7 +1085,7 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
           uint8_t vs = 0;
           int4 r0 = make_int4(-1, -1, -1, -1), r1 = r0;  // w's ELL row (used if w is pulled)
           if (w >= 0) {
-            rw = region[w], sw = a.slot_of[w], vs = a.vside[w];
+            rw = region[w], sw = slot_of[w], vs = vside[w];
             const int4* row = reinterpret_cast<const int4*>(ell + static_cast<int64_t>(w) * 8);
             r0 = row[0], r1 = row[1];
           }
@@ -1081,7 +1106,7 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
               ws = tail + __popc(mf & ((1u << lane) - 1));
               lv[ws] = w;
               lown[ws] = vs;
-              a.slot_of[w] = ws;
+              slot_of[w] = ws;
             }
             lin[ws] = 2;  // 2 = pulled by this move
           }
@@ -1098,7 +1123,7 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
             for (int k = 0; k < 8; ++k) {
               const int32_t x = xs[k];
               rx[k] = x >= 0 ? region[x] : int8_t(3);
-              ix[k] = x >= 0 ? a.slot_of[x] : -1;
+              ix[k] = x >= 0 ? slot_of[x] : -1;
             }
             auto visit = [&](int32_t x, int8_t r, int32_t slot) {
               if (x == mv) r = own;
@@ -1115,7 +1140,7 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
             if (xs[7] < -1)  // CSR tail of a pulled vertex with more than 8 neighbours
               for (int32_t j = -xs[7] - 2; j < a.g.off[w + 1]; ++j) {
                 const int32_t x = a.g.nbr[j];
-                visit(x, region[x], a.slot_of[x]);
+                visit(x, region[x], slot_of[x]);
               }
             lpull[ws] = cntp;
           }
@@ -1134,7 +1159,7 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
           const int32_t w = k0 + lane < dmv ? nbr_at(mv, k0 + lane) : -1;
           const bool pull = w >= 0 && region[w] == opp;
           const uint32_t m = __ballot_sync(0xffffffffu, pull);
-          const bool fresh = pull && a.slot_of[w] < 0;
+          const bool fresh = pull && slot_of[w] < 0;
           const uint32_t mf = __ballot_sync(0xffffffffu, fresh);
           if (pull) {
             region[w] = 2;
@@ -1143,14 +1168,14 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
           if (fresh) {
             const int32_t k2 = tail + __popc(mf & ((1u << lane) - 1));
             lv[k2] = w;
-            lown[k2] = a.vside[w];
-            a.slot_of[w] = k2;
+            lown[k2] = vside[w];
+            slot_of[w] = k2;
           }
           tail += __popc(mf);
           np += __popc(m);
         }
         __syncwarp();
-        for (int32_t t = lane; t < np; t += 32) lin[a.slot_of[pulled[t]]] = 2;  // 2 = pulled by this move
+        for (int32_t t = lane; t < np; t += 32) lin[slot_of[pulled[t]]] = 2;  // 2 = pulled by this move
         if (lane == 0) {
           region[mv] = own;
           lin[im] = 0;
@@ -1161,7 +1186,7 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
         for (int32_t k0 = 0; k0 < dmv; k0 += 32) {
           const int32_t x = k0 + lane < dmv ? nbr_at(mv, k0 + lane) : -1;
           if (x >= 0 && region[x] == 2) {
-            const int32_t ix = a.slot_of[x];
+            const int32_t ix = slot_of[x];
             if (lin[ix] == 1 && lown[ix] == opp) atomicAdd(&lpull[ix], 1);
           }
         }
@@ -1170,7 +1195,7 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
           const int32_t t = t0 + (lane >> 3);
           const int32_t wv = t < np ? pulled[t] : -1;
           const int32_t dw = wv >= 0 ? degree(wv) : 0;
-          const uint8_t wopp = wv >= 0 ? static_cast<uint8_t>(1 - a.vside[wv]) : 0;
+          const uint8_t wopp = wv >= 0 ? static_cast<uint8_t>(1 - vside[wv]) : 0;
           int32_t cntp = 0;
           for (int32_t k = (lane & 7); k < dw; k += 8) {
             const int32_t x = nbr_at(wv, k);
@@ -1178,7 +1203,7 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
             const int8_t rx = region[x];
             cntp += rx == wopp;
             if (rx == 2) {
-              const int32_t ix = a.slot_of[x];
+              const int32_t ix = slot_of[x];
               if (lin[ix] == 1 && lown[ix] == own) atomicSub(&lpull[ix], 1);
             }
           }
@@ -1186,10 +1211,10 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
           cntp += __shfl_xor_sync(0xffffffffu, cntp, 1);
           cntp += __shfl_xor_sync(0xffffffffu, cntp, 2);
           cntp += __shfl_xor_sync(0xffffffffu, cntp, 4);
-          if (wv >= 0 && (lane & 7) == 0) lpull[a.slot_of[wv]] = cntp;
+          if (wv >= 0 && (lane & 7) == 0) lpull[slot_of[wv]] = cntp;
         }
         __syncwarp();
-        for (int32_t t = lane; t < np; t += 32) lin[a.slot_of[pulled[t]]] = 1;
+        for (int32_t t = lane; t < np; t += 32) lin[slot_of[pulled[t]]] = 1;
         }
         const int64_t nrw0 = s_rw[0] + (own == 0 ? 1 : -np), nrw1 = s_rw[1] + (own == 1 ? 1 : -np);
         // imbalance table of the next move
@@ -1214,8 +1239,9 @@ __global__ void __launch_bounds__(kNodeThreads) refine_kernel(LevelArgs a) {
   // moves the sides to the children
   for (int32_t i = threadIdx.x; i < s_list; i += blockDim.x) {
     const int32_t v = lv[i];
-    a.slot_of[v] = -1;
+    slot_of[v] = -1;
     if (region[v] == 2) region[v] = 3;  // the separator leaves the game
+    if constexpr (SM) a.slot_of[v] = -1, a.region[v] = region[v];
   }
   if (threadIdx.x == 0) atomicAdd(&a.stats[1], static_cast<unsigned long long>(s_moves));
 }
@@ -1595,11 +1621,16 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     MP_CUDA(cudaMemsetAsync(ref_rw, 0, sizeof(int32_t) * 2 * width, s));
     a.ref_cnt = ref_cnt, a.ref_rw = ref_rw;
     const size_t ref_smem = static_cast<size_t>(kRefSmemList) * 10;  // 120 KB
-    allow_max_smem(refine_kernel, ctx.device);
+    const bool ref_sm_state = n <= kRefSmemN;
+    allow_max_smem(refine_kernel<false>, ctx.device);
+    allow_max_smem(refine_kernel<true>, ctx.device);
     {
       const int kt__ = ctx.ktime_begin(kKRefine);
       MP_KERNEL(ctx, ref_init<<<lgrid, 256, 0, s>>>(a));
-      MP_KERNEL(ctx, refine_kernel<<<width, kNodeThreads, ref_smem, s>>>(a));
+      if (ref_sm_state)  // lists of kRefSmemN entries + 38 B of state per vertex
+        MP_KERNEL(ctx, refine_kernel<true><<<width, kNodeThreads, 10 * kRefSmemN + 38 * static_cast<size_t>(n), s>>>(a));
+      else
+        MP_KERNEL(ctx, refine_kernel<false><<<width, kNodeThreads, ref_smem, s>>>(a));
       ctx.ktime_end(kt__);
     }
     st.mark("level/super+refine");
