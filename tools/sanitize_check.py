@@ -28,8 +28,6 @@ perm = np.random.default_rng(1).permutation(g2.n).astype(np.int32)
 fe = mp.elimination_fill(g2, perm)
 rows, offs = [], [0]
 b = 12
-for v in range(g.n if False else 300):
-    pass
 g4 = mp.mesh_to_graph(mp.make_grid_mesh(12, 9))
 blk_rows, blk_off = [], [0]
 for v in range(g4.n):
@@ -42,4 +40,8 @@ for v in range(g4.n):
 g5 = mp.AdjacencyGraph(g4.n * b, np.asarray(blk_off, np.int32), np.concatenate(blk_rows).astype(np.int32))
 r5 = mp.order(g5, patch_size=64, nd_level=2)
 r6 = mp.order(mp.mesh_to_graph(mp.make_grid_mesh(90, 90)), patch_size=2000, nd_level=1)
-print("round2 paths ok", rg.fill.nnz_L, fe.nnz_L, r5.fill.nnz_L, r6.fill.nnz_L)
+# session-d paths: 7K-vertex leaves (the compact MD layout), and the small
+# mesh paths of C1 above (shared-memory FPS, one-CTA Lloyd, refine with
+# shared-memory state, the shared-memory repair split)
+r7 = mp.order(mp.mesh_to_graph(mp.make_grid_mesh(120, 120)), patch_size=256, nd_level=1)
+print("round2 paths ok", rg.fill.nnz_L, fe.nnz_L, r5.fill.nnz_L, r6.fill.nnz_L, r7.fill.nnz_L)
