@@ -212,6 +212,22 @@ def check_tree_properties(g, res):
     assert int(res.fill.column_counts.sum()) == res.fill.nnz_L
 
 
+@pytest.mark.parametrize("tune", [{"lloyd_cluster_n": -1}, {"lloyd_cluster_n": 1 << 20}, {"md_threads": 32},
+                                  {"md_threads": 64}])
+def test_c1_kernel_variants_match_reference_digests(tune):
+    """C1 through the other Lloyd variants (grid-wide instead of the
+    shared-memory CTA) and MD on one or two warps: the same digests."""
+    gold = json.loads((GOLDEN / "bench_golden.json").read_text())["c1"]
+    ctx = mp.Context(0)
+    for k, v in tune.items():
+        ctx.set_tuning(k, v)
+    res = mp.order(mp.mesh_to_graph(mp.make_grid_mesh(64, 64)), ctx=ctx)
+    assert digest(res.patch.assignment) == gold["sha_assignment"]
+    assert digest(res.tree.local_perm) == gold["sha_local_perm"]
+    assert digest(res.perm.perm) == gold["sha_perm"]
+    assert res.fill.nnz_L == gold["nnz_L"]
+
+
 @pytest.mark.parametrize("name", ["c1", "ico158", "c2", "c3"])
 def test_baseline_configs_match_reference_digests(name):
     gold = json.loads((GOLDEN / "bench_golden.json").read_text())[name]
