@@ -156,6 +156,61 @@ __global__ void set_lidx(int32_t total, const int32_t* plist, const int32_t* pno
     lidx[p] = i - poff[pnode[p]];
   }
 }
+// Small quotients (P <= kSmallP): the alive patches of the active nodes,
+// grouped by node and ascending inside it (the stable radix sort of the
+// general path), with the per-node offsets and the node-local indices -- in
+// ONE CTA: a bitonic sort of (node << 13 | patch) keys in shared memory and a
+// block scan of the node counts, instead of a dozen small launches per level.
+constexpr int32_t kSmallP = 8192;
+__global__ void __launch_bounds__(1024) level_lists_small(int32_t P, int32_t width, const int32_t* pw,
+                                                          const int32_t* pnode, const int32_t* np_node,
+                                                          const int32_t* active, int32_t* plist, int32_t* poff,
+                                                          int32_t* lidx, int32_t* cnt) {
+  __shared__ uint32_t key[kSmallP];
+  __shared__ int32_t sh[32], s_na;
+  int32_t N = 1;
+  while (N < P) N <<= 1;
+  if (threadIdx.x == 0) s_na = 0;
+  __syncthreads();
+  int32_t mine = 0;
+  for (int32_t q = threadIdx.x; q < N; q += blockDim.x) {
+    const bool ok = q < P && pw[q] > 0 && active[pnode[q]];
+    key[q] = ok ? (static_cast<uint32_t>(pnode[q]) << 13) | static_cast<uint32_t>(q) : 0xffffffffu;
+    mine += ok;
+  }
+  atomicAdd(&s_na, mine);
+  for (int32_t k = 2; k <= N; k <<= 1)
+    for (int32_t j = k >> 1; j > 0; j >>= 1) {
+      __syncthreads();
+      for (int32_t i = threadIdx.x; i < N; i += blockDim.x) {
+        const int32_t l = i ^ j;
+        if (l > i) {
+          const uint32_t x = key[i], y = key[l];
+          if (((i & k) == 0) == (x > y)) key[i] = y, key[l] = x;
+        }
+      }
+    }
+  __syncthreads();
+  // per-node offsets: exclusive scan of the active nodes' patch counts
+  int32_t run = 0;
+  for (int32_t b0 = 0; b0 <= width; b0 += blockDim.x) {
+    const int32_t i = b0 + threadIdx.x;
+    const int32_t c = (i < width && active[i]) ? np_node[i] : 0;
+    int32_t tot;
+    const int32_t ex = block_excl_scan(c, sh, &tot);
+    if (i <= width) poff[i] = run + ex;
+    run += tot;
+  }
+  __syncthreads();
+  const int32_t na = s_na;
+  for (int32_t i = threadIdx.x; i < na; i += blockDim.x) {
+    const uint32_t kk = key[i];
+    const int32_t q = static_cast<int32_t>(kk & 0x1fffu), node = static_cast<int32_t>(kk >> 13);
+    plist[i] = q;
+    lidx[q] = i - poff[node];
+  }
+  if (threadIdx.x == 0) cnt[1] = na, cnt[2] = na;
+}
 // Crossing-edge keys among alive vertices of active nodes; both directions.
 __global__ void emit_crossing(LevelArgs a, uint64_t* keys, int32_t* count) {
   for (int32_t li = blockIdx.y; li < a.width; li += gridDim.y) {
@@ -1502,6 +1557,15 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     MP_KERNEL(ctx, level_patch_counts<<<grid_for(ctx, P), 256, 0, s>>>(a));
     MP_KERNEL(ctx, level_activity<<<grid_for(ctx, width), 256, 0, s>>>(a, L, level, cnt.get()));
     // alive patches of active nodes, grouped by node, ascending
+    if (P <= kSmallP) {
+      MP_KERNEL(ctx, level_lists_small<<<1, 1024, 0, s>>>(P, width, pw, pnode, np_node, active, plist, poff, lidx,
+                                                           cnt));
+      int32_t hc[2];
+      MP_CUDA(cudaMemcpyAsync(hc, cnt.get(), 8, cudaMemcpyDeviceToHost, s));
+      MP_CUDA(cudaStreamSynchronize(s));
+      if (hc[0] == 0) break;  // no active node at this level: the tree is complete
+      na_level = hc[1];
+    } else {
     MP_KERNEL(ctx, flag_alive_patches<<<grid_for(ctx, P), 256, 0, s>>>(P, pw, pnode, active, flag, pkey));
     {
       DevBuf<int32_t> ids(Pm, s), sel(Pm, s), selkey(Pm, s);
@@ -1535,6 +1599,7 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
       MP_CUDA(cub::DeviceScan::ExclusiveSum(t4.get(), tmp3, npm.get(), poff.get(), width + 1, s));
       na_level = na;
       MP_KERNEL(ctx, set_lidx<<<grid_for(ctx, na), 256, 0, s>>>(na, plist, pnode, poff, lidx));
+    }
     }
     a.plist = plist, a.poff = poff;
     st.mark("level/patches");
