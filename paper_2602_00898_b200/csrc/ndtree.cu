@@ -1635,19 +1635,6 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     size_t fm_smem = 1024;
     bool fm_hybrid = false;  // a node whose state fits shared memory but whose adjacency does not
     {
-      // room for the packed adjacency of the largest node that fits
-      std::vector<int64_t> hfo(width + 1);
-      std::vector<int32_t> hpo(width + 1);
-      MP_CUDA(cudaMemcpyAsync(hfo.data(), fifo_off.get(), sizeof(int64_t) * (width + 1), cudaMemcpyDeviceToHost, s));
-      MP_CUDA(cudaMemcpyAsync(hpo.data(), poff.get(), sizeof(int32_t) * (width + 1), cudaMemcpyDeviceToHost, s));
-      MP_CUDA(cudaStreamSynchronize(s));
-      size_t need = 0, need_state = 0;
-      for (int32_t i = 0; i < width; ++i) {
-        const int64_t np_i = hpo[i + 1] - hpo[i];
-        if (np_i == 0) continue;
-        need = std::max<size_t>(need, static_cast<size_t>(fm_node_smem(np_i, (hfo[i + 1] - hfo[i]) - np_i)));
-        need_state = std::max<size_t>(need_state, static_cast<size_t>(fm_node_smem(np_i, 0)));
-      }
       // opt-in limit minus the kernels' static shared memory
       cudaFuncAttributes fa32{}, fa64{}, fah{};
       MP_CUDA(cudaFuncGetAttributes(&fa32, fm_kernel<uint32_t, true>));
@@ -1655,13 +1642,34 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
       MP_CUDA(cudaFuncGetAttributes(&fah, fm_kernel<uint32_t, true, true>));
       const size_t cap = static_cast<size_t>(ctx.smem_optin) -
                          std::max({fa32.sharedSizeBytes, fa64.sharedSizeBytes, fah.sharedSizeBytes});
-      fm_smem = std::min<size_t>(std::max(fm_smem, need), cap);
-      fm_hybrid = need > cap && need_state <= cap;
+      // every node holds at most the level's alive patches and quotient
+      // entries: when that bound fits, no per-node sizes are read back
+      const size_t bound = static_cast<size_t>(fm_node_smem(na_level, U));
+      if (bound <= cap) {
+        fm_smem = std::max(fm_smem, bound);
+      } else {
+        // room for the packed adjacency of the largest node that fits
+        std::vector<int64_t> hfo(width + 1);
+        std::vector<int32_t> hpo(width + 1);
+        MP_CUDA(cudaMemcpyAsync(hfo.data(), fifo_off.get(), sizeof(int64_t) * (width + 1), cudaMemcpyDeviceToHost, s));
+        MP_CUDA(cudaMemcpyAsync(hpo.data(), poff.get(), sizeof(int32_t) * (width + 1), cudaMemcpyDeviceToHost, s));
+        MP_CUDA(cudaStreamSynchronize(s));
+        size_t need = 0, need_state = 0;
+        for (int32_t i = 0; i < width; ++i) {
+          const int64_t np_i = hpo[i + 1] - hpo[i];
+          if (np_i == 0) continue;
+          need = std::max<size_t>(need, static_cast<size_t>(fm_node_smem(np_i, (hfo[i + 1] - hfo[i]) - np_i)));
+          need_state = std::max<size_t>(need_state, static_cast<size_t>(fm_node_smem(np_i, 0)));
+        }
+        fm_smem = std::min<size_t>(std::max(fm_smem, need), cap);
+        fm_hybrid = need > cap && need_state <= cap;
+      }
     }
     a.fm_smem_bytes = static_cast<int64_t>(fm_smem);
     // 32-bit move keys when every node fits (patch count and gain range)
-    int32_t hgb = 0;
-    {
+    // (a patch's quotient weight is at most the level's crossing entries)
+    int32_t hgb = nkeys;
+    if (nkeys >= 32768) {
       DevBuf<int32_t> gb(1, s);
       MP_CUDA(cudaMemsetAsync(gb, 0, 4, s));
       if (na_level > 0) MP_KERNEL(ctx, fm_gain_bound<<<grid_for(ctx, na_level), 256, 0, s>>>(na_level, plist, qoff, qw, gb));
