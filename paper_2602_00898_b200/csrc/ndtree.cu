@@ -211,6 +211,88 @@ __global__ void __launch_bounds__(1024) level_lists_small(int32_t P, int32_t wid
   }
   if (threadIdx.x == 0) cnt[1] = na, cnt[2] = na;
 }
+// Small levels (nkeys <= kSmallKeys, P <= kSmallP, width <= 1024): the
+// quotient CSR of the alive vertices (sort + run-length encoding of the
+// crossing keys), the per-node fifo offsets and the node-local adjacency in
+// ONE CTA -- the general path's CUB sort, run-length encoding, scans and four
+// small kernels, and its read-back of the run count, become one launch.
+constexpr int32_t kSmallKeys = 8192;
+__global__ void __launch_bounds__(1024) quotient_small(int32_t nk, const uint64_t* keys, int32_t P, int32_t width,
+                                                       int32_t na, const int32_t* plist, const int32_t* pnode,
+                                                       const int32_t* lidx, int32_t* qoff, int32_t* qnbr, int32_t* qw,
+                                                       int32_t* qloc, int64_t* fifo_off) {
+  extern __shared__ uint64_t qsm[];
+  uint64_t* k64 = qsm;                                           // N sorted keys
+  int32_t* rstart = reinterpret_cast<int32_t*>(k64 + kSmallKeys);  // run starts (U + 1)
+  int32_t* qdeg = rstart + kSmallKeys + 1;                       // P + 1
+  int32_t* ecnt = qdeg + kSmallP + 1;                            // width + 1
+  __shared__ int32_t sh[32], s_u;
+  int32_t N = 1;
+  while (N < nk) N <<= 1;
+  for (int32_t i = threadIdx.x; i < N; i += blockDim.x) k64[i] = i < nk ? keys[i] : ~0ull;
+  for (int32_t i = threadIdx.x; i <= P; i += blockDim.x) qdeg[i] = 0;
+  for (int32_t i = threadIdx.x; i <= width; i += blockDim.x) ecnt[i] = 0;
+  for (int32_t k = 2; k <= N; k <<= 1)
+    for (int32_t j = k >> 1; j > 0; j >>= 1) {
+      __syncthreads();
+      for (int32_t i = threadIdx.x; i < N; i += blockDim.x) {
+        const int32_t l = i ^ j;
+        if (l > i) {
+          const uint64_t x = k64[i], y = k64[l];
+          if (((i & k) == 0) == (x > y)) k64[i] = y, k64[l] = x;
+        }
+      }
+    }
+  __syncthreads();
+  // run-length encoding: run r starts at rstart[r]
+  int32_t run = 0;
+  for (int32_t b0 = 0; b0 < nk; b0 += blockDim.x) {
+    const int32_t i = b0 + threadIdx.x;
+    const int32_t f = (i < nk && (i == 0 || k64[i] != k64[i - 1])) ? 1 : 0;
+    int32_t tot;
+    const int32_t ex = block_excl_scan(f, sh, &tot);
+    if (f) {
+      const int32_t r = run + ex;
+      rstart[r] = i;
+      qnbr[r] = static_cast<int32_t>(k64[i] & 0xffffffffu);
+      atomicAdd(&qdeg[static_cast<int32_t>(k64[i] >> 32)], 1);
+    }
+    run += tot;
+  }
+  if (threadIdx.x == 0) s_u = run, rstart[run] = nk;
+  __syncthreads();
+  const int32_t U = s_u;
+  for (int32_t r = threadIdx.x; r < U; r += blockDim.x) {
+    qw[r] = rstart[r + 1] - rstart[r];
+    qloc[r] = lidx[qnbr[r]];
+  }
+  // qoff: exclusive scan of the patch degrees
+  run = 0;
+  for (int32_t b0 = 0; b0 <= P; b0 += blockDim.x) {
+    const int32_t i = b0 + threadIdx.x;
+    const int32_t c = i < P ? qdeg[i] : 0;
+    int32_t tot;
+    const int32_t ex = block_excl_scan(c, sh, &tot);
+    if (i <= P) qoff[i] = run + ex;
+    run += tot;
+  }
+  __syncthreads();
+  // fifo slabs: a node's quotient entries + 1 per alive patch (partition.cpp:76-77)
+  for (int32_t i = threadIdx.x; i < na; i += blockDim.x) {
+    const int32_t q = plist[i];
+    atomicAdd(&ecnt[pnode[q]], qoff[q + 1] - qoff[q] + 1);
+  }
+  __syncthreads();
+  int64_t run64 = 0;
+  for (int32_t b0 = 0; b0 <= width; b0 += blockDim.x) {
+    const int32_t i = b0 + threadIdx.x;
+    const int32_t c = i < width ? ecnt[i] : 0;
+    int32_t tot;
+    const int32_t ex = block_excl_scan(c, sh, &tot);
+    if (i <= width) fifo_off[i] = run64 + ex;
+    run64 += tot;
+  }
+}
 // Crossing-edge keys among alive vertices of active nodes; both directions.
 __global__ void emit_crossing(LevelArgs a, uint64_t* keys, int32_t* count) {
   for (int32_t li = blockIdx.y; li < a.width; li += gridDim.y) {
@@ -1609,16 +1691,30 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     int32_t nkeys = 0;
     MP_CUDA(cudaMemcpyAsync(&nkeys, cnt.get() + 3, 4, cudaMemcpyDeviceToHost, s));
     MP_CUDA(cudaStreamSynchronize(s));
-    DevBuf<int32_t> qoff, qnbr, qw;
-    const int64_t U = quotient_from_keys(ctx, keys, nkeys, P, qoff, qnbr, qw);
+    DevBuf<int32_t> qoff, qnbr, qw, qloc;
+    int64_t U = 0;  // quotient entries (an upper bound on the small path: the key count)
+    const bool small_q = nkeys <= kSmallKeys && P <= kSmallP && width <= 1024;
+    if (small_q) {
+      U = nkeys;
+      qoff.alloc(P + 1, s);
+      qnbr.alloc(std::max<int64_t>(U, 1), s);
+      qw.alloc(std::max<int64_t>(U, 1), s);
+      qloc.alloc(std::max<int64_t>(U, 1), s);
+      const size_t qs = sizeof(uint64_t) * kSmallKeys + sizeof(int32_t) * (kSmallKeys + 1 + kSmallP + 1 + 1025);
+      allow_max_smem(quotient_small, ctx.device);
+      MP_KERNEL(ctx, quotient_small<<<1, 1024, qs, s>>>(nkeys, keys, P, width, na_level, plist, pnode, lidx, qoff, qnbr,
+                                                        qw, qloc, fifo_off));
+    } else {
+      U = quotient_from_keys(ctx, keys, nkeys, P, qoff, qnbr, qw);
+    }
     a.qoff = qoff, a.qnbr = qnbr, a.qw = qw;
     // fifo slab per node: every push follows a directed quotient entry of the
     // node, so its entries + 1 bound the pushes (partition.cpp:76-77)
-    DevBuf<int64_t> ecnt(width + 1, s);
-    MP_CUDA(cudaMemsetAsync(ecnt, 0, sizeof(int64_t) * (width + 1), s));
-    if (na_level > 0)
-      MP_KERNEL(ctx, node_edge_count<<<grid_for(ctx, na_level), 256, 0, s>>>(na_level, plist, pnode, qoff, ecnt));
-    {
+    if (!small_q) {
+      DevBuf<int64_t> ecnt(width + 1, s);
+      MP_CUDA(cudaMemsetAsync(ecnt, 0, sizeof(int64_t) * (width + 1), s));
+      if (na_level > 0)
+        MP_KERNEL(ctx, node_edge_count<<<grid_for(ctx, na_level), 256, 0, s>>>(na_level, plist, pnode, qoff, ecnt));
       size_t tmp = 0;
       MP_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ecnt.get(), fifo_off.get(), width + 1, s));
       DevBuf<char> t(tmp, s);
@@ -1629,8 +1725,11 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     st.mark("level/quotient");
     // bipartition per node
     const int32_t maxnp = na_level;
-    DevBuf<int32_t> qloc(std::max<int64_t>(U, 1), s);
-    if (U > 0) MP_KERNEL(ctx, local_adjacency<<<grid_for(ctx, U), 256, 0, s>>>(static_cast<int32_t>(U), qnbr, lidx, qloc));
+    if (!small_q) {
+      qloc.alloc(std::max<int64_t>(U, 1), s);
+      if (U > 0)
+        MP_KERNEL(ctx, local_adjacency<<<grid_for(ctx, U), 256, 0, s>>>(static_cast<int32_t>(U), qnbr, lidx, qloc));
+    }
     a.qloc = qloc;
     size_t fm_smem = 1024;
     bool fm_hybrid = false;  // a node whose state fits shared memory but whose adjacency does not
