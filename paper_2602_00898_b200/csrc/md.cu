@@ -25,7 +25,7 @@ namespace mp {
 namespace {
 
 constexpr int kMdThreads = 512;
-constexpr int32_t kSmemDegCap = 12 * 1024;  // nodes up to this size keep degrees in smem
+constexpr int32_t kSmemDegCap = 48 * 1024;  // nodes up to this size keep degrees in smem (C3's 39K-vertex leaves)
 constexpr uint32_t kInfDeg = 0xffffffffu;
 constexpr int32_t kMdDirtyCap = 1024;  // dirty blocks listed per pivot (more: recompute all)
 
@@ -85,7 +85,7 @@ __device__ __forceinline__ void md_node_global(const MdArgs& a, int32_t node) {
   uint32_t* deg = smem_deg ? sdeg_dyn : a.gdeg + vb;  // indexed by local id
 
   __shared__ uint64_t red[32];
-  __shared__ int32_t s_nb, s_cursor, s_half, s_need_compact, s_ndirty, s_dlist[kMdDirtyCap];
+  __shared__ int32_t s_nb, s_cursor, s_half, s_need_compact, s_ndirty, s_ip, s_dlist[kMdDirtyCap];
   const int64_t pbase = a.pool_off[node];
   const int64_t pcap = (a.pool_off[node + 1] - pbase) / 2;
 
@@ -113,7 +113,7 @@ __device__ __forceinline__ void md_node_global(const MdArgs& a, int32_t node) {
   // recomputed at the end of the pivot (blk / dirty bits in shared memory
   // after the degrees when they fit, else in the node's global slab)
   const int32_t nbk = (nv + 31) / 32, lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  const int64_t deg_bytes = smem_deg ? 4LL * kSmemDegCap : 0;
+  const int64_t deg_bytes = smem_deg ? ((4LL * nv + 7) & ~7LL) : 0;
   const bool blk_sm = deg_bytes + 8LL * nbk + 4LL * (nbk / 32 + 1) <= a.gsmem_bytes;
   uint64_t* blk = blk_sm ? reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(sdeg_dyn) + deg_bytes)
                          : a.gblk + (vb >> 5) + node;
@@ -192,23 +192,44 @@ __device__ __forceinline__ void md_node_global(const MdArgs& a, int32_t node) {
     }
     int32_t* half = a.pool + pbase + (s_half ? pcap : 0);
     int32_t* out = half + s_cursor;
-    // ---- reach set: variables of p plus boundaries of p's elements
-    for (int32_t i = threadIdx.x; i < np_adj; i += blockDim.x) {
-      const int32_t w = padj[i];
-      if (atomicExch(&a.vmark[w], tok) != tok) out[atomicAdd(&s_nb, 1)] = w;
-    }
-    for (int32_t ei = 0; ei < np_el; ++ei) {
-      const int32_t e = pel[ei];
-      const int32_t* bd = half + a.bptr[e];
-      const int32_t sz = a.bsz[e];
-      for (int32_t i = threadIdx.x; i < sz; i += blockDim.x) {
-        const int32_t w = bd[i];
+    // ---- reach set: variables of p plus boundaries of p's elements.  With
+    // at most one element the parts are disjoint and duplicate-free (adj(p)
+    // lost that element's boundary when it formed; p appears in it once), so
+    // they are copied with plain stores and p is swapped out after the
+    // member updates; several elements deduplicate through the marks.
+    const bool simple = np_el <= 1;
+    int32_t ptotal = 0;
+    if (simple) {
+      const int32_t e1 = np_el ? pel[0] : 0;
+      const int32_t* bd = half + (np_el ? a.bptr[e1] : 0);
+      const int32_t sz = np_el ? a.bsz[e1] : 0;
+      ptotal = np_adj + sz;
+      for (int32_t i = threadIdx.x; i < ptotal; i += blockDim.x) {
+        const int32_t w = i < np_adj ? padj[i] : bd[i - np_adj];
+        out[i] = w;
+        if (w == p) s_ip = i;
+        else a.vmark[w] = tok;
+      }
+      if (threadIdx.x == 0) s_nb = ptotal - np_el;
+    } else {
+      for (int32_t i = threadIdx.x; i < np_adj; i += blockDim.x) {
+        const int32_t w = padj[i];
         if (atomicExch(&a.vmark[w], tok) != tok) out[atomicAdd(&s_nb, 1)] = w;
+      }
+      for (int32_t ei = 0; ei < np_el; ++ei) {
+        const int32_t e = pel[ei];
+        const int32_t* bd = half + a.bptr[e];
+        const int32_t sz = a.bsz[e];
+        for (int32_t i = threadIdx.x; i < sz; i += blockDim.x) {
+          const int32_t w = bd[i];
+          if (atomicExch(&a.vmark[w], tok) != tok) out[atomicAdd(&s_nb, 1)] = w;
+        }
       }
     }
     for (int32_t ei = threadIdx.x; ei < np_el; ei += blockDim.x) a.emark[pel[ei]] = tok;
     __syncthreads();
     const int32_t nb = s_nb;
+    const int32_t nscan = simple ? ptotal : nb;  // out entries to visit (p among them when simple)
     if (threadIdx.x == 0) {
       a.bptr[p] = s_cursor;
       a.bsz[p] = nb;
@@ -220,8 +241,9 @@ __device__ __forceinline__ void md_node_global(const MdArgs& a, int32_t node) {
     // absorbed elements' boundaries are dropped after the member updates
     __syncthreads();
     // ---- update every boundary member (elimination.cpp:75-83)
-    for (int32_t i = threadIdx.x; i < nb; i += blockDim.x) {
+    for (int32_t i = threadIdx.x; i < nscan; i += blockDim.x) {
       const int32_t w = out[i];
+      if (w == p) continue;
       const int32_t o = a.g.off[w];
       int32_t* wa = a.adj + o;
       int32_t c = 0;
@@ -267,6 +289,8 @@ __device__ __forceinline__ void md_node_global(const MdArgs& a, int32_t node) {
         rekey(lw, od, nd);
       }
     }
+    __syncthreads();
+    if (simple && np_el && threadIdx.x == 0 && s_ip != ptotal - 1) out[s_ip] = out[ptotal - 1];  // p's boundary without p
     __syncthreads();
     for (int32_t ei = threadIdx.x; ei < np_el; ei += blockDim.x) a.bsz[pel[ei]] = 0;
     if (threadIdx.x == 0) {
@@ -328,6 +352,13 @@ __device__ __forceinline__ void md_node_global(const MdArgs& a, int32_t node) {
     }
     __syncthreads();
   }
+}
+
+// md_kernel's dynamic shared memory for nodes up to nv vertices: their
+// degrees (when nv <= kSmemDegCap) plus room for the block minima and
+// dirty bits (16 KB covers 2K blocks = 64K vertices).
+inline size_t md_global_smem(int64_t nv) {
+  return sizeof(uint32_t) * static_cast<size_t>(std::min<int64_t>(std::max<int64_t>(nv, 1), kSmemDegCap)) + 16384 + 512;
 }
 
 __global__ void __launch_bounds__(kMdThreads) md_kernel(MdArgs a) {
@@ -776,7 +807,7 @@ void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t L, const int
   a.pool_off = pool_off, a.order_ws = order, a.local_perm = local_perm, a.overflow = overflow;
   a.node_mask = node_mask;
   // md_kernel: degrees (kSmemDegCap) + block minima / dirty bits of nodes up to 64K vertices
-  const size_t smem = sizeof(uint32_t) * kSmemDegCap + 16384 + 512;
+  const size_t smem = md_global_smem(kMdSmemMaxNv);
   DevBuf<uint64_t> gblk(static_cast<size_t>(n >> 5) + nn + 1, s);
   DevBuf<uint32_t> gdbits(static_cast<size_t>(n >> 10) + 2LL * nn + 2, s);
   a.gblk = gblk, a.gdbits = gdbits;
@@ -809,7 +840,12 @@ void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t L, const int
       MP_CUDA(cudaStreamWaitEvent(ctx.aux_stream, ctx.fork_ev[0], 0));
       MdArgs ab = a;
       ab.sched = dsched;
-      MP_KERNEL(ctx, md_kernel<<<big, kMdThreads, smem, ctx.aux_stream>>>(ab));
+      // degrees of the largest such node in shared memory, plus block minima
+      int64_t maxnv = 0;
+      for (int32_t i = 0; i < big; ++i) maxnv = std::max<int64_t>(maxnv, hoff[sched[i] + 1] - hoff[sched[i]]);
+      const size_t bsmem = md_global_smem(maxnv);
+      ab.gsmem_bytes = static_cast<int64_t>(bsmem);
+      MP_KERNEL(ctx, md_kernel<<<big, kMdThreads, bsmem, ctx.aux_stream>>>(ab));
       MP_CUDA(cudaEventRecord(ctx.fork_ev[1], ctx.aux_stream));
     }
     if (ns > big) {
@@ -850,7 +886,13 @@ void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t L, const int
     }
     if (big > 0) MP_CUDA(cudaStreamWaitEvent(s, ctx.fork_ev[1], 0));
   } else {
-    MP_KERNEL(ctx, md_kernel<<<nn, kMdThreads, smem, s>>>(a));
+    std::vector<int32_t> hoff(nn + 1);
+    MP_CUDA(cudaMemcpyAsync(hoff.data(), node_offsets, sizeof(int32_t) * (nn + 1), cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+    int64_t maxnv = 0;
+    for (int32_t i = 0; i < nn; ++i) maxnv = std::max<int64_t>(maxnv, hoff[i + 1] - hoff[i]);
+    a.gsmem_bytes = static_cast<int64_t>(md_global_smem(maxnv));
+    MP_KERNEL(ctx, md_kernel<<<nn, kMdThreads, static_cast<size_t>(a.gsmem_bytes), s>>>(a));
   }
   ctx.ktime_end(kt__);
   int32_t h_over = 0;
