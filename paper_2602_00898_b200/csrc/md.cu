@@ -240,41 +240,59 @@ __device__ __forceinline__ void md_node_global(const MdArgs& a, int32_t node) {
     }
     // absorbed elements' boundaries are dropped after the member updates
     __syncthreads();
-    // ---- update every boundary member (elimination.cpp:75-83)
+    // ---- update every boundary member (elimination.cpp:75-83).  The
+    // member's scalars, then the first eight slots of BOTH its lists, then
+    // their marks and element sizes are loaded as three waves of independent
+    // L2 requests (the stores of the in-place compactions come after them);
+    // longer lists continue eight slots at a time.
     for (int32_t i = threadIdx.x; i < nscan; i += blockDim.x) {
       const int32_t w = out[i];
       if (w == p) continue;
       const int32_t o = a.g.off[w];
+      const int32_t na = a.nadj[w], ne = a.nel[w];
+      const int32_t lw = a.mode == 0 ? a.local_of[w] : 0;
       int32_t* wa = a.adj + o;
+      int32_t* we = a.el + o;
+      int32_t xs[8], es[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) xs[q] = q < na ? wa[q] : -1, es[q] = q < ne ? we[q] : -1;
+      int32_t mx[8], me[8], bs[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        mx[q] = xs[q] >= 0 ? a.vmark[xs[q]] : tok;
+        me[q] = es[q] >= 0 ? a.emark[es[q]] : tok;
+        bs[q] = es[q] >= 0 ? a.bsz[es[q]] : 0;
+      }
       int32_t c = 0;
-      const int32_t na = a.nadj[w];
-      // in-place compaction with 8 reads in flight ahead of the writes
-      for (int32_t j0 = 0; j0 < na; j0 += 8) {
-        int32_t xs[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (mx[q] != tok) wa[c++] = xs[q];
+      for (int32_t j0 = 8; j0 < na; j0 += 8) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) xs[q] = j0 + q < na ? wa[j0 + q] : -1;
-        int32_t mk[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) mk[q] = xs[q] >= 0 ? a.vmark[xs[q]] : tok;
+        for (int q = 0; q < 8; ++q) mx[q] = xs[q] >= 0 ? a.vmark[xs[q]] : tok;
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          if (mk[q] != tok) wa[c++] = xs[q];
+          if (mx[q] != tok) wa[c++] = xs[q];
       }
       a.nadj[w] = c;
-      int32_t* we = a.el + o;
       int32_t ce = 0;
-      const int32_t ne = a.nel[w];
       int64_t d = c;
-      for (int32_t j0 = 0; j0 < ne; j0 += 8) {
-        int32_t es[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (me[q] != tok) {
+          we[ce++] = es[q];
+          d += bs[q];
+        }
+      for (int32_t j0 = 8; j0 < ne; j0 += 8) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) es[q] = j0 + q < ne ? we[j0 + q] : -1;
-        int32_t mk[8], bs[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) mk[q] = es[q] >= 0 ? a.emark[es[q]] : tok, bs[q] = es[q] >= 0 ? a.bsz[es[q]] : 0;
+        for (int q = 0; q < 8; ++q) me[q] = es[q] >= 0 ? a.emark[es[q]] : tok, bs[q] = es[q] >= 0 ? a.bsz[es[q]] : 0;
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          if (mk[q] != tok) {
+          if (me[q] != tok) {
             we[ce++] = es[q];
             d += bs[q];
           }
@@ -283,7 +301,6 @@ __device__ __forceinline__ void md_node_global(const MdArgs& a, int32_t node) {
       d += nb;
       a.nel[w] = ce;
       if (a.mode == 0) {
-        const int32_t lw = a.local_of[w];
         const uint32_t od = deg[lw], nd = md_key_deg(d);
         deg[lw] = nd;
         rekey(lw, od, nd);
