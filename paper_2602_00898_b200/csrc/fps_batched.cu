@@ -843,33 +843,41 @@ __global__ void __launch_bounds__(kThreads, 1) fps_cluster_phase(BatchArgs a, in
     int64_t my_slot = -1;  // this lane's reserved queue slot (kept until its item arrives)
     int32_t u = -1, du = 0;  // this lane's item
     for (int idle = 0;;) {
-      // idle lanes reserve a queue slot (once) and poll it without blocking
-      const uint32_t needy = __ballot_sync(0xffffffffu, u < 0 && my_slot < 0);
-      if (needy) {
-        int32_t h0 = 0;
-        if (lane == 0) h0 = atomicAdd(&qc[kQHead], __popc(needy));
-        h0 = __shfl_sync(0xffffffffu, h0, 0);
-        if (u < 0 && my_slot < 0) my_slot = static_cast<int64_t>(h0) + __popc(needy & ((1u << lane) - 1));
-      }
-      if (__any_sync(0xffffffffu, my_slot >= qcap)) {
-        if (lane == 0) atomicExch(&a.ctl[12], 1), atomicExch(&qc[kQPend], 0);  // abort: the main kernel redoes FPS
-        break;
-      }
-      if (u < 0 && my_slot >= 0) {
-        const uint64_t it = *reinterpret_cast<volatile uint64_t*>(&q[my_slot]);
-        if (it != ~0ull) u = static_cast<int32_t>(static_cast<uint32_t>(it)), du = static_cast<int32_t>(it >> 32), my_slot = -1;
-      }
-      const bool have = u >= 0;
+      // Lanes holding a queue reservation poll it; the load is issued here and
+      // consumed after this step's relaxations (a working warp does not wait
+      // for it).  Only a warp without any item reserves new slots, so a
+      // working warp keeps the vertices it lowers in its own lanes (its front
+      // grows locally; the excess is spilled) and its step is one ELL row
+      // load plus the atomicMin round trip -- no queue round trips.
+      uint64_t pv = ~0ull;
+      if (u < 0 && my_slot >= 0) pv = *reinterpret_cast<volatile uint64_t*>(&q[my_slot]);
+      bool have = u >= 0;
       if (!__any_sync(0xffffffffu, have)) {
-        int32_t pend = lane == 0 ? *reinterpret_cast<volatile int32_t*>(&qc[kQPend]) : 0;
-        pend = __shfl_sync(0xffffffffu, pend, 0);  // one verdict per warp
-        if (pend == 0) break;                       // no work anywhere: region complete
-        if (++idle > (1 << 22)) {                   // watchdog (never expected): fall back
-          if (lane == 0) atomicExch(&a.ctl[12], 1), atomicExch(&qc[kQPend], 0);
+        if (pv != ~0ull) u = static_cast<int32_t>(static_cast<uint32_t>(pv)), du = static_cast<int32_t>(pv >> 32), my_slot = -1;
+        pv = ~0ull;
+        const uint32_t needy = __ballot_sync(0xffffffffu, u < 0 && my_slot < 0);
+        if (needy) {
+          int32_t h0 = 0;
+          if (lane == 0) h0 = atomicAdd(&qc[kQHead], __popc(needy));
+          h0 = __shfl_sync(0xffffffffu, h0, 0);
+          if (u < 0 && my_slot < 0) my_slot = static_cast<int64_t>(h0) + __popc(needy & ((1u << lane) - 1));
+        }
+        if (__any_sync(0xffffffffu, my_slot >= qcap)) {
+          if (lane == 0) atomicExch(&a.ctl[12], 1), atomicExch(&qc[kQPend], 0);  // abort: the main kernel redoes FPS
           break;
         }
-        if (idle > 2) __nanosleep(min(64 * idle, kBackoffNs));  // back off: idle polls must not starve the atomics
-        continue;
+        have = u >= 0;
+        if (!__any_sync(0xffffffffu, have)) {
+          int32_t pend = lane == 0 ? *reinterpret_cast<volatile int32_t*>(&qc[kQPend]) : 0;
+          pend = __shfl_sync(0xffffffffu, pend, 0);  // one verdict per warp
+          if (pend == 0) break;                       // no work anywhere: region complete
+          if (++idle > (1 << 22)) {                   // watchdog (never expected): fall back
+            if (lane == 0) atomicExch(&a.ctl[12], 1), atomicExch(&qc[kQPend], 0);
+            break;
+          }
+          if (idle > 2) __nanosleep(min(64 * idle, kBackoffNs));  // back off: idle polls must not starve the atomics
+          continue;
+        }
       }
       idle = 0;
       // relax the items' neighbours
@@ -943,6 +951,8 @@ __global__ void __launch_bounds__(kThreads, 1) fps_cluster_phase(BatchArgs a, in
           else atomicExch(&a.ctl[12], 1);
         }
       }
+      // a reserved slot that was filled: its item is this lane's next one
+      if (pv != ~0ull) u = static_cast<int32_t>(static_cast<uint32_t>(pv)), du = static_cast<int32_t>(pv >> 32), my_slot = -1;
       // (same-address atomics of one thread are ordered: the increment above
       //  lands before this decrement, so pending never reads 0 early)
       if (lane == 0 && nproc) atomicSub(&qc[kQPend], nproc);
