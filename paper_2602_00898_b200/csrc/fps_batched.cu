@@ -880,21 +880,25 @@ __global__ void __launch_bounds__(kThreads, 1) fps_cluster_phase(BatchArgs a, in
         }
       }
       idle = 0;
-      // relax the items' neighbours
-      int32_t np = 0;
-      uint64_t mine[8];
+      // relax the items' neighbours (the lowered ones as a slot mask: the
+      // candidates stay in registers, no local-memory array)
+      uint32_t lmask = 0;
+      int32_t cand[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) cand[k] = -1;
+      const uint64_t hi = static_cast<uint64_t>(du + 1) << 32;
       if (have) {
         const int32_t nd = du + 1;
         const int4* row = reinterpret_cast<const int4*>(a.ell + static_cast<int64_t>(u) * 8);
         const int4 r0 = row[0], r1 = row[1];
-        const int32_t cand[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+        cand[0] = r0.x, cand[1] = r0.y, cand[2] = r0.z, cand[3] = r0.w;
+        cand[4] = r1.x, cand[5] = r1.y, cand[6] = r1.z, cand[7] = r1.w;
         int32_t old[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) old[k] = cand[k] >= 0 ? atomicMin(&a.dist[cand[k]], nd) : 0;
-        const uint64_t hi = static_cast<uint64_t>(nd) << 32;
 #pragma unroll
         for (int k = 0; k < 8; ++k)
-          if (cand[k] >= 0 && old[k] > nd) mine[np++] = hi | static_cast<uint32_t>(cand[k]);
+          if (cand[k] >= 0 && old[k] > nd) lmask |= 1u << k;
         scans += a.g.off[u + 1] - a.g.off[u];
         if (cand[7] < -1)  // CSR tail of a vertex with more than 8 neighbours: straight to the queue
           for (int32_t j = -cand[7] - 2; j < a.g.off[u + 1]; ++j) {
@@ -911,6 +915,7 @@ __global__ void __launch_bounds__(kThreads, 1) fps_cluster_phase(BatchArgs a, in
           }
       }
       // stage the lowered vertices warp-wide
+      const int32_t np = __popc(lmask);
       int32_t inc = np;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -919,7 +924,9 @@ __global__ void __launch_bounds__(kThreads, 1) fps_cluster_phase(BatchArgs a, in
       }
       const int32_t tot = __shfl_sync(0xffffffffu, inc, 31);
       const int32_t nproc = __popc(__ballot_sync(0xffffffffu, have));
-      for (int k = 0; k < np; ++k) stage[inc - np + k] = mine[k];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if ((lmask >> k) & 1u) stage[inc - np + __popc(lmask & ((1u << k) - 1))] = hi | static_cast<uint32_t>(cand[k]);
       u = -1;
       // lanes without a reservation take the first items; the rest is spilled
       const uint32_t freel = __ballot_sync(0xffffffffu, my_slot < 0);
