@@ -15,6 +15,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "mp_context.h"
@@ -406,24 +407,59 @@ __device__ __forceinline__ bool fm_imb_less(int32_t a0, int32_t a1, int32_t b0, 
   }
 }
 
+// Patch status views.  get() / set() speak the wide format of fm_st (side |
+// flag << 8 | slot << 16) whatever the storage.  Wide: one u32 per patch
+// (bytes side, lock / visited flag, cache slot).  Compact: one u16 (byte 0 =
+// side | flag << 1, byte 1 = slot) -- with 16-bit gains, 4 B of shared state
+// per patch, so nodes up to ~54K patches (C3's root) keep the state on chip.
+struct FmStWide {
+  uint32_t* p;
+  __device__ __forceinline__ uint32_t get(int32_t i) const { return p[i]; }
+  __device__ __forceinline__ void set(int32_t i, uint32_t v) const { p[i] = v; }
+  __device__ __forceinline__ uint32_t side(int32_t i) const { return reinterpret_cast<const uint8_t*>(p)[4 * i]; }
+  __device__ __forceinline__ uint32_t flag(int32_t i) const { return reinterpret_cast<const uint8_t*>(p)[4 * i + 1]; }
+  __device__ __forceinline__ void set_slot(int32_t i, uint32_t sl) const {
+    reinterpret_cast<uint8_t*>(p)[4 * i + 2] = static_cast<uint8_t>(sl);
+  }
+  __device__ __forceinline__ void flip(int32_t i) const { reinterpret_cast<uint8_t*>(p)[4 * i] ^= 1; }
+};
+struct FmStCompact {
+  uint16_t* p;
+  __device__ __forceinline__ uint32_t get(int32_t i) const {
+    const uint32_t v = p[i];
+    return (v & 1u) | (((v >> 1) & 1u) << 8) | ((v >> 8) << 16);
+  }
+  __device__ __forceinline__ void set(int32_t i, uint32_t v) const {
+    p[i] = static_cast<uint16_t>((v & 1u) | (((v >> 8) & 1u) << 1) | (((v >> 16) & 0xffu) << 8));
+  }
+  __device__ __forceinline__ uint32_t side(int32_t i) const { return reinterpret_cast<const uint8_t*>(p)[2 * i] & 1u; }
+  __device__ __forceinline__ uint32_t flag(int32_t i) const {
+    return (reinterpret_cast<const uint8_t*>(p)[2 * i] >> 1) & 1u;
+  }
+  __device__ __forceinline__ void set_slot(int32_t i, uint32_t sl) const {
+    reinterpret_cast<uint8_t*>(p)[2 * i + 1] = static_cast<uint8_t>(sl);
+  }
+  __device__ __forceinline__ void flip(int32_t i) const { reinterpret_cast<uint8_t*>(p)[2 * i] ^= 1; }
+};
+
 // CTA-wide: refill the side-t cache with the 32 largest keys of the unlocked
 // side-t patches; B[t] = the 33rd largest (0 when there are at most 32).
 // The threshold is an MSD radix select over the bits below the common prefix
 // of the largest and smallest candidate key.
-template <class K, class G, class W>
-__device__ __forceinline__ void fm_refill(int32_t t, int32_t np, G gain, W st, K (*ck)[32], int32_t (*cp)[32], K* B, int32_t* hist, uint64_t* red,
+template <class K, class G, class SV>
+__device__ __forceinline__ void fm_refill(int32_t t, int32_t np, G gain, SV st, K (*ck)[32], int32_t (*cp)[32], K* B, int32_t* hist, uint64_t* red,
                           int32_t* sh) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if (threadIdx.x < 32) {
     const int32_t p = cp[t][threadIdx.x];
-    if (p >= 0) reinterpret_cast<uint8_t*>(st)[4 * p + 2] = kNoSlot;
+    if (p >= 0) st.set_slot(p, kNoSlot);
     cp[t][threadIdx.x] = -1;
     ck[t][threadIdx.x] = 0;
   }
   int64_t c = 0;
   uint64_t mx = 0, mn = ~0ull;
   for (int32_t i = threadIdx.x; i < np; i += blockDim.x)
-    if ((st[i] & 0xffffu) == static_cast<uint32_t>(t)) {  // unlocked, side t
+    if ((st.get(i) & 0xffffu) == static_cast<uint32_t>(t)) {  // unlocked, side t
       const uint64_t k = FmKey<K>::make(gain[i], i);
       ++c, mx = k > mx ? k : mx, mn = k < mn ? k : mn;
     }
@@ -445,7 +481,7 @@ __device__ __forceinline__ void fm_refill(int32_t t, int32_t np, G gain, W st, K
       for (int32_t i0 = wid * 32; i0 < np; i0 += nw * 32) {
         const int32_t i = i0 + lane;
         int32_t d = -1;
-        if (i < np && (st[i] & 0xffffu) == static_cast<uint32_t>(t)) {
+        if (i < np && (st.get(i) & 0xffffu) == static_cast<uint32_t>(t)) {
           const uint64_t k = FmKey<K>::make(gain[i], i);
           if ((k & pmask) == prefix) d = static_cast<int32_t>((k >> lo) & static_cast<uint64_t>(nbins - 1));
         }
@@ -488,12 +524,12 @@ __device__ __forceinline__ void fm_refill(int32_t t, int32_t np, G gain, W st, K
   if (threadIdx.x == 0) sh[2] = 0;
   __syncthreads();
   for (int32_t i = threadIdx.x; i < np; i += blockDim.x)
-    if ((st[i] & 0xffffu) == static_cast<uint32_t>(t)) {
+    if ((st.get(i) & 0xffffu) == static_cast<uint32_t>(t)) {
       const K k = FmKey<K>::make(gain[i], i);
       if (k > T) {
         const int32_t slot = atomicAdd(&sh[2], 1);
         ck[t][slot] = k, cp[t][slot] = i;
-        reinterpret_cast<uint8_t*>(st)[4 * i + 2] = static_cast<uint8_t>((t << 5) | slot);
+        st.set_slot(i, (t << 5) | slot);
       }
     }
   if (threadIdx.x == 0) B[t] = static_cast<K>(T);
@@ -505,34 +541,45 @@ __device__ __forceinline__ void fm_refill(int32_t t, int32_t np, G gain, W st, K
 // adjacency (local id << 16 | weight) is in shared memory too, else it is
 // read from qloc / qw (read-only, L2) -- the middle case keeps nodes whose
 // adjacency does not fit (C5 root) on shared-memory state.
-template <class K, bool EXACT, bool SM, bool SMA = SM>
+// SMC: compact state -- 16-bit gains and status in shared memory, weights and
+// adjacency bounds in global scratch, adjacency from L2 (C3's root and level
+// 1: 39K / 19K patches, whose 20-byte state does not fit).
+template <class K, bool EXACT, bool SM, bool SMA = SM, bool SMC = false>
 __device__ __forceinline__ void fm_node(const LevelArgs& a, int32_t li, int32_t pbeg, int32_t np) {
   static_assert(SM || !SMA, "packed adjacency in shared memory needs the shared state layout");
+  static_assert(!(SM && SMC), "one state layout");
+  using G = typename std::conditional<SMC, int16_t, int32_t>::type;
+  using SV = typename std::conditional<SMC, FmStCompact, FmStWide>::type;
   const int32_t* pl = a.plist + pbeg;
   int32_t* fifo = a.fm_fifo + a.fm_fifo_off[li];
   int32_t* moves = a.fm_moves + pbeg;
   extern __shared__ uint64_t fm_sm64_[];
   int32_t* w;
-  int32_t* gain;
+  G* gain;
   int2* abe;
-  uint32_t* st;  // status words (fm_st)
+  SV stv;  // status (fm_st)
   uint32_t* packed = nullptr;
   if constexpr (SM) {  // byte offsets from the shared base (keeps the address space visible)
     char* base = reinterpret_cast<char*>(fm_sm64_);
     w = reinterpret_cast<int32_t*>(base);
-    gain = w + np;
+    gain = reinterpret_cast<G*>(w + np);
     abe = reinterpret_cast<int2*>(base + 8LL * np);
-    st = reinterpret_cast<uint32_t*>(base + 16LL * np);
+    stv.p = reinterpret_cast<uint32_t*>(base + 16LL * np);
     if constexpr (SMA) packed = reinterpret_cast<uint32_t*>(base + ((20LL * np + 15) & ~15LL));
+  } else if constexpr (SMC) {
+    char* base = reinterpret_cast<char*>(fm_sm64_);
+    w = a.fm_w + pbeg;
+    abe = reinterpret_cast<int2*>(a.fm_ab) + pbeg;
+    gain = reinterpret_cast<G*>(base);
+    stv.p = reinterpret_cast<uint16_t*>(base + ((2LL * np + 15) & ~15LL));
   } else {
     w = a.fm_w + pbeg;
     gain = a.fm_gain + pbeg;
     abe = reinterpret_cast<int2*>(a.fm_ab) + pbeg;
-    st = reinterpret_cast<uint32_t*>(a.fm_side) + pbeg;
+    stv.p = reinterpret_cast<uint32_t*>(a.fm_side) + pbeg;
   }
-  uint8_t* stb = reinterpret_cast<uint8_t*>(st);
-  auto side = [&](int32_t i) -> uint32_t { return stb[4 * i]; };
-  auto flag = [&](int32_t i) -> uint32_t { return stb[4 * i + 1]; };
+  auto side = [&](int32_t i) -> uint32_t { return stv.side(i); };
+  auto flag = [&](int32_t i) -> uint32_t { return stv.flag(i); };
   auto A_nb = [&](int32_t j) -> int32_t {
     if constexpr (SMA) return static_cast<int32_t>(packed[j] >> 16);
     else return __ldg(&a.qloc[j]);
@@ -555,7 +602,7 @@ __device__ __forceinline__ void fm_node(const LevelArgs& a, int32_t li, int32_t 
     const int32_t p = pl[i];
     w[i] = a.pw[p];
     abe[i] = make_int2(a.qoff[p], a.qoff[p + 1]);
-    st[i] = fm_st(1, 0, kNoSlot);  // right (partition.cpp:34)
+    stv.set(i, fm_st(1, 0, kNoSlot));  // right (partition.cpp:34)
     tot += w[i];
   }
   tot = block_sum_i64(tot, reinterpret_cast<int64_t*>(red));
@@ -604,7 +651,7 @@ __device__ __forceinline__ void fm_node(const LevelArgs& a, int32_t li, int32_t 
           }
         u = static_cast<int32_t>(key_max_id(warp_max_u64(best)));
       }
-      if (lane == 0) st[u] = fm_st(0, 1, kNoSlot);
+      if (lane == 0) stv.set(u, fm_st(0, 1, kNoSlot));
       left += w[u];
       __syncwarp();
       const int2 e = abe[u];
@@ -653,7 +700,7 @@ __device__ __forceinline__ void fm_node(const LevelArgs& a, int32_t li, int32_t 
     }
     __syncthreads();
     for (int32_t i = threadIdx.x; i < np; i += blockDim.x) {
-      st[i] = fm_st(side(i), 0, kNoSlot);  // unlocked
+      stv.set(i, fm_st(side(i), 0, kNoSlot));  // unlocked
     }
     if (threadIdx.x < 64) s_cp[threadIdx.x >> 5][threadIdx.x & 31] = -1;
     if (threadIdx.x == 0) {
@@ -666,8 +713,8 @@ __device__ __forceinline__ void fm_node(const LevelArgs& a, int32_t li, int32_t 
     __syncthreads();
     for (;;) {
       const int32_t need = s_need;
-      if (need & 1) fm_refill<K>(0, np, gain, st, s_ck, s_cp, s_B, hist, red, sh);
-      if (need & 2) fm_refill<K>(1, np, gain, st, s_ck, s_cp, s_B, hist, red, sh);
+      if (need & 1) fm_refill<K>(0, np, gain, stv, s_ck, s_cp, s_B, hist, red, sh);
+      if (need & 2) fm_refill<K>(1, np, gain, stv, s_ck, s_cp, s_B, hist, red, sh);
       if (need & kFmExact) {  // the reference's own scan: max key over every feasible unlocked patch
         const int32_t sw0 = s_sw[0], sw1 = s_sw[1], H = max(sw0, sw1), L = min(sw0, sw1);
         uint64_t best = 0;
@@ -698,14 +745,20 @@ __device__ __forceinline__ void fm_node(const LevelArgs& a, int32_t li, int32_t 
         auto apply = [&](K kbest, int32_t sd) {
           const int32_t ch = FmKey<K>::id(kbest);
           const int2 e = abe[ch];
-          const int32_t wc = w[ch];
           const uint32_t own = __ballot_sync(0xffffffffu, (sd ? cp1 : cp0) == ch);
+          int32_t wc;
+          if constexpr (SM) {
+            wc = w[ch];
+          } else {  // global weights: the cached copy of the lane holding ch
+            const int32_t cwl = __shfl_sync(0xffffffffu, sd ? cw1 : cw0, own ? __ffs(own) - 1 : 0);
+            wc = own ? cwl : w[ch];
+          }
           if (own && lane == __ffs(own) - 1) {
             if (sd) cp1 = -1, ck1 = 0, cw1 = 0;
             else cp0 = -1, ck0 = 0, cw0 = 0;
           }
           if (lane == 0) {
-            st[ch] = fm_st(1 - sd, 1, kNoSlot);
+            stv.set(ch, fm_st(1 - sd, 1, kNoSlot));
             moves[nm] = ch;
           }
           ++nm;
@@ -723,7 +776,7 @@ __device__ __forceinline__ void fm_node(const LevelArgs& a, int32_t li, int32_t 
             if (j < e.y) {
               nb = A_nb(j);
               const int32_t wj = A_w(j);
-              const uint32_t sw = st[nb];
+              const uint32_t sw = stv.get(nb);
               if (!(sw & 0xff00u)) {  // unlocked
                 sn = static_cast<int32_t>(sw & 1u);
                 const int32_t g = gain[nb] + (sn == sc ? -2 * wj : 2 * wj);
@@ -760,13 +813,13 @@ __device__ __forceinline__ void fm_node(const LevelArgs& a, int32_t li, int32_t 
                 o = __ffs(__ballot_sync(0xffffffffu, ct == mn)) - 1;
                 if (t) B1 = max(B1, mn);
                 else B0 = max(B0, mn);
-                if (lane == o) stb[4 * (t ? cp1 : cp0) + 2] = kNoSlot;
+                if (lane == o) stv.set_slot(t ? cp1 : cp0, kNoSlot);
               }
               if (lane == o) {
                 const int32_t wq = w[nbp];
                 if (t) ck1 = nbk, cp1 = nbp, cw1 = wq;
                 else ck0 = nbk, cp0 = nbp, cw0 = wq;
-                stb[4 * nbp + 2] = static_cast<uint8_t>((t << 5) | o);
+                stv.set_slot(nbp, (t << 5) | o);
               }
             }
             __syncwarp();
@@ -817,7 +870,7 @@ __device__ __forceinline__ void fm_node(const LevelArgs& a, int32_t li, int32_t 
     }
     const int32_t nm = s_nm, bl = s_best_len;
     total_moves += nm;
-    for (int32_t m = bl + threadIdx.x; m < nm; m += blockDim.x) stb[4 * moves[m]] ^= 1;
+    for (int32_t m = bl + threadIdx.x; m < nm; m += blockDim.x) stv.flip(moves[m]);
     __syncthreads();
     if (threadIdx.x == 0) {  // the state after the best prefix (partition.cpp:150-156)
       s_cut = s_best_cut;
@@ -839,13 +892,17 @@ __device__ __forceinline__ void fm_node(const LevelArgs& a, int32_t li, int32_t 
 __host__ __device__ inline int64_t fm_node_smem(int64_t np, int64_t entries) {
   return ((20 * np + 15) & ~int64_t(15)) + 4 * entries + 16;
 }
+// Shared-memory bytes of a node's compact state (fm_node<SMC>).
+__host__ __device__ inline int64_t fm_node_smem_compact(int64_t np) {
+  return 2 * ((2 * np + 15) & ~int64_t(15)) + 16;
+}
 
 // EXACT: integer feasibility (n < 2^26).  32-bit keys imply < 65536 patches
 // and edge weights < 32768, so a node whose state fits uses the packed
 // shared-memory layout; 64-bit-key nodes always use the global layout.
 // HYB: the level has a node whose adjacency does not fit but whose state
-// does (a separate instantiation, so levels without one keep the smaller
-// kernel).
+// does, or whose wide state does not fit but whose compact state does (a
+// separate instantiation, so levels without one keep the smaller kernel).
 template <class K, bool EXACT, bool HYB = false>
 __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
   const int32_t li = blockIdx.x;
@@ -860,6 +917,10 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
     if constexpr (HYB) {
       if (fm_node_smem(np, 0) <= a.fm_smem_bytes) {  // state only; adjacency from L2
         fm_node<K, EXACT, true, false>(a, li, pbeg, np);
+        return;
+      }
+      if (fm_node_smem_compact(np) <= a.fm_smem_bytes) {  // 16-bit gains (32-bit keys: |gain| < 32768)
+        fm_node<K, EXACT, false, false, true>(a, li, pbeg, np);
         return;
       }
     }
@@ -1753,15 +1814,17 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
         MP_CUDA(cudaMemcpyAsync(hfo.data(), fifo_off.get(), sizeof(int64_t) * (width + 1), cudaMemcpyDeviceToHost, s));
         MP_CUDA(cudaMemcpyAsync(hpo.data(), poff.get(), sizeof(int32_t) * (width + 1), cudaMemcpyDeviceToHost, s));
         MP_CUDA(cudaStreamSynchronize(s));
-        size_t need = 0, need_state = 0;
+        size_t need = 0;
+        bool partial = false;  // some node fits only as state or compact state
         for (int32_t i = 0; i < width; ++i) {
           const int64_t np_i = hpo[i + 1] - hpo[i];
           if (np_i == 0) continue;
-          need = std::max<size_t>(need, static_cast<size_t>(fm_node_smem(np_i, (hfo[i + 1] - hfo[i]) - np_i)));
-          need_state = std::max<size_t>(need_state, static_cast<size_t>(fm_node_smem(np_i, 0)));
+          const size_t full = static_cast<size_t>(fm_node_smem(np_i, (hfo[i + 1] - hfo[i]) - np_i));
+          need = std::max(need, full);
+          partial |= full > cap && static_cast<size_t>(fm_node_smem_compact(np_i)) <= cap;
         }
-        fm_smem = std::min<size_t>(std::max(fm_smem, need), cap);
-        fm_hybrid = need > cap && need_state <= cap;
+        fm_smem = partial ? cap : std::min<size_t>(std::max(fm_smem, need), cap);
+        fm_hybrid = partial;
       }
     }
     a.fm_smem_bytes = static_cast<int64_t>(fm_smem);

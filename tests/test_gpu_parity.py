@@ -372,16 +372,19 @@ def test_fm_state_in_smem_adjacency_in_l2(rows, patch):
     assert np.array_equal(res.perm.perm, o["perm"])
 
 
-@pytest.mark.parametrize("rows,patch", [(240, 4), (150, 2)])
-def test_fm_large_nodes_global_state(rows, patch):
-    """Root quotients beyond the shared-memory FM capacity (>10,240 patches,
-    C3 has 39,063) take the global-state path with super-block summaries."""
+@pytest.mark.parametrize("rows,patch,lo,hi", [(240, 4, 10240, 54000), (150, 2, 10240, 54000),
+                                              (540, 4, 58000, 65536), (600, 4, 65536, 1 << 30)])
+def test_fm_large_nodes_global_state(rows, patch, lo, hi):
+    """Root quotients beyond the wide shared-memory FM capacity (>10,240
+    patches; C3 has 39,063) keep 16-bit gains and 16-bit status in shared
+    memory (compact state) up to ~57K patches; beyond that the state is in
+    global memory (32-bit keys below 65,536 patches, 64-bit keys above)."""
     from oracle.oracle import Restatement
     R = Restatement()
     g = mp.mesh_to_graph(mp.make_grid_mesh(rows, rows))
     o = R.order(g, patch_size=patch)
     res = mp.order(g, patch_size=patch)
-    assert o["patch_count"] > 10240 and res.patch.patch_count == o["patch_count"]
+    assert lo < o["patch_count"] < hi and res.patch.patch_count == o["patch_count"]
     assert np.array_equal(res.tree.node_offsets, o["node_offsets"])
     assert np.array_equal(res.tree.vertices, o["node_vertices"])
     assert np.array_equal(res.perm.perm, o["perm"])

@@ -11,6 +11,8 @@ import paper_2602_00898_b200 as mp  # noqa: E402
 arg = sys.argv[1] if len(sys.argv) > 1 else "64"
 if arg.startswith("ico"):
     g = mp.mesh_to_graph(mp.make_icosphere_mesh(int(arg[3:])))
+elif arg.startswith("torus"):
+    g = mp.mesh_to_graph(mp.make_torus_mesh(2000, 5000))
 elif arg.startswith("rand"):
     g = mp.mesh_to_graph(mp.make_random_mesh(500, 500, seed=0))
 else:
