@@ -91,6 +91,7 @@ struct LevelArgs {
   uint8_t* vside;          // per vertex: side of its patch (this level)
   const int32_t* ell;      // n * 8 ELL adjacency
   int64_t fm_smem_bytes;   // dynamic shared memory of the FM launch
+  int32_t fm_w16;          // every patch weight of the level is below 65536 (fm_node<SMC, W16>)
   int32_t* fm_moves;
   const uint8_t* own_mask; // sharded build (mp_order_sharded): nodes this rank splits; NULL = all
   int32_t* ref_cnt;        // per level node: initial separator size (ref_init)
@@ -442,6 +443,30 @@ struct FmStCompact {
   __device__ __forceinline__ void flip(int32_t i) const { reinterpret_cast<uint8_t*>(p)[2 * i] ^= 1; }
 };
 
+// Byte status (compact layout with shared-memory weights): side (bit 0),
+// flag (bit 1), cache-slot valid (bit 2), slot lane (bits 3-7).  A valid
+// slot's side is always the patch's own side (side-t caches hold side-t
+// patches; a move locks its patch and drops its slot first), so the wide
+// slot side << 5 | lane is rebuilt from the side bit.
+struct FmStByte {
+  uint8_t* p;
+  __device__ __forceinline__ uint32_t get(int32_t i) const {
+    const uint32_t v = p[i];
+    const uint32_t sl = (v & 4u) ? (((v & 1u) << 5) | (v >> 3)) : 0xffu;
+    return (v & 1u) | (((v >> 1) & 1u) << 8) | (sl << 16);
+  }
+  __device__ __forceinline__ void set(int32_t i, uint32_t v) const {
+    const uint32_t sl = (v >> 16) & 0xffu;
+    p[i] = static_cast<uint8_t>((v & 1u) | (((v >> 8) & 1u) << 1) | (sl == 0xffu ? 0u : (4u | ((sl & 31u) << 3))));
+  }
+  __device__ __forceinline__ uint32_t side(int32_t i) const { return p[i] & 1u; }
+  __device__ __forceinline__ uint32_t flag(int32_t i) const { return (p[i] >> 1) & 1u; }
+  __device__ __forceinline__ void set_slot(int32_t i, uint32_t sl) const {
+    p[i] = static_cast<uint8_t>((p[i] & 3u) | (sl == 0xffu ? 0u : (4u | ((sl & 31u) << 3))));
+  }
+  __device__ __forceinline__ void flip(int32_t i) const { p[i] ^= 1u; }
+};
+
 // CTA-wide: refill the side-t cache with the 32 largest keys of the unlocked
 // side-t patches; B[t] = the 33rd largest (0 when there are at most 32).
 // The threshold is an MSD radix select over the bits below the common prefix
@@ -536,25 +561,71 @@ __device__ __forceinline__ void fm_refill(int32_t t, int32_t np, G gain, SV st, 
   __syncthreads();
 }
 
+// Prefetch helper for the layouts whose adjacency (and, SMC / global, the
+// weights) stay in global memory: warp 0 appends every patch that enters a
+// candidate cache to a shared ring; while warp 0 runs its move segment, warp 1
+// loads each such patch's adjacency bounds and prefetches its adjacency rows
+// and its neighbours' weights into L1 (the SM's L1 serves warp 0's later
+// loads: a cached candidate is usually moved within a few moves, and its move
+// then reads these lines).  Pure hints: a stale or overwritten ring entry is
+// still a valid patch index, and the loop leaves as soon as warp 0 posts the
+// segment's end (s_done == iter) -- or after a bounded idle spin.
+constexpr int32_t kFmPfRing = 256;
+__device__ __forceinline__ void prefetch_l1(const int32_t* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+template <bool WGLOBAL>
+__device__ __forceinline__ void fm_prefetch_helper(const int2* abe, const int32_t* qloc, const int32_t* qw,
+                                                   const int32_t* w, const int32_t* ring, const volatile int32_t* tailp,
+                                                   const volatile int32_t* donep, int32_t iter, int32_t& head) {
+  const int lane = threadIdx.x & 31;
+  for (int32_t spins = 0; spins < (1 << 26);) {  // idle polls: shared-memory loads on the helper's own SMSP
+    const int32_t tail = *tailp;
+    if (tail == head) {
+      if (*donep == iter) break;
+      ++spins;
+      continue;
+    }
+    const int32_t h = max(head, tail - kFmPfRing);
+    const int32_t cnt = min(tail - h, 32);
+    if (lane < cnt) {
+      const int32_t p = ring[(h + lane) & (kFmPfRing - 1)];
+      const int2 e = abe[p];
+      if (e.y > e.x) {
+        prefetch_l1(qloc + e.x), prefetch_l1(qloc + e.y - 1);
+        prefetch_l1(qw + e.x), prefetch_l1(qw + e.y - 1);
+        if constexpr (WGLOBAL)
+          for (int32_t j = e.x; j < e.y; ++j) prefetch_l1(w + __ldg(&qloc[j]));
+      }
+    }
+    head = h + cnt;
+  }
+}
+
 // One node's bipartition.  SM: the patch state (20 B per patch) lives in
 // shared memory, else in global scratch (plist layout).  SMA: the packed
 // adjacency (local id << 16 | weight) is in shared memory too, else it is
 // read from qloc / qw (read-only, L2) -- the middle case keeps nodes whose
 // adjacency does not fit (C5 root) on shared-memory state.
 // SMC: compact state -- 16-bit gains and status in shared memory, weights and
+// adjacency bounds in global scratch, adjacency from L2; with W16, 16-bit
+// weights join them and the status shrinks to one byte (5 B per patch: C3's
+// 39K-patch root keeps its weights on chip; the host checks they fit 16 bits).
 // adjacency bounds in global scratch, adjacency from L2 (C3's root and level
 // 1: 39K / 19K patches, whose 20-byte state does not fit).
-template <class K, bool EXACT, bool SM, bool SMA = SM, bool SMC = false>
+template <class K, bool EXACT, bool SM, bool SMA = SM, bool SMC = false, bool W16 = false>
 __device__ __forceinline__ void fm_node(const LevelArgs& a, int32_t li, int32_t pbeg, int32_t np) {
   static_assert(SM || !SMA, "packed adjacency in shared memory needs the shared state layout");
   static_assert(!(SM && SMC), "one state layout");
+  static_assert(SMC || !W16, "16-bit shared weights are a compact-layout variant");
   using G = typename std::conditional<SMC, int16_t, int32_t>::type;
-  using SV = typename std::conditional<SMC, FmStCompact, FmStWide>::type;
+  using SV = typename std::conditional<W16, FmStByte, typename std::conditional<SMC, FmStCompact, FmStWide>::type>::type;
+  using WT = typename std::conditional<W16, uint16_t, int32_t>::type;
   const int32_t* pl = a.plist + pbeg;
   int32_t* fifo = a.fm_fifo + a.fm_fifo_off[li];
   int32_t* moves = a.fm_moves + pbeg;
   extern __shared__ uint64_t fm_sm64_[];
-  int32_t* w;
+  WT* w;
   G* gain;
   int2* abe;
   SV stv;  // status (fm_st)
@@ -568,10 +639,16 @@ __device__ __forceinline__ void fm_node(const LevelArgs& a, int32_t li, int32_t 
     if constexpr (SMA) packed = reinterpret_cast<uint32_t*>(base + ((20LL * np + 15) & ~15LL));
   } else if constexpr (SMC) {
     char* base = reinterpret_cast<char*>(fm_sm64_);
-    w = a.fm_w + pbeg;
     abe = reinterpret_cast<int2*>(a.fm_ab) + pbeg;
     gain = reinterpret_cast<G*>(base);
-    stv.p = reinterpret_cast<uint16_t*>(base + ((2LL * np + 15) & ~15LL));
+    const int64_t a1 = (2LL * np + 15) & ~15LL;
+    if constexpr (W16) {  // gains | byte status | 16-bit weights
+      stv.p = reinterpret_cast<uint8_t*>(base + a1);
+      w = reinterpret_cast<WT*>(base + a1 + ((np + 15LL) & ~15LL));
+    } else {
+      w = a.fm_w + pbeg;
+      stv.p = reinterpret_cast<uint16_t*>(base + a1);
+    }
   } else {
     w = a.fm_w + pbeg;
     gain = a.fm_gain + pbeg;
@@ -595,12 +672,20 @@ __device__ __forceinline__ void fm_node(const LevelArgs& a, int32_t li, int32_t 
   __shared__ int32_t s_cp[2][32];
   __shared__ int32_t s_left, s_cut, s_sw[2], s_best_cut, s_pass_cut, s_best_s[2], s_pass_s[2];
   __shared__ int32_t s_nm, s_best_len, s_need, s_stop;
+  constexpr bool PF = !SMA;  // adjacency from global memory: prefetch the candidates' rows
+  __shared__ int32_t s_pf_ring[PF ? kFmPfRing : 1];
+  __shared__ volatile int32_t s_pf_tail, s_pf_done;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int32_t pf_head = 0, seg_iter = 0;  // helper warp's ring position; segment counter (every thread)
+  if constexpr (PF) {
+    for (int32_t i = threadIdx.x; i < kFmPfRing; i += blockDim.x) s_pf_ring[i] = 0;
+    if (threadIdx.x == 0) s_pf_tail = 0, s_pf_done = -1;
+  }
 
   int64_t tot = 0;
   for (int32_t i = threadIdx.x; i < np; i += blockDim.x) {
     const int32_t p = pl[i];
-    w[i] = a.pw[p];
+    w[i] = static_cast<WT>(a.pw[p]);
     abe[i] = make_int2(a.qoff[p], a.qoff[p + 1]);
     stv.set(i, fm_st(1, 0, kNoSlot));  // right (partition.cpp:34)
     tot += w[i];
@@ -715,6 +800,15 @@ __device__ __forceinline__ void fm_node(const LevelArgs& a, int32_t li, int32_t 
       const int32_t need = s_need;
       if (need & 1) fm_refill<K>(0, np, gain, stv, s_ck, s_cp, s_B, hist, red, sh);
       if (need & 2) fm_refill<K>(1, np, gain, stv, s_ck, s_cp, s_B, hist, red, sh);
+      if constexpr (PF) {  // warps 2-3: the refilled caches' adjacency rows (warp 0 starts its segment at once)
+        if ((need & 3) && wid >= 2 && wid < 4) {
+          const int32_t p = s_cp[wid - 2][lane];
+          if (p >= 0) {
+            const int2 e = abe[p];
+            if (e.y > e.x) prefetch_l1(a.qloc + e.x), prefetch_l1(a.qloc + e.y - 1), prefetch_l1(a.qw + e.x), prefetch_l1(a.qw + e.y - 1);
+          }
+        }
+      }
       if (need & kFmExact) {  // the reference's own scan: max key over every feasible unlocked patch
         const int32_t sw0 = s_sw[0], sw1 = s_sw[1], H = max(sw0, sw1), L = min(sw0, sw1);
         uint64_t best = 0;
@@ -741,6 +835,7 @@ __device__ __forceinline__ void fm_node(const LevelArgs& a, int32_t li, int32_t 
         int32_t cw0 = cp0 >= 0 ? w[cp0] : 0, cw1 = cp1 >= 0 ? w[cp1] : 0;
         __syncwarp();  // every lane has read the shared state before lane 0 rewrites it
         uint32_t refilled = static_cast<uint32_t>(need & 3);
+        int32_t pf_tail = PF ? s_pf_tail : 0;
         // one move: lock ch, flip it, update the neighbours' gains and the caches
         auto apply = [&](K kbest, int32_t sd) {
           const int32_t ch = FmKey<K>::id(kbest);
@@ -820,7 +915,12 @@ __device__ __forceinline__ void fm_node(const LevelArgs& a, int32_t li, int32_t 
                 if (t) ck1 = nbk, cp1 = nbp, cw1 = wq;
                 else ck0 = nbk, cp0 = nbp, cw0 = wq;
                 stv.set_slot(nbp, (t << 5) | o);
+                if constexpr (PF) {
+                  s_pf_ring[pf_tail & (kFmPfRing - 1)] = nbp;
+                  s_pf_tail = pf_tail + 1;
+                }
               }
+              if constexpr (PF) ++pf_tail;
             }
             __syncwarp();
           }
@@ -863,8 +963,13 @@ __device__ __forceinline__ void fm_node(const LevelArgs& a, int32_t li, int32_t 
           s_nm = nm, s_best_len = best_len;
           s_B[0] = B0, s_B[1] = B1;
           s_need = reason;
+          if constexpr (PF) s_pf_done = seg_iter;
         }
+      } else if (PF && wid == 1) {
+        if constexpr (W16) fm_prefetch_helper<false>(abe, a.qloc, a.qw, nullptr, s_pf_ring, &s_pf_tail, &s_pf_done, seg_iter, pf_head);
+        else fm_prefetch_helper<!SM>(abe, a.qloc, a.qw, w, s_pf_ring, &s_pf_tail, &s_pf_done, seg_iter, pf_head);
       }
+      ++seg_iter;
       __syncthreads();
       if (s_need == kFmDone) break;
     }
@@ -896,6 +1001,10 @@ __host__ __device__ inline int64_t fm_node_smem(int64_t np, int64_t entries) {
 __host__ __device__ inline int64_t fm_node_smem_compact(int64_t np) {
   return 2 * ((2 * np + 15) & ~int64_t(15)) + 16;
 }
+// ... and of the 5-byte compact state with 16-bit weights (fm_node<SMC, W16>).
+__host__ __device__ inline int64_t fm_node_smem_compact_w16(int64_t np) {
+  return 2 * ((2 * np + 15) & ~int64_t(15)) + ((np + 15) & ~int64_t(15)) + 16;
+}
 
 // EXACT: integer feasibility (n < 2^26).  32-bit keys imply < 65536 patches
 // and edge weights < 32768, so a node whose state fits uses the packed
@@ -919,6 +1028,10 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
         fm_node<K, EXACT, true, false>(a, li, pbeg, np);
         return;
       }
+      if (a.fm_w16 && fm_node_smem_compact_w16(np) <= a.fm_smem_bytes) {  // + 16-bit weights, byte status
+        fm_node<K, EXACT, false, false, true, true>(a, li, pbeg, np);
+        return;
+      }
       if (fm_node_smem_compact(np) <= a.fm_smem_bytes) {  // 16-bit gains (32-bit keys: |gain| < 32768)
         fm_node<K, EXACT, false, false, true>(a, li, pbeg, np);
         return;
@@ -929,6 +1042,14 @@ __global__ void __launch_bounds__(kFmThreads, 1) fm_kernel(LevelArgs a) {
 }
 
 // largest total quotient edge weight of a patch: bounds |gain| for the key width
+// Largest weight of the level's alive patches (fm_node<SMC, W16> needs < 65536).
+__global__ void max_alive_weight(int32_t na, const int32_t* plist, const int32_t* pw, int32_t* out) {
+  int32_t m = 0;
+  for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) m = max(m, pw[plist[i]]);
+  m = __reduce_max_sync(0xffffffffu, m);
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
 __global__ void fm_gain_bound(int32_t na, const int32_t* plist, const int32_t* qoff, const int32_t* qw, int32_t* out) {
   for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x) {
     const int32_t p = plist[i];
@@ -1794,6 +1915,7 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
     a.qloc = qloc;
     size_t fm_smem = 1024;
     bool fm_hybrid = false;  // a node whose state fits shared memory but whose adjacency does not
+    bool fm_w16 = false;     // every alive patch weight fits 16 bits
     {
       // opt-in limit minus the kernels' static shared memory
       cudaFuncAttributes fa32{}, fa64{}, fah{};
@@ -1811,9 +1933,16 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
         // room for the packed adjacency of the largest node that fits
         std::vector<int64_t> hfo(width + 1);
         std::vector<int32_t> hpo(width + 1);
+        DevBuf<int32_t> dmaxw(1, s);
+        int32_t hmaxw = 0;
+        MP_CUDA(cudaMemsetAsync(dmaxw, 0, 4, s));
+        if (na_level > 0)
+          MP_KERNEL(ctx, max_alive_weight<<<grid_for(ctx, na_level), 256, 0, s>>>(na_level, plist, a.pw, dmaxw));
         MP_CUDA(cudaMemcpyAsync(hfo.data(), fifo_off.get(), sizeof(int64_t) * (width + 1), cudaMemcpyDeviceToHost, s));
         MP_CUDA(cudaMemcpyAsync(hpo.data(), poff.get(), sizeof(int32_t) * (width + 1), cudaMemcpyDeviceToHost, s));
+        MP_CUDA(cudaMemcpyAsync(&hmaxw, dmaxw.get(), 4, cudaMemcpyDeviceToHost, s));
         MP_CUDA(cudaStreamSynchronize(s));
+        fm_w16 = hmaxw < 65536;
         size_t need = 0;
         bool partial = false;  // some node fits only as state or compact state
         for (int32_t i = 0; i < width; ++i) {
@@ -1828,6 +1957,7 @@ void build_etree_dev(mp_context& ctx, const DGraph& g, const int32_t* assign, in
       }
     }
     a.fm_smem_bytes = static_cast<int64_t>(fm_smem);
+    a.fm_w16 = fm_w16 ? 1 : 0;
     // 32-bit move keys when every node fits (patch count and gain range)
     // (a patch's quotient weight is at most the level's crossing entries)
     int32_t hgb = nkeys;

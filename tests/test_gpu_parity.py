@@ -373,11 +373,12 @@ def test_fm_state_in_smem_adjacency_in_l2(rows, patch):
 
 
 @pytest.mark.parametrize("rows,patch,lo,hi", [(240, 4, 10240, 54000), (150, 2, 10240, 54000),
-                                              (540, 4, 58000, 65536), (600, 4, 65536, 1 << 30)])
+                                              (485, 4, 46000, 57000), (540, 4, 58000, 65536), (600, 4, 65536, 1 << 30)])
 def test_fm_large_nodes_global_state(rows, patch, lo, hi):
     """Root quotients beyond the wide shared-memory FM capacity (>10,240
-    patches; C3 has 39,063) keep 16-bit gains and 16-bit status in shared
-    memory (compact state) up to ~57K patches; beyond that the state is in
+    patches; C3 has 39,063) keep 16-bit gains, byte status and 16-bit weights
+    in shared memory up to ~45K patches, 16-bit gains and 16-bit status
+    (compact state) up to ~57K patches; beyond that the state is in
     global memory (32-bit keys below 65,536 patches, 64-bit keys above)."""
     from oracle.oracle import Restatement
     R = Restatement()
