@@ -70,6 +70,14 @@ __device__ __forceinline__ uint32_t md_key_deg(int64_t d) {
 // One node with its lists, pool and (above kSmemDegCap) degrees in global
 // memory: exact mode, natural mode, and approximate-mode nodes too large for
 // md_smem_kernel.
+// DT = uint16_t: degrees in shared memory as 16 bits (0xffff = eliminated),
+// for nodes below 65,535 vertices -- half the shared memory, so two 256-thread
+// CTAs share an SM (C3's 256 leaves of ~39K vertices run in one wave).  The
+// pivot loop is SM-throughput bound, not latency bound: two co-resident
+// leaves each run at about half speed, so the gain over two waves of one
+// 512-thread CTA per SM comes from the 256-thread CTA (C3 MD 370 -> 335 ms;
+// 256 threads one per SM: 334; 128 threads two per SM: 394).
+template <class DT = uint32_t>
 __device__ __forceinline__ void md_node_global(const MdArgs& a, int32_t node) {
   const int32_t vb = a.node_offsets[node], nv = a.node_offsets[node + 1] - vb;
   if (nv == 0 || (a.node_mask && !a.node_mask[node])) return;
@@ -81,8 +89,21 @@ __device__ __forceinline__ void md_node_global(const MdArgs& a, int32_t node) {
     return;
   }
   extern __shared__ uint32_t sdeg_dyn[];
-  const bool smem_deg = nv <= kSmemDegCap;
-  uint32_t* deg = smem_deg ? sdeg_dyn : a.gdeg + vb;  // indexed by local id
+  constexpr bool kDeg16 = sizeof(DT) == 2;
+  const bool smem_deg = kDeg16 || nv <= kSmemDegCap;
+  DT* deg;  // indexed by local id
+  if constexpr (kDeg16) deg = reinterpret_cast<DT*>(sdeg_dyn);
+  else deg = smem_deg ? sdeg_dyn : a.gdeg + vb;
+  // stored degree <-> 32-bit degree (kInfDeg once eliminated)
+  auto dget = [&](int32_t i) -> uint32_t {
+    const uint32_t d = deg[i];
+    if constexpr (kDeg16) return d == 0xffffu ? kInfDeg : d;
+    else return d;
+  };
+  auto dput = [&](int32_t i, uint32_t d) {
+    if constexpr (kDeg16) deg[i] = static_cast<DT>(d == kInfDeg ? 0xffffu : d);
+    else deg[i] = d;
+  };
 
   __shared__ uint64_t red[32];
   __shared__ int32_t s_nb, s_cursor, s_half, s_need_compact, s_ndirty, s_ip, s_dlist[kMdDirtyCap];
@@ -103,7 +124,7 @@ __device__ __forceinline__ void md_node_global(const MdArgs& a, int32_t node) {
     a.bsz[v] = 0;
     a.vmark[v] = 0;
     a.emark[v] = 0;
-    deg[k] = static_cast<uint32_t>(c);  // approx degree with no elements = |adj|
+    dput(k, static_cast<uint32_t>(c));  // approx degree with no elements = |adj|
   }
   if (threadIdx.x == 0) s_cursor = 0, s_half = 0, s_ndirty = 0;
   __syncthreads();
@@ -113,13 +134,13 @@ __device__ __forceinline__ void md_node_global(const MdArgs& a, int32_t node) {
   // recomputed at the end of the pivot (blk / dirty bits in shared memory
   // after the degrees when they fit, else in the node's global slab)
   const int32_t nbk = (nv + 31) / 32, lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  const int64_t deg_bytes = smem_deg ? ((4LL * nv + 7) & ~7LL) : 0;
+  const int64_t deg_bytes = smem_deg ? ((static_cast<int64_t>(sizeof(DT)) * nv + 7) & ~7LL) : 0;
   const bool blk_sm = deg_bytes + 8LL * nbk + 4LL * (nbk / 32 + 1) <= a.gsmem_bytes;
   uint64_t* blk = blk_sm ? reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(sdeg_dyn) + deg_bytes)
                          : a.gblk + (vb >> 5) + node;
   uint32_t* dbits = blk_sm ? reinterpret_cast<uint32_t*>(blk + nbk) : a.gdbits + (vb >> 10) + 2 * node;
   auto key_of = [&](int32_t i) -> uint64_t {
-    const uint32_t d = i < nv ? deg[i] : kInfDeg;
+    const uint32_t d = i < nv ? dget(i) : kInfDeg;
     return d != kInfDeg ? key_min(d, static_cast<uint32_t>(i)) : ~0ull;
   };
   auto mark_dirty = [&](int32_t b) {
@@ -235,7 +256,7 @@ __device__ __forceinline__ void md_node_global(const MdArgs& a, int32_t node) {
       a.bsz[p] = nb;
       order[k] = p;
       lperm[k] = kp;
-      deg[kp] = kInfDeg;
+      dput(kp, kInfDeg);
       mark_dirty(kp >> 5);  // the pivot was its block's minimum
     }
     // absorbed elements' boundaries are dropped after the member updates
@@ -301,8 +322,8 @@ __device__ __forceinline__ void md_node_global(const MdArgs& a, int32_t node) {
       d += nb;
       a.nel[w] = ce;
       if (a.mode == 0) {
-        const uint32_t od = deg[lw], nd = md_key_deg(d);
-        deg[lw] = nd;
+        const uint32_t od = dget(lw), nd = md_key_deg(d);
+        dput(lw, nd);
         rekey(lw, od, nd);
       }
     }
@@ -342,8 +363,8 @@ __device__ __forceinline__ void md_node_global(const MdArgs& a, int32_t node) {
         __syncthreads();
         if (threadIdx.x == 0) {
           const int32_t lw = a.local_of[w];
-          const uint32_t od = deg[lw], nd = static_cast<uint32_t>(s_cnt);
-          deg[lw] = nd;
+          const uint32_t od = dget(lw), nd = static_cast<uint32_t>(s_cnt);
+          dput(lw, nd);
           rekey(lw, od, nd);
         }
         __syncthreads();
@@ -380,6 +401,14 @@ inline size_t md_global_smem(int64_t nv) {
 
 __global__ void __launch_bounds__(kMdThreads) md_kernel(MdArgs a) {
   md_node_global(a, a.sched ? a.sched[blockIdx.x] : static_cast<int32_t>(blockIdx.x));
+}
+constexpr int kMd16Threads = 256;
+constexpr int64_t kMd16MaxNv = 65534;  // 16-bit degrees: every degree < nv <= 0xfffe
+inline size_t md_global_smem16(int64_t nv) {
+  return ((2 * static_cast<size_t>(std::max<int64_t>(nv, 1)) + 7) & ~size_t(7)) + 16384 + 512;
+}
+__global__ void __launch_bounds__(kMd16Threads, 2) md_kernel16(MdArgs a) {
+  md_node_global<uint16_t>(a, a.sched[blockIdx.x]);
 }
 
 // Shared-memory approximate-MD kernel (the default mode).  The whole
@@ -860,9 +889,17 @@ void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t L, const int
       // degrees of the largest such node in shared memory, plus block minima
       int64_t maxnv = 0;
       for (int32_t i = 0; i < big; ++i) maxnv = std::max<int64_t>(maxnv, hoff[sched[i] + 1] - hoff[sched[i]]);
-      const size_t bsmem = md_global_smem(maxnv);
-      ab.gsmem_bytes = static_cast<int64_t>(bsmem);
-      MP_KERNEL(ctx, md_kernel<<<big, kMdThreads, bsmem, ctx.aux_stream>>>(ab));
+      if (maxnv <= kMd16MaxNv && big > ctx.num_sms) {
+        // more big nodes than SMs: 16-bit degrees, two CTAs per SM, one wave
+        const size_t bsmem = md_global_smem16(maxnv);
+        ab.gsmem_bytes = static_cast<int64_t>(bsmem);
+        allow_max_smem(md_kernel16, ctx.device);
+        MP_KERNEL(ctx, md_kernel16<<<big, kMd16Threads, bsmem, ctx.aux_stream>>>(ab));
+      } else {
+        const size_t bsmem = md_global_smem(maxnv);
+        ab.gsmem_bytes = static_cast<int64_t>(bsmem);
+        MP_KERNEL(ctx, md_kernel<<<big, kMdThreads, bsmem, ctx.aux_stream>>>(ab));
+      }
       MP_CUDA(cudaEventRecord(ctx.fork_ev[1], ctx.aux_stream));
     }
     if (ns > big) {
