@@ -10,4 +10,4 @@ ctx = mp.Context(0)
 for _ in range(2):
     r = mp.order(g, ctx=ctx, want_fill=False)
 print({k: round(v, 1) for k, v in r.stage_ms.items()}, {k: round(v, 1) for k, v in r.kernel_ms.items()},
-      "work", r.work[:8], flush=True)
+      "work", r.work[:16], flush=True)
