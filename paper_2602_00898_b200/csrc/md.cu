@@ -889,9 +889,12 @@ void order_tree_nodes_dev(mp_context& ctx, const DGraph& g, int32_t L, const int
       // degrees of the largest such node in shared memory, plus block minima
       int64_t maxnv = 0;
       for (int32_t i = 0; i < big; ++i) maxnv = std::max<int64_t>(maxnv, hoff[sched[i] + 1] - hoff[sched[i]]);
-      if (maxnv <= kMd16MaxNv && big > ctx.num_sms) {
-        // more big nodes than SMs: 16-bit degrees, two CTAs per SM, one wave
-        const size_t bsmem = md_global_smem16(maxnv);
+      if (maxnv <= kMd16MaxNv) {
+        // 16-bit degrees, 256-thread CTAs: two per SM (one wave) when the big
+        // nodes outnumber the SMs, else one per SM (the shared memory is padded
+        // past half an SM so the scheduler cannot pair two leaves on one SM)
+        size_t bsmem = md_global_smem16(maxnv);
+        if (big <= ctx.num_sms) bsmem = std::max<size_t>(bsmem, 120 * 1024);
         ab.gsmem_bytes = static_cast<int64_t>(bsmem);
         allow_max_smem(md_kernel16, ctx.device);
         MP_KERNEL(ctx, md_kernel16<<<big, kMd16Threads, bsmem, ctx.aux_stream>>>(ab));

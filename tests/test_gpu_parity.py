@@ -593,6 +593,21 @@ def test_pattern_to_graph_errors_and_lift():
     assert lifted.assignment.tolist() == [1, 1, 0, 0, 2, 2] and lifted.patch_count == 3
 
 
+@pytest.mark.parametrize("rows,cols,L", [(110, 100, 0), (200, 200, 2)])
+def test_md_nodes_above_8k_vertices_match_reference(rows, cols, L):
+    """Nodes above 8K vertices leave the shared-memory MD kernel for
+    md_kernel16 (16-bit degrees in shared memory, 256-thread CTAs, one per SM
+    when the big nodes fit the SMs): one 11K-vertex node (the md baseline) and
+    four ~10K-vertex leaves, local orders and permutation vs the reference."""
+    from oracle.oracle import Reference
+    g = mp.mesh_to_graph(mp.make_grid_mesh(rows, cols))
+    o = Reference().order(g, nd_level=L, mode=0)
+    res = mp.order(g, nd_level=L)
+    assert np.diff(o["node_offsets"]).max() > 8192
+    assert np.array_equal(res.tree.vertices, o["node_vertices"])
+    assert np.array_equal(res.perm.perm, o["perm"])
+
+
 @pytest.mark.parametrize("name", ["natural", "md", "nd-vertex"])
 def test_baselines_match_reference(name):
     """run_baselines (pipeline.cpp:162-186) configurations vs the reference."""
