@@ -194,8 +194,20 @@ __device__ void select_candidates(const BatchArgs& a, int32_t W, uint64_t* sS, i
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int32_t tsize = 1 << a.tile_shift;
   // histogram of tile-max distances, binned so the largest fits
+  // (the tile scans keep kU loads in flight per thread: C3 has 39K tiles,
+  // ~38 per thread, and one dependent L2 round trip each cost ~30 us a batch)
+  constexpr int kU = 8;
   uint64_t mx = 0;
-  for (int32_t t = threadIdx.x; t < a.ntile; t += blockDim.x) mx = max(mx, __ldcg(&a.tkey[t]) >> 32);
+  for (int32_t t0 = threadIdx.x; t0 < a.ntile; t0 += kU * blockDim.x) {
+    uint64_t v[kU];
+#pragma unroll
+    for (int g = 0; g < kU; ++g) {
+      const int32_t t = t0 + g * static_cast<int32_t>(blockDim.x);
+      v[g] = t < a.ntile ? __ldcg(&a.tkey[t]) : 0;
+    }
+#pragma unroll
+    for (int g = 0; g < kU; ++g) mx = max(mx, v[g] >> 32);
+  }
   mx = block_max_u64(mx, red);
   int32_t shift = 0;
   while ((mx >> shift) >= static_cast<uint64_t>(kBins)) ++shift;
@@ -203,11 +215,19 @@ __device__ void select_candidates(const BatchArgs& a, int32_t W, uint64_t* sS, i
   __syncthreads();
   // late batches put most tiles in a few bins: one shared atomic per distinct
   // bin per warp instead of one per tile
-  for (int32_t t0 = 0; t0 < a.ntile; t0 += blockDim.x) {
-    const int32_t t = t0 + threadIdx.x;
-    const int32_t b = t < a.ntile ? static_cast<int32_t>((__ldcg(&a.tkey[t]) >> 32) >> shift) : -1;
-    const uint32_t m = __match_any_sync(0xffffffffu, b);
-    if (b >= 0 && lane == __ffs(m) - 1) atomicAdd(&hist[b], __popc(m));
+  for (int32_t t0 = 0; t0 < a.ntile; t0 += kU * blockDim.x) {
+    int32_t bs[kU];
+#pragma unroll
+    for (int g = 0; g < kU; ++g) {
+      const int32_t t = t0 + g * static_cast<int32_t>(blockDim.x) + static_cast<int32_t>(threadIdx.x);
+      bs[g] = t < a.ntile ? static_cast<int32_t>((__ldcg(&a.tkey[t]) >> 32) >> shift) : -1;
+    }
+#pragma unroll
+    for (int g = 0; g < kU; ++g) {
+      const int32_t b = bs[g];
+      const uint32_t m = __match_any_sync(0xffffffffu, b);
+      if (b >= 0 && lane == __ffs(m) - 1) atomicAdd(&hist[b], __popc(m));
+    }
   }
   __syncthreads();
   // the highest bin b where the suffix count reaches W: tiles in bins > b are
@@ -1012,7 +1032,16 @@ __global__ void __launch_bounds__(kThreads, 1) fps_cluster_phase(BatchArgs a, in
     if (done >= a.k) break;
     // the next seed: argmax (dist desc, id asc) over the tile maxima (every CTA)
     uint64_t best = 0;
-    for (int32_t t = threadIdx.x; t < a.ntile; t += blockDim.x) best = max(best, __ldcg(&a.tkey[t]));
+    for (int32_t t0 = threadIdx.x; t0 < a.ntile; t0 += 8 * blockDim.x) {
+      uint64_t v[8];
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        const int32_t t = t0 + g * static_cast<int32_t>(blockDim.x);
+        v[g] = t < a.ntile ? __ldcg(&a.tkey[t]) : 0;
+      }
+#pragma unroll
+      for (int g = 0; g < 8; ++g) best = max(best, v[g]);
+    }
     best = block_max_u64(best, s_red);
     if (static_cast<int32_t>(best >> 32) <= a.grid_radius) break;
     c = static_cast<int32_t>(key_max_id(best));
