@@ -45,3 +45,18 @@ r6 = mp.order(mp.mesh_to_graph(mp.make_grid_mesh(90, 90)), patch_size=2000, nd_l
 # shared-memory state, the shared-memory repair split)
 r7 = mp.order(mp.mesh_to_graph(mp.make_grid_mesh(120, 120)), patch_size=256, nd_level=1)
 print("round2 paths ok", rg.fill.nnz_L, fe.nnz_L, r5.fill.nnz_L, r6.fill.nnz_L, r7.fill.nnz_L)
+# session f paths (MP_SAN_LARGE=1): the FM compact 5-byte layout with the
+# prefetch helper warp (a root of ~11K patches) and md_kernel16 (one 11K-vertex
+# node: 16-bit shared-memory degrees, 256-thread CTA)
+import os
+if os.environ.get("MP_SAN_LARGE"):
+    from oracle.oracle import Reference
+    g4 = mp.mesh_to_graph(mp.make_grid_mesh(150, 150))
+    r4 = mp.order(g4, patch_size=2, want_fill=False)
+    o4 = Reference().order(g4, patch_size=2)
+    assert np.array_equal(r4.perm.perm, o4["perm"]), "fm compact"
+    g5 = mp.mesh_to_graph(mp.make_grid_mesh(110, 100))
+    r5 = mp.order(g5, nd_level=0, want_fill=False)
+    o5 = Reference().order(g5, nd_level=0, mode=0)
+    assert np.array_equal(r5.perm.perm, o5["perm"]), "md16"
+    print("sanitize large ok", r4.patch.patch_count, g5.n)
